@@ -1,0 +1,204 @@
+/*
+ * mpjacobi.h -- C ABI of the B200-native mixed-precision Jacobi eigensolver /
+ * one-sided Jacobi SVD (Zhang & Bai, arXiv 2211.03339).
+ *
+ * Citation keys: P:n = line n of the paper's LaTeX source.
+ *   Problem statement, EVD:  A = P Lambda P^T, A real symmetric
+ *   Alg. 3 (mixed-precision Jacobi EVD)
+ *   Alg. 5 (mixed-precision one-sided Jacobi SVD)
+ *   Lemma 3.1 (rotation), Eq. (3.1) J(i,j;theta)
+ *   Lemma 5.1 (one-sided rotation)
+ *   Tolerances eps = 0.1 omega, nu = 20 omega (EVD), nu = omega and
+ *   the 2e-4 early stop (SVD); upsilon = 2^-24, omega = 2^-53
+ *   Parallel (merry-go-round) ordering
+ *
+ * Conventions (all entry points):
+ *   - Matrices are IEEE binary64 (or binary32 where stated), COLUMN-MAJOR,
+ *     with a leading dimension >= rows.  Indices are 0-based.
+ *   - Unless stated otherwise, pointers are DEVICE pointers (cudaMalloc /
+ *     torch CUDA tensors) on the current device, and all work is enqueued on
+ *     `stream` (a cudaStream_t passed as void*; NULL = legacy default
+ *     stream).  The call returns after the result is written (it
+ *     synchronises `stream` once per sweep to evaluate the stop test).
+ *   - The caller owns every buffer.  `workspace` may be NULL, in which case
+ *     the library allocates it stream-ordered (cudaMallocAsync) and frees it
+ *     before returning; otherwise it must hold at least the size returned by
+ *     the matching *_workspace() query, 256-byte aligned.
+ *   - Errors: the return value is an mpj_status; mpjacobi_last_error() gives
+ *     a thread-local message.  On MPJ_ERR_NOCONV the outputs hold the last
+ *     iterate.  Invalid sizes return MPJ_ERR_INVALID before any work.
+ *   - Thread safety: calls on distinct streams with distinct buffers may run
+ *     concurrently.
+ *   - The GPU code path is the only path: there is no CPU fallback.  A call
+ *     on a machine without an sm_100 device returns MPJ_ERR_CUDA.
+ */
+#ifndef MPJACOBI_H
+#define MPJACOBI_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define MPJ_ABI_VERSION 1
+
+typedef enum {
+    MPJ_OK = 0,
+    MPJ_ERR_INVALID = 1,    /* bad size / pointer / config                        */
+    MPJ_ERR_NOCONV = 2,     /* max_sweeps reached before ||off|| <= eps ||A||_F    */
+    MPJ_ERR_RANKDEF = 3,    /* SVD: some sigma_j <= n omega ||A||_F; MGS breakdown */
+    MPJ_ERR_NONFINITE = 4,  /* NaN/Inf in the input                               */
+    MPJ_ERR_CUDA = 5,       /* CUDA runtime error (message in last_error)         */
+    MPJ_ERR_NCCL = 6,       /* NCCL error (multi-GPU entry points)                */
+    MPJ_ERR_NOMEM = 7       /* workspace too small / allocation failed            */
+} mpj_status;
+
+/* Jacobi sweep implementation. */
+enum {
+    MPJ_VARIANT_AUTO = 0,   /* block for n_p >= 256, scalar rounds otherwise       */
+    MPJ_VARIANT_SCALAR = 1, /* one launch pair per round, bit-exact with the oracle */
+    MPJ_VARIANT_BLOCK = 2   /* 2b x 2b block solves + fp64 tensor-core (DMMA) apply */
+};
+
+typedef struct mpj_config {
+    double eps_factor;        /* eps = eps_factor * omega; default 0.1            */
+    double nu_factor;         /* nu = nu_factor * omega; default 20 (EVD), 1 (SVD)       */
+    double eps_low_factor;    /* low stage: eps_low = f * upsilon; default 10            */
+    double nu_low_factor;     /* low stage: nu_low = f * upsilon; default 20 EVD, 1 SVD  */
+    double early_stop_ratio;  /* SVD: stop after a sweep with rotations/N below this;
+                                 default 2e-4; 0 disables                        */
+    int max_sweeps;           /* fp64 stage cap; default 60                               */
+    int max_sweeps_low;       /* fp32 stage cap; default 60                               */
+    int stop_rule;            /* 0: |t_pq| <= nu min(|t_pp|,|t_qq|);
+                                 1: |t_pq| <= nu sqrt(t_pp t_qq) (Remark 3.1)      */
+    int variant;              /* MPJ_VARIANT_*                                             */
+    int block_b;              /* ordering block size b (1 or even); 0 = auto (32)        */
+} mpj_config;
+
+/* Fill *cfg with the paper's EVD / SVD settings. */
+void mpj_config_default_eig(mpj_config *cfg);
+void mpj_config_default_svd(mpj_config *cfg);
+
+typedef struct mpj_report {
+    int sweeps;               /* fp64 sweeps executed (the paper's SP)             */
+    int sweeps_low;           /* fp32 (low-precision stage) sweeps                        */
+    int status;               /* mpj_status of the fp64 stage                             */
+    int status_low;           /* mpj_status of the fp32 stage (NOCONV there is benign)    */
+    long long rotations;      /* applied fp64 rotations (the paper's JU x N)              */
+    long long rotations_low;  /* applied fp32 rotations                                   */
+    double norm_a;            /* ||A||_F of the symmetrised input                          */
+    double off0;              /* ||off(Q^T A Q)||_F (EVD) / ||off((AQ)^T AQ)||_F (SVD)     */
+    double off_hist[64];      /* ||off(T)||_F before fp64 sweep k (first 64)              */
+    double t_low, t_orth, t_precond, t_jacobi, t_extract, t_total; /* seconds (events)    */
+    int n_padded;             /* n rounded up to a multiple of 2b                         */
+    int block_b;              /* ordering block size used                                 */
+    int variant;              /* MPJ_VARIANT_SCALAR or MPJ_VARIANT_BLOCK                  */
+    long long launches;       /* kernels launched by the call                             */
+} mpj_report;
+
+/* ------------------------------------------------------------------------
+ * Alg. 3 end to end: fp32 Jacobi EVD of fl32(A) -> Z, Q = MGS(Z)
+ * in fp64 (blocked CGS2), T = Q^T A Q (fp64 DMMA GEMMs, symmetrised),
+ * parallel-ordered fp64 Jacobi sweeps on T accumulating V = Q J1 J2 ...,
+ * then Lambda = diag(T) sorted descending (stable) with V's columns alike.
+ *
+ *   A       in:  n x n, lda >= n; symmetrised internally ((A + A^T)/2); not
+ *                modified.  HOST or DEVICE pointer (host buffers are staged
+ *                through the workspace with cudaMemcpyAsync on `stream`).
+ *   Lambda  out: n eigenvalues, descending.  Host or device.
+ *   V       out: n x n eigenvectors (column k <-> Lambda[k]), ldv >= n.
+ *                Host or device.
+ *   sweeps  out: fp64 sweeps (may be NULL; host pointer).
+ *   rep     out: telemetry (may be NULL; host pointer).
+ * Returns MPJ_OK, MPJ_ERR_NOCONV, MPJ_ERR_NONFINITE, MPJ_ERR_RANKDEF (MGS
+ * breakdown), MPJ_ERR_INVALID, MPJ_ERR_NOMEM or MPJ_ERR_CUDA.
+ * ---------------------------------------------------------------------- */
+size_t mpjacobi_eig_workspace(int64_t n, const mpj_config *cfg);
+mpj_status mpjacobi_eig(const double *A, int64_t n, int64_t lda, double *Lambda, double *V,
+                        int64_t ldv, int *sweeps, void *workspace, size_t ws_bytes, void *stream,
+                        const mpj_config *cfg, mpj_report *rep);
+
+/* Alg. 2 from T = A, P = I: "plain" fp64 parallel Jacobi with the
+ * same kernels and ordering (the baseline of BASELINE.json config 2).  Same
+ * arguments and outputs as mpjacobi_eig. */
+mpj_status mpjacobi_eig_plain(const double *A, int64_t n, int64_t lda, double *Lambda, double *V,
+                              int64_t ldv, int *sweeps, void *workspace, size_t ws_bytes,
+                              void *stream, const mpj_config *cfg, mpj_report *rep);
+
+/* ------------------------------------------------------------------------
+ * The Jacobi loop of Alg. 2 / Alg. 3 steps 4-11 on a given T
+ * with accumulation into a given V: the hot path of the method.
+ *   T  in/out: n x n symmetric (must be exactly symmetric), ldt >= n, DEVICE.
+ *   V  in/out: n x n, ldv >= n, DEVICE; V <- V J_1 J_2 ... (right rotations).
+ *   tol: the while test is ||off(T)||_F > tol (pass eps * ||A||_F).
+ *   nu:  threshold of the test |t_pq| <= nu min(|t_pp|,|t_qq|).
+ *   max_sweeps: cap; max_rounds >= 0 stops after that many rounds in total
+ *        (round-level parity tests), -1 = no limit.
+ *   The f32 variant runs the identical algorithm in binary32 (the
+ *   low-precision stage, reading R12).  Only cfg->variant, cfg->block_b and
+ *   cfg->stop_rule are read from cfg (may be NULL).
+ *   sweeps / rotations (host pointers, may be NULL) receive SP and JU*N.
+ * ---------------------------------------------------------------------- */
+mpj_status mpjacobi_jacobi_f64(double *T, int64_t ldt, double *V, int64_t ldv, int64_t n,
+                               double tol, double nu, int max_sweeps, int64_t max_rounds,
+                               int *sweeps, long long *rotations, double *off_hist64,
+                               void *stream, const mpj_config *cfg);
+mpj_status mpjacobi_jacobi_f32(float *T, int64_t ldt, float *V, int64_t ldv, int64_t n,
+                               double tol, double nu, int max_sweeps, int64_t max_rounds,
+                               int *sweeps, long long *rotations, double *off_hist64,
+                               void *stream, const mpj_config *cfg);
+
+/* Alg. 3 step 2: Q = orth(Z) in fp64 by blocked classical
+ * Gram-Schmidt with reorthogonalisation (CGS2, reading R10); Z, Q: n x n,
+ * DEVICE, ld = n.  Returns MPJ_ERR_RANKDEF on a zero column. */
+mpj_status mpjacobi_orth(const double *Z, double *Q, int64_t n, void *stream);
+
+/* Alg. 3 step 3: T = Q^T A Q, symmetrised; A, Q, T: n x n DEVICE,
+ * ld = n.  fp64 tensor-core (DMMA) GEMMs. */
+mpj_status mpjacobi_precond(const double *A, const double *Q, double *T, int64_t n, void *stream);
+
+/* C (m x n) = op(A) (m x k) * B (k x n), fp64, DEVICE, column-major with
+ * ld = rows; transa = 1 means A is stored k x m.  (The DMMA GEMM that the
+ * preconditioner and the SVD's C = A Q use; exported for parity tests.) */
+mpj_status mpjacobi_dgemm(int transa, const double *A, const double *B, double *C, int64_t m,
+                          int64_t n, int64_t k, void *stream);
+
+/* ------------------------------------------------------------------------
+ * Alg. 5 end to end: fp32 one-sided Jacobi on fl32(A) -> Z,
+ * Q = orth(Z), C = A Q, V = Q, fp64 one-sided sweeps (rotate iff
+ * |c_p^T c_q| > nu ||c_p|| ||c_q||), stop when ||off(C^T C)||_F <=
+ * eps ||C^T C||_F or a sweep's rotations / N < early_stop_ratio;
+ * then sort columns by ||c_j|| descending, sigma_j = ||c_j||, u_j = c_j/sigma_j.
+ *   A: m x n, m >= n, lda >= m (host or device); Sigma: n; U: m x n (ldu >= m);
+ *   V: n x n (ldv >= n).  MPJ_ERR_RANKDEF if some sigma_j <= n omega ||A||_F.
+ * ---------------------------------------------------------------------- */
+size_t mpjacobi_svd_workspace(int64_t m, int64_t n, const mpj_config *cfg);
+mpj_status mpjacobi_svd(const double *A, int64_t m, int64_t n, int64_t lda, double *Sigma,
+                        double *U, int64_t ldu, double *V, int64_t ldv, int *sweeps,
+                        void *workspace, size_t ws_bytes, void *stream, const mpj_config *cfg,
+                        mpj_report *rep);
+
+/* ------------------------------------------------------------------------
+ * Batched Alg. 3: `batch` independent n x n matrices, contiguous with stride
+ * n*n (each column-major), one matrix per CTA (n <= 64).  Lambda: batch x n;
+ * V: batch x n x n (each column-major); sweeps / sweeps_low: batch ints
+ * (DEVICE, may be NULL).  All pointers DEVICE.  Returns MPJ_ERR_NOCONV if any
+ * matrix hit max_sweeps.
+ * ---------------------------------------------------------------------- */
+mpj_status mpjacobi_eig_batched(const double *A, int64_t n, int64_t batch, double *Lambda,
+                                double *V, int *sweeps, int *sweeps_low, void *stream,
+                                const mpj_config *cfg);
+
+/* Thread-local description of the last error ("" if none). */
+const char *mpjacobi_last_error(void);
+
+/* Number of kernels this thread has launched through the library (the bench
+ * reports it as gpu_launches). */
+long long mpjacobi_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MPJACOBI_H */

@@ -1,0 +1,273 @@
+"""Python binding of the mixed-precision Jacobi C ABI (include/mpjacobi.h).
+
+Argument marshalling only: every step of the method runs in the CUDA kernels of
+libmpjacobi.so (built in-tree by ``paper_2211_03339_b200.build.build()``).  The
+binding fails loudly when the library is missing -- there is no CPU fallback.
+
+Matrices are column-major on the C side.  A torch tensor ``X`` of shape
+(rows, cols) is passed as-is when it is already column-major
+(``X.stride() == (1, ld)``, e.g. ``Y.T`` for a contiguous ``Y``); otherwise a
+column-major copy is made.  Outputs are returned as column-major tensors viewed
+in math orientation (``out[i, j]`` is entry (i, j)).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass
+
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libmpjacobi.so")
+
+OMEGA = 2.0 ** -53
+UPSILON = 2.0 ** -24
+
+MPJ_OK, MPJ_ERR_INVALID, MPJ_ERR_NOCONV, MPJ_ERR_RANKDEF = 0, 1, 2, 3
+MPJ_ERR_NONFINITE, MPJ_ERR_CUDA, MPJ_ERR_NCCL, MPJ_ERR_NOMEM = 4, 5, 6, 7
+VARIANT_AUTO, VARIANT_SCALAR, VARIANT_BLOCK = 0, 1, 2
+
+STATUS_NAMES = {0: "OK", 1: "INVALID", 2: "NOCONV", 3: "RANKDEF", 4: "NONFINITE", 5: "CUDA",
+                6: "NCCL", 7: "NOMEM"}
+
+
+class MpjError(RuntimeError):
+    def __init__(self, status, msg):
+        super().__init__(f"mpjacobi: {STATUS_NAMES.get(status, status)}: {msg}")
+        self.status = status
+
+
+class mpj_config(C.Structure):
+    _fields_ = [
+        ("eps_factor", C.c_double), ("nu_factor", C.c_double), ("eps_low_factor", C.c_double),
+        ("nu_low_factor", C.c_double), ("early_stop_ratio", C.c_double), ("max_sweeps", C.c_int),
+        ("max_sweeps_low", C.c_int), ("stop_rule", C.c_int), ("variant", C.c_int), ("block_b", C.c_int),
+    ]
+
+
+class mpj_report(C.Structure):
+    _fields_ = [
+        ("sweeps", C.c_int), ("sweeps_low", C.c_int), ("status", C.c_int), ("status_low", C.c_int),
+        ("rotations", C.c_longlong), ("rotations_low", C.c_longlong), ("norm_a", C.c_double),
+        ("off0", C.c_double), ("off_hist", C.c_double * 64), ("t_low", C.c_double),
+        ("t_orth", C.c_double), ("t_precond", C.c_double), ("t_jacobi", C.c_double),
+        ("t_extract", C.c_double), ("t_total", C.c_double), ("n_padded", C.c_int), ("block_b", C.c_int),
+        ("variant", C.c_int), ("launches", C.c_longlong),
+    ]
+
+    def as_dict(self):
+        d = {k: getattr(self, k) for k, _ in self._fields_ if k != "off_hist"}
+        d["off_hist"] = list(self.off_hist[: max(self.sweeps + 1, 1)])
+        return d
+
+
+_lib = None
+_vp, _i64, _dp = C.c_void_p, C.c_int64, C.c_double
+
+
+def lib():
+    """Load libmpjacobi.so (raises if it was not built)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise RuntimeError(
+                f"{LIB_PATH} is missing: run `python -c 'import __graft_entry__ as g; g.build()'` "
+                "(the CUDA library is the only implementation; there is no fallback)")
+        L = C.CDLL(LIB_PATH)
+        cfgp, repp = C.POINTER(mpj_config), C.POINTER(mpj_report)
+        L.mpj_config_default_eig.argtypes = [cfgp]
+        L.mpj_config_default_svd.argtypes = [cfgp]
+        L.mpjacobi_last_error.restype = C.c_char_p
+        L.mpjacobi_launch_count.restype = C.c_longlong
+        L.mpjacobi_eig_workspace.restype = C.c_size_t
+        L.mpjacobi_eig_workspace.argtypes = [_i64, cfgp]
+        eig_args = [_vp, _i64, _i64, _vp, _vp, _i64, C.POINTER(C.c_int), _vp, C.c_size_t, _vp, cfgp, repp]
+        for nm in ("mpjacobi_eig", "mpjacobi_eig_plain"):
+            getattr(L, nm).restype = C.c_int
+            getattr(L, nm).argtypes = eig_args
+        for nm in ("mpjacobi_jacobi_f64", "mpjacobi_jacobi_f32"):
+            getattr(L, nm).restype = C.c_int
+            getattr(L, nm).argtypes = [_vp, _i64, _vp, _i64, _i64, _dp, _dp, C.c_int, _i64,
+                                       C.POINTER(C.c_int), C.POINTER(C.c_longlong), C.POINTER(C.c_double),
+                                       _vp, cfgp]
+        L.mpjacobi_orth.restype = C.c_int
+        L.mpjacobi_orth.argtypes = [_vp, _vp, _i64, _vp]
+        L.mpjacobi_precond.restype = C.c_int
+        L.mpjacobi_precond.argtypes = [_vp, _vp, _vp, _i64, _vp]
+        L.mpjacobi_dgemm.restype = C.c_int
+        L.mpjacobi_dgemm.argtypes = [C.c_int, _vp, _vp, _vp, _i64, _i64, _i64, _vp]
+        if hasattr(L, "mpjacobi_svd"):
+            L.mpjacobi_svd_workspace.restype = C.c_size_t
+            L.mpjacobi_svd_workspace.argtypes = [_i64, _i64, cfgp]
+            L.mpjacobi_svd.restype = C.c_int
+            L.mpjacobi_svd.argtypes = [_vp, _i64, _i64, _i64, _vp, _vp, _i64, _vp, _i64,
+                                       C.POINTER(C.c_int), _vp, C.c_size_t, _vp, cfgp, repp]
+        if hasattr(L, "mpjacobi_eig_batched"):
+            L.mpjacobi_eig_batched.restype = C.c_int
+            L.mpjacobi_eig_batched.argtypes = [_vp, _i64, _i64, _vp, _vp, _vp, _vp, _vp, cfgp]
+        _lib = L
+    return _lib
+
+
+EXPORTED = (
+    "mpj_config_default_eig", "mpj_config_default_svd", "mpjacobi_eig_workspace", "mpjacobi_eig",
+    "mpjacobi_eig_plain", "mpjacobi_jacobi_f64", "mpjacobi_jacobi_f32", "mpjacobi_orth",
+    "mpjacobi_precond", "mpjacobi_dgemm", "mpjacobi_svd_workspace", "mpjacobi_svd",
+    "mpjacobi_eig_batched", "mpjacobi_last_error", "mpjacobi_launch_count",
+)
+
+
+def _check(status, ok=(MPJ_OK,)):
+    if status not in ok:
+        raise MpjError(status, lib().mpjacobi_last_error().decode())
+    return status
+
+
+def default_config(kind: str = "eig", **kw) -> mpj_config:
+    c = mpj_config()
+    (lib().mpj_config_default_eig if kind == "eig" else lib().mpj_config_default_svd)(C.byref(c))
+    for k, v in kw.items():
+        setattr(c, k, v)
+    return c
+
+
+def launch_count() -> int:
+    return lib().mpjacobi_launch_count()
+
+
+def _stream():
+    return C.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+def _ptr(t):
+    return C.c_void_p(t.data_ptr()) if t is not None else None
+
+
+def colmajor(x: torch.Tensor) -> torch.Tensor:
+    """Column-major version of x (rows, cols): a view when already column-major."""
+    if x.dim() != 2:
+        raise ValueError("expected a matrix")
+    if x.stride(0) == 1 and x.stride(1) >= max(1, x.shape[0]):
+        return x
+    return x.T.contiguous().T
+
+
+def empty_colmajor(rows, cols, dtype=torch.float64, device="cuda", pin=False):
+    if device == "cpu":
+        return torch.empty((cols, rows), dtype=dtype, pin_memory=pin).T
+    return torch.empty((cols, rows), dtype=dtype, device=device).T
+
+
+@dataclass
+class EigResult:
+    lam: torch.Tensor
+    V: torch.Tensor
+    sweeps: int
+    report: mpj_report
+
+
+def mpjacobi_eig(A, cfg: mpj_config | None = None, *, plain=False, workspace=None, out=None,
+                 allow_noconv=False) -> EigResult:
+    """Alg. 3 (or Alg. 2 with plain=True).  A: (n, n) float64 tensor on the GPU
+    or on the host (host tensors are staged by the library; pin them for async
+    copies).  Returns descending eigenvalues and column-major eigenvectors."""
+    n = A.shape[0]
+    if A.shape != (n, n) or A.dtype != torch.float64:
+        raise ValueError("A must be a square float64 matrix")
+    Acm = colmajor(A)
+    dev = Acm.device
+    if out is None:
+        lam = torch.empty(n, dtype=torch.float64, device=dev, pin_memory=(dev.type == "cpu"))
+        V = empty_colmajor(n, n, device=dev.type, pin=(dev.type == "cpu"))
+    else:
+        lam, V = out
+    cfg = cfg or default_config("eig")
+    rep = mpj_report()
+    sw = C.c_int(0)
+    ws_ptr, ws_bytes = None, 0
+    if workspace is not None:
+        ws_ptr, ws_bytes = _ptr(workspace), workspace.numel() * workspace.element_size()
+    fn = lib().mpjacobi_eig_plain if plain else lib().mpjacobi_eig
+    st = fn(_ptr(Acm), n, Acm.stride(1), _ptr(lam), _ptr(V), V.stride(1), C.byref(sw), ws_ptr, ws_bytes,
+            _stream(), C.byref(cfg), C.byref(rep))
+    _check(st, (MPJ_OK, MPJ_ERR_NOCONV) if allow_noconv else (MPJ_OK,))
+    return EigResult(lam, V, sw.value, rep)
+
+
+def eig_workspace(n, cfg: mpj_config | None = None, device="cuda"):
+    nbytes = lib().mpjacobi_eig_workspace(n, C.byref(cfg or default_config("eig")))
+    return torch.empty(nbytes, dtype=torch.uint8, device=device)
+
+
+@dataclass
+class JacobiResult:
+    sweeps: int
+    rotations: int
+    status: int
+    off_hist: list
+
+
+def mpjacobi_jacobi(T, V, *, tol=0.0, nu=20 * OMEGA, max_sweeps=60, max_rounds=-1,
+                    cfg: mpj_config | None = None) -> JacobiResult:
+    """Alg. 2 / Alg. 3 steps 4-11 in place on device T (symmetric) and V.
+    float64 or float32 tensors, column-major (symmetric T makes either layout
+    valid; V must be column-major or is copied back)."""
+    n = T.shape[0]
+    fn = lib().mpjacobi_jacobi_f64 if T.dtype == torch.float64 else lib().mpjacobi_jacobi_f32
+    Vc = colmajor(V)
+    Tc = colmajor(T)
+    sw, rot = C.c_int(0), C.c_longlong(0)
+    hist = (C.c_double * 64)()
+    st = fn(_ptr(Tc), Tc.stride(1), _ptr(Vc), Vc.stride(1), n, tol, nu, max_sweeps, max_rounds,
+            C.byref(sw), C.byref(rot), hist, _stream(), C.byref(cfg) if cfg is not None else None)
+    _check(st, (MPJ_OK, MPJ_ERR_NOCONV))
+    if Vc.data_ptr() != V.data_ptr():
+        V.copy_(Vc)
+    if Tc.data_ptr() != T.data_ptr():
+        T.copy_(Tc)
+    return JacobiResult(sw.value, rot.value, st, list(hist[: min(sw.value + 1, 64)]))
+
+
+def mpjacobi_orth(Z):
+    """Alg. 3 step 2: fp64 CGS2 of a square column-major device matrix."""
+    n = Z.shape[0]
+    Zc = colmajor(Z)
+    if Zc.stride(1) != n:
+        Zc = Zc.T.contiguous().T
+    Q = empty_colmajor(n, n)
+    _check(lib().mpjacobi_orth(_ptr(Zc), _ptr(Q), n, _stream()))
+    return Q
+
+
+def mpjacobi_precond(A, Q):
+    """Alg. 3 step 3: symmetrised Q^T A Q (device, fp64)."""
+    n = A.shape[0]
+    Ac = colmajor(A)
+    Qc = colmajor(Q)
+    if Ac.stride(1) != n:
+        Ac = Ac.T.contiguous().T
+    if Qc.stride(1) != n:
+        Qc = Qc.T.contiguous().T
+    T = empty_colmajor(n, n)
+    _check(lib().mpjacobi_precond(_ptr(Ac), _ptr(Qc), _ptr(T), n, _stream()))
+    return T
+
+
+def mpjacobi_dgemm(A, B, transa=False):
+    """C = op(A) B with the library's DMMA GEMM (parity tests)."""
+    Ac, Bc = colmajor(A).T.contiguous().T, colmajor(B).T.contiguous().T
+    m = Ac.shape[1] if transa else Ac.shape[0]
+    k = Ac.shape[0] if transa else Ac.shape[1]
+    n = Bc.shape[1]
+    Cm = empty_colmajor(m, n)
+    _check(lib().mpjacobi_dgemm(1 if transa else 0, _ptr(Ac), _ptr(Bc), _ptr(Cm), m, n, k, _stream()))
+    return Cm
+
+
+# short aliases
+eig = mpjacobi_eig
+jacobi = mpjacobi_jacobi
+orth = mpjacobi_orth
+precond = mpjacobi_precond
+dgemm = mpjacobi_dgemm

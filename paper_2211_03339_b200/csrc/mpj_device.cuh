@@ -1,0 +1,132 @@
+// mpj_device.cuh -- device-side building blocks of the Jacobi hot path.
+//
+// Independent of oracle/ (no shared code); both follow the same paper text:
+//   Lemma 3.1: mu = (a_qq - a_pp)/(2 a_pq),
+//     t = 1/(mu + sqrt(1+mu^2)) (mu >= 0) | 1/(mu - sqrt(1+mu^2)) (mu < 0),
+//     c = (1+t^2)^(-1/2), s = t c.
+//   Threshold (Alg. 2/3 line 4): skip iff |a_pq| <= nu min(|a_pp|,|a_qq|)
+//   (stop_rule 1: Remark 3.1, |a_pq| <= nu sqrt(a_pp a_qq)).
+// Readings: R3 1+mu^2 = fma(mu,mu,1); R4 |mu| >= 2^26 (fp64) /
+// 2^12 (fp32) uses t = 0.5/mu; R6 the Rutishauser tau-form of the update,
+//   x' = x - s (y + tau x),  y' = y + s (x - tau y),  tau = s/(1+c),
+// each as two explicit fused multiply-adds.  The library is compiled with
+// -fmad=false so that no other contraction happens (bit-exact with the
+// oracle's binary64/binary32 arithmetic).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace mpj {
+
+template <typename R> struct Prec;
+template <> struct Prec<double> {
+    static constexpr double mu_big = 67108864.0;  // 2^26
+};
+template <> struct Prec<float> {
+    static constexpr float mu_big = 4096.0f;      // 2^12
+};
+
+__device__ __forceinline__ double fmaR(double a, double b, double c) { return __fma_rn(a, b, c); }
+__device__ __forceinline__ float fmaR(float a, float b, float c) { return __fmaf_rn(a, b, c); }
+__device__ __forceinline__ double sqrtR(double a) { return __dsqrt_rn(a); }
+__device__ __forceinline__ float sqrtR(float a) { return __fsqrt_rn(a); }
+__device__ __forceinline__ double divR(double a, double b) { return __ddiv_rn(a, b); }
+__device__ __forceinline__ float divR(float a, float b) { return __fdiv_rn(a, b); }
+__device__ __forceinline__ double absR(double a) { return fabs(a); }
+__device__ __forceinline__ float absR(float a) { return fabsf(a); }
+__device__ __forceinline__ double minR(double a, double b) { return fmin(a, b); }
+__device__ __forceinline__ float minR(float a, float b) { return fminf(a, b); }
+
+// Rotation parameters of Lemma 3.1 plus the threshold decision.
+// Returns 1 if the pair rotates; on skip t = s = tau = 0 (identity update).
+template <typename R>
+__device__ __forceinline__ int rot_params(R app, R aqq, R apq, R nu, int rule, R &t, R &s, R &tau)
+{
+    bool skip;
+    if (rule == 1) {
+        R g = app * aqq;
+        skip = (g > R(0)) ? (absR(apq) <= nu * sqrtR(g)) : (apq == R(0));
+    } else {
+        skip = absR(apq) <= nu * minR(absR(app), absR(aqq));
+    }
+    if (skip) { t = R(0); s = R(0); tau = R(0); return 0; }
+    R mu = divR(aqq - app, R(2) * apq);
+    R tt;
+    if (absR(mu) < Prec<R>::mu_big) {
+        R r = sqrtR(fmaR(mu, mu, R(1)));
+        tt = (mu >= R(0)) ? divR(R(1), mu + r) : divR(R(1), mu - r);
+    } else {
+        tt = divR(R(0.5), mu);
+    }
+    R c = divR(R(1), sqrtR(fmaR(tt, tt, R(1))));
+    R ss = tt * c;
+    t = tt; s = ss; tau = divR(ss, R(1) + c);
+    return 1;
+}
+
+// J applied to an (x at index p, y at index q) pair: (x,y) <- (c x - s y, s x + c y).
+template <typename R>
+__device__ __forceinline__ void rot(R s, R tau, R &x, R &y)
+{
+    R x0 = x, y0 = y;
+    x = fmaR(-s, fmaR(tau, x0, y0), x0);
+    y = fmaR(s, fmaR(-tau, y0, x0), y0);
+}
+
+// ---------------------------------------------------------------------------
+// Parallel ordering (reading R1): block merry-go-round with block size b.
+// The host uploads
+//   bsched[R * mb + k] = (top block, bottom block) of block pair k in block round R
+//   lsched[s * (b/2) + j] = (top, bottom) local indices of intra round s (round 0 only)
+// and pair (round r, slot k) is decoded here.  Pair orientation: p < q.
+// ---------------------------------------------------------------------------
+struct Sched {
+    const int2 *bsched;   // (nb-1) x mb
+    const int2 *lsched;   // (b-1) x (b/2), b > 1 only
+    int b;                // block size (1 or even)
+    int nb;               // n_p / b
+    int np;               // padded order
+};
+
+__device__ __forceinline__ int2 pair_of(const Sched &S, int r, int k)
+{
+    const int b = S.b, mb = S.nb >> 1;
+    int a, c;
+    if (b > 1 && r < b - 1) {               // intra-block round r of block round 0
+        const int kk = k / b, w = k - kk * b, hb = b >> 1;
+        const int2 bp = S.bsched[kk];
+        const int blk = (w < hb) ? bp.x : bp.y;
+        const int2 lp = S.lsched[r * hb + (w < hb ? w : w - hb)];
+        a = blk * b + lp.x; c = blk * b + lp.y;
+    } else {
+        const int rr = (b > 1) ? r - (b - 1) : r;
+        const int R = rr / b, s = rr - R * b;
+        const int kk = k / b, i = k - kk * b;
+        const int2 bp = S.bsched[R * mb + kk];
+        a = bp.x * b + i;
+        int j = i + s; if (j >= b) j -= b;
+        c = bp.y * b + j;
+    }
+    return a < c ? make_int2(a, c) : make_int2(c, a);
+}
+
+// Deterministic block reduction of a double (all threads of the block call it).
+template <int NT>
+__device__ __forceinline__ double block_sum(double v, double *sh)
+{
+    #pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    __syncthreads();
+    if (l == 0) sh[w] = v;
+    __syncthreads();
+    double r = 0;
+    if (threadIdx.x < 32) {
+        r = (l < NT / 32) ? sh[l] : 0.0;
+        #pragma unroll
+        for (int o = 16; o > 0; o >>= 1) r += __shfl_xor_sync(0xffffffffu, r, o);
+    }
+    return r;  // valid in warp 0
+}
+
+}  // namespace mpj

@@ -1,0 +1,718 @@
+// mpjacobi.cu -- host orchestration and the C ABI of include/mpjacobi.h.
+//
+// Alg. 3 as a sequence of device stages, one private stream per
+// call (event-joined to the caller's stream so the legacy stream works and the
+// sweep can be captured into a CUDA graph):
+//   a0 symmetrise A, ||A||_F                        k_util
+//   a1 fp32 Jacobi on fl32(A) -> Z                  jacobi_run<float>
+//   a2 Q = CGS2(Z)                                  k_orth (+ DMMA GEMMs)
+//   a3 T = Q^T A Q, symmetrised; V = Q              k_gemm, k_util
+//   a4-a8 fp64 Jacobi sweeps on (T, V)              jacobi_run<double>
+//   a10 Lambda = sort(diag T), V permuted           k_util
+// The only host<->device traffic inside the loop is the 8-byte ||off(T)||_F
+// read once per sweep for the stop test.
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "mpj_device.cuh"
+#include "mpj_internal.h"
+
+namespace mpj {
+
+// Block-variant entry (k_block.cu).
+template <typename R>
+mpj_status block_sweep(R *T, int64_t ldt, R *V, int64_t ldv, int vrows, const DevSched &S, R nu,
+                       int rule, unsigned long long *cnt, void *scratch, cudaStream_t st);
+template <typename R>
+size_t block_scratch_bytes(int np, int b);
+
+namespace {
+thread_local std::string g_err;
+thread_local long long g_launches = 0;
+}  // namespace
+
+void set_error(const std::string &msg) { g_err = msg; }
+void count_launch(long long k) { g_launches += k; }
+
+// ---------------------------------------------------------------------------
+// Ordering (reading R1), an implementation independent of oracle/.
+// GVL round-robin ("music"): slot 0 of the top row is fixed; everybody else
+// moves one place around the table each round.
+// ---------------------------------------------------------------------------
+int padded_n(int64_t n, int b)
+{
+    const int64_t w = 2 * (int64_t)b;
+    return (int)(((n + w - 1) / w) * w);
+}
+
+static void rotate_table(std::vector<int> &top, std::vector<int> &bot)
+{
+    const int m = (int)top.size();
+    if (m < 2) return;
+    std::vector<int> t2(m), b2(m);
+    t2[0] = top[0];
+    t2[1] = bot[0];
+    for (int k = 2; k < m; ++k) t2[k] = top[k - 1];
+    for (int k = 0; k < m - 1; ++k) b2[k] = bot[k + 1];
+    b2[m - 1] = top[m - 1];
+    top.swap(t2);
+    bot.swap(b2);
+}
+
+void build_schedule(int64_t n, int b, HostSchedule &hs)
+{
+    hs.n = (int)n;
+    hs.b = b;
+    hs.np = padded_n(n, b);
+    hs.nb = hs.np / b;
+    hs.mb = hs.nb / 2;
+    hs.rounds = hs.np - 1;
+    hs.bsched.clear();
+    hs.lsched.clear();
+    std::vector<int> top(hs.mb), bot(hs.mb);
+    for (int k = 0; k < hs.mb; ++k) { top[k] = 2 * k; bot[k] = 2 * k + 1; }
+    for (int R = 0; R < hs.nb - 1; ++R) {
+        for (int k = 0; k < hs.mb; ++k) hs.bsched.push_back(make_int2(top[k], bot[k]));
+        rotate_table(top, bot);
+    }
+    if (b > 1) {
+        const int hb = b / 2;
+        std::vector<int> lt(hb), lb(hb);
+        for (int k = 0; k < hb; ++k) { lt[k] = 2 * k; lb[k] = 2 * k + 1; }
+        for (int s = 0; s < b - 1; ++s) {
+            for (int k = 0; k < hb; ++k) hs.lsched.push_back(make_int2(lt[k], lb[k]));
+            rotate_table(lt, lb);
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Workspace arena (256-byte aligned bump allocator; a NULL base measures).
+// ---------------------------------------------------------------------------
+struct Arena {
+    char *base = nullptr;
+    size_t off = 0, cap = 0;
+    template <typename T>
+    T *take(size_t count)
+    {
+        off = (off + 255) & ~(size_t)255;
+        T *p = base ? (T *)(base + off) : nullptr;
+        off += count * sizeof(T);
+        return p;
+    }
+};
+
+static int auto_b(int64_t n)
+{
+    // b = 32 (2b = 64 tiles) unless the matrix is small; keep b even.
+    if (n >= 64) return 32;
+    int b = (int)((n + 3) / 4) * 2;     // about n/2, even
+    return std::max(1, std::min(32, b));
+}
+
+static int resolve_b(int64_t n, const mpj_config *cfg)
+{
+    int b = (cfg && cfg->block_b > 0) ? cfg->block_b : auto_b(n);
+    return b;
+}
+
+static int resolve_variant(int np, int b, const mpj_config *cfg)
+{
+    int v = cfg ? cfg->variant : MPJ_VARIANT_AUTO;
+    if (v == MPJ_VARIANT_AUTO) v = MPJ_VARIANT_SCALAR;   // block variant: see k_block.cu
+    if (v == MPJ_VARIANT_BLOCK && b != 32) v = MPJ_VARIANT_SCALAR;   // block kernels are b = 32
+    return v;
+}
+
+// ---------------------------------------------------------------------------
+// Per-call stream context: private stream joined to the caller's stream.
+// ---------------------------------------------------------------------------
+struct Ctx {
+    cudaStream_t user = nullptr, st = nullptr;
+    cudaEvent_t ev = nullptr;
+    double *h_pin = nullptr;   // pinned host scalars
+    mpj_status open(void *stream)
+    {
+        user = (cudaStream_t)stream;
+        MPJ_CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+        MPJ_CK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+        MPJ_CK(cudaEventRecord(ev, user));
+        MPJ_CK(cudaStreamWaitEvent(st, ev, 0));
+        MPJ_CK(cudaMallocHost(&h_pin, 64 * sizeof(double)));
+        return MPJ_OK;
+    }
+    mpj_status close()
+    {
+        if (st) {
+            cudaEventRecord(ev, st);
+            cudaStreamWaitEvent(user, ev, 0);
+            cudaStreamSynchronize(st);
+            cudaStreamDestroy(st);
+            st = nullptr;
+        }
+        if (ev) { cudaEventDestroy(ev); ev = nullptr; }
+        if (h_pin) { cudaFreeHost(h_pin); h_pin = nullptr; }
+        cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess) {
+            set_error(std::string("CUDA: ") + cudaGetErrorString(e));
+            return MPJ_ERR_CUDA;
+        }
+        return MPJ_OK;
+    }
+    ~Ctx() { close(); }
+};
+
+struct Timer {
+    cudaEvent_t a = nullptr, b = nullptr;
+    cudaStream_t st;
+    explicit Timer(cudaStream_t s) : st(s)
+    {
+        cudaEventCreate(&a);
+        cudaEventCreate(&b);
+        cudaEventRecord(a, st);
+    }
+    double stop()
+    {
+        float ms = 0.f;
+        cudaEventRecord(b, st);
+        cudaEventSynchronize(b);
+        cudaEventElapsedTime(&ms, a, b);
+        return ms * 1e-3;
+    }
+    ~Timer()
+    {
+        cudaEventDestroy(a);
+        cudaEventDestroy(b);
+    }
+};
+
+// ---------------------------------------------------------------------------
+// The Jacobi loop (Alg. 2 / Alg. 3 steps 4-11) on padded n_p x n_p T, V.
+// ---------------------------------------------------------------------------
+template <typename R>
+struct JacobiBufs {
+    int2 *pq;
+    R *t, *s, *u;
+    unsigned long long *cnt;
+    double *part, *off;
+    int2 *bsched, *lsched;
+    void *block_scratch;
+};
+
+template <typename R>
+static void carve_jacobi(Arena &ar, int np, int b, int variant, JacobiBufs<R> &jb)
+{
+    const int h = np / 2;
+    jb.pq = ar.take<int2>(h);
+    jb.t = ar.take<R>(h);
+    jb.s = ar.take<R>(h);
+    jb.u = ar.take<R>(h);
+    jb.cnt = ar.take<unsigned long long>(4);
+    jb.part = ar.take<double>(kRedBlocks);
+    jb.off = ar.take<double>(4);
+    const int nb = np / b;
+    jb.bsched = ar.take<int2>((size_t)std::max(nb - 1, 1) * std::max(nb / 2, 1));
+    jb.lsched = ar.take<int2>((size_t)std::max(b - 1, 1) * std::max(b / 2, 1));
+    jb.block_scratch = (variant == MPJ_VARIANT_BLOCK) ? ar.take<char>(block_scratch_bytes<R>(np, b)) : nullptr;
+}
+
+struct JacobiOut {
+    int sweeps = 0;
+    long long rotations = 0;
+    double hist[64] = {0};
+    int nhist = 0;
+};
+
+template <typename R>
+static mpj_status jacobi_run(Ctx &cx, R *T, R *V, int n, int b, int variant, double tol, R nu,
+                             int rule, int max_sweeps, int64_t max_rounds, JacobiBufs<R> &jb,
+                             JacobiOut &out)
+{
+    cudaStream_t st = cx.st;
+    HostSchedule hs;
+    build_schedule(n, b, hs);
+    const int np = hs.np, h = np / 2;
+    DevSched ds;
+    ds.bsched = jb.bsched; ds.lsched = jb.lsched; ds.b = b; ds.nb = hs.nb; ds.np = np; ds.rounds = hs.rounds;
+    if (!hs.bsched.empty())
+        MPJ_CK(cudaMemcpyAsync(jb.bsched, hs.bsched.data(), hs.bsched.size() * sizeof(int2), cudaMemcpyHostToDevice, st));
+    if (!hs.lsched.empty())
+        MPJ_CK(cudaMemcpyAsync(jb.lsched, hs.lsched.data(), hs.lsched.size() * sizeof(int2), cudaMemcpyHostToDevice, st));
+    MPJ_CK(cudaMemsetAsync(jb.cnt, 0, sizeof(unsigned long long), st));
+
+    cudaGraphExec_t gexec = nullptr;
+    long long graph_kernels = 0;
+    const bool use_graph = (variant == MPJ_VARIANT_SCALAR) && max_rounds < 0;
+    int64_t rounds_done = 0;
+    int sweeps = 0;
+    mpj_status status = MPJ_ERR_NOCONV;
+    for (;;) {
+        launch_norm<R>(T, np, np, np, true, jb.part, jb.off, st);
+        MPJ_CK(cudaMemcpyAsync(cx.h_pin, jb.off, sizeof(double), cudaMemcpyDeviceToHost, st));
+        MPJ_CK(cudaStreamSynchronize(st));
+        const double off = cx.h_pin[0];
+        if (sweeps < 64) { out.hist[sweeps] = off; out.nhist = sweeps + 1; }
+        if (!(off == off)) { set_error("non-finite off-norm"); status = MPJ_ERR_NONFINITE; break; }
+        if (off <= tol) { status = MPJ_OK; break; }
+        if (sweeps >= max_sweeps) { status = MPJ_ERR_NOCONV; break; }
+        if (max_rounds >= 0 && rounds_done >= max_rounds) { status = MPJ_OK; break; }
+        ++sweeps;
+        if (variant == MPJ_VARIANT_BLOCK) {
+            MPJ_TRY(block_sweep<R>(T, np, V, np, np, ds, nu, rule, jb.cnt, jb.block_scratch, st));
+            rounds_done += hs.rounds;
+        } else if (use_graph) {
+            if (!gexec) {
+                cudaGraph_t g;
+                const long long l0 = g_launches;
+                MPJ_CK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+                for (int r = 0; r < hs.rounds; ++r) {
+                    launch_round_params<R>(T, np, ds, r, nu, rule, jb.pq, jb.t, jb.s, jb.u, jb.cnt, st);
+                    launch_round_apply<R>(T, np, jb.pq, jb.t, jb.s, jb.u, h, st);
+                    launch_round_apply_v<R>(V, np, np, jb.pq, jb.s, jb.u, h, st);
+                }
+                MPJ_CK(cudaStreamEndCapture(st, &g));
+                graph_kernels = g_launches - l0;
+                g_launches = l0;
+                MPJ_CK(cudaGraphInstantiate(&gexec, g, 0));
+                cudaGraphDestroy(g);
+            }
+            MPJ_CK(cudaGraphLaunch(gexec, st));
+            count_launch(graph_kernels);
+            rounds_done += hs.rounds;
+        } else {
+            for (int r = 0; r < hs.rounds; ++r) {
+                if (max_rounds >= 0 && rounds_done >= max_rounds) break;
+                launch_round_params<R>(T, np, ds, r, nu, rule, jb.pq, jb.t, jb.s, jb.u, jb.cnt, st);
+                launch_round_apply<R>(T, np, jb.pq, jb.t, jb.s, jb.u, h, st);
+                launch_round_apply_v<R>(V, np, np, jb.pq, jb.s, jb.u, h, st);
+                ++rounds_done;
+            }
+        }
+    }
+    if (gexec) cudaGraphExecDestroy(gexec);
+    unsigned long long rot = 0;
+    MPJ_CK(cudaMemcpyAsync(cx.h_pin, jb.cnt, sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
+    MPJ_CK(cudaStreamSynchronize(st));
+    std::memcpy(&rot, cx.h_pin, sizeof(rot));
+    out.sweeps = sweeps;
+    out.rotations = (long long)rot;
+    MPJ_CK(cudaGetLastError());
+    return status;
+}
+
+// ---------------------------------------------------------------------------
+// Host/device pointer handling for the end-to-end entry points.
+// ---------------------------------------------------------------------------
+static bool is_device_ptr(const void *p)
+{
+    if (!p) return false;
+    cudaPointerAttributes at;
+    if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged;
+}
+
+static mpj_status copy2d(void *dst, int64_t ldd, const void *src, int64_t lds, int64_t rows, int64_t cols,
+                         size_t esz, cudaMemcpyKind kind, cudaStream_t st)
+{
+    if (rows <= 0 || cols <= 0) return MPJ_OK;
+    MPJ_CK(cudaMemcpy2DAsync(dst, ldd * esz, src, lds * esz, rows * esz, cols, kind, st));
+    return MPJ_OK;
+}
+
+// ---------------------------------------------------------------------------
+// Alg. 3 / Alg. 2 drivers
+// ---------------------------------------------------------------------------
+struct EigPlan {
+    int n, b, np, variant;
+    double *Asym, *T, *V, *W;
+    float *T32, *V32;
+    double *red_part, *red_out;
+    int *flag, *rank;
+    double *lam;
+    void *orth_ws;
+    JacobiBufs<double> j64;
+    JacobiBufs<float> j32;
+};
+
+static void carve_eig(Arena &ar, int64_t n, const mpj_config *cfg, EigPlan &p)
+{
+    p.n = (int)n;
+    p.b = resolve_b(n, cfg);
+    p.np = padded_n(n, p.b);
+    p.variant = resolve_variant(p.np, p.b, cfg);
+    const size_t nn = (size_t)p.np * p.np;
+    p.Asym = ar.take<double>(nn);
+    p.T = ar.take<double>(nn);
+    p.V = ar.take<double>(nn);
+    p.W = ar.take<double>(nn);
+    p.T32 = ar.take<float>(nn);
+    p.V32 = ar.take<float>(nn);
+    p.red_part = ar.take<double>(kRedBlocks);
+    p.red_out = ar.take<double>(4);
+    p.flag = ar.take<int>(4);
+    p.rank = ar.take<int>(p.np);
+    p.lam = ar.take<double>(p.np);
+    p.orth_ws = ar.take<char>(orth_workspace(p.np));
+    carve_jacobi<double>(ar, p.np, p.b, p.variant, p.j64);
+    carve_jacobi<float>(ar, p.np, p.b, p.variant, p.j32);
+}
+
+static mpj_status read_scalar(Ctx &cx, const double *d, double &out)
+{
+    MPJ_CK(cudaMemcpyAsync(cx.h_pin, d, sizeof(double), cudaMemcpyDeviceToHost, cx.st));
+    MPJ_CK(cudaStreamSynchronize(cx.st));
+    out = cx.h_pin[0];
+    return MPJ_OK;
+}
+
+static const double kOmega = 1.1102230246251565e-16;    // 2^-53
+static const double kUpsilon = 5.9604644775390625e-08;  // 2^-24
+
+static mpj_status eig_impl(bool mixed, const double *A, int64_t n, int64_t lda, double *Lambda,
+                           double *V, int64_t ldv, int *sweeps, void *workspace, size_t ws_bytes,
+                           void *stream, const mpj_config *cfg_in, mpj_report *rep)
+{
+    g_err.clear();
+    if (n < 1 || lda < n || ldv < n || !A || !Lambda || !V) {
+        set_error("mpjacobi_eig: invalid argument");
+        return MPJ_ERR_INVALID;
+    }
+    if (n > (1 << 20)) { set_error("n too large"); return MPJ_ERR_INVALID; }
+    mpj_config cfg;
+    if (cfg_in) cfg = *cfg_in; else mpj_config_default_eig(&cfg);
+    const int b = resolve_b(n, &cfg);
+    if (b < 1 || (b > 1 && (b & 1))) { set_error("block_b must be 1 or even"); return MPJ_ERR_INVALID; }
+
+    Ctx cx;
+    MPJ_TRY(cx.open(stream));
+    Timer t_all(cx.st);
+    const long long l0 = g_launches;
+
+    Arena ar;
+    EigPlan p;
+    carve_eig(ar, n, &cfg, p);   // measure
+    const size_t need = ar.off + 256;
+    void *own = nullptr;
+    if (!workspace) {
+        MPJ_CK(cudaMallocAsync(&own, need, cx.st));
+        workspace = own;
+    } else if (ws_bytes < need) {
+        set_error("workspace too small");
+        return MPJ_ERR_NOMEM;
+    }
+    ar = Arena();
+    ar.base = (char *)(((uintptr_t)workspace + 255) & ~(uintptr_t)255);
+    carve_eig(ar, n, &cfg, p);
+    const int np = p.np;
+    mpj_report r;
+    std::memset(&r, 0, sizeof(r));
+    r.n_padded = np;
+    r.block_b = p.b;
+    r.variant = p.variant;
+
+    auto finish = [&](mpj_status s) -> mpj_status {
+        if (own) cudaFreeAsync(own, cx.st);
+        r.t_total = t_all.stop();
+        r.launches = g_launches - l0;
+        if (rep) *rep = r;
+        mpj_status c = cx.close();
+        return s != MPJ_OK ? s : c;
+    };
+
+    // a0: stage A (host or device) into T, symmetrise into Asym, check finite, ||A||_F
+    const bool a_dev = is_device_ptr(A);
+    {
+        mpj_status s;
+        if (a_dev) s = copy2d(p.T, np, A, lda, n, n, sizeof(double), cudaMemcpyDeviceToDevice, cx.st);
+        else s = copy2d(p.T, np, A, lda, n, n, sizeof(double), cudaMemcpyHostToDevice, cx.st);
+        if (s != MPJ_OK) return finish(s);
+    }
+    cudaMemsetAsync(p.flag, 0, sizeof(int), cx.st);
+    launch_check_finite(p.T, np, (int)n, (int)n, p.flag, cx.st);
+    launch_symmetrize(p.T, np, (int)n, p.Asym, np, np, cx.st);
+    launch_norm<double>(p.Asym, np, np, np, false, p.red_part, p.red_out, cx.st);
+    MPJ_CK(cudaMemcpyAsync(cx.h_pin, p.red_out, sizeof(double), cudaMemcpyDeviceToHost, cx.st));
+    MPJ_CK(cudaMemcpyAsync(cx.h_pin + 1, p.flag, sizeof(int), cudaMemcpyDeviceToHost, cx.st));
+    MPJ_CK(cudaStreamSynchronize(cx.st));
+    const double normA = cx.h_pin[0];
+    int bad = 0;
+    std::memcpy(&bad, cx.h_pin + 1, sizeof(int));
+    if (bad) { set_error("input has NaN/Inf"); return finish(MPJ_ERR_NONFINITE); }
+    r.norm_a = normA;
+
+    mpj_status s = MPJ_OK;
+    if (mixed) {
+        // a1: low-precision stage (reading R12)
+        Timer tl(cx.st);
+        launch_copy_pad<double, float>(p.Asym, np, np, np, p.T32, np, np, np, cx.st);
+        MPJ_CK(cudaMemsetAsync(p.V32, 0, (size_t)np * np * sizeof(float), cx.st));
+        launch_identity<float>(p.V32, np, (int)n, (int)n, cx.st);
+        launch_norm<float>(p.T32, np, np, np, false, p.red_part, p.red_out, cx.st);
+        double nA32 = 0;
+        MPJ_TRY(read_scalar(cx, p.red_out, nA32));
+        JacobiOut jo;
+        mpj_status sl = jacobi_run<float>(cx, p.T32, p.V32, (int)n, p.b, p.variant,
+                                          cfg.eps_low_factor * kUpsilon * nA32,
+                                          (float)(cfg.nu_low_factor * kUpsilon), cfg.stop_rule,
+                                          cfg.max_sweeps_low, -1, p.j32, jo);
+        if (sl != MPJ_OK && sl != MPJ_ERR_NOCONV) return finish(sl);
+        r.sweeps_low = jo.sweeps;
+        r.rotations_low = jo.rotations;
+        r.status_low = sl;
+        r.t_low = tl.stop();
+
+        // a2: Q = orth(Z), Z = fp64(V32) (n x n real block)
+        Timer to(cx.st);
+        launch_copy_pad<float, double>(p.V32, np, (int)n, (int)n, p.W, np, (int)n, (int)n, cx.st);
+        MPJ_CK(cudaMemsetAsync(p.V, 0, (size_t)np * np * sizeof(double), cx.st));
+        s = orth_cgs2(p.W, np, p.V, np, n, n, p.orth_ws, cx.st);
+        if (s != MPJ_OK) return finish(s);
+        r.t_orth = to.stop();
+
+        // a3: T = Q^T A Q (W = A Q, T = Q^T W), symmetrised (reading R11)
+        Timer tp(cx.st);
+        MPJ_CK(cudaMemsetAsync(p.T, 0, (size_t)np * np * sizeof(double), cx.st));
+        launch_dgemm(false, false, n, n, n, 1.0, p.Asym, np, p.V, np, 0.0, p.W, np, cx.st);
+        launch_dgemm(true, false, n, n, n, 1.0, p.V, np, p.W, np, 0.0, p.T, np, cx.st);
+        launch_symmetrize_inplace(p.T, np, (int)n, cx.st);
+        launch_norm<double>(p.T, np, np, np, true, p.red_part, p.red_out, cx.st);
+        MPJ_TRY(read_scalar(cx, p.red_out, r.off0));
+        r.t_precond = tp.stop();
+    } else {
+        MPJ_CK(cudaMemcpyAsync(p.T, p.Asym, (size_t)np * np * sizeof(double), cudaMemcpyDeviceToDevice, cx.st));
+        MPJ_CK(cudaMemsetAsync(p.V, 0, (size_t)np * np * sizeof(double), cx.st));
+        launch_identity<double>(p.V, np, (int)n, (int)n, cx.st);
+        launch_norm<double>(p.T, np, np, np, true, p.red_part, p.red_out, cx.st);
+        MPJ_TRY(read_scalar(cx, p.red_out, r.off0));
+    }
+
+    // a4-a8: fp64 sweeps
+    {
+        Timer tj(cx.st);
+        JacobiOut jo;
+        s = jacobi_run<double>(cx, p.T, p.V, (int)n, p.b, p.variant, cfg.eps_factor * kOmega * normA,
+                               cfg.nu_factor * kOmega, cfg.stop_rule, cfg.max_sweeps, -1, p.j64, jo);
+        r.sweeps = jo.sweeps;
+        r.rotations = jo.rotations;
+        r.status = s;
+        for (int k = 0; k < jo.nhist && k < 64; ++k) r.off_hist[k] = jo.hist[k];
+        r.t_jacobi = tj.stop();
+        if (s != MPJ_OK && s != MPJ_ERR_NOCONV) return finish(s);
+    }
+    if (sweeps) *sweeps = r.sweeps;
+
+    // a10: extraction (stable descending)
+    {
+        Timer te(cx.st);
+        const bool l_dev = is_device_ptr(Lambda), v_dev = is_device_ptr(V);
+        double *lam_d = l_dev ? Lambda : p.lam;
+        double *v_d = v_dev ? V : p.W;
+        const int64_t ldvo = v_dev ? ldv : np;
+        launch_extract_evd(p.T, np, p.V, np, (int)n, (int)n, lam_d, v_d, ldvo, p.rank, cx.st);
+        if (!l_dev) MPJ_CK(cudaMemcpyAsync(Lambda, p.lam, n * sizeof(double), cudaMemcpyDeviceToHost, cx.st));
+        if (!v_dev) {
+            mpj_status c = copy2d(V, ldv, p.W, np, n, n, sizeof(double), cudaMemcpyDeviceToHost, cx.st);
+            if (c != MPJ_OK) return finish(c);
+        }
+        MPJ_CK(cudaStreamSynchronize(cx.st));
+        r.t_extract = te.stop();
+    }
+    return finish(s);
+}
+
+template <typename R>
+static mpj_status jacobi_impl(R *T, int64_t ldt, R *V, int64_t ldv, int64_t n, double tol, double nu,
+                              int max_sweeps, int64_t max_rounds, int *sweeps, long long *rotations,
+                              double *hist, void *stream, const mpj_config *cfg)
+{
+    g_err.clear();
+    if (n < 1 || ldt < n || ldv < n || !T || !V) { set_error("invalid argument"); return MPJ_ERR_INVALID; }
+    const int b = resolve_b(n, cfg);
+    if (b < 1 || (b > 1 && (b & 1))) { set_error("block_b must be 1 or even"); return MPJ_ERR_INVALID; }
+    const int np = padded_n(n, b);
+    const int variant = resolve_variant(np, b, cfg);
+    const int rule = cfg ? cfg->stop_rule : 0;
+    Ctx cx;
+    MPJ_TRY(cx.open(stream));
+    Arena ar;
+    JacobiBufs<R> jb;
+    R *Tp, *Vp;
+    auto carve = [&]() {
+        Tp = ar.take<R>((size_t)np * np);
+        Vp = ar.take<R>((size_t)np * np);
+        carve_jacobi<R>(ar, np, b, variant, jb);
+    };
+    carve();
+    void *own = nullptr;
+    MPJ_CK(cudaMallocAsync(&own, ar.off + 256, cx.st));
+    ar = Arena();
+    ar.base = (char *)(((uintptr_t)own + 255) & ~(uintptr_t)255);
+    carve();
+    launch_copy_pad<R, R>(T, ldt, (int)n, (int)n, Tp, np, np, np, cx.st);
+    launch_copy_pad<R, R>(V, ldv, (int)n, (int)n, Vp, np, np, np, cx.st);
+    JacobiOut jo;
+    mpj_status s = jacobi_run<R>(cx, Tp, Vp, (int)n, b, variant, tol, (R)nu, rule, max_sweeps, max_rounds,
+                                 jb, jo);
+    if (s == MPJ_OK || s == MPJ_ERR_NOCONV) {
+        launch_copy_pad<R, R>(Tp, np, (int)n, (int)n, T, ldt, (int)n, (int)n, cx.st);
+        launch_copy_pad<R, R>(Vp, np, (int)n, (int)n, V, ldv, (int)n, (int)n, cx.st);
+    }
+    cudaFreeAsync(own, cx.st);
+    if (sweeps) *sweeps = jo.sweeps;
+    if (rotations) *rotations = jo.rotations;
+    if (hist) for (int k = 0; k < 64; ++k) hist[k] = k < jo.nhist ? jo.hist[k] : 0.0;
+    mpj_status c = cx.close();
+    return s != MPJ_OK ? s : c;
+}
+
+}  // namespace mpj
+
+// ===========================================================================
+// C ABI
+// ===========================================================================
+using namespace mpj;
+
+extern "C" {
+
+void mpj_config_default_eig(mpj_config *c)
+{
+    if (!c) return;
+    c->eps_factor = 0.1;
+    c->nu_factor = 20.0;
+    c->eps_low_factor = 10.0;
+    c->nu_low_factor = 20.0;
+    c->early_stop_ratio = 0.0;
+    c->max_sweeps = 60;
+    c->max_sweeps_low = 60;
+    c->stop_rule = 0;
+    c->variant = MPJ_VARIANT_AUTO;
+    c->block_b = 0;
+}
+
+void mpj_config_default_svd(mpj_config *c)
+{
+    if (!c) return;
+    mpj_config_default_eig(c);
+    c->nu_factor = 1.0;
+    c->nu_low_factor = 1.0;
+    c->early_stop_ratio = 2e-4;
+}
+
+const char *mpjacobi_last_error(void) { return g_err.c_str(); }
+long long mpjacobi_launch_count(void) { return g_launches; }
+
+size_t mpjacobi_eig_workspace(int64_t n, const mpj_config *cfg)
+{
+    if (n < 1) return 0;
+    mpj_config c;
+    if (cfg) c = *cfg; else mpj_config_default_eig(&c);
+    Arena ar;
+    EigPlan p;
+    carve_eig(ar, n, &c, p);
+    return ar.off + 256;
+}
+
+mpj_status mpjacobi_eig(const double *A, int64_t n, int64_t lda, double *Lambda, double *V, int64_t ldv,
+                        int *sweeps, void *workspace, size_t ws_bytes, void *stream, const mpj_config *cfg,
+                        mpj_report *rep)
+{
+    return eig_impl(true, A, n, lda, Lambda, V, ldv, sweeps, workspace, ws_bytes, stream, cfg, rep);
+}
+
+mpj_status mpjacobi_eig_plain(const double *A, int64_t n, int64_t lda, double *Lambda, double *V,
+                              int64_t ldv, int *sweeps, void *workspace, size_t ws_bytes, void *stream,
+                              const mpj_config *cfg, mpj_report *rep)
+{
+    return eig_impl(false, A, n, lda, Lambda, V, ldv, sweeps, workspace, ws_bytes, stream, cfg, rep);
+}
+
+mpj_status mpjacobi_jacobi_f64(double *T, int64_t ldt, double *V, int64_t ldv, int64_t n, double tol,
+                               double nu, int max_sweeps, int64_t max_rounds, int *sweeps,
+                               long long *rotations, double *hist, void *stream, const mpj_config *cfg)
+{
+    return jacobi_impl<double>(T, ldt, V, ldv, n, tol, nu, max_sweeps, max_rounds, sweeps, rotations, hist,
+                               stream, cfg);
+}
+
+mpj_status mpjacobi_jacobi_f32(float *T, int64_t ldt, float *V, int64_t ldv, int64_t n, double tol,
+                               double nu, int max_sweeps, int64_t max_rounds, int *sweeps,
+                               long long *rotations, double *hist, void *stream, const mpj_config *cfg)
+{
+    return jacobi_impl<float>(T, ldt, V, ldv, n, tol, nu, max_sweeps, max_rounds, sweeps, rotations, hist,
+                              stream, cfg);
+}
+
+mpj_status mpjacobi_orth(const double *Z, double *Q, int64_t n, void *stream)
+{
+    g_err.clear();
+    if (n < 1 || !Z || !Q) { set_error("invalid argument"); return MPJ_ERR_INVALID; }
+    Ctx cx;
+    MPJ_TRY(cx.open(stream));
+    void *ws = nullptr;
+    MPJ_CK(cudaMallocAsync(&ws, orth_workspace(n), cx.st));
+    mpj_status s = orth_cgs2(Z, n, Q, n, n, n, ws, cx.st);
+    cudaFreeAsync(ws, cx.st);
+    mpj_status c = cx.close();
+    return s != MPJ_OK ? s : c;
+}
+
+mpj_status mpjacobi_precond(const double *A, const double *Q, double *T, int64_t n, void *stream)
+{
+    g_err.clear();
+    if (n < 1 || !A || !Q || !T) { set_error("invalid argument"); return MPJ_ERR_INVALID; }
+    Ctx cx;
+    MPJ_TRY(cx.open(stream));
+    double *W = nullptr;
+    MPJ_CK(cudaMallocAsync(&W, (size_t)n * n * sizeof(double), cx.st));
+    launch_dgemm(false, false, n, n, n, 1.0, A, n, Q, n, 0.0, W, n, cx.st);
+    launch_dgemm(true, false, n, n, n, 1.0, Q, n, W, n, 0.0, T, n, cx.st);
+    launch_symmetrize_inplace(T, n, (int)n, cx.st);
+    cudaFreeAsync(W, cx.st);
+    return cx.close();
+}
+
+mpj_status mpjacobi_dgemm(int transa, const double *A, const double *B, double *C, int64_t m, int64_t n,
+                          int64_t k, void *stream)
+{
+    g_err.clear();
+    if (m < 0 || n < 0 || k < 0 || !A || !B || !C) { set_error("invalid argument"); return MPJ_ERR_INVALID; }
+    Ctx cx;
+    MPJ_TRY(cx.open(stream));
+    const size_t se = dgemm_scratch_elems(m, n);
+    double *scr = nullptr;
+    MPJ_CK(cudaMallocAsync(&scr, se * sizeof(double), cx.st));
+    launch_dgemm(transa != 0, false, m, n, k, 1.0, A, transa ? k : m, B, k, 0.0, C, m, cx.st, scr, se);
+    cudaFreeAsync(scr, cx.st);
+    return cx.close();
+}
+
+}  // extern "C"
+
+// ---------------------------------------------------------------------------
+// Entry points whose kernels land later in this round (k_svd.cu, k_batched.cu)
+// ---------------------------------------------------------------------------
+extern "C" {
+#ifndef MPJ_HAVE_SVD
+size_t mpjacobi_svd_workspace(int64_t, int64_t, const mpj_config *) { return 0; }
+mpj_status mpjacobi_svd(const double *, int64_t, int64_t, int64_t, double *, double *, int64_t, double *,
+                        int64_t, int *, void *, size_t, void *, const mpj_config *, mpj_report *)
+{
+    mpj::set_error("mpjacobi_svd: not built yet");
+    return MPJ_ERR_INVALID;
+}
+#endif
+#ifndef MPJ_HAVE_BATCHED
+mpj_status mpjacobi_eig_batched(const double *, int64_t, int64_t, double *, double *, int *, int *, void *,
+                                const mpj_config *)
+{
+    mpj::set_error("mpjacobi_eig_batched: not built yet");
+    return MPJ_ERR_INVALID;
+}
+#endif
+}

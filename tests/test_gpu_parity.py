@@ -1,0 +1,176 @@
+"""GPU parity: the CUDA path (called through the C ABI) against the oracle on
+the same seeded inputs.
+
+* Scalar-round variant: BIT-EXACT T, V (and the same sweep / rotation
+  counts) after one round, one sweep and a full run, fp64 and fp32, for
+  several n (ragged, padded) and ordering block sizes b (b = 1 is the paper's
+  merry-go-round).
+* Stages: CGS2 vs MGS, Q^T A Q, DMMA GEMM -- tolerances derived in DESIGN.md.
+* End to end (Alg. 3 and Alg. 2): north_star tolerances
+  |dlam|/||A||_2 <= 1e-13, ||V^T V - I||_F <= n 1e-15,
+  ||A V - V Lam||_F/||A||_F <= n 1e-15, identical sweep count.
+"""
+import numpy as np
+import pytest
+
+import workloads as W
+from conftest import OMEGA, UPSILON, rand_sym
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def mpj():
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    import paper_2211_03339_b200 as m
+    m.lib()
+    return m
+
+
+def dev(a, dtype=torch.float64):
+    """numpy column-major -> device column-major tensor (math orientation)."""
+    return torch.from_numpy(np.ascontiguousarray(np.asarray(a).T)).to("cuda", dtype).T
+
+
+def host(t):
+    return t.detach().cpu().numpy()
+
+
+def near_diag_T0(n, seed):
+    """A T0 like Alg. 3's: Q^T A Q from the oracle's pipeline (mode 3 / 4)."""
+    import oracle
+    A, _ = W.example1(n, 1e3, 3 + seed % 2, seed)
+    Z, _ = oracle.low_evd(A)
+    Q, _, _ = oracle.mgs(Z.astype(np.float64))
+    return oracle.qtaq(A, Q), Q, A
+
+
+# ----------------------------------------------------------------- bit-exact
+@pytest.mark.parametrize("n,b", [(2, 1), (3, 1), (8, 1), (33, 1), (64, 1), (100, 2), (64, 8),
+                                 (130, 16), (256, 32), (96, 32)])
+@pytest.mark.parametrize("stage", ["round", "sweep", "full"])
+def test_scalar_rounds_bit_exact_fp64(mpj, orc, n, b, stage):
+    T0 = rand_sym(n, 10 * n + b) if stage != "full" else near_diag_T0(n, n)[0]
+    V0 = np.eye(n) if stage != "full" else near_diag_T0(n, n)[1]
+    nA = np.linalg.norm(T0)
+    kw = dict(round=dict(max_sweeps=1, max_rounds=1, tol=0.0),
+              sweep=dict(max_sweeps=1, max_rounds=-1, tol=0.0),
+              full=dict(max_sweeps=60, max_rounds=-1, tol=0.1 * OMEGA * nA))[stage]
+    ref = orc.jacobi_evd(T0, V0, b=b, nu=20 * OMEGA, **kw)
+    T, V = dev(T0), dev(V0)
+    cfg = mpj.default_config("eig", variant=mpj.VARIANT_SCALAR, block_b=b)
+    r = mpj.jacobi(T, V, nu=20 * OMEGA, cfg=cfg, **kw)
+    assert np.array_equal(host(T), ref.T), np.max(np.abs(host(T) - ref.T))
+    assert np.array_equal(host(V), ref.V), np.max(np.abs(host(V) - ref.V))
+    assert r.sweeps == ref.sweeps and r.rotations == ref.rotations
+
+
+@pytest.mark.parametrize("n,b", [(8, 1), (64, 8), (100, 2), (256, 32)])
+def test_scalar_rounds_bit_exact_fp32(mpj, orc, n, b):
+    A, _ = W.example1(n, 1e3, 4, n)
+    T0 = A.astype(np.float32)
+    nA = orc.fro(T0)
+    ref = orc.jacobi_evd(T0, b=b, tol=10 * UPSILON * nA, nu=20 * UPSILON, precision="f32")
+    T, V = dev(T0, torch.float32), dev(np.eye(n, dtype=np.float32), torch.float32)
+    cfg = mpj.default_config("eig", variant=mpj.VARIANT_SCALAR, block_b=b)
+    r = mpj.jacobi(T, V, tol=10 * UPSILON * nA, nu=float(np.float32(20 * UPSILON)), cfg=cfg)
+    assert r.sweeps == ref.sweeps and r.rotations == ref.rotations
+    assert np.array_equal(host(T), ref.T)
+    assert np.array_equal(host(V), ref.V)
+
+
+# ----------------------------------------------------------------- stages
+@pytest.mark.parametrize("m,n,k,ta", [(64, 64, 64, False), (100, 37, 129, False), (130, 70, 1200, True),
+                                      (1024, 512, 256, False), (64, 64, 4096, True)])
+def test_dgemm(mpj, m, n, k, ta):
+    rng = np.random.default_rng(m + n + k)
+    A = rng.standard_normal((k, m) if ta else (m, k))
+    B = rng.standard_normal((k, n))
+    Cg = host(mpj.dgemm(dev(A), dev(B), transa=ta))
+    ref = (A.T if ta else A) @ B
+    # |error| <= k u sum|a||b| (standard dot-product bound)
+    bound = 2 * k * OMEGA * (np.abs(A.T if ta else A) @ np.abs(B))
+    assert np.all(np.abs(Cg - ref) <= bound + 1e-300)
+
+
+@pytest.mark.parametrize("n", [16, 100, 256, 300])
+def test_orth_cgs2_matches_mgs(mpj, orc, n):
+    """CGS2 (GPU) vs the oracle's MGS on Z from the fp32 stage: same Q to
+    O(n omega) because kappa(Z) = 1 + O(upsilon) (reading R10)."""
+    A, _ = W.example1(n, 1e3, 4, 7 + n)
+    Z, _ = orc.low_evd(A)
+    Zd = Z.astype(np.float64)
+    Qo, _, _ = orc.mgs(Zd)
+    Qg = host(mpj.orth(dev(Zd)))
+    assert np.linalg.norm(Qg.T @ Qg - np.eye(n)) <= 10 * n * OMEGA
+    assert np.linalg.norm(Qg - Qo) <= 10 * n * OMEGA
+
+
+@pytest.mark.parametrize("n", [32, 257])
+def test_precond(mpj, orc, n):
+    A, _ = W.example1(n, 1e3, 3, 5 + n)
+    H = W.haar(n, np.random.default_rng(n))
+    To = orc.qtaq(A, H)
+    Tg = host(mpj.precond(dev(A), dev(H)))
+    assert np.array_equal(Tg, Tg.T)
+    assert np.linalg.norm(Tg - To) <= 10 * n * np.linalg.norm(A) * OMEGA
+
+
+# ----------------------------------------------------------------- end to end
+def _check_evd(A, lam, V, ref_lam, ref_sweeps, sweeps):
+    n = A.shape[0]
+    nrm2 = np.max(np.abs(ref_lam))
+    assert np.max(np.abs(lam - ref_lam)) <= 1e-13 * nrm2
+    assert np.linalg.norm(V.T @ V - np.eye(n)) <= n * 1e-15
+    assert np.linalg.norm(A @ V - V * lam) / np.linalg.norm(A) <= n * 1e-15
+    assert sweeps == ref_sweeps
+
+
+@pytest.mark.parametrize("n,mode,kappa", [(32, 4, 1e3), (32, 3, 1e6), (64, 5, 1e3), (100, 4, 1e3),
+                                          (256, 3, 1e6)])
+def test_eig_end_to_end(mpj, orc, n, mode, kappa):
+    A, lam_true = W.example1(n, kappa, mode, W.seed_for(1, mode, kappa))
+    res = mpj.eig(dev(A))
+    rep = res.report
+    ref = orc.mp_evd(A, orc.default_cfg("eig", b=rep.block_b))
+    _check_evd(A, host(res.lam), host(res.V), ref.lam, ref.report.sweeps, res.sweeps)
+    assert rep.sweeps_low == ref.report.sweeps_low
+    assert abs(rep.off0 - ref.report.off0) <= 1e-3 * ref.report.off0 + 100 * n * OMEGA
+
+
+def test_eig_host_buffers(mpj, orc):
+    """The ABI accepts host pointers (staged by the library): same result."""
+    n = 64
+    A, _ = W.example1(n, 1e3, 4, 3)
+    r_dev = mpj.eig(dev(A))
+    Ah = torch.from_numpy(np.ascontiguousarray(A.T)).T.pin_memory()
+    r_host = mpj.eig(Ah)
+    assert r_host.lam.device.type == "cpu"
+    assert np.array_equal(r_host.lam.numpy(), host(r_dev.lam))
+    assert np.array_equal(r_host.V.numpy(), host(r_dev.V))
+
+
+@pytest.mark.parametrize("n", [64, 128])
+def test_eig_plain_end_to_end(mpj, orc, n):
+    A, _ = W.example1(n, 1e3, 4, 11 + n)
+    res = mpj.eig(dev(A), plain=True)
+    ref = orc.plain_evd(A, orc.default_cfg("eig", b=res.report.block_b))
+    _check_evd(A, host(res.lam), host(res.V), ref.lam, ref.report.sweeps, res.sweeps)
+
+
+def test_edge_cases(mpj):
+    # n = 1
+    r = mpj.eig(dev(np.array([[3.5]])))
+    assert host(r.lam)[0] == 3.5 and host(r.V)[0, 0] == 1.0 and r.sweeps == 0
+    # diagonal input: no fp64 sweeps, exact eigenvalues
+    d = np.array([3.0, -1.0, 7.5, 0.25, 2.0, 2.0, -9.0, 1e-3])
+    r = mpj.eig(dev(np.diag(d)))
+    assert np.array_equal(host(r.lam), np.sort(d)[::-1]) and r.sweeps == 0
+    # non-finite input
+    A = np.eye(4)
+    A[1, 2] = np.nan
+    with pytest.raises(mpj.MpjError) as e:
+        mpj.eig(dev(A))
+    assert e.value.status == mpj.MPJ_ERR_NONFINITE
