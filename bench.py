@@ -1,0 +1,370 @@
+#!/usr/bin/env python
+"""Benchmark of the mixed-precision Jacobi EVD (Alg. 3, arXiv 2211.03339) on B200.
+
+Metric (BASELINE.json): fp64 EVD seconds at n = 8192 (graded spectrum,
+Example 1 mode 3, kappa = 1e6; BASELINE config 4), sweeps, % of roofline.
+A "step" is one full Alg. 3 EVD (fp32 stage, CGS2, Q^T A Q, fp64 sweeps,
+extraction) of one n x n matrix through the C ABI.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--n 8192]
+
+Prints ONE JSON line (rank 0).  --impl reference times the oracle (plain C,
+oracle/) on the host cores on a bounded sample of the same workload and
+extrapolates to seconds per EVD (the only other place the oracle runs).
+Multi-GPU (torchrun, N > 1): every rank runs its own replica of the workload
+("replicas only": the column-partitioned NCCL path is not built yet, see
+DESIGN.md); the device time is the max over ranks.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+OMEGA = 2.0 ** -53
+UPSILON = 2.0 ** -24
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--n", type=int, default=8192)
+    ap.add_argument("--mode", type=int, default=3)
+    ap.add_argument("--kappa", type=float, default=1e6)
+    ap.add_argument("--variant", type=int, default=0, help="0 auto, 1 scalar rounds, 2 block")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-sample-seconds", type=float, default=20.0)
+    return ap.parse_args()
+
+
+def peaks():
+    """Roofline denominators.  HBM / bf16 from the driver-written
+    MEASURED_PEAKS.json; FP64 (DMMA / DFMA) and FP32 (FFMA) from
+    profiles/r01_fp64_fp32_peaks.json (tools/fp64_peak.cu on this pool's B200)."""
+    out = {"hbm_gbs": 6650.0, "hbm_src": "fallback (B200_PROFILING.md)"}
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        m = json.load(open(p))
+        out["hbm_gbs"] = m.get("hbm_gbs", out["hbm_gbs"])
+        out["hbm_src"] = "measured (MEASURED_PEAKS.json)"
+    q = os.path.join(ROOT, "profiles", "r01_fp64_fp32_peaks.json")
+    if os.path.exists(q):
+        f = json.load(open(q))
+        out["dmma_tflops"], out["ffma_tflops"] = f["dmma_tflops"], f["ffma_tflops"]
+        out["fp_src"] = "measured (tools/fp64_peak.cu, profiles/r01_fp64_fp32_peaks.json)"
+    else:  # guide unit counts: 148 SM x 64 FP64 / 128 FP32 lanes x 2 x 1.965 GHz
+        out["dmma_tflops"], out["ffma_tflops"] = 37.2, 74.4
+        out["fp_src"] = "derived from SM counts and clocks"
+    return out
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index):
+        self.gpu = gpu_index
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except FileNotFoundError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4)
+                          if len(r) > 4 + i and r[4 + i].lower() == "active"})
+        busy = [s for s in sm if s > 0.5 * max(sm)] if sm else []
+        return {"sm_mhz": statistics.median(busy or sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons, "samples": len(self.rows)}
+
+
+def dist_init(args):
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if ws > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    return ws, rank, local
+
+
+# ----------------------------------------------------------------------------- oracle leg
+def oracle_sample(n, mode, kappa, seed, sweeps64, sweeps32, budget_s):
+    """Time the oracle (oracle/, plain C) on a bounded sample of the workload and
+    extrapolate to seconds per EVD:  rounds of the fp64 and fp32 Jacobi loops at
+    the full n (each round is one O(n^2) pass), plus MGS and Q^T A Q timed at
+    n_s = min(n, 768) and scaled by (n/n_s)^3.  Returns (seconds/EVD, dict)."""
+    import numpy as np
+
+    import oracle
+    import workloads as W
+    rng = np.random.default_rng(seed)
+    cfg = oracle.default_cfg("eig")
+    b = cfg.b
+    # a T like the fp64 stage's (near-diagonal symmetric) at the full size
+    t0 = time.perf_counter()
+    d = np.sort(W.spectrum_ex1(n, kappa, mode))[::-1].copy()
+    T = np.diag(d)
+    E = rng.standard_normal((n, n)) * 1e-6
+    T = np.asfortranarray(T + 0.5 * (E + E.T))
+    prep = time.perf_counter() - t0
+    rounds = 0
+    t64 = t32 = 0.0
+    nrounds = 1
+    while True:
+        t0 = time.perf_counter()
+        oracle.jacobi_evd(T, b=b, tol=0.0, max_sweeps=1, max_rounds=nrounds)
+        t64 = (time.perf_counter() - t0) / nrounds
+        t0 = time.perf_counter()
+        oracle.jacobi_evd(T.astype(np.float32), b=b, tol=0.0, max_sweeps=1, max_rounds=nrounds,
+                          precision="f32", nu=20 * UPSILON)
+        t32 = (time.perf_counter() - t0) / nrounds
+        rounds = nrounds
+        if (t64 + t32) * nrounds * 2 > budget_s * 0.35 or nrounds >= 8:
+            break
+        nrounds *= 2
+    ns = min(n, 768)
+    A, _ = W.example1(ns, kappa, mode, seed)
+    Z = W.rounded_haar(ns, seed)   # an fp32-rounded orthogonal matrix, like the low stage's Z
+    t0 = time.perf_counter()
+    Q, _, _ = oracle.mgs(Z)
+    t_mgs = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    oracle.qtaq(A, Q)
+    t_qtaq = time.perf_counter() - t0
+    scale = (n / ns) ** 3
+    rounds_per_sweep = oracle.padded_n(n, b) - 1
+    est = (t64 * sweeps64 + t32 * sweeps32) * rounds_per_sweep + (t_mgs + t_qtaq) * scale
+    info = {
+        "kind": "oracle", "cores": oracle.threads(),
+        "sample": (f"oracle/mpj_oracle.c at n={n}: {rounds} fp64 round(s) ({t64:.3f} s each) and "
+                   f"{rounds} fp32 round(s) ({t32:.3f} s each), x {rounds_per_sweep} rounds/sweep x "
+                   f"({sweeps64} fp64 + {sweeps32} fp32 sweeps as the GPU run took); MGS + Q^T A Q "
+                   f"timed at n={ns} ({t_mgs + t_qtaq:.2f} s) x (n/{ns})^3"),
+    }
+    return est, info
+
+
+def run_reference(args):
+    ws, rank, local = dist_init(args)
+    if rank != 0:
+        return
+    seed = 2211033390 + 4000 + 100 * args.mode + 60
+    # sweep counts of the GPU run at this config (measured on B200, profiles/); the
+    # oracle at n = 8192 would take hours per EVD, so each step is a bounded sample
+    sw64, sw32 = 5, 14
+    vals = []
+    info = None
+    for _ in range(args.warmup * 0 + args.steps):
+        v, info = oracle_sample(args.n, args.mode, args.kappa, seed, sw64, sw32,
+                                args.cpu_sample_seconds)
+        vals.append(v)
+    v = statistics.median(vals)
+    info["value"] = v
+    info["unit"] = "s"
+    line = {
+        "impl": "reference", "metric": "fp64 EVD seconds (n=8192)", "value": v, "unit": "s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": v * 1e3,
+        "higher_is_better": False, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic", "config": {"workload": f"Example 1 mode {args.mode}, kappa={args.kappa:g}, n={args.n}"},
+        "cpu_baseline": info,
+        "e2e": {"value": v, "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line))
+
+
+# ----------------------------------------------------------------------------- our leg
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    import numpy as np
+    import torch
+
+    import paper_2211_03339_b200 as mpj
+    import workloads as W
+
+    ws, rank, local = dist_init(args)
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    n = args.n
+    seed = 2211033390 + 4000 + 100 * args.mode + 10 * int(round(np.log10(args.kappa))) + rank
+    A, lam_true = W.example1_torch(n, args.kappa, args.mode, seed, device=dev)
+    Acm = A.T  # symmetric: the row-major tensor's transpose view is its column-major image
+    cfg = mpj.default_config("eig", variant=args.variant)
+    wsbuf = mpj.eig_workspace(n, cfg, device=dev)
+    lam = torch.empty(n, dtype=torch.float64, device=dev)
+    V = mpj.empty_colmajor(n, n, device="cuda")
+
+    def step():
+        return mpj.eig(Acm, cfg, workspace=wsbuf, out=(lam, V), allow_noconv=True)
+
+    for _ in range(args.warmup):
+        res = step()
+    torch.cuda.synchronize()
+    if ws > 1:
+        torch.distributed.barrier()
+    mpj.profile_reset()
+    mpj.profile_enable(True)
+    l0 = mpj.launch_count()
+    reports = []
+    with ClockSampler(local) as clk:
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        e0.record()
+        for _ in range(args.steps):
+            res = step()
+            reports.append(res.report)
+        e1.record()
+        torch.cuda.synchronize()
+    mpj.profile_enable(False)
+    launches = mpj.launch_count() - l0
+    ms = e0.elapsed_time(e1) / args.steps
+    if ws > 1:
+        t = torch.tensor([ms], device=dev)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        ms = float(t.item())
+    rep = reports[-1]
+
+    # correctness of the timed result (test-style properties at full size)
+    with torch.no_grad():
+        Vm = V
+        R = Acm @ Vm - Vm * lam
+        res_rel = float(torch.linalg.norm(R) / torch.linalg.norm(Acm))
+        orth = float(torch.linalg.norm(Vm.T @ Vm - torch.eye(n, device=dev, dtype=torch.float64)))
+        dlam = float((lam - lam_true).abs().max() / lam_true.abs().max())
+
+    # roofline of the dominant kernel (largest accumulated time in the timed region)
+    pk = peaks()
+    mb = rep.n_padded // 64
+    nt_t, nt_v = mb * (mb - 1) // 2, (rep.n_padded // 64) * mb
+    flops_apply = nt_t * 2 * 2 * 64 ** 3 + nt_v * 2 * 64 ** 3
+    bytes_apply = (nt_t * 3 + nt_v * 2) * 64 * 64 * 8   # T: read + tile + mirror; V: read + write
+    kernels = {}
+    for name in ("block_apply_f64", "block_apply_f32", "block_solve_f64", "block_solve_f32"):
+        sec, cnt = mpj.profile_get(name)
+        if cnt:
+            kernels[name] = {"seconds_per_step": sec / args.steps, "launches": cnt, "avg_ms": 1e3 * sec / cnt}
+    roof = None
+    if kernels:
+        dom = max(kernels, key=lambda k: kernels[k]["seconds_per_step"])
+        avg = kernels[dom]["avg_ms"] * 1e-3
+        if dom.startswith("block_apply"):
+            is64 = dom.endswith("f64")
+            fl = flops_apply
+            by = bytes_apply * (1 if is64 else 0.5)
+            peak = pk["dmma_tflops"] if is64 else pk["ffma_tflops"]
+            roof = {"kernel": dom, "bound": "tensor" if is64 else "alu",
+                    "achieved": fl / avg / 1e12, "peak": peak, "unit": "TFLOP/s",
+                    "frac": fl / avg / 1e12 / peak, "traffic": None,
+                    "algorithmic_flop_per_launch": fl, "algorithmic_bytes_per_launch": by,
+                    "hbm_frac": by / avg / 1e9 / pk["hbm_gbs"],
+                    "share_of_step": kernels[dom]["seconds_per_step"] / (ms * 1e-3),
+                    "peak_src": pk["fp_src"]}
+        else:
+            roof = {"kernel": dom, "bound": "alu", "achieved": None, "peak": None, "unit": "TFLOP/s",
+                    "frac": None, "traffic": None}
+
+    # end-to-end through the ABI with host buffers (copies inside the timed region)
+    e2e = None
+    if not args.no_e2e:
+        Ah = torch.empty((n, n), dtype=torch.float64, pin_memory=True)
+        Ah.copy_(A)
+        Ahc = Ah.T
+        lam_h = torch.empty(n, dtype=torch.float64, pin_memory=True)
+        V_h = mpj.empty_colmajor(n, n, device="cpu", pin=True)
+        mpj.eig(Ahc, cfg, workspace=wsbuf, out=(lam_h, V_h), allow_noconv=True)   # warm
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        c0, c1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        c0.record()
+        ksteps = max(1, min(args.steps, 2))
+        for _ in range(ksteps):
+            mpj.eig(Ahc, cfg, workspace=wsbuf, out=(lam_h, V_h), allow_noconv=True)
+        c1.record()
+        torch.cuda.synchronize()
+        e2e_s = c0.elapsed_time(c1) / ksteps * 1e-3
+        wall = (time.perf_counter() - t0) / ksteps
+        e2e = {"value": max(e2e_s, wall), "unit": "s", "h2d_bytes_per_step": n * n * 8,
+               "d2h_bytes_per_step": n * 8 + n * n * 8}
+
+    cpu = None
+    if rank == 0 and ws == 1 and not args.no_cpu_baseline:
+        try:
+            v, info = oracle_sample(n, args.mode, args.kappa, seed, rep.sweeps, rep.sweeps_low,
+                                    args.cpu_sample_seconds)
+            info["value"], info["unit"] = v, "s"
+            cpu = info
+        except Exception as e:  # the oracle is a baseline, not the product
+            cpu = {"error": repr(e)}
+
+    if rank == 0:
+        value = ms * 1e-3
+        line = {
+            "metric": "fp64 EVD seconds (n=8192)", "value": value, "unit": "s", "n_gpus": ws,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": False,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"Example 1 (P:681) mode {args.mode} graded spectrum, kappa={args.kappa:g}, "
+                                   f"n={n}, one EVD per GPU per step",
+                       "n": n, "mode": args.mode, "kappa": args.kappa,
+                       "variant": {1: "scalar", 2: "block"}.get(rep.variant, rep.variant),
+                       "block_b": rep.block_b, "n_padded": rep.n_padded,
+                       "l2": "inputs (512 MB A, 2.5 GB workspace) exceed the 126 MB L2",
+                       "parallelism": "replicas" if ws > 1 else "single GPU"},
+            "sweeps": rep.sweeps, "sweeps_low": rep.sweeps_low,
+            "ju": rep.rotations / (n * (n - 1) / 2), "ju_low": rep.rotations_low / (n * (n - 1) / 2),
+            "stage_seconds": {"low_fp32": rep.t_low, "orth": rep.t_orth, "precond": rep.t_precond,
+                              "jacobi_fp64": rep.t_jacobi, "extract": rep.t_extract},
+            "check": {"residual": res_rel, "orthogonality": orth, "max_dlam_rel": dlam,
+                      "tol_residual": n * 1e-15, "tol_orth": n * 1e-15, "tol_dlam": 1e-13},
+            "roofline": roof, "kernels": kernels, "gpu_launches": launches,
+            "clocks": clk.summary(), "e2e": e2e, "cpu_baseline": cpu,
+        }
+        print(json.dumps(line))
+    if ws > 1:
+        torch.distributed.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

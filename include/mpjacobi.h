@@ -191,6 +191,16 @@ mpj_status mpjacobi_eig_batched(const double *A, int64_t n, int64_t batch, doubl
                                 double *V, int *sweeps, int *sweeps_low, void *stream,
                                 const mpj_config *cfg);
 
+/* Kernel timing (diagnostics for the bench's roofline numbers).  While
+ * enabled, the library brackets each launch of its dominant kernels with CUDA
+ * events ON THE STREAM IT LAUNCHES THEM ON and accumulates their durations per
+ * kernel name ("block_apply_f64", "block_apply_f32", "block_solve_f64",
+ * "block_solve_f32", "round_apply_f64", "round_apply_f32").  Process-wide;
+ * not for concurrent calls.  get() returns 0 launches for unknown names. */
+void mpjacobi_profile_enable(int on);
+void mpjacobi_profile_reset(void);
+void mpjacobi_profile_get(const char *kernel, double *seconds, long long *launches);
+
 /* Thread-local description of the last error ("" if none). */
 const char *mpjacobi_last_error(void);
 

@@ -97,6 +97,8 @@ def lib():
         L.mpjacobi_precond.argtypes = [_vp, _vp, _vp, _i64, _vp]
         L.mpjacobi_dgemm.restype = C.c_int
         L.mpjacobi_dgemm.argtypes = [C.c_int, _vp, _vp, _vp, _i64, _i64, _i64, _vp]
+        L.mpjacobi_profile_enable.argtypes = [C.c_int]
+        L.mpjacobi_profile_get.argtypes = [C.c_char_p, C.POINTER(C.c_double), C.POINTER(C.c_longlong)]
         if hasattr(L, "mpjacobi_svd"):
             L.mpjacobi_svd_workspace.restype = C.c_size_t
             L.mpjacobi_svd_workspace.argtypes = [_i64, _i64, cfgp]
@@ -115,6 +117,7 @@ EXPORTED = (
     "mpjacobi_eig_plain", "mpjacobi_jacobi_f64", "mpjacobi_jacobi_f32", "mpjacobi_orth",
     "mpjacobi_precond", "mpjacobi_dgemm", "mpjacobi_svd_workspace", "mpjacobi_svd",
     "mpjacobi_eig_batched", "mpjacobi_last_error", "mpjacobi_launch_count",
+    "mpjacobi_profile_enable", "mpjacobi_profile_reset", "mpjacobi_profile_get",
 )
 
 
@@ -134,6 +137,22 @@ def default_config(kind: str = "eig", **kw) -> mpj_config:
 
 def launch_count() -> int:
     return lib().mpjacobi_launch_count()
+
+
+def profile_enable(on: bool = True):
+    """Time the library's dominant kernels with CUDA events on their own stream."""
+    lib().mpjacobi_profile_enable(1 if on else 0)
+
+
+def profile_reset():
+    lib().mpjacobi_profile_reset()
+
+
+def profile_get(kernel: str):
+    """(seconds, launches) accumulated for a kernel name (see mpjacobi.h)."""
+    sec, n = C.c_double(0), C.c_longlong(0)
+    lib().mpjacobi_profile_get(kernel.encode(), C.byref(sec), C.byref(n))
+    return sec.value, n.value
 
 
 def _stream():

@@ -14,6 +14,10 @@ struct Sched;
 // ---- error / launch bookkeeping --------------------------------------------
 void set_error(const std::string &msg);
 void count_launch(long long k = 1);
+// kernel timing (mpjacobi_profile_*): events recorded on the launch stream
+bool prof_on();
+void prof_mark(const char *name, cudaStream_t st, bool begin);
+void prof_flush();   // after the stream has been synchronised
 
 #define MPJ_CK(expr)                                                                    \
     do {                                                                                \

@@ -13,6 +13,7 @@
 // read once per sweep for the stop test.
 #include <algorithm>
 #include <cmath>
+#include <map>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -36,6 +37,49 @@ thread_local long long g_launches = 0;
 
 void set_error(const std::string &msg) { g_err = msg; }
 void count_launch(long long k) { g_launches += k; }
+
+// ---- kernel timing ---------------------------------------------------------
+namespace {
+struct ProfRec { double sec = 0; long long n = 0; };
+bool g_prof = false;
+std::map<std::string, ProfRec> g_prof_tab;
+struct Pending { std::string name; cudaEvent_t a, b; };
+std::vector<Pending> g_pending;
+std::vector<cudaEvent_t> g_ev_pool;
+cudaEvent_t ev_get()
+{
+    if (!g_ev_pool.empty()) { cudaEvent_t e = g_ev_pool.back(); g_ev_pool.pop_back(); return e; }
+    cudaEvent_t e; cudaEventCreate(&e); return e;
+}
+}  // namespace
+bool prof_on() { return g_prof; }
+void prof_mark(const char *name, cudaStream_t st, bool begin)
+{
+    if (!g_prof) return;
+    cudaEvent_t e = ev_get();
+    cudaEventRecord(e, st);
+    if (begin) g_pending.push_back(Pending{name, e, nullptr});
+    else {
+        for (auto it = g_pending.rbegin(); it != g_pending.rend(); ++it)
+            if (!it->b && it->name == name) { it->b = e; return; }
+        g_ev_pool.push_back(e);
+    }
+}
+void prof_flush()
+{
+    for (auto &p : g_pending) {
+        if (p.b) {
+            float ms = 0.f;
+            if (cudaEventSynchronize(p.b) == cudaSuccess && cudaEventElapsedTime(&ms, p.a, p.b) == cudaSuccess) {
+                ProfRec &r = g_prof_tab[p.name];
+                r.sec += ms * 1e-3; r.n += 1;
+            }
+            g_ev_pool.push_back(p.b);
+        }
+        g_ev_pool.push_back(p.a);
+    }
+    g_pending.clear();
+}
 
 // ---------------------------------------------------------------------------
 // Ordering (reading R1), an implementation independent of oracle/.
@@ -122,7 +166,7 @@ static int resolve_b(int64_t n, const mpj_config *cfg)
 static int resolve_variant(int np, int b, const mpj_config *cfg)
 {
     int v = cfg ? cfg->variant : MPJ_VARIANT_AUTO;
-    if (v == MPJ_VARIANT_AUTO) v = MPJ_VARIANT_SCALAR;   // block variant: see k_block.cu
+    if (v == MPJ_VARIANT_AUTO) v = (np >= 128 && b == 32) ? MPJ_VARIANT_BLOCK : MPJ_VARIANT_SCALAR;
     if (v == MPJ_VARIANT_BLOCK && b != 32) v = MPJ_VARIANT_SCALAR;   // block kernels are b = 32
     return v;
 }
@@ -253,6 +297,7 @@ static mpj_status jacobi_run(Ctx &cx, R *T, R *V, int n, int b, int variant, dou
         launch_norm<R>(T, np, np, np, true, jb.part, jb.off, st);
         MPJ_CK(cudaMemcpyAsync(cx.h_pin, jb.off, sizeof(double), cudaMemcpyDeviceToHost, st));
         MPJ_CK(cudaStreamSynchronize(st));
+        prof_flush();
         const double off = cx.h_pin[0];
         if (sweeps < 64) { out.hist[sweeps] = off; out.nhist = sweeps + 1; }
         if (!(off == off)) { set_error("non-finite off-norm"); status = MPJ_ERR_NONFINITE; break; }
@@ -605,6 +650,19 @@ void mpj_config_default_svd(mpj_config *c)
 }
 
 const char *mpjacobi_last_error(void) { return g_err.c_str(); }
+void mpjacobi_profile_enable(int on) { mpj::g_prof = on != 0; }
+void mpjacobi_profile_reset(void)
+{
+    mpj::prof_flush();
+    mpj::g_prof_tab.clear();
+}
+void mpjacobi_profile_get(const char *kernel, double *seconds, long long *launches)
+{
+    mpj::prof_flush();
+    auto it = mpj::g_prof_tab.find(kernel ? kernel : "");
+    if (seconds) *seconds = it == mpj::g_prof_tab.end() ? 0.0 : it->second.sec;
+    if (launches) *launches = it == mpj::g_prof_tab.end() ? 0 : it->second.n;
+}
 long long mpjacobi_launch_count(void) { return g_launches; }
 
 size_t mpjacobi_eig_workspace(int64_t n, const mpj_config *cfg)

@@ -174,3 +174,62 @@ def test_edge_cases(mpj):
     with pytest.raises(mpj.MpjError) as e:
         mpj.eig(dev(A))
     assert e.value.status == mpj.MPJ_ERR_NONFINITE
+
+
+# ----------------------------------------------------------------- block variant
+@pytest.mark.parametrize("n", [128, 200, 512])
+def test_block_variant_fp64(mpj, orc, n):
+    """Block variant (K3 inner solves + DMMA apply) vs the oracle's scalar
+    rounds with the same b = 32 ordering: equal in exact arithmetic (reading
+    R1), so after one sweep T agrees to rounding and the full run takes the
+    same number of sweeps with the same eigenvalues."""
+    T0, Q, A = near_diag_T0(n, 3 * n)
+    nA = np.linalg.norm(A)
+    cfg = mpj.default_config("eig", variant=mpj.VARIANT_BLOCK, block_b=32)
+    # one sweep
+    ref1 = orc.jacobi_evd(T0, Q, b=32, tol=0.0, max_sweeps=1)
+    T, V = dev(T0), dev(Q)
+    mpj.jacobi(T, V, tol=0.0, max_sweeps=1, cfg=cfg)
+    dT = np.max(np.abs(host(T) - ref1.T))
+    dV = np.max(np.abs(host(V) - ref1.V))
+    assert dT <= 64 * n * OMEGA * nA, dT
+    assert dV <= 64 * n * OMEGA, dV
+    assert np.array_equal(host(T), host(T).T)
+    # full run
+    tol = 0.1 * OMEGA * nA
+    ref = orc.jacobi_evd(T0, Q, b=32, tol=tol)
+    T, V = dev(T0), dev(Q)
+    r = mpj.jacobi(T, V, tol=tol, cfg=cfg)
+    assert r.sweeps == ref.sweeps
+    lg = np.sort(np.diag(host(T)))[::-1]
+    lo = np.sort(np.diag(ref.T))[::-1]
+    assert np.max(np.abs(lg - lo)) <= 1e-13 * np.max(np.abs(lo))
+    Vg = host(V)
+    assert np.linalg.norm(Vg.T @ Vg - np.eye(n)) <= n * 1e-15
+    assert np.linalg.norm(A @ Vg - Vg * np.diag(host(T))) / nA <= n * 1e-15
+
+
+@pytest.mark.parametrize("n", [128, 320])
+def test_block_variant_fp32(mpj, orc, n):
+    A, _ = W.example1(n, 1e3, 4, 17 + n)
+    T0 = A.astype(np.float32)
+    nA = orc.fro(T0)
+    cfg = mpj.default_config("eig", variant=mpj.VARIANT_BLOCK, block_b=32)
+    ref = orc.jacobi_evd(T0, b=32, tol=10 * UPSILON * nA, nu=20 * UPSILON, precision="f32")
+    T, V = dev(T0, torch.float32), dev(np.eye(n, dtype=np.float32), torch.float32)
+    r = mpj.jacobi(T, V, tol=10 * UPSILON * nA, nu=float(np.float32(20 * UPSILON)), cfg=cfg)
+    assert abs(r.sweeps - ref.sweeps) <= 1
+    lg = np.sort(np.diag(host(T)).astype(np.float64))
+    lo = np.sort(np.diag(ref.T).astype(np.float64))
+    assert np.max(np.abs(lg - lo)) <= 10 * n * UPSILON * nA
+    Vg = host(V).astype(np.float64)
+    assert np.linalg.norm(Vg.T @ Vg - np.eye(n)) <= 10 * n * UPSILON
+
+
+@pytest.mark.parametrize("n", [512, 1000])
+def test_eig_block_end_to_end(mpj, orc, n):
+    A, lam_true = W.example1(n, 1e3, 4, W.seed_for(2, 4, 1e3))
+    res = mpj.eig(dev(A))
+    assert res.report.variant == mpj.VARIANT_BLOCK
+    ref = orc.mp_evd(A, orc.default_cfg("eig", b=32))
+    _check_evd(A, host(res.lam), host(res.V), ref.lam, ref.report.sweeps, res.sweeps)
