@@ -353,6 +353,8 @@ def main():
                        "l2": "inputs (512 MB A, 2.5 GB workspace) exceed the 126 MB L2",
                        "parallelism": "replicas" if ws > 1 else "single GPU"},
             "sweeps": rep.sweeps, "sweeps_low": rep.sweeps_low,
+            "off_hist_rel": [h / rep.norm_a for h in list(rep.off_hist)[: rep.sweeps + 1]],
+            "off0_rel": rep.off0 / rep.norm_a,
             "ju": rep.rotations / (n * (n - 1) / 2), "ju_low": rep.rotations_low / (n * (n - 1) / 2),
             "stage_seconds": {"low_fp32": rep.t_low, "orth": rep.t_orth, "precond": rep.t_precond,
                               "jacobi_fp64": rep.t_jacobi, "extract": rep.t_extract},

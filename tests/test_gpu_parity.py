@@ -137,7 +137,10 @@ def test_eig_end_to_end(mpj, orc, n, mode, kappa):
     ref = orc.mp_evd(A, orc.default_cfg("eig", b=rep.block_b))
     _check_evd(A, host(res.lam), host(res.V), ref.lam, ref.report.sweeps, res.sweeps)
     assert rep.sweeps_low == ref.report.sweeps_low
-    assert abs(rep.off0 - ref.report.off0) <= 1e-3 * ref.report.off0 + 100 * n * OMEGA
+    # T0 quality: the block variant's fp32 stage differs from the oracle's by
+    # rounding (DMMA/FFMA products), so off(T0) agrees to the same order only
+    tol = 1e-12 if rep.variant == mpj.VARIANT_SCALAR else 0.1
+    assert abs(rep.off0 - ref.report.off0) <= tol * ref.report.off0 + 100 * n * OMEGA
 
 
 def test_eig_host_buffers(mpj, orc):
