@@ -149,21 +149,20 @@ def oracle_sample(n, mode, kappa, seed, sweeps64, sweeps32, budget_s):
     E = rng.standard_normal((n, n)) * 1e-6
     T = np.asfortranarray(T + 0.5 * (E + E.T))
     prep = time.perf_counter() - t0
-    rounds = 0
-    t64 = t32 = 0.0
-    nrounds = 1
-    while True:
+    # per-round cost = t(2 rounds) - t(1 round): cancels the call's fixed cost
+    # (padding copies, schedule table, the off-norm before the sweep)
+    def timed(prec, k):
         t0 = time.perf_counter()
-        oracle.jacobi_evd(T, b=b, tol=0.0, max_sweeps=1, max_rounds=nrounds)
-        t64 = (time.perf_counter() - t0) / nrounds
-        t0 = time.perf_counter()
-        oracle.jacobi_evd(T.astype(np.float32), b=b, tol=0.0, max_sweeps=1, max_rounds=nrounds,
-                          precision="f32", nu=20 * UPSILON)
-        t32 = (time.perf_counter() - t0) / nrounds
-        rounds = nrounds
-        if (t64 + t32) * nrounds * 2 > budget_s * 0.35 or nrounds >= 8:
-            break
-        nrounds *= 2
+        if prec == "f64":
+            oracle.jacobi_evd(T, b=b, tol=0.0, max_sweeps=1, max_rounds=k)
+        else:
+            oracle.jacobi_evd(T32, b=b, tol=0.0, max_sweeps=1, max_rounds=k, precision="f32",
+                              nu=20 * UPSILON)
+        return time.perf_counter() - t0
+    T32 = T.astype(np.float32)
+    t64 = max(timed("f64", 2) - timed("f64", 1), 1e-9)
+    t32 = max(timed("f32", 2) - timed("f32", 1), 1e-9)
+    rounds = 1
     ns = min(n, 768)
     A, _ = W.example1(ns, kappa, mode, seed)
     Z = W.rounded_haar(ns, seed)   # an fp32-rounded orthogonal matrix, like the low stage's Z
