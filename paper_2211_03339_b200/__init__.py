@@ -284,7 +284,36 @@ def mpjacobi_dgemm(A, B, transa=False):
     return Cm
 
 
+@dataclass
+class BatchedResult:
+    lam: torch.Tensor          # (batch, n), descending per matrix
+    V: torch.Tensor            # (batch, n, n), V[k][i, j] = entry (i, j) of matrix k's eigenvectors
+    sweeps: torch.Tensor       # (batch,) int32 fp64 sweeps
+    sweeps_low: torch.Tensor   # (batch,) int32 fp32 sweeps
+    status: int
+
+
+def mpjacobi_eig_batched(A, cfg: mpj_config | None = None, allow_noconv=False) -> BatchedResult:
+    """Batched Alg. 3, one matrix per CTA (n <= 64).  A: (batch, n, n) float64
+    CUDA tensor; A[k] is matrix k (symmetric, so either memory order is its
+    column-major image).  Outputs are column-major per matrix, returned as
+    math-orientation views."""
+    if A.dim() != 3 or A.shape[1] != A.shape[2] or A.dtype != torch.float64 or not A.is_cuda:
+        raise ValueError("A must be a (batch, n, n) float64 CUDA tensor")
+    batch, n, _ = A.shape
+    Ac = A.transpose(1, 2).contiguous()          # memory of matrix k = column-major image of A[k]
+    lam = torch.empty((batch, n), dtype=torch.float64, device=A.device)
+    V = torch.empty((batch, n, n), dtype=torch.float64, device=A.device)
+    sw = torch.empty(batch, dtype=torch.int32, device=A.device)
+    swl = torch.empty(batch, dtype=torch.int32, device=A.device)
+    st = lib().mpjacobi_eig_batched(_ptr(Ac), n, batch, _ptr(lam), _ptr(V), _ptr(sw), _ptr(swl), _stream(),
+                                    C.byref(cfg or default_config("eig")))
+    _check(st, (MPJ_OK, MPJ_ERR_NOCONV) if allow_noconv else (MPJ_OK,))
+    return BatchedResult(lam, V.transpose(1, 2), sw, swl, st)
+
+
 # short aliases
+eig_batched = mpjacobi_eig_batched
 eig = mpjacobi_eig
 jacobi = mpjacobi_jacobi
 orth = mpjacobi_orth

@@ -765,12 +765,4 @@ mpj_status mpjacobi_svd(const double *, int64_t, int64_t, int64_t, double *, dou
     return MPJ_ERR_INVALID;
 }
 #endif
-#ifndef MPJ_HAVE_BATCHED
-mpj_status mpjacobi_eig_batched(const double *, int64_t, int64_t, double *, double *, int *, int *, void *,
-                                const mpj_config *)
-{
-    mpj::set_error("mpjacobi_eig_batched: not built yet");
-    return MPJ_ERR_INVALID;
-}
-#endif
 }

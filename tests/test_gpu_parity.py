@@ -236,3 +236,24 @@ def test_eig_block_end_to_end(mpj, orc, n):
     assert res.report.variant == mpj.VARIANT_BLOCK
     ref = orc.mp_evd(A, orc.default_cfg("eig", b=32))
     _check_evd(A, host(res.lam), host(res.V), ref.lam, ref.report.sweeps, res.sweeps)
+
+
+# ----------------------------------------------------------------- batched
+@pytest.mark.parametrize("n,batch", [(64, 48), (40, 9), (7, 5)])
+def test_eig_batched(mpj, orc, n, batch):
+    """Batched Alg. 3 (one matrix per CTA) vs the oracle's Alg. 3 (b = 32
+    ordering) matrix by matrix: north_star tolerances and identical fp64 /
+    fp32 sweep counts."""
+    As = np.stack([W.example1(n, 1e3, 3 + k % 3, W.seed_for(3, 3 + k % 3, 1e3, k))[0] for k in range(batch)])
+    res = mpj.eig_batched(torch.from_numpy(As).cuda())
+    lam, V = host(res.lam), host(res.V)
+    sw, swl = host(res.sweeps), host(res.sweeps_low)
+    for k in range(batch):
+        ref = orc.mp_evd(As[k], orc.default_cfg("eig", b=32))
+        _check_evd(As[k], lam[k], V[k], ref.lam, ref.report.sweeps, int(sw[k]))
+        assert int(swl[k]) == ref.report.sweeps_low
+
+
+def test_eig_batched_invalid(mpj):
+    with pytest.raises(mpj.MpjError):
+        mpj.eig_batched(torch.zeros((2, 65, 65), dtype=torch.float64, device="cuda"))
