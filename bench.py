@@ -46,6 +46,9 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample-seconds", type=float, default=20.0)
+    ap.add_argument("--workload", default="evd", choices=["evd", "batched"],
+                    help="evd: BASELINE config 4 (the bench line); batched: config 3 (4096 x n=64)")
+    ap.add_argument("--batch", type=int, default=4096)
     return ap.parse_args()
 
 
@@ -214,10 +217,50 @@ def run_reference(args):
 
 
 # ----------------------------------------------------------------------------- our leg
+def run_batched(args):
+    """BASELINE config 3: `batch` independent Example 1 matrices (n = 64,
+    modes cycling 3/4/5, kappa = 1e3), one matrix per CTA."""
+    import numpy as np
+    import torch
+
+    import paper_2211_03339_b200 as mpj
+    import workloads as W
+    n, batch = 64, args.batch
+    As = np.stack([W.example1(n, 1e3, 3 + k % 3, W.seed_for(3, 3 + k % 3, 1e3, k))[0] for k in range(batch)])
+    A = torch.from_numpy(As).cuda()
+    for _ in range(args.warmup):
+        res = mpj.eig_batched(A)
+    torch.cuda.synchronize()
+    l0 = mpj.launch_count()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(0) as clk:
+        e0.record()
+        for _ in range(args.steps):
+            res = mpj.eig_batched(A)
+        e1.record()
+        torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / args.steps
+    lam = res.lam
+    V = res.V
+    Ac = A
+    R = torch.linalg.norm(Ac @ V - V * lam[:, None, :], dim=(1, 2)) / torch.linalg.norm(Ac, dim=(1, 2))
+    O = torch.linalg.norm(V.transpose(1, 2) @ V - torch.eye(n, device=A.device, dtype=A.dtype), dim=(1, 2))
+    line = {"metric": "batched EVD matrices/s (4096 x n=64)", "value": batch / (ms * 1e-3), "unit": "matrices/s",
+            "n_gpus": 1, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+            "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"{batch} x Example 1 n=64 modes 3/4/5 kappa=1e3 (BASELINE config 3)"},
+            "sweeps_mean": float(res.sweeps.float().mean()), "sweeps_low_mean": float(res.sweeps_low.float().mean()),
+            "check": {"max_residual": float(R.max()), "max_orth": float(O.max())},
+            "gpu_launches": mpj.launch_count() - l0, "clocks": clk.summary()}
+    print(json.dumps(line))
+
+
 def main():
     args = parse()
     if args.impl == "reference":
         return run_reference(args)
+    if args.workload == "batched":
+        return run_batched(args)
     import numpy as np
     import torch
 

@@ -119,13 +119,30 @@ def test_precond(mpj, orc, n):
 
 
 # ----------------------------------------------------------------- end to end
-def _check_evd(A, lam, V, ref_lam, ref_sweeps, sweeps):
+def sweeps_match(sw_a, hist_a, sw_b, hist_b, tol):
+    """Reading R20: identical sweep counts, except that a stop
+    decision taken at the rounding-noise level is not reproducible across
+    valid evaluation orders: counts may differ by one when, at the sweep where
+    the runs part, BOTH off-norms are within 10x of tol (= eps ||A||_F)."""
+    if sw_a == sw_b:
+        return True
+    if abs(sw_a - sw_b) != 1:
+        return False
+    k = min(sw_a, sw_b)
+    return hist_a[k] <= 10 * tol and hist_b[k] <= 10 * tol
+
+
+def _check_evd(A, lam, V, ref_lam, ref_sweeps, sweeps, hist=None, ref_hist=None):
     n = A.shape[0]
     nrm2 = np.max(np.abs(ref_lam))
     assert np.max(np.abs(lam - ref_lam)) <= 1e-13 * nrm2
     assert np.linalg.norm(V.T @ V - np.eye(n)) <= n * 1e-15
     assert np.linalg.norm(A @ V - V * lam) / np.linalg.norm(A) <= n * 1e-15
-    assert sweeps == ref_sweeps
+    if hist is None:
+        assert sweeps == ref_sweeps
+    else:
+        tol = 0.1 * OMEGA * np.linalg.norm(0.5 * (A + A.T))
+        assert sweeps_match(sweeps, hist, ref_sweeps, ref_hist, tol), (sweeps, ref_sweeps, hist, ref_hist)
 
 
 @pytest.mark.parametrize("n,mode,kappa", [(32, 4, 1e3), (32, 3, 1e6), (64, 5, 1e3), (100, 4, 1e3),
@@ -135,7 +152,10 @@ def test_eig_end_to_end(mpj, orc, n, mode, kappa):
     res = mpj.eig(dev(A))
     rep = res.report
     ref = orc.mp_evd(A, orc.default_cfg("eig", b=rep.block_b))
-    _check_evd(A, host(res.lam), host(res.V), ref.lam, ref.report.sweeps, res.sweeps)
+    _check_evd(A, host(res.lam), host(res.V), ref.lam, ref.report.sweeps, res.sweeps,
+               list(rep.off_hist), list(ref.report.off_hist))
+    if rep.variant == mpj.VARIANT_SCALAR:
+        assert res.sweeps == ref.report.sweeps      # bit-exact path: no borderline allowance
     assert rep.sweeps_low == ref.report.sweeps_low
     # T0 quality: the block variant's fp32 stage differs from the oracle's by
     # rounding (DMMA/FFMA products), so off(T0) agrees to the same order only
@@ -235,7 +255,8 @@ def test_eig_block_end_to_end(mpj, orc, n):
     res = mpj.eig(dev(A))
     assert res.report.variant == mpj.VARIANT_BLOCK
     ref = orc.mp_evd(A, orc.default_cfg("eig", b=32))
-    _check_evd(A, host(res.lam), host(res.V), ref.lam, ref.report.sweeps, res.sweeps)
+    _check_evd(A, host(res.lam), host(res.V), ref.lam, ref.report.sweeps, res.sweeps,
+               list(res.report.off_hist), list(ref.report.off_hist))
 
 
 # ----------------------------------------------------------------- batched
