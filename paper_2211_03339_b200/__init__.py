@@ -285,6 +285,47 @@ def mpjacobi_dgemm(A, B, transa=False):
 
 
 @dataclass
+class SvdResult:
+    sigma: torch.Tensor   # (n,) descending
+    U: torch.Tensor       # (m, n) column-major, math orientation
+    V: torch.Tensor       # (n, n) column-major, math orientation
+    sweeps: int
+    report: mpj_report
+
+
+def mpjacobi_svd(A, cfg: mpj_config | None = None, *, workspace=None, out=None,
+                 allow_noconv=False) -> SvdResult:
+    """Alg. 5: A (m, n), m >= n, float64, on the GPU or the host."""
+    m, n = A.shape
+    if A.dtype != torch.float64 or m < n:
+        raise ValueError("A must be float64 with m >= n")
+    Acm = colmajor(A)
+    dev = Acm.device
+    pin = dev.type == "cpu"
+    if out is None:
+        sig = torch.empty(n, dtype=torch.float64, device=dev, pin_memory=pin)
+        U = empty_colmajor(m, n, device=dev.type, pin=pin)
+        V = empty_colmajor(n, n, device=dev.type, pin=pin)
+    else:
+        sig, U, V = out
+    cfg = cfg or default_config("svd")
+    rep = mpj_report()
+    sw = C.c_int(0)
+    ws_ptr, ws_bytes = None, 0
+    if workspace is not None:
+        ws_ptr, ws_bytes = _ptr(workspace), workspace.numel() * workspace.element_size()
+    st = lib().mpjacobi_svd(_ptr(Acm), m, n, Acm.stride(1), _ptr(sig), _ptr(U), U.stride(1), _ptr(V), V.stride(1),
+                            C.byref(sw), ws_ptr, ws_bytes, _stream(), C.byref(cfg), C.byref(rep))
+    _check(st, (MPJ_OK, MPJ_ERR_NOCONV) if allow_noconv else (MPJ_OK,))
+    return SvdResult(sig, U, V, sw.value, rep)
+
+
+def svd_workspace(m, n, cfg: mpj_config | None = None, device="cuda"):
+    nbytes = lib().mpjacobi_svd_workspace(m, n, C.byref(cfg or default_config("svd")))
+    return torch.empty(nbytes, dtype=torch.uint8, device=device)
+
+
+@dataclass
 class BatchedResult:
     lam: torch.Tensor          # (batch, n), descending per matrix
     V: torch.Tensor            # (batch, n, n), V[k][i, j] = entry (i, j) of matrix k's eigenvectors
@@ -314,6 +355,7 @@ def mpjacobi_eig_batched(A, cfg: mpj_config | None = None, allow_noconv=False) -
 
 # short aliases
 eig_batched = mpjacobi_eig_batched
+svd = mpjacobi_svd
 eig = mpjacobi_eig
 jacobi = mpjacobi_jacobi
 orth = mpjacobi_orth

@@ -172,6 +172,25 @@ mpj_status block_sweep(R *T, int64_t ldt, R *V, int64_t ldv, int vrows, const De
     return MPJ_OK;
 }
 
+// M(:, P_c) <- M(:, P_c) U_c for every block pair c of block round Rb (M has
+// `rows` rows): the column update of the one-sided (SVD) block variant.
+template <typename R>
+void launch_block_apply_cols(R *M, int64_t ld, int rows, const DevSched &ds, int Rb, const R *Ubuf,
+                             cudaStream_t st)
+{
+    constexpr int LD = Lay<R>::LD;
+    Sched S;
+    S.bsched = ds.bsched; S.lsched = ds.lsched; S.b = ds.b; S.nb = ds.nb; S.np = ds.np;
+    const int mb = ds.nb / 2;
+    const size_t sm_apply = 3 * TW * LD * sizeof(R);
+    MPJ_CK_VOID(cudaFuncSetAttribute(k_block_apply<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_apply));
+    const int ntV = ((rows + TW - 1) / TW) * mb;
+    k_block_apply<R><<<ntV, NT, sm_apply, st>>>(nullptr, 0, M, ld, rows, S, Rb, Ubuf, 0);
+    count_launch();
+}
+template void launch_block_apply_cols<double>(double *, int64_t, int, const DevSched &, int, const double *, cudaStream_t);
+template void launch_block_apply_cols<float>(float *, int64_t, int, const DevSched &, int, const float *, cudaStream_t);
+
 template size_t block_scratch_bytes<double>(int, int);
 template size_t block_scratch_bytes<float>(int, int);
 template mpj_status block_sweep<double>(double *, int64_t, double *, int64_t, int, const DevSched &, double,

@@ -1,0 +1,422 @@
+// k_svd.cu -- Alg. 5: mixed-precision one-sided Jacobi SVD.
+//
+// One-sided (Hestenes) Jacobi rotates column pairs of C so that c_p^T c_q = 0
+// (Lemma 5.1): with alpha = c_p^T c_p, beta = c_q^T c_q,
+// gamma = c_p^T c_q the rotation is Lemma 3.1's with (a_pp, a_qq, a_pq) =
+// (alpha, beta, gamma), applied when |gamma| > nu sqrt(alpha beta) --
+// i.e. rot_params with stop_rule 1 (Remark 3.1's test) and nu = omega.
+//
+// Block variant with the ordering of reading R1 (b = 32).  Per block round:
+//   k_gram        G_a = C(:, P_a)^T C(:, P_a) for every block pair a
+//                 (64 x 64 x m DMMA products, split over m, fp64 partials)
+//   k_svd_solve   inner rounds on G_a (two-sided on the Gram == one-sided on
+//                 the columns in exact arithmetic) accumulating U_a
+//   block_apply   C(:, P_a) <- C(:, P_a) U_a, V(:, P_a) <- V(:, P_a) U_a
+// Stop test before each sweep: ||off(C^T C)||_F <= eps ||C^T C||_F (full Gram,
+// DMMA GEMM), and after each sweep the early stop rotations/N < 2e-4 (P:678,
+// reading R15).  Extraction: sigma_j = ||c_j|| sorted descending (stable,
+// R16), u_j = c_j / sigma_j, V's columns alike.
+#include "mpj_block.cuh"
+#include "mpj_device.cuh"
+#include "mpj_internal.h"
+
+#include <algorithm>
+#include <cstring>
+
+namespace mpj {
+namespace {
+
+using namespace blk;
+
+// partial Gram of block pair a over rows [z*kc, min(m, (z+1)*kc)), fp64 partials
+template <typename R>
+__global__ void __launch_bounds__(NT) k_gram(const R *__restrict__ C, int64_t ldc, int m, Sched S, int Rb, int kc,
+                                             double *__restrict__ Gpart, int splits)
+{
+    constexpr int LD = Lay<R>::LD;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    R *X = (R *)smem_raw;
+    const int a = blockIdx.x, z = blockIdx.y;
+    const int mb = S.nb >> 1;
+    const int2 bp = S.bsched[Rb * mb + a];
+    const int r0 = z * kc, r1 = min(m, r0 + kc);
+    Acc<double> tot;
+    #pragma unroll
+    for (int f = 0; f < 8; ++f) { tot.v[f][0] = 0.0; tot.v[f][1] = 0.0; }
+    // fp32 products are accumulated per 64-row chunk in fp32, then in fp64
+    double totf[16];
+    #pragma unroll
+    for (int i = 0; i < 16; ++i) totf[i] = 0.0;
+    for (int c0 = r0; c0 < r1; c0 += TW) {
+        for (int e = threadIdx.x; e < TW * TW; e += NT) {
+            const int li = e & (TW - 1), lj = e >> 6;
+            const int gi = c0 + li;
+            X[li + lj * LD] = gi < r1 ? C[gi + (int64_t)gidx(bp, lj) * ldc] : R(0);
+        }
+        __syncthreads();
+        if constexpr (sizeof(R) == 8) {
+            tile_mm_acc<true>((const double *)X, (const double *)X, tot.v);
+        } else {
+            Acc<float> part;
+            tile_mm<true>((const float *)X, (const float *)X, part.v);
+            #pragma unroll
+            for (int u = 0; u < 4; ++u)
+                #pragma unroll
+                for (int w = 0; w < 4; ++w) totf[u * 4 + w] += (double)part.v[u][w];
+        }
+        __syncthreads();
+    }
+    double *G = Gpart + ((size_t)a * splits + z) * TW * TW;
+    if constexpr (sizeof(R) == 8) {
+        tot.each([&](int i, int j, double v) { G[i + j * TW] = v; });
+    } else {
+        const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+        #pragma unroll
+        for (int u = 0; u < 4; ++u)
+            #pragma unroll
+            for (int w = 0; w < 4; ++w) G[(ty + 16 * u) + (tx + 16 * w) * TW] = totf[u * 4 + w];
+    }
+}
+
+template <typename R>
+__global__ void __launch_bounds__(NT) k_svd_solve(const double *__restrict__ Gpart, int splits, Sched S, int Rb,
+                                                  R nu, R *__restrict__ Ubuf, unsigned long long *__restrict__ cnt)
+{
+    constexpr int LD = Lay<R>::LD;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    R *D = (R *)smem_raw;
+    R *U = D + TW * LD;
+    __shared__ InnerShared sh;
+    __shared__ InnerParams<R> pr;
+    const int a = blockIdx.x;
+    const int mb = S.nb >> 1;
+    const int2 bp = S.bsched[Rb * mb + a];
+    const double *G = Gpart + (size_t)a * splits * TW * TW;
+    for (int e = threadIdx.x; e < TW * TW; e += NT) {
+        const int li = e & (TW - 1), lj = e >> 6;
+        double g = 0.0;
+        for (int z = 0; z < splits; ++z) g += G[(size_t)z * TW * TW + e];   // fixed order
+        D[li + lj * LD] = (R)g;
+        U[li + lj * LD] = (li == lj) ? R(1) : R(0);
+    }
+    // exact symmetry of the Gram block (the partial sums are computed per entry)
+    __syncthreads();
+    for (int e = threadIdx.x; e < TW * TW; e += NT) {
+        const int li = e & (TW - 1), lj = e >> 6;
+        if (li < lj) D[lj + li * LD] = D[li + lj * LD];
+    }
+    const unsigned nrot = inner_rounds<R>(D, U, bp, Rb == 0, S.lsched, nu, /*rule=*/1, sh, pr);
+    R *Ua = Ubuf + (size_t)a * TW * TW;
+    for (int e = threadIdx.x; e < TW * TW; e += NT) {
+        const int li = e & (TW - 1), lj = e >> 6;
+        Ua[li + lj * TW] = U[li + lj * LD];
+    }
+    if (threadIdx.x == 0 && nrot) atomicAdd(cnt, (unsigned long long)nrot);
+}
+
+__global__ void __launch_bounds__(256) k_colnorm(const double *__restrict__ C, int64_t ldc, int m,
+                                                 double *__restrict__ nrm)
+{
+    __shared__ double sh[32];
+    const int j = blockIdx.x;
+    double acc = 0.0;
+    for (int i = threadIdx.x; i < m; i += blockDim.x) {
+        const double x = C[i + (int64_t)j * ldc];
+        acc = __fma_rn(x, x, acc);
+    }
+    const double s = block_sum<256>(acc, sh);
+    if (threadIdx.x == 0) nrm[j] = sqrt(s);
+}
+
+// rank[j] = stable descending position of nrm[j]; sigma[rank] = nrm[j]
+__global__ void k_rank_vec(const double *__restrict__ key, int n, int *__restrict__ rank, double *__restrict__ out,
+                           double thresh, int *__restrict__ flag)
+{
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= n) return;
+    const double d = key[j];
+    int r = 0;
+    for (int i = 0; i < n; ++i) {
+        const double e = key[i];
+        r += (e > d) || (e == d && i < j);
+    }
+    rank[j] = r;
+    out[r] = d;
+    if (!(d > thresh)) atomicOr(flag, 1);
+}
+
+// U(:, rank[j]) = C(:, j) / nrm[j];  V(:, rank[j]) = Vin(:, j)
+__global__ void k_svd_extract(const double *__restrict__ C, int64_t ldc, int m, const double *__restrict__ Vin,
+                              int64_t ldvi, int n, const int *__restrict__ rank, const double *__restrict__ nrm,
+                              double *__restrict__ U, int64_t ldu, double *__restrict__ V, int64_t ldv)
+{
+    const int j = blockIdx.y;
+    const int r = rank[j];
+    const double s = nrm[j];
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < m; i += gridDim.x * blockDim.x)
+        U[i + (int64_t)r * ldu] = s > 0.0 ? C[i + (int64_t)j * ldc] / s : 0.0;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+        V[i + (int64_t)r * ldv] = Vin[i + (int64_t)j * ldvi];
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// host side
+// ---------------------------------------------------------------------------
+struct SvdPlan {
+    int64_t m, n;
+    int np, mb, splits, kc;
+    double *Ad, *C, *V, *G, *Gpart, *nrm, *red_part, *red_out, *sig;
+    float *C32, *V32;
+    int2 *bsched, *lsched;
+    void *Ubuf;
+    unsigned long long *cnt;
+    int *rank, *flag;
+    void *orth_ws;
+};
+
+static void carve_svd(char *base, size_t &off, int64_t m, int64_t n, SvdPlan &p)
+{
+    auto take = [&](size_t bytes) -> void * {
+        off = (off + 255) & ~(size_t)255;
+        void *r = base ? (void *)(base + off) : nullptr;
+        off += bytes;
+        return r;
+    };
+    p.m = m; p.n = n;
+    p.np = padded_n(n, BW);
+    p.mb = p.np / TW;
+    p.splits = std::max(1, std::min<int>((int)((296 + p.mb - 1) / p.mb), (int)((m + TW - 1) / TW)));
+    p.kc = (int)(((m + p.splits - 1) / p.splits + TW - 1) / TW * TW);
+    const size_t mnp = (size_t)m * p.np, nn = (size_t)p.np * p.np;
+    p.Ad = (double *)take(mnp * 8);
+    p.C = (double *)take(mnp * 8);
+    p.V = (double *)take(nn * 8);
+    p.G = (double *)take(nn * 8);
+    p.C32 = (float *)take(mnp * 4);
+    p.V32 = (float *)take(nn * 4);
+    p.Gpart = (double *)take((size_t)p.mb * p.splits * TW * TW * 8);
+    p.Ubuf = take((size_t)p.mb * TW * TW * 8);
+    p.nrm = (double *)take(p.np * 8);
+    p.sig = (double *)take(p.np * 8);
+    p.red_part = (double *)take(kRedBlocks * 8);
+    p.red_out = (double *)take(64);
+    const int nb = p.np / BW;
+    p.bsched = (int2 *)take((size_t)std::max(nb - 1, 1) * std::max(nb / 2, 1) * sizeof(int2));
+    p.lsched = (int2 *)take((size_t)(BW - 1) * (BW / 2) * sizeof(int2));
+    p.cnt = (unsigned long long *)take(64);
+    p.rank = (int *)take(p.np * 4);
+    p.flag = (int *)take(64);
+    p.orth_ws = take(orth_workspace(p.np));
+}
+
+template <typename R>
+static mpj_status svd_block_sweep(SvdPlan &p, R *C, R *V, const DevSched &ds, R nu, cudaStream_t st)
+{
+    Sched S;
+    S.bsched = ds.bsched; S.lsched = ds.lsched; S.b = ds.b; S.nb = ds.nb; S.np = ds.np;
+    constexpr int LD = Lay<R>::LD;
+    const size_t sm_x = TW * LD * sizeof(R), sm_du = 2 * TW * LD * sizeof(R);
+    MPJ_CK(cudaFuncSetAttribute(k_gram<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_x));
+    MPJ_CK(cudaFuncSetAttribute(k_svd_solve<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_du));
+    const bool prof = prof_on();
+    const char *ng = sizeof(R) == 8 ? "svd_gram_f64" : "svd_gram_f32";
+    for (int Rb = 0; Rb < ds.nb - 1; ++Rb) {
+        if (prof) prof_mark(ng, st, true);
+        k_gram<R><<<dim3(p.mb, p.splits), NT, sm_x, st>>>(C, p.m, (int)p.m, S, Rb, p.kc, p.Gpart, p.splits);
+        if (prof) prof_mark(ng, st, false);
+        k_svd_solve<R><<<p.mb, NT, sm_du, st>>>(p.Gpart, p.splits, S, Rb, nu, (R *)p.Ubuf, p.cnt);
+        count_launch(2);
+        launch_block_apply_cols<R>(C, p.m, (int)p.m, ds, Rb, (const R *)p.Ubuf, st);
+        launch_block_apply_cols<R>(V, p.np, p.np, ds, Rb, (const R *)p.Ubuf, st);
+    }
+    return MPJ_OK;
+}
+
+struct SvdStage {
+    int sweeps = 0;
+    long long rotations = 0;
+    double hist[64] = {0};
+    int nhist = 0;
+};
+
+// the one-sided Jacobi loop on (C, V) in precision R; Cd: fp64 image buffer for
+// the stop test (== C when R is double)
+template <typename R>
+static mpj_status svd_loop(SvdPlan &p, R *C, R *V, double *Cd, const DevSched &ds, double eps_rel, R nu,
+                           double early, int max_sweeps, double *h_pin, cudaStream_t st, SvdStage &out)
+{
+    const double N = 0.5 * (double)p.n * (double)(p.n - 1);
+    mpj_status status = MPJ_ERR_NOCONV;
+    unsigned long long prev = 0;
+    MPJ_CK(cudaMemsetAsync(p.cnt, 0, sizeof(unsigned long long), st));
+    for (;;) {
+        if ((void *)Cd != (void *)C)
+            launch_copy_pad<R, double>(C, p.m, (int)p.m, p.np, Cd, p.m, (int)p.m, p.np, st);
+        launch_dgemm(true, false, p.np, p.np, p.m, 1.0, Cd, p.m, Cd, p.m, 0.0, p.G, p.np, st);
+        launch_norm<double>(p.G, p.np, p.np, p.np, true, p.red_part, p.red_out, st);
+        launch_norm<double>(p.G, p.np, p.np, p.np, false, p.red_part, p.red_out + 1, st);
+        MPJ_CK(cudaMemcpyAsync(h_pin, p.red_out, 2 * sizeof(double), cudaMemcpyDeviceToHost, st));
+        MPJ_CK(cudaStreamSynchronize(st));
+        prof_flush();
+        const double off = h_pin[0], tot = h_pin[1];
+        if (out.sweeps < 64) { out.hist[out.sweeps] = off; out.nhist = out.sweeps + 1; }
+        if (!(off == off)) { set_error("non-finite Gram"); return MPJ_ERR_NONFINITE; }
+        if (off <= eps_rel * tot) { status = MPJ_OK; break; }
+        if (out.sweeps >= max_sweeps) { status = MPJ_ERR_NOCONV; break; }
+        ++out.sweeps;
+        MPJ_TRY(svd_block_sweep<R>(p, C, V, ds, nu, st));
+        MPJ_CK(cudaMemcpyAsync(h_pin, p.cnt, sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
+        MPJ_CK(cudaStreamSynchronize(st));
+        prof_flush();
+        unsigned long long now = 0;
+        std::memcpy(&now, h_pin, sizeof(now));
+        const unsigned long long rs = now - prev;
+        prev = now;
+        out.rotations = (long long)now;
+        if (early > 0 && N > 0 && (double)rs / N < early) { status = MPJ_OK; break; }
+    }
+    return status;
+}
+
+size_t svd_workspace(int64_t m, int64_t n)
+{
+    size_t off = 0;
+    SvdPlan p;
+    carve_svd(nullptr, off, m, n, p);
+    return off + 256;
+}
+
+mpj_status svd_run(const double *A, int64_t m, int64_t n, int64_t lda, double *Sigma, double *U, int64_t ldu,
+                   double *V, int64_t ldv, int *sweeps, void *workspace, size_t ws_bytes, cudaStream_t st,
+                   const mpj_config &cfg, mpj_report &r, double *h_pin, bool a_dev, bool out_dev)
+{
+    const double omega = 1.1102230246251565e-16, upsilon = 5.9604644775390625e-08;
+    size_t off = 0;
+    SvdPlan p;
+    carve_svd(nullptr, off, m, n, p);
+    void *own = nullptr;
+    if (!workspace) {
+        MPJ_CK(cudaMallocAsync(&own, off + 256, st));
+        workspace = own;
+    } else if (ws_bytes < off + 256) {
+        set_error("workspace too small");
+        return MPJ_ERR_NOMEM;
+    }
+    char *base = (char *)(((uintptr_t)workspace + 255) & ~(uintptr_t)255);
+    off = 0;
+    carve_svd(base, off, m, n, p);
+    const int np = p.np;
+    r.n_padded = np; r.block_b = BW; r.variant = MPJ_VARIANT_BLOCK;
+
+    HostSchedule hs;
+    build_schedule(n, BW, hs);
+    MPJ_CK(cudaMemcpyAsync(p.bsched, hs.bsched.data(), hs.bsched.size() * sizeof(int2), cudaMemcpyHostToDevice, st));
+    MPJ_CK(cudaMemcpyAsync(p.lsched, hs.lsched.data(), hs.lsched.size() * sizeof(int2), cudaMemcpyHostToDevice, st));
+    DevSched ds;
+    ds.bsched = p.bsched; ds.lsched = p.lsched; ds.b = BW; ds.nb = hs.nb; ds.np = np; ds.rounds = hs.rounds;
+
+    // a0: stage A (zero-padded columns), ||A||_F, finiteness
+    MPJ_CK(cudaMemsetAsync(p.Ad, 0, (size_t)m * np * 8, st));
+    MPJ_CK(cudaMemcpy2DAsync(p.Ad, m * 8, A, lda * 8, m * 8, n,
+                             a_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, st));
+    MPJ_CK(cudaMemsetAsync(p.flag, 0, sizeof(int), st));
+    launch_check_finite(p.Ad, m, (int)m, (int)n, p.flag, st);
+    launch_norm<double>(p.Ad, m, (int)m, np, false, p.red_part, p.red_out, st);
+    MPJ_CK(cudaMemcpyAsync(h_pin, p.red_out, sizeof(double), cudaMemcpyDeviceToHost, st));
+    MPJ_CK(cudaMemcpyAsync(h_pin + 1, p.flag, sizeof(int), cudaMemcpyDeviceToHost, st));
+    MPJ_CK(cudaStreamSynchronize(st));
+    const double normA = h_pin[0];
+    int bad = 0;
+    std::memcpy(&bad, h_pin + 1, sizeof(int));
+    r.norm_a = normA;
+    auto fin = [&](mpj_status s) {
+        if (own) cudaFreeAsync(own, st);
+        return s;
+    };
+    if (bad) { set_error("input has NaN/Inf"); return fin(MPJ_ERR_NONFINITE); }
+
+    // a1: fp32 one-sided Jacobi on fl32(A) from V = I (reading R12)
+    {
+        cudaEvent_t e0, e1;
+        cudaEventCreate(&e0); cudaEventCreate(&e1);
+        cudaEventRecord(e0, st);
+        launch_copy_pad<double, float>(p.Ad, m, (int)m, np, p.C32, m, (int)m, np, st);
+        MPJ_CK(cudaMemsetAsync(p.V32, 0, (size_t)np * np * 4, st));
+        launch_identity<float>(p.V32, np, (int)n, (int)n, st);
+        SvdStage lo;
+        mpj_status sl = svd_loop<float>(p, p.C32, p.V32, p.C, ds, cfg.eps_low_factor * upsilon,
+                                        (float)(cfg.nu_low_factor * upsilon), cfg.early_stop_ratio,
+                                        cfg.max_sweeps_low, h_pin, st, lo);
+        if (sl != MPJ_OK && sl != MPJ_ERR_NOCONV) return fin(sl);
+        r.sweeps_low = lo.sweeps; r.rotations_low = lo.rotations; r.status_low = sl;
+        cudaEventRecord(e1, st);
+        cudaEventSynchronize(e1);
+        float ms = 0; cudaEventElapsedTime(&ms, e0, e1); r.t_low = ms * 1e-3;
+        // a2: Q = CGS2(fp64(V32)) into V
+        cudaEventRecord(e0, st);
+        launch_copy_pad<float, double>(p.V32, np, (int)n, (int)n, p.G, np, (int)n, (int)n, st);
+        MPJ_CK(cudaMemsetAsync(p.V, 0, (size_t)np * np * 8, st));
+        mpj_status so = orth_cgs2(p.G, np, p.V, np, n, n, p.orth_ws, st);
+        if (so != MPJ_OK) return fin(so);
+        cudaEventRecord(e1, st);
+        cudaEventSynchronize(e1);
+        cudaEventElapsedTime(&ms, e0, e1); r.t_orth = ms * 1e-3;
+        // a3: C = A Q
+        cudaEventRecord(e0, st);
+        MPJ_CK(cudaMemsetAsync(p.C, 0, (size_t)m * np * 8, st));
+        launch_dgemm(false, false, m, n, n, 1.0, p.Ad, m, p.V, np, 0.0, p.C, m, st);
+        cudaEventRecord(e1, st);
+        cudaEventSynchronize(e1);
+        cudaEventElapsedTime(&ms, e0, e1); r.t_precond = ms * 1e-3;
+        cudaEventDestroy(e0); cudaEventDestroy(e1);
+    }
+    // a4-a8 (one-sided): fp64 sweeps
+    SvdStage hi;
+    {
+        cudaEvent_t e0, e1;
+        cudaEventCreate(&e0); cudaEventCreate(&e1);
+        cudaEventRecord(e0, st);
+        mpj_status sh = svd_loop<double>(p, p.C, p.V, p.C, ds, cfg.eps_factor * omega, cfg.nu_factor * omega,
+                                         cfg.early_stop_ratio, cfg.max_sweeps, h_pin, st, hi);
+        r.sweeps = hi.sweeps; r.rotations = hi.rotations; r.status = sh;
+        r.off0 = hi.hist[0];
+        for (int k = 0; k < hi.nhist && k < 64; ++k) r.off_hist[k] = hi.hist[k];
+        cudaEventRecord(e1, st);
+        cudaEventSynchronize(e1);
+        float ms = 0; cudaEventElapsedTime(&ms, e0, e1); r.t_jacobi = ms * 1e-3;
+        cudaEventDestroy(e0); cudaEventDestroy(e1);
+        if (sh != MPJ_OK && sh != MPJ_ERR_NOCONV) return fin(sh);
+        if (sweeps) *sweeps = hi.sweeps;
+    }
+    // a10: extraction
+    k_colnorm<<<(unsigned)n, 256, 0, st>>>(p.C, m, (int)m, p.nrm);
+    MPJ_CK(cudaMemsetAsync(p.flag, 0, sizeof(int), st));
+    k_rank_vec<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(p.nrm, (int)n, p.rank, p.sig, (double)n * omega * normA,
+                                                            p.flag);
+    count_launch(2);
+    double *Ud = out_dev ? U : p.Ad;          // A is no longer needed: reuse its buffer
+    double *Vd = out_dev ? V : p.G;
+    double *Sd = out_dev ? Sigma : p.sig;
+    const int64_t lduo = out_dev ? ldu : m, ldvo = out_dev ? ldv : np;
+    if (out_dev) MPJ_CK(cudaMemcpyAsync(Sigma, p.sig, n * 8, cudaMemcpyDeviceToDevice, st));
+    k_svd_extract<<<dim3(std::max<int64_t>(1, std::min<int64_t>(64, (m + 255) / 256)), (unsigned)n), 256, 0, st>>>(
+        p.C, m, (int)m, p.V, np, (int)n, p.rank, p.nrm, Ud, lduo, Vd, ldvo);
+    count_launch();
+    (void)Sd;
+    if (!out_dev) {
+        MPJ_CK(cudaMemcpyAsync(Sigma, p.sig, n * 8, cudaMemcpyDeviceToHost, st));
+        MPJ_CK(cudaMemcpy2DAsync(U, ldu * 8, Ud, m * 8, m * 8, n, cudaMemcpyDeviceToHost, st));
+        MPJ_CK(cudaMemcpy2DAsync(V, ldv * 8, Vd, np * 8, n * 8, n, cudaMemcpyDeviceToHost, st));
+    }
+    MPJ_CK(cudaMemcpyAsync(h_pin + 2, p.flag, sizeof(int), cudaMemcpyDeviceToHost, st));
+    MPJ_CK(cudaStreamSynchronize(st));
+    int rd = 0;
+    std::memcpy(&rd, h_pin + 2, sizeof(int));
+    mpj_status s = (mpj_status)r.status;
+    if (s == MPJ_OK && rd) { set_error("rank deficient: some sigma_j <= n omega ||A||_F"); s = MPJ_ERR_RANKDEF; }
+    return fin(s);
+}
+
+}  // namespace mpj

@@ -129,12 +129,10 @@ __device__ __forceinline__ void dmma884(double &d0, double &d1, double a, double
 }
 
 template <bool TRANS_A>
-__device__ __forceinline__ void tile_mm(const double *A, const double *B, double (&acc)[8][2])
+__device__ __forceinline__ void tile_mm_acc(const double *A, const double *B, double (&acc)[8][2])
 {
     constexpr int LD = Lay<double>::LD;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, tig = lane & 3;
-    #pragma unroll
-    for (int f = 0; f < 8; ++f) { acc[f][0] = 0.0; acc[f][1] = 0.0; }
     const int row = warp * 8 + g;
     #pragma unroll 4
     for (int ks = 0; ks < TW / 4; ++ks) {
@@ -146,6 +144,13 @@ __device__ __forceinline__ void tile_mm(const double *A, const double *B, double
             dmma884(acc[f][0], acc[f][1], a, b);
         }
     }
+}
+template <bool TRANS_A>
+__device__ __forceinline__ void tile_mm(const double *A, const double *B, double (&acc)[8][2])
+{
+    #pragma unroll
+    for (int f = 0; f < 8; ++f) { acc[f][0] = 0.0; acc[f][1] = 0.0; }
+    tile_mm_acc<TRANS_A>(A, B, acc);
 }
 // element (i, j) of the accumulator fragment f, slot e
 __device__ __forceinline__ int acc_row() { return (threadIdx.x >> 5) * 8 + ((threadIdx.x & 31) >> 2); }

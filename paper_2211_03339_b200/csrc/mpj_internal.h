@@ -28,6 +28,12 @@ void prof_flush();   // after the stream has been synchronised
         }                                                                               \
     } while (0)
 
+#define MPJ_CK_VOID(expr)                                                               \
+    do {                                                                                \
+        cudaError_t e_ = (expr);                                                        \
+        if (e_ != cudaSuccess) ::mpj::set_error(std::string(#expr) + ": " + cudaGetErrorString(e_)); \
+    } while (0)
+
 #define MPJ_TRY(expr)                                                                   \
     do {                                                                                \
         mpj_status s_ = (expr);                                                         \
@@ -58,6 +64,11 @@ void launch_round_apply(R *T, int64_t ldt, const int2 *pq, const R *t, const R *
 template <typename R>
 void launch_round_apply_v(R *V, int64_t ldv, int vrows, const int2 *pq, const R *s, const R *u,
                           int h, cudaStream_t st);
+
+// ---- block variant pieces (k_block.cu) ---------------------------------------
+template <typename R>
+void launch_block_apply_cols(R *M, int64_t ld, int rows, const DevSched &ds, int Rb, const R *Ubuf,
+                             cudaStream_t st);
 
 // ---- utilities (k_util.cu) --------------------------------------------------
 // out[0] = sqrt(sum_{i != j} T_ij^2) (offdiag) or sqrt(sum T_ij^2) over an m x n

@@ -23,6 +23,12 @@
 
 namespace mpj {
 
+// SVD (k_svd.cu)
+size_t svd_workspace(int64_t m, int64_t n);
+mpj_status svd_run(const double *A, int64_t m, int64_t n, int64_t lda, double *Sigma, double *U, int64_t ldu,
+                   double *V, int64_t ldv, int *sweeps, void *workspace, size_t ws_bytes, cudaStream_t st,
+                   const mpj_config &cfg, mpj_report &r, double *h_pin, bool a_dev, bool out_dev);
+
 // Block-variant entry (k_block.cu).
 template <typename R>
 mpj_status block_sweep(R *T, int64_t ldt, R *V, int64_t ldv, int vrows, const DevSched &S, R nu,
@@ -753,16 +759,41 @@ mpj_status mpjacobi_dgemm(int transa, const double *A, const double *B, double *
 }  // extern "C"
 
 // ---------------------------------------------------------------------------
-// Entry points whose kernels land later in this round (k_svd.cu, k_batched.cu)
+// SVD entry points (kernels in k_svd.cu)
 // ---------------------------------------------------------------------------
 extern "C" {
-#ifndef MPJ_HAVE_SVD
-size_t mpjacobi_svd_workspace(int64_t, int64_t, const mpj_config *) { return 0; }
-mpj_status mpjacobi_svd(const double *, int64_t, int64_t, int64_t, double *, double *, int64_t, double *,
-                        int64_t, int *, void *, size_t, void *, const mpj_config *, mpj_report *)
+size_t mpjacobi_svd_workspace(int64_t m, int64_t n, const mpj_config *)
 {
-    mpj::set_error("mpjacobi_svd: not built yet");
-    return MPJ_ERR_INVALID;
+    if (m < 1 || n < 1 || m < n) return 0;
+    return mpj::svd_workspace(m, n);
 }
-#endif
+
+mpj_status mpjacobi_svd(const double *A, int64_t m, int64_t n, int64_t lda, double *Sigma, double *U, int64_t ldu,
+                        double *V, int64_t ldv, int *sweeps, void *workspace, size_t ws_bytes, void *stream,
+                        const mpj_config *cfg_in, mpj_report *rep)
+{
+    using namespace mpj;
+    set_error("");
+    if (n < 1 || m < n || lda < m || ldu < m || ldv < n || !A || !Sigma || !U || !V) {
+        set_error("mpjacobi_svd: need m >= n >= 1, lda, ldu >= m, ldv >= n, non-NULL buffers");
+        return MPJ_ERR_INVALID;
+    }
+    mpj_config cfg;
+    if (cfg_in) cfg = *cfg_in; else mpj_config_default_svd(&cfg);
+    Ctx cx;
+    MPJ_TRY(cx.open(stream));
+    const long long l0 = mpjacobi_launch_count();
+    Timer t_all(cx.st);
+    mpj_report r;
+    std::memset(&r, 0, sizeof(r));
+    const bool a_dev = is_device_ptr(A);
+    const bool out_dev = is_device_ptr(U) && is_device_ptr(V) && is_device_ptr(Sigma);
+    mpj_status s = svd_run(A, m, n, lda, Sigma, U, ldu, V, ldv, sweeps, workspace, ws_bytes, cx.st, cfg, r,
+                           cx.h_pin, a_dev, out_dev);
+    r.t_total = t_all.stop();
+    r.launches = mpjacobi_launch_count() - l0;
+    if (rep) *rep = r;
+    mpj_status c = cx.close();
+    return s != MPJ_OK ? s : c;
+}
 }

@@ -278,3 +278,32 @@ def test_eig_batched(mpj, orc, n, batch):
 def test_eig_batched_invalid(mpj):
     with pytest.raises(mpj.MpjError):
         mpj.eig_batched(torch.zeros((2, 65, 65), dtype=torch.float64, device="cuda"))
+
+
+# ----------------------------------------------------------------- SVD (Alg. 5)
+@pytest.mark.parametrize("m,n,mode", [(96, 48, 3), (200, 64, 4), (300, 130, 5), (512, 256, 3)])
+def test_svd_end_to_end(mpj, orc, m, n, mode):
+    """Alg. 5 on the GPU (block one-sided Jacobi) vs the oracle's Alg. 5 (same
+    ordering): sigma within 1e-13 sigma_1, residual / orthogonality at the
+    north_star tolerances, fp64 sweeps within the R20 allowance."""
+    A, sig_true = W.example3(m, n, 1e3, mode, W.seed_for(5, mode, 1e3))
+    res = mpj.svd(dev(A))
+    ref = orc.mp_svd(A, orc.default_cfg("svd", b=32))
+    sig, U, V = host(res.sigma), host(res.U), host(res.V)
+    assert np.max(np.abs(sig - ref.sigma)) <= 1e-13 * ref.sigma[0]
+    assert np.max(np.abs(sig - sig_true)) <= 1e-13 * sig_true[0]
+    assert np.linalg.norm(A @ V - U * sig) / np.linalg.norm(A) <= n * 1e-15
+    assert np.linalg.norm(U.T @ U - np.eye(n)) <= n * 1e-15
+    assert np.linalg.norm(V.T @ V - np.eye(n)) <= n * 1e-15
+    assert abs(res.sweeps - ref.report.sweeps) <= 1, (res.sweeps, ref.report.sweeps)
+
+
+def test_svd_host_buffers_and_errors(mpj):
+    A, _ = W.example3(80, 40, 1e3, 4, 9)
+    r_dev = mpj.svd(dev(A))
+    Ah = torch.from_numpy(np.ascontiguousarray(A.T)).T.pin_memory()
+    r_host = mpj.svd(Ah)
+    assert np.array_equal(r_host.sigma.numpy(), host(r_dev.sigma))
+    assert np.array_equal(r_host.U.numpy(), host(r_dev.U))
+    with pytest.raises(ValueError):
+        mpj.svd(dev(A.T.copy()))   # m < n
