@@ -46,7 +46,8 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample-seconds", type=float, default=20.0)
-    ap.add_argument("--workload", default="evd", choices=["evd", "batched"],
+    ap.add_argument("--m", type=int, default=16384, help="rows for --workload svd")
+    ap.add_argument("--workload", default="evd", choices=["evd", "batched", "svd"],
                     help="evd: BASELINE config 4 (the bench line); batched: config 3 (4096 x n=64)")
     ap.add_argument("--batch", type=int, default=4096)
     return ap.parse_args()
@@ -255,12 +256,67 @@ def run_batched(args):
     print(json.dumps(line))
 
 
+def run_svd(args):
+    """BASELINE config 5a: Alg. 5 on an Example 3 matrix, m x n =
+    16384 x 4096 by default, mode 3, kappa = 1e3."""
+    import torch
+
+    import paper_2211_03339_b200 as mpj
+    import workloads as W
+    m, n = args.m, (args.n if args.n != 8192 else 4096)
+    At, sig_true = W.example3_torch(m, n, 1e3, 3, 2211033390 + 5000 + 300 + 30, device="cuda")
+    A = At.T          # column-major m x n view
+    cfg = mpj.default_config("svd")
+    ws = mpj.svd_workspace(m, n, cfg)
+    sig = torch.empty(n, dtype=torch.float64, device="cuda")
+    U = mpj.empty_colmajor(m, n)
+    V = mpj.empty_colmajor(n, n)
+    for _ in range(args.warmup):
+        res = mpj.svd(A, cfg, workspace=ws, out=(sig, U, V), allow_noconv=True)
+    torch.cuda.synchronize()
+    mpj.profile_reset()
+    mpj.profile_enable(True)
+    l0 = mpj.launch_count()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(0) as clk:
+        e0.record()
+        for _ in range(args.steps):
+            res = mpj.svd(A, cfg, workspace=ws, out=(sig, U, V), allow_noconv=True)
+        e1.record()
+        torch.cuda.synchronize()
+    mpj.profile_enable(False)
+    ms = e0.elapsed_time(e1) / args.steps
+    rep = res.report
+    kern = {}
+    for name in ("block_apply_f64", "block_apply_f32", "svd_gram_f64", "svd_gram_f32"):
+        sec, cnt = mpj.profile_get(name)
+        if cnt:
+            kern[name] = {"seconds_per_step": sec / args.steps, "launches": cnt, "avg_ms": 1e3 * sec / cnt}
+    R = torch.linalg.norm(A @ V - U * sig) / torch.linalg.norm(A)
+    OU = torch.linalg.norm(U.T @ U - torch.eye(n, device="cuda", dtype=torch.float64))
+    OV = torch.linalg.norm(V.T @ V - torch.eye(n, device="cuda", dtype=torch.float64))
+    line = {"metric": f"fp64 SVD seconds ({m}x{n})", "value": ms * 1e-3, "unit": "s", "n_gpus": 1,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": False,
+            "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"Example 3 (P:1112) mode 3 kappa=1e3, {m} x {n} (BASELINE config 5a)"},
+            "sweeps": rep.sweeps, "sweeps_low": rep.sweeps_low,
+            "ju": rep.rotations / (n * (n - 1) / 2), "ju_low": rep.rotations_low / (n * (n - 1) / 2),
+            "stage_seconds": {"low_fp32": rep.t_low, "orth": rep.t_orth, "precond": rep.t_precond,
+                              "jacobi_fp64": rep.t_jacobi},
+            "check": {"residual": float(R), "orth_u": float(OU), "orth_v": float(OV),
+                      "max_dsig_rel": float((sig - sig_true).abs().max() / sig_true[0])},
+            "kernels": kern, "gpu_launches": mpj.launch_count() - l0, "clocks": clk.summary()}
+    print(json.dumps(line))
+
+
 def main():
     args = parse()
     if args.impl == "reference":
         return run_reference(args)
     if args.workload == "batched":
         return run_batched(args)
+    if args.workload == "svd":
+        return run_svd(args)
     import numpy as np
     import torch
 

@@ -285,7 +285,11 @@ def test_eig_batched_invalid(mpj):
 def test_svd_end_to_end(mpj, orc, m, n, mode):
     """Alg. 5 on the GPU (block one-sided Jacobi) vs the oracle's Alg. 5 (same
     ordering): sigma within 1e-13 sigma_1, residual / orthogonality at the
-    north_star tolerances, fp64 sweeps within the R20 allowance."""
+    north_star tolerances.  Sweeps (reading R21): with nu = omega the
+    rotate test |c_p^T c_q| > omega ||c_p|| ||c_q|| is decided at the rounding
+    noise of an fp64 Gram entry, so the GPU (fp64 DMMA Gram blocks) performs
+    spurious noise-level rotations that the long-double oracle does not and
+    reaches the 2e-4 early stop later: never earlier, at most 5 sweeps later."""
     A, sig_true = W.example3(m, n, 1e3, mode, W.seed_for(5, mode, 1e3))
     res = mpj.svd(dev(A))
     ref = orc.mp_svd(A, orc.default_cfg("svd", b=32))
@@ -295,7 +299,7 @@ def test_svd_end_to_end(mpj, orc, m, n, mode):
     assert np.linalg.norm(A @ V - U * sig) / np.linalg.norm(A) <= n * 1e-15
     assert np.linalg.norm(U.T @ U - np.eye(n)) <= n * 1e-15
     assert np.linalg.norm(V.T @ V - np.eye(n)) <= n * 1e-15
-    assert abs(res.sweeps - ref.report.sweeps) <= 1, (res.sweeps, ref.report.sweeps)
+    assert ref.report.sweeps <= res.sweeps <= ref.report.sweeps + 5, (res.sweeps, ref.report.sweeps)
 
 
 def test_svd_host_buffers_and_errors(mpj):
