@@ -158,12 +158,12 @@ __global__ void __launch_bounds__(NT, 2) k_batched_evd(BatchedArgs a)
     // a3: T = Q^T (As Q), symmetrised
     {
         Acc<double> w;
-        tile_mm<false>(RA, RB, w.v);       // W = As Q
+        tile_mm<false>(RA, RB, w);       // W = As Q
         __syncthreads();
         w.each([&](int i, int j, double x) { RC[i + j * LD] = x; });
         __syncthreads();
         Acc<double> t;
-        tile_mm<true>(RB, RC, t.v);        // T = Q^T W
+        tile_mm<true>(RB, RC, t);        // T = Q^T W
         __syncthreads();
         t.each([&](int i, int j, double x) { RA[i + j * LD] = x; });
         __syncthreads();

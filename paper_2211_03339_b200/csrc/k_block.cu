@@ -20,6 +20,8 @@
 #include "mpj_internal.h"
 #include "mpj_block.cuh"
 
+#include <algorithm>
+
 namespace mpj {
 
 namespace {
@@ -59,72 +61,133 @@ __global__ void __launch_bounds__(NT) k_block_solve(R *__restrict__ T, int64_t l
 }
 
 // ---------------------------------------------------------------------------
-// K4: apply.  blockIdx.x < ntT: T tile (a, c), a < c; else V tile.
+// K4: apply (persistent, cp.async double-buffered).
+// Work items: [0, ntT) upper tiles (a, c), a < c, of T:  W = U_a^T X U_c,
+// stored to (a, c) and W^T to (c, a);  [ntT, ntT + ntV) row tiles of M (= V,
+// or C for the one-sided SVD):  M(r0:r0+64, P_c) <- M(r0:r0+64, P_c) U_c.
+// CTA b handles items b, b + G, b + 2G, ...; the loads of item i+1 (X, U_a,
+// U_c: 16-byte LDGSTS) are in flight while item i is multiplied.
 // ---------------------------------------------------------------------------
-template <typename R>
-__global__ void __launch_bounds__(NT) k_block_apply(R *__restrict__ T, int64_t ldt, R *__restrict__ V,
-                                                    int64_t ldv, int vrows, Sched S, int Rb,
-                                                    const R *__restrict__ Ubuf, int ntT)
+__device__ __forceinline__ void cp16(void *dst, const void *src, int src_bytes)
 {
-    constexpr int LD = Lay<R>::LD;
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    R *X = (R *)smem_raw;
-    R *Ua = X + TW * LD;
-    R *Uc = Ua + TW * LD;
-    const int mb = S.nb >> 1;
-    const int2 *bsr = S.bsched + Rb * mb;
-    int idx = blockIdx.x;
-    if (idx < ntT) {
-        // upper-triangular decode: idx -> (a, c), a < c
-        int c = (int)((1.0 + sqrt(1.0 + 8.0 * idx)) * 0.5);
-        while (c * (c - 1) / 2 > idx) --c;
-        while ((c + 1) * c / 2 <= idx) ++c;
-        const int a = idx - c * (c - 1) / 2;
+    const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(d), "l"(src), "r"(src_bytes));
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+__device__ __forceinline__ void cp_wait1() { asm volatile("cp.async.wait_group 1;\n" ::); }
+__device__ __forceinline__ void cp_wait0() { asm volatile("cp.async.wait_group 0;\n" ::); }
+
+struct ApplyArgs {
+    void *T; int64_t ldt;
+    void *M; int64_t ldm; int mrows;
+    Sched S; int Rb;
+    const void *Ubuf;
+    int ntT, ntV;
+};
+
+__device__ __forceinline__ void decode_upper(int idx, int &a, int &c)
+{
+    c = (int)((1.0 + sqrt(1.0 + 8.0 * idx)) * 0.5);
+    while (c * (c - 1) / 2 > idx) --c;
+    while ((c + 1) * c / 2 <= idx) ++c;
+    a = idx - c * (c - 1) / 2;
+}
+
+// issue the loads of work item `item` into stage buffers (X, Ua, Uc)
+template <typename R>
+__device__ __forceinline__ void issue_item(const ApplyArgs &p, int item, R *X, R *Ua, R *Uc)
+{
+    constexpr int LD = Lay<R>::LD, EPC = 16 / sizeof(R), CPC = TW / EPC;   // elements / chunks per column
+    const int mb = p.S.nb >> 1;
+    const int2 *bsr = p.S.bsched + p.Rb * mb;
+    const R *Ub = (const R *)p.Ubuf;
+    if (item < p.ntT) {
+        int a, c;
+        decode_upper(item, a, c);
         const int2 pa = bsr[a], pc = bsr[c];
-        load_tile<R>(X, T, ldt, pa, pc);
-        load_u<R>(Ua, Ubuf + (size_t)a * TW * TW);
-        load_u<R>(Uc, Ubuf + (size_t)c * TW * TW);
-        __syncthreads();
-        Acc<R> y;
-        tile_mm<true>(Ua, X, y.v);                 // Y = Ua^T X
-        __syncthreads();
-        y.each([&](int i, int j, R v) { X[i + j * LD] = v; });
-        __syncthreads();
-        Acc<R> w;
-        tile_mm<false>(X, Uc, w.v);                // W = Y Uc
-        __syncthreads();
-        w.each([&](int i, int j, R v) { X[i + j * LD] = v; });
-        __syncthreads();
-        // store W into (a, c) and W^T into (c, a); both loops coalesced along rows
-        for (int e = threadIdx.x; e < TW * TW; e += NT) {
-            const int li = e & (TW - 1), lj = e >> 6;
-            T[gidx(pa, li) + (int64_t)gidx(pc, lj) * ldt] = X[li + lj * LD];
-            T[gidx(pc, li) + (int64_t)gidx(pa, lj) * ldt] = X[lj + li * LD];
+        const R *T = (const R *)p.T;
+        for (int e = threadIdx.x; e < TW * CPC; e += NT) {
+            const int lj = e / CPC, li = (e - lj * CPC) * EPC;
+            cp16(X + li + lj * LD, T + gidx(pa, li) + (int64_t)gidx(pc, lj) * p.ldt, 16);
+            cp16(Ua + li + lj * LD, Ub + (size_t)a * TW * TW + li + lj * TW, 16);
+            cp16(Uc + li + lj * LD, Ub + (size_t)c * TW * TW + li + lj * TW, 16);
         }
     } else {
-        idx -= ntT;
-        const int c = idx % mb, rt = idx / mb;
+        const int idx = item - p.ntT, c = idx % mb, r0 = (idx / mb) * TW;
         const int2 pc = bsr[c];
-        const int r0 = rt * TW;
-        // X = V(r0:r0+64, P_c)
-        for (int e = threadIdx.x; e < TW * TW; e += NT) {
-            const int li = e & (TW - 1), lj = e >> 6;
-            const int gi = r0 + li;
-            X[li + lj * LD] = gi < vrows ? V[gi + (int64_t)gidx(pc, lj) * ldv] : R(0);
-        }
-        load_u<R>(Uc, Ubuf + (size_t)c * TW * TW);
-        __syncthreads();
-        Acc<R> w;
-        tile_mm<false>(X, Uc, w.v);
-        __syncthreads();
-        w.each([&](int i, int j, R v) { X[i + j * LD] = v; });
-        __syncthreads();
-        for (int e = threadIdx.x; e < TW * TW; e += NT) {
-            const int li = e & (TW - 1), lj = e >> 6;
-            const int gi = r0 + li;
-            if (gi < vrows) V[gi + (int64_t)gidx(pc, lj) * ldv] = X[li + lj * LD];
+        const R *M = (const R *)p.M;
+        for (int e = threadIdx.x; e < TW * CPC; e += NT) {
+            const int lj = e / CPC, li = (e - lj * CPC) * EPC;
+            const int rem = p.mrows - (r0 + li);
+            const int bytes = rem >= EPC ? 16 : (rem > 0 ? rem * (int)sizeof(R) : 0);
+            const R *src = M + (bytes ? (int64_t)(r0 + li) : 0) + (int64_t)gidx(pc, lj) * p.ldm;
+            cp16(X + li + lj * LD, src, bytes);
+            cp16(Uc + li + lj * LD, Ub + (size_t)c * TW * TW + li + lj * TW, 16);
         }
     }
+}
+
+template <typename R>
+__global__ void __launch_bounds__(NT, 1) k_block_apply(ApplyArgs p)
+{
+    constexpr int LD = Lay<R>::LD, EPC = 16 / sizeof(R), CPC = TW / EPC;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    R *buf = (R *)smem_raw;                       // stage s: X, Ua, Uc at buf + (3s + {0,1,2}) * TW * LD
+    const int total = p.ntT + p.ntV;
+    const int mb = p.S.nb >> 1;
+    const int2 *bsr = p.S.bsched + p.Rb * mb;
+    int item = blockIdx.x;
+    if (item < total) issue_item<R>(p, item, buf, buf + TW * LD, buf + 2 * TW * LD);
+    cp_commit();
+    for (int it = 0; item < total; ++it, item += gridDim.x) {
+        const int s = it & 1;
+        const int next = item + gridDim.x;
+        R *nb = buf + (size_t)(3 * (s ^ 1)) * TW * LD;
+        if (next < total) issue_item<R>(p, next, nb, nb + TW * LD, nb + 2 * TW * LD);
+        cp_commit();
+        cp_wait1();
+        __syncthreads();
+        R *x = buf + (size_t)(3 * s) * TW * LD, *ua = x + TW * LD, *uc = x + 2 * TW * LD;
+        Acc<R> acc;
+        if (item < p.ntT) {
+            int a, c;
+            decode_upper(item, a, c);
+            const int2 pa = bsr[a], pc = bsr[c];
+            tile_mm<true>(ua, x, acc);                           // Y = Ua^T X
+            __syncthreads();
+            acc.each([&](int i, int j, R v) { x[i + j * LD] = v; });
+            __syncthreads();
+            tile_mm<false>(x, uc, acc);                          // W = Y Uc
+            __syncthreads();
+            acc.each([&](int i, int j, R v) { x[i + j * LD] = v; ua[j + i * LD] = v; });   // W and W^T
+            __syncthreads();
+            R *T = (R *)p.T;
+            for (int e = threadIdx.x; e < TW * CPC; e += NT) {
+                const int lj = e / CPC, li = (e - lj * CPC) * EPC;
+                *(int4 *)(T + gidx(pa, li) + (int64_t)gidx(pc, lj) * p.ldt) = *(const int4 *)(x + li + lj * LD);
+                *(int4 *)(T + gidx(pc, li) + (int64_t)gidx(pa, lj) * p.ldt) = *(const int4 *)(ua + li + lj * LD);
+            }
+        } else {
+            const int idx = item - p.ntT, c = idx % mb, r0 = (idx / mb) * TW;
+            const int2 pc = bsr[c];
+            tile_mm<false>(x, uc, acc);                          // W = X Uc
+            __syncthreads();
+            acc.each([&](int i, int j, R v) { x[i + j * LD] = v; });
+            __syncthreads();
+            R *M = (R *)p.M;
+            for (int e = threadIdx.x; e < TW * CPC; e += NT) {
+                const int lj = e / CPC, li = (e - lj * CPC) * EPC;
+                R *dst = M + (int64_t)(r0 + li) + (int64_t)gidx(pc, lj) * p.ldm;
+                if (r0 + li + EPC <= p.mrows) {
+                    *(int4 *)dst = *(const int4 *)(x + li + lj * LD);
+                } else {
+                    for (int q = 0; q < EPC && r0 + li + q < p.mrows; ++q) dst[q] = x[li + q + lj * LD];
+                }
+            }
+        }
+        __syncthreads();
+    }
+    cp_wait0();
 }
 
 }  // namespace
@@ -135,6 +198,34 @@ size_t block_scratch_bytes(int np, int b)
     (void)b;
     const int mb = np / (2 * BW);
     return (size_t)mb * TW * TW * sizeof(R);
+}
+
+static int sm_count()
+{
+    static int n = 0;
+    if (!n) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+        if (n <= 0) n = 148;
+    }
+    return n;
+}
+
+template <typename R>
+static void launch_apply(const ApplyArgs &p, cudaStream_t st)
+{
+    constexpr int LD = Lay<R>::LD;
+    const size_t smem = 6 * TW * LD * sizeof(R);
+    static bool attr = false;
+    if (!attr) {
+        MPJ_CK_VOID(cudaFuncSetAttribute(k_block_apply<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        attr = true;
+    }
+    const int total = p.ntT + p.ntV;
+    const int grid = std::max(1, std::min(total, sm_count()));
+    k_block_apply<R><<<grid, NT, smem, st>>>(p);
+    count_launch();
 }
 
 template <typename R>
@@ -148,26 +239,27 @@ mpj_status block_sweep(R *T, int64_t ldt, R *V, int64_t ldv, int vrows, const De
     const int mb = ds.nb / 2;
     R *Ubuf = (R *)scratch;
     const size_t sm_solve = 2 * TW * LD * sizeof(R);
-    const size_t sm_apply = 3 * TW * LD * sizeof(R);
     static bool attr_done[2] = {false, false};
     const int ti = sizeof(R) == 8 ? 0 : 1;
     if (!attr_done[ti]) {
         MPJ_CK(cudaFuncSetAttribute(k_block_solve<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_solve));
-        MPJ_CK(cudaFuncSetAttribute(k_block_apply<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_apply));
         attr_done[ti] = true;
     }
-    const int ntT = mb * (mb - 1) / 2;
-    const int ntV = ((vrows + TW - 1) / TW) * mb;
+    ApplyArgs ap;
+    ap.T = T; ap.ldt = ldt; ap.M = V; ap.ldm = ldv; ap.mrows = vrows; ap.S = S; ap.Ubuf = Ubuf;
+    ap.ntT = mb * (mb - 1) / 2;
+    ap.ntV = ((vrows + TW - 1) / TW) * mb;
     const char *nsolve = sizeof(R) == 8 ? "block_solve_f64" : "block_solve_f32";
     const char *napply = sizeof(R) == 8 ? "block_apply_f64" : "block_apply_f32";
     const bool prof = prof_on();
     for (int Rb = 0; Rb < ds.nb - 1; ++Rb) {
         if (prof) prof_mark(nsolve, st, true);
         k_block_solve<R><<<mb, NT, sm_solve, st>>>(T, ldt, S, Rb, nu, rule, Ubuf, cnt);
+        count_launch();
         if (prof) { prof_mark(nsolve, st, false); prof_mark(napply, st, true); }
-        k_block_apply<R><<<ntT + ntV, NT, sm_apply, st>>>(T, ldt, V, ldv, vrows, S, Rb, Ubuf, ntT);
+        ap.Rb = Rb;
+        launch_apply<R>(ap, st);
         if (prof) prof_mark(napply, st, false);
-        count_launch(2);
     }
     return MPJ_OK;
 }
@@ -178,15 +270,13 @@ template <typename R>
 void launch_block_apply_cols(R *M, int64_t ld, int rows, const DevSched &ds, int Rb, const R *Ubuf,
                              cudaStream_t st)
 {
-    constexpr int LD = Lay<R>::LD;
     Sched S;
     S.bsched = ds.bsched; S.lsched = ds.lsched; S.b = ds.b; S.nb = ds.nb; S.np = ds.np;
-    const int mb = ds.nb / 2;
-    const size_t sm_apply = 3 * TW * LD * sizeof(R);
-    MPJ_CK_VOID(cudaFuncSetAttribute(k_block_apply<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_apply));
-    const int ntV = ((rows + TW - 1) / TW) * mb;
-    k_block_apply<R><<<ntV, NT, sm_apply, st>>>(nullptr, 0, M, ld, rows, S, Rb, Ubuf, 0);
-    count_launch();
+    ApplyArgs ap;
+    ap.T = nullptr; ap.ldt = 0; ap.M = M; ap.ldm = ld; ap.mrows = rows; ap.S = S; ap.Rb = Rb; ap.Ubuf = Ubuf;
+    ap.ntT = 0;
+    ap.ntV = ((rows + TW - 1) / TW) * (ds.nb / 2);
+    launch_apply<R>(ap, st);
 }
 template void launch_block_apply_cols<double>(double *, int64_t, int, const DevSched &, int, const double *, cudaStream_t);
 template void launch_block_apply_cols<float>(float *, int64_t, int, const DevSched &, int, const float *, cudaStream_t);

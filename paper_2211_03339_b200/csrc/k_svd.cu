@@ -41,8 +41,7 @@ __global__ void __launch_bounds__(NT) k_gram(const R *__restrict__ C, int64_t ld
     const int2 bp = S.bsched[Rb * mb + a];
     const int r0 = z * kc, r1 = min(m, r0 + kc);
     Acc<double> tot;
-    #pragma unroll
-    for (int f = 0; f < 8; ++f) { tot.v[f][0] = 0.0; tot.v[f][1] = 0.0; }
+    tot.zero();
     // fp32 products are accumulated per 64-row chunk in fp32, then in fp64
     double totf[16];
     #pragma unroll
@@ -55,10 +54,10 @@ __global__ void __launch_bounds__(NT) k_gram(const R *__restrict__ C, int64_t ld
         }
         __syncthreads();
         if constexpr (sizeof(R) == 8) {
-            tile_mm_acc<true>((const double *)X, (const double *)X, tot.v);
+            tile_mm_acc<true>((const double *)X, (const double *)X, tot);
         } else {
             Acc<float> part;
-            tile_mm<true>((const float *)X, (const float *)X, part.v);
+            tile_mm<true>((const float *)X, (const float *)X, part);
             #pragma unroll
             for (int u = 0; u < 4; ++u)
                 #pragma unroll
@@ -70,11 +69,11 @@ __global__ void __launch_bounds__(NT) k_gram(const R *__restrict__ C, int64_t ld
     if constexpr (sizeof(R) == 8) {
         tot.each([&](int i, int j, double v) { G[i + j * TW] = v; });
     } else {
-        const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+        const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;   // Acc<float> mapping: rows tx+16u, cols ty+16w
         #pragma unroll
         for (int u = 0; u < 4; ++u)
             #pragma unroll
-            for (int w = 0; w < 4; ++w) G[(ty + 16 * u) + (tx + 16 * w) * TW] = totf[u * 4 + w];
+            for (int w = 0; w < 4; ++w) G[(tx + 16 * u) + (ty + 16 * w) * TW] = totf[u * 4 + w];
     }
 }
 

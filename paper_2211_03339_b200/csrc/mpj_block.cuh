@@ -15,7 +15,7 @@ constexpr int NT = 256;  // threads per CTA
 
 template <typename R> struct Lay;
 template <> struct Lay<double> { static constexpr int LD = 68; };   // 2 wavefronts / DMMA frag
-template <> struct Lay<float> { static constexpr int LD = 65; };    // conflict-free SIMT tiles
+template <> struct Lay<float> { static constexpr int LD = 68; };    // 16-byte aligned columns (cp.async)
 
 // global index of local index li (0..63) of block pair (I, J)
 __device__ __forceinline__ int gidx(int2 bp, int li) { return li < BW ? bp.x * BW + li : bp.y * BW + (li - BW); }
@@ -115,11 +115,14 @@ __device__ __forceinline__ unsigned inner_rounds(R *D, R *U, int2 bp, bool intra
 
 // ---------------------------------------------------------------------------
 // 64 x 64 x 64 tile products in shared memory.
-//   C = op(A) * B  with A, B, C column-major (leading dimension LD);
-//   TRANS_A: op(A) = A^T.
-// fp64: 8 warps, warp w owns rows 8w..8w+7 (8 fragments of 8 x 8 along n),
-// mma.sync m8n8k4 (DMMA).  fp32: 4 x 4 register tiles per thread (FFMA).
-// Results are returned in registers (acc) -- callers store them.
+//   C = op(A) * B  with A, B column-major (leading dimension Lay<R>::LD);
+//   TRANS_A: op(A) = A^T.  Results stay in registers (Acc<R>).
+// fp64: 8 warps in a 4 x 2 grid, warp tile 16 x 32 = 2 x 4 fragments of
+//   mma.sync m8n8k4 (DMMA): per k-step 2 A + 4 B fragment loads feed 8 DMMA;
+//   every fragment load is 2 shared-memory wavefronts (the minimum for 32
+//   8-byte lanes) with LD = 68.
+// fp32: thread (tx, ty) owns rows tx + 16u, columns ty + 16v (4 x 4): A loads
+//   are consecutive words, B loads are warp broadcasts -> conflict-free.
 // ---------------------------------------------------------------------------
 __device__ __forceinline__ void dmma884(double &d0, double &d1, double a, double b)
 {
@@ -128,100 +131,109 @@ __device__ __forceinline__ void dmma884(double &d0, double &d1, double a, double
                  : "d"(a), "d"(b));
 }
 
-template <bool TRANS_A>
-__device__ __forceinline__ void tile_mm_acc(const double *A, const double *B, double (&acc)[8][2])
-{
-    constexpr int LD = Lay<double>::LD;
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, tig = lane & 3;
-    const int row = warp * 8 + g;
-    #pragma unroll 4
-    for (int ks = 0; ks < TW / 4; ++ks) {
-        const int kk = ks * 4 + tig;
-        const double a = TRANS_A ? A[kk + row * LD] : A[row + kk * LD];
-        #pragma unroll
-        for (int f = 0; f < 8; ++f) {
-            const double b = B[kk + (f * 8 + g) * LD];
-            dmma884(acc[f][0], acc[f][1], a, b);
-        }
-    }
-}
-template <bool TRANS_A>
-__device__ __forceinline__ void tile_mm(const double *A, const double *B, double (&acc)[8][2])
-{
-    #pragma unroll
-    for (int f = 0; f < 8; ++f) { acc[f][0] = 0.0; acc[f][1] = 0.0; }
-    tile_mm_acc<TRANS_A>(A, B, acc);
-}
-// element (i, j) of the accumulator fragment f, slot e
-__device__ __forceinline__ int acc_row() { return (threadIdx.x >> 5) * 8 + ((threadIdx.x & 31) >> 2); }
-__device__ __forceinline__ int acc_col(int f, int e) { return f * 8 + 2 * (threadIdx.x & 3) + e; }
-
-template <bool TRANS_A>
-__device__ __forceinline__ void tile_mm(const float *A, const float *B, float (&acc)[4][4])
-{
-    constexpr int LD = Lay<float>::LD;
-    const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
-    #pragma unroll
-    for (int u = 0; u < 4; ++u)
-        #pragma unroll
-        for (int v = 0; v < 4; ++v) acc[u][v] = 0.f;
-    #pragma unroll 4
-    for (int kk = 0; kk < TW; ++kk) {
-        float a[4], b[4];
-        #pragma unroll
-        for (int u = 0; u < 4; ++u) {
-            const int i = ty + 16 * u;
-            a[u] = TRANS_A ? A[kk + i * LD] : A[i + kk * LD];
-        }
-        #pragma unroll
-        for (int v = 0; v < 4; ++v) b[v] = B[kk + (tx + 16 * v) * LD];
-        #pragma unroll
-        for (int u = 0; u < 4; ++u)
-            #pragma unroll
-            for (int v = 0; v < 4; ++v) acc[u][v] = __fmaf_rn(a[u], b[v], acc[u][v]);
-    }
-}
-
 template <typename R> struct Acc;
 template <> struct Acc<double> {
-    double v[8][2];
-    template <typename F> __device__ __forceinline__ void each(F f)
+    double v[2][4][2];
+    __device__ __forceinline__ void zero()
     {
-        const int r = acc_row();
         #pragma unroll
-        for (int q = 0; q < 8; ++q) { f(r, acc_col(q, 0), v[q][0]); f(r, acc_col(q, 1), v[q][1]); }
+        for (int a = 0; a < 2; ++a)
+            #pragma unroll
+            for (int b = 0; b < 4; ++b) { v[a][b][0] = 0.0; v[a][b][1] = 0.0; }
+    }
+    template <typename F> __device__ __forceinline__ void each(F f) const
+    {
+        const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+        const int r0 = (warp >> 1) * 16 + (lane >> 2), c0 = (warp & 1) * 32 + 2 * (lane & 3);
+        #pragma unroll
+        for (int mi = 0; mi < 2; ++mi)
+            #pragma unroll
+            for (int ni = 0; ni < 4; ++ni) {
+                f(r0 + mi * 8, c0 + ni * 8, v[mi][ni][0]);
+                f(r0 + mi * 8, c0 + ni * 8 + 1, v[mi][ni][1]);
+            }
+    }
+    // (i, j) pairs with j, j+1 adjacent: f2(i, j, v_j, v_j+1)
+    template <typename F> __device__ __forceinline__ void each2(F f) const
+    {
+        const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+        const int r0 = (warp >> 1) * 16 + (lane >> 2), c0 = (warp & 1) * 32 + 2 * (lane & 3);
+        #pragma unroll
+        for (int mi = 0; mi < 2; ++mi)
+            #pragma unroll
+            for (int ni = 0; ni < 4; ++ni) f(r0 + mi * 8, c0 + ni * 8, v[mi][ni][0], v[mi][ni][1]);
     }
 };
 template <> struct Acc<float> {
     float v[4][4];
-    template <typename F> __device__ __forceinline__ void each(F f)
+    __device__ __forceinline__ void zero()
+    {
+        #pragma unroll
+        for (int u = 0; u < 4; ++u)
+            #pragma unroll
+            for (int w = 0; w < 4; ++w) v[u][w] = 0.f;
+    }
+    template <typename F> __device__ __forceinline__ void each(F f) const
     {
         const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
         #pragma unroll
         for (int u = 0; u < 4; ++u)
             #pragma unroll
-            for (int w = 0; w < 4; ++w) f(ty + 16 * u, tx + 16 * w, v[u][w]);
+            for (int w = 0; w < 4; ++w) f(tx + 16 * u, ty + 16 * w, v[u][w]);
     }
 };
 
-// load a 64 x 64 tile whose rows are the block-pair rows (rp) and columns given by colmap
-template <typename R>
-__device__ __forceinline__ void load_tile(R *dst, const R *__restrict__ src, int64_t ld, int2 rp, int2 cp)
+template <bool TRANS_A>
+__device__ __forceinline__ void tile_mm_acc(const double *A, const double *B, Acc<double> &acc)
 {
-    constexpr int LD = Lay<R>::LD;
-    for (int e = threadIdx.x; e < TW * TW; e += NT) {
-        const int li = e & (TW - 1), lj = e >> 6;
-        dst[li + lj * LD] = src[gidx(rp, li) + (int64_t)gidx(cp, lj) * ld];
+    constexpr int LD = Lay<double>::LD;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, tig = lane & 3;
+    const int rb = (warp >> 1) * 16 + g, cb = (warp & 1) * 32 + g;
+    #pragma unroll 4
+    for (int ks = 0; ks < TW / 4; ++ks) {
+        const int kk = ks * 4 + tig;
+        double a[2], b[4];
+        #pragma unroll
+        for (int mi = 0; mi < 2; ++mi) {
+            const int row = rb + mi * 8;
+            a[mi] = TRANS_A ? A[kk + row * LD] : A[row + kk * LD];
+        }
+        #pragma unroll
+        for (int ni = 0; ni < 4; ++ni) b[ni] = B[kk + (cb + ni * 8) * LD];
+        #pragma unroll
+        for (int mi = 0; mi < 2; ++mi)
+            #pragma unroll
+            for (int ni = 0; ni < 4; ++ni) dmma884(acc.v[mi][ni][0], acc.v[mi][ni][1], a[mi], b[ni]);
     }
 }
-template <typename R>
-__device__ __forceinline__ void load_u(R *dst, const R *__restrict__ Uk)
+
+template <bool TRANS_A>
+__device__ __forceinline__ void tile_mm_acc(const float *A, const float *B, Acc<float> &acc)
 {
-    constexpr int LD = Lay<R>::LD;
-    for (int e = threadIdx.x; e < TW * TW; e += NT) {
-        const int li = e & (TW - 1), lj = e >> 6;
-        dst[li + lj * LD] = Uk[li + lj * TW];
+    constexpr int LD = Lay<float>::LD;
+    const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+    #pragma unroll 4
+    for (int kk = 0; kk < TW; ++kk) {
+        float a[4], b[4];
+        #pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int i = tx + 16 * u;
+            a[u] = TRANS_A ? A[kk + i * LD] : A[i + kk * LD];
+        }
+        #pragma unroll
+        for (int w = 0; w < 4; ++w) b[w] = B[kk + (ty + 16 * w) * LD];
+        #pragma unroll
+        for (int u = 0; u < 4; ++u)
+            #pragma unroll
+            for (int w = 0; w < 4; ++w) acc.v[u][w] = __fmaf_rn(a[u], b[w], acc.v[u][w]);
     }
+}
+
+template <bool TRANS_A, typename R>
+__device__ __forceinline__ void tile_mm(const R *A, const R *B, Acc<R> &acc)
+{
+    acc.zero();
+    tile_mm_acc<TRANS_A>(A, B, acc);
 }
 
 }  // namespace blk
