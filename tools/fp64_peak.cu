@@ -52,6 +52,44 @@ __global__ void ffma_kernel(float *out, int iters, float a, float b)
     if (s == 12345.678f) out[0] = s;
 }
 
+__global__ void tf32_kernel(float *out, int iters)
+{
+    unsigned a0 = threadIdx.x, a1 = a0 + 1, a2 = a0 + 2, a3 = a0 + 3, b0 = a0 ^ 5, b1 = a0 ^ 7;
+    float d[8][4];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) d[i][0] = d[i][1] = d[i][2] = d[i][3] = 0.f;
+    for (int it = 0; it < iters; ++it) {
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+            asm volatile("mma.sync.aligned.m16n8k8.row.col.f32.tf32.tf32.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};\n"
+                         : "+f"(d[i][0]), "+f"(d[i][1]), "+f"(d[i][2]), "+f"(d[i][3])
+                         : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+    }
+    float s = 0;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) s += d[i][0] + d[i][1] + d[i][2] + d[i][3];
+    if (s == 12345.678f) out[0] = s;
+}
+
+__global__ void bf16_kernel(float *out, int iters)
+{
+    unsigned a0 = threadIdx.x, a1 = a0 + 1, a2 = a0 + 2, a3 = a0 + 3, b0 = a0 ^ 5, b1 = a0 ^ 7;
+    float d[8][4];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) d[i][0] = d[i][1] = d[i][2] = d[i][3] = 0.f;
+    for (int it = 0; it < iters; ++it) {
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+            asm volatile("mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};\n"
+                         : "+f"(d[i][0]), "+f"(d[i][1]), "+f"(d[i][2]), "+f"(d[i][3])
+                         : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+    }
+    float s = 0;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) s += d[i][0] + d[i][1] + d[i][2] + d[i][3];
+    if (s == 12345.678f) out[0] = s;
+}
+
 int main()
 {
     int nsm = 0;
@@ -63,7 +101,7 @@ int main()
     cudaEventCreate(&b);
     const int iters = 20000;
     float ms;
-    double best_dfma = 0, best_dmma = 0, best_ffma = 0;
+    double best_dfma = 0, best_dmma = 0, best_ffma = 0, best_tf32 = 0, best_bf16 = 0;
     for (int rep = 0; rep < 5; ++rep) {
         int blocks = nsm * 4, threads = 512;
         cudaEventRecord(a);
@@ -89,9 +127,27 @@ int main()
         cudaEventElapsedTime(&ms, a, b);
         fl = 2.0 * 8 * iters * (double)blocks * threads;
         if (fl / (ms * 1e-3) > best_ffma) best_ffma = fl / (ms * 1e-3);
+
+        cudaEventRecord(a);
+        tf32_kernel<<<blocks, threads>>>((float *)dout, iters / 4);
+        cudaEventRecord(b);
+        cudaEventSynchronize(b);
+        cudaEventElapsedTime(&ms, a, b);
+        fl = 2.0 * 16 * 8 * 8 * 8 * (iters / 4) * (double)blocks * (threads / 32);
+        if (fl / (ms * 1e-3) > best_tf32) best_tf32 = fl / (ms * 1e-3);
+
+        cudaEventRecord(a);
+        bf16_kernel<<<blocks, threads>>>((float *)dout, iters / 4);
+        cudaEventRecord(b);
+        cudaEventSynchronize(b);
+        cudaEventElapsedTime(&ms, a, b);
+        fl = 2.0 * 16 * 8 * 16 * 8 * (iters / 4) * (double)blocks * (threads / 32);
+        if (fl / (ms * 1e-3) > best_bf16) best_bf16 = fl / (ms * 1e-3);
     }
     cudaError_t e = cudaGetLastError();
-    printf("{\"sms\": %d, \"dfma_tflops\": %.3f, \"dmma_tflops\": %.3f, \"ffma_tflops\": %.3f, \"err\": \"%s\"}\n",
-           nsm, best_dfma * 1e-12, best_dmma * 1e-12, best_ffma * 1e-12, cudaGetErrorString(e));
+    printf("{\"sms\": %d, \"dfma_tflops\": %.3f, \"dmma_tflops\": %.3f, \"ffma_tflops\": %.3f, "
+           "\"mma_sync_tf32_tflops\": %.3f, \"mma_sync_bf16_tflops\": %.3f, \"err\": \"%s\"}\n",
+           nsm, best_dfma * 1e-12, best_dmma * 1e-12, best_ffma * 1e-12, best_tf32 * 1e-12, best_bf16 * 1e-12,
+           cudaGetErrorString(e));
     return e == cudaSuccess ? 0 : 1;
 }
