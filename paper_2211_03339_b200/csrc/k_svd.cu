@@ -58,8 +58,10 @@ __global__ void __launch_bounds__(NT) k_gram(const R *__restrict__ C, int64_t ld
         } else {
             Acc<float> part;
             tile_mm<true>((const float *)X, (const float *)X, part);
-            int q = 0;
-            part.each([&](int, int, float v) { totf[q++] += (double)v; });
+            #pragma unroll
+            for (int u = 0; u < 4; ++u)
+                #pragma unroll
+                for (int w = 0; w < 4; ++w) totf[u * 4 + w] += (double)part.v[u][w];
         }
         __syncthreads();
     }
@@ -67,9 +69,11 @@ __global__ void __launch_bounds__(NT) k_gram(const R *__restrict__ C, int64_t ld
     if constexpr (sizeof(R) == 8) {
         tot.each([&](int i, int j, double v) { G[i + j * TW] = v; });
     } else {
-        Acc<float> shape;
-        int q = 0;
-        shape.each([&](int i, int j, float) { G[i + j * TW] = totf[q++]; });
+        const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;   // Acc<float> mapping: rows tx+16u, cols ty+16w
+        #pragma unroll
+        for (int u = 0; u < 4; ++u)
+            #pragma unroll
+            for (int w = 0; w < 4; ++w) G[(tx + 16 * u) + (ty + 16 * w) * TW] = totf[u * 4 + w];
     }
 }
 

@@ -15,7 +15,7 @@ constexpr int NT = 256;  // threads per CTA
 
 template <typename R> struct Lay;
 template <> struct Lay<double> { static constexpr int LD = 68; };   // 2 wavefronts / DMMA frag
-template <> struct Lay<float> { static constexpr int LD = 72; };    // 16-B aligned; conflict-free tf32 fragments
+template <> struct Lay<float> { static constexpr int LD = 68; };    // 16-byte aligned columns (cp.async)
 
 // global index of local index li (0..63) of block pair (I, J)
 __device__ __forceinline__ int gidx(int2 bp, int li) { return li < BW ? bp.x * BW + li : bp.y * BW + (li - BW); }
@@ -121,8 +121,8 @@ __device__ __forceinline__ unsigned inner_rounds(R *D, R *U, int2 bp, bool intra
 //   mma.sync m8n8k4 (DMMA): per k-step 2 A + 4 B fragment loads feed 8 DMMA;
 //   every fragment load is 2 shared-memory wavefronts (the minimum for 32
 //   8-byte lanes) with LD = 68.
-// fp32: 3 x TF32 on the tensor pipe (mma.sync m16n8k8), warp tile 32 x 16;
-//   LD = 72 makes every fragment load conflict-free.
+// fp32: thread (tx, ty) owns rows tx + 16u, columns ty + 16v (4 x 4): A loads
+//   are consecutive words, B loads are warp broadcasts -> conflict-free.
 // ---------------------------------------------------------------------------
 __device__ __forceinline__ void dmma884(double &d0, double &d1, double a, double b)
 {
@@ -165,30 +165,21 @@ template <> struct Acc<double> {
     }
 };
 template <> struct Acc<float> {
-    float v[2][2][4];   // [m-tile][n-tile][mma.m16n8 accumulator]
+    float v[4][4];
     __device__ __forceinline__ void zero()
     {
         #pragma unroll
-        for (int a = 0; a < 2; ++a)
+        for (int u = 0; u < 4; ++u)
             #pragma unroll
-            for (int b = 0; b < 2; ++b)
-                #pragma unroll
-                for (int c = 0; c < 4; ++c) v[a][b][c] = 0.f;
+            for (int w = 0; w < 4; ++w) v[u][w] = 0.f;
     }
     template <typename F> __device__ __forceinline__ void each(F f) const
     {
-        const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, tig = lane & 3;
-        const int r0 = (warp >> 2) * 32 + g, c0 = (warp & 3) * 16 + 2 * tig;
+        const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
         #pragma unroll
-        for (int mi = 0; mi < 2; ++mi)
+        for (int u = 0; u < 4; ++u)
             #pragma unroll
-            for (int ni = 0; ni < 2; ++ni) {
-                const int r = r0 + mi * 16, c = c0 + ni * 8;
-                f(r, c, v[mi][ni][0]);
-                f(r, c + 1, v[mi][ni][1]);
-                f(r + 8, c, v[mi][ni][2]);
-                f(r + 8, c + 1, v[mi][ni][3]);
-            }
+            for (int w = 0; w < 4; ++w) f(tx + 16 * u, ty + 16 * w, v[u][w]);
     }
 };
 
@@ -216,53 +207,25 @@ __device__ __forceinline__ void tile_mm_acc(const double *A, const double *B, Ac
     }
 }
 
-// fp32 products on the tensor pipe as 3 x TF32 (reading R22): x = hi + lo with
-// hi = tf32(x), lo = tf32(x - hi); A B ~ A_lo B_hi + A_hi B_lo + A_hi B_hi
-// (each TF32 product exact in the fp32 accumulator), mma.sync m16n8k8.
-__device__ __forceinline__ void split_tf32(float x, unsigned &hi, unsigned &lo)
-{
-    asm("cvt.rna.tf32.f32 %0, %1;\n" : "=r"(hi) : "f"(x));
-    const float r = x - __uint_as_float(hi);
-    asm("cvt.rna.tf32.f32 %0, %1;\n" : "=r"(lo) : "f"(r));
-}
-__device__ __forceinline__ void mma_tf32(float (&d)[4], const unsigned (&a)[4], unsigned b0, unsigned b1)
-{
-    asm volatile("mma.sync.aligned.m16n8k8.row.col.f32.tf32.tf32.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
-                 "{%0,%1,%2,%3};\n"
-                 : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
-                 : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
-}
-
 template <bool TRANS_A>
 __device__ __forceinline__ void tile_mm_acc(const float *A, const float *B, Acc<float> &acc)
 {
     constexpr int LD = Lay<float>::LD;
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, tig = lane & 3;
-    const int rb = (warp >> 2) * 32 + g, cb = (warp & 3) * 16 + g;
-    #pragma unroll 2
-    for (int k0 = 0; k0 < TW; k0 += 8) {
-        unsigned ah[2][4], al[2][4], bh[2][2], bl[2][2];
+    const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+    #pragma unroll 4
+    for (int kk = 0; kk < TW; ++kk) {
+        float a[4], b[4];
         #pragma unroll
-        for (int mi = 0; mi < 2; ++mi) {
-            #pragma unroll
-            for (int q = 0; q < 4; ++q) {
-                const int row = rb + mi * 16 + (q & 1) * 8, kk = k0 + tig + (q >> 1) * 4;
-                const float x = TRANS_A ? A[kk + row * LD] : A[row + kk * LD];
-                split_tf32(x, ah[mi][q], al[mi][q]);
-            }
+        for (int u = 0; u < 4; ++u) {
+            const int i = tx + 16 * u;
+            a[u] = TRANS_A ? A[kk + i * LD] : A[i + kk * LD];
         }
         #pragma unroll
-        for (int ni = 0; ni < 2; ++ni)
-            #pragma unroll
-            for (int q = 0; q < 2; ++q) split_tf32(B[k0 + tig + q * 4 + (cb + ni * 8) * LD], bh[ni][q], bl[ni][q]);
+        for (int w = 0; w < 4; ++w) b[w] = B[kk + (ty + 16 * w) * LD];
         #pragma unroll
-        for (int mi = 0; mi < 2; ++mi)
+        for (int u = 0; u < 4; ++u)
             #pragma unroll
-            for (int ni = 0; ni < 2; ++ni) {
-                mma_tf32(acc.v[mi][ni], al[mi], bh[ni][0], bh[ni][1]);
-                mma_tf32(acc.v[mi][ni], ah[mi], bl[ni][0], bl[ni][1]);
-                mma_tf32(acc.v[mi][ni], ah[mi], bh[ni][0], bh[ni][1]);
-            }
+            for (int w = 0; w < 4; ++w) acc.v[u][w] = __fmaf_rn(a[u], b[w], acc.v[u][w]);
     }
 }
 
