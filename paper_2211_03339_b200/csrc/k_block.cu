@@ -52,10 +52,12 @@ __global__ void __launch_bounds__(NT) k_block_solve(R *__restrict__ T, int64_t l
     }
     const unsigned nrot = inner_rounds<R>(D, U, bp, Rb == 0, S.lsched, nu, rule, sh, pr);
     R *Uk = Ubuf + (size_t)k * TW * TW;
+    R *UkT = Ubuf + (size_t)(S.nb >> 1) * TW * TW + (size_t)k * TW * TW;   // U^T (fp32 apply operand)
     for (int e = threadIdx.x; e < TW * TW; e += NT) {
         const int li = e & (TW - 1), lj = e >> 6;
         T[gidx(bp, li) + (int64_t)gidx(bp, lj) * ldt] = D[li + lj * LD];
         Uk[li + lj * TW] = U[li + lj * LD];
+        if (sizeof(R) == 4) UkT[li + lj * TW] = U[lj + li * LD];
     }
     if (threadIdx.x == 0 && nrot) atomicAdd(cnt, (unsigned long long)nrot);
 }
@@ -101,16 +103,21 @@ __device__ __forceinline__ void issue_item(const ApplyArgs &p, int item, R *X, R
     const int mb = p.S.nb >> 1;
     const int2 *bsr = p.S.bsched + p.Rb * mb;
     const R *Ub = (const R *)p.Ubuf;
+    // fp32 uses the k-major operands U^T (second half of Ubuf) and, for T
+    // tiles, X^T = T(P_c, P_a) (T is exactly symmetric)
+    const bool f32 = sizeof(R) == 4;
+    const R *UbO = f32 ? Ub + (size_t)mb * TW * TW : Ub;
     if (item < p.ntT) {
         int a, c;
         decode_upper(item, a, c);
         const int2 pa = bsr[a], pc = bsr[c];
+        const int2 rr = f32 ? pc : pa, cc = f32 ? pa : pc;
         const R *T = (const R *)p.T;
         for (int e = threadIdx.x; e < TW * CPC; e += NT) {
             const int lj = e / CPC, li = (e - lj * CPC) * EPC;
-            cp16(X + li + lj * LD, T + gidx(pa, li) + (int64_t)gidx(pc, lj) * p.ldt, 16);
-            cp16(Ua + li + lj * LD, Ub + (size_t)a * TW * TW + li + lj * TW, 16);
-            cp16(Uc + li + lj * LD, Ub + (size_t)c * TW * TW + li + lj * TW, 16);
+            cp16(X + li + lj * LD, T + gidx(rr, li) + (int64_t)gidx(cc, lj) * p.ldt, 16);
+            cp16(Ua + li + lj * LD, UbO + (size_t)a * TW * TW + li + lj * TW, 16);
+            cp16(Uc + li + lj * LD, UbO + (size_t)c * TW * TW + li + lj * TW, 16);
         }
     } else {
         const int idx = item - p.ntT, c = idx % mb, r0 = (idx / mb) * TW;
@@ -122,7 +129,7 @@ __device__ __forceinline__ void issue_item(const ApplyArgs &p, int item, R *X, R
             const int bytes = rem >= EPC ? 16 : (rem > 0 ? rem * (int)sizeof(R) : 0);
             const R *src = M + (bytes ? (int64_t)(r0 + li) : 0) + (int64_t)gidx(pc, lj) * p.ldm;
             cp16(X + li + lj * LD, src, bytes);
-            cp16(Uc + li + lj * LD, Ub + (size_t)c * TW * TW + li + lj * TW, 16);
+            cp16(Uc + li + lj * LD, UbO + (size_t)c * TW * TW + li + lj * TW, 16);
         }
     }
 }
@@ -148,18 +155,29 @@ __global__ void __launch_bounds__(NT, 1) k_block_apply(ApplyArgs p)
         cp_wait1();
         __syncthreads();
         R *x = buf + (size_t)(3 * s) * TW * LD, *ua = x + TW * LD, *uc = x + 2 * TW * LD;
-        Acc<R> acc;
         if (item < p.ntT) {
             int a, c;
             decode_upper(item, a, c);
             const int2 pa = bsr[a], pc = bsr[c];
-            tile_mm<true>(ua, x, acc);                           // Y = Ua^T X
-            __syncthreads();
-            acc.each([&](int i, int j, R v) { x[i + j * LD] = v; });
-            __syncthreads();
-            tile_mm<false>(x, uc, acc);                          // W = Y Uc
-            __syncthreads();
-            acc.each([&](int i, int j, R v) { x[i + j * LD] = v; ua[j + i * LD] = v; });   // W and W^T
+            if constexpr (sizeof(R) == 4) {
+                AccOP o;
+                tile_op((const float *)ua, (const float *)x, o);   // Y = Ua^T X  (U_a^T, X^T k-major)
+                __syncthreads();
+                store_op(o, (float *)x, nullptr);                   // Y column-major (k-major for GEMM 2)
+                __syncthreads();
+                tile_op((const float *)x, (const float *)uc, o);   // W = Y Uc   (Y, U_c^T k-major)
+                __syncthreads();
+                store_op(o, (float *)x, (float *)ua);               // W and W^T
+            } else {
+                Acc<R> acc;
+                tile_mm<true>(ua, x, acc);                           // Y = Ua^T X
+                __syncthreads();
+                acc.each([&](int i, int j, R v) { x[i + j * LD] = v; });
+                __syncthreads();
+                tile_mm<false>(x, uc, acc);                          // W = Y Uc
+                __syncthreads();
+                acc.each([&](int i, int j, R v) { x[i + j * LD] = v; ua[j + i * LD] = v; });   // W and W^T
+            }
             __syncthreads();
             R *T = (R *)p.T;
             for (int e = threadIdx.x; e < TW * CPC; e += NT) {
@@ -170,9 +188,17 @@ __global__ void __launch_bounds__(NT, 1) k_block_apply(ApplyArgs p)
         } else {
             const int idx = item - p.ntT, c = idx % mb, r0 = (idx / mb) * TW;
             const int2 pc = bsr[c];
-            tile_mm<false>(x, uc, acc);                          // W = X Uc
-            __syncthreads();
-            acc.each([&](int i, int j, R v) { x[i + j * LD] = v; });
+            if constexpr (sizeof(R) == 4) {
+                AccOP o;
+                tile_op((const float *)x, (const float *)uc, o);   // W = X Uc (X column-major, U_c^T)
+                __syncthreads();
+                store_op(o, (float *)x, nullptr);
+            } else {
+                Acc<R> acc;
+                tile_mm<false>(x, uc, acc);                          // W = X Uc
+                __syncthreads();
+                acc.each([&](int i, int j, R v) { x[i + j * LD] = v; });
+            }
             __syncthreads();
             R *M = (R *)p.M;
             for (int e = threadIdx.x; e < TW * CPC; e += NT) {
@@ -197,7 +223,7 @@ size_t block_scratch_bytes(int np, int b)
 {
     (void)b;
     const int mb = np / (2 * BW);
-    return (size_t)mb * TW * TW * sizeof(R);
+    return 2 * (size_t)mb * TW * TW * sizeof(R);   // U and U^T per block pair
 }
 
 static int sm_count()

@@ -106,9 +106,11 @@ __global__ void __launch_bounds__(NT) k_svd_solve(const double *__restrict__ Gpa
     }
     const unsigned nrot = inner_rounds<R>(D, U, bp, Rb == 0, S.lsched, nu, /*rule=*/1, sh, pr);
     R *Ua = Ubuf + (size_t)a * TW * TW;
+    R *UaT = Ubuf + (size_t)mb * TW * TW + (size_t)a * TW * TW;   // U^T: operand of the fp32 apply
     for (int e = threadIdx.x; e < TW * TW; e += NT) {
         const int li = e & (TW - 1), lj = e >> 6;
         Ua[li + lj * TW] = U[li + lj * LD];
+        if (sizeof(R) == 4) UaT[li + lj * TW] = U[lj + li * LD];
     }
     if (threadIdx.x == 0 && nrot) atomicAdd(cnt, (unsigned long long)nrot);
 }

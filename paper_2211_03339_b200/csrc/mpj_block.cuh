@@ -229,6 +229,49 @@ __device__ __forceinline__ void tile_mm_acc(const float *A, const float *B, Acc<
     }
 }
 
+// fp32 outer-product form for operands stored "k-major": C[i, j] = sum_k
+// A[i + k LD] B[j + k LD].  Thread (tx, ty) = (tid & 15, tid >> 4) owns rows
+// 4tx..4tx+3 and columns 4ty..4ty+3: one 128-bit LDS for each operand per k
+// (A: 16 distinct contiguous vectors per warp, B: a broadcast) feeds 16 FFMA.
+struct AccOP {
+    float v[4][4];
+    __device__ __forceinline__ int r0() const { return 4 * (threadIdx.x & 15); }
+    __device__ __forceinline__ int c0() const { return 4 * (threadIdx.x >> 4); }
+};
+__device__ __forceinline__ void tile_op(const float *A, const float *B, AccOP &acc)
+{
+    constexpr int LD = 68;
+    const int ra = 4 * (threadIdx.x & 15), cb = 4 * (threadIdx.x >> 4);
+    #pragma unroll
+    for (int u = 0; u < 4; ++u)
+        #pragma unroll
+        for (int w = 0; w < 4; ++w) acc.v[u][w] = 0.f;
+    #pragma unroll 8
+    for (int k = 0; k < TW; ++k) {
+        const float4 a = *(const float4 *)(A + ra + k * LD);
+        const float4 b = *(const float4 *)(B + cb + k * LD);
+        const float av[4] = {a.x, a.y, a.z, a.w}, bv[4] = {b.x, b.y, b.z, b.w};
+        #pragma unroll
+        for (int u = 0; u < 4; ++u)
+            #pragma unroll
+            for (int w = 0; w < 4; ++w) acc.v[u][w] = __fmaf_rn(av[u], bv[w], acc.v[u][w]);
+    }
+}
+// C (column-major) and C^T (column-major) stores of an AccOP, 128-bit each
+__device__ __forceinline__ void store_op(const AccOP &acc, float *C, float *CT)
+{
+    constexpr int LD = 68;
+    const int r = acc.r0(), c = acc.c0();
+    #pragma unroll
+    for (int w = 0; w < 4; ++w)
+        *(float4 *)(C + r + (c + w) * LD) = make_float4(acc.v[0][w], acc.v[1][w], acc.v[2][w], acc.v[3][w]);
+    if (CT) {
+        #pragma unroll
+        for (int u = 0; u < 4; ++u)
+            *(float4 *)(CT + c + (r + u) * LD) = make_float4(acc.v[u][0], acc.v[u][1], acc.v[u][2], acc.v[u][3]);
+    }
+}
+
 template <bool TRANS_A, typename R>
 __device__ __forceinline__ void tile_mm(const R *A, const R *B, Acc<R> &acc)
 {
