@@ -135,7 +135,7 @@ __device__ __forceinline__ void issue_item(const ApplyArgs &p, int item, R *X, R
 }
 
 template <typename R>
-__global__ void __launch_bounds__(NT, 1) k_block_apply(ApplyArgs p)
+__global__ void __launch_bounds__(NT) k_block_apply(ApplyArgs p)
 {
     constexpr int LD = Lay<R>::LD, EPC = 16 / sizeof(R), CPC = TW / EPC;
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -248,8 +248,13 @@ static void launch_apply(const ApplyArgs &p, cudaStream_t st)
         MPJ_CK_VOID(cudaFuncSetAttribute(k_block_apply<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         attr = true;
     }
+    static int per_sm = 0;
+    if (!per_sm) {
+        MPJ_CK_VOID(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_block_apply<R>, NT, smem));
+        per_sm = std::max(1, per_sm);
+    }
     const int total = p.ntT + p.ntV;
-    const int grid = std::max(1, std::min(total, sm_count()));
+    const int grid = std::max(1, std::min(total, sm_count() * per_sm));
     k_block_apply<R><<<grid, NT, smem, st>>>(p);
     count_launch();
 }
