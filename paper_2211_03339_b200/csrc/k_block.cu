@@ -21,6 +21,7 @@
 #include "mpj_block.cuh"
 
 #include <algorithm>
+#include <cstdlib>
 
 namespace mpj {
 
@@ -134,7 +135,9 @@ __device__ __forceinline__ void issue_item(const ApplyArgs &p, int item, R *X, R
     }
 }
 
-template <typename R>
+// STAGES = 2: one CTA per SM prefetches item i+1 while computing item i;
+// STAGES = 1: two CTAs per SM overlap each other's loads and epilogues.
+template <typename R, int STAGES>
 __global__ void __launch_bounds__(NT) k_block_apply(ApplyArgs p)
 {
     constexpr int LD = Lay<R>::LD, EPC = 16 / sizeof(R), CPC = TW / EPC;
@@ -144,15 +147,23 @@ __global__ void __launch_bounds__(NT) k_block_apply(ApplyArgs p)
     const int mb = p.S.nb >> 1;
     const int2 *bsr = p.S.bsched + p.Rb * mb;
     int item = blockIdx.x;
-    if (item < total) issue_item<R>(p, item, buf, buf + TW * LD, buf + 2 * TW * LD);
-    cp_commit();
-    for (int it = 0; item < total; ++it, item += gridDim.x) {
-        const int s = it & 1;
-        const int next = item + gridDim.x;
-        R *nb = buf + (size_t)(3 * (s ^ 1)) * TW * LD;
-        if (next < total) issue_item<R>(p, next, nb, nb + TW * LD, nb + 2 * TW * LD);
+    if (STAGES == 2) {
+        if (item < total) issue_item<R>(p, item, buf, buf + TW * LD, buf + 2 * TW * LD);
         cp_commit();
-        cp_wait1();
+    }
+    for (int it = 0; item < total; ++it, item += gridDim.x) {
+        const int s = STAGES == 2 ? (it & 1) : 0;
+        if (STAGES == 2) {
+            const int next = item + gridDim.x;
+            R *nb = buf + (size_t)(3 * (s ^ 1)) * TW * LD;
+            if (next < total) issue_item<R>(p, next, nb, nb + TW * LD, nb + 2 * TW * LD);
+            cp_commit();
+            cp_wait1();
+        } else {
+            issue_item<R>(p, item, buf, buf + TW * LD, buf + 2 * TW * LD);
+            cp_commit();
+            cp_wait0();
+        }
         __syncthreads();
         R *x = buf + (size_t)(3 * s) * TW * LD, *ua = x + TW * LD, *uc = x + 2 * TW * LD;
         if (item < p.ntT) {
@@ -238,25 +249,41 @@ static int sm_count()
     return n;
 }
 
-template <typename R>
-static void launch_apply(const ApplyArgs &p, cudaStream_t st)
+static int apply_stages()
+{
+    static int s = 0;
+    if (!s) {
+        const char *e = getenv("MPJ_APPLY_STAGES");
+        s = (e && atoi(e) == 2) ? 2 : 1;
+    }
+    return s;
+}
+
+template <typename R, int STAGES>
+static void launch_apply_s(const ApplyArgs &p, cudaStream_t st)
 {
     constexpr int LD = Lay<R>::LD;
-    const size_t smem = 6 * TW * LD * sizeof(R);
+    const size_t smem = 3 * STAGES * TW * LD * sizeof(R);
     static bool attr = false;
-    if (!attr) {
-        MPJ_CK_VOID(cudaFuncSetAttribute(k_block_apply<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        attr = true;
-    }
     static int per_sm = 0;
-    if (!per_sm) {
-        MPJ_CK_VOID(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_block_apply<R>, NT, smem));
+    if (!attr) {
+        MPJ_CK_VOID(cudaFuncSetAttribute(k_block_apply<R, STAGES>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)smem));
+        MPJ_CK_VOID(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_block_apply<R, STAGES>, NT, smem));
         per_sm = std::max(1, per_sm);
+        attr = true;
     }
     const int total = p.ntT + p.ntV;
     const int grid = std::max(1, std::min(total, sm_count() * per_sm));
-    k_block_apply<R><<<grid, NT, smem, st>>>(p);
+    k_block_apply<R, STAGES><<<grid, NT, smem, st>>>(p);
     count_launch();
+}
+
+template <typename R>
+static void launch_apply(const ApplyArgs &p, cudaStream_t st)
+{
+    if (apply_stages() == 2) launch_apply_s<R, 2>(p, st);
+    else launch_apply_s<R, 1>(p, st);
 }
 
 template <typename R>

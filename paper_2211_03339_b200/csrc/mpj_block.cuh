@@ -246,11 +246,14 @@ __device__ __forceinline__ void tile_op(const float *A, const float *B, AccOP &a
     for (int u = 0; u < 4; ++u)
         #pragma unroll
         for (int w = 0; w < 4; ++w) acc.v[u][w] = 0.f;
+    float4 a = *(const float4 *)(A + ra), b = *(const float4 *)(B + cb);
     #pragma unroll 8
     for (int k = 0; k < TW; ++k) {
-        const float4 a = *(const float4 *)(A + ra + k * LD);
-        const float4 b = *(const float4 *)(B + cb + k * LD);
         const float av[4] = {a.x, a.y, a.z, a.w}, bv[4] = {b.x, b.y, b.z, b.w};
+        if (k + 1 < TW) {                         // register prefetch of the next k
+            a = *(const float4 *)(A + ra + (k + 1) * LD);
+            b = *(const float4 *)(B + cb + (k + 1) * LD);
+        }
         #pragma unroll
         for (int u = 0; u < 4; ++u)
             #pragma unroll
