@@ -50,6 +50,7 @@ def parse():
     ap.add_argument("--workload", default="evd", choices=["evd", "batched", "svd"],
                     help="evd: BASELINE config 4 (the bench line); batched: config 3 (4096 x n=64)")
     ap.add_argument("--batch", type=int, default=4096)
+    ap.add_argument("--eps-low", type=float, default=10.0, help="low stage eps = f * upsilon (reading R12)")
     return ap.parse_args()
 
 
@@ -330,7 +331,7 @@ def main():
     seed = 2211033390 + 4000 + 100 * args.mode + 10 * int(round(np.log10(args.kappa))) + rank
     A, lam_true = W.example1_torch(n, args.kappa, args.mode, seed, device=dev)
     Acm = A.T  # symmetric: the row-major tensor's transpose view is its column-major image
-    cfg = mpj.default_config("eig", variant=args.variant)
+    cfg = mpj.default_config("eig", variant=args.variant, eps_low_factor=args.eps_low)
     wsbuf = mpj.eig_workspace(n, cfg, device=dev)
     lam = torch.empty(n, dtype=torch.float64, device=dev)
     V = mpj.empty_colmajor(n, n, device="cuda")
@@ -453,6 +454,7 @@ def main():
             "sweeps": rep.sweeps, "sweeps_low": rep.sweeps_low,
             "off_hist_rel": [h / rep.norm_a for h in list(rep.off_hist)[: rep.sweeps + 1]],
             "off0_rel": rep.off0 / rep.norm_a,
+            "off_hist_low_rel": [h / rep.norm_a for h in list(rep.off_hist_low)[: rep.sweeps_low + 1]],
             "ju": rep.rotations / (n * (n - 1) / 2), "ju_low": rep.rotations_low / (n * (n - 1) / 2),
             "stage_seconds": {"low_fp32": rep.t_low, "orth": rep.t_orth, "precond": rep.t_precond,
                               "jacobi_fp64": rep.t_jacobi, "extract": rep.t_extract},

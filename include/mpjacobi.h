@@ -96,6 +96,7 @@ typedef struct mpj_report {
     int block_b;              /* ordering block size used                                 */
     int variant;              /* MPJ_VARIANT_SCALAR or MPJ_VARIANT_BLOCK                  */
     long long launches;       /* kernels launched by the call                             */
+    double off_hist_low[64];  /* ||off(T32)||_F before fp32 sweep k (first 64)            */
 } mpj_report;
 
 /* ------------------------------------------------------------------------

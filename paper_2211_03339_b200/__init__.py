@@ -53,12 +53,13 @@ class mpj_report(C.Structure):
         ("off0", C.c_double), ("off_hist", C.c_double * 64), ("t_low", C.c_double),
         ("t_orth", C.c_double), ("t_precond", C.c_double), ("t_jacobi", C.c_double),
         ("t_extract", C.c_double), ("t_total", C.c_double), ("n_padded", C.c_int), ("block_b", C.c_int),
-        ("variant", C.c_int), ("launches", C.c_longlong),
+        ("variant", C.c_int), ("launches", C.c_longlong), ("off_hist_low", C.c_double * 64),
     ]
 
     def as_dict(self):
-        d = {k: getattr(self, k) for k, _ in self._fields_ if k != "off_hist"}
+        d = {k: getattr(self, k) for k, _ in self._fields_ if k not in ("off_hist", "off_hist_low")}
         d["off_hist"] = list(self.off_hist[: max(self.sweeps + 1, 1)])
+        d["off_hist_low"] = list(self.off_hist_low[: max(self.sweeps_low + 1, 1)])
         return d
 
 

@@ -516,6 +516,7 @@ static mpj_status eig_impl(bool mixed, const double *A, int64_t n, int64_t lda, 
         r.sweeps_low = jo.sweeps;
         r.rotations_low = jo.rotations;
         r.status_low = sl;
+        for (int k = 0; k < jo.nhist && k < 64; ++k) r.off_hist_low[k] = jo.hist[k];
         r.t_low = tl.stop();
 
         // a2: Q = orth(Z), Z = fp64(V32) (n x n real block)
