@@ -50,7 +50,8 @@ def parse():
     ap.add_argument("--workload", default="evd", choices=["evd", "batched", "svd"],
                     help="evd: BASELINE config 4 (the bench line); batched: config 3 (4096 x n=64)")
     ap.add_argument("--batch", type=int, default=4096)
-    ap.add_argument("--eps-low", type=float, default=10.0, help="low stage eps = f * upsilon (reading R12)")
+    ap.add_argument("--eps-low", type=float, default=0.0,
+                    help="low stage eps = f * upsilon; 0 = the rule of reading R12")
     return ap.parse_args()
 
 

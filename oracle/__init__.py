@@ -159,12 +159,13 @@ def _p(a):
 
 def default_cfg(kind: str = "eig", b: int = 32, **kw) -> Cfg:
     """The paper's settings: eps = 0.1 omega; nu = 20 omega (EVD) or
-    omega (SVD, with the 2e-4 early stop).  Low stage: eps_low = 10 upsilon,
-    nu_low = 20 upsilon (EVD) / upsilon (SVD) -- reading R12."""
+    omega (SVD, with the 2e-4 early stop).  Low stage (reading R12): eps_low =
+    max(10, 1.25 sqrt(n)) upsilon (eps_low_factor = 0 selects the rule), nu_low
+    = 20 upsilon (EVD) / upsilon (SVD)."""
     c = Cfg()
     c.eps_factor = 0.1
     c.nu_factor = 20.0 if kind == "eig" else 1.0
-    c.eps_low_factor = 10.0
+    c.eps_low_factor = 0.0
     c.nu_low_factor = 20.0 if kind == "eig" else 1.0
     c.early_stop = 0.0 if kind == "eig" else 2e-4
     c.max_sweeps = 60

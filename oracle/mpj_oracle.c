@@ -480,7 +480,7 @@ void orc_sort_desc(const double *key, int n, int *perm)
 typedef struct {
     double eps_factor;      /* eps = eps_factor * omega (0.1)              */
     double nu_factor;       /* nu = nu_factor * omega (20 eig, 1 svd)      */
-    double eps_low_factor;  /* low stage eps = eps_low_factor * upsilon (R12: 10)  */
+    double eps_low_factor;  /* low stage eps = f * upsilon; <= 0: R12's rule       */
     double nu_low_factor;   /* low stage nu = nu_low_factor * upsilon (R12: 20/1)  */
     double early_stop;      /* svd: stop when sweep rotations / N < this (2e-4)    */
     int max_sweeps;         /* R13: 60                                             */
@@ -498,6 +498,16 @@ typedef struct {
 
 #define OMEGA 1.1102230246251565e-16     /* 2^-53 */
 #define UPSILON 5.9604644775390625e-08   /* 2^-24 */
+
+/* Low-stage stop tolerance factor (reading R12): the fp32 stage's attainable
+ * ||off(T32)||/||A||_F grows like sqrt(n) upsilon, so eps_low = max(10,
+ * 1.25 sqrt(n)) upsilon (= 10 upsilon at n = 64) unless eps_low_factor > 0. */
+static double orc_eps_low(const orc_cfg *cfg, int n)
+{
+    if (cfg->eps_low_factor > 0) return cfg->eps_low_factor;
+    double f = 1.25 * sqrt((double)n);
+    return f > 10.0 ? f : 10.0;
+}
 
 /* Extract (Alg. 3 output): lambda = diag(T) sorted descending       */
 /* (stable), columns of V permuted alike.                                   */
@@ -527,7 +537,7 @@ int orc_low_evd(const double *A, int n, const orc_cfg *cfg, float *Z, orc_report
     for (int i = 0; i < n; ++i) Z[IDX(i, i, n)] = 1.0f;
     double nA32 = orc_fro_f32(T32, n, n, n);
     int sw = 0; long long rot = 0;
-    int st = orc_jacobi_evd_f32(T32, Z, n, cfg->b, cfg->eps_low_factor * UPSILON * nA32,
+    int st = orc_jacobi_evd_f32(T32, Z, n, cfg->b, orc_eps_low(cfg, n) * UPSILON * nA32,
                                 cfg->nu_low_factor * UPSILON, cfg->rule, cfg->max_sweeps_low,
                                 -1, &sw, &rot, NULL);
     if (rep) { rep->sweeps_low = sw; rep->rotations_low = rot; rep->status_low = st; }
@@ -733,7 +743,7 @@ int orc_mp_svd(const double *A, int m, int n, const orc_cfg *cfg, const float *Z
         memset(Z, 0, sizeof(float) * nn);
         for (int i = 0; i < n; ++i) Z[IDX(i, i, n)] = 1.0f;
         int sw = 0; long long rot = 0;
-        r0.status_low = orc_jacobi_svd_f32(C32, Z, m, n, cfg->b, cfg->eps_low_factor * UPSILON,
+        r0.status_low = orc_jacobi_svd_f32(C32, Z, m, n, cfg->b, orc_eps_low(cfg, n) * UPSILON,
                                            cfg->nu_low_factor * UPSILON, cfg->early_stop,
                                            cfg->max_sweeps_low, &sw, &rot, NULL);
         r0.sweeps_low = sw; r0.rotations_low = rot;

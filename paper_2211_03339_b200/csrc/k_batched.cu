@@ -233,7 +233,7 @@ mpj_status batched_evd(const double *A, int64_t n, int64_t batch, double *Lambda
     a.flag = flag; a.lsched = lsched;
     const double omega = 1.1102230246251565e-16, upsilon = 5.9604644775390625e-08;
     a.eps = cfg.eps_factor * omega; a.nu = cfg.nu_factor * omega;
-    a.eps_low = cfg.eps_low_factor * upsilon; a.nu_low = cfg.nu_low_factor * upsilon;
+    a.eps_low = eps_low_factor(cfg, n) * upsilon; a.nu_low = cfg.nu_low_factor * upsilon;
     a.max_sweeps = cfg.max_sweeps; a.max_sweeps_low = cfg.max_sweeps_low; a.rule = cfg.stop_rule;
     const int smem = 3 * TW * Lay<double>::LD * sizeof(double);
     MPJ_CK(cudaFuncSetAttribute(k_batched_evd, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));

@@ -347,7 +347,7 @@ mpj_status svd_run(const double *A, int64_t m, int64_t n, int64_t lda, double *S
         MPJ_CK(cudaMemsetAsync(p.V32, 0, (size_t)np * np * 4, st));
         launch_identity<float>(p.V32, np, (int)n, (int)n, st);
         SvdStage lo;
-        mpj_status sl = svd_loop<float>(p, p.C32, p.V32, p.C, ds, cfg.eps_low_factor * upsilon,
+        mpj_status sl = svd_loop<float>(p, p.C32, p.V32, p.C, ds, eps_low_factor(cfg, n) * upsilon,
                                         (float)(cfg.nu_low_factor * upsilon), cfg.early_stop_ratio,
                                         cfg.max_sweeps_low, h_pin, st, lo);
         if (sl != MPJ_OK && sl != MPJ_ERR_NOCONV) return fin(sl);

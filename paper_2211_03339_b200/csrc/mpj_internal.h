@@ -40,6 +40,9 @@ void prof_flush();   // after the stream has been synchronised
         if (s_ != MPJ_OK) return s_;                                                    \
     } while (0)
 
+// low-stage stop tolerance factor (reading R12)
+double eps_low_factor(const mpj_config &cfg, int64_t n);
+
 // ---- ordering (host side) --------------------------------------------------
 struct HostSchedule {
     int n = 0, b = 1, np = 0, nb = 0, mb = 0, rounds = 0;

@@ -422,6 +422,13 @@ static mpj_status read_scalar(Ctx &cx, const double *d, double &out)
     return MPJ_OK;
 }
 
+// Low-stage stop tolerance factor (reading R12): max(10, 1.25 sqrt(n)) unless set.
+double eps_low_factor(const mpj_config &cfg, int64_t n)
+{
+    if (cfg.eps_low_factor > 0) return cfg.eps_low_factor;
+    return std::max(10.0, 1.25 * std::sqrt((double)n));
+}
+
 static const double kOmega = 1.1102230246251565e-16;    // 2^-53
 static const double kUpsilon = 5.9604644775390625e-08;  // 2^-24
 
@@ -509,7 +516,7 @@ static mpj_status eig_impl(bool mixed, const double *A, int64_t n, int64_t lda, 
         MPJ_TRY(read_scalar(cx, p.red_out, nA32));
         JacobiOut jo;
         mpj_status sl = jacobi_run<float>(cx, p.T32, p.V32, (int)n, p.b, p.variant,
-                                          cfg.eps_low_factor * kUpsilon * nA32,
+                                          eps_low_factor(cfg, n) * kUpsilon * nA32,
                                           (float)(cfg.nu_low_factor * kUpsilon), cfg.stop_rule,
                                           cfg.max_sweeps_low, -1, p.j32, jo);
         if (sl != MPJ_OK && sl != MPJ_ERR_NOCONV) return finish(sl);
@@ -637,7 +644,7 @@ void mpj_config_default_eig(mpj_config *c)
     if (!c) return;
     c->eps_factor = 0.1;
     c->nu_factor = 20.0;
-    c->eps_low_factor = 10.0;
+    c->eps_low_factor = 0.0;   /* reading R12: max(10, 1.25 sqrt(n)) */
     c->nu_low_factor = 20.0;
     c->early_stop_ratio = 0.0;
     c->max_sweeps = 60;
