@@ -395,9 +395,15 @@ def main():
             fl = flops_apply
             by = bytes_apply * (1 if is64 else 0.5)
             peak = pk["dmma_tflops"] if is64 else pk["ffma_tflops"]
+            traffic = None
+            tp = os.path.join(ROOT, "profiles", "r01_traffic.json")
+            if os.path.exists(tp):
+                t = json.load(open(tp)).get(dom)
+                if t and t.get("n_padded") == rep.n_padded:
+                    traffic = t["dram_bytes_per_launch"]
             roof = {"kernel": dom, "bound": "tensor" if is64 else "alu",
                     "achieved": fl / avg / 1e12, "peak": peak, "unit": "TFLOP/s",
-                    "frac": fl / avg / 1e12 / peak, "traffic": None,
+                    "frac": fl / avg / 1e12 / peak, "traffic": traffic,
                     "algorithmic_flop_per_launch": fl, "algorithmic_bytes_per_launch": by,
                     "hbm_frac": by / avg / 1e9 / pk["hbm_gbs"],
                     "share_of_step": kernels[dom]["seconds_per_step"] / (ms * 1e-3),

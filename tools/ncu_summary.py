@@ -18,14 +18,23 @@ def short(name):
     return base
 
 
-def main(path, out=None):
+def main(path, out=None, window=None):
+    """window = (first_kernel_substring, last_kernel_substring): restrict to the
+    launches from the first match of the former to the last match of the latter
+    that precedes the next match of the former (one complete step)."""
     tot = defaultdict(float)
     cnt = defaultdict(int)
     with open(path) as f:
         lines = [ln for ln in f if ln.startswith('"')]
-    for row in csv.DictReader(lines):
-        if row.get("Metric Name") != "gpu__time_duration.sum":
-            continue
+    rows = [r for r in csv.DictReader(lines) if r.get("Metric Name") == "gpu__time_duration.sum"]
+    note = ""
+    if window:
+        first, last = window
+        i0 = next(i for i, r in enumerate(rows) if first in r["Kernel Name"])
+        ilast = max(i for i, r in enumerate(rows) if last in r["Kernel Name"])
+        rows = rows[i0: ilast + 1]
+        note = f" (window: first '{first}' .. last '{last}')"
+    for row in rows:
         k = short(row["Kernel Name"])
         v = float(row["Metric Value"].replace(",", ""))
         unit = row.get("Metric Unit", "ns")
@@ -34,7 +43,7 @@ def main(path, out=None):
         cnt[k] += 1
     all_t = sum(tot.values())
     rows = sorted(tot, key=lambda k: -tot[k])
-    lines = [f"# {path}: {sum(cnt.values())} launches, {all_t*1e3:.2f} ms total device time (cold-cache, serialised)",
+    lines = [f"# {path}{note}: {sum(cnt.values())} launches, {all_t*1e3:.2f} ms total device time (cold-cache, serialised)",
              f"{'kernel':40s} {'launches':>9s} {'total_ms':>11s} {'avg_us':>9s} {'share':>7s}"]
     for k in rows:
         lines.append(f"{k:40s} {cnt[k]:9d} {tot[k]*1e3:11.3f} {tot[k]/cnt[k]*1e6:9.2f} {tot[k]/all_t*100:6.2f}%")
@@ -45,4 +54,5 @@ def main(path, out=None):
 
 
 if __name__ == "__main__":
-    main(sys.argv[1], sys.argv[2] if len(sys.argv) > 2 else None)
+    win = tuple(sys.argv[3].split("..")) if len(sys.argv) > 3 else None
+    main(sys.argv[1], sys.argv[2] if len(sys.argv) > 2 else None, win)
