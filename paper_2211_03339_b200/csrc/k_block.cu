@@ -33,28 +33,29 @@ using namespace blk;
 // K3: inner solver.  One CTA per block pair.
 // ---------------------------------------------------------------------------
 template <typename R>
-__global__ void __launch_bounds__(NT) k_block_solve(R *__restrict__ T, int64_t ldt, Sched S, int Rb, R nu,
-                                                    int rule, R *__restrict__ Ubuf,
-                                                    unsigned long long *__restrict__ cnt)
+__global__ void __launch_bounds__(NTW) k_block_solve(R *__restrict__ T, int64_t ldt, Sched S, int Rb, R nu,
+                                                     int rule, R *__restrict__ Ubuf,
+                                                     unsigned long long *__restrict__ cnt)
 {
     constexpr int LD = Lay<R>::LD;
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    R *D = (R *)smem_raw;          // 64 x LD, column-major
-    R *U = D + TW * LD;            // 64 x LD
-    __shared__ InnerShared sh;
-    __shared__ InnerParams<R> pr;
+    R *D0 = (R *)smem_raw;          // 64 x LD, column-major (double-buffered)
+    R *D1 = D0 + TW * LD;
+    R *U = D1 + TW * LD;            // 64 x LD
+    __shared__ unsigned nrot;
     const int k = blockIdx.x;
     const int mb = S.nb >> 1;
     const int2 bp = S.bsched[Rb * mb + k];
-    for (int e = threadIdx.x; e < TW * TW; e += NT) {
+    for (int e = threadIdx.x; e < TW * TW; e += NTW) {
         const int li = e & (TW - 1), lj = e >> 6;
-        D[li + lj * LD] = T[gidx(bp, li) + (int64_t)gidx(bp, lj) * ldt];
+        D0[li + lj * LD] = T[gidx(bp, li) + (int64_t)gidx(bp, lj) * ldt];
         U[li + lj * LD] = (li == lj) ? R(1) : R(0);
     }
-    const unsigned nrot = inner_rounds<R>(D, U, bp, Rb == 0, S.lsched, nu, rule, sh, pr);
+    __syncthreads();
+    const R *D = inner_rounds_wide<R>(D0, D1, U, bp, Rb == 0, S.lsched, nu, rule, &nrot);
     R *Uk = Ubuf + (size_t)k * TW * TW;
-    R *UkT = Ubuf + (size_t)(S.nb >> 1) * TW * TW + (size_t)k * TW * TW;   // U^T (fp32 apply operand)
-    for (int e = threadIdx.x; e < TW * TW; e += NT) {
+    R *UkT = Ubuf + (size_t)mb * TW * TW + (size_t)k * TW * TW;   // U^T (fp32 apply operand)
+    for (int e = threadIdx.x; e < TW * TW; e += NTW) {
         const int li = e & (TW - 1), lj = e >> 6;
         T[gidx(bp, li) + (int64_t)gidx(bp, lj) * ldt] = D[li + lj * LD];
         Uk[li + lj * TW] = U[li + lj * LD];
@@ -296,7 +297,7 @@ mpj_status block_sweep(R *T, int64_t ldt, R *V, int64_t ldv, int vrows, const De
     S.bsched = ds.bsched; S.lsched = ds.lsched; S.b = ds.b; S.nb = ds.nb; S.np = ds.np;
     const int mb = ds.nb / 2;
     R *Ubuf = (R *)scratch;
-    const size_t sm_solve = 2 * TW * LD * sizeof(R);
+    const size_t sm_solve = 3 * TW * LD * sizeof(R);
     static bool attr_done[2] = {false, false};
     const int ti = sizeof(R) == 8 ? 0 : 1;
     if (!attr_done[ti]) {
@@ -312,7 +313,7 @@ mpj_status block_sweep(R *T, int64_t ldt, R *V, int64_t ldv, int vrows, const De
     const bool prof = prof_on();
     for (int Rb = 0; Rb < ds.nb - 1; ++Rb) {
         if (prof) prof_mark(nsolve, st, true);
-        k_block_solve<R><<<mb, NT, sm_solve, st>>>(T, ldt, S, Rb, nu, rule, Ubuf, cnt);
+        k_block_solve<R><<<mb, NTW, sm_solve, st>>>(T, ldt, S, Rb, nu, rule, Ubuf, cnt);
         count_launch();
         if (prof) { prof_mark(nsolve, st, false); prof_mark(napply, st, true); }
         ap.Rb = Rb;

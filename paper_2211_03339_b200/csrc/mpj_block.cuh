@@ -114,6 +114,85 @@ __device__ __forceinline__ unsigned inner_rounds(R *D, R *U, int2 bp, bool intra
 }
 
 // ---------------------------------------------------------------------------
+// Wide variant of inner_rounds for 1024 threads (32 warps): warp w owns pair
+// l = w, lane k owns pair k.  Every warp computes all 32 rotation parameters
+// (lane k -> pair k) and broadcasts pair w's by shuffle, so no shared
+// parameter table and no barrier between the parameter and update phases;
+// D is double-buffered (read Dc, write Dn: every entry of the 64 x 64 block is
+// rewritten each round), U is updated in place, one barrier per round.
+// Per element the arithmetic is exactly inner_rounds' (same results).
+// Returns the buffer holding the final D; *nrot (thread 0) = rotations.
+// ---------------------------------------------------------------------------
+constexpr int NTW = 1024;
+
+template <typename R>
+__device__ __forceinline__ R *inner_rounds_wide(R *D0, R *D1, R *U, int2 bp, bool intra,
+                                                const int2 *__restrict__ lsched, R nu, int rule, unsigned *nrot)
+{
+    constexpr int LD = Lay<R>::LD;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    R *Dc = D0, *Dn = D1;
+    unsigned cnt = 0;
+    const int nrounds = intra ? (BW - 1) + BW : BW;
+    for (int s = 0; s < nrounds; ++s) {
+        // pair `lane` of this round (every warp computes the same table)
+        int a, c;
+        if (intra && s < BW - 1) {
+            const int hb = BW / 2;
+            const int2 lp = lsched[s * hb + (lane < hb ? lane : lane - hb)];
+            const int off = (lane < hb) ? 0 : BW;
+            a = off + lp.x; c = off + lp.y;
+        } else {
+            const int sc = intra ? s - (BW - 1) : s;
+            a = lane;
+            int j = lane + sc; if (j >= BW) j -= BW;
+            c = BW + j;
+        }
+        const int ga = gidx(bp, a), gc = gidx(bp, c);
+        const int pk = ga < gc ? a : c, qk = ga < gc ? c : a, gpk = ga < gc ? ga : gc;
+        R t, sk, uk;
+        const int did = rot_params<R>(Dc[pk + pk * LD], Dc[qk + qk * LD], Dc[pk + qk * LD], nu, rule, t, sk, uk);
+        if (w == 0) cnt += __popc(__ballot_sync(0xffffffffu, did));
+        // pair l = w, broadcast from lane w
+        const int pl = __shfl_sync(0xffffffffu, pk, w), ql = __shfl_sync(0xffffffffu, qk, w);
+        const int gpl = __shfl_sync(0xffffffffu, gpk, w);
+        const R sl = __shfl_sync(0xffffffffu, sk, w), ul = __shfl_sync(0xffffffffu, uk, w);
+        // tile (k = lane, l = w)
+        if (lane == w) {
+            const R apq = Dc[pk + qk * LD];
+            Dn[pk + pk * LD] = fmaR(-t, apq, Dc[pk + pk * LD]);
+            Dn[qk + qk * LD] = fmaR(t, apq, Dc[qk + qk * LD]);
+            Dn[pk + qk * LD] = R(0);
+            Dn[qk + pk * LD] = R(0);
+        } else {
+            R x11 = Dc[pk + pl * LD], x21 = Dc[qk + pl * LD], x12 = Dc[pk + ql * LD], x22 = Dc[qk + ql * LD];
+            if (gpk < gpl) {
+                rot<R>(sk, uk, x11, x21); rot<R>(sk, uk, x12, x22);
+                rot<R>(sl, ul, x11, x12); rot<R>(sl, ul, x21, x22);
+            } else {
+                rot<R>(sl, ul, x11, x12); rot<R>(sl, ul, x21, x22);
+                rot<R>(sk, uk, x11, x21); rot<R>(sk, uk, x12, x22);
+            }
+            Dn[pk + pl * LD] = x11; Dn[qk + pl * LD] = x21; Dn[pk + ql * LD] = x12; Dn[qk + ql * LD] = x22;
+        }
+        // U <- U J for pair l = w: rows lane, lane + 32
+        if (U && sl != R(0)) {
+            #pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const int r = lane + 32 * h;
+                R x = U[r + pl * LD], y = U[r + ql * LD];
+                rot<R>(sl, ul, x, y);
+                U[r + pl * LD] = x; U[r + ql * LD] = y;
+            }
+        }
+        __syncthreads();
+        R *tmp = Dc; Dc = Dn; Dn = tmp;
+    }
+    if (threadIdx.x == 0) *nrot = cnt;
+    return Dc;
+}
+
+// ---------------------------------------------------------------------------
 // 64 x 64 x 64 tile products in shared memory.
 //   C = op(A) * B  with A, B column-major (leading dimension Lay<R>::LD);
 //   TRANS_A: op(A) = A^T.  Results stay in registers (Acc<R>).
