@@ -43,6 +43,7 @@ __global__ void __launch_bounds__(NTW) k_block_solve(R *__restrict__ T, int64_t 
     R *D1 = D0 + TW * LD;
     R *U = D1 + TW * LD;            // 64 x LD
     __shared__ unsigned nrot;
+    __shared__ WideParams<R> P;
     const int k = blockIdx.x;
     const int mb = S.nb >> 1;
     const int2 bp = S.bsched[Rb * mb + k];
@@ -52,7 +53,7 @@ __global__ void __launch_bounds__(NTW) k_block_solve(R *__restrict__ T, int64_t 
         U[li + lj * LD] = (li == lj) ? R(1) : R(0);
     }
     __syncthreads();
-    const R *D = inner_rounds_wide<R>(D0, D1, U, bp, Rb == 0, S.lsched, nu, rule, &nrot);
+    const R *D = inner_rounds_wide<R>(D0, D1, U, bp, Rb == 0, S.lsched, nu, rule, P, &nrot);
     R *Uk = Ubuf + (size_t)k * TW * TW;
     R *UkT = Ubuf + (size_t)mb * TW * TW + (size_t)k * TW * TW;   // U^T (fp32 apply operand)
     for (int e = threadIdx.x; e < TW * TW; e += NTW) {

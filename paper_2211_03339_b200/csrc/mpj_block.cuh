@@ -114,59 +114,66 @@ __device__ __forceinline__ unsigned inner_rounds(R *D, R *U, int2 bp, bool intra
 }
 
 // ---------------------------------------------------------------------------
-// Wide variant of inner_rounds for 1024 threads (32 warps): warp w owns pair
-// l = w, lane k owns pair k.  Every warp computes all 32 rotation parameters
-// (lane k -> pair k) and broadcasts pair w's by shuffle, so no shared
-// parameter table and no barrier between the parameter and update phases;
-// D is double-buffered (read Dc, write Dn: every entry of the 64 x 64 block is
-// rewritten each round), U is updated in place, one barrier per round.
-// Per element the arithmetic is exactly inner_rounds' (same results).
-// Returns the buffer holding the final D; *nrot (thread 0) = rotations.
+// Wide variant of inner_rounds (NTW = 512 threads) for the block variant's K3.
+// Per round: warp 0 computes the 32 rotation parameters into a shared table;
+// then 528 threads each own one tile -- the 496 off-diagonal tiles (k < l) are
+// computed once in the canonical order (reading R7) and written together with
+// their mirror, the 32 diagonal tiles use the t_pp - t a_pq form -- while all
+// 512 threads apply 4 (row, pair) updates of U.  D is double-buffered (every
+// entry is rewritten each round), so a round needs two barriers.  The per
+// element arithmetic is exactly inner_rounds' (same results).
 // ---------------------------------------------------------------------------
-constexpr int NTW = 1024;
+constexpr int NTW = 512;
+
+template <typename R>
+struct WideParams {
+    R t[BW], s[BW], u[BW];
+    int p[BW], q[BW], gp[BW];
+};
 
 template <typename R>
 __device__ __forceinline__ R *inner_rounds_wide(R *D0, R *D1, R *U, int2 bp, bool intra,
-                                                const int2 *__restrict__ lsched, R nu, int rule, unsigned *nrot)
+                                                const int2 *__restrict__ lsched, R nu, int rule,
+                                                WideParams<R> &P, unsigned *nrot)
 {
     constexpr int LD = Lay<R>::LD;
-    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int tid = threadIdx.x, lane = tid & 31;
     R *Dc = D0, *Dn = D1;
     unsigned cnt = 0;
     const int nrounds = intra ? (BW - 1) + BW : BW;
     for (int s = 0; s < nrounds; ++s) {
-        // pair `lane` of this round (every warp computes the same table)
-        int a, c;
-        if (intra && s < BW - 1) {
-            const int hb = BW / 2;
-            const int2 lp = lsched[s * hb + (lane < hb ? lane : lane - hb)];
-            const int off = (lane < hb) ? 0 : BW;
-            a = off + lp.x; c = off + lp.y;
-        } else {
-            const int sc = intra ? s - (BW - 1) : s;
-            a = lane;
-            int j = lane + sc; if (j >= BW) j -= BW;
-            c = BW + j;
+        if (tid < 32) {
+            int a, c;
+            if (intra && s < BW - 1) {
+                const int hb = BW / 2;
+                const int2 lp = lsched[s * hb + (lane < hb ? lane : lane - hb)];
+                const int off = (lane < hb) ? 0 : BW;
+                a = off + lp.x; c = off + lp.y;
+            } else {
+                const int sc = intra ? s - (BW - 1) : s;
+                a = lane;
+                int j = lane + sc; if (j >= BW) j -= BW;
+                c = BW + j;
+            }
+            const int ga = gidx(bp, a), gc = gidx(bp, c);
+            const int pk = ga < gc ? a : c, qk = ga < gc ? c : a;
+            R t, sk, uk;
+            const int did = rot_params<R>(Dc[pk + pk * LD], Dc[qk + qk * LD], Dc[pk + qk * LD], nu, rule, t, sk, uk);
+            cnt += __popc(__ballot_sync(0xffffffffu, did));
+            P.t[lane] = t; P.s[lane] = sk; P.u[lane] = uk;
+            P.p[lane] = pk; P.q[lane] = qk; P.gp[lane] = ga < gc ? ga : gc;
         }
-        const int ga = gidx(bp, a), gc = gidx(bp, c);
-        const int pk = ga < gc ? a : c, qk = ga < gc ? c : a, gpk = ga < gc ? ga : gc;
-        R t, sk, uk;
-        const int did = rot_params<R>(Dc[pk + pk * LD], Dc[qk + qk * LD], Dc[pk + qk * LD], nu, rule, t, sk, uk);
-        if (w == 0) cnt += __popc(__ballot_sync(0xffffffffu, did));
-        // pair l = w, broadcast from lane w
-        const int pl = __shfl_sync(0xffffffffu, pk, w), ql = __shfl_sync(0xffffffffu, qk, w);
-        const int gpl = __shfl_sync(0xffffffffu, gpk, w);
-        const R sl = __shfl_sync(0xffffffffu, sk, w), ul = __shfl_sync(0xffffffffu, uk, w);
-        // tile (k = lane, l = w)
-        if (lane == w) {
-            const R apq = Dc[pk + qk * LD];
-            Dn[pk + pk * LD] = fmaR(-t, apq, Dc[pk + pk * LD]);
-            Dn[qk + qk * LD] = fmaR(t, apq, Dc[qk + qk * LD]);
-            Dn[pk + qk * LD] = R(0);
-            Dn[qk + pk * LD] = R(0);
-        } else {
+        __syncthreads();
+        if (tid < BW * (BW - 1) / 2) {
+            // upper tile index -> (k, l), k < l
+            int l = (int)((1.0f + sqrtf(1.0f + 8.0f * tid)) * 0.5f);
+            while (l * (l - 1) / 2 > tid) --l;
+            while ((l + 1) * l / 2 <= tid) ++l;
+            const int k = tid - l * (l - 1) / 2;
+            const int pk = P.p[k], qk = P.q[k], pl = P.p[l], ql = P.q[l];
+            const R sk = P.s[k], uk = P.u[k], sl = P.s[l], ul = P.u[l];
             R x11 = Dc[pk + pl * LD], x21 = Dc[qk + pl * LD], x12 = Dc[pk + ql * LD], x22 = Dc[qk + ql * LD];
-            if (gpk < gpl) {
+            if (P.gp[k] < P.gp[l]) {
                 rot<R>(sk, uk, x11, x21); rot<R>(sk, uk, x12, x22);
                 rot<R>(sl, ul, x11, x12); rot<R>(sl, ul, x21, x22);
             } else {
@@ -174,21 +181,33 @@ __device__ __forceinline__ R *inner_rounds_wide(R *D0, R *D1, R *U, int2 bp, boo
                 rot<R>(sk, uk, x11, x21); rot<R>(sk, uk, x12, x22);
             }
             Dn[pk + pl * LD] = x11; Dn[qk + pl * LD] = x21; Dn[pk + ql * LD] = x12; Dn[qk + ql * LD] = x22;
+            Dn[pl + pk * LD] = x11; Dn[pl + qk * LD] = x21; Dn[ql + pk * LD] = x12; Dn[ql + qk * LD] = x22;
+        } else if (tid < BW * (BW - 1) / 2 + BW) {
+            const int k = tid - BW * (BW - 1) / 2;
+            const int pk = P.p[k], qk = P.q[k];
+            const R apq = Dc[pk + qk * LD], t = P.t[k];
+            Dn[pk + pk * LD] = fmaR(-t, apq, Dc[pk + pk * LD]);
+            Dn[qk + qk * LD] = fmaR(t, apq, Dc[qk + qk * LD]);
+            Dn[pk + qk * LD] = R(0);
+            Dn[qk + pk * LD] = R(0);
         }
-        // U <- U J for pair l = w: rows lane, lane + 32
-        if (U && sl != R(0)) {
+        if (U) {
             #pragma unroll
-            for (int h = 0; h < 2; ++h) {
-                const int r = lane + 32 * h;
-                R x = U[r + pl * LD], y = U[r + ql * LD];
-                rot<R>(sl, ul, x, y);
-                U[r + pl * LD] = x; U[r + ql * LD] = y;
+            for (int h = 0; h < (BW * TW) / NTW; ++h) {
+                const int e = tid + h * NTW, r = e & (TW - 1), k = e >> 6;
+                const R sk = P.s[k];
+                if (sk != R(0)) {
+                    const int pk = P.p[k], qk = P.q[k];
+                    R x = U[r + pk * LD], y = U[r + qk * LD];
+                    rot<R>(sk, P.u[k], x, y);
+                    U[r + pk * LD] = x; U[r + qk * LD] = y;
+                }
             }
         }
         __syncthreads();
         R *tmp = Dc; Dc = Dn; Dn = tmp;
     }
-    if (threadIdx.x == 0) *nrot = cnt;
+    if (tid == 0) *nrot = cnt;
     return Dc;
 }
 
