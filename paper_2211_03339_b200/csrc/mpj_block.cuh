@@ -116,9 +116,9 @@ __device__ __forceinline__ unsigned inner_rounds(R *D, R *U, int2 bp, bool intra
 // ---------------------------------------------------------------------------
 // Wide variant of inner_rounds (NTW = 512 threads) for the block variant's K3.
 // Per round: warp 0 computes the 32 rotation parameters into a shared table;
-// then 528 threads each own one tile -- the 496 off-diagonal tiles (k < l) are
-// computed once in the canonical order (reading R7) and written together with
-// their mirror, the 32 diagonal tiles use the t_pp - t a_pq form -- while all
+// then the 496 off-diagonal tiles (k < l) are computed once each in the
+// canonical order (reading R7) and written together with their mirror, the
+// remaining 16 threads take the 32 diagonal tiles (t_pp - t a_pq form), and all
 // 512 threads apply 4 (row, pair) updates of U.  D is double-buffered (every
 // entry is rewritten each round), so a round needs two barriers.  The per
 // element arithmetic is exactly inner_rounds' (same results).
@@ -182,14 +182,16 @@ __device__ __forceinline__ R *inner_rounds_wide(R *D0, R *D1, R *U, int2 bp, boo
             }
             Dn[pk + pl * LD] = x11; Dn[qk + pl * LD] = x21; Dn[pk + ql * LD] = x12; Dn[qk + ql * LD] = x22;
             Dn[pl + pk * LD] = x11; Dn[pl + qk * LD] = x21; Dn[ql + pk * LD] = x12; Dn[ql + qk * LD] = x22;
-        } else if (tid < BW * (BW - 1) / 2 + BW) {
-            const int k = tid - BW * (BW - 1) / 2;
-            const int pk = P.p[k], qk = P.q[k];
-            const R apq = Dc[pk + qk * LD], t = P.t[k];
-            Dn[pk + pk * LD] = fmaR(-t, apq, Dc[pk + pk * LD]);
-            Dn[qk + qk * LD] = fmaR(t, apq, Dc[qk + qk * LD]);
-            Dn[pk + qk * LD] = R(0);
-            Dn[qk + pk * LD] = R(0);
+        } else {
+            // the NTW - 496 remaining threads take the 32 diagonal tiles
+            for (int k = tid - BW * (BW - 1) / 2; k < BW; k += NTW - BW * (BW - 1) / 2) {
+                const int pk = P.p[k], qk = P.q[k];
+                const R apq = Dc[pk + qk * LD], t = P.t[k];
+                Dn[pk + pk * LD] = fmaR(-t, apq, Dc[pk + pk * LD]);
+                Dn[qk + qk * LD] = fmaR(t, apq, Dc[qk + qk * LD]);
+                Dn[pk + qk * LD] = R(0);
+                Dn[qk + pk * LD] = R(0);
+            }
         }
         if (U) {
             #pragma unroll
