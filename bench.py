@@ -301,6 +301,7 @@ def run_svd(args):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": False,
             "dtype": "f64", "data": "synthetic",
             "config": {"workload": f"Example 3 (P:1112) mode 3 kappa=1e3, {m} x {n} (BASELINE config 5a)"},
+            "step_ms": step_ms, "lib_t_total": [r.t_total for r in reports],
             "sweeps": rep.sweeps, "sweeps_low": rep.sweeps_low,
             "ju": rep.rotations / (n * (n - 1) / 2), "ju_low": rep.rotations_low / (n * (n - 1) / 2),
             "stage_seconds": {"low_fp32": rep.t_low, "orth": rep.t_orth, "precond": rep.t_precond,
@@ -349,15 +350,21 @@ def main():
     mpj.profile_enable(True)
     l0 = mpj.launch_count()
     reports = []
+    step_ms = []
     with ClockSampler(local) as clk:
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         torch.cuda.synchronize()
         e0.record()
         for _ in range(args.steps):
+            s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            s0.record()
             res = step()
+            s1.record()
             reports.append(res.report)
+            step_ms.append((s0, s1))
         e1.record()
         torch.cuda.synchronize()
+    step_ms = [a.elapsed_time(b) for a, b in step_ms]
     mpj.profile_enable(False)
     launches = mpj.launch_count() - l0
     ms = e0.elapsed_time(e1) / args.steps
@@ -458,6 +465,7 @@ def main():
                        "block_b": rep.block_b, "n_padded": rep.n_padded,
                        "l2": "inputs (512 MB A, 2.5 GB workspace) exceed the 126 MB L2",
                        "parallelism": "replicas" if ws > 1 else "single GPU"},
+            "step_ms": step_ms, "lib_t_total": [r.t_total for r in reports],
             "sweeps": rep.sweeps, "sweeps_low": rep.sweeps_low,
             "off_hist_rel": [h / rep.norm_a for h in list(rep.off_hist)[: rep.sweeps + 1]],
             "off0_rel": rep.off0 / rep.norm_a,
