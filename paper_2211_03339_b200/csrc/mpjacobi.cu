@@ -180,31 +180,44 @@ static int resolve_variant(int np, int b, const mpj_config *cfg)
 // ---------------------------------------------------------------------------
 // Per-call stream context: private stream joined to the caller's stream.
 // ---------------------------------------------------------------------------
+struct CtxCache {            // per-thread, created once: no per-call allocation or sync
+    cudaStream_t st = nullptr;
+    cudaEvent_t ev = nullptr;
+    double *h_pin = nullptr;
+    int dev = -1;
+};
+static thread_local CtxCache g_ctx;
+
 struct Ctx {
     cudaStream_t user = nullptr, st = nullptr;
     cudaEvent_t ev = nullptr;
     double *h_pin = nullptr;   // pinned host scalars
+    bool open_ = false;
     mpj_status open(void *stream)
     {
         user = (cudaStream_t)stream;
-        MPJ_CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
-        MPJ_CK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+        int dev = 0;
+        MPJ_CK(cudaGetDevice(&dev));
+        if (g_ctx.st == nullptr || g_ctx.dev != dev) {
+            MPJ_CK(cudaStreamCreateWithFlags(&g_ctx.st, cudaStreamNonBlocking));
+            MPJ_CK(cudaEventCreateWithFlags(&g_ctx.ev, cudaEventDisableTiming));
+            MPJ_CK(cudaMallocHost(&g_ctx.h_pin, 64 * sizeof(double)));
+            g_ctx.dev = dev;
+        }
+        st = g_ctx.st; ev = g_ctx.ev; h_pin = g_ctx.h_pin;
         MPJ_CK(cudaEventRecord(ev, user));
         MPJ_CK(cudaStreamWaitEvent(st, ev, 0));
-        MPJ_CK(cudaMallocHost(&h_pin, 64 * sizeof(double)));
+        open_ = true;
         return MPJ_OK;
     }
     mpj_status close()
     {
-        if (st) {
+        if (open_) {
             cudaEventRecord(ev, st);
             cudaStreamWaitEvent(user, ev, 0);
             cudaStreamSynchronize(st);
-            cudaStreamDestroy(st);
-            st = nullptr;
+            open_ = false;
         }
-        if (ev) { cudaEventDestroy(ev); ev = nullptr; }
-        if (h_pin) { cudaFreeHost(h_pin); h_pin = nullptr; }
         cudaError_t e = cudaGetLastError();
         if (e != cudaSuccess) {
             set_error(std::string("CUDA: ") + cudaGetErrorString(e));
