@@ -193,6 +193,30 @@ mpj_status mpjacobi_eig_batched(const double *A, int64_t n, int64_t batch, doubl
                                 double *V, int *sweeps, int *sweeps_low, void *stream,
                                 const mpj_config *cfg);
 
+/* ------------------------------------------------------------------------
+ * Multi-GPU Alg. 3, one process per GPU: the block-pair slots
+ * of the block merry-go-round (and the columns of T and V they own) are
+ * split over `nranks` ranks; per block round the 64 x 64 rotation blocks are
+ * all-gathered and the column blocks that cross rank boundaries exchanged
+ * over NCCL (NVLink); the off-norm is all-reduced per sweep.
+ *   A       in: the full n x n matrix on EVERY rank (host or device, lda >= n).
+ *   Lambda, V  out: replicated on every rank (host or device), as mpjacobi_eig.
+ *   nccl_id 128 bytes from mpjacobi_nccl_unique_id() on rank 0, broadcast to
+ *           all ranks (e.g. torch.distributed); NULL -> single process.
+ *   rank, nranks  this rank and the world size (nranks must divide n_p/64;
+ *           n is padded to a multiple of 64 * nranks).
+ *   emulate_ranks  with nccl_id == NULL: run that many ranks inside this
+ *           process on this GPU (device copies instead of NCCL) -- a testing
+ *           mode for the partitioned algorithm on one GPU.
+ * Every rank must call it with the same n, config and id.
+ * ---------------------------------------------------------------------- */
+mpj_status mpjacobi_eig_mg(const double *A, int64_t n, int64_t lda, double *Lambda, double *V, int64_t ldv,
+                           int *sweeps, const void *nccl_id, int rank, int nranks, int emulate_ranks,
+                           void *stream, const mpj_config *cfg, mpj_report *rep);
+
+/* ncclGetUniqueId into out (>= 128 bytes). */
+mpj_status mpjacobi_nccl_unique_id(void *out, size_t bytes);
+
 /* Kernel timing (diagnostics for the bench's roofline numbers).  While
  * enabled, the library brackets each launch of its dominant kernels with CUDA
  * events ON THE STREAM IT LAUNCHES THEM ON and accumulates their durations per

@@ -106,6 +106,11 @@ def lib():
             L.mpjacobi_svd.restype = C.c_int
             L.mpjacobi_svd.argtypes = [_vp, _i64, _i64, _i64, _vp, _vp, _i64, _vp, _i64,
                                        C.POINTER(C.c_int), _vp, C.c_size_t, _vp, cfgp, repp]
+        L.mpjacobi_eig_mg.restype = C.c_int
+        L.mpjacobi_eig_mg.argtypes = [_vp, _i64, _i64, _vp, _vp, _i64, C.POINTER(C.c_int), _vp, C.c_int, C.c_int,
+                                      C.c_int, _vp, cfgp, repp]
+        L.mpjacobi_nccl_unique_id.restype = C.c_int
+        L.mpjacobi_nccl_unique_id.argtypes = [_vp, C.c_size_t]
         if hasattr(L, "mpjacobi_eig_batched"):
             L.mpjacobi_eig_batched.restype = C.c_int
             L.mpjacobi_eig_batched.argtypes = [_vp, _i64, _i64, _vp, _vp, _vp, _vp, _vp, cfgp]
@@ -119,6 +124,7 @@ EXPORTED = (
     "mpjacobi_precond", "mpjacobi_dgemm", "mpjacobi_svd_workspace", "mpjacobi_svd",
     "mpjacobi_eig_batched", "mpjacobi_last_error", "mpjacobi_launch_count",
     "mpjacobi_profile_enable", "mpjacobi_profile_reset", "mpjacobi_profile_get",
+    "mpjacobi_eig_mg", "mpjacobi_nccl_unique_id",
 )
 
 
@@ -354,7 +360,39 @@ def mpjacobi_eig_batched(A, cfg: mpj_config | None = None, allow_noconv=False) -
     return BatchedResult(lam, V.transpose(1, 2), sw, swl, st)
 
 
+def nccl_unique_id() -> bytes:
+    """128-byte NCCL id (rank 0 creates it, then broadcasts it)."""
+    buf = C.create_string_buffer(128)
+    _check(lib().mpjacobi_nccl_unique_id(buf, 128))
+    return buf.raw
+
+
+def mpjacobi_eig_mg(A, cfg: mpj_config | None = None, *, nccl_id: bytes | None = None, rank: int = 0,
+                    nranks: int = 1, emulate_ranks: int = 1, out=None, allow_noconv=False) -> EigResult:
+    """Multi-GPU Alg. 3 (column-block partition).  With nccl_id (bytes from
+    nccl_unique_id() on rank 0, broadcast with torch.distributed), one call per
+    rank/GPU; without it, `emulate_ranks` ranks run inside this process on the
+    current GPU.  A (full, every rank) and the replicated outputs as in eig()."""
+    n = A.shape[0]
+    Acm = colmajor(A)
+    dev = Acm.device
+    if out is None:
+        lam = torch.empty(n, dtype=torch.float64, device=dev, pin_memory=(dev.type == "cpu"))
+        V = empty_colmajor(n, n, device=dev.type, pin=(dev.type == "cpu"))
+    else:
+        lam, V = out
+    cfg = cfg or default_config("eig")
+    rep = mpj_report()
+    sw = C.c_int(0)
+    idbuf = C.create_string_buffer(nccl_id, 128) if nccl_id is not None else None
+    st = lib().mpjacobi_eig_mg(_ptr(Acm), n, Acm.stride(1), _ptr(lam), _ptr(V), V.stride(1), C.byref(sw), idbuf,
+                               rank, nranks, emulate_ranks, _stream(), C.byref(cfg), C.byref(rep))
+    _check(st, (MPJ_OK, MPJ_ERR_NOCONV) if allow_noconv else (MPJ_OK,))
+    return EigResult(lam, V, sw.value, rep)
+
+
 # short aliases
+eig_mg = mpjacobi_eig_mg
 eig_batched = mpjacobi_eig_batched
 svd = mpjacobi_svd
 eig = mpjacobi_eig

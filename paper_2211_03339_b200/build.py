@@ -22,6 +22,18 @@ NVCC_FLAGS = [
 ]
 
 
+def nccl_lib_dir():
+    """The NCCL torch ships (libnccl.so.2, SONAME-shared with torch's copy)."""
+    try:
+        import nvidia.nccl
+        d = os.path.join(list(nvidia.nccl.__path__)[0], "lib")
+        if os.path.exists(os.path.join(d, "libnccl.so.2")):
+            return d
+    except Exception:
+        pass
+    return "/usr/lib/x86_64-linux-gnu"
+
+
 def sources():
     return sorted(glob.glob(os.path.join(CSRC, "*.cu")))
 
@@ -51,8 +63,9 @@ def build(force: bool = False, verbose: bool = False) -> str:
             raise RuntimeError(f"nvcc failed on {src}:\n{out.decode()}")
         if verbose and out:
             print(out.decode())
+    nd = nccl_lib_dir()
     subprocess.check_call([NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", OUT, *objs,
-                           "-lcudart"])
+                           "-lcudart", f"-L{nd}", "-l:libnccl.so.2", f"-Xlinker=-rpath,{nd}"])
     for o in objs:
         os.remove(o)
     return OUT

@@ -23,6 +23,11 @@
 
 namespace mpj {
 
+// multi-GPU (k_mg.cu)
+mpj_status mg_eig(bool mixed, const double *A, int64_t n, int64_t lda, double *Lambda, double *V, int64_t ldv,
+                  int *sweeps_out, const void *nccl_id, int rank, int nranks, int emulate, cudaStream_t user,
+                  const mpj_config &cfg, mpj_report &rep, double *h_pin);
+
 // SVD (k_svd.cu)
 size_t svd_workspace(int64_t m, int64_t n);
 mpj_status svd_run(const double *A, int64_t m, int64_t n, int64_t lda, double *Sigma, double *U, int64_t ldu,
@@ -780,6 +785,36 @@ mpj_status mpjacobi_dgemm(int transa, const double *A, const double *B, double *
 }  // extern "C"
 
 // ---------------------------------------------------------------------------
+// multi-GPU entry point (kernels in k_mg.cu)
+mpj_status mpjacobi_eig_mg(const double *A, int64_t n, int64_t lda, double *Lambda, double *V, int64_t ldv,
+                           int *sweeps, const void *nccl_id, int rank, int nranks, int emulate_ranks, void *stream,
+                           const mpj_config *cfg_in, mpj_report *rep)
+{
+    using namespace mpj;
+    set_error("");
+    const int G = nccl_id ? nranks : std::max(1, emulate_ranks);
+    if (n < 1 || lda < n || ldv < n || !A || !Lambda || !V || G < 1 || (nccl_id && (rank < 0 || rank >= nranks))) {
+        set_error("mpjacobi_eig_mg: invalid argument");
+        return MPJ_ERR_INVALID;
+    }
+    mpj_config cfg;
+    if (cfg_in) cfg = *cfg_in; else mpj_config_default_eig(&cfg);
+    if (cfg.block_b != 0 && cfg.block_b != 32) { set_error("mpjacobi_eig_mg: block_b must be 32"); return MPJ_ERR_INVALID; }
+    Ctx cx;
+    MPJ_TRY(cx.open(stream));
+    const long long l0 = mpjacobi_launch_count();
+    Timer t_all(cx.st);
+    mpj_report r;
+    std::memset(&r, 0, sizeof(r));
+    mpj_status s = mg_eig(true, A, n, lda, Lambda, V, ldv, sweeps, nccl_id, rank, nranks, emulate_ranks, cx.st, cfg,
+                          r, cx.h_pin);
+    r.t_total = t_all.stop();
+    r.launches = mpjacobi_launch_count() - l0;
+    if (rep) *rep = r;
+    mpj_status c = cx.close();
+    return s != MPJ_OK ? s : c;
+}
+
 // SVD entry points (kernels in k_svd.cu)
 // ---------------------------------------------------------------------------
 extern "C" {

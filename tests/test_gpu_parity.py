@@ -311,3 +311,23 @@ def test_svd_host_buffers_and_errors(mpj):
     assert np.array_equal(r_host.U.numpy(), host(r_dev.U))
     with pytest.raises(ValueError):
         mpj.svd(dev(A.T.copy()))   # m < n
+
+
+# ----------------------------------------------------------------- multi-GPU partition (emulated ranks)
+@pytest.mark.parametrize("n,mode", [(256, 4), (512, 3), (200, 5)])
+def test_eig_mg_emulated(mpj, orc, n, mode):
+    """the column-block partitioned Alg. 3 (slots split over G
+    ranks, U all-gather, boundary block exchange, off-norm all-reduce) run as
+    G ranks inside one process on one GPU.  vs the oracle (same b = 32
+    ordering): north_star tolerances and sweep counts (R20); and G-invariance:
+    G = 1, 2, 4 give the same eigenvalues to rounding."""
+    A, lam_true = W.example1(n, 1e3, mode, W.seed_for(4, mode, 1e3))
+    ref = orc.mp_evd(A, orc.default_cfg("eig", b=32))
+    lams = []
+    for G in (1, 2, 4):
+        res = mpj.eig_mg(dev(A), emulate_ranks=G)
+        _check_evd(A, host(res.lam), host(res.V), ref.lam, ref.report.sweeps, res.sweeps,
+                   list(res.report.off_hist), list(ref.report.off_hist))
+        lams.append(host(res.lam))
+    assert np.max(np.abs(lams[1] - lams[0])) <= 1e-14 * np.abs(lams[0]).max()
+    assert np.max(np.abs(lams[2] - lams[0])) <= 1e-14 * np.abs(lams[0]).max()
