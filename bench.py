@@ -11,9 +11,11 @@ extraction) of one n x n matrix through the C ABI.
 Prints ONE JSON line (rank 0).  --impl reference times the oracle (plain C,
 oracle/) on the host cores on a bounded sample of the same workload and
 extrapolates to seconds per EVD (the only other place the oracle runs).
-Multi-GPU (torchrun, N > 1): every rank runs its own replica of the workload
-("replicas only": the column-partitioned NCCL path is not built yet, see
-DESIGN.md); the device time is the max over ranks.
+Multi-GPU (torchrun, N > 1): strong scaling of the same n = 8192 EVD, the
+block-pair slots (and their columns of T and V) partitioned over the N ranks
+(mpjacobi_eig_mg: NCCL all-gather of the 64 x 64 rotation blocks and exchange
+of the boundary column blocks per block round); rank 0 draws A and broadcasts
+it; the device time is the max over ranks.
 """
 from __future__ import annotations
 
@@ -330,16 +332,29 @@ def main():
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     n = args.n
-    seed = 2211033390 + 4000 + 100 * args.mode + 10 * int(round(np.log10(args.kappa))) + rank
+    seed = 2211033390 + 4000 + 100 * args.mode + 10 * int(round(np.log10(args.kappa)))
     A, lam_true = W.example1_torch(n, args.kappa, args.mode, seed, device=dev)
+    if ws > 1:
+        # strong scaling of ONE EVD: every rank must hold the same bits of A
+        torch.distributed.broadcast(A, src=0)
+        torch.distributed.broadcast(lam_true, src=0)
     Acm = A.T  # symmetric: the row-major tensor's transpose view is its column-major image
     cfg = mpj.default_config("eig", variant=args.variant, eps_low_factor=args.eps_low)
-    wsbuf = mpj.eig_workspace(n, cfg, device=dev)
     lam = torch.empty(n, dtype=torch.float64, device=dev)
     V = mpj.empty_colmajor(n, n, device="cuda")
+    if ws > 1:
+        ids = [mpj.nccl_unique_id() if rank == 0 else None]
+        torch.distributed.broadcast_object_list(ids, src=0)
+        nccl_id = ids[0]
+        wsbuf = None
 
-    def step():
-        return mpj.eig(Acm, cfg, workspace=wsbuf, out=(lam, V), allow_noconv=True)
+        def step():
+            return mpj.eig_mg(Acm, cfg, nccl_id=nccl_id, rank=rank, nranks=ws, out=(lam, V), allow_noconv=True)
+    else:
+        wsbuf = mpj.eig_workspace(n, cfg, device=dev)
+
+        def step():
+            return mpj.eig(Acm, cfg, workspace=wsbuf, out=(lam, V), allow_noconv=True)
 
     for _ in range(args.warmup):
         res = step()
@@ -389,7 +404,8 @@ def main():
     flops_apply = nt_t * 2 * 2 * 64 ** 3 + nt_v * 2 * 64 ** 3
     bytes_apply = (nt_t * 3 + nt_v * 2) * 64 * 64 * 8   # T: read + tile + mirror; V: read + write
     kernels = {}
-    for name in ("block_apply_f64", "block_apply_f32", "block_solve_f64", "block_solve_f32"):
+    for name in ("block_apply_f64", "block_apply_f32", "block_solve_f64", "block_solve_f32",
+                 "mg_apply_f64", "mg_apply_f32", "mg_solve_f64", "mg_solve_f32"):
         sec, cnt = mpj.profile_get(name)
         if cnt:
             kernels[name] = {"seconds_per_step": sec / args.steps, "launches": cnt, "avg_ms": 1e3 * sec / cnt}
@@ -397,10 +413,13 @@ def main():
     if kernels:
         dom = max(kernels, key=lambda k: kernels[k]["seconds_per_step"])
         avg = kernels[dom]["avg_ms"] * 1e-3
-        if dom.startswith("block_apply"):
+        if dom.startswith("block_apply") or dom.startswith("mg_apply"):
             is64 = dom.endswith("f64")
-            fl = flops_apply
-            by = bytes_apply * (1 if is64 else 0.5)
+            fl, by = flops_apply, bytes_apply * (1 if is64 else 0.5)
+            if dom.startswith("mg_apply"):     # per rank: every slot a x own slots c, no mirror
+                mbl = mb // ws
+                fl = mbl * (mb - 1) * 2 * 2 * 64 ** 3 + (rep.n_padded // 64) * mbl * 2 * 64 ** 3
+                by = (mbl * (mb - 1) * 2 + (rep.n_padded // 64) * mbl * 2) * 64 * 64 * (8 if is64 else 4)
             peak = pk["dmma_tflops"] if is64 else pk["ffma_tflops"]
             traffic = None
             tp = os.path.join(ROOT, "profiles", "r01_traffic.json")
@@ -427,18 +446,27 @@ def main():
         Ahc = Ah.T
         lam_h = torch.empty(n, dtype=torch.float64, pin_memory=True)
         V_h = mpj.empty_colmajor(n, n, device="cpu", pin=True)
-        mpj.eig(Ahc, cfg, workspace=wsbuf, out=(lam_h, V_h), allow_noconv=True)   # warm
+        def host_step():
+            if ws > 1:
+                return mpj.eig_mg(Ahc, cfg, nccl_id=nccl_id, rank=rank, nranks=ws, out=(lam_h, V_h),
+                                  allow_noconv=True)
+            return mpj.eig(Ahc, cfg, workspace=wsbuf, out=(lam_h, V_h), allow_noconv=True)
+        host_step()   # warm
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         c0, c1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         c0.record()
         ksteps = max(1, min(args.steps, 2))
         for _ in range(ksteps):
-            mpj.eig(Ahc, cfg, workspace=wsbuf, out=(lam_h, V_h), allow_noconv=True)
+            host_step()
         c1.record()
         torch.cuda.synchronize()
         e2e_s = c0.elapsed_time(c1) / ksteps * 1e-3
         wall = (time.perf_counter() - t0) / ksteps
+        if ws > 1:
+            t = torch.tensor([max(e2e_s, wall)], device=dev)
+            torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+            e2e_s = wall = float(t.item())
         e2e = {"value": max(e2e_s, wall), "unit": "s", "h2d_bytes_per_step": n * n * 8,
                "d2h_bytes_per_step": n * 8 + n * n * 8}
 
@@ -457,14 +485,14 @@ def main():
         line = {
             "metric": "fp64 EVD seconds (n=8192)", "value": value, "unit": "s", "n_gpus": ws,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": False,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "scaling": "strong" if ws > 1 else "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": f"Example 1 (P:681) mode {args.mode} graded spectrum, kappa={args.kappa:g}, "
-                                   f"n={n}, one EVD per GPU per step",
+                                   f"n={n}, one EVD per step" + (f" partitioned over {ws} GPUs" if ws > 1 else ""),
                        "n": n, "mode": args.mode, "kappa": args.kappa,
                        "variant": {1: "scalar", 2: "block"}.get(rep.variant, rep.variant),
                        "block_b": rep.block_b, "n_padded": rep.n_padded,
                        "l2": "inputs (512 MB A, 2.5 GB workspace) exceed the 126 MB L2",
-                       "parallelism": "replicas" if ws > 1 else "single GPU"},
+                       "parallelism": f"column-block partition over {ws} GPUs (NCCL)" if ws > 1 else "single GPU"},
             "step_ms": step_ms, "lib_t_total": [r.t_total for r in reports],
             "sweeps": rep.sweeps, "sweeps_low": rep.sweeps_low,
             "off_hist_rel": [h / rep.norm_a for h in list(rep.off_hist)[: rep.sweeps + 1]],

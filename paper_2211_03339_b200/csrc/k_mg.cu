@@ -439,19 +439,25 @@ static mpj_status mg_sweep(Group &g, R **Ts, R **Vs, R nu, int rule)
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
     const size_t blk_bytes = (size_t)BW * g.np * sizeof(R);
+    const bool prof = prof_on();
+    const char *nsolve = sizeof(R) == 8 ? "mg_solve_f64" : "mg_solve_f32";
+    const char *napply = sizeof(R) == 8 ? "mg_apply_f64" : "mg_apply_f32";
     for (int r = 0; r < rounds; ++r) {
+        if (prof) prof_mark(nsolve, g.st, true);
         for (int i = 0; i < g.nlocal; ++i) {
             const int rr = g.rank_of(i);
             k_mg_solve<R><<<P.mbl, NTW, sm_solve, g.st>>>(Ts[i], g.np, g.rk[i].slots + (size_t)r * P.mbl, rr * P.mbl,
                                                           g.lsched, r == 0, nu, rule, (R *)g.Ubuf, g.cnt);
             count_launch();
         }
+        if (prof) prof_mark(nsolve, g.st, false);
         if (g.nlocal == 1 && g.G > 1) {
             const size_t per = (size_t)P.mbl * TW * TW;
             R *U = (R *)g.Ubuf;
             MPJ_TRY(nccl_ck(ncclAllGather(U + g.me * per, U, per * sizeof(R), ncclChar, g.comm, g.st),
                             "ncclAllGather(U)"));
         }
+        if (prof) prof_mark(napply, g.st, true);
         for (int i = 0; i < g.nlocal; ++i) {
             const int rr = g.rank_of(i);
             MgApply ap;
@@ -465,6 +471,7 @@ static mpj_status mg_sweep(Group &g, R **Ts, R **Vs, R nu, int rule)
             k_mg_apply<R><<<grid, NT, sm_apply, g.st>>>(ap);
             count_launch();
         }
+        if (prof) prof_mark(napply, g.st, false);
         // block moves across rank boundaries
         const std::vector<Xfer> &xs = P.xfers[r];
         if (xs.empty()) continue;
@@ -528,6 +535,7 @@ static mpj_status mg_loop(Group &g, R **Ts, R **Vs, double tol, R nu, int rule, 
         upload_colg(g);
         double off = 0;
         MPJ_TRY(mg_norm<R>(g, true, Ts, off));
+        prof_flush();
         if (hist && sweeps < 64) hist[sweeps] = off;
         if (!(off == off)) { set_error("non-finite off-norm"); return MPJ_ERR_NONFINITE; }
         if (off <= tol) { status = MPJ_OK; break; }
