@@ -214,6 +214,15 @@ mpj_status mpjacobi_eig_mg(const double *A, int64_t n, int64_t lda, double *Lamb
                            int *sweeps, const void *nccl_id, int rank, int nranks, int emulate_ranks,
                            void *stream, const mpj_config *cfg, mpj_report *rep);
 
+/* Host-only: the partition plan of one sweep of mpjacobi_eig_mg (no GPU
+ * needed; used by the CPU multi-rank tests).  Pass NULL arrays to query
+ * n_p and the number of block rounds.  slots: rounds x mb x 4 (top block,
+ * bottom block, physical position of each on its rank; mb = n_p/64), xfers:
+ * rounds x (4 nranks) x 4 (src rank, src position, dst rank, dst position),
+ * nxfer: rounds.  Positions count blocks of 32 columns. */
+mpj_status mpjacobi_mg_plan(int64_t n, int nranks, int *np_out, int *rounds_out, int *slots, int *xfers,
+                            int *nxfer);
+
 /* ncclGetUniqueId into out (>= 128 bytes). */
 mpj_status mpjacobi_nccl_unique_id(void *out, size_t bytes);
 

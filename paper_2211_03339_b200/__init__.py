@@ -109,6 +109,8 @@ def lib():
         L.mpjacobi_eig_mg.restype = C.c_int
         L.mpjacobi_eig_mg.argtypes = [_vp, _i64, _i64, _vp, _vp, _i64, C.POINTER(C.c_int), _vp, C.c_int, C.c_int,
                                       C.c_int, _vp, cfgp, repp]
+        L.mpjacobi_mg_plan.restype = C.c_int
+        L.mpjacobi_mg_plan.argtypes = [_i64, C.c_int, C.POINTER(C.c_int), C.POINTER(C.c_int), _vp, _vp, _vp]
         L.mpjacobi_nccl_unique_id.restype = C.c_int
         L.mpjacobi_nccl_unique_id.argtypes = [_vp, C.c_size_t]
         if hasattr(L, "mpjacobi_eig_batched"):
@@ -124,7 +126,7 @@ EXPORTED = (
     "mpjacobi_precond", "mpjacobi_dgemm", "mpjacobi_svd_workspace", "mpjacobi_svd",
     "mpjacobi_eig_batched", "mpjacobi_last_error", "mpjacobi_launch_count",
     "mpjacobi_profile_enable", "mpjacobi_profile_reset", "mpjacobi_profile_get",
-    "mpjacobi_eig_mg", "mpjacobi_nccl_unique_id",
+    "mpjacobi_eig_mg", "mpjacobi_nccl_unique_id", "mpjacobi_mg_plan",
 )
 
 
@@ -358,6 +360,20 @@ def mpjacobi_eig_batched(A, cfg: mpj_config | None = None, allow_noconv=False) -
                                     C.byref(cfg or default_config("eig")))
     _check(st, (MPJ_OK, MPJ_ERR_NOCONV) if allow_noconv else (MPJ_OK,))
     return BatchedResult(lam, V.transpose(1, 2), sw, swl, st)
+
+
+def mg_plan(n: int, nranks: int):
+    """The partition plan of one sweep of eig_mg (host-only, no GPU):
+    (n_p, slots[rounds, mb, 4], xfers: list per round of (src, sphys, dst, dphys))."""
+    import numpy as np
+    npd, rounds = C.c_int(0), C.c_int(0)
+    _check(lib().mpjacobi_mg_plan(n, nranks, C.byref(npd), C.byref(rounds), None, None, None))
+    mb = npd.value // 64
+    slots = np.zeros((rounds.value, mb, 4), dtype=np.int32)
+    xf = np.zeros((rounds.value, 4 * nranks, 4), dtype=np.int32)
+    nx = np.zeros(rounds.value, dtype=np.int32)
+    _check(lib().mpjacobi_mg_plan(n, nranks, None, None, slots.ctypes.data, xf.ctypes.data, nx.ctypes.data))
+    return npd.value, slots, [xf[r, : nx[r]].tolist() for r in range(rounds.value)]
 
 
 def nccl_unique_id() -> bytes:

@@ -790,6 +790,41 @@ mpj_status mg_eig(bool mixed, const double *A, int64_t n, int64_t lda, double *L
 
 }  // namespace mpj
 
+// Host-only view of the partition plan of one sweep (tests of the multi-rank
+// bookkeeping without GPUs).  slots: rounds x mb x 4 ints (top, bot, ptop, pbot
+// of global slot k, physical positions on rank k / mbl); xfers: rounds x
+// (4 * nranks) x 4 ints (src, sphys, dst, dphys; physical positions in blocks
+// of 32 columns); nxfer: rounds ints.
+extern "C" mpj_status mpjacobi_mg_plan(int64_t n, int nranks, int *np_out, int *rounds_out, int *slots, int *xfers,
+                                       int *nxfer)
+{
+    using namespace mpj;
+    if (n < 1 || nranks < 1) { set_error("mpjacobi_mg_plan: invalid argument"); return MPJ_ERR_INVALID; }
+    Plan P;
+    const int np = padded_n(n, BW * nranks);
+    P.init((int)n, np, nranks);
+    if (np_out) *np_out = np;
+    if (rounds_out) *rounds_out = P.nb - 1;
+    if (!slots || !xfers || !nxfer) return MPJ_OK;
+    P.build_sweep();
+    const int maxx = 4 * nranks;
+    for (int r = 0; r < P.nb - 1; ++r) {
+        for (int k = 0; k < P.mb; ++k) {
+            const SlotInfo &si = P.slots[r][k];   // index g * mbl + kl == global slot k
+            int *o = slots + ((size_t)r * P.mb + k) * 4;
+            o[0] = si.top; o[1] = si.bot; o[2] = si.ptop / BW; o[3] = si.pbot / BW;
+        }
+        const std::vector<Xfer> &xs = P.xfers[r];
+        if ((int)xs.size() > maxx) { set_error("mpjacobi_mg_plan: too many transfers"); return MPJ_ERR_INVALID; }
+        nxfer[r] = (int)xs.size();
+        for (size_t i = 0; i < xs.size(); ++i) {
+            int *o = xfers + ((size_t)r * maxx + i) * 4;
+            o[0] = xs[i].src; o[1] = xs[i].sphys; o[2] = xs[i].dst; o[3] = xs[i].dphys;
+        }
+    }
+    return MPJ_OK;
+}
+
 extern "C" mpj_status mpjacobi_nccl_unique_id(void *out, size_t bytes)
 {
     if (!out || bytes < sizeof(ncclUniqueId)) {
