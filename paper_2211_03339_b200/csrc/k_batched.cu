@@ -252,7 +252,6 @@ mpj_status batched_evd(const double *A, int64_t n, int64_t batch, double *Lambda
     int h_flag = 0;
     MPJ_CK(cudaMemcpyAsync(&h_flag, flag, sizeof(int), cudaMemcpyDeviceToHost, st));
     MPJ_CK(cudaStreamSynchronize(st));
-    prof_flush();
     cudaFreeAsync(lsched, st);
     if (h_flag & 2) { set_error("batched: rank-deficient Z in CGS2"); return MPJ_ERR_RANKDEF; }
     if (h_flag & 1) { set_error("batched: some matrix reached max_sweeps"); return MPJ_ERR_NOCONV; }

@@ -535,7 +535,6 @@ static mpj_status mg_loop(Group &g, R **Ts, R **Vs, double tol, R nu, int rule, 
         upload_colg(g);
         double off = 0;
         MPJ_TRY(mg_norm<R>(g, true, Ts, off));
-        prof_flush();
         if (hist && sweeps < 64) hist[sweeps] = off;
         if (!(off == off)) { set_error("non-finite off-norm"); return MPJ_ERR_NONFINITE; }
         if (off <= tol) { status = MPJ_OK; break; }

@@ -260,7 +260,6 @@ static mpj_status svd_loop(SvdPlan &p, R *C, R *V, double *Cd, const DevSched &d
         launch_norm<double>(p.G, p.np, p.np, p.np, false, p.red_part, p.red_out + 1, st);
         MPJ_CK(cudaMemcpyAsync(h_pin, p.red_out, 2 * sizeof(double), cudaMemcpyDeviceToHost, st));
         MPJ_CK(cudaStreamSynchronize(st));
-        prof_flush();
         const double off = h_pin[0], tot = h_pin[1];
         if (out.sweeps < 64) { out.hist[out.sweeps] = off; out.nhist = out.sweeps + 1; }
         if (!(off == off)) { set_error("non-finite Gram"); return MPJ_ERR_NONFINITE; }
@@ -270,7 +269,6 @@ static mpj_status svd_loop(SvdPlan &p, R *C, R *V, double *Cd, const DevSched &d
         MPJ_TRY(svd_block_sweep<R>(p, C, V, ds, nu, st));
         MPJ_CK(cudaMemcpyAsync(h_pin, p.cnt, sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
         MPJ_CK(cudaStreamSynchronize(st));
-        prof_flush();
         unsigned long long now = 0;
         std::memcpy(&now, h_pin, sizeof(now));
         const unsigned long long rs = now - prev;

@@ -321,7 +321,6 @@ static mpj_status jacobi_run(Ctx &cx, R *T, R *V, int n, int b, int variant, dou
         launch_norm<R>(T, np, np, np, true, jb.part, jb.off, st);
         MPJ_CK(cudaMemcpyAsync(cx.h_pin, jb.off, sizeof(double), cudaMemcpyDeviceToHost, st));
         MPJ_CK(cudaStreamSynchronize(st));
-        prof_flush();
         const double off = cx.h_pin[0];
         if (sweeps < 64) { out.hist[sweeps] = off; out.nhist = sweeps + 1; }
         if (!(off == off)) { set_error("non-finite off-norm"); status = MPJ_ERR_NONFINITE; break; }
