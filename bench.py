@@ -49,7 +49,7 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample-seconds", type=float, default=20.0)
     ap.add_argument("--m", type=int, default=16384, help="rows for --workload svd")
-    ap.add_argument("--workload", default="evd", choices=["evd", "batched", "svd"],
+    ap.add_argument("--workload", default="evd", choices=["evd", "batched", "svd", "config2"],
                     help="evd: BASELINE config 4 (the bench line); batched: config 3 (4096 x n=64)")
     ap.add_argument("--batch", type=int, default=4096)
     ap.add_argument("--eps-low", type=float, default=0.0,
@@ -260,6 +260,39 @@ def run_batched(args):
     print(json.dumps(line))
 
 
+def run_config2(args):
+    """BASELINE config 2: n = 1024, uniform and clustered spectra, Alg. 3 vs
+    Alg. 2 (same kernels and ordering): seconds and fp64 sweeps."""
+    import torch
+
+    import paper_2211_03339_b200 as mpj
+    import workloads as W
+    n = 1024
+    rows = []
+    for kind, gen, mode in (("uniform (Ex.1 mode 4)", W.example1, 4), ("clustered (Ex.2 mode 4, x4)", W.example2, 4),
+                            ("one large (Ex.1 mode 1)", W.example1, 1), ("geometric (Ex.1 mode 3, k=1e6)", W.example1, 3)):
+        kappa = 1e6 if mode == 3 else 1e3
+        A, lam_true = gen(n, kappa, mode, W.seed_for(2, mode, kappa))
+        At = torch.from_numpy(A).cuda()
+        out = {}
+        for label, plain in (("mp", False), ("plain", True)):
+            for _ in range(args.warmup):
+                r = mpj.eig(At, plain=plain)
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            for _ in range(args.steps):
+                r = mpj.eig(At, plain=plain)
+            e1.record()
+            torch.cuda.synchronize()
+            out[label] = {"seconds": e0.elapsed_time(e1) / args.steps * 1e-3, "sweeps": r.sweeps,
+                          "sweeps_low": r.report.sweeps_low,
+                          "max_dlam": float(abs(r.lam.cpu().numpy() - lam_true).max())}
+        rows.append({"spectrum": kind, **out})
+    print(json.dumps({"metric": "config 2: n=1024 EVD seconds and fp64 sweeps, Alg. 3 vs Alg. 2", "rows": rows,
+                      "steps": args.steps, "warmup": args.warmup}))
+
+
 def run_svd(args):
     """BASELINE config 5a: Alg. 5 on an Example 3 matrix, m x n =
     16384 x 4096 by default, mode 3, kappa = 1e3."""
@@ -322,6 +355,8 @@ def main():
         return run_batched(args)
     if args.workload == "svd":
         return run_svd(args)
+    if args.workload == "config2":
+        return run_config2(args)
     import numpy as np
     import torch
 

@@ -331,3 +331,27 @@ def test_eig_mg_emulated(mpj, orc, n, mode):
         lams.append(host(res.lam))
     assert np.max(np.abs(lams[1] - lams[0])) <= 1e-14 * np.abs(lams[0]).max()
     assert np.max(np.abs(lams[2] - lams[0])) <= 1e-14 * np.abs(lams[0]).max()
+
+
+# ----------------------------------------------------------------- BASELINE config 2 (n = 1024)
+@pytest.mark.parametrize("kind,mode,kappa", [("uniform", 4, 1e3), ("clustered", 4, 1e3), ("ex1_mode1", 1, 1e3)])
+def test_config2_n1024_mp_vs_plain(mpj, kind, mode, kappa):
+    """BASELINE config 2: n = 1024, uniform (Example 1 mode 4) and clustered
+    (Example 2 mode 4, multiplicity 4; Example 1 mode 1) spectra, Alg. 3 vs
+    Alg. 2 with the same kernels and ordering.  Full-size checks the oracle can
+    make without running: the generator's exact spectrum (|dlam| <= 1e-13
+    ||A||_2), residual and orthogonality (n 1e-15); and the paper's claim that
+    the mixed-precision run needs fewer fp64 sweeps on distinct spectra (P:687,
+    Tables 2-5) -- on clusters the parallel ordering may not gain (Tables 6-9)."""
+    n = 1024
+    gen = W.example2 if kind == "clustered" else W.example1
+    A, lam_true = gen(n, kappa, mode, W.seed_for(2, mode, kappa))
+    mp = mpj.eig(dev(A))
+    pl = mpj.eig(dev(A), plain=True)
+    for r in (mp, pl):
+        lam, V = host(r.lam), host(r.V)
+        assert np.max(np.abs(lam - lam_true)) <= 1e-13 * np.abs(lam_true).max()
+        assert np.linalg.norm(V.T @ V - np.eye(n)) <= n * 1e-15
+        assert np.linalg.norm(A @ V - V * lam) / np.linalg.norm(A) <= n * 1e-15
+    if kind == "uniform":
+        assert mp.sweeps <= 4 and pl.sweeps >= 8 and mp.sweeps < pl.sweeps
