@@ -204,6 +204,13 @@ struct Ctx {
         int dev = 0;
         MPJ_CK(cudaGetDevice(&dev));
         if (g_ctx.st == nullptr || g_ctx.dev != dev) {
+            // keep stream-ordered allocations (library-owned workspaces) cached in the
+            // device's default pool instead of trimming it at every synchronisation
+            cudaMemPool_t pool;
+            if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+                uint64_t thr = UINT64_MAX;
+                cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+            }
             MPJ_CK(cudaStreamCreateWithFlags(&g_ctx.st, cudaStreamNonBlocking));
             MPJ_CK(cudaEventCreateWithFlags(&g_ctx.ev, cudaEventDisableTiming));
             MPJ_CK(cudaMallocHost(&g_ctx.h_pin, 64 * sizeof(double)));
