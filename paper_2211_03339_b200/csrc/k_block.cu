@@ -43,7 +43,7 @@ __global__ void __launch_bounds__(NTW) k_block_solve(R *__restrict__ T, int64_t 
     R *D1 = D0 + TW * LD;
     R *U = D1 + TW * LD;            // 64 x LD
     __shared__ unsigned nrot;
-    __shared__ WideParams<R> P;
+    __shared__ WideParams<R> P[2];
     const int k = blockIdx.x;
     const int mb = S.nb >> 1;
     const int2 bp = S.bsched[Rb * mb + k];

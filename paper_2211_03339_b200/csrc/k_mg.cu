@@ -58,7 +58,7 @@ __global__ void __launch_bounds__(NTW) k_mg_solve(R *__restrict__ T, int64_t ldt
     R *D1 = D0 + TW * LD;
     R *U = D1 + TW * LD;
     __shared__ unsigned nrot;
-    __shared__ WideParams<R> P;
+    __shared__ WideParams<R> P[2];
     const SlotInfo si = slots[blockIdx.x];
     const int2 bp = make_int2(si.top, si.bot);
     for (int e = threadIdx.x; e < TW * TW; e += NTW) {

@@ -114,14 +114,16 @@ __device__ __forceinline__ unsigned inner_rounds(R *D, R *U, int2 bp, bool intra
 }
 
 // ---------------------------------------------------------------------------
-// Wide variant of inner_rounds (NTW = 512 threads) for the block variant's K3.
-// Per round: warp 0 computes the 32 rotation parameters into a shared table;
-// then the 496 off-diagonal tiles (k < l) are computed once each in the
-// canonical order (reading R7) and written together with their mirror, the
-// remaining 16 threads take the 32 diagonal tiles (t_pp - t a_pq form), and all
-// 512 threads apply 4 (row, pair) updates of U.  D is double-buffered (every
-// entry is rewritten each round), so a round needs two barriers.  The per
-// element arithmetic is exactly inner_rounds' (same results).
+// Pipelined inner rounds (NTW = 512 threads) for the block variant's K3.
+// Warps 1..15 apply round s (496 off-diagonal 2x2 tiles computed once in the
+// canonical order of reading R7 and mirrored, 32 diagonal tiles, U <- U J),
+// reading Dc and writing Dn; meanwhile warp 0 computes the rotation
+// parameters of round s+1: for each next pair (p', q') it recomputes from Dc,
+// with the very same arithmetic, the three entries Lemma 3.1 needs after
+// round s (two diagonal updates and one element of one 2x2 tile), then runs
+// rot_params.  One barrier per round; the parameter latency (divides,
+// square roots) is hidden under the update phase.  Results are identical to
+// inner_rounds.
 // ---------------------------------------------------------------------------
 constexpr int NTW = 512;
 
@@ -129,80 +131,139 @@ template <typename R>
 struct WideParams {
     R t[BW], s[BW], u[BW];
     int p[BW], q[BW], gp[BW];
+    int pos[TW];            // local index -> pair of this round
 };
+
+// local pair (a, c) of `lane` in round s
+__device__ __forceinline__ void round_pair(int s, int lane, bool intra, const int2 *__restrict__ lsched, int &a,
+                                           int &c)
+{
+    if (intra && s < BW - 1) {
+        const int hb = BW / 2;
+        const int2 lp = lsched[s * hb + (lane < hb ? lane : lane - hb)];
+        const int off = (lane < hb) ? 0 : BW;
+        a = off + lp.x; c = off + lp.y;
+    } else {
+        const int sc = intra ? s - (BW - 1) : s;
+        a = lane;
+        int j = lane + sc; if (j >= BW) j -= BW;
+        c = BW + j;
+    }
+}
+
+// the canonical 2x2 tile (rows of pair k, columns of pair l) after the round
+template <typename R>
+__device__ __forceinline__ void tile_after(const R *Dc, const WideParams<R> &P, int k, int l, R &x11, R &x21,
+                                           R &x12, R &x22)
+{
+    constexpr int LD = Lay<R>::LD;
+    const int pk = P.p[k], qk = P.q[k], pl = P.p[l], ql = P.q[l];
+    const R sk = P.s[k], uk = P.u[k], sl = P.s[l], ul = P.u[l];
+    x11 = Dc[pk + pl * LD]; x21 = Dc[qk + pl * LD]; x12 = Dc[pk + ql * LD]; x22 = Dc[qk + ql * LD];
+    if (P.gp[k] < P.gp[l]) {
+        rot<R>(sk, uk, x11, x21); rot<R>(sk, uk, x12, x22);
+        rot<R>(sl, ul, x11, x12); rot<R>(sl, ul, x21, x22);
+    } else {
+        rot<R>(sl, ul, x11, x12); rot<R>(sl, ul, x21, x22);
+        rot<R>(sk, uk, x11, x21); rot<R>(sk, uk, x12, x22);
+    }
+}
+
+// diagonal entry of local index i after the round
+template <typename R>
+__device__ __forceinline__ R diag_after(const R *Dc, const WideParams<R> &P, int i)
+{
+    constexpr int LD = Lay<R>::LD;
+    const int k = P.pos[i], pk = P.p[k], qk = P.q[k];
+    const R apq = Dc[pk + qk * LD];
+    return i == pk ? fmaR(-P.t[k], apq, Dc[pk + pk * LD]) : fmaR(P.t[k], apq, Dc[qk + qk * LD]);
+}
 
 template <typename R>
 __device__ __forceinline__ R *inner_rounds_wide(R *D0, R *D1, R *U, int2 bp, bool intra,
                                                 const int2 *__restrict__ lsched, R nu, int rule,
-                                                WideParams<R> &P, unsigned *nrot)
+                                                WideParams<R> (&PP)[2], unsigned *nrot)
 {
     constexpr int LD = Lay<R>::LD;
-    const int tid = threadIdx.x, lane = tid & 31;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     R *Dc = D0, *Dn = D1;
     unsigned cnt = 0;
     const int nrounds = intra ? (BW - 1) + BW : BW;
+    // parameters of round 0
+    if (warp == 0) {
+        int a, c;
+        round_pair(0, lane, intra, lsched, a, c);
+        const int ga = gidx(bp, a), gc = gidx(bp, c);
+        const int pk = ga < gc ? a : c, qk = ga < gc ? c : a;
+        R t, sk, uk;
+        const int did = rot_params<R>(Dc[pk + pk * LD], Dc[qk + qk * LD], Dc[pk + qk * LD], nu, rule, t, sk, uk);
+        cnt += __popc(__ballot_sync(0xffffffffu, did));
+        WideParams<R> &P = PP[0];
+        P.t[lane] = t; P.s[lane] = sk; P.u[lane] = uk;
+        P.p[lane] = pk; P.q[lane] = qk; P.gp[lane] = ga < gc ? ga : gc;
+        P.pos[pk] = lane; P.pos[qk] = lane;
+    }
+    __syncthreads();
     for (int s = 0; s < nrounds; ++s) {
-        if (tid < 32) {
-            int a, c;
-            if (intra && s < BW - 1) {
-                const int hb = BW / 2;
-                const int2 lp = lsched[s * hb + (lane < hb ? lane : lane - hb)];
-                const int off = (lane < hb) ? 0 : BW;
-                a = off + lp.x; c = off + lp.y;
-            } else {
-                const int sc = intra ? s - (BW - 1) : s;
-                a = lane;
-                int j = lane + sc; if (j >= BW) j -= BW;
-                c = BW + j;
+        const WideParams<R> &P = PP[s & 1];
+        if (warp == 0) {
+            if (s + 1 < nrounds) {
+                WideParams<R> &N = PP[(s + 1) & 1];
+                int a, c;
+                round_pair(s + 1, lane, intra, lsched, a, c);
+                const int ga = gidx(bp, a), gc = gidx(bp, c);
+                const int pn = ga < gc ? a : c, qn = ga < gc ? c : a;
+                const R app = diag_after<R>(Dc, P, pn), aqq = diag_after<R>(Dc, P, qn);
+                // (pn, qn) lies in the tile of pairs k = pos[pn], l = pos[qn] (k != l)
+                const int k = P.pos[pn], l = P.pos[qn];
+                R x11, x21, x12, x22, apq;
+                if (k < l) {            // computed tile (k, l): rows of k, columns of l
+                    tile_after<R>(Dc, P, k, l, x11, x21, x12, x22);
+                    apq = (pn == P.p[k]) ? (qn == P.p[l] ? x11 : x12) : (qn == P.p[l] ? x21 : x22);
+                } else {                // mirror of tile (l, k): entry (qn, pn)
+                    tile_after<R>(Dc, P, l, k, x11, x21, x12, x22);
+                    apq = (qn == P.p[l]) ? (pn == P.p[k] ? x11 : x12) : (pn == P.p[k] ? x21 : x22);
+                }
+                R t, sk, uk;
+                const int did = rot_params<R>(app, aqq, apq, nu, rule, t, sk, uk);
+                cnt += __popc(__ballot_sync(0xffffffffu, did));
+                N.t[lane] = t; N.s[lane] = sk; N.u[lane] = uk;
+                N.p[lane] = pn; N.q[lane] = qn; N.gp[lane] = ga < gc ? ga : gc;
+                N.pos[pn] = lane; N.pos[qn] = lane;
             }
-            const int ga = gidx(bp, a), gc = gidx(bp, c);
-            const int pk = ga < gc ? a : c, qk = ga < gc ? c : a;
-            R t, sk, uk;
-            const int did = rot_params<R>(Dc[pk + pk * LD], Dc[qk + qk * LD], Dc[pk + qk * LD], nu, rule, t, sk, uk);
-            cnt += __popc(__ballot_sync(0xffffffffu, did));
-            P.t[lane] = t; P.s[lane] = sk; P.u[lane] = uk;
-            P.p[lane] = pk; P.q[lane] = qk; P.gp[lane] = ga < gc ? ga : gc;
-        }
-        __syncthreads();
-        if (tid < BW * (BW - 1) / 2) {
-            // upper tile index -> (k, l), k < l
-            int l = (int)((1.0f + sqrtf(1.0f + 8.0f * tid)) * 0.5f);
-            while (l * (l - 1) / 2 > tid) --l;
-            while ((l + 1) * l / 2 <= tid) ++l;
-            const int k = tid - l * (l - 1) / 2;
-            const int pk = P.p[k], qk = P.q[k], pl = P.p[l], ql = P.q[l];
-            const R sk = P.s[k], uk = P.u[k], sl = P.s[l], ul = P.u[l];
-            R x11 = Dc[pk + pl * LD], x21 = Dc[qk + pl * LD], x12 = Dc[pk + ql * LD], x22 = Dc[qk + ql * LD];
-            if (P.gp[k] < P.gp[l]) {
-                rot<R>(sk, uk, x11, x21); rot<R>(sk, uk, x12, x22);
-                rot<R>(sl, ul, x11, x12); rot<R>(sl, ul, x21, x22);
-            } else {
-                rot<R>(sl, ul, x11, x12); rot<R>(sl, ul, x21, x22);
-                rot<R>(sk, uk, x11, x21); rot<R>(sk, uk, x12, x22);
-            }
-            Dn[pk + pl * LD] = x11; Dn[qk + pl * LD] = x21; Dn[pk + ql * LD] = x12; Dn[qk + ql * LD] = x22;
-            Dn[pl + pk * LD] = x11; Dn[pl + qk * LD] = x21; Dn[ql + pk * LD] = x12; Dn[ql + qk * LD] = x22;
         } else {
-            // the NTW - 496 remaining threads take the 32 diagonal tiles
-            for (int k = tid - BW * (BW - 1) / 2; k < BW; k += NTW - BW * (BW - 1) / 2) {
-                const int pk = P.p[k], qk = P.q[k];
-                const R apq = Dc[pk + qk * LD], t = P.t[k];
-                Dn[pk + pk * LD] = fmaR(-t, apq, Dc[pk + pk * LD]);
-                Dn[qk + qk * LD] = fmaR(t, apq, Dc[qk + qk * LD]);
-                Dn[pk + qk * LD] = R(0);
-                Dn[qk + pk * LD] = R(0);
-            }
-        }
-        if (U) {
-            #pragma unroll
-            for (int h = 0; h < (BW * TW) / NTW; ++h) {
-                const int e = tid + h * NTW, r = e & (TW - 1), k = e >> 6;
-                const R sk = P.s[k];
-                if (sk != R(0)) {
+            const int w = tid - 32, NW = NTW - 32;
+            for (int e = w; e < BW * (BW - 1) / 2 + BW; e += NW) {
+                if (e < BW * (BW - 1) / 2) {
+                    int l = (int)((1.0f + sqrtf(1.0f + 8.0f * e)) * 0.5f);
+                    while (l * (l - 1) / 2 > e) --l;
+                    while ((l + 1) * l / 2 <= e) ++l;
+                    const int k = e - l * (l - 1) / 2;
+                    R x11, x21, x12, x22;
+                    tile_after<R>(Dc, P, k, l, x11, x21, x12, x22);
+                    const int pk = P.p[k], qk = P.q[k], pl = P.p[l], ql = P.q[l];
+                    Dn[pk + pl * LD] = x11; Dn[qk + pl * LD] = x21; Dn[pk + ql * LD] = x12; Dn[qk + ql * LD] = x22;
+                    Dn[pl + pk * LD] = x11; Dn[pl + qk * LD] = x21; Dn[ql + pk * LD] = x12; Dn[ql + qk * LD] = x22;
+                } else {
+                    const int k = e - BW * (BW - 1) / 2;
                     const int pk = P.p[k], qk = P.q[k];
-                    R x = U[r + pk * LD], y = U[r + qk * LD];
-                    rot<R>(sk, P.u[k], x, y);
-                    U[r + pk * LD] = x; U[r + qk * LD] = y;
+                    const R apq = Dc[pk + qk * LD], t = P.t[k];
+                    Dn[pk + pk * LD] = fmaR(-t, apq, Dc[pk + pk * LD]);
+                    Dn[qk + qk * LD] = fmaR(t, apq, Dc[qk + qk * LD]);
+                    Dn[pk + qk * LD] = R(0);
+                    Dn[qk + pk * LD] = R(0);
+                }
+            }
+            if (U) {
+                for (int e = w; e < BW * TW; e += NW) {
+                    const int r = e & (TW - 1), k = e >> 6;
+                    const R sk = P.s[k];
+                    if (sk != R(0)) {
+                        const int pk = P.p[k], qk = P.q[k];
+                        R x = U[r + pk * LD], y = U[r + qk * LD];
+                        rot<R>(sk, P.u[k], x, y);
+                        U[r + pk * LD] = x; U[r + qk * LD] = y;
+                    }
                 }
             }
         }
