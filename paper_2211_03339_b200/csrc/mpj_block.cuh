@@ -114,8 +114,8 @@ __device__ __forceinline__ unsigned inner_rounds(R *D, R *U, int2 bp, bool intra
 }
 
 // ---------------------------------------------------------------------------
-// Pipelined inner rounds (NTW = 512 threads) for the block variant's K3.
-// Warps 1..15 apply round s (496 off-diagonal 2x2 tiles computed once in the
+// Pipelined inner rounds (NTW = 1024 threads) for the block variant's K3.
+// Warps 1..31 apply round s (496 off-diagonal 2x2 tiles computed once in the
 // canonical order of reading R7 and mirrored, 32 diagonal tiles, U <- U J),
 // reading Dc and writing Dn; meanwhile warp 0 computes the rotation
 // parameters of round s+1: for each next pair (p', q') it recomputes from Dc,
@@ -125,7 +125,7 @@ __device__ __forceinline__ unsigned inner_rounds(R *D, R *U, int2 bp, bool intra
 // square roots) is hidden under the update phase.  Results are identical to
 // inner_rounds.
 // ---------------------------------------------------------------------------
-constexpr int NTW = 512;
+constexpr int NTW = 1024;
 
 template <typename R>
 struct WideParams {
@@ -189,6 +189,24 @@ __device__ __forceinline__ R *inner_rounds_wide(R *D0, R *D1, R *U, int2 bp, boo
     R *Dc = D0, *Dn = D1;
     unsigned cnt = 0;
     const int nrounds = intra ? (BW - 1) + BW : BW;
+    // static assignment of the update work to threads 32..NTW-1
+    int tk = -1, tl = -1, ur[3] = {0, 0, 0}, uk[3] = {-1, -1, -1};
+    if (warp > 0) {
+        const int w = tid - 32, NW = NTW - 32;
+        if (w < BW * (BW - 1) / 2) {
+            int l = (int)((1.0f + sqrtf(1.0f + 8.0f * w)) * 0.5f);
+            while (l * (l - 1) / 2 > w) --l;
+            while ((l + 1) * l / 2 <= w) ++l;
+            tk = w - l * (l - 1) / 2; tl = l;
+        } else if (w < BW * (BW - 1) / 2 + BW) {
+            tk = w - BW * (BW - 1) / 2; tl = -1;
+        }
+        #pragma unroll
+        for (int j = 0; j < 3; ++j) {
+            const int e = w + j * NW;
+            if (e < BW * TW) { ur[j] = e & (TW - 1); uk[j] = e >> 6; }
+        }
+    }
     // parameters of round 0
     if (warp == 0) {
         int a, c;
@@ -232,22 +250,18 @@ __device__ __forceinline__ R *inner_rounds_wide(R *D0, R *D1, R *U, int2 bp, boo
                 N.pos[pn] = lane; N.pos[qn] = lane;
             }
         } else {
-            const int w = tid - 32, NW = NTW - 32;
-            for (int e = w; e < BW * (BW - 1) / 2 + BW; e += NW) {
-                if (e < BW * (BW - 1) / 2) {
-                    int l = (int)((1.0f + sqrtf(1.0f + 8.0f * e)) * 0.5f);
-                    while (l * (l - 1) / 2 > e) --l;
-                    while ((l + 1) * l / 2 <= e) ++l;
-                    const int k = e - l * (l - 1) / 2;
+            // static work of this thread (computed before the loop): tile (tk, tl)
+            // (tl < 0: diagonal tile tk; tk < 0: none) and U items (ur[j], uk[j])
+            if (tk >= 0) {
+                if (tl >= 0) {
                     R x11, x21, x12, x22;
-                    tile_after<R>(Dc, P, k, l, x11, x21, x12, x22);
-                    const int pk = P.p[k], qk = P.q[k], pl = P.p[l], ql = P.q[l];
+                    tile_after<R>(Dc, P, tk, tl, x11, x21, x12, x22);
+                    const int pk = P.p[tk], qk = P.q[tk], pl = P.p[tl], ql = P.q[tl];
                     Dn[pk + pl * LD] = x11; Dn[qk + pl * LD] = x21; Dn[pk + ql * LD] = x12; Dn[qk + ql * LD] = x22;
                     Dn[pl + pk * LD] = x11; Dn[pl + qk * LD] = x21; Dn[ql + pk * LD] = x12; Dn[ql + qk * LD] = x22;
                 } else {
-                    const int k = e - BW * (BW - 1) / 2;
-                    const int pk = P.p[k], qk = P.q[k];
-                    const R apq = Dc[pk + qk * LD], t = P.t[k];
+                    const int pk = P.p[tk], qk = P.q[tk];
+                    const R apq = Dc[pk + qk * LD], t = P.t[tk];
                     Dn[pk + pk * LD] = fmaR(-t, apq, Dc[pk + pk * LD]);
                     Dn[qk + qk * LD] = fmaR(t, apq, Dc[qk + qk * LD]);
                     Dn[pk + qk * LD] = R(0);
@@ -255,14 +269,15 @@ __device__ __forceinline__ R *inner_rounds_wide(R *D0, R *D1, R *U, int2 bp, boo
                 }
             }
             if (U) {
-                for (int e = w; e < BW * TW; e += NW) {
-                    const int r = e & (TW - 1), k = e >> 6;
-                    const R sk = P.s[k];
+                #pragma unroll
+                for (int j = 0; j < 3; ++j) {
+                    if (uk[j] < 0) continue;
+                    const R sk = P.s[uk[j]];
                     if (sk != R(0)) {
-                        const int pk = P.p[k], qk = P.q[k];
-                        R x = U[r + pk * LD], y = U[r + qk * LD];
-                        rot<R>(sk, P.u[k], x, y);
-                        U[r + pk * LD] = x; U[r + qk * LD] = y;
+                        const int pk = P.p[uk[j]], qk = P.q[uk[j]];
+                        R x = U[ur[j] + pk * LD], y = U[ur[j] + qk * LD];
+                        rot<R>(sk, P.u[uk[j]], x, y);
+                        U[ur[j] + pk * LD] = x; U[ur[j] + qk * LD] = y;
                     }
                 }
             }
