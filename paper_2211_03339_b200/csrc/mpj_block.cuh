@@ -185,14 +185,16 @@ __device__ __forceinline__ R *inner_rounds_wide(R *D0, R *D1, R *U, int2 bp, boo
                                                 WideParams<R> (&PP)[2], unsigned *nrot)
 {
     constexpr int LD = Lay<R>::LD;
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    // the parameter warp is the LAST warp: the SM's warp arbiter issues
+    // highest-warp-id first, and this warp's dependent chain is the critical path
+    const int tid = threadIdx.x, lane = tid & 31, warp = (NTW / 32 - 1) - (tid >> 5);
     R *Dc = D0, *Dn = D1;
     unsigned cnt = 0;
     const int nrounds = intra ? (BW - 1) + BW : BW;
-    // static assignment of the update work to threads 32..NTW-1
+    // static assignment of the update work to the other threads
     int tk = -1, tl = -1, ur[3] = {0, 0, 0}, uk[3] = {-1, -1, -1};
     if (warp > 0) {
-        const int w = tid - 32, NW = NTW - 32;
+        const int w = (warp - 1) * 32 + lane, NW = NTW - 32;
         if (w < BW * (BW - 1) / 2) {
             int l = (int)((1.0f + sqrtf(1.0f + 8.0f * w)) * 0.5f);
             while (l * (l - 1) / 2 > w) --l;
@@ -285,7 +287,7 @@ __device__ __forceinline__ R *inner_rounds_wide(R *D0, R *D1, R *U, int2 bp, boo
         __syncthreads();
         R *tmp = Dc; Dc = Dn; Dn = tmp;
     }
-    if (tid == 0) *nrot = cnt;
+    if (warp == 0 && lane == 0) *nrot = cnt;
     return Dc;
 }
 

@@ -42,6 +42,12 @@ __device__ __forceinline__ float minR(float a, float b) { return fminf(a, b); }
 template <typename R>
 __device__ __forceinline__ int rot_params(R app, R aqq, R apq, R nu, int rule, R &t, R &s, R &tau)
 {
+    // Branch-free form (no warp divergence on the K3 critical path).  It is
+    // bit-identical to the literal reading: for mu < 0, 1/(mu - r) is exactly
+    // -(1/(|mu| + r)) (the negation is exact), the sign follows "mu >= 0"
+    // (so mu = -0 takes the + branch like the literal code), and for |mu| >=
+    // 2^26 (2^12 fp32) 0.5/mu == sgn * (1/(2|mu|)) (2|mu| is exact and both
+    // are the correctly rounded 1/(2 mu)).
     bool skip;
     if (rule == 1) {
         R g = app * aqq;
@@ -49,19 +55,20 @@ __device__ __forceinline__ int rot_params(R app, R aqq, R apq, R nu, int rule, R
     } else {
         skip = absR(apq) <= nu * minR(absR(app), absR(aqq));
     }
-    if (skip) { t = R(0); s = R(0); tau = R(0); return 0; }
-    R mu = divR(aqq - app, R(2) * apq);
-    R tt;
-    if (absR(mu) < Prec<R>::mu_big) {
-        R r = sqrtR(fmaR(mu, mu, R(1)));
-        tt = (mu >= R(0)) ? divR(R(1), mu + r) : divR(R(1), mu - r);
-    } else {
-        tt = divR(R(0.5), mu);
-    }
-    R c = divR(R(1), sqrtR(fmaR(tt, tt, R(1))));
-    R ss = tt * c;
-    t = tt; s = ss; tau = divR(ss, R(1) + c);
-    return 1;
+    const R den = skip ? R(1) : R(2) * apq;
+    const R mu = divR(aqq - app, den);
+    const R amu = absR(mu);
+    const R r = sqrtR(fmaR(mu, mu, R(1)));                    // inf for huge mu: not selected
+    const R d = (amu < Prec<R>::mu_big) ? amu + r : R(2) * amu;
+    const R sgn = (mu >= R(0)) ? R(1) : R(-1);
+    const R tt = sgn * divR(R(1), d);
+    const R c = divR(R(1), sqrtR(fmaR(tt, tt, R(1))));
+    const R ss = tt * c;
+    const R uu = divR(ss, R(1) + c);
+    t = skip ? R(0) : tt;
+    s = skip ? R(0) : ss;
+    tau = skip ? R(0) : uu;
+    return skip ? 0 : 1;
 }
 
 // J applied to an (x at index p, y at index q) pair: (x,y) <- (c x - s y, s x + c y).
