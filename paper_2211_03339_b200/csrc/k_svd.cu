@@ -78,36 +78,34 @@ __global__ void __launch_bounds__(NT) k_gram(const R *__restrict__ C, int64_t ld
 }
 
 template <typename R>
-__global__ void __launch_bounds__(NT) k_svd_solve(const double *__restrict__ Gpart, int splits, Sched S, int Rb,
-                                                  R nu, R *__restrict__ Ubuf, unsigned long long *__restrict__ cnt)
+__global__ void __launch_bounds__(NTW) k_svd_solve(const double *__restrict__ Gpart, int splits, Sched S, int Rb,
+                                                   R nu, R *__restrict__ Ubuf, unsigned long long *__restrict__ cnt)
 {
     constexpr int LD = Lay<R>::LD;
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    R *D = (R *)smem_raw;
-    R *U = D + TW * LD;
-    __shared__ InnerShared sh;
-    __shared__ InnerParams<R> pr;
+    R *D0 = (R *)smem_raw;
+    R *D1 = D0 + TW * LD;
+    R *U = D1 + TW * LD;
+    __shared__ unsigned nrot;
+    __shared__ WideParams<R> P[2];
     const int a = blockIdx.x;
     const int mb = S.nb >> 1;
     const int2 bp = S.bsched[Rb * mb + a];
     const double *G = Gpart + (size_t)a * splits * TW * TW;
-    for (int e = threadIdx.x; e < TW * TW; e += NT) {
+    for (int e = threadIdx.x; e < TW * TW; e += NTW) {
         const int li = e & (TW - 1), lj = e >> 6;
+        // the Gram block, exactly symmetric: both triangles from the (li <= lj) partial sums
+        const int i0 = li < lj ? li : lj, j0 = li < lj ? lj : li;
         double g = 0.0;
-        for (int z = 0; z < splits; ++z) g += G[(size_t)z * TW * TW + e];   // fixed order
-        D[li + lj * LD] = (R)g;
+        for (int z = 0; z < splits; ++z) g += G[(size_t)z * TW * TW + i0 + j0 * TW];   // fixed order
+        D0[li + lj * LD] = (R)g;
         U[li + lj * LD] = (li == lj) ? R(1) : R(0);
     }
-    // exact symmetry of the Gram block (the partial sums are computed per entry)
     __syncthreads();
-    for (int e = threadIdx.x; e < TW * TW; e += NT) {
-        const int li = e & (TW - 1), lj = e >> 6;
-        if (li < lj) D[lj + li * LD] = D[li + lj * LD];
-    }
-    const unsigned nrot = inner_rounds<R>(D, U, bp, Rb == 0, S.lsched, nu, /*rule=*/1, sh, pr);
+    inner_rounds_wide<R>(D0, D1, U, bp, Rb == 0, S.lsched, nu, /*rule=*/1, P, &nrot);
     R *Ua = Ubuf + (size_t)a * TW * TW;
     R *UaT = Ubuf + (size_t)mb * TW * TW + (size_t)a * TW * TW;   // U^T: operand of the fp32 apply
-    for (int e = threadIdx.x; e < TW * TW; e += NT) {
+    for (int e = threadIdx.x; e < TW * TW; e += NTW) {
         const int li = e & (TW - 1), lj = e >> 6;
         Ua[li + lj * TW] = U[li + lj * LD];
         if (sizeof(R) == 4) UaT[li + lj * TW] = U[lj + li * LD];
@@ -218,7 +216,7 @@ static mpj_status svd_block_sweep(SvdPlan &p, R *C, R *V, const DevSched &ds, R 
     Sched S;
     S.bsched = ds.bsched; S.lsched = ds.lsched; S.b = ds.b; S.nb = ds.nb; S.np = ds.np;
     constexpr int LD = Lay<R>::LD;
-    const size_t sm_x = TW * LD * sizeof(R), sm_du = 2 * TW * LD * sizeof(R);
+    const size_t sm_x = TW * LD * sizeof(R), sm_du = 3 * TW * LD * sizeof(R);
     MPJ_CK(cudaFuncSetAttribute(k_gram<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_x));
     MPJ_CK(cudaFuncSetAttribute(k_svd_solve<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_du));
     const bool prof = prof_on();
@@ -227,7 +225,7 @@ static mpj_status svd_block_sweep(SvdPlan &p, R *C, R *V, const DevSched &ds, R 
         if (prof) prof_mark(ng, st, true);
         k_gram<R><<<dim3(p.mb, p.splits), NT, sm_x, st>>>(C, p.m, (int)p.m, S, Rb, p.kc, p.Gpart, p.splits);
         if (prof) prof_mark(ng, st, false);
-        k_svd_solve<R><<<p.mb, NT, sm_du, st>>>(p.Gpart, p.splits, S, Rb, nu, (R *)p.Ubuf, p.cnt);
+        k_svd_solve<R><<<p.mb, NTW, sm_du, st>>>(p.Gpart, p.splits, S, Rb, nu, (R *)p.Ubuf, p.cnt);
         count_launch(2);
         launch_block_apply_cols<R>(C, p.m, (int)p.m, ds, Rb, (const R *)p.Ubuf, st);
         launch_block_apply_cols<R>(V, p.np, p.np, ds, Rb, (const R *)p.Ubuf, st);
