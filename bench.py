@@ -336,7 +336,6 @@ def run_svd(args):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": False,
             "dtype": "f64", "data": "synthetic",
             "config": {"workload": f"Example 3 (P:1112) mode 3 kappa=1e3, {m} x {n} (BASELINE config 5a)"},
-            "step_ms": step_ms, "lib_t_total": [r.t_total for r in reports],
             "sweeps": rep.sweeps, "sweeps_low": rep.sweeps_low,
             "ju": rep.rotations / (n * (n - 1) / 2), "ju_low": rep.rotations_low / (n * (n - 1) / 2),
             "stage_seconds": {"low_fp32": rep.t_low, "orth": rep.t_orth, "precond": rep.t_precond,
