@@ -22,7 +22,6 @@
 
 #include <algorithm>
 #include <cstdlib>
-#include <string>
 
 namespace mpj {
 
@@ -99,9 +98,8 @@ __device__ __forceinline__ void decode_upper(int idx, int &a, int &c)
     a = idx - c * (c - 1) / 2;
 }
 
-// issue the loads of work item `item` into stage buffers (X, Ua, Uc);
-// KMAJ: the fp32 FFMA outer-product path's k-major operands (U^T, X^T)
-template <typename R, bool KMAJ = (sizeof(R) == 4)>
+// issue the loads of work item `item` into stage buffers (X, Ua, Uc)
+template <typename R>
 __device__ __forceinline__ void issue_item(const ApplyArgs &p, int item, R *X, R *Ua, R *Uc)
 {
     constexpr int LD = Lay<R>::LD, EPC = 16 / sizeof(R), CPC = TW / EPC;   // elements / chunks per column
@@ -110,7 +108,7 @@ __device__ __forceinline__ void issue_item(const ApplyArgs &p, int item, R *X, R
     const R *Ub = (const R *)p.Ubuf;
     // fp32 uses the k-major operands U^T (second half of Ubuf) and, for T
     // tiles, X^T = T(P_c, P_a) (T is exactly symmetric)
-    const bool f32 = KMAJ;
+    const bool f32 = sizeof(R) == 4;
     const R *UbO = f32 ? Ub + (size_t)mb * TW * TW : Ub;
     if (item < p.ntT) {
         int a, c;
@@ -231,77 +229,6 @@ __global__ void __launch_bounds__(NT) k_block_apply(ApplyArgs p)
     cp_wait0();
 }
 
-// fp32 apply on the tensor pipe: every 64^3 product as 6 BF16 products of the
-// exact 3-way bf16 split (reading R22).  Operands natural (column-major U, X);
-// one stage, 2 CTAs per SM (107.5 KB shared memory each).
-__global__ void __launch_bounds__(NT) k_block_apply_bf(ApplyArgs p)
-{
-    constexpr int LD = Lay<float>::LD, EPC = 4, CPC = TW / EPC;
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    float *x = (float *)smem_raw;
-    float *ua = x + TW * LD, *uc = ua + TW * LD;
-    __nv_bfloat16 *P1 = (__nv_bfloat16 *)(uc + TW * LD);
-    __nv_bfloat16 *P2 = P1 + 3 * PLANE;
-    const int total = p.ntT + p.ntV;
-    const int mb = p.S.nb >> 1;
-    const int2 *bsr = p.S.bsched + p.Rb * mb;
-    for (int item = blockIdx.x; item < total; item += gridDim.x) {
-        issue_item<float, false>(p, item, x, ua, uc);
-        cp_commit();
-        cp_wait0();
-        __syncthreads();
-        AccBF acc;
-        if (item < p.ntT) {
-            int a, c;
-            decode_upper(item, a, c);
-            const int2 pa = bsr[a], pc = bsr[c];
-            to_planes(ua, LD, 1, P1);                 // A = U_a^T: A(i, k) = U_a(k, i)
-            to_planes(x, LD, 1, P2);                  // B = X:     B(k, j) = X(k, j)
-            __syncthreads();
-            tile_mm_bf16x6(P1, P2, acc);              // Y = U_a^T X
-            __syncthreads();
-            acc.each([&](int i, int j, float v) {     // Y -> planes (A of the second product)
-                __nv_bfloat16 h0, h1, h2;
-                split3(v, h0, h1, h2);
-                P1[i * PL + j] = h0; P1[PLANE + i * PL + j] = h1; P1[2 * PLANE + i * PL + j] = h2;
-            });
-            to_planes(uc, LD, 1, P2);                 // B = U_c
-            __syncthreads();
-            tile_mm_bf16x6(P1, P2, acc);              // W = Y U_c
-            __syncthreads();
-            acc.each([&](int i, int j, float v) { x[i + j * LD] = v; ua[j + i * LD] = v; });
-            __syncthreads();
-            float *T = (float *)p.T;
-            for (int e = threadIdx.x; e < TW * CPC; e += NT) {
-                const int lj = e / CPC, li = (e - lj * CPC) * EPC;
-                *(int4 *)(T + gidx(pa, li) + (int64_t)gidx(pc, lj) * p.ldt) = *(const int4 *)(x + li + lj * LD);
-                *(int4 *)(T + gidx(pc, li) + (int64_t)gidx(pa, lj) * p.ldt) = *(const int4 *)(ua + li + lj * LD);
-            }
-        } else {
-            const int idx = item - p.ntT, c = idx % mb, r0 = (idx / mb) * TW;
-            const int2 pc = bsr[c];
-            to_planes(x, 1, LD, P1);                  // A = X: A(i, k) = X(i, k)
-            to_planes(uc, LD, 1, P2);                 // B = U_c
-            __syncthreads();
-            tile_mm_bf16x6(P1, P2, acc);
-            __syncthreads();
-            acc.each([&](int i, int j, float v) { x[i + j * LD] = v; });
-            __syncthreads();
-            float *M = (float *)p.M;
-            for (int e = threadIdx.x; e < TW * CPC; e += NT) {
-                const int lj = e / CPC, li = (e - lj * CPC) * EPC;
-                float *dst = M + (int64_t)(r0 + li) + (int64_t)gidx(pc, lj) * p.ldm;
-                if (r0 + li + EPC <= p.mrows) {
-                    *(int4 *)dst = *(const int4 *)(x + li + lj * LD);
-                } else {
-                    for (int q = 0; q < EPC && r0 + li + q < p.mrows; ++q) dst[q] = x[li + q + lj * LD];
-                }
-            }
-        }
-        __syncthreads();
-    }
-}
-
 }  // namespace
 
 template <typename R>
@@ -354,37 +281,9 @@ static void launch_apply_s(const ApplyArgs &p, cudaStream_t st)
     count_launch();
 }
 
-static bool fp32_apply_bf16()
-{
-    static int v = -1;
-    if (v < 0) {
-        const char *e = getenv("MPJ_FP32_APPLY");
-        v = (e && std::string(e) == "ffma") ? 0 : 1;
-    }
-    return v == 1;
-}
-
-static void launch_apply_bf(const ApplyArgs &p, cudaStream_t st)
-{
-    const size_t smem = 3 * TW * Lay<float>::LD * sizeof(float) + 2 * 3 * PLANE * sizeof(__nv_bfloat16);
-    static bool attr = false;
-    static int per_sm = 0;
-    if (!attr) {
-        MPJ_CK_VOID(cudaFuncSetAttribute(k_block_apply_bf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        MPJ_CK_VOID(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_block_apply_bf, NT, smem));
-        per_sm = std::max(1, per_sm);
-        attr = true;
-    }
-    const int total = p.ntT + p.ntV;
-    const int grid = std::max(1, std::min(total, sm_count() * per_sm));
-    k_block_apply_bf<<<grid, NT, smem, st>>>(p);
-    count_launch();
-}
-
 template <typename R>
 static void launch_apply(const ApplyArgs &p, cudaStream_t st)
 {
-    if (sizeof(R) == 4 && fp32_apply_bf16()) { launch_apply_bf(p, st); return; }
     if (apply_stages() == 2) launch_apply_s<R, 2>(p, st);
     else launch_apply_s<R, 1>(p, st);
 }

@@ -6,8 +6,6 @@
 #pragma once
 #include "mpj_device.cuh"
 
-#include <cuda_bf16.h>
-
 namespace mpj {
 namespace blk {
 
@@ -452,117 +450,6 @@ __device__ __forceinline__ void store_op(const AccOP &acc, float *C, float *CT)
         #pragma unroll
         for (int u = 0; u < 4; ++u)
             *(float4 *)(CT + c + (r + u) * LD) = make_float4(acc.v[u][0], acc.v[u][1], acc.v[u][2], acc.v[u][3]);
-    }
-}
-
-// ---------------------------------------------------------------------------
-// fp32 products as 6 BF16 tensor-core products (reading R22): x = x0 + x1 + x2
-// with x0 = bf16(x), x1 = bf16(x - x0), x2 = bf16(x - x0 - x1) represents
-// binary32 x to within 2^-25 |x| (8 + 8 + 8 significand bits); A B ~
-// sum_{i + j <= 2} A_i B_j (the dropped A_1 B_2 + A_2 B_1 + A_2 B_2 are
-// O(2^-24) relative); every bf16 x bf16 product is exact in the fp32
-// accumulator of mma.sync.m16n8k16.  Operands live in shared memory as three
-// bf16 "planes", each stored k-contiguous (element (r, k) at r * PL + k) so
-// that every fragment register is one conflict-free 32-bit load (PL = 72).
-// ---------------------------------------------------------------------------
-constexpr int PL = 72;                   // plane row stride (bf16 elements)
-constexpr int PLANE = TW * PL;           // bf16 elements per plane
-
-__device__ __forceinline__ void split3(float x, __nv_bfloat16 &h0, __nv_bfloat16 &h1, __nv_bfloat16 &h2)
-{
-    h0 = __float2bfloat16_rn(x);
-    const float r1 = x - __bfloat162float(h0);
-    h1 = __float2bfloat16_rn(r1);
-    const float r2 = r1 - __bfloat162float(h1);
-    h2 = __float2bfloat16_rn(r2);
-}
-
-// planes[p][r * PL + k] = split_p(src(r, k)); src(r, k) = src[r * rs + k * ks]
-__device__ __forceinline__ void to_planes(const float *src, int rs, int ks, __nv_bfloat16 *planes)
-{
-    for (int e = threadIdx.x; e < TW * TW; e += NT) {
-        const int r = e >> 6, k = e & (TW - 1);
-        __nv_bfloat16 h0, h1, h2;
-        split3(src[r * rs + k * ks], h0, h1, h2);
-        planes[r * PL + k] = h0;
-        planes[PLANE + r * PL + k] = h1;
-        planes[2 * PLANE + r * PL + k] = h2;
-    }
-}
-
-__device__ __forceinline__ void mma_bf16(float (&d)[4], const unsigned (&a)[4], unsigned b0, unsigned b1)
-{
-    asm volatile("mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
-                 "{%0,%1,%2,%3};\n"
-                 : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
-                 : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
-}
-
-// C (64 x 64, accumulator fragments) = A B with A given as planes of A(i, k)
-// (row i, k contiguous) and B as planes of B^T, i.e. B(k, j) at j * PL + k.
-// 8 warps as 2 x 4, warp tile 32 x 16 (2 m16 x 2 n8 fragments).
-struct AccBF {
-    float v[2][2][4];
-    template <typename F> __device__ __forceinline__ void each(F f) const
-    {
-        const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
-        const int r0 = (warp >> 2) * 32 + g, c0 = (warp & 3) * 16 + 2 * t;
-        #pragma unroll
-        for (int mi = 0; mi < 2; ++mi)
-            #pragma unroll
-            for (int ni = 0; ni < 2; ++ni) {
-                const int r = r0 + mi * 16, c = c0 + ni * 8;
-                f(r, c, v[mi][ni][0]);
-                f(r, c + 1, v[mi][ni][1]);
-                f(r + 8, c, v[mi][ni][2]);
-                f(r + 8, c + 1, v[mi][ni][3]);
-            }
-    }
-};
-
-__device__ __forceinline__ void tile_mm_bf16x6(const __nv_bfloat16 *Ap, const __nv_bfloat16 *Bp, AccBF &acc)
-{
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
-    const int rb = (warp >> 2) * 32 + g, cb = (warp & 3) * 16 + g;
-    #pragma unroll
-    for (int a = 0; a < 2; ++a)
-        #pragma unroll
-        for (int b = 0; b < 2; ++b)
-            #pragma unroll
-            for (int c = 0; c < 4; ++c) acc.v[a][b][c] = 0.f;
-    #pragma unroll
-    for (int k0 = 0; k0 < TW; k0 += 16) {
-        unsigned af[3][2][4], bf[3][2][2];
-        #pragma unroll
-        for (int p = 0; p < 3; ++p) {
-            const __nv_bfloat16 *A = Ap + p * PLANE, *B = Bp + p * PLANE;
-            #pragma unroll
-            for (int mi = 0; mi < 2; ++mi) {
-                const int r = rb + mi * 16;
-                af[p][mi][0] = *(const unsigned *)(A + r * PL + k0 + 2 * t);
-                af[p][mi][1] = *(const unsigned *)(A + (r + 8) * PL + k0 + 2 * t);
-                af[p][mi][2] = *(const unsigned *)(A + r * PL + k0 + 2 * t + 8);
-                af[p][mi][3] = *(const unsigned *)(A + (r + 8) * PL + k0 + 2 * t + 8);
-            }
-            #pragma unroll
-            for (int ni = 0; ni < 2; ++ni) {
-                const int c = cb + ni * 8;
-                bf[p][ni][0] = *(const unsigned *)(B + c * PL + k0 + 2 * t);
-                bf[p][ni][1] = *(const unsigned *)(B + c * PL + k0 + 2 * t + 8);
-            }
-        }
-        #pragma unroll
-        for (int mi = 0; mi < 2; ++mi)
-            #pragma unroll
-            for (int ni = 0; ni < 2; ++ni) {
-                // smallest terms first
-                mma_bf16(acc.v[mi][ni], af[2][mi], bf[0][ni][0], bf[0][ni][1]);
-                mma_bf16(acc.v[mi][ni], af[1][mi], bf[1][ni][0], bf[1][ni][1]);
-                mma_bf16(acc.v[mi][ni], af[0][mi], bf[2][ni][0], bf[2][ni][1]);
-                mma_bf16(acc.v[mi][ni], af[1][mi], bf[0][ni][0], bf[0][ni][1]);
-                mma_bf16(acc.v[mi][ni], af[0][mi], bf[1][ni][0], bf[1][ni][1]);
-                mma_bf16(acc.v[mi][ni], af[0][mi], bf[0][ni][0], bf[0][ni][1]);
-            }
     }
 }
 
