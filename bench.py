@@ -443,6 +443,10 @@ def main():
         sec, cnt = mpj.profile_get(name)
         if cnt:
             kernels[name] = {"seconds_per_step": sec / args.steps, "launches": cnt, "avg_ms": 1e3 * sec / cnt}
+            items = mpj.profile_get(name + ".items")[1]
+            if items:
+                sk = mpj.profile_get(name + ".skipped_t")[1] + mpj.profile_get(name + ".skipped_v")[1]
+                kernels[name]["items_skipped_frac"] = sk / items
     roof = None
     if kernels:
         dom = max(kernels, key=lambda k: kernels[k]["seconds_per_step"])
@@ -454,6 +458,14 @@ def main():
                 mbl = mb // ws
                 fl = mbl * (mb - 1) * 2 * 2 * 64 ** 3 + (rep.n_padded // 64) * mbl * 2 * 64 ** 3
                 by = (mbl * (mb - 1) * 2 + (rep.n_padded // 64) * mbl * 2) * 64 * 64 * (8 if is64 else 4)
+            # tiles of identity rotation blocks are skipped (exactly unchanged):
+            # count only the work done, averaged over the launches
+            nl = kernels[dom]["launches"]
+            skt = mpj.profile_get(dom + ".skipped_t")[1]
+            skv = mpj.profile_get(dom + ".skipped_v")[1]
+            if skt or skv:
+                fl = fl - (skt * 2 * 2 * 64 ** 3 + skv * 2 * 64 ** 3) / nl
+                by = by - (skt * 3 + skv * 2) * 64 * 64 * (8 if is64 else 4) / nl
             peak = pk["dmma_tflops"] if is64 else pk["ffma_tflops"]
             traffic = None
             tp = os.path.join(ROOT, "profiles", "r01_traffic.json")

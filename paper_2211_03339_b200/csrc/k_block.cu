@@ -22,6 +22,8 @@
 
 #include <algorithm>
 #include <cstdlib>
+#include <string>
+#include <vector>
 
 namespace mpj {
 
@@ -35,9 +37,10 @@ using namespace blk;
 template <typename R>
 __global__ void __launch_bounds__(NTW) k_block_solve(R *__restrict__ T, int64_t ldt, Sched S, int Rb, R nu,
                                                      int rule, R *__restrict__ Ubuf,
-                                                     unsigned long long *__restrict__ cnt)
+                                                     unsigned long long *__restrict__ cnt,
+                                                     int *__restrict__ uid, int *__restrict__ nid)
 {
-    constexpr int LD = Lay<R>::LD;
+    constexpr int LD = LayK<R>::LD;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     R *D0 = (R *)smem_raw;          // 64 x LD, column-major (double-buffered)
     R *D1 = D0 + TW * LD;
@@ -62,7 +65,11 @@ __global__ void __launch_bounds__(NTW) k_block_solve(R *__restrict__ T, int64_t 
         Uk[li + lj * TW] = U[li + lj * LD];
         if (sizeof(R) == 4) UkT[li + lj * TW] = U[lj + li * LD];
     }
-    if (threadIdx.x == 0 && nrot) atomicAdd(cnt, (unsigned long long)nrot);
+    if (threadIdx.x == 0) {
+        if (nrot) atomicAdd(cnt, (unsigned long long)nrot);
+        uid[k] = nrot == 0;   // no rotation: U_k is exactly I (K4 may skip it)
+        if (nrot == 0) atomicAdd(nid, 1);
+    }
 }
 
 // ---------------------------------------------------------------------------
@@ -87,19 +94,21 @@ struct ApplyArgs {
     void *M; int64_t ldm; int mrows;
     Sched S; int Rb;
     const void *Ubuf;
+    const int *uid;       // per block pair: U is exactly I (nullptr: never skip)
+    const int *nid;       // number of such block pairs this block round
     int ntT, ntV;
 };
 
 __device__ __forceinline__ void decode_upper(int idx, int &a, int &c)
 {
-    c = (int)((1.0 + sqrt(1.0 + 8.0 * idx)) * 0.5);
+    c = (int)((1.0f + sqrtf(1.0f + 8.0f * (float)idx)) * 0.5f);   // fp32 estimate, exact after the fix-ups
     while (c * (c - 1) / 2 > idx) --c;
     while ((c + 1) * c / 2 <= idx) ++c;
     a = idx - c * (c - 1) / 2;
 }
 
 // issue the loads of work item `item` into stage buffers (X, Ua, Uc)
-template <typename R>
+template <typename R, int NTH = NT>
 __device__ __forceinline__ void issue_item(const ApplyArgs &p, int item, R *X, R *Ua, R *Uc)
 {
     constexpr int LD = Lay<R>::LD, EPC = 16 / sizeof(R), CPC = TW / EPC;   // elements / chunks per column
@@ -116,7 +125,7 @@ __device__ __forceinline__ void issue_item(const ApplyArgs &p, int item, R *X, R
         const int2 pa = bsr[a], pc = bsr[c];
         const int2 rr = f32 ? pc : pa, cc = f32 ? pa : pc;
         const R *T = (const R *)p.T;
-        for (int e = threadIdx.x; e < TW * CPC; e += NT) {
+        for (int e = threadIdx.x; e < TW * CPC; e += NTH) {
             const int lj = e / CPC, li = (e - lj * CPC) * EPC;
             cp16(X + li + lj * LD, T + gidx(rr, li) + (int64_t)gidx(cc, lj) * p.ldt, 16);
             cp16(Ua + li + lj * LD, UbO + (size_t)a * TW * TW + li + lj * TW, 16);
@@ -126,7 +135,7 @@ __device__ __forceinline__ void issue_item(const ApplyArgs &p, int item, R *X, R
         const int idx = item - p.ntT, c = idx % mb, r0 = (idx / mb) * TW;
         const int2 pc = bsr[c];
         const R *M = (const R *)p.M;
-        for (int e = threadIdx.x; e < TW * CPC; e += NT) {
+        for (int e = threadIdx.x; e < TW * CPC; e += NTH) {
             const int lj = e / CPC, li = (e - lj * CPC) * EPC;
             const int rem = p.mrows - (r0 + li);
             const int bytes = rem >= EPC ? 16 : (rem > 0 ? rem * (int)sizeof(R) : 0);
@@ -135,6 +144,20 @@ __device__ __forceinline__ void issue_item(const ApplyArgs &p, int item, R *X, R
             cp16(Uc + li + lj * LD, UbO + (size_t)c * TW * TW + li + lj * TW, 16);
         }
     }
+}
+
+// An item whose rotation blocks are all exactly I (no rotation in K3: U_a =
+// U_c = I for a T tile, U_c = I for an M tile) leaves its tile unchanged and is
+// skipped -- exact, and in the last fp64 sweeps nearly every item.
+__device__ __forceinline__ bool item_identity(const ApplyArgs &p, int item, int mb)
+{
+    if (!p.uid) return false;
+    if (item < p.ntT) {
+        int a, c;
+        decode_upper(item, a, c);
+        return p.uid[a] && p.uid[c];
+    }
+    return p.uid[(item - p.ntT) % mb] != 0;
 }
 
 // STAGES = 2: one CTA per SM prefetches item i+1 while computing item i;
@@ -148,15 +171,20 @@ __global__ void __launch_bounds__(NT) k_block_apply(ApplyArgs p)
     const int total = p.ntT + p.ntV;
     const int mb = p.S.nb >> 1;
     const int2 *bsr = p.S.bsched + p.Rb * mb;
-    int item = blockIdx.x;
+    const bool skips = p.uid && *p.nid > 0;
+    auto advance = [&](int i) {
+        while (skips && i < total && item_identity(p, i, mb)) i += gridDim.x;
+        return i;
+    };
+    int item = advance(blockIdx.x);
     if (STAGES == 2) {
         if (item < total) issue_item<R>(p, item, buf, buf + TW * LD, buf + 2 * TW * LD);
         cp_commit();
     }
-    for (int it = 0; item < total; ++it, item += gridDim.x) {
+    for (int it = 0; item < total; ++it, item = advance(item + gridDim.x)) {
         const int s = STAGES == 2 ? (it & 1) : 0;
         if (STAGES == 2) {
-            const int next = item + gridDim.x;
+            const int next = advance(item + gridDim.x);
             R *nb = buf + (size_t)(3 * (s ^ 1)) * TW * LD;
             if (next < total) issue_item<R>(p, next, nb, nb + TW * LD, nb + 2 * TW * LD);
             cp_commit();
@@ -229,6 +257,118 @@ __global__ void __launch_bounds__(NT) k_block_apply(ApplyArgs p)
     cp_wait0();
 }
 
+// fp32 apply with 8 x 4 register tiles: 128 threads per 64 x 64 tile, thread
+// (tx, ty) = (tid & 7, tid >> 3) owns rows 4tx..4tx+3, 32+4tx..32+4tx+3 (so
+// that the 8 lanes' vectors are 128 contiguous bytes, conflict-free) and
+// columns 4ty..4ty+3;
+// 4 CTAs per SM.  Per k and warp: two 128-bit LDS of A (8 distinct vectors,
+// one wavefront each) and one of B (4 distinct, one wavefront) feed 32 FFMA --
+// half the shared-memory wavefronts per FFMA of the 4 x 4 tile (AccOP), whose
+// K4 is bound by the shared-memory pipe (ncu: L1 85%, FMA 49%).
+constexpr int NT128 = 128;
+
+struct Acc84 {
+    float v[8][4];
+};
+
+__device__ __forceinline__ void tile_op84(const float *A, const float *B, Acc84 &acc)
+{
+    constexpr int LD = Lay<float>::LD;
+    const int ra = 4 * (threadIdx.x & 7), cb = 4 * (threadIdx.x >> 3);
+    #pragma unroll
+    for (int u = 0; u < 8; ++u)
+        #pragma unroll
+        for (int w = 0; w < 4; ++w) acc.v[u][w] = 0.f;
+    float4 a0 = *(const float4 *)(A + ra), a1 = *(const float4 *)(A + ra + 32), b = *(const float4 *)(B + cb);
+    #pragma unroll 4
+    for (int k = 0; k < TW; ++k) {
+        const float av[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w}, bv[4] = {b.x, b.y, b.z, b.w};
+        if (k + 1 < TW) {                         // register prefetch of the next k
+            a0 = *(const float4 *)(A + ra + (k + 1) * LD);
+            a1 = *(const float4 *)(A + ra + 32 + (k + 1) * LD);
+            b = *(const float4 *)(B + cb + (k + 1) * LD);
+        }
+        #pragma unroll
+        for (int u = 0; u < 8; ++u)
+            #pragma unroll
+            for (int w = 0; w < 4; ++w) acc.v[u][w] = __fmaf_rn(av[u], bv[w], acc.v[u][w]);
+    }
+}
+
+__device__ __forceinline__ void store_op84(const Acc84 &acc, float *C, float *CT)
+{
+    constexpr int LD = Lay<float>::LD;
+    const int r = 4 * (threadIdx.x & 7), c = 4 * (threadIdx.x >> 3);
+    #pragma unroll
+    for (int w = 0; w < 4; ++w) {
+        *(float4 *)(C + r + (c + w) * LD) = make_float4(acc.v[0][w], acc.v[1][w], acc.v[2][w], acc.v[3][w]);
+        *(float4 *)(C + r + 32 + (c + w) * LD) = make_float4(acc.v[4][w], acc.v[5][w], acc.v[6][w], acc.v[7][w]);
+    }
+    if (CT) {
+        #pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const int row = r + (u & 3) + (u >> 2) * 32;
+            *(float4 *)(CT + c + row * LD) = make_float4(acc.v[u][0], acc.v[u][1], acc.v[u][2], acc.v[u][3]);
+        }
+    }
+}
+
+__global__ void __launch_bounds__(NT128) k_block_apply_f32w(ApplyArgs p)
+{
+    constexpr int LD = Lay<float>::LD, EPC = 4, CPC = TW / EPC;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    float *x = (float *)smem_raw, *ua = x + TW * LD, *uc = ua + TW * LD;
+    const int total = p.ntT + p.ntV;
+    const int mb = p.S.nb >> 1;
+    const int2 *bsr = p.S.bsched + p.Rb * mb;
+    const bool skips = p.uid && *p.nid > 0;
+    Acc84 acc;
+    for (int item = blockIdx.x; item < total; item += gridDim.x) {
+        if (skips && item_identity(p, item, mb)) continue;
+        issue_item<float, NT128>(p, item, x, ua, uc);
+        cp_commit();
+        cp_wait0();
+        __syncthreads();
+        if (item < p.ntT) {
+            int a, c;
+            decode_upper(item, a, c);
+            const int2 pa = bsr[a], pc = bsr[c];
+            tile_op84(ua, x, acc);                      // Y = U_a^T X  (U_a^T, X^T k-major)
+            __syncthreads();
+            store_op84(acc, x, nullptr);
+            __syncthreads();
+            tile_op84(x, uc, acc);                      // W = Y U_c
+            __syncthreads();
+            store_op84(acc, x, ua);                     // W and W^T
+            __syncthreads();
+            float *T = (float *)p.T;
+            for (int e = threadIdx.x; e < TW * CPC; e += NT128) {
+                const int lj = e / CPC, li = (e - lj * CPC) * EPC;
+                *(int4 *)(T + gidx(pa, li) + (int64_t)gidx(pc, lj) * p.ldt) = *(const int4 *)(x + li + lj * LD);
+                *(int4 *)(T + gidx(pc, li) + (int64_t)gidx(pa, lj) * p.ldt) = *(const int4 *)(ua + li + lj * LD);
+            }
+        } else {
+            const int idx = item - p.ntT, c = idx % mb, r0 = (idx / mb) * TW;
+            const int2 pc = bsr[c];
+            tile_op84(x, uc, acc);                      // W = X U_c
+            __syncthreads();
+            store_op84(acc, x, nullptr);
+            __syncthreads();
+            float *M = (float *)p.M;
+            for (int e = threadIdx.x; e < TW * CPC; e += NT128) {
+                const int lj = e / CPC, li = (e - lj * CPC) * EPC;
+                float *dst = M + (int64_t)(r0 + li) + (int64_t)gidx(pc, lj) * p.ldm;
+                if (r0 + li + EPC <= p.mrows) {
+                    *(int4 *)dst = *(const int4 *)(x + li + lj * LD);
+                } else {
+                    for (int q = 0; q < EPC && r0 + li + q < p.mrows; ++q) dst[q] = x[li + q + lj * LD];
+                }
+            }
+        }
+        __syncthreads();
+    }
+}
+
 }  // namespace
 
 template <typename R>
@@ -236,7 +376,8 @@ size_t block_scratch_bytes(int np, int b)
 {
     (void)b;
     const int mb = np / (2 * BW);
-    return 2 * (size_t)mb * TW * TW * sizeof(R);   // U and U^T per block pair
+    // U, U^T, identity flags, identity counts per block round
+    return 2 * (size_t)mb * TW * TW * sizeof(R) + (size_t)(mb + 2 * mb) * sizeof(int);
 }
 
 static int sm_count()
@@ -281,9 +422,37 @@ static void launch_apply_s(const ApplyArgs &p, cudaStream_t st)
     count_launch();
 }
 
+static int fp32_apply_kind()
+{
+    static int v = -1;
+    if (v < 0) {
+        const char *e = getenv("MPJ_FP32_APPLY");
+        v = (e && std::string(e) == "4x4") ? 0 : 1;
+    }
+    return v;
+}
+
+static void launch_apply_f32w(const ApplyArgs &p, cudaStream_t st)
+{
+    const size_t smem = 3 * TW * Lay<float>::LD * sizeof(float);
+    static bool attr = false;
+    static int per_sm = 0;
+    if (!attr) {
+        MPJ_CK_VOID(cudaFuncSetAttribute(k_block_apply_f32w, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        MPJ_CK_VOID(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_block_apply_f32w, NT128, smem));
+        per_sm = std::max(1, per_sm);
+        attr = true;
+    }
+    const int total = p.ntT + p.ntV;
+    const int grid = std::max(1, std::min(total, sm_count() * per_sm));
+    k_block_apply_f32w<<<grid, NT128, smem, st>>>(p);
+    count_launch();
+}
+
 template <typename R>
 static void launch_apply(const ApplyArgs &p, cudaStream_t st)
 {
+    if (sizeof(R) == 4 && fp32_apply_kind() == 1) { launch_apply_f32w(p, st); return; }
     if (apply_stages() == 2) launch_apply_s<R, 2>(p, st);
     else launch_apply_s<R, 1>(p, st);
 }
@@ -298,7 +467,10 @@ mpj_status block_sweep(R *T, int64_t ldt, R *V, int64_t ldv, int vrows, const De
     S.bsched = ds.bsched; S.lsched = ds.lsched; S.b = ds.b; S.nb = ds.nb; S.np = ds.np;
     const int mb = ds.nb / 2;
     R *Ubuf = (R *)scratch;
-    const size_t sm_solve = 3 * TW * LD * sizeof(R);
+    int *uid = (int *)(Ubuf + 2 * (size_t)mb * TW * TW);
+    int *nid = uid + mb;                         // nb - 1 <= 2 mb block rounds
+    MPJ_CK(cudaMemsetAsync(nid, 0, (size_t)(ds.nb - 1) * sizeof(int), st));
+    const size_t sm_solve = 3 * TW * LayK<R>::LD * sizeof(R);
     static bool attr_done[2] = {false, false};
     const int ti = sizeof(R) == 8 ? 0 : 1;
     if (!attr_done[ti]) {
@@ -306,7 +478,7 @@ mpj_status block_sweep(R *T, int64_t ldt, R *V, int64_t ldv, int vrows, const De
         attr_done[ti] = true;
     }
     ApplyArgs ap;
-    ap.T = T; ap.ldt = ldt; ap.M = V; ap.ldm = ldv; ap.mrows = vrows; ap.S = S; ap.Ubuf = Ubuf;
+    ap.T = T; ap.ldt = ldt; ap.M = V; ap.ldm = ldv; ap.mrows = vrows; ap.S = S; ap.Ubuf = Ubuf; ap.uid = uid;
     ap.ntT = mb * (mb - 1) / 2;
     ap.ntV = ((vrows + TW - 1) / TW) * mb;
     const char *nsolve = sizeof(R) == 8 ? "block_solve_f64" : "block_solve_f32";
@@ -314,12 +486,25 @@ mpj_status block_sweep(R *T, int64_t ldt, R *V, int64_t ldv, int vrows, const De
     const bool prof = prof_on();
     for (int Rb = 0; Rb < ds.nb - 1; ++Rb) {
         if (prof) prof_mark(nsolve, st, true);
-        k_block_solve<R><<<mb, NTW, sm_solve, st>>>(T, ldt, S, Rb, nu, rule, Ubuf, cnt);
+        k_block_solve<R><<<mb, NTW, sm_solve, st>>>(T, ldt, S, Rb, nu, rule, Ubuf, cnt, uid, nid + Rb);
         count_launch();
         if (prof) { prof_mark(nsolve, st, false); prof_mark(napply, st, true); }
         ap.Rb = Rb;
+        ap.nid = nid + Rb;
         launch_apply<R>(ap, st);
         if (prof) prof_mark(napply, st, false);
+    }
+    if (prof) {   // identity-skip statistics (for the algorithmic-flop count of the roofline)
+        std::vector<int> h(ds.nb - 1);
+        MPJ_CK(cudaMemcpyAsync(h.data(), nid, h.size() * sizeof(int), cudaMemcpyDeviceToHost, st));
+        MPJ_CK(cudaStreamSynchronize(st));
+        long long ids = 0, skt = 0, skv = 0;
+        for (int c : h) { ids += c; skt += (long long)c * (c - 1) / 2; skv += (long long)c * ((vrows + TW - 1) / TW); }
+        const std::string base(napply);
+        prof_add(base + ".identity_blocks", ids);
+        prof_add(base + ".items", (long long)(ds.nb - 1) * (ap.ntT + ap.ntV));
+        prof_add(base + ".skipped_t", skt);
+        prof_add(base + ".skipped_v", skv);
     }
     return MPJ_OK;
 }
@@ -333,7 +518,7 @@ void launch_block_apply_cols(R *M, int64_t ld, int rows, const DevSched &ds, int
     Sched S;
     S.bsched = ds.bsched; S.lsched = ds.lsched; S.b = ds.b; S.nb = ds.nb; S.np = ds.np;
     ApplyArgs ap;
-    ap.T = nullptr; ap.ldt = 0; ap.M = M; ap.ldm = ld; ap.mrows = rows; ap.S = S; ap.Rb = Rb; ap.Ubuf = Ubuf;
+    ap.T = nullptr; ap.ldt = 0; ap.M = M; ap.ldm = ld; ap.mrows = rows; ap.S = S; ap.Rb = Rb; ap.Ubuf = Ubuf; ap.uid = nullptr; ap.nid = nullptr;
     ap.ntT = 0;
     ap.ntV = ((rows + TW - 1) / TW) * (ds.nb / 2);
     launch_apply<R>(ap, st);

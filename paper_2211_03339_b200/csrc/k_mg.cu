@@ -52,7 +52,7 @@ __global__ void __launch_bounds__(NTW) k_mg_solve(R *__restrict__ T, int64_t ldt
                                                   int slot0, const int2 *__restrict__ lsched, int intra, R nu,
                                                   int rule, R *__restrict__ Ubuf, unsigned long long *__restrict__ cnt)
 {
-    constexpr int LD = Lay<R>::LD;
+    constexpr int LD = LayK<R>::LD;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     R *D0 = (R *)smem_raw;
     R *D1 = D0 + TW * LD;
@@ -428,7 +428,7 @@ static mpj_status mg_sweep(Group &g, R **Ts, R **Vs, R nu, int rule)
     }
     MPJ_CK(cudaStreamSynchronize(g.st));   // the host vectors above are about to die
     constexpr int LD = Lay<R>::LD;
-    const size_t sm_solve = 3 * TW * LD * sizeof(R), sm_apply = 3 * TW * LD * sizeof(R);
+    const size_t sm_solve = 3 * TW * LayK<R>::LD * sizeof(R), sm_apply = 3 * TW * LD * sizeof(R);
     static bool attr[2] = {false, false};
     if (!attr[sizeof(R) == 8]) {
         MPJ_CK(cudaFuncSetAttribute(k_mg_solve<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_solve));

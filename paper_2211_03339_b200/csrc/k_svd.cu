@@ -81,7 +81,7 @@ template <typename R>
 __global__ void __launch_bounds__(NTW) k_svd_solve(const double *__restrict__ Gpart, int splits, Sched S, int Rb,
                                                    R nu, R *__restrict__ Ubuf, unsigned long long *__restrict__ cnt)
 {
-    constexpr int LD = Lay<R>::LD;
+    constexpr int LD = LayK<R>::LD;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     R *D0 = (R *)smem_raw;
     R *D1 = D0 + TW * LD;
@@ -216,7 +216,7 @@ static mpj_status svd_block_sweep(SvdPlan &p, R *C, R *V, const DevSched &ds, R 
     Sched S;
     S.bsched = ds.bsched; S.lsched = ds.lsched; S.b = ds.b; S.nb = ds.nb; S.np = ds.np;
     constexpr int LD = Lay<R>::LD;
-    const size_t sm_x = TW * LD * sizeof(R), sm_du = 3 * TW * LD * sizeof(R);
+    const size_t sm_x = TW * LD * sizeof(R), sm_du = 3 * TW * LayK<R>::LD * sizeof(R);
     MPJ_CK(cudaFuncSetAttribute(k_gram<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_x));
     MPJ_CK(cudaFuncSetAttribute(k_svd_solve<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_du));
     const bool prof = prof_on();

@@ -18,6 +18,7 @@ void count_launch(long long k = 1);
 bool prof_on();
 void prof_mark(const char *name, cudaStream_t st, bool begin);
 void prof_flush();   // after the stream has been synchronised
+void prof_add(const std::string &name, long long n);   // a counter (launches field only)
 
 #define MPJ_CK(expr)                                                                    \
     do {                                                                                \

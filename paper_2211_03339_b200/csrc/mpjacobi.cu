@@ -76,6 +76,10 @@ void prof_mark(const char *name, cudaStream_t st, bool begin)
         g_ev_pool.push_back(e);
     }
 }
+void prof_add(const std::string &name, long long n)
+{
+    if (g_prof) g_prof_tab[name].n += n;
+}
 void prof_flush()
 {
     for (auto &p : g_pending) {

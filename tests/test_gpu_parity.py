@@ -249,6 +249,34 @@ def test_block_variant_fp32(mpj, orc, n):
     assert np.linalg.norm(Vg.T @ Vg - np.eye(n)) <= 10 * n * UPSILON
 
 
+@pytest.mark.parametrize("n", [300, 448])
+def test_block_variant_identity_skip(mpj, orc, n):
+    """K4 skips tiles whose rotation blocks did no rotation (U exactly I).
+    With nu = 1e-3 the dense 1e-4 background never rotates but is mixed by the
+    few large pairs that do, so a wrongly skipped (or wrongly applied) tile
+    would be off by ~1e-4, far above the 64 n omega rounding tolerance."""
+    rng = np.random.default_rng(n)
+    E = 1e-4 * rng.uniform(-1, 1, (n, n))
+    T0 = np.diag(np.linspace(1.0, 2.0, n)) + 0.5 * (E + E.T)
+    for i, j in ((5, 6), (40, n - 50), (130, 131), (n - 2, n - 1)):
+        T0[i, j] = T0[j, i] = 0.3
+    nA = np.linalg.norm(T0)
+    cfg = mpj.default_config("eig", variant=mpj.VARIANT_BLOCK, block_b=32)
+    ref = orc.jacobi_evd(T0, np.eye(n), b=32, tol=0.0, nu=1e-3, max_sweeps=1)
+    T, V = dev(T0), dev(np.eye(n))
+    r = mpj.jacobi(T, V, tol=0.0, nu=1e-3, max_sweeps=1, cfg=cfg)
+    assert r.rotations == ref.rotations
+    assert 0 < r.rotations < n // 2
+    assert np.max(np.abs(host(T) - ref.T)) <= 64 * n * OMEGA * nA
+    assert np.max(np.abs(host(V) - ref.V)) <= 64 * n * OMEGA
+    # a diagonal matrix: every block is the identity, T and V come back unchanged
+    D = np.diag(np.linspace(1.0, 2.0, n))
+    T, V = dev(D), dev(np.eye(n))
+    r = mpj.jacobi(T, V, tol=0.0, max_sweeps=1, cfg=cfg)
+    assert r.rotations == 0
+    assert np.array_equal(host(T), D) and np.array_equal(host(V), np.eye(n))
+
+
 @pytest.mark.parametrize("n", [512, 1000])
 def test_eig_block_end_to_end(mpj, orc, n):
     A, lam_true = W.example1(n, 1e3, 4, W.seed_for(2, 4, 1e3))
