@@ -189,7 +189,15 @@ __device__ __forceinline__ R diag_after(const R *Dc, const WideParams<R> &P, int
     return i == pk ? fmaR(-P.t[k], apq, Dc[pk + pk * LD]) : fmaR(P.t[k], apq, Dc[qk + qk * LD]);
 }
 
-template <typename R>
+// UREG (cross rounds only): U lives in registers instead of shared memory.
+// Update warp w (1..31) holds rows 2(w-1), 2(w-1)+1 (warps 1, 2 also rows 62,
+// 63) at columns a_k = k and b_k = 32 + (k + s) mod 32 in lane k; pair k of
+// round s rotates exactly these two columns, and b_k(s+1) = b_{k+1}(s), so
+// the bottoms move one lane per round (shuffle).  This removes U's loads,
+// stores and index reads -- about half of a round's shared-memory traffic,
+// which bounds the rounds (tools/k3_trace.cu: the parameter warp's dependent
+// loads queue behind it).  Same arithmetic (rot on (U(r,p), U(r,q))).
+template <typename R, bool UREG>
 __device__ __forceinline__ R *smem_rounds_wide(R *D0, R *D1, R *U, int2 bp, bool intra, int nrounds,
                                                const int2 *__restrict__ lsched, R nu, int rule,
                                                WideParams<R> (&PP)[2], unsigned &cnt)
@@ -211,11 +219,23 @@ __device__ __forceinline__ R *smem_rounds_wide(R *D0, R *D1, R *U, int2 bp, bool
         } else if (w < BW * (BW - 1) / 2 + BW) {
             tk = w - BW * (BW - 1) / 2; tl = -1;
         }
-        #pragma unroll
-        for (int j = 0; j < 3; ++j) {
-            const int e = w + j * NW;
-            if (e < BW * TW) { ur[j] = e & (TW - 1); uk[j] = e >> 6; }
+        if (!UREG) {
+            #pragma unroll
+            for (int j = 0; j < 3; ++j) {
+                const int e = w + j * NW;
+                if (e < BW * TW) { ur[j] = e & (TW - 1); uk[j] = e >> 6; }
+            }
         }
+    }
+    // UREG: rows of U in registers (update warps only)
+    const bool flip = bp.x > bp.y;          // cross pair k: p = b_k if the bottom block comes first
+    const int nrow = (warp == 1 || warp == 2) ? 3 : (warp > 0 ? 2 : 0);
+    const int urow[3] = {2 * (warp - 1), 2 * (warp - 1) + 1, 62 + (warp - 1)};
+    R ua[3] = {R(0), R(0), R(0)}, ub[3] = {R(0), R(0), R(0)};
+    if (UREG) {
+        #pragma unroll
+        for (int j = 0; j < 3; ++j)
+            if (j < nrow) { ua[j] = U[urow[j] + lane * LD]; ub[j] = U[urow[j] + (BW + lane) * LD]; }
     }
     // parameters of round 0
     if (warp == 0) {
@@ -279,7 +299,20 @@ __device__ __forceinline__ R *smem_rounds_wide(R *D0, R *D1, R *U, int2 bp, bool
                     Dn[qk + pk * LD] = R(0);
                 }
             }
-            if (U) {
+            if (UREG) {
+                const R sk = P.s[lane];
+                if (sk != R(0)) {
+                    const R tk = P.u[lane];
+                    #pragma unroll
+                    for (int j = 0; j < 3; ++j)
+                        if (j < nrow) {
+                            if (!flip) rot<R>(sk, tk, ua[j], ub[j]);
+                            else rot<R>(sk, tk, ub[j], ua[j]);
+                        }
+                }
+                #pragma unroll
+                for (int j = 0; j < 3; ++j) ub[j] = __shfl_sync(0xffffffffu, ub[j], (lane + 1) & 31);
+            } else if (U) {
                 #pragma unroll
                 for (int j = 0; j < 3; ++j) {
                     if (uk[j] < 0) continue;
@@ -298,148 +331,23 @@ __device__ __forceinline__ R *smem_rounds_wide(R *D0, R *D1, R *U, int2 bp, bool
         MPJ_K3_TRACE(2, s);
         R *tmp = Dc; Dc = Dn; Dn = tmp;
     }
+    if (UREG) {                             // back to shared memory (the shuffle after the last round is undone)
+        #pragma unroll
+        for (int j = 0; j < 3; ++j) {
+            const R v = __shfl_sync(0xffffffffu, ub[j], (lane + 31) & 31);
+            if (j < nrow) {
+                U[urow[j] + lane * LD] = ua[j];
+                U[urow[j] + (BW + ((lane + nrounds - 1) & 31)) * LD] = v;
+            }
+        }
+        __syncthreads();
+    }
     return Dc;
 }
 
-// ---------------------------------------------------------------------------
-// Register-resident cross rounds (the b rounds of a block round in which top
-// index k (0..31) meets bottom index 32 + (k + s) mod 32, reading R1).
-// Thread (k, l) = (lane, warp) of the 1024 holds the 2x2 tile of pairs k and l
-// -- Y_aa = D(a_k, a_l), Y_ba = D(b_k, a_l), Y_ab = D(a_k, b_l), Y_bb =
-// D(b_k, b_l) -- and rows 2l, 2l+1 of U at columns a_k, b_k.  Round s: every
-// thread applies pairs k and l to its tile (the pair with the smaller global p
-// first: the element arithmetic of tile_after, so the result is bit-identical
-// to the shared-memory rounds) and pair k to its U rows, then moves to the
-// next layout: b_k(s+1) = b_{k+1}(s), so Y_ba and the U bottoms come from lane
-// k+1 (shuffle), Y_ab from warp l+1 and Y_bb from (k+1, l+1) (one exchange
-// through shared memory); one barrier per round.  Meanwhile the parameter
-// warp (the last one; the arbiter issues it first) computes round s+1's
-// parameters for all 32 pairs from the pre-round values of the diagonal and
-// super-diagonal tiles, which their owners publish with the exchange -- the
-// same arithmetic again, then rot_params.  Shared-memory traffic per round: 2
-// words per thread plus ~7 x 32 published words and the parameters, instead
-// of the whole 64 x 64 D and U (which made the shared-memory rounds bandwidth
-// bound and queued the parameter warp's loads behind the update traffic).
-// ---------------------------------------------------------------------------
-template <typename R>
-struct RegPub {            // pre-round values of tiles (k, k) and (k, k+1), next layout
-    R daa[BW], dbb[BW], dab[BW];
-    R taa[BW], tba[BW], tab[BW], tbb[BW];
-};
-
-// the canonical tile update (pairs k: rows, l: columns) in the a/b layout
-template <typename R>
-__device__ __forceinline__ void reg_tile(bool flip, bool kfirst, R sk, R uk, R sl, R ul, R &yaa, R &yba, R &yab,
-                                         R &ybb)
-{
-    R x11 = flip ? ybb : yaa, x21 = flip ? yab : yba, x12 = flip ? yba : yab, x22 = flip ? yaa : ybb;
-    if (kfirst) {
-        rot<R>(sk, uk, x11, x21); rot<R>(sk, uk, x12, x22);
-        rot<R>(sl, ul, x11, x12); rot<R>(sl, ul, x21, x22);
-    } else {
-        rot<R>(sl, ul, x11, x12); rot<R>(sl, ul, x21, x22);
-        rot<R>(sk, uk, x11, x21); rot<R>(sk, uk, x12, x22);
-    }
-    yaa = flip ? x22 : x11; yba = flip ? x12 : x21; yab = flip ? x21 : x12; ybb = flip ? x11 : x22;
-}
-
-template <typename R>
-__device__ __forceinline__ void cross_rounds_reg(R *Dc, R *X, R *U, int2 bp, R nu, int rule,
-                                                 WideParams<R> (&PP)[2], RegPub<R> (&pub)[2], unsigned &cnt)
-{
-    constexpr int LD = LayK<R>::LD;
-    static_assert(4 * NTW <= TW * LD, "two exchange buffers must fit in one 64 x LD buffer");
-    const int k = threadIdx.x & 31, l = (NTW / 32 - 1) - (threadIdx.x >> 5);   // warp l = 31 is issued first
-    const int k1 = (k + 1) & 31, l1 = (l + 1) & 31;
-    const bool flip = bp.x > bp.y;          // bottom block first in the global order: p = b, q = a
-    const bool pw = (l == BW - 1);          // the parameter warp
-    R yaa = Dc[k + l * LD], yba = Dc[BW + k + l * LD], yab = Dc[k + (BW + l) * LD], ybb = Dc[BW + k + (BW + l) * LD];
-    const int r0 = 2 * l, r1 = 2 * l + 1;
-    R ua0 = U[r0 + k * LD], ub0 = U[r0 + (BW + k) * LD], ua1 = U[r1 + k * LD], ub1 = U[r1 + (BW + k) * LD];
-    // X: two exchange buffers (round parity) of 2 x 1024 words; pub likewise --
-    // one barrier per round orders a round's writes before the next round's
-    // reads, and the parity keeps a fast warp's next writes off unread data
-    // parameter warp: round-0 parameters, and the pre-round-0 values it needs for round 1
-    R pt = 0, ps = 0, pu = 0;               // parameters of pair `k` (lane) of the current round
-    R daa, dbb, dab, taa, tba, tab, tbb;
-    if (pw) {
-        daa = Dc[k + k * LD]; dbb = Dc[BW + k + (BW + k) * LD]; dab = Dc[k + (BW + k) * LD];
-        taa = Dc[k + k1 * LD]; tba = Dc[BW + k + k1 * LD]; tab = Dc[k + (BW + k1) * LD]; tbb = Dc[BW + k + (BW + k1) * LD];
-        cnt += rot_params<R>(flip ? dbb : daa, flip ? daa : dbb, dab, nu, rule, pt, ps, pu);
-        PP[0].t[k] = pt; PP[0].s[k] = ps; PP[0].u[k] = pu;
-    }
-    __syncthreads();
-    for (int s = 0; s < BW; ++s) {
-        const WideParams<R> &P = PP[s & 1];
-        if (pw && s + 1 < BW) {
-            // pre-round-s values of tiles (k, k), (k+1, k+1) and (k, k+1) -> round s+1 pair k
-            if (s > 0) {
-                const RegPub<R> &q = pub[s & 1];
-                daa = q.daa[k]; dbb = q.dbb[k]; dab = q.dab[k];
-                taa = q.taa[k]; tba = q.tba[k]; tab = q.tab[k]; tbb = q.tbb[k];
-            }
-            const R t1 = __shfl_sync(0xffffffffu, pt, k1), s1 = __shfl_sync(0xffffffffu, ps, k1),
-                    u1 = __shfl_sync(0xffffffffu, pu, k1);
-            const R dbb1 = __shfl_sync(0xffffffffu, dbb, k1), dab1 = __shfl_sync(0xffffffffu, dab, k1);
-            // D(a_k, a_k) and D(b_{k+1}, b_{k+1}) after round s (diagonal formula; p/q by flip)
-            const R aa = flip ? fmaR(pt, dab, daa) : fmaR(-pt, dab, daa);
-            const R bb = flip ? fmaR(-t1, dab1, dbb1) : fmaR(t1, dab1, dbb1);
-            // D(a_k, b_{k+1}) after round s: entry Y_ab of tile (k, k+1)
-            R xaa = taa, xba = tba, xab = tab, xbb = tbb;
-            const int gk = flip ? ((k + s) & 31) : k, gl = flip ? ((k1 + s) & 31) : k1;
-            reg_tile<R>(flip, gk < gl, ps, pu, s1, u1, xaa, xba, xab, xbb);
-            R nt, ns, nu2;
-            cnt += rot_params<R>(flip ? bb : aa, flip ? aa : bb, xab, nu, rule, nt, ns, nu2);
-            MPJ_K3_TRACE(0, s);
-            WideParams<R> &N = PP[(s + 1) & 1];
-            N.t[k] = nt; N.s[k] = ns; N.u[k] = nu2;
-            pt = nt; ps = ns; pu = nu2;
-        }
-        const R sk = P.s[k], uk = P.u[k], sl = P.s[l], ul = P.u[l];
-        if (k == l) {
-            const R t = P.t[k];
-            const R xpp = fmaR(-t, yab, flip ? ybb : yaa), xqq = fmaR(t, yab, flip ? yaa : ybb);
-            yaa = flip ? xqq : xpp;
-            ybb = flip ? xpp : xqq;
-            yab = R(0);
-            yba = R(0);
-        } else {
-            const int gk = flip ? ((k + s) & 31) : k, gl = flip ? ((l + s) & 31) : l;
-            reg_tile<R>(flip, gk < gl, sk, uk, sl, ul, yaa, yba, yab, ybb);
-        }
-        if (sk != R(0)) {
-            if (!flip) { rot<R>(sk, uk, ua0, ub0); rot<R>(sk, uk, ua1, ub1); }
-            else       { rot<R>(sk, uk, ub0, ua0); rot<R>(sk, uk, ub1, ua1); }
-        }
-        MPJ_K3_TRACE(1, s);
-        if (s + 1 < BW) {
-            // publish (next layout: tile (k', l') <- aa (k', l'), ba (k'+1, l'), ab (k', l'+1), bb (k'+1, l'+1))
-            const int d = (l - k) & 31;
-            RegPub<R> &q = pub[(s + 1) & 1];
-            if (d == 0) { q.daa[k] = yaa; q.dbb[(k + 31) & 31] = ybb; q.tba[(k + 31) & 31] = yba; }
-            else if (d == 1) { q.dab[k] = yab; q.taa[k] = yaa; q.tbb[(k + 31) & 31] = ybb; }
-            else if (d == 2) { q.tab[k] = yab; }
-            R *xab = X + (s & 1) * 2 * NTW, *xbb = xab + NTW;
-            xab[l * 32 + k] = yab;
-            xbb[l * 32 + k] = ybb;
-            yba = __shfl_sync(0xffffffffu, yba, k1);
-            ub0 = __shfl_sync(0xffffffffu, ub0, k1);
-            ub1 = __shfl_sync(0xffffffffu, ub1, k1);
-            __syncthreads();
-            yab = xab[l1 * 32 + k];
-            ybb = xbb[l1 * 32 + k1];
-        }
-        MPJ_K3_TRACE(2, s);
-    }
-    __syncthreads();                        // exchange reads done before D is written back
-    const int bk = BW + ((k + BW - 1) & 31), bl = BW + ((l + BW - 1) & 31);   // b after the last round
-    Dc[k + l * LD] = yaa; Dc[bk + l * LD] = yba; Dc[k + bl * LD] = yab; Dc[bk + bl * LD] = ybb;
-    U[r0 + k * LD] = ua0; U[r0 + bk * LD] = ub0; U[r1 + k * LD] = ua1; U[r1 + bk * LD] = ub1;
-    __syncthreads();
-}
-
 // K3's inner rounds: the intra-block rounds of block round 0 in shared memory
-// (their pairs follow the local schedule), the cross rounds in registers.
+// (their pairs follow the local schedule), then the cross rounds with U in
+// registers.
 template <typename R>
 __device__ __forceinline__ R *inner_rounds_wide(R *D0, R *D1, R *U, int2 bp, bool intra,
                                                 const int2 *__restrict__ lsched, R nu, int rule,
@@ -448,11 +356,10 @@ __device__ __forceinline__ R *inner_rounds_wide(R *D0, R *D1, R *U, int2 bp, boo
     unsigned cnt = 0;
     R *Dc = D0, *X = D1;
     if (intra) {
-        Dc = smem_rounds_wide<R>(D0, D1, U, bp, true, BW - 1, lsched, nu, rule, PP, cnt);
+        Dc = smem_rounds_wide<R, false>(D0, D1, U, bp, true, BW - 1, lsched, nu, rule, PP, cnt);
         X = (Dc == D0) ? D1 : D0;
     }
-    __shared__ RegPub<R> pub[2];
-    cross_rounds_reg<R>(Dc, X, U, bp, nu, rule, PP, pub, cnt);
+    Dc = smem_rounds_wide<R, true>(Dc, X, U, bp, false, BW, lsched, nu, rule, PP, cnt);
     // rotation count: per-thread counts of the diagonal threads and the parameter warp
     for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
     if (threadIdx.x == 0) *nrot = 0;

@@ -42,7 +42,7 @@ __global__ void __launch_bounds__(NTW) k3(const R *Din, R *Uout, R nu)
     for (int e = threadIdx.x; e < TW * TW; e += NTW) Uout[e] = U[(e & 63) + (e >> 6) * LD] + D[(e & 63) + (e >> 6) * LD];
 }
 
-// old (shared-memory) cross rounds vs the register rounds: must be bit-identical
+// shared-memory cross rounds vs the library rounds (U in registers): bit-identical
 template <typename R>
 __global__ void __launch_bounds__(NTW) k3ab(const R *Din, R *out, R nu, int2 bp, int reg)
 {
@@ -60,7 +60,7 @@ __global__ void __launch_bounds__(NTW) k3ab(const R *Din, R *out, R nu, int2 bp,
     unsigned cnt = 0;
     const R *D;
     if (reg) D = inner_rounds_wide<R>(D0, D1, U, bp, false, nullptr, nu, 0, P, &nrot);
-    else { D = smem_rounds_wide<R>(D0, D1, U, bp, false, BW, nullptr, nu, 0, P, cnt); __syncthreads(); }
+    else { D = smem_rounds_wide<R, false>(D0, D1, U, bp, false, BW, nullptr, nu, 0, P, cnt); __syncthreads(); }
     for (int e = threadIdx.x; e < TW * TW; e += NTW) {
         out[e] = D[(e & 63) + (e >> 6) * LD];
         out[4096 + e] = U[(e & 63) + (e >> 6) * LD];
