@@ -467,15 +467,19 @@ def main():
                 fl = fl - (skt * 2 * 2 * 64 ** 3 + skv * 2 * 64 ** 3) / nl
                 by = by - (skt * 3 + skv * 2) * 64 * 64 * (8 if is64 else 4) / nl
             peak = pk["dmma_tflops"] if is64 else pk["ffma_tflops"]
-            traffic = None
+            traffic = traffic_alg = None
             tp = os.path.join(ROOT, "profiles", "r01_traffic.json")
             if os.path.exists(tp):
                 t = json.load(open(tp)).get(dom)
                 if t and t.get("n_padded") == rep.n_padded:
                     traffic = t["dram_bytes_per_launch"]
+                    traffic_alg = t.get("algorithmic_bytes_per_launch")
             roof = {"kernel": dom, "bound": "tensor" if is64 else "alu",
                     "achieved": fl / avg / 1e12, "peak": peak, "unit": "TFLOP/s",
                     "frac": fl / avg / 1e12 / peak, "traffic": traffic,
+                    # traffic is from one full launch (no identity blocks); compare it with that
+                    # launch's algorithmic bytes, not the skip-averaged ones below
+                    "traffic_launch_algorithmic_bytes": traffic_alg,
                     "algorithmic_flop_per_launch": fl, "algorithmic_bytes_per_launch": by,
                     "hbm_frac": by / avg / 1e9 / pk["hbm_gbs"],
                     "share_of_step": kernels[dom]["seconds_per_step"] / (ms * 1e-3),

@@ -17,6 +17,8 @@
 // Diagonal blocks come from K3 directly.  Per block round and n_p = 8192 this
 // is 8.5e9 + 8.6e9 flop (T upper tiles + V) on 1.8 GB of HBM traffic.
 #include "mpj_device.cuh"
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include "mpj_internal.h"
 #include "mpj_block.cuh"
 
@@ -59,11 +61,16 @@ __global__ void __launch_bounds__(NTW) k_block_solve(R *__restrict__ T, int64_t 
     const R *D = inner_rounds_wide<R>(D0, D1, U, bp, Rb == 0, S.lsched, nu, rule, P, &nrot);
     R *Uk = Ubuf + (size_t)k * TW * TW;
     R *UkT = Ubuf + (size_t)mb * TW * TW + (size_t)k * TW * TW;   // U^T (fp32 apply operand)
+    R *UkS = Ubuf + 2 * (size_t)mb * TW * TW + (size_t)k * TW * TW;   // U^T, split-half layout
     for (int e = threadIdx.x; e < TW * TW; e += NTW) {
         const int li = e & (TW - 1), lj = e >> 6;
         T[gidx(bp, li) + (int64_t)gidx(bp, lj) * ldt] = D[li + lj * LD];
         Uk[li + lj * TW] = U[li + lj * LD];
-        if (sizeof(R) == 4) UkT[li + lj * TW] = U[lj + li * LD];
+        if (sizeof(R) == 4) {
+            UkT[li + lj * TW] = U[lj + li * LD];
+            // split-half U^T for the TMA apply: element (i, k) of U^T = U(k, i)
+            UkS[(li >> 5) * (BW * TW) + lj * BW + (li & 31)] = U[lj + li * LD];
+        }
     }
     if (threadIdx.x == 0) {
         if (nrot) atomicAdd(cnt, (unsigned long long)nrot);
@@ -271,10 +278,10 @@ struct Acc84 {
     float v[8][4];
 };
 
-__device__ __forceinline__ void tile_op84(const float *A, const float *B, Acc84 &acc)
+__device__ __forceinline__ void tile_op84_t(const float *A, const float *B, Acc84 &acc, int tid)
 {
     constexpr int LD = Lay<float>::LD;
-    const int ra = 4 * (threadIdx.x & 7), cb = 4 * (threadIdx.x >> 3);
+    const int ra = 4 * (tid & 7), cb = 4 * (tid >> 3);
     #pragma unroll
     for (int u = 0; u < 8; ++u)
         #pragma unroll
@@ -295,10 +302,10 @@ __device__ __forceinline__ void tile_op84(const float *A, const float *B, Acc84 
     }
 }
 
-__device__ __forceinline__ void store_op84(const Acc84 &acc, float *C, float *CT)
+__device__ __forceinline__ void store_op84_t(const Acc84 &acc, float *C, float *CT, int tid)
 {
     constexpr int LD = Lay<float>::LD;
-    const int r = 4 * (threadIdx.x & 7), c = 4 * (threadIdx.x >> 3);
+    const int r = 4 * (tid & 7), c = 4 * (tid >> 3);
     #pragma unroll
     for (int w = 0; w < 4; ++w) {
         *(float4 *)(C + r + (c + w) * LD) = make_float4(acc.v[0][w], acc.v[1][w], acc.v[2][w], acc.v[3][w]);
@@ -311,6 +318,15 @@ __device__ __forceinline__ void store_op84(const Acc84 &acc, float *C, float *CT
             *(float4 *)(CT + c + row * LD) = make_float4(acc.v[u][0], acc.v[u][1], acc.v[u][2], acc.v[u][3]);
         }
     }
+}
+
+__device__ __forceinline__ void tile_op84(const float *A, const float *B, Acc84 &acc)
+{
+    tile_op84_t(A, B, acc, threadIdx.x);
+}
+__device__ __forceinline__ void store_op84(const Acc84 &acc, float *C, float *CT)
+{
+    store_op84_t(acc, C, CT, threadIdx.x);
 }
 
 __global__ void __launch_bounds__(NT128) k_block_apply_f32w(ApplyArgs p)
@@ -369,6 +385,221 @@ __global__ void __launch_bounds__(NT128) k_block_apply_f32w(ApplyArgs p)
     }
 }
 
+// ---------------------------------------------------------------------------
+// fp32 apply, warp-specialised TMA pipeline: one persistent CTA per SM = 1
+// producer warp + 2 consumer groups of 128 threads (8 x 4 FFMA tiles).  A
+// ring of WS_NS stages, each one work item's operands (X, U_a^T, U_c^T; 16 KB
+// each, "split-half" layout: element (i, k) at (i / 32) * 2048 + 32 k + i % 32,
+// so every 32 x 32 box is a contiguous 4 KB chunk and the GEMM's 128-bit
+// operand reads stay conflict-free).  The producer loads item j into stage
+// j % WS_NS: X as four 32 x 32 tensor-TMA boxes (T or V tensor map; rows past
+// the end of V are zero-filled) and each U^T block as one 16 KB bulk copy
+// (K3 writes them in this layout), all completing on the stage's "full"
+// mbarrier; consumer group j % 2 waits on it, multiplies, stores its tile with
+// 128-bit thread stores and releases the stage on its "empty" mbarrier.  Six
+// TMA requests per item (per-column bulk copies -- 256 per item -- made the
+// first version of this kernel request-rate bound, 2.4x slower).
+// ---------------------------------------------------------------------------
+constexpr int WS_NS = 4;
+constexpr int WS_CG = 128;                     // threads per consumer group
+constexpr int WS_NT = 32 + 2 * WS_CG;
+constexpr int SH_HALF = BW * TW;               // 2048 floats: one 32-row half of a 64 x 64 operand
+constexpr int SH_TILE = 2 * SH_HALF;           // 4096 floats = 16 KB
+
+__device__ __forceinline__ int sh_idx(int i, int k) { return (i >> 5) * SH_HALF + k * BW + (i & 31); }
+
+__device__ __forceinline__ unsigned smem_u32(const void *p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t *b, unsigned count)
+{
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(b)), "r"(count));
+}
+__device__ __forceinline__ void mbar_arrive_tx(uint64_t *b, unsigned bytes)
+{
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t *b)
+{
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *b, unsigned parity)
+{
+    asm volatile("{\n .reg .pred p;\n WAIT_%=:\n"
+                 " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+                 " @!p bra WAIT_%=;\n}\n" ::"r"(smem_u32(b)), "r"(parity) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, unsigned bytes, uint64_t *bar)
+{
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n"
+                 ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void tma_box(void *dst, const CUtensorMap *map, int row, int col, uint64_t *bar)
+{
+    asm volatile("cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];\n"
+                 ::"r"(smem_u32(dst)), "l"(map), "r"(row), "r"(col), "r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void group_sync(int id) { asm volatile("bar.sync %0, %1;\n" ::"r"(id), "r"(WS_CG) : "memory"); }
+
+// C = A B^T-style k-major product of split-half operands, 4 x 8 per thread:
+// quarter-warp Q = tid / 8 of the group owns rows 32 (Q % 2) + 4 (tid % 8) ..+3
+// and columns 8 (Q / 2) ..+7.  128-bit shared loads are serviced per quarter
+// warp: A (8 lanes, 128 contiguous bytes) costs one wavefront per quarter and
+// B is a broadcast inside each quarter, so a k-step is ~6-8 wavefronts per
+// warp for 32 FFMA (the 8 x 4 mapping of k_block_apply_f32w: ~10, which made
+// that kernel shared-memory bound).
+struct Acc48 {
+    float v[4][8];
+};
+
+__device__ __forceinline__ void tile_op_sh(const float *A, const float *B, Acc48 &acc, int tid)
+{
+    const int q = tid >> 3, l8 = tid & 7;
+    const float *Ar = A + (q & 1) * SH_HALF + 4 * l8;
+    const int cb = 8 * (q >> 1);
+    const float *Bc = B + (cb >> 5) * SH_HALF + (cb & 31);
+    #pragma unroll
+    for (int u = 0; u < 4; ++u)
+        #pragma unroll
+        for (int w = 0; w < 8; ++w) acc.v[u][w] = 0.f;
+    float4 a = *(const float4 *)Ar, b0 = *(const float4 *)Bc, b1 = *(const float4 *)(Bc + 4);
+    #pragma unroll 4
+    for (int k = 0; k < TW; ++k) {
+        const float av[4] = {a.x, a.y, a.z, a.w}, bv[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+        if (k + 1 < TW) {
+            a = *(const float4 *)(Ar + (k + 1) * BW);
+            b0 = *(const float4 *)(Bc + (k + 1) * BW);
+            b1 = *(const float4 *)(Bc + 4 + (k + 1) * BW);
+        }
+        #pragma unroll
+        for (int u = 0; u < 4; ++u)
+            #pragma unroll
+            for (int w = 0; w < 8; ++w) acc.v[u][w] = __fmaf_rn(av[u], bv[w], acc.v[u][w]);
+    }
+}
+
+// C (split-half) and C^T stores of an Acc48
+__device__ __forceinline__ void store_op_sh(const Acc48 &acc, float *C, float *CT, int tid)
+{
+    const int q = tid >> 3, l8 = tid & 7;
+    const int r = 32 * (q & 1) + 4 * l8, c = 8 * (q >> 1);
+    #pragma unroll
+    for (int w = 0; w < 8; ++w)
+        *(float4 *)(C + sh_idx(r, c + w)) = make_float4(acc.v[0][w], acc.v[1][w], acc.v[2][w], acc.v[3][w]);
+    if (CT) {
+        #pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            *(float4 *)(CT + sh_idx(c, r + u)) = make_float4(acc.v[u][0], acc.v[u][1], acc.v[u][2], acc.v[u][3]);
+            *(float4 *)(CT + sh_idx(c + 4, r + u)) = make_float4(acc.v[u][4], acc.v[u][5], acc.v[u][6], acc.v[u][7]);
+        }
+    }
+}
+
+__global__ void __launch_bounds__(WS_NT, 1) k_block_apply_f32ws(ApplyArgs p, const __grid_constant__ CUtensorMap tmT,
+                                                                const __grid_constant__ CUtensorMap tmM)
+{
+    constexpr int EPC = 4, CPC = TW / EPC, SBUF = 3 * SH_TILE;
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    float *ring = (float *)smem_raw;
+    uint64_t *full = (uint64_t *)(smem_raw + (size_t)WS_NS * SBUF * sizeof(float));
+    uint64_t *empty = full + WS_NS;
+    const int total = p.ntT + p.ntV;
+    const int mb = p.S.nb >> 1;
+    const int2 *bsr = p.S.bsched + p.Rb * mb;
+    const bool skips = p.uid && *p.nid > 0;
+    auto advance = [&](int i) {
+        while (skips && i < total && item_identity(p, i, mb)) i += gridDim.x;
+        return i;
+    };
+    if (threadIdx.x == 0) {
+        for (int st = 0; st < WS_NS; ++st) { mbar_init(full + st, 1); mbar_init(empty + st, 1); }
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    __syncthreads();
+    const int warp = threadIdx.x >> 5;
+    if (warp == 0) {
+        // ------------------------------------------------------------- producer
+        if (threadIdx.x != 0) return;
+        const float *UbS = (const float *)p.Ubuf + 2 * (size_t)mb * TW * TW;   // split-half U^T
+        int j = 0;
+        for (int item = advance(blockIdx.x); item < total; item = advance(item + gridDim.x), ++j) {
+            const int st = j % WS_NS;
+            mbar_wait(empty + st, ((j / WS_NS) & 1) ^ 1);
+            float *x = ring + (size_t)st * SBUF, *ua = x + SH_TILE, *uc = ua + SH_TILE;
+            uint64_t *bar = full + st;
+            if (item < p.ntT) {
+                int a, c;
+                decode_upper(item, a, c);
+                const int2 pa = bsr[a], pc = bsr[c];
+                mbar_arrive_tx(bar, 3 * SH_TILE * sizeof(float));
+                // X^T = T(P_c, P_a): box (rows of block h of pc, columns of block v of pa)
+                tma_box(x, &tmT, pc.x * BW, pa.x * BW, bar);
+                tma_box(x + SH_HALF, &tmT, pc.y * BW, pa.x * BW, bar);
+                tma_box(x + BW * BW, &tmT, pc.x * BW, pa.y * BW, bar);
+                tma_box(x + SH_HALF + BW * BW, &tmT, pc.y * BW, pa.y * BW, bar);
+                bulk_g2s(ua, UbS + (size_t)a * SH_TILE, SH_TILE * sizeof(float), bar);
+                bulk_g2s(uc, UbS + (size_t)c * SH_TILE, SH_TILE * sizeof(float), bar);
+            } else {
+                const int idx = item - p.ntT, c = idx % mb, r0 = (idx / mb) * TW;
+                const int2 pc = bsr[c];
+                mbar_arrive_tx(bar, 2 * SH_TILE * sizeof(float));   // out-of-range rows are zero-filled
+                tma_box(x, &tmM, r0, pc.x * BW, bar);
+                tma_box(x + SH_HALF, &tmM, r0 + BW, pc.x * BW, bar);
+                tma_box(x + BW * BW, &tmM, r0, pc.y * BW, bar);
+                tma_box(x + SH_HALF + BW * BW, &tmM, r0 + BW, pc.y * BW, bar);
+                bulk_g2s(uc, UbS + (size_t)c * SH_TILE, SH_TILE * sizeof(float), bar);
+            }
+        }
+        return;
+    }
+    // ----------------------------------------------------------------- consumers
+    const int g = (warp - 1) / (WS_CG / 32);               // group 0 / 1
+    const int gt = threadIdx.x - 32 - g * WS_CG;            // thread within the group
+    const int bar_id = 1 + g;
+    Acc48 acc;
+    int j = 0;
+    for (int item = advance(blockIdx.x); item < total; item = advance(item + gridDim.x), ++j) {
+        if ((j & 1) != g) continue;
+        const int st = j % WS_NS;
+        mbar_wait(full + st, (j / WS_NS) & 1);
+        float *x = ring + (size_t)st * SBUF, *ua = x + SH_TILE, *uc = ua + SH_TILE;
+        if (item < p.ntT) {
+            int a, c;
+            decode_upper(item, a, c);
+            const int2 pa = bsr[a], pc = bsr[c];
+            tile_op_sh(ua, x, acc, gt);                      // Y = U_a^T X
+            group_sync(bar_id);
+            store_op_sh(acc, x, nullptr, gt);
+            group_sync(bar_id);
+            tile_op_sh(x, uc, acc, gt);                      // W = Y U_c
+            group_sync(bar_id);
+            store_op_sh(acc, x, ua, gt);                     // W and W^T
+            group_sync(bar_id);
+            float *T = (float *)p.T;
+            for (int e = gt; e < TW * CPC; e += WS_CG) {
+                const int lj = e / CPC, li = (e - lj * CPC) * EPC;
+                *(int4 *)(T + gidx(pa, li) + (int64_t)gidx(pc, lj) * p.ldt) = *(const int4 *)(x + sh_idx(li, lj));
+                *(int4 *)(T + gidx(pc, li) + (int64_t)gidx(pa, lj) * p.ldt) = *(const int4 *)(ua + sh_idx(li, lj));
+            }
+        } else {
+            const int idx = item - p.ntT, c = idx % mb, r0 = (idx / mb) * TW;
+            const int2 pc = bsr[c];
+            tile_op_sh(x, uc, acc, gt);                      // W = X U_c
+            group_sync(bar_id);
+            store_op_sh(acc, x, nullptr, gt);
+            group_sync(bar_id);
+            float *M = (float *)p.M;
+            for (int e = gt; e < TW * CPC; e += WS_CG) {
+                const int lj = e / CPC, li = (e - lj * CPC) * EPC;
+                if (r0 + li < p.mrows)   // mrows % 4 == 0 on this path
+                    *(int4 *)(M + (int64_t)(r0 + li) + (int64_t)gidx(pc, lj) * p.ldm) = *(const int4 *)(x + sh_idx(li, lj));
+            }
+        }
+        // all generic-proxy accesses of the stage are done before the async proxy refills it
+        asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+        group_sync(bar_id);
+        if (gt == 0) mbar_arrive(empty + st);
+    }
+}
+
 }  // namespace
 
 template <typename R>
@@ -377,7 +608,7 @@ size_t block_scratch_bytes(int np, int b)
     (void)b;
     const int mb = np / (2 * BW);
     // U, U^T, identity flags, identity counts per block round
-    return 2 * (size_t)mb * TW * TW * sizeof(R) + (size_t)(mb + 2 * mb) * sizeof(int);
+    return (sizeof(R) == 4 ? 3 : 2) * (size_t)mb * TW * TW * sizeof(R) + (size_t)(mb + 2 * mb) * sizeof(int);
 }
 
 static int sm_count()
@@ -427,7 +658,7 @@ static int fp32_apply_kind()
     static int v = -1;
     if (v < 0) {
         const char *e = getenv("MPJ_FP32_APPLY");
-        v = (e && std::string(e) == "4x4") ? 0 : 1;
+        v = (e && std::string(e) == "4x4") ? 0 : (e && std::string(e) == "8x4") ? 1 : 2;
     }
     return v;
 }
@@ -449,10 +680,58 @@ static void launch_apply_f32w(const ApplyArgs &p, cudaStream_t st)
     count_launch();
 }
 
+static PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder()
+{
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    static bool tried = false;
+    if (!tried) {
+        tried = true;
+        void *f = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = (PFN_cuTensorMapEncodeTiled_v12000)f;
+    }
+    return fn;
+}
+
+// 2-D fp32 tensor map of a column-major rows x cols matrix, 32 x 32 boxes
+static bool make_map32(CUtensorMap &m, const void *base, int64_t rows, int64_t cols, int64_t ld)
+{
+    auto enc = tensor_map_encoder();
+    if (!enc) return false;
+    cuuint64_t dims[2] = {(cuuint64_t)rows, (cuuint64_t)cols};
+    cuuint64_t strides[1] = {(cuuint64_t)ld * sizeof(float)};
+    cuuint32_t box[2] = {BW, BW}, es[2] = {1, 1};
+    return enc(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void *>(base), dims, strides, box, es,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+static bool launch_apply_f32ws(const ApplyArgs &p, cudaStream_t st)
+{
+    CUtensorMap mT, mM;
+    if (!make_map32(mT, p.T, p.S.np, p.S.np, p.ldt) || !make_map32(mM, p.M, p.mrows, p.S.np, p.ldm)) return false;
+    const size_t smem = (size_t)WS_NS * 3 * SH_TILE * sizeof(float) + 2 * WS_NS * sizeof(uint64_t);
+    static bool attr = false;
+    if (!attr) {
+        if (cudaFuncSetAttribute(k_block_apply_f32ws, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+            cudaSuccess)
+            return false;
+        attr = true;
+    }
+    const int total = p.ntT + p.ntV;
+    const int grid = std::max(1, std::min(total, sm_count()));
+    k_block_apply_f32ws<<<grid, WS_NT, smem, st>>>(p, mT, mM);
+    count_launch();
+    return true;
+}
+
 template <typename R>
 static void launch_apply(const ApplyArgs &p, cudaStream_t st)
 {
-    if (sizeof(R) == 4 && fp32_apply_kind() == 1) { launch_apply_f32w(p, st); return; }
+    if (sizeof(R) == 4 && fp32_apply_kind() == 2 && p.T && p.mrows % 4 == 0 && launch_apply_f32ws(p, st)) return;
+    if (sizeof(R) == 4 && fp32_apply_kind() >= 1) { launch_apply_f32w(p, st); return; }
     if (apply_stages() == 2) launch_apply_s<R, 2>(p, st);
     else launch_apply_s<R, 1>(p, st);
 }
@@ -467,7 +746,7 @@ mpj_status block_sweep(R *T, int64_t ldt, R *V, int64_t ldv, int vrows, const De
     S.bsched = ds.bsched; S.lsched = ds.lsched; S.b = ds.b; S.nb = ds.nb; S.np = ds.np;
     const int mb = ds.nb / 2;
     R *Ubuf = (R *)scratch;
-    int *uid = (int *)(Ubuf + 2 * (size_t)mb * TW * TW);
+    int *uid = (int *)(Ubuf + (sizeof(R) == 4 ? 3 : 2) * (size_t)mb * TW * TW);
     int *nid = uid + mb;                         // nb - 1 <= 2 mb block rounds
     MPJ_CK(cudaMemsetAsync(nid, 0, (size_t)(ds.nb - 1) * sizeof(int), st));
     const size_t sm_solve = 3 * TW * LayK<R>::LD * sizeof(R);

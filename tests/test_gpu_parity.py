@@ -277,6 +277,41 @@ def test_block_variant_identity_skip(mpj, orc, n):
     assert np.array_equal(host(T), D) and np.array_equal(host(V), np.eye(n))
 
 
+_FP32_APPLY_SCRIPT = r"""
+import sys, numpy as np, torch
+sys.path.insert(0, sys.argv[1])
+import paper_2211_03339_b200 as mpj, workloads as W
+n = int(sys.argv[2])
+A, _ = W.example1(n, 1e3, 4, 4242 + n)
+T = torch.from_numpy(A.astype(np.float32)).cuda().T.contiguous().T
+V = torch.eye(n, dtype=torch.float32, device="cuda").T.contiguous().T
+cfg = mpj.default_config("eig", variant=mpj.VARIANT_BLOCK, block_b=32)
+mpj.jacobi(T, V, tol=0.0, max_sweeps=2, nu=float(np.float32(20 * 2.0 ** -24)), cfg=cfg)
+np.save(sys.argv[3], np.concatenate([T.cpu().numpy().ravel(), V.cpu().numpy().ravel()]))
+"""
+
+
+@pytest.mark.parametrize("n", [256, 330])
+def test_fp32_apply_kernels_bit_identical(tmp_path, n):
+    """The three fp32 K4 kernels (4x4 outer product, 8x4 tiles, warp-specialised
+    TMA pipeline) accumulate every output in the same k order: two fp32 block
+    sweeps must give bit-identical T and V whichever runs (MPJ_FP32_APPLY)."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    script = tmp_path / "run.py"
+    script.write_text(_FP32_APPLY_SCRIPT)
+    outs = {}
+    for kind in ("4x4", "8x4", "ws"):
+        env = dict(os.environ, MPJ_FP32_APPLY=kind)
+        out = tmp_path / f"{kind}.npy"
+        subprocess.run([sys.executable, str(script), root, str(n), str(out)], env=env, check=True, timeout=300)
+        outs[kind] = np.load(out)
+    assert np.array_equal(outs["4x4"].view(np.uint32), outs["8x4"].view(np.uint32))
+    assert np.array_equal(outs["4x4"].view(np.uint32), outs["ws"].view(np.uint32))
+
+
 @pytest.mark.parametrize("n", [512, 1000])
 def test_eig_block_end_to_end(mpj, orc, n):
     A, lam_true = W.example1(n, 1e3, 4, W.seed_for(2, 4, 1e3))
