@@ -463,8 +463,9 @@ def main():
             nl = kernels[dom]["launches"]
             skt = mpj.profile_get(dom + ".skipped_t")[1]
             skv = mpj.profile_get(dom + ".skipped_v")[1]
-            if skt or skv:
-                fl = fl - (skt * 2 * 2 * 64 ** 3 + skv * 2 * 64 ** 3) / nl
+            half = mpj.profile_get(dom + ".half_t")[1]      # T tiles with one identity block: one product
+            if skt or skv or half:
+                fl = fl - (skt * 2 * 2 * 64 ** 3 + skv * 2 * 64 ** 3 + half * 2 * 64 ** 3) / nl
                 by = by - (skt * 3 + skv * 2) * 64 * 64 * (8 if is64 else 4) / nl
             peak = pk["dmma_tflops"] if is64 else pk["ffma_tflops"]
             traffic = traffic_alg = None

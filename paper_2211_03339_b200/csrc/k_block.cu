@@ -114,9 +114,17 @@ __device__ __forceinline__ void decode_upper(int idx, int &a, int &c)
     a = idx - c * (c - 1) / 2;
 }
 
-// issue the loads of work item `item` into stage buffers (X, Ua, Uc)
+// rotation block k of this block round is exactly I (no rotation in K3)
+// (`skips` = p.uid && *p.nid > 0, read once per CTA)
+__device__ __forceinline__ bool block_identity(const ApplyArgs &p, int k, bool skips)
+{
+    return skips && p.uid[k] != 0;
+}
+
+// issue the loads of work item `item` into stage buffers (X, Ua, Uc); fp64 T
+// tiles with one identity block skip that block's load (see k_block_apply)
 template <typename R, int NTH = NT>
-__device__ __forceinline__ void issue_item(const ApplyArgs &p, int item, R *X, R *Ua, R *Uc)
+__device__ __forceinline__ void issue_item(const ApplyArgs &p, int item, R *X, R *Ua, R *Uc, bool skips = false)
 {
     constexpr int LD = Lay<R>::LD, EPC = 16 / sizeof(R), CPC = TW / EPC;   // elements / chunks per column
     const int mb = p.S.nb >> 1;
@@ -131,12 +139,13 @@ __device__ __forceinline__ void issue_item(const ApplyArgs &p, int item, R *X, R
         decode_upper(item, a, c);
         const int2 pa = bsr[a], pc = bsr[c];
         const int2 rr = f32 ? pc : pa, cc = f32 ? pa : pc;
+        const bool la = f32 || !block_identity(p, a, skips), lc = f32 || !block_identity(p, c, skips);
         const R *T = (const R *)p.T;
         for (int e = threadIdx.x; e < TW * CPC; e += NTH) {
             const int lj = e / CPC, li = (e - lj * CPC) * EPC;
             cp16(X + li + lj * LD, T + gidx(rr, li) + (int64_t)gidx(cc, lj) * p.ldt, 16);
-            cp16(Ua + li + lj * LD, UbO + (size_t)a * TW * TW + li + lj * TW, 16);
-            cp16(Uc + li + lj * LD, UbO + (size_t)c * TW * TW + li + lj * TW, 16);
+            if (la) cp16(Ua + li + lj * LD, UbO + (size_t)a * TW * TW + li + lj * TW, 16);
+            if (lc) cp16(Uc + li + lj * LD, UbO + (size_t)c * TW * TW + li + lj * TW, 16);
         }
     } else {
         const int idx = item - p.ntT, c = idx % mb, r0 = (idx / mb) * TW;
@@ -185,7 +194,7 @@ __global__ void __launch_bounds__(NT) k_block_apply(ApplyArgs p)
     };
     int item = advance(blockIdx.x);
     if (STAGES == 2) {
-        if (item < total) issue_item<R>(p, item, buf, buf + TW * LD, buf + 2 * TW * LD);
+        if (item < total) issue_item<R>(p, item, buf, buf + TW * LD, buf + 2 * TW * LD, skips);
         cp_commit();
     }
     for (int it = 0; item < total; ++it, item = advance(item + gridDim.x)) {
@@ -193,11 +202,11 @@ __global__ void __launch_bounds__(NT) k_block_apply(ApplyArgs p)
         if (STAGES == 2) {
             const int next = advance(item + gridDim.x);
             R *nb = buf + (size_t)(3 * (s ^ 1)) * TW * LD;
-            if (next < total) issue_item<R>(p, next, nb, nb + TW * LD, nb + 2 * TW * LD);
+            if (next < total) issue_item<R>(p, next, nb, nb + TW * LD, nb + 2 * TW * LD, skips);
             cp_commit();
             cp_wait1();
         } else {
-            issue_item<R>(p, item, buf, buf + TW * LD, buf + 2 * TW * LD);
+            issue_item<R>(p, item, buf, buf + TW * LD, buf + 2 * TW * LD, skips);
             cp_commit();
             cp_wait0();
         }
@@ -217,12 +226,20 @@ __global__ void __launch_bounds__(NT) k_block_apply(ApplyArgs p)
                 __syncthreads();
                 store_op(o, (float *)x, (float *)ua);               // W and W^T
             } else {
+                // one identity block: a single product (the identity's load was skipped)
+                const bool ia = block_identity(p, a, skips), ic = block_identity(p, c, skips);
                 Acc<R> acc;
-                tile_mm<true>(ua, x, acc);                           // Y = Ua^T X
-                __syncthreads();
-                acc.each([&](int i, int j, R v) { x[i + j * LD] = v; });
-                __syncthreads();
-                tile_mm<false>(x, uc, acc);                          // W = Y Uc
+                if (ia) {
+                    tile_mm<false>(x, uc, acc);                      // W = X Uc
+                } else if (ic) {
+                    tile_mm<true>(ua, x, acc);                       // W = Ua^T X
+                } else {
+                    tile_mm<true>(ua, x, acc);                       // Y = Ua^T X
+                    __syncthreads();
+                    acc.each([&](int i, int j, R v) { x[i + j * LD] = v; });
+                    __syncthreads();
+                    tile_mm<false>(x, uc, acc);                      // W = Y Uc
+                }
                 __syncthreads();
                 acc.each([&](int i, int j, R v) { x[i + j * LD] = v; ua[j + i * LD] = v; });   // W and W^T
             }
@@ -529,14 +546,17 @@ __global__ void __launch_bounds__(WS_NT, 1) k_block_apply_f32ws(ApplyArgs p, con
                 int a, c;
                 decode_upper(item, a, c);
                 const int2 pa = bsr[a], pc = bsr[c];
-                mbar_arrive_tx(bar, 3 * SH_TILE * sizeof(float));
-                // X^T = T(P_c, P_a): box (rows of block h of pc, columns of block v of pa)
-                tma_box(x, &tmT, pc.x * BW, pa.x * BW, bar);
-                tma_box(x + SH_HALF, &tmT, pc.y * BW, pa.x * BW, bar);
-                tma_box(x + BW * BW, &tmT, pc.x * BW, pa.y * BW, bar);
-                tma_box(x + SH_HALF + BW * BW, &tmT, pc.y * BW, pa.y * BW, bar);
-                bulk_g2s(ua, UbS + (size_t)a * SH_TILE, SH_TILE * sizeof(float), bar);
-                bulk_g2s(uc, UbS + (size_t)c * SH_TILE, SH_TILE * sizeof(float), bar);
+                // one identity block: one product, no load of that block; if U_a = I the
+                // consumer computes X U_c and needs X = T(P_a, P_c) itself, else X^T = T(P_c, P_a)
+                const bool ia = block_identity(p, a, skips), ic = block_identity(p, c, skips);
+                mbar_arrive_tx(bar, (ia || ic ? 2 : 3) * SH_TILE * sizeof(float));
+                const int2 br = ia ? pa : pc, bc = ia ? pc : pa;   // box rows / columns
+                tma_box(x, &tmT, br.x * BW, bc.x * BW, bar);
+                tma_box(x + SH_HALF, &tmT, br.y * BW, bc.x * BW, bar);
+                tma_box(x + BW * BW, &tmT, br.x * BW, bc.y * BW, bar);
+                tma_box(x + SH_HALF + BW * BW, &tmT, br.y * BW, bc.y * BW, bar);
+                if (!ia) bulk_g2s(ua, UbS + (size_t)a * SH_TILE, SH_TILE * sizeof(float), bar);
+                if (!ic) bulk_g2s(uc, UbS + (size_t)c * SH_TILE, SH_TILE * sizeof(float), bar);
             } else {
                 const int idx = item - p.ntT, c = idx % mb, r0 = (idx / mb) * TW;
                 const int2 pc = bsr[c];
@@ -565,11 +585,18 @@ __global__ void __launch_bounds__(WS_NT, 1) k_block_apply_f32ws(ApplyArgs p, con
             int a, c;
             decode_upper(item, a, c);
             const int2 pa = bsr[a], pc = bsr[c];
-            tile_op_sh(ua, x, acc, gt);                      // Y = U_a^T X
-            group_sync(bar_id);
-            store_op_sh(acc, x, nullptr, gt);
-            group_sync(bar_id);
-            tile_op_sh(x, uc, acc, gt);                      // W = Y U_c
+            const bool ia = block_identity(p, a, skips), ic = block_identity(p, c, skips);
+            if (ia) {
+                tile_op_sh(x, uc, acc, gt);                  // W = X U_c   (x = X)
+            } else if (ic) {
+                tile_op_sh(ua, x, acc, gt);                  // W = U_a^T X (x = X^T)
+            } else {
+                tile_op_sh(ua, x, acc, gt);                  // Y = U_a^T X
+                group_sync(bar_id);
+                store_op_sh(acc, x, nullptr, gt);
+                group_sync(bar_id);
+                tile_op_sh(x, uc, acc, gt);                  // W = Y U_c
+            }
             group_sync(bar_id);
             store_op_sh(acc, x, ua, gt);                     // W and W^T
             group_sync(bar_id);
@@ -777,13 +804,19 @@ mpj_status block_sweep(R *T, int64_t ldt, R *V, int64_t ldv, int vrows, const De
         std::vector<int> h(ds.nb - 1);
         MPJ_CK(cudaMemcpyAsync(h.data(), nid, h.size() * sizeof(int), cudaMemcpyDeviceToHost, st));
         MPJ_CK(cudaStreamSynchronize(st));
-        long long ids = 0, skt = 0, skv = 0;
-        for (int c : h) { ids += c; skt += (long long)c * (c - 1) / 2; skv += (long long)c * ((vrows + TW - 1) / TW); }
+        long long ids = 0, skt = 0, skv = 0, half = 0;
+        for (int c : h) {
+            ids += c;
+            skt += (long long)c * (c - 1) / 2;
+            skv += (long long)c * ((vrows + TW - 1) / TW);
+            if (sizeof(R) == 8 || fp32_apply_kind() == 2) half += (long long)c * (mb - c);   // one product
+        }
         const std::string base(napply);
         prof_add(base + ".identity_blocks", ids);
         prof_add(base + ".items", (long long)(ds.nb - 1) * (ap.ntT + ap.ntV));
         prof_add(base + ".skipped_t", skt);
         prof_add(base + ".skipped_v", skv);
+        prof_add(base + ".half_t", half);
     }
     return MPJ_OK;
 }
