@@ -325,7 +325,8 @@ def run_svd(args):
     ms = e0.elapsed_time(e1) / args.steps
     rep = res.report
     kern = {}
-    for name in ("block_apply_f64", "block_apply_f32", "svd_gram_f64", "svd_gram_f32"):
+    for name in ("svd_gram_f64", "svd_gram_f32", "svd_solve_f64", "svd_solve_f32", "svd_apply_f64",
+                 "svd_apply_f32"):
         sec, cnt = mpj.profile_get(name)
         if cnt:
             kern[name] = {"seconds_per_step": sec / args.steps, "launches": cnt, "avg_ms": 1e3 * sec / cnt}

@@ -823,20 +823,23 @@ mpj_status block_sweep(R *T, int64_t ldt, R *V, int64_t ldv, int vrows, const De
 
 // M(:, P_c) <- M(:, P_c) U_c for every block pair c of block round Rb (M has
 // `rows` rows): the column update of the one-sided (SVD) block variant.
+// uid / nid (optional): identity flags and count of this block round (skip).
 template <typename R>
 void launch_block_apply_cols(R *M, int64_t ld, int rows, const DevSched &ds, int Rb, const R *Ubuf,
-                             cudaStream_t st)
+                             cudaStream_t st, const int *uid, const int *nid)
 {
     Sched S;
     S.bsched = ds.bsched; S.lsched = ds.lsched; S.b = ds.b; S.nb = ds.nb; S.np = ds.np;
     ApplyArgs ap;
-    ap.T = nullptr; ap.ldt = 0; ap.M = M; ap.ldm = ld; ap.mrows = rows; ap.S = S; ap.Rb = Rb; ap.Ubuf = Ubuf; ap.uid = nullptr; ap.nid = nullptr;
+    ap.T = nullptr; ap.ldt = 0; ap.M = M; ap.ldm = ld; ap.mrows = rows; ap.S = S; ap.Rb = Rb; ap.Ubuf = Ubuf; ap.uid = uid; ap.nid = nid;
     ap.ntT = 0;
     ap.ntV = ((rows + TW - 1) / TW) * (ds.nb / 2);
     launch_apply<R>(ap, st);
 }
-template void launch_block_apply_cols<double>(double *, int64_t, int, const DevSched &, int, const double *, cudaStream_t);
-template void launch_block_apply_cols<float>(float *, int64_t, int, const DevSched &, int, const float *, cudaStream_t);
+template void launch_block_apply_cols<double>(double *, int64_t, int, const DevSched &, int, const double *,
+                                              cudaStream_t, const int *, const int *);
+template void launch_block_apply_cols<float>(float *, int64_t, int, const DevSched &, int, const float *,
+                                             cudaStream_t, const int *, const int *);
 
 template size_t block_scratch_bytes<double>(int, int);
 template size_t block_scratch_bytes<float>(int, int);

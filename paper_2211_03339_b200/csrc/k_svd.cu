@@ -79,7 +79,8 @@ __global__ void __launch_bounds__(NT) k_gram(const R *__restrict__ C, int64_t ld
 
 template <typename R>
 __global__ void __launch_bounds__(NTW) k_svd_solve(const double *__restrict__ Gpart, int splits, Sched S, int Rb,
-                                                   R nu, R *__restrict__ Ubuf, unsigned long long *__restrict__ cnt)
+                                                   R nu, R *__restrict__ Ubuf, unsigned long long *__restrict__ cnt,
+                                                   int *__restrict__ uid, int *__restrict__ nid)
 {
     constexpr int LD = LayK<R>::LD;
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -110,7 +111,11 @@ __global__ void __launch_bounds__(NTW) k_svd_solve(const double *__restrict__ Gp
         Ua[li + lj * TW] = U[li + lj * LD];
         if (sizeof(R) == 4) UaT[li + lj * TW] = U[lj + li * LD];
     }
-    if (threadIdx.x == 0 && nrot) atomicAdd(cnt, (unsigned long long)nrot);
+    if (threadIdx.x == 0) {
+        if (nrot) atomicAdd(cnt, (unsigned long long)nrot);
+        uid[a] = nrot == 0;   // U_a exactly I: the column updates skip block pair a
+        if (nrot == 0) atomicAdd(nid, 1);
+    }
 }
 
 __global__ void __launch_bounds__(256) k_colnorm(const double *__restrict__ C, int64_t ldc, int m,
@@ -171,6 +176,7 @@ struct SvdPlan {
     int2 *bsched, *lsched;
     void *Ubuf;
     unsigned long long *cnt;
+    int *uid;                 // mb identity flags + (nb - 1) per-round identity counts
     int *rank, *flag;
     void *orth_ws;
 };
@@ -205,6 +211,7 @@ static void carve_svd(char *base, size_t &off, int64_t m, int64_t n, SvdPlan &p)
     p.bsched = (int2 *)take((size_t)std::max(nb - 1, 1) * std::max(nb / 2, 1) * sizeof(int2));
     p.lsched = (int2 *)take((size_t)(BW - 1) * (BW / 2) * sizeof(int2));
     p.cnt = (unsigned long long *)take(64);
+    p.uid = (int *)take((size_t)(p.mb + std::max(nb - 1, 1)) * sizeof(int));
     p.rank = (int *)take(p.np * 4);
     p.flag = (int *)take(64);
     p.orth_ws = take(orth_workspace(p.np));
@@ -221,14 +228,20 @@ static mpj_status svd_block_sweep(SvdPlan &p, R *C, R *V, const DevSched &ds, R 
     MPJ_CK(cudaFuncSetAttribute(k_svd_solve<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_du));
     const bool prof = prof_on();
     const char *ng = sizeof(R) == 8 ? "svd_gram_f64" : "svd_gram_f32";
+    const char *ns = sizeof(R) == 8 ? "svd_solve_f64" : "svd_solve_f32";
+    const char *na = sizeof(R) == 8 ? "svd_apply_f64" : "svd_apply_f32";
+    int *uid = p.uid, *nid = p.uid + p.mb;
+    MPJ_CK(cudaMemsetAsync(nid, 0, (size_t)(ds.nb - 1) * sizeof(int), st));
     for (int Rb = 0; Rb < ds.nb - 1; ++Rb) {
         if (prof) prof_mark(ng, st, true);
         k_gram<R><<<dim3(p.mb, p.splits), NT, sm_x, st>>>(C, p.m, (int)p.m, S, Rb, p.kc, p.Gpart, p.splits);
-        if (prof) prof_mark(ng, st, false);
-        k_svd_solve<R><<<p.mb, NTW, sm_du, st>>>(p.Gpart, p.splits, S, Rb, nu, (R *)p.Ubuf, p.cnt);
+        if (prof) { prof_mark(ng, st, false); prof_mark(ns, st, true); }
+        k_svd_solve<R><<<p.mb, NTW, sm_du, st>>>(p.Gpart, p.splits, S, Rb, nu, (R *)p.Ubuf, p.cnt, uid, nid + Rb);
         count_launch(2);
-        launch_block_apply_cols<R>(C, p.m, (int)p.m, ds, Rb, (const R *)p.Ubuf, st);
-        launch_block_apply_cols<R>(V, p.np, p.np, ds, Rb, (const R *)p.Ubuf, st);
+        if (prof) { prof_mark(ns, st, false); prof_mark(na, st, true); }
+        launch_block_apply_cols<R>(C, p.m, (int)p.m, ds, Rb, (const R *)p.Ubuf, st, uid, nid + Rb);
+        launch_block_apply_cols<R>(V, p.np, p.np, ds, Rb, (const R *)p.Ubuf, st, uid, nid + Rb);
+        if (prof) prof_mark(na, st, false);
     }
     return MPJ_OK;
 }
