@@ -448,44 +448,56 @@ def main():
             if items:
                 sk = mpj.profile_get(name + ".skipped_t")[1] + mpj.profile_get(name + ".skipped_v")[1]
                 kernels[name]["items_skipped_frac"] = sk / items
+    def roof_of(name, sec, nl):
+        """Roofline of an apply kernel over `nl` launches taking `sec` seconds
+        (name: profiler key, e.g. block_apply_f64 or block_apply_f64.sweep1)."""
+        base = name.split(".")[0]
+        is64 = base.endswith("f64")
+        avg = sec / nl
+        fl, by = flops_apply, bytes_apply * (1 if is64 else 0.5)
+        if base.startswith("mg_apply"):     # per rank: every slot a x own slots c, no mirror
+            mbl = mb // ws
+            fl = mbl * (mb - 1) * 2 * 2 * 64 ** 3 + (rep.n_padded // 64) * mbl * 2 * 64 ** 3
+            by = (mbl * (mb - 1) * 2 + (rep.n_padded // 64) * mbl * 2) * 64 * 64 * (8 if is64 else 4)
+        # tiles of identity rotation blocks are skipped (exactly unchanged) or take one
+        # product: count only the work done, averaged over the launches
+        skt = mpj.profile_get(name + ".skipped_t")[1]
+        skv = mpj.profile_get(name + ".skipped_v")[1]
+        half = mpj.profile_get(name + ".half_t")[1]
+        if skt or skv or half:
+            fl = fl - (skt * 2 * 2 * 64 ** 3 + skv * 2 * 64 ** 3 + half * 2 * 64 ** 3) / nl
+            by = by - (skt * 3 + skv * 2) * 64 * 64 * (8 if is64 else 4) / nl
+        peak = pk["dmma_tflops"] if is64 else pk["ffma_tflops"]
+        traffic = traffic_alg = None
+        tp = os.path.join(ROOT, "profiles", "r01_traffic.json")
+        if os.path.exists(tp):
+            t = json.load(open(tp)).get(base)
+            if t and t.get("n_padded") == rep.n_padded:
+                traffic = t["dram_bytes_per_launch"]
+                traffic_alg = t.get("algorithmic_bytes_per_launch")
+        return {"kernel": name, "bound": "tensor" if is64 else "alu",
+                "achieved": fl / avg / 1e12, "peak": peak, "unit": "TFLOP/s",
+                "frac": fl / avg / 1e12 / peak, "traffic": traffic,
+                # traffic is from one full launch (no identity blocks); compare it with that
+                # launch's algorithmic bytes, not the skip-averaged ones below
+                "traffic_launch_algorithmic_bytes": traffic_alg,
+                "algorithmic_flop_per_launch": fl, "algorithmic_bytes_per_launch": by,
+                "avg_launch_ms": avg * 1e3, "launches": nl,
+                "hbm_frac": by / avg / 1e9 / pk["hbm_gbs"],
+                "share_of_step": sec / args.steps / (ms * 1e-3),
+                "peak_src": pk["fp_src"]}
+
     roof = None
+    rooflines = {}
+    for name in ("block_apply_f64", "block_apply_f32", "mg_apply_f64", "mg_apply_f32"):
+        for key in (name, name + ".sweep1"):
+            sec, cnt = mpj.profile_get(key)
+            if cnt:
+                rooflines[key] = roof_of(key, sec, cnt)
     if kernels:
         dom = max(kernels, key=lambda k: kernels[k]["seconds_per_step"])
-        avg = kernels[dom]["avg_ms"] * 1e-3
-        if dom.startswith("block_apply") or dom.startswith("mg_apply"):
-            is64 = dom.endswith("f64")
-            fl, by = flops_apply, bytes_apply * (1 if is64 else 0.5)
-            if dom.startswith("mg_apply"):     # per rank: every slot a x own slots c, no mirror
-                mbl = mb // ws
-                fl = mbl * (mb - 1) * 2 * 2 * 64 ** 3 + (rep.n_padded // 64) * mbl * 2 * 64 ** 3
-                by = (mbl * (mb - 1) * 2 + (rep.n_padded // 64) * mbl * 2) * 64 * 64 * (8 if is64 else 4)
-            # tiles of identity rotation blocks are skipped (exactly unchanged):
-            # count only the work done, averaged over the launches
-            nl = kernels[dom]["launches"]
-            skt = mpj.profile_get(dom + ".skipped_t")[1]
-            skv = mpj.profile_get(dom + ".skipped_v")[1]
-            half = mpj.profile_get(dom + ".half_t")[1]      # T tiles with one identity block: one product
-            if skt or skv or half:
-                fl = fl - (skt * 2 * 2 * 64 ** 3 + skv * 2 * 64 ** 3 + half * 2 * 64 ** 3) / nl
-                by = by - (skt * 3 + skv * 2) * 64 * 64 * (8 if is64 else 4) / nl
-            peak = pk["dmma_tflops"] if is64 else pk["ffma_tflops"]
-            traffic = traffic_alg = None
-            tp = os.path.join(ROOT, "profiles", "r01_traffic.json")
-            if os.path.exists(tp):
-                t = json.load(open(tp)).get(dom)
-                if t and t.get("n_padded") == rep.n_padded:
-                    traffic = t["dram_bytes_per_launch"]
-                    traffic_alg = t.get("algorithmic_bytes_per_launch")
-            roof = {"kernel": dom, "bound": "tensor" if is64 else "alu",
-                    "achieved": fl / avg / 1e12, "peak": peak, "unit": "TFLOP/s",
-                    "frac": fl / avg / 1e12 / peak, "traffic": traffic,
-                    # traffic is from one full launch (no identity blocks); compare it with that
-                    # launch's algorithmic bytes, not the skip-averaged ones below
-                    "traffic_launch_algorithmic_bytes": traffic_alg,
-                    "algorithmic_flop_per_launch": fl, "algorithmic_bytes_per_launch": by,
-                    "hbm_frac": by / avg / 1e9 / pk["hbm_gbs"],
-                    "share_of_step": kernels[dom]["seconds_per_step"] / (ms * 1e-3),
-                    "peak_src": pk["fp_src"]}
+        if dom in rooflines:
+            roof = dict(rooflines[dom])
         else:
             roof = {"kernel": dom, "bound": "alu", "achieved": None, "peak": None, "unit": "TFLOP/s",
                     "frac": None, "traffic": None}
@@ -556,7 +568,7 @@ def main():
             "check": {"residual": res_rel, "orthogonality": orth, "max_dlam_rel": dlam,
                       "tol_residual": n * 1e-15, "tol_orth": n * 1e-15, "tol_dlam": 1e-13},
             "roofline": roof, "kernels": kernels, "gpu_launches": launches,
-            "clocks": clk.summary(), "e2e": e2e, "cpu_baseline": cpu,
+            "clocks": clk.summary(), "e2e": e2e, "cpu_baseline": cpu, "rooflines": rooflines,
         }
         print(json.dumps(line))
     if ws > 1:

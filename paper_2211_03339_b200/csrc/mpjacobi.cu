@@ -37,7 +37,7 @@ mpj_status svd_run(const double *A, int64_t m, int64_t n, int64_t lda, double *S
 // Block-variant entry (k_block.cu).
 template <typename R>
 mpj_status block_sweep(R *T, int64_t ldt, R *V, int64_t ldv, int vrows, const DevSched &S, R nu,
-                       int rule, unsigned long long *cnt, void *scratch, cudaStream_t st);
+                       int rule, unsigned long long *cnt, void *scratch, cudaStream_t st, bool first_sweep);
 template <typename R>
 size_t block_scratch_bytes(int np, int b);
 
@@ -340,7 +340,7 @@ static mpj_status jacobi_run(Ctx &cx, R *T, R *V, int n, int b, int variant, dou
         if (max_rounds >= 0 && rounds_done >= max_rounds) { status = MPJ_OK; break; }
         ++sweeps;
         if (variant == MPJ_VARIANT_BLOCK) {
-            MPJ_TRY(block_sweep<R>(T, np, V, np, np, ds, nu, rule, jb.cnt, jb.block_scratch, st));
+            MPJ_TRY(block_sweep<R>(T, np, V, np, np, ds, nu, rule, jb.cnt, jb.block_scratch, st, sweeps == 1));
             rounds_done += hs.rounds;
         } else if (use_graph) {
             if (!gexec) {

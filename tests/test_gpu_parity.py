@@ -396,6 +396,19 @@ def test_eig_mg_emulated(mpj, orc, n, mode):
     assert np.max(np.abs(lams[2] - lams[0])) <= 1e-14 * np.abs(lams[0]).max()
 
 
+@pytest.mark.parametrize("n", [256, 300])
+def test_eig_mg_nccl_single_rank(mpj, n):
+    """The real NCCL path (communicator from mpjacobi_nccl_unique_id, U
+    all-gather and off-norm all-reduce through NCCL) with one rank on this GPU:
+    bit-identical to the emulated G = 1 run (same kernels, same order)."""
+    A, _ = W.example1(n, 1e3, 4, W.seed_for(4, 4, 1e3) + n)
+    emu = mpj.eig_mg(dev(A), emulate_ranks=1)
+    nccl = mpj.eig_mg(dev(A), nccl_id=mpj.nccl_unique_id(), rank=0, nranks=1)
+    assert nccl.sweeps == emu.sweeps
+    assert np.array_equal(host(nccl.lam), host(emu.lam))
+    assert np.array_equal(host(nccl.V), host(emu.V))
+
+
 # ----------------------------------------------------------------- BASELINE config 2 (n = 1024)
 @pytest.mark.parametrize("kind,mode,kappa", [("uniform", 4, 1e3), ("clustered", 4, 1e3), ("ex1_mode1", 1, 1e3)])
 def test_config2_n1024_mp_vs_plain(mpj, kind, mode, kappa):
