@@ -7,9 +7,10 @@
 // blocked Gram-Schmidt with reorthogonalisation, panel width 64:
 //   for each panel X = Z(:, p0:p0+64):
 //     twice:  R = Q(:, :p0)^T X ;  X = X - Q(:, :p0) R        (CGS2, DMMA GEMMs)
-//     twice:  G = X^T X ; G = R^T R (Cholesky) ; X = X R^{-1} (CholeskyQR2)
+//     twice:  G = X^T X ; G = R^T R (Cholesky) ; X = X R^{-1} (CholeskyQR2,
+//             the last step as a row-parallel triangular solve)
 // Every step is a dense fp64 tensor-core product except the 64 x 64
-// Cholesky / triangular inverse (one CTA).  Orthogonality O(omega), same Q as
+// Cholesky (one CTA) and the row-wise forward substitution.  Orthogonality O(omega), same Q as
 // MGS to O(n omega) (tests/test_gpu_parity.py::test_orth_cgs2_matches_mgs).
 #include "mpj_device.cuh"
 #include "mpj_internal.h"
@@ -22,58 +23,78 @@ namespace {
 constexpr int kPanel = 64;
 constexpr int kLDG = kPanel + 1;
 
-// G (w x w, ld w) -> Rinv (w x w, ld w) with G = R^T R, R upper, Rinv = R^{-1};
-// fail = 1 on a non-positive pivot.
-__global__ void __launch_bounds__(256) k_chol_inv(const double *__restrict__ G, int w, double *__restrict__ Rinv,
-                                                  int *__restrict__ fail)
+// Cholesky G = R^T R of a w x w panel Gram matrix (w <= 64): R upper (ld w,
+// zero below the diagonal); fail = 1 on a non-positive pivot.  Right-looking;
+// thread t owns column j = t % 64 and rows i = t / 64 (mod 4) of the trailing
+// triangle, so a step is a few FMAs per thread and two barriers (k_chol_inv's
+// flat loop over all w^2 entries with an integer division per entry made it
+// issue-bound: 150 us per call, 1% of an n = 8192 EVD).
+__global__ void __launch_bounds__(256) k_chol(const double *__restrict__ G, int w, double *__restrict__ Rf,
+                                              int *__restrict__ fail)
 {
-    __shared__ double A[kPanel * kLDG];    // working copy, upper triangle -> R
-    const int tid = threadIdx.x;
-    for (int e = tid; e < w * w; e += blockDim.x) {
-        const int i = e % w, j = e / w;
-        A[i + j * kLDG] = 0.5 * (G[i + j * w] + G[j + i * w]);
-        Rinv[i + j * w] = 0.0;
-    }
+    __shared__ double A[kPanel * kLDG];
+    const int tid = threadIdx.x, cj = tid & (kPanel - 1), ri = tid >> 6;
+    if (cj < w)
+        for (int i = ri; i <= cj; i += 4) A[i + cj * kLDG] = 0.5 * (G[i + cj * w] + G[cj + i * w]);
     __syncthreads();
-    __shared__ int bad;
-    if (tid == 0) bad = 0;
-    __syncthreads();
+    bool bad = false;
     for (int k = 0; k < w; ++k) {
-        // pivot
         const double d = A[k + k * kLDG];
-        if (!(d > 0.0)) { if (tid == 0) bad = 1; }
         const double r = sqrt(fmax(d, 1e-300));
+        bad |= !(d > 0.0);
+        if (ri == 0 && cj > k && cj < w) A[k + cj * kLDG] /= r;      // row k of R (A(k,k) is written below)
         __syncthreads();
-        // row k of R:  R(k, j) = A(k, j) / r, j >= k
-        for (int j = k + tid; j < w; j += blockDim.x) A[k + j * kLDG] = (j == k) ? r : A[k + j * kLDG] / r;
-        __syncthreads();
-        // trailing update A(i, j) -= R(k, i) R(k, j), k < i <= j
-        for (int e = tid; e < w * w; e += blockDim.x) {
-            const int i = e % w, j = e / w;
-            if (i > k && j >= i) A[i + j * kLDG] = __fma_rn(-A[k + i * kLDG], A[k + j * kLDG], A[i + j * kLDG]);
+        if (cj > k && cj < w) {                                       // A(i, j) -= R(k, i) R(k, j), k < i <= j
+            const double rkj = A[k + cj * kLDG];
+            for (int i = k + 1 + ri; i <= cj; i += 4) A[i + cj * kLDG] = __fma_rn(-A[k + i * kLDG], rkj, A[i + cj * kLDG]);
         }
+        if (ri == 0 && cj == k) A[k + k * kLDG] = r;
         __syncthreads();
     }
-    // R^{-1}: column j by back substitution (thread j), into the strictly lower
-    // part of A (transposed: X(i, j) stored at A(j, i), i < j) and the diagonal buffer
-    __shared__ double dinv[kPanel];
-    if (tid < w) dinv[tid] = 1.0 / A[tid + tid * kLDG];
-    __syncthreads();
-    if (tid < w) {
-        const int j = tid;
-        for (int i = j - 1; i >= 0; --i) {
-            double acc = A[i + j * kLDG] * dinv[j];   // k = j term: R(i,j) X(j,j)
-            for (int k = i + 1; k < j; ++k) acc = __fma_rn(A[i + k * kLDG], A[j + k * kLDG], acc);
-            A[j + i * kLDG] = -acc * dinv[i];          // X(i, j) = -acc / R(i,i)
-        }
-    }
-    __syncthreads();
-    for (int e = tid; e < w * w; e += blockDim.x) {
-        const int i = e % w, j = e / w;
-        if (i < j) Rinv[i + j * w] = A[j + i * kLDG];
-        else if (i == j) Rinv[i + j * w] = dinv[i];
-    }
+    if (cj < w)
+        for (int i = ri; i < w; i += 4) Rf[i + cj * w] = (i <= cj) ? A[i + cj * kLDG] : 0.0;
     if (tid == 0 && bad) *fail = 1;
+}
+
+// Q(r, :) = X(r, :) R^{-1} for every row r (forward substitution
+// q_j = (x_j - sum_{k<j} q_k R(k, j)) / R(j, j)): one thread per row, the row in
+// registers, R broadcast from shared memory.  Replaces R^{-1} + a GEMM.
+template <int W>
+__global__ void __launch_bounds__(64) k_trsm_rows(const double *__restrict__ X, int64_t ldx, int64_t m,
+                                                  const double *__restrict__ Rf, double *__restrict__ Q, int64_t ldq)
+{
+    __shared__ double R[W * W];
+    for (int e = threadIdx.x; e < W * W; e += blockDim.x) R[e] = Rf[e];
+    __syncthreads();
+    const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= m) return;
+    double q[W];
+    #pragma unroll
+    for (int j = 0; j < W; ++j) q[j] = X[r + j * ldx];
+    #pragma unroll
+    for (int j = 0; j < W; ++j) {
+        double acc = q[j];
+        #pragma unroll
+        for (int k = 0; k < j; ++k) acc = __fma_rn(-q[k], R[k + j * W], acc);
+        q[j] = __ddiv_rn(acc, R[j + j * W]);
+        Q[r + j * ldq] = q[j];
+    }
+}
+
+// the same for a narrow last panel (w < 64)
+__global__ void __launch_bounds__(64) k_trsm_rows_w(const double *__restrict__ X, int64_t ldx, int64_t m, int w,
+                                                    const double *__restrict__ Rf, double *__restrict__ Q, int64_t ldq)
+{
+    __shared__ double R[kPanel * kPanel];
+    for (int e = threadIdx.x; e < w * w; e += blockDim.x) R[e] = Rf[e];
+    __syncthreads();
+    const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= m) return;
+    for (int j = 0; j < w; ++j) {
+        double acc = X[r + j * ldx];
+        for (int k = 0; k < j; ++k) acc = __fma_rn(-Q[r + k * ldq], R[k + j * w], acc);
+        Q[r + j * ldq] = __ddiv_rn(acc, R[j + j * w]);
+    }
 }
 }  // namespace
 
@@ -85,7 +106,7 @@ size_t dgemm_scratch_elems(int64_t m, int64_t n)
 
 size_t orth_workspace(int64_t n)
 {
-    // R (n x 64) + S (n x 64) + split-K scratch + G + Rinv + flag
+    // R (n x 64) + S (n x 64) + split-K scratch + G + the Cholesky factor + flag
     return ((size_t)2 * n * kPanel + dgemm_scratch_elems(n, kPanel) + 2 * kPanel * kPanel + 64) * sizeof(double);
 }
 
@@ -97,8 +118,8 @@ mpj_status orth_cgs2(const double *Z, int64_t ldz, double *Q, int64_t ldq, int64
     double *scratch = S + (size_t)m * kPanel;
     const size_t scratch_elems = dgemm_scratch_elems(n, kPanel);
     double *G = scratch + scratch_elems;
-    double *Rinv = G + kPanel * kPanel;
-    int *fail = (int *)(Rinv + kPanel * kPanel);
+    double *Rf = G + kPanel * kPanel;      // Cholesky factor of the panel Gram matrix
+    int *fail = (int *)(Rf + kPanel * kPanel);
 
     MPJ_CK(cudaMemsetAsync(fail, 0, sizeof(int), st));
     if (Q != Z || ldq != ldz) launch_copy_pad<double, double>(Z, ldz, (int)m, (int)n, Q, ldq, (int)m, (int)n, st);
@@ -120,9 +141,11 @@ mpj_status orth_cgs2(const double *Z, int64_t ldz, double *Q, int64_t ldq, int64
             double *dst = rep == 0 ? S : X;
             const int64_t ldd = rep == 0 ? m : ldq;
             launch_dgemm(true, false, w, w, m, 1.0, src, lds, src, lds, 0.0, G, w, st, scratch, scratch_elems);
-            k_chol_inv<<<1, 256, 0, st>>>(G, w, Rinv, fail);
-            count_launch();
-            launch_dgemm(false, false, m, w, w, 1.0, src, lds, Rinv, w, 0.0, dst, ldd, st);
+            k_chol<<<1, 256, 0, st>>>(G, w, Rf, fail);
+            const int nblk = (int)((m + 63) / 64);
+            if (w == kPanel) k_trsm_rows<kPanel><<<nblk, 64, 0, st>>>(src, lds, m, Rf, dst, ldd);
+            else k_trsm_rows_w<<<nblk, 64, 0, st>>>(src, lds, m, w, Rf, dst, ldd);
+            count_launch(2);
         }
     }
     int h_fail = 0;
