@@ -28,33 +28,58 @@ namespace {
 
 using namespace blk;
 
-// partial Gram of block pair a over rows [z*kc, min(m, (z+1)*kc)), fp64 partials
+__device__ __forceinline__ void g_cp16(void *dst, const void *src, int src_bytes)
+{
+    const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(d), "l"(src), "r"(src_bytes));
+}
+
+// partial Gram of block pair a over rows [z*kc, min(m, (z+1)*kc)), fp64 partials.
+// 64-row chunks double-buffered with cp.async (rows past r1 zero-filled).
+// Only the upper triangle of G is read (k_svd_solve), so in fp64 the two warps
+// of the lower-left 32 x 32 quadrant (rows 32.., columns ..31) skip it: 3/4 of
+// the DMMA work.
 template <typename R>
 __global__ void __launch_bounds__(NT) k_gram(const R *__restrict__ C, int64_t ldc, int m, Sched S, int Rb, int kc,
                                              double *__restrict__ Gpart, int splits)
 {
-    constexpr int LD = Lay<R>::LD;
+    constexpr int LD = Lay<R>::LD, EPC = 16 / sizeof(R), CPC = TW / EPC;
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    R *X = (R *)smem_raw;
+    R *Xb = (R *)smem_raw;                         // two 64 x LD buffers
     const int a = blockIdx.x, z = blockIdx.y;
     const int mb = S.nb >> 1;
     const int2 bp = S.bsched[Rb * mb + a];
     const int r0 = z * kc, r1 = min(m, r0 + kc);
+    const int warp = threadIdx.x >> 5;
+    const bool lower_left = sizeof(R) == 8 && (warp == 4 || warp == 6);
     Acc<double> tot;
     tot.zero();
     // fp32 products are accumulated per 64-row chunk in fp32, then in fp64
     double totf[16];
     #pragma unroll
     for (int i = 0; i < 16; ++i) totf[i] = 0.0;
-    for (int c0 = r0; c0 < r1; c0 += TW) {
-        for (int e = threadIdx.x; e < TW * TW; e += NT) {
-            const int li = e & (TW - 1), lj = e >> 6;
-            const int gi = c0 + li;
-            X[li + lj * LD] = gi < r1 ? C[gi + (int64_t)gidx(bp, lj) * ldc] : R(0);
+    auto issue = [&](int c0, R *X) {
+        for (int e = threadIdx.x; e < TW * CPC; e += NT) {
+            const int lj = e / CPC, li = (e - lj * CPC) * EPC;
+            const int rem = r1 - (c0 + li);
+            const int bytes = rem >= EPC ? 16 : (rem > 0 ? rem * (int)sizeof(R) : 0);
+            const R *src = C + (bytes ? (int64_t)(c0 + li) : 0) + (int64_t)gidx(bp, lj) * ldc;
+            g_cp16(X + li + lj * LD, src, bytes);
+        }
+        asm volatile("cp.async.commit_group;\n" ::);
+    };
+    if (r0 < r1) issue(r0, Xb);
+    for (int c0 = r0, it = 0; c0 < r1; c0 += TW, ++it) {
+        R *X = Xb + (size_t)(it & 1) * TW * LD;
+        if (c0 + TW < r1) {
+            issue(c0 + TW, Xb + (size_t)((it + 1) & 1) * TW * LD);
+            asm volatile("cp.async.wait_group 1;\n" ::);
+        } else {
+            asm volatile("cp.async.wait_group 0;\n" ::);
         }
         __syncthreads();
         if constexpr (sizeof(R) == 8) {
-            tile_mm_acc<true>((const double *)X, (const double *)X, tot);
+            if (!lower_left) tile_mm_acc<true>((const double *)X, (const double *)X, tot);
         } else {
             Acc<float> part;
             tile_mm<true>((const float *)X, (const float *)X, part);
@@ -67,7 +92,7 @@ __global__ void __launch_bounds__(NT) k_gram(const R *__restrict__ C, int64_t ld
     }
     double *G = Gpart + ((size_t)a * splits + z) * TW * TW;
     if constexpr (sizeof(R) == 8) {
-        tot.each([&](int i, int j, double v) { G[i + j * TW] = v; });
+        if (!lower_left) tot.each([&](int i, int j, double v) { G[i + j * TW] = v; });
     } else {
         const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;   // Acc<float> mapping: rows tx+16u, cols ty+16w
         #pragma unroll
@@ -223,7 +248,7 @@ static mpj_status svd_block_sweep(SvdPlan &p, R *C, R *V, const DevSched &ds, R 
     Sched S;
     S.bsched = ds.bsched; S.lsched = ds.lsched; S.b = ds.b; S.nb = ds.nb; S.np = ds.np;
     constexpr int LD = Lay<R>::LD;
-    const size_t sm_x = TW * LD * sizeof(R), sm_du = 3 * TW * LayK<R>::LD * sizeof(R);
+    const size_t sm_x = 2 * TW * LD * sizeof(R), sm_du = 3 * TW * LayK<R>::LD * sizeof(R);
     MPJ_CK(cudaFuncSetAttribute(k_gram<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_x));
     MPJ_CK(cudaFuncSetAttribute(k_svd_solve<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_du));
     const bool prof = prof_on();
