@@ -178,12 +178,13 @@ __device__ __forceinline__ bool item_identity(const ApplyArgs &p, int item, int 
 
 // STAGES = 2: one CTA per SM prefetches item i+1 while computing item i;
 // STAGES = 1: two CTAs per SM overlap each other's loads and epilogues.
-template <typename R, int STAGES>
+template <typename R, int STAGES, bool VONLY = false>
 __global__ void __launch_bounds__(NT) k_block_apply(ApplyArgs p)
 {
+    constexpr int NB = VONLY ? 2 : 3;             // buffers per stage (V tiles: X, Uc)
     constexpr int LD = Lay<R>::LD, EPC = 16 / sizeof(R), CPC = TW / EPC;
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    R *buf = (R *)smem_raw;                       // stage s: X, Ua, Uc at buf + (3s + {0,1,2}) * TW * LD
+    R *buf = (R *)smem_raw;                       // stage s: X, Ua, Uc at buf + (NB s + {0,1,2}) * TW * LD
     const int total = p.ntT + p.ntV;
     const int mb = p.S.nb >> 1;
     const int2 *bsr = p.S.bsched + p.Rb * mb;
@@ -194,24 +195,24 @@ __global__ void __launch_bounds__(NT) k_block_apply(ApplyArgs p)
     };
     int item = advance(blockIdx.x);
     if (STAGES == 2) {
-        if (item < total) issue_item<R>(p, item, buf, buf + TW * LD, buf + 2 * TW * LD, skips);
+        if (item < total) issue_item<R>(p, item, buf, buf + TW * LD, buf + (NB - 1) * TW * LD, skips);
         cp_commit();
     }
     for (int it = 0; item < total; ++it, item = advance(item + gridDim.x)) {
         const int s = STAGES == 2 ? (it & 1) : 0;
         if (STAGES == 2) {
             const int next = advance(item + gridDim.x);
-            R *nb = buf + (size_t)(3 * (s ^ 1)) * TW * LD;
-            if (next < total) issue_item<R>(p, next, nb, nb + TW * LD, nb + 2 * TW * LD, skips);
+            R *nb = buf + (size_t)(NB * (s ^ 1)) * TW * LD;
+            if (next < total) issue_item<R>(p, next, nb, nb + TW * LD, nb + (NB - 1) * TW * LD, skips);
             cp_commit();
             cp_wait1();
         } else {
-            issue_item<R>(p, item, buf, buf + TW * LD, buf + 2 * TW * LD, skips);
+            issue_item<R>(p, item, buf, buf + TW * LD, buf + (NB - 1) * TW * LD, skips);
             cp_commit();
             cp_wait0();
         }
         __syncthreads();
-        R *x = buf + (size_t)(3 * s) * TW * LD, *ua = x + TW * LD, *uc = x + 2 * TW * LD;
+        R *x = buf + (size_t)(NB * s) * TW * LD, *ua = x + TW * LD, *uc = x + (NB - 1) * TW * LD;
         if (item < p.ntT) {
             int a, c;
             decode_upper(item, a, c);
@@ -660,23 +661,23 @@ static int apply_stages()
     return s;
 }
 
-template <typename R, int STAGES>
+template <typename R, int STAGES, bool VONLY = false>
 static void launch_apply_s(const ApplyArgs &p, cudaStream_t st)
 {
     constexpr int LD = Lay<R>::LD;
-    const size_t smem = 3 * STAGES * TW * LD * sizeof(R);
+    const size_t smem = (VONLY ? 2 : 3) * STAGES * TW * LD * sizeof(R);
     static bool attr = false;
     static int per_sm = 0;
     if (!attr) {
-        MPJ_CK_VOID(cudaFuncSetAttribute(k_block_apply<R, STAGES>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        MPJ_CK_VOID(cudaFuncSetAttribute(k_block_apply<R, STAGES, VONLY>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)smem));
-        MPJ_CK_VOID(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_block_apply<R, STAGES>, NT, smem));
+        MPJ_CK_VOID(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_block_apply<R, STAGES, VONLY>, NT, smem));
         per_sm = std::max(1, per_sm);
         attr = true;
     }
     const int total = p.ntT + p.ntV;
     const int grid = std::max(1, std::min(total, sm_count() * per_sm));
-    k_block_apply<R, STAGES><<<grid, NT, smem, st>>>(p);
+    k_block_apply<R, STAGES, VONLY><<<grid, NT, smem, st>>>(p);
     count_launch();
 }
 
@@ -759,8 +760,11 @@ static void launch_apply(const ApplyArgs &p, cudaStream_t st)
 {
     if (sizeof(R) == 4 && fp32_apply_kind() == 2 && p.T && p.mrows % 4 == 0 && launch_apply_f32ws(p, st)) return;
     if (sizeof(R) == 4 && fp32_apply_kind() >= 1) { launch_apply_f32w(p, st); return; }
-    if (apply_stages() == 2) launch_apply_s<R, 2>(p, st);
-    else launch_apply_s<R, 1>(p, st);
+    if (apply_stages() == 2) { launch_apply_s<R, 2>(p, st); return; }
+    // column updates only (the SVD): two buffers per CTA, 3 CTAs/SM (an
+    // EVD launch split into T-only and V-only kernels gained nothing)
+    if (p.ntT == 0) { launch_apply_s<R, 1, true>(p, st); return; }
+    launch_apply_s<R, 1>(p, st);
 }
 
 template <typename R>
