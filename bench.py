@@ -187,7 +187,7 @@ def oracle_sample(n, mode, kappa, seed, sweeps64, sweeps32, budget_s):
         "kind": "oracle", "cores": oracle.threads(),
         "sample": (f"oracle/mpj_oracle.c at n={n}: {rounds} fp64 round(s) ({t64:.3f} s each) and "
                    f"{rounds} fp32 round(s) ({t32:.3f} s each), x {rounds_per_sweep} rounds/sweep x "
-                   f"({sweeps64} fp64 + {sweeps32} fp32 sweeps as the GPU run took); MGS + Q^T A Q "
+                   f"({sweeps64} fp64 + {sweeps32} fp32 sweeps, the GPU run's counts); MGS + Q^T A Q "
                    f"timed at n={ns} ({t_mgs + t_qtaq:.2f} s) x (n/{ns})^3"),
     }
     return est, info
@@ -198,9 +198,17 @@ def run_reference(args):
     if rank != 0:
         return
     seed = 2211033390 + 4000 + 100 * args.mode + 60
-    # sweep counts of the GPU run at this config (measured on B200, profiles/); the
-    # oracle at n = 8192 would take hours per EVD, so each step is a bounded sample
-    sw64, sw32 = 5, 14
+    # sweep counts of the GPU run at this config (measured on B200 and committed in
+    # profiles/r01_bench_n8192.json); the oracle at n = 8192 would take hours per
+    # EVD, so each step is a bounded sample scaled by these counts
+    sw64, sw32 = 9, 12
+    prof = os.path.join(ROOT, "profiles", "r01_bench_n8192.json")
+    try:
+        d = json.load(open(prof))
+        if d.get("config", {}).get("n") == args.n and d.get("config", {}).get("mode") == args.mode:
+            sw64, sw32 = int(d["sweeps"]), int(d["sweeps_low"])
+    except (OSError, ValueError, KeyError):
+        pass
     vals = []
     info = None
     for _ in range(args.warmup * 0 + args.steps):
