@@ -511,6 +511,55 @@ __device__ __forceinline__ void store_op_sh(const Acc48 &acc, float *C, float *C
     }
 }
 
+// V super-items: two row tiles of the same column block (128 x 64 of M, one
+// U_c) in a "split-quarter" layout (element (i, k) at (i / 32) 2048 + 32 k +
+// i % 32).  8 x 8 per thread: quarter-warp Q owns rows 32 (Q % 2) + 4 l8 ..+3
+// and 32 (Q % 2 + 2) + 4 l8 ..+3 and columns 8 (Q / 2) ..+7: a k-step is ~12
+// shared-memory wavefronts per warp for 64 FFMA (4 x 8 tiles: ~16).
+struct Acc88 {
+    float v[8][8];
+};
+
+__device__ __forceinline__ void tile_op_88(const float *A, const float *B, Acc88 &acc, int tid)
+{
+    const int q = tid >> 3, l8 = tid & 7;
+    const float *A0 = A + (q & 1) * SH_HALF + 4 * l8, *A1 = A0 + 2 * SH_HALF;
+    const int cb = 8 * (q >> 1);
+    const float *Bc = B + (cb >> 5) * SH_HALF + (cb & 31);
+    #pragma unroll
+    for (int u = 0; u < 8; ++u)
+        #pragma unroll
+        for (int w = 0; w < 8; ++w) acc.v[u][w] = 0.f;
+    float4 a0 = *(const float4 *)A0, a1 = *(const float4 *)A1, b0 = *(const float4 *)Bc,
+           b1 = *(const float4 *)(Bc + 4);
+    #pragma unroll 2
+    for (int k = 0; k < TW; ++k) {
+        const float av[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
+        const float bv[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+        if (k + 1 < TW) {
+            a0 = *(const float4 *)(A0 + (k + 1) * BW);
+            a1 = *(const float4 *)(A1 + (k + 1) * BW);
+            b0 = *(const float4 *)(Bc + (k + 1) * BW);
+            b1 = *(const float4 *)(Bc + 4 + (k + 1) * BW);
+        }
+        #pragma unroll
+        for (int u = 0; u < 8; ++u)
+            #pragma unroll
+            for (int w = 0; w < 8; ++w) acc.v[u][w] = __fmaf_rn(av[u], bv[w], acc.v[u][w]);
+    }
+}
+
+__device__ __forceinline__ void store_op_88(const Acc88 &acc, float *C, int tid)
+{
+    const int q = tid >> 3, l8 = tid & 7;
+    const int r = 32 * (q & 1) + 4 * l8, c = 8 * (q >> 1);
+    #pragma unroll
+    for (int w = 0; w < 8; ++w) {
+        *(float4 *)(C + sh_idx(r, c + w)) = make_float4(acc.v[0][w], acc.v[1][w], acc.v[2][w], acc.v[3][w]);
+        *(float4 *)(C + sh_idx(r + 64, c + w)) = make_float4(acc.v[4][w], acc.v[5][w], acc.v[6][w], acc.v[7][w]);
+    }
+}
+
 __global__ void __launch_bounds__(WS_NT, 1) k_block_apply_f32ws(ApplyArgs p, const __grid_constant__ CUtensorMap tmT,
                                                                 const __grid_constant__ CUtensorMap tmM)
 {
@@ -519,8 +568,10 @@ __global__ void __launch_bounds__(WS_NT, 1) k_block_apply_f32ws(ApplyArgs p, con
     float *ring = (float *)smem_raw;
     uint64_t *full = (uint64_t *)(smem_raw + (size_t)WS_NS * SBUF * sizeof(float));
     uint64_t *empty = full + WS_NS;
-    const int total = p.ntT + p.ntV;
     const int mb = p.S.nb >> 1;
+    // M tiles are processed as super-items of two row tiles (same column block)
+    const int nrt = p.ntV / mb;
+    const int total = p.ntT + ((nrt + 1) / 2) * mb;
     const int2 *bsr = p.S.bsched + p.Rb * mb;
     const bool skips = p.uid && *p.nid > 0;
     auto advance = [&](int i) {
@@ -559,13 +610,15 @@ __global__ void __launch_bounds__(WS_NT, 1) k_block_apply_f32ws(ApplyArgs p, con
                 if (!ia) bulk_g2s(ua, UbS + (size_t)a * SH_TILE, SH_TILE * sizeof(float), bar);
                 if (!ic) bulk_g2s(uc, UbS + (size_t)c * SH_TILE, SH_TILE * sizeof(float), bar);
             } else {
-                const int idx = item - p.ntT, c = idx % mb, r0 = (idx / mb) * TW;
+                // super-item: rows r0 .. r0 + 127 of M (X occupies the X and U_a slots)
+                const int idx = item - p.ntT, c = idx % mb, r0 = (idx / mb) * 2 * TW;
                 const int2 pc = bsr[c];
-                mbar_arrive_tx(bar, 2 * SH_TILE * sizeof(float));   // out-of-range rows are zero-filled
-                tma_box(x, &tmM, r0, pc.x * BW, bar);
-                tma_box(x + SH_HALF, &tmM, r0 + BW, pc.x * BW, bar);
-                tma_box(x + BW * BW, &tmM, r0, pc.y * BW, bar);
-                tma_box(x + SH_HALF + BW * BW, &tmM, r0 + BW, pc.y * BW, bar);
+                const int nq = (r0 + TW < p.mrows) ? 4 : 2;      // a lone last row tile: its half only
+                mbar_arrive_tx(bar, (nq * 2 * BW * BW + SH_TILE) * sizeof(float));   // partial rows zero-filled
+                for (int qh = 0; qh < nq; ++qh) {
+                    tma_box(x + qh * SH_HALF, &tmM, r0 + qh * BW, pc.x * BW, bar);
+                    tma_box(x + qh * SH_HALF + BW * BW, &tmM, r0 + qh * BW, pc.y * BW, bar);
+                }
                 bulk_g2s(uc, UbS + (size_t)c * SH_TILE, SH_TILE * sizeof(float), bar);
             }
         }
@@ -576,6 +629,7 @@ __global__ void __launch_bounds__(WS_NT, 1) k_block_apply_f32ws(ApplyArgs p, con
     const int gt = threadIdx.x - 32 - g * WS_CG;            // thread within the group
     const int bar_id = 1 + g;
     Acc48 acc;
+    Acc88 acc8;
     int j = 0;
     for (int item = advance(blockIdx.x); item < total; item = advance(item + gridDim.x), ++j) {
         if ((j & 1) != g) continue;
@@ -608,15 +662,15 @@ __global__ void __launch_bounds__(WS_NT, 1) k_block_apply_f32ws(ApplyArgs p, con
                 *(int4 *)(T + gidx(pc, li) + (int64_t)gidx(pa, lj) * p.ldt) = *(const int4 *)(ua + sh_idx(li, lj));
             }
         } else {
-            const int idx = item - p.ntT, c = idx % mb, r0 = (idx / mb) * TW;
+            const int idx = item - p.ntT, c = idx % mb, r0 = (idx / mb) * 2 * TW;
             const int2 pc = bsr[c];
-            tile_op_sh(x, uc, acc, gt);                      // W = X U_c
+            tile_op_88(x, uc, acc8, gt);                     // W = X U_c (128 x 64)
             group_sync(bar_id);
-            store_op_sh(acc, x, nullptr, gt);
+            store_op_88(acc8, x, gt);
             group_sync(bar_id);
             float *M = (float *)p.M;
-            for (int e = gt; e < TW * CPC; e += WS_CG) {
-                const int lj = e / CPC, li = (e - lj * CPC) * EPC;
+            for (int e = gt; e < 2 * TW * CPC; e += WS_CG) {
+                const int lj = e / (2 * CPC), li = (e - lj * 2 * CPC) * EPC;
                 if (r0 + li < p.mrows)   // mrows % 4 == 0 on this path
                     *(int4 *)(M + (int64_t)(r0 + li) + (int64_t)gidx(pc, lj) * p.ldm) = *(const int4 *)(x + sh_idx(li, lj));
             }

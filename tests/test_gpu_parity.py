@@ -291,11 +291,13 @@ np.save(sys.argv[3], np.concatenate([T.cpu().numpy().ravel(), V.cpu().numpy().ra
 """
 
 
-@pytest.mark.parametrize("n", [256, 330])
+@pytest.mark.parametrize("n", [256, 300, 330])
 def test_fp32_apply_kernels_bit_identical(tmp_path, n):
     """The three fp32 K4 kernels (4x4 outer product, 8x4 tiles, warp-specialised
     TMA pipeline) accumulate every output in the same k order: two fp32 block
-    sweeps must give bit-identical T and V whichever runs (MPJ_FP32_APPLY)."""
+    sweeps must give bit-identical T and V whichever runs (MPJ_FP32_APPLY).
+    n = 300 (n_p = 320: 5 row tiles) leaves the TMA kernel's last V
+    super-item with a single row tile."""
     import os
     import subprocess
     import sys
