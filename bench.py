@@ -121,8 +121,16 @@ class ClockSampler:
         reasons = sorted({names[i] for r in self.rows for i in range(4)
                           if len(r) > 4 + i and r[4 + i].lower() == "active"})
         busy = [s for s in sm if s > 0.5 * max(sm)] if sm else []
+        pw = []
+        for r in self.rows:
+            try:
+                pw.append(float(r[3]))
+            except (IndexError, ValueError):
+                pass
         return {"sm_mhz": statistics.median(busy or sm) if sm else None,
-                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons, "samples": len(self.rows)}
+                "sm_min_mhz": min(busy or sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons, "samples": len(self.rows),
+                "power_w_median": statistics.median(pw) if pw else None, "power_w_max": max(pw) if pw else None}
 
 
 def dist_init(args):

@@ -123,7 +123,7 @@ __device__ __forceinline__ bool block_identity(const ApplyArgs &p, int k, bool s
 
 // issue the loads of work item `item` into stage buffers (X, Ua, Uc); fp64 T
 // tiles with one identity block skip that block's load (see k_block_apply)
-template <typename R, int NTH = NT>
+template <typename R, int NTH = NT, bool V2 = false>
 __device__ __forceinline__ void issue_item(const ApplyArgs &p, int item, R *X, R *Ua, R *Uc, bool skips = false)
 {
     constexpr int LD = Lay<R>::LD, EPC = 16 / sizeof(R), CPC = TW / EPC;   // elements / chunks per column
@@ -148,15 +148,19 @@ __device__ __forceinline__ void issue_item(const ApplyArgs &p, int item, R *X, R
             if (lc) cp16(Uc + li + lj * LD, UbO + (size_t)c * TW * TW + li + lj * TW, 16);
         }
     } else {
-        const int idx = item - p.ntT, c = idx % mb, r0 = (idx / mb) * TW;
+        // V2: super-item of two row tiles (rows r0.. into X, r0+64.. into the Ua buffer)
+        const int idx = item - p.ntT, c = idx % mb, r0 = (idx / mb) * (V2 ? 2 : 1) * TW;
         const int2 pc = bsr[c];
         const R *M = (const R *)p.M;
         for (int e = threadIdx.x; e < TW * CPC; e += NTH) {
             const int lj = e / CPC, li = (e - lj * CPC) * EPC;
-            const int rem = p.mrows - (r0 + li);
-            const int bytes = rem >= EPC ? 16 : (rem > 0 ? rem * (int)sizeof(R) : 0);
-            const R *src = M + (bytes ? (int64_t)(r0 + li) : 0) + (int64_t)gidx(pc, lj) * p.ldm;
-            cp16(X + li + lj * LD, src, bytes);
+            #pragma unroll
+            for (int h = 0; h < (V2 ? 2 : 1); ++h) {
+                const int rem = p.mrows - (r0 + h * TW + li);
+                const int bytes = rem >= EPC ? 16 : (rem > 0 ? rem * (int)sizeof(R) : 0);
+                const R *src = M + (bytes ? (int64_t)(r0 + h * TW + li) : 0) + (int64_t)gidx(pc, lj) * p.ldm;
+                cp16((h ? Ua : X) + li + lj * LD, src, bytes);
+            }
             cp16(Uc + li + lj * LD, UbO + (size_t)c * TW * TW + li + lj * TW, 16);
         }
     }
@@ -182,11 +186,14 @@ template <typename R, int STAGES, bool VONLY = false>
 __global__ void __launch_bounds__(NT) k_block_apply(ApplyArgs p)
 {
     constexpr int NB = VONLY ? 2 : 3;             // buffers per stage (V tiles: X, Uc)
+    // fp64 V tiles as super-items of two row tiles (X in the X and Ua buffers):
+    // each U_c fragment feeds both tiles' DMMAs, half the per-item overhead
+    constexpr bool V2 = sizeof(R) == 8 && !VONLY;
     constexpr int LD = Lay<R>::LD, EPC = 16 / sizeof(R), CPC = TW / EPC;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     R *buf = (R *)smem_raw;                       // stage s: X, Ua, Uc at buf + (NB s + {0,1,2}) * TW * LD
-    const int total = p.ntT + p.ntV;
     const int mb = p.S.nb >> 1;
+    const int total = p.ntT + (V2 ? ((p.ntV / mb + 1) / 2) * mb : p.ntV);
     const int2 *bsr = p.S.bsched + p.Rb * mb;
     const bool skips = p.uid && *p.nid > 0;
     auto advance = [&](int i) {
@@ -195,7 +202,7 @@ __global__ void __launch_bounds__(NT) k_block_apply(ApplyArgs p)
     };
     int item = advance(blockIdx.x);
     if (STAGES == 2) {
-        if (item < total) issue_item<R>(p, item, buf, buf + TW * LD, buf + (NB - 1) * TW * LD, skips);
+        if (item < total) issue_item<R, NT, V2>(p, item, buf, buf + TW * LD, buf + (NB - 1) * TW * LD, skips);
         cp_commit();
     }
     for (int it = 0; item < total; ++it, item = advance(item + gridDim.x)) {
@@ -203,11 +210,11 @@ __global__ void __launch_bounds__(NT) k_block_apply(ApplyArgs p)
         if (STAGES == 2) {
             const int next = advance(item + gridDim.x);
             R *nb = buf + (size_t)(NB * (s ^ 1)) * TW * LD;
-            if (next < total) issue_item<R>(p, next, nb, nb + TW * LD, nb + (NB - 1) * TW * LD, skips);
+            if (next < total) issue_item<R, NT, V2>(p, next, nb, nb + TW * LD, nb + (NB - 1) * TW * LD, skips);
             cp_commit();
             cp_wait1();
         } else {
-            issue_item<R>(p, item, buf, buf + TW * LD, buf + (NB - 1) * TW * LD, skips);
+            issue_item<R, NT, V2>(p, item, buf, buf + TW * LD, buf + (NB - 1) * TW * LD, skips);
             cp_commit();
             cp_wait0();
         }
@@ -252,13 +259,20 @@ __global__ void __launch_bounds__(NT) k_block_apply(ApplyArgs p)
                 *(int4 *)(T + gidx(pc, li) + (int64_t)gidx(pa, lj) * p.ldt) = *(const int4 *)(ua + li + lj * LD);
             }
         } else {
-            const int idx = item - p.ntT, c = idx % mb, r0 = (idx / mb) * TW;
+            constexpr int NH = V2 ? 2 : 1;               // row tiles in this item
+            const int idx = item - p.ntT, c = idx % mb, r0 = (idx / mb) * NH * TW;
             const int2 pc = bsr[c];
             if constexpr (sizeof(R) == 4) {
                 AccOP o;
                 tile_op((const float *)x, (const float *)uc, o);   // W = X Uc (X column-major, U_c^T)
                 __syncthreads();
                 store_op(o, (float *)x, nullptr);
+            } else if constexpr (V2) {
+                Acc<R> acc, acc2;
+                tile_mm2(x, ua, uc, acc, acc2);                      // W = X Uc for both row tiles
+                __syncthreads();
+                acc.each([&](int i, int j, R v) { x[i + j * LD] = v; });
+                acc2.each([&](int i, int j, R v) { ua[i + j * LD] = v; });
             } else {
                 Acc<R> acc;
                 tile_mm<false>(x, uc, acc);                          // W = X Uc
@@ -267,13 +281,15 @@ __global__ void __launch_bounds__(NT) k_block_apply(ApplyArgs p)
             }
             __syncthreads();
             R *M = (R *)p.M;
-            for (int e = threadIdx.x; e < TW * CPC; e += NT) {
-                const int lj = e / CPC, li = (e - lj * CPC) * EPC;
-                R *dst = M + (int64_t)(r0 + li) + (int64_t)gidx(pc, lj) * p.ldm;
-                if (r0 + li + EPC <= p.mrows) {
-                    *(int4 *)dst = *(const int4 *)(x + li + lj * LD);
+            for (int e = threadIdx.x; e < NH * TW * CPC; e += NT) {
+                const int lj = e / (NH * CPC), lr = (e - lj * NH * CPC) * EPC;   // lr: row in the item
+                const int h = lr >= TW, li = lr - h * TW;
+                const R *srcw = (h ? ua : x) + li + lj * LD;
+                R *dst = M + (int64_t)(r0 + lr) + (int64_t)gidx(pc, lj) * p.ldm;
+                if (r0 + lr + EPC <= p.mrows) {
+                    *(int4 *)dst = *(const int4 *)srcw;
                 } else {
-                    for (int q = 0; q < EPC && r0 + li + q < p.mrows; ++q) dst[q] = x[li + q + lj * LD];
+                    for (int q = 0; q < EPC && r0 + lr + q < p.mrows; ++q) dst[q] = srcw[q];
                 }
             }
         }

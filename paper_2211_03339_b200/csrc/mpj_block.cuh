@@ -463,6 +463,37 @@ __device__ __forceinline__ void tile_mm_acc(const double *A, const double *B, Ac
     }
 }
 
+// C1 = A1 B, C2 = A2 B (fp64, A column-major): the same warp tile of two
+// row tiles, every B fragment feeding both (16 DMMA per 8 fragment loads)
+__device__ __forceinline__ void tile_mm2(const double *A1, const double *A2, const double *B, Acc<double> &c1,
+                                         Acc<double> &c2)
+{
+    constexpr int LD = Lay<double>::LD;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, tig = lane & 3;
+    const int rb = (warp >> 1) * 16 + g, cb = (warp & 1) * 32 + g;
+    c1.zero();
+    c2.zero();
+    #pragma unroll 2
+    for (int ks = 0; ks < TW / 4; ++ks) {
+        const int kk = ks * 4 + tig;
+        double a1[2], a2[2], b[4];
+        #pragma unroll
+        for (int mi = 0; mi < 2; ++mi) {
+            a1[mi] = A1[rb + mi * 8 + kk * LD];
+            a2[mi] = A2[rb + mi * 8 + kk * LD];
+        }
+        #pragma unroll
+        for (int ni = 0; ni < 4; ++ni) b[ni] = B[kk + (cb + ni * 8) * LD];
+        #pragma unroll
+        for (int mi = 0; mi < 2; ++mi)
+            #pragma unroll
+            for (int ni = 0; ni < 4; ++ni) {
+                dmma884(c1.v[mi][ni][0], c1.v[mi][ni][1], a1[mi], b[ni]);
+                dmma884(c2.v[mi][ni][0], c2.v[mi][ni][1], a2[mi], b[ni]);
+            }
+    }
+}
+
 template <bool TRANS_A>
 __device__ __forceinline__ void tile_mm_acc(const float *A, const float *B, Acc<float> &acc)
 {
