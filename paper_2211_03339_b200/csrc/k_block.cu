@@ -182,20 +182,22 @@ __device__ __forceinline__ bool item_identity(const ApplyArgs &p, int item, int 
 
 // STAGES = 2: one CTA per SM prefetches item i+1 while computing item i;
 // STAGES = 1: two CTAs per SM overlap each other's loads and epilogues.
-template <typename R, int STAGES, bool VONLY = false>
-__global__ void __launch_bounds__(NT) k_block_apply(ApplyArgs p)
+// SKIP: this block round has identity blocks (skip / one-product logic); the
+// kernel picks the instantiation once per CTA so that launches without
+// identities run the plain loop (the checks cost 3% per full launch).
+template <typename R, int STAGES, bool VONLY, bool SKIP>
+__device__ __forceinline__ void apply_body(const ApplyArgs &p, unsigned char *smem_raw)
 {
     constexpr int NB = VONLY ? 2 : 3;             // buffers per stage (V tiles: X, Uc)
     // fp64 V tiles as super-items of two row tiles (X in the X and Ua buffers):
     // each U_c fragment feeds both tiles' DMMAs, half the per-item overhead
     constexpr bool V2 = sizeof(R) == 8 && !VONLY;
     constexpr int LD = Lay<R>::LD, EPC = 16 / sizeof(R), CPC = TW / EPC;
-    extern __shared__ __align__(16) unsigned char smem_raw[];
     R *buf = (R *)smem_raw;                       // stage s: X, Ua, Uc at buf + (NB s + {0,1,2}) * TW * LD
     const int mb = p.S.nb >> 1;
     const int total = p.ntT + (V2 ? ((p.ntV / mb + 1) / 2) * mb : p.ntV);
     const int2 *bsr = p.S.bsched + p.Rb * mb;
-    const bool skips = p.uid && *p.nid > 0;
+    constexpr bool skips = SKIP;
     auto advance = [&](int i) {
         while (skips && i < total && item_identity(p, i, mb)) i += gridDim.x;
         return i;
@@ -296,6 +298,14 @@ __global__ void __launch_bounds__(NT) k_block_apply(ApplyArgs p)
         __syncthreads();
     }
     cp_wait0();
+}
+
+template <typename R, int STAGES, bool VONLY = false>
+__global__ void __launch_bounds__(NT) k_block_apply(ApplyArgs p)
+{
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    if (p.uid && *p.nid > 0) apply_body<R, STAGES, VONLY, true>(p, smem_raw);
+    else apply_body<R, STAGES, VONLY, false>(p, smem_raw);
 }
 
 // fp32 apply with 8 x 4 register tiles: 128 threads per 64 x 64 tile, thread
