@@ -586,11 +586,11 @@ __device__ __forceinline__ void store_op_88(const Acc88 &acc, float *C, int tid)
     }
 }
 
-__global__ void __launch_bounds__(WS_NT, 1) k_block_apply_f32ws(ApplyArgs p, const __grid_constant__ CUtensorMap tmT,
-                                                                const __grid_constant__ CUtensorMap tmM)
+template <bool SKIP>
+__device__ __forceinline__ void apply_f32ws_body(const ApplyArgs &p, const CUtensorMap &tmT, const CUtensorMap &tmM,
+                                                 unsigned char *smem_raw)
 {
     constexpr int EPC = 4, CPC = TW / EPC, SBUF = 3 * SH_TILE;
-    extern __shared__ __align__(128) unsigned char smem_raw[];
     float *ring = (float *)smem_raw;
     uint64_t *full = (uint64_t *)(smem_raw + (size_t)WS_NS * SBUF * sizeof(float));
     uint64_t *empty = full + WS_NS;
@@ -599,7 +599,7 @@ __global__ void __launch_bounds__(WS_NT, 1) k_block_apply_f32ws(ApplyArgs p, con
     const int nrt = p.ntV / mb;
     const int total = p.ntT + ((nrt + 1) / 2) * mb;
     const int2 *bsr = p.S.bsched + p.Rb * mb;
-    const bool skips = p.uid && *p.nid > 0;
+    constexpr bool skips = SKIP;
     auto advance = [&](int i) {
         while (skips && i < total && item_identity(p, i, mb)) i += gridDim.x;
         return i;
@@ -706,6 +706,14 @@ __global__ void __launch_bounds__(WS_NT, 1) k_block_apply_f32ws(ApplyArgs p, con
         group_sync(bar_id);
         if (gt == 0) mbar_arrive(empty + st);
     }
+}
+
+__global__ void __launch_bounds__(WS_NT, 1) k_block_apply_f32ws(ApplyArgs p, const __grid_constant__ CUtensorMap tmT,
+                                                                const __grid_constant__ CUtensorMap tmM)
+{
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    if (p.uid && *p.nid > 0) apply_f32ws_body<true>(p, tmT, tmM, smem_raw);
+    else apply_f32ws_body<false>(p, tmT, tmM, smem_raw);
 }
 
 }  // namespace
