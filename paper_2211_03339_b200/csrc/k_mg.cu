@@ -79,11 +79,14 @@ __global__ void __launch_bounds__(NTW) k_mg_solve(R *__restrict__ T, int64_t ldt
     }
     __syncthreads();
     const R *D = inner_rounds_wide<R>(D1, D0, U, bp, intra != 0, lsched, nu, rule, P, &nrot);
-    R *Uk = Ubuf + (size_t)(slot0 + blockIdx.x) * TW * TW;
+    // slot stride: 64 x 64 fp64 words; an fp32 slot holds U and then U^T (the
+    // k-major operand of the fp32 apply), so one all-gather carries both
+    R *Uk = Ubuf + (size_t)(slot0 + blockIdx.x) * TW * TW * (8 / sizeof(R));
     for (int e = threadIdx.x; e < TW * TW; e += NTW) {
         const int li = e & (TW - 1), lj = e >> 6;
         T[gidx(bp, li) + (int64_t)pcol(si, lj) * ldt] = D[li + lj * LD];
         Uk[li + lj * TW] = U[li + lj * LD];
+        if (sizeof(R) == 4) Uk[TW * TW + li + lj * TW] = U[lj + li * LD];
     }
     if (threadIdx.x == 0 && nrot) atomicAdd(cnt, (unsigned long long)nrot);
 }
@@ -94,6 +97,24 @@ __device__ __forceinline__ void mg_cp16(void *dst, const void *src, int bytes)
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(d), "l"(src), "r"(bytes));
 }
 
+// uid[s] = 1 iff the (all-gathered) rotation block of slot s is exactly I --
+// no rotation happened there (a rotation with s = 0 is the identity too), so
+// the tiles it multiplies are unchanged: exact to skip.  One CTA per slot.
+template <typename R>
+__global__ void __launch_bounds__(256) k_mg_uid(const R *__restrict__ Ubuf, int *__restrict__ uid,
+                                                int *__restrict__ nid)
+{
+    const R *U = Ubuf + (size_t)blockIdx.x * TW * TW * (8 / sizeof(R));
+    int ok = 1;
+    for (int e = threadIdx.x; e < TW * TW; e += blockDim.x)
+        ok &= (U[e] == ((e & (TW - 1)) == (e >> 6) ? R(1) : R(0)));
+    ok = __syncthreads_and(ok);
+    if (threadIdx.x == 0) {
+        uid[blockIdx.x] = ok;
+        if (ok) atomicAdd(nid, 1);
+    }
+}
+
 struct MgApply {
     void *T, *V;
     int64_t ld;               // leading dimension of local T and V (= n_p)
@@ -102,8 +123,37 @@ struct MgApply {
     const int2 *gslots;       // global slot -> (top, bot) this round
     int slot0, mb, mbl;
     const void *Ubuf;
+    const int *uid;           // per global slot: U exactly I
+    const int *nid;           // number of such slots this round
     int ntT, ntV;
 };
+
+// item decode shared by the mg apply kernels: T tile (local slot cl, global
+// slot a != own) or V tile (local slot cl, row tile r0)
+__device__ __forceinline__ void mg_decode(const MgApply &p, int item, bool &ttile, int &cl, int &a, int &r0)
+{
+    ttile = item < p.ntT;
+    a = 0;
+    r0 = 0;
+    if (ttile) {
+        cl = item / (p.mb - 1);
+        const int ai = item - cl * (p.mb - 1);
+        a = ai < p.slot0 + cl ? ai : ai + 1;
+    } else {
+        const int idx = item - p.ntT;
+        cl = idx % p.mbl;
+        r0 = (idx / p.mbl) * TW;
+    }
+}
+
+__device__ __forceinline__ bool mg_item_identity(const MgApply &p, int item)
+{
+    bool tt;
+    int cl, a, r0;
+    mg_decode(p, item, tt, cl, a, r0);
+    const int cg = p.slot0 + cl;
+    return p.uid[cg] && (!tt || p.uid[a]);
+}
 
 template <typename R>
 __global__ void __launch_bounds__(NT) k_mg_apply(MgApply p)
@@ -114,18 +164,16 @@ __global__ void __launch_bounds__(NT) k_mg_apply(MgApply p)
     R *ua = x + TW * LD;
     R *uc = ua + TW * LD;
     const R *Ub = (const R *)p.Ubuf;
-    for (int item = blockIdx.x; item < p.ntT + p.ntV; item += gridDim.x) {
-        const bool ttile = item < p.ntT;
-        int cl, a = 0, r0 = 0;
-        if (ttile) {
-            cl = item / (p.mb - 1);
-            const int ai = item - cl * (p.mb - 1);
-            a = ai < p.slot0 + cl ? ai : ai + 1;
-        } else {
-            const int idx = item - p.ntT;
-            cl = idx % p.mbl;
-            r0 = (idx / p.mbl) * TW;
-        }
+    const int total = p.ntT + p.ntV;
+    const bool skips = p.uid && *p.nid > 0;
+    auto advance = [&](int i) {
+        while (skips && i < total && mg_item_identity(p, i)) i += gridDim.x;
+        return i;
+    };
+    for (int item = advance(blockIdx.x); item < total; item = advance(item + gridDim.x)) {
+        bool ttile;
+        int cl, a, r0;
+        mg_decode(p, item, ttile, cl, a, r0);
         const SlotInfo sc = p.slots[cl];
         const int cg = p.slot0 + cl;
         R *M = (R *)(ttile ? p.T : p.V);
@@ -135,29 +183,111 @@ __global__ void __launch_bounds__(NT) k_mg_apply(MgApply p)
             const int64_t col = (int64_t)pcol(sc, lj) * p.ld;
             if (ttile) {
                 mg_cp16(x + li + lj * LD, M + gidx(ra, li) + col, 16);
-                mg_cp16(ua + li + lj * LD, Ub + (size_t)a * TW * TW + li + lj * TW, 16);
+                mg_cp16(ua + li + lj * LD, Ub + (size_t)a * TW * TW * (8 / sizeof(R)) + li + lj * TW, 16);
             } else {
                 const int rem = p.vrows - (r0 + li);
                 const int bytes = rem >= EPC ? 16 : (rem > 0 ? rem * (int)sizeof(R) : 0);
                 mg_cp16(x + li + lj * LD, M + (bytes ? (int64_t)(r0 + li) : 0) + col, bytes);
             }
-            mg_cp16(uc + li + lj * LD, Ub + (size_t)cg * TW * TW + li + lj * TW, 16);
+            mg_cp16(uc + li + lj * LD, Ub + (size_t)cg * TW * TW * (8 / sizeof(R)) + li + lj * TW, 16);
         }
         asm volatile("cp.async.commit_group;\n" ::);
         asm volatile("cp.async.wait_group 0;\n" ::);
         __syncthreads();
         Acc<R> acc;
-        if (ttile) {
+        // identity blocks (fp64): U_c = I -> W = U_a^T X only; U_a = I -> W = X U_c only
+        const bool ic = skips && ttile && p.uid[cg];
+        const bool ia = skips && ttile && p.uid[a];
+        if (ttile && !ia) {
             tile_mm<true>(ua, x, acc);                  // Y = U_a^T X
             __syncthreads();
             acc.each([&](int i, int j, R v) { x[i + j * LD] = v; });
             __syncthreads();
         }
-        tile_mm<false>(x, uc, acc);                     // W = Y U_c  (or X U_c)
+        if (!ic) tile_mm<false>(x, uc, acc);            // W = Y U_c  (or X U_c)
         __syncthreads();
         acc.each([&](int i, int j, R v) { x[i + j * LD] = v; });
         __syncthreads();
         for (int e = threadIdx.x; e < TW * CPC; e += NT) {
+            const int lj = e / CPC, li = (e - lj * CPC) * EPC;
+            const int64_t col = (int64_t)pcol(sc, lj) * p.ld;
+            if (ttile) {
+                *(int4 *)(M + gidx(ra, li) + col) = *(const int4 *)(x + li + lj * LD);
+            } else if (r0 + li + EPC <= p.vrows) {
+                *(int4 *)(M + (r0 + li) + col) = *(const int4 *)(x + li + lj * LD);
+            } else {
+                for (int q = 0; q < EPC && r0 + li + q < p.vrows; ++q) M[r0 + li + q + col] = x[li + q + lj * LD];
+            }
+        }
+        __syncthreads();
+    }
+}
+
+// fp32 apply of the partitioned sweep: 128-thread CTAs with 8 x 4 FFMA tiles
+// (4 CTAs/SM; k-major operands U^T from the slot's second half).  T tiles:
+// Z = X U_c with X as stored (rows of slot a, own columns), then W = U_a^T Z
+// from Z^T staged k-major (U_a = I: W = Z, U_a^T not loaded); V tiles: X U_c.
+__device__ __forceinline__ void store_T84(const Acc84 &acc, float *CT, int tid)
+{
+    constexpr int LD = Lay<float>::LD;
+    const int r = 4 * (tid & 7), c = 4 * (tid >> 3);
+    #pragma unroll
+    for (int u = 0; u < 8; ++u) {
+        const int row = r + (u & 3) + (u >> 2) * 32;
+        *(float4 *)(CT + c + row * LD) = make_float4(acc.v[u][0], acc.v[u][1], acc.v[u][2], acc.v[u][3]);
+    }
+}
+
+__global__ void __launch_bounds__(128) k_mg_apply_f32(MgApply p)
+{
+    constexpr int LD = Lay<float>::LD, EPC = 4, CPC = TW / EPC, NTH = 128;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    float *x = (float *)smem_raw, *uaT = x + TW * LD, *ucT = uaT + TW * LD;
+    const float *Ub = (const float *)p.Ubuf;         // slot s: U at 8192 s, U^T at 8192 s + 4096
+    const int total = p.ntT + p.ntV;
+    const bool skips = p.uid && *p.nid > 0;
+    auto advance = [&](int i) {
+        while (skips && i < total && mg_item_identity(p, i)) i += gridDim.x;
+        return i;
+    };
+    const int tid = threadIdx.x;
+    Acc84 acc;
+    for (int item = advance(blockIdx.x); item < total; item = advance(item + gridDim.x)) {
+        bool ttile;
+        int cl, a, r0;
+        mg_decode(p, item, ttile, cl, a, r0);
+        const SlotInfo sc = p.slots[cl];
+        const int cg = p.slot0 + cl;
+        float *M = (float *)(ttile ? p.T : p.V);
+        const int2 ra = ttile ? p.gslots[a] : make_int2(0, 0);
+        const bool two = ttile && !(skips && p.uid[a]);   // U_a^T Z needed
+        for (int e = tid; e < TW * CPC; e += NTH) {
+            const int lj = e / CPC, li = (e - lj * CPC) * EPC;
+            const int64_t col = (int64_t)pcol(sc, lj) * p.ld;
+            if (ttile) {
+                mg_cp16(x + li + lj * LD, M + gidx(ra, li) + col, 16);
+                if (two) mg_cp16(uaT + li + lj * LD, Ub + (size_t)a * 2 * TW * TW + TW * TW + li + lj * TW, 16);
+            } else {
+                const int rem = p.vrows - (r0 + li);
+                const int bytes = rem >= EPC ? 16 : (rem > 0 ? rem * (int)sizeof(float) : 0);
+                mg_cp16(x + li + lj * LD, M + (bytes ? (int64_t)(r0 + li) : 0) + col, bytes);
+            }
+            mg_cp16(ucT + li + lj * LD, Ub + (size_t)cg * 2 * TW * TW + TW * TW + li + lj * TW, 16);
+        }
+        asm volatile("cp.async.commit_group;\n" ::);
+        asm volatile("cp.async.wait_group 0;\n" ::);
+        __syncthreads();
+        tile_op84_t(x, ucT, acc, tid);                      // Z = X U_c
+        __syncthreads();
+        if (two) {
+            store_T84(acc, x, tid);                          // Z^T, k-major for the next product
+            __syncthreads();
+            tile_op84_t(uaT, x, acc, tid);                   // W = U_a^T Z
+            __syncthreads();
+        }
+        store_op84_t(acc, x, nullptr, tid);                  // W, column-major
+        __syncthreads();
+        for (int e = tid; e < TW * CPC; e += NTH) {
             const int lj = e / CPC, li = (e - lj * CPC) * EPC;
             const int64_t col = (int64_t)pcol(sc, lj) * p.ld;
             if (ttile) {
@@ -357,7 +487,8 @@ struct Group {
     Plan plan;
     int n = 0, np = 0, ncl = 0;        // ncl: local columns
     std::vector<RankBufs> rk;
-    void *Ubuf = nullptr;              // mb * 64 * 64 (fp64 size; fp32 uses the front)
+    void *Ubuf = nullptr;              // mb * 64 * 64 fp64 words (an fp32 slot: U, then U^T)
+    int *uid = nullptr;                // mb identity flags + one count per round
     int2 *gslots = nullptr;            // [round][mb]
     int2 *lsched = nullptr;
     unsigned long long *cnt = nullptr;
@@ -433,8 +564,12 @@ static mpj_status mg_sweep(Group &g, R **Ts, R **Vs, R nu, int rule)
     if (!attr[sizeof(R) == 8]) {
         MPJ_CK(cudaFuncSetAttribute(k_mg_solve<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_solve));
         MPJ_CK(cudaFuncSetAttribute(k_mg_apply<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_apply));
+        if (sizeof(R) == 4)
+            MPJ_CK(cudaFuncSetAttribute(k_mg_apply_f32, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_apply));
         attr[sizeof(R) == 8] = true;
     }
+    int *nid = g.uid + P.mb;
+    MPJ_CK(cudaMemsetAsync(nid, 0, (size_t)rounds * sizeof(int), g.st));
     int nsm = 148, dev = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
@@ -452,11 +587,14 @@ static mpj_status mg_sweep(Group &g, R **Ts, R **Vs, R nu, int rule)
         }
         if (prof) prof_mark(nsolve, g.st, false);
         if (g.nlocal == 1 && g.G > 1) {
-            const size_t per = (size_t)P.mbl * TW * TW;
+            const size_t per = (size_t)P.mbl * TW * TW * (8 / sizeof(R));   // fp32: U and U^T per slot
             R *U = (R *)g.Ubuf;
             MPJ_TRY(nccl_ck(ncclAllGather(U + g.me * per, U, per * sizeof(R), ncclChar, g.comm, g.st),
                             "ncclAllGather(U)"));
         }
+        // identity rotation blocks (every rank sees the same all-gathered U)
+        k_mg_uid<R><<<P.mb, 256, 0, g.st>>>((const R *)g.Ubuf, g.uid, nid + r);
+        count_launch();
         if (prof) prof_mark(napply, g.st, true);
         for (int i = 0; i < g.nlocal; ++i) {
             const int rr = g.rank_of(i);
@@ -465,10 +603,16 @@ static mpj_status mg_sweep(Group &g, R **Ts, R **Vs, R nu, int rule)
             ap.slots = g.rk[i].slots + (size_t)r * P.mbl;
             ap.gslots = g.gslots + (size_t)r * P.mb;
             ap.slot0 = rr * P.mbl; ap.mb = P.mb; ap.mbl = P.mbl; ap.Ubuf = g.Ubuf;
+            ap.uid = g.uid; ap.nid = nid + r;
             ap.ntT = P.mbl * (P.mb - 1);
             ap.ntV = (g.np / TW) * P.mbl;
-            const int grid = std::min(ap.ntT + ap.ntV, 2 * nsm);
-            k_mg_apply<R><<<grid, NT, sm_apply, g.st>>>(ap);
+            if (sizeof(R) == 4) {
+                const int grid = std::min(ap.ntT + ap.ntV, 4 * nsm);
+                k_mg_apply_f32<<<grid, 128, sm_apply, g.st>>>(ap);
+            } else {
+                const int grid = std::min(ap.ntT + ap.ntV, 2 * nsm);
+                k_mg_apply<R><<<grid, NT, sm_apply, g.st>>>(ap);
+            }
             count_launch();
         }
         if (prof) prof_mark(napply, g.st, false);
@@ -660,6 +804,7 @@ mpj_status mg_eig(bool mixed, const double *A, int64_t n, int64_t lda, double *L
         b.stage = (char *)alloc(4 * (size_t)BW * np * 8);
     }
     g.Ubuf = alloc((size_t)mb * TW * TW * 8);
+    g.uid = (int *)alloc((size_t)(mb + g.plan.nb) * sizeof(int));
     g.gslots = (int2 *)alloc((size_t)g.plan.nb * mb * sizeof(int2));
     g.lsched = (int2 *)alloc((BW - 1) * (BW / 2) * sizeof(int2));
     g.cnt = (unsigned long long *)alloc(64);

@@ -562,6 +562,55 @@ __device__ __forceinline__ void store_op(const AccOP &acc, float *C, float *CT)
     }
 }
 
+// fp32 8 x 4 register tiles (128 threads per 64 x 64 tile): thread tid =
+// (tx, ty) = (tid % 8, tid / 8) owns rows 4tx..4tx+3, 32+4tx..32+4tx+3 and
+// columns 4ty..4ty+3; C = A B^T-style k-major product (A[i + k LD], B[j + k LD]).
+struct Acc84 {
+    float v[8][4];
+};
+
+__device__ __forceinline__ void tile_op84_t(const float *A, const float *B, Acc84 &acc, int tid)
+{
+    constexpr int LD = Lay<float>::LD;
+    const int ra = 4 * (tid & 7), cb = 4 * (tid >> 3);
+    #pragma unroll
+    for (int u = 0; u < 8; ++u)
+        #pragma unroll
+        for (int w = 0; w < 4; ++w) acc.v[u][w] = 0.f;
+    float4 a0 = *(const float4 *)(A + ra), a1 = *(const float4 *)(A + ra + 32), b = *(const float4 *)(B + cb);
+    #pragma unroll 4
+    for (int k = 0; k < TW; ++k) {
+        const float av[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w}, bv[4] = {b.x, b.y, b.z, b.w};
+        if (k + 1 < TW) {                         // register prefetch of the next k
+            a0 = *(const float4 *)(A + ra + (k + 1) * LD);
+            a1 = *(const float4 *)(A + ra + 32 + (k + 1) * LD);
+            b = *(const float4 *)(B + cb + (k + 1) * LD);
+        }
+        #pragma unroll
+        for (int u = 0; u < 8; ++u)
+            #pragma unroll
+            for (int w = 0; w < 4; ++w) acc.v[u][w] = __fmaf_rn(av[u], bv[w], acc.v[u][w]);
+    }
+}
+
+__device__ __forceinline__ void store_op84_t(const Acc84 &acc, float *C, float *CT, int tid)
+{
+    constexpr int LD = Lay<float>::LD;
+    const int r = 4 * (tid & 7), c = 4 * (tid >> 3);
+    #pragma unroll
+    for (int w = 0; w < 4; ++w) {
+        *(float4 *)(C + r + (c + w) * LD) = make_float4(acc.v[0][w], acc.v[1][w], acc.v[2][w], acc.v[3][w]);
+        *(float4 *)(C + r + 32 + (c + w) * LD) = make_float4(acc.v[4][w], acc.v[5][w], acc.v[6][w], acc.v[7][w]);
+    }
+    if (CT) {
+        #pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const int row = r + (u & 3) + (u >> 2) * 32;
+            *(float4 *)(CT + c + row * LD) = make_float4(acc.v[u][0], acc.v[u][1], acc.v[u][2], acc.v[u][3]);
+        }
+    }
+}
+
 template <bool TRANS_A, typename R>
 __device__ __forceinline__ void tile_mm(const R *A, const R *B, Acc<R> &acc)
 {
