@@ -161,15 +161,23 @@ __device__ __forceinline__ void round_pair(int s, int lane, bool intra, const in
     }
 }
 
+// position of D(i, j): full storage, or (SYM) the upper triangle only
+template <typename R, bool SYM>
+__device__ __forceinline__ int didx(int i, int j)
+{
+    constexpr int LD = LayK<R>::LD;
+    return (!SYM || i <= j) ? i + j * LD : j + i * LD;
+}
+
 // the canonical 2x2 tile (rows of pair k, columns of pair l) after the round
-template <typename R>
+template <typename R, bool SYM = false>
 __device__ __forceinline__ void tile_after(const R *Dc, const WideParams<R> &P, int k, int l, R &x11, R &x21,
                                            R &x12, R &x22)
 {
-    constexpr int LD = LayK<R>::LD;
     const int pk = P.p[k], qk = P.q[k], pl = P.p[l], ql = P.q[l];
     const R sk = P.s[k], uk = P.u[k], sl = P.s[l], ul = P.u[l];
-    x11 = Dc[pk + pl * LD]; x21 = Dc[qk + pl * LD]; x12 = Dc[pk + ql * LD]; x22 = Dc[qk + ql * LD];
+    x11 = Dc[didx<R, SYM>(pk, pl)]; x21 = Dc[didx<R, SYM>(qk, pl)];
+    x12 = Dc[didx<R, SYM>(pk, ql)]; x22 = Dc[didx<R, SYM>(qk, ql)];
     if (P.gp[k] < P.gp[l]) {
         rot<R>(sk, uk, x11, x21); rot<R>(sk, uk, x12, x22);
         rot<R>(sl, ul, x11, x12); rot<R>(sl, ul, x21, x22);
@@ -180,12 +188,12 @@ __device__ __forceinline__ void tile_after(const R *Dc, const WideParams<R> &P, 
 }
 
 // diagonal entry of local index i after the round
-template <typename R>
+template <typename R, bool SYM = false>
 __device__ __forceinline__ R diag_after(const R *Dc, const WideParams<R> &P, int i)
 {
     constexpr int LD = LayK<R>::LD;
     const int k = P.pos[i], pk = P.p[k], qk = P.q[k];
-    const R apq = Dc[pk + qk * LD];
+    const R apq = Dc[didx<R, SYM>(pk, qk)];
     return i == pk ? fmaR(-P.t[k], apq, Dc[pk + pk * LD]) : fmaR(P.t[k], apq, Dc[qk + qk * LD]);
 }
 
@@ -244,7 +252,8 @@ __device__ __forceinline__ R *smem_rounds_wide(R *D0, R *D1, R *U, int2 bp, bool
         const int ga = gidx(bp, a), gc = gidx(bp, c);
         const int pk = ga < gc ? a : c, qk = ga < gc ? c : a;
         R t, sk, uk;
-        const int did = rot_params<R>(Dc[pk + pk * LD], Dc[qk + qk * LD], Dc[pk + qk * LD], nu, rule, t, sk, uk);
+        const int did = rot_params<R>(Dc[pk + pk * LD], Dc[qk + qk * LD], Dc[didx<R, UREG>(pk, qk)], nu, rule, t,
+                                      sk, uk);
         cnt += did;
         WideParams<R> &P = PP[0];
         P.t[lane] = t; P.s[lane] = sk; P.u[lane] = uk;
@@ -261,15 +270,15 @@ __device__ __forceinline__ R *smem_rounds_wide(R *D0, R *D1, R *U, int2 bp, bool
                 round_pair(s + 1, lane, intra, lsched, a, c);
                 const int ga = gidx(bp, a), gc = gidx(bp, c);
                 const int pn = ga < gc ? a : c, qn = ga < gc ? c : a;
-                const R app = diag_after<R>(Dc, P, pn), aqq = diag_after<R>(Dc, P, qn);
+                const R app = diag_after<R, UREG>(Dc, P, pn), aqq = diag_after<R, UREG>(Dc, P, qn);
                 // (pn, qn) lies in the tile of pairs k = pos[pn], l = pos[qn] (k != l)
                 const int k = P.pos[pn], l = P.pos[qn];
                 R x11, x21, x12, x22, apq;
                 if (k < l) {            // computed tile (k, l): rows of k, columns of l
-                    tile_after<R>(Dc, P, k, l, x11, x21, x12, x22);
+                    tile_after<R, UREG>(Dc, P, k, l, x11, x21, x12, x22);
                     apq = (pn == P.p[k]) ? (qn == P.p[l] ? x11 : x12) : (qn == P.p[l] ? x21 : x22);
                 } else {                // mirror of tile (l, k): entry (qn, pn)
-                    tile_after<R>(Dc, P, l, k, x11, x21, x12, x22);
+                    tile_after<R, UREG>(Dc, P, l, k, x11, x21, x12, x22);
                     apq = (qn == P.p[l]) ? (pn == P.p[k] ? x11 : x12) : (pn == P.p[k] ? x21 : x22);
                 }
                 R t, sk, uk;
@@ -286,17 +295,22 @@ __device__ __forceinline__ R *smem_rounds_wide(R *D0, R *D1, R *U, int2 bp, bool
             if (tk >= 0) {
                 if (tl >= 0) {
                     R x11, x21, x12, x22;
-                    tile_after<R>(Dc, P, tk, tl, x11, x21, x12, x22);
+                    tile_after<R, UREG>(Dc, P, tk, tl, x11, x21, x12, x22);
                     const int pk = P.p[tk], qk = P.q[tk], pl = P.p[tl], ql = P.q[tl];
-                    Dn[pk + pl * LD] = x11; Dn[qk + pl * LD] = x21; Dn[pk + ql * LD] = x12; Dn[qk + ql * LD] = x22;
-                    Dn[pl + pk * LD] = x11; Dn[pl + qk * LD] = x21; Dn[ql + pk * LD] = x12; Dn[ql + qk * LD] = x22;
+                    if (UREG) {   // cross rounds keep the upper triangle only (mirrored at the end)
+                        Dn[didx<R, true>(pk, pl)] = x11; Dn[didx<R, true>(qk, pl)] = x21;
+                        Dn[didx<R, true>(pk, ql)] = x12; Dn[didx<R, true>(qk, ql)] = x22;
+                    } else {
+                        Dn[pk + pl * LD] = x11; Dn[qk + pl * LD] = x21; Dn[pk + ql * LD] = x12; Dn[qk + ql * LD] = x22;
+                        Dn[pl + pk * LD] = x11; Dn[pl + qk * LD] = x21; Dn[ql + pk * LD] = x12; Dn[ql + qk * LD] = x22;
+                    }
                 } else {
                     const int pk = P.p[tk], qk = P.q[tk];
-                    const R apq = Dc[pk + qk * LD], t = P.t[tk];
+                    const R apq = Dc[didx<R, UREG>(pk, qk)], t = P.t[tk];
                     Dn[pk + pk * LD] = fmaR(-t, apq, Dc[pk + pk * LD]);
                     Dn[qk + qk * LD] = fmaR(t, apq, Dc[qk + qk * LD]);
-                    Dn[pk + qk * LD] = R(0);
-                    Dn[qk + pk * LD] = R(0);
+                    Dn[didx<R, UREG>(pk, qk)] = R(0);
+                    if (!UREG) Dn[qk + pk * LD] = R(0);
                 }
             }
             if (UREG) {
@@ -330,6 +344,12 @@ __device__ __forceinline__ R *smem_rounds_wide(R *D0, R *D1, R *U, int2 bp, bool
         __syncthreads();
         MPJ_K3_TRACE(2, s);
         R *tmp = Dc; Dc = Dn; Dn = tmp;
+    }
+    if (UREG) {                             // lower triangle of D from the upper one
+        for (int e = tid; e < TW * TW; e += NTW) {
+            const int i = e & (TW - 1), j = e >> 6;
+            if (i > j) Dc[i + j * LD] = Dc[j + i * LD];
+        }
     }
     if (UREG) {                             // back to shared memory (the shuffle after the last round is undone)
         #pragma unroll
