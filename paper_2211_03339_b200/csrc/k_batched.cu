@@ -13,7 +13,9 @@
 //       symmetrised (R11)
 //   a4-a8 fp64 sweeps on T with V = Q, stop test ||off(T)||_F <= eps ||As||_F
 //   a10 lambda = diag(T) stable-descending, V's columns alike.
-// Shared memory: three 64 x 68 fp64 panels (104 KB) -> 2 CTAs per SM.
+// a1 runs as its own kernel (k_batched_low: T32 and V32 only, 35 KB of shared
+// memory -> 6 CTAs per SM); the rest (a0, a2-a10) in k_batched_evd: three
+// 64 x 68 fp64 panels (104 KB) -> 2 CTAs per SM.
 #include "mpj_block.cuh"
 #include "mpj_device.cuh"
 #include "mpj_internal.h"
@@ -28,6 +30,7 @@ using namespace blk;
 struct BatchedArgs {
     const double *A;
     int n;
+    float *Z;                 // fp32 stage output: V32 per matrix (64 x 64, ld 64)
     double *lam, *V;
     int *sweeps, *sweeps_low, *flag;
     const int2 *lsched;
@@ -64,9 +67,47 @@ __device__ __forceinline__ double sq_norm(const R *M, bool offdiag, double *red)
     return cta_sum(acc, red);
 }
 
+// a1 as its own kernel: the fp32 stage needs only T32 and V32 (35 KB of
+// shared memory -> 6 matrices per SM instead of the 2 of the fp64 kernel); it
+// is ~80% of a matrix's inner rounds, which are latency bound, so concurrency
+// is what speeds it up.  Writes V32 (and the low sweep count).
+__global__ void __launch_bounds__(NT) k_batched_low(BatchedArgs a)
+{
+    constexpr int LF = Lay<float>::LD;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    float *T32 = (float *)smem_raw, *V32 = T32 + TW * LF;
+    __shared__ double red[NT / 32];
+    __shared__ InnerShared sh;
+    __shared__ InnerParams<float> pf;
+    const int n = a.n, tid = threadIdx.x;
+    const size_t mat = blockIdx.x;
+    const double *Ag = a.A + mat * (size_t)n * n;
+    const int2 bp = make_int2(0, 1);
+    // T32 = fl32((A + A^T) / 2) (the fp64 symmetrisation of a0, then rounded)
+    for (int e = tid; e < TW * TW; e += NT) {
+        const int i = e & (TW - 1), j = e >> 6;
+        const double x = (i < n && j < n) ? (Ag[i + (size_t)j * n] + Ag[j + (size_t)i * n]) * 0.5 : 0.0;
+        T32[i + j * LF] = (float)x;
+        V32[i + j * LF] = (i == j && i < n) ? 1.0f : 0.0f;
+    }
+    __syncthreads();
+    const double nA32 = sqrt(sq_norm<float>(T32, false, red));
+    const double tol_low = a.eps_low * nA32;
+    int swl = 0;
+    for (;;) {
+        const double off = sqrt(sq_norm<float>(T32, true, red));
+        if (off <= tol_low || swl >= a.max_sweeps_low) break;
+        ++swl;
+        inner_rounds<float>(T32, V32, bp, true, a.lsched, (float)a.nu_low, a.rule, sh, pf);
+    }
+    float *Zg = a.Z + mat * (size_t)TW * TW;
+    for (int e = tid; e < TW * TW; e += NT) Zg[e] = V32[(e & (TW - 1)) + (e >> 6) * LF];
+    if (tid == 0 && a.sweeps_low) a.sweeps_low[mat] = swl;
+}
+
 __global__ void __launch_bounds__(NT, 2) k_batched_evd(BatchedArgs a)
 {
-    constexpr int LD = Lay<double>::LD, LF = Lay<float>::LD;
+    constexpr int LD = Lay<double>::LD;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     double *RA = (double *)smem_raw;   // As, later T
     double *RB = RA + TW * LD;         // A staging, later Q = V
@@ -74,7 +115,6 @@ __global__ void __launch_bounds__(NT, 2) k_batched_evd(BatchedArgs a)
     __shared__ double red[NT / 32];
     __shared__ double coef[TW];
     __shared__ InnerShared sh;
-    __shared__ InnerParams<float> pf;
     __shared__ InnerParams<double> pd;
     __shared__ int rank_[TW];
     const int n = a.n, tid = threadIdx.x;
@@ -95,28 +135,13 @@ __global__ void __launch_bounds__(NT, 2) k_batched_evd(BatchedArgs a)
     __syncthreads();
     const double normA = sqrt(sq_norm<double>(RA, false, red));
 
-    // a1: low-precision stage
-    float *T32 = (float *)RC, *V32 = T32 + TW * LF;
-    for (int e = tid; e < TW * TW; e += NT) {
-        const int i = e & (TW - 1), j = e >> 6;
-        T32[i + j * LF] = (float)RA[i + j * LD];
-        V32[i + j * LF] = (i == j && i < n) ? 1.0f : 0.0f;
-    }
-    __syncthreads();
-    const double nA32 = sqrt(sq_norm<float>(T32, false, red));
-    const double tol_low = a.eps_low * nA32;
-    int swl = 0;
-    for (;;) {
-        const double off = sqrt(sq_norm<float>(T32, true, red));
-        if (off <= tol_low || swl >= a.max_sweeps_low) break;
-        ++swl;
-        inner_rounds<float>(T32, V32, bp, true, a.lsched, (float)a.nu_low, a.rule, sh, pf);
-    }
+    // a1 ran in k_batched_low: Z = V32 of this matrix
+    const float *Zg = a.Z + mat * (size_t)TW * TW;
 
     // a2: Q = CGS2(Z), Z = fp64(V32) (real n x n block)
     for (int e = tid; e < TW * TW; e += NT) {
         const int i = e & (TW - 1), j = e >> 6;
-        RB[i + j * LD] = (i < n && j < n) ? (double)V32[i + j * LF] : 0.0;
+        RB[i + j * LD] = (i < n && j < n) ? (double)Zg[i + j * TW] : 0.0;
     }
     __syncthreads();
     const int warp = tid >> 5, lane = tid & 31;
@@ -209,7 +234,6 @@ __global__ void __launch_bounds__(NT, 2) k_batched_evd(BatchedArgs a)
     }
     if (tid == 0) {
         if (a.sweeps) a.sweeps[mat] = sw;
-        if (a.sweeps_low) a.sweeps_low[mat] = swl;
         if (!conv) atomicOr(a.flag, 1);
         if (bad) atomicOr(a.flag, 2);
     }
@@ -224,35 +248,41 @@ mpj_status batched_evd(const double *A, int64_t n, int64_t batch, double *Lambda
     build_schedule(64, 32, hs);
     int2 *lsched = nullptr;
     int *flag = nullptr;
+    float *Z = nullptr;
     MPJ_CK(cudaMallocAsync(&lsched, hs.lsched.size() * sizeof(int2) + 256, st));
+    constexpr int64_t kChunk = 16384;   // matrices per launch pair (Z: 256 MB at most)
+    MPJ_CK(cudaMallocAsync(&Z, (size_t)std::min<int64_t>(batch, kChunk) * TW * TW * sizeof(float), st));
     flag = (int *)(lsched + hs.lsched.size());
     MPJ_CK(cudaMemcpyAsync(lsched, hs.lsched.data(), hs.lsched.size() * sizeof(int2), cudaMemcpyHostToDevice, st));
     MPJ_CK(cudaMemsetAsync(flag, 0, sizeof(int), st));
     BatchedArgs a;
     a.A = A; a.n = (int)n; a.lam = Lambda; a.V = V; a.sweeps = sweeps; a.sweeps_low = sweeps_low;
-    a.flag = flag; a.lsched = lsched;
+    a.flag = flag; a.lsched = lsched; a.Z = Z;
     const double omega = 1.1102230246251565e-16, upsilon = 5.9604644775390625e-08;
     a.eps = cfg.eps_factor * omega; a.nu = cfg.nu_factor * omega;
     a.eps_low = eps_low_factor(cfg, n) * upsilon; a.nu_low = cfg.nu_low_factor * upsilon;
     a.max_sweeps = cfg.max_sweeps; a.max_sweeps_low = cfg.max_sweeps_low; a.rule = cfg.stop_rule;
     const int smem = 3 * TW * Lay<double>::LD * sizeof(double);
+    const int smem_low = 2 * TW * Lay<float>::LD * sizeof(float);
     MPJ_CK(cudaFuncSetAttribute(k_batched_evd, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     const bool prof = prof_on();
     if (prof) prof_mark("batched_evd", st, true);
-    for (int64_t b0 = 0; b0 < batch; b0 += 65535) {
+    for (int64_t b0 = 0; b0 < batch; b0 += kChunk) {
         BatchedArgs ab = a;
-        const int64_t nb = std::min<int64_t>(65535, batch - b0);
+        const int64_t nb = std::min<int64_t>(kChunk, batch - b0);
         ab.A = A + b0 * n * n; ab.lam = Lambda + b0 * n; ab.V = V + b0 * n * n;
         ab.sweeps = sweeps ? sweeps + b0 : nullptr;
         ab.sweeps_low = sweeps_low ? sweeps_low + b0 : nullptr;
+        k_batched_low<<<(unsigned)nb, NT, smem_low, st>>>(ab);
         k_batched_evd<<<(unsigned)nb, NT, smem, st>>>(ab);
-        count_launch();
+        count_launch(2);
     }
     if (prof) prof_mark("batched_evd", st, false);
     int h_flag = 0;
     MPJ_CK(cudaMemcpyAsync(&h_flag, flag, sizeof(int), cudaMemcpyDeviceToHost, st));
     MPJ_CK(cudaStreamSynchronize(st));
     cudaFreeAsync(lsched, st);
+    cudaFreeAsync(Z, st);
     if (h_flag & 2) { set_error("batched: rank-deficient Z in CGS2"); return MPJ_ERR_RANKDEF; }
     if (h_flag & 1) { set_error("batched: some matrix reached max_sweeps"); return MPJ_ERR_NOCONV; }
     return MPJ_OK;
