@@ -6,7 +6,7 @@
 //   a0  As = (A + A^T)/2, ||As||_F
 //   a1  fp32 sweeps on fl32(As) with V32 = I (reading R12): the ordering for
 //       n_p = 64, b = 32 is one block round (31 intra + 32 cross rounds, R1),
-//       run by the same inner_rounds<> as the block variant's K3
+//       run by inner_rounds_b<> (mpj_block.cuh: U in registers)
 //   a2  Q = CGS2(fp64(V32)) (reading R10), column by column in shared memory,
 //       dot products by warp-shuffle reductions
 //   a3  T = Q^T As Q on the FP64 tensor pipe (two 64^3 DMMA tile products),
@@ -71,13 +71,13 @@ __device__ __forceinline__ double sq_norm(const R *M, bool offdiag, double *red)
 // shared memory -> 6 matrices per SM instead of the 2 of the fp64 kernel); it
 // is ~80% of a matrix's inner rounds, which are latency bound, so concurrency
 // is what speeds it up.  Writes V32 (and the low sweep count).
-__global__ void __launch_bounds__(NT) k_batched_low(BatchedArgs a)
+__global__ void __launch_bounds__(NT, 5) k_batched_low(BatchedArgs a)
 {
     constexpr int LF = Lay<float>::LD;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     float *T32 = (float *)smem_raw, *V32 = T32 + TW * LF;
     __shared__ double red[NT / 32];
-    __shared__ InnerShared sh;
+    __shared__ InnerSharedB sh;
     __shared__ InnerParams<float> pf;
     const int n = a.n, tid = threadIdx.x;
     const size_t mat = blockIdx.x;
@@ -98,7 +98,7 @@ __global__ void __launch_bounds__(NT) k_batched_low(BatchedArgs a)
         const double off = sqrt(sq_norm<float>(T32, true, red));
         if (off <= tol_low || swl >= a.max_sweeps_low) break;
         ++swl;
-        inner_rounds<float>(T32, V32, bp, true, a.lsched, (float)a.nu_low, a.rule, sh, pf);
+        inner_rounds_b<float>(T32, V32, true, a.lsched, (float)a.nu_low, a.rule, sh, pf);
     }
     float *Zg = a.Z + mat * (size_t)TW * TW;
     for (int e = tid; e < TW * TW; e += NT) Zg[e] = V32[(e & (TW - 1)) + (e >> 6) * LF];
@@ -114,7 +114,7 @@ __global__ void __launch_bounds__(NT, 2) k_batched_evd(BatchedArgs a)
     double *RC = RB + TW * LD;         // T32/V32, later W
     __shared__ double red[NT / 32];
     __shared__ double coef[TW];
-    __shared__ InnerShared sh;
+    __shared__ InnerSharedB sh;
     __shared__ InnerParams<double> pd;
     __shared__ int rank_[TW];
     const int n = a.n, tid = threadIdx.x;
@@ -212,7 +212,7 @@ __global__ void __launch_bounds__(NT, 2) k_batched_evd(BatchedArgs a)
         if (off <= tol) { conv = true; break; }
         if (sw >= a.max_sweeps) break;
         ++sw;
-        inner_rounds<double>(RA, RB, bp, true, a.lsched, a.nu, a.rule, sh, pd);
+        inner_rounds_b<double>(RA, RB, true, a.lsched, a.nu, a.rule, sh, pd);
     }
 
     // a10: extraction (stable descending rank)

@@ -25,40 +25,64 @@ template <typename R> struct LayK { static constexpr int LD = 65; };
 // global index of local index li (0..63) of block pair (I, J)
 __device__ __forceinline__ int gidx(int2 bp, int li) { return li < BW ? bp.x * BW + li : bp.y * BW + (li - BW); }
 
-// ---------------------------------------------------------------------------
-// The rounds of one block pair on its 64 x 64 diagonal block D (shared memory,
-// column-major, leading dimension LD), accumulating U <- U J (U may be NULL).
-// Local index li <-> global index gidx(bp, li).  Rounds: if `intra`, the b-1
-// merry-go-round rounds inside each half first (block round 0, reading R1),
-// then the b cyclic-shift cross rounds.  Same Lemma 3.1 arithmetic and the
-// same canonical tile order as the scalar kernels (k_rounds.cu).  Must be
-// called by all NT threads of the CTA.  Returns the number of rotations
-// (valid in thread 0).
-// ---------------------------------------------------------------------------
-struct InnerShared {
-    int lp[BW], lq[BW], gp[BW];
-    unsigned nrot;
-};
+// Rotation parameters of one round (pair k: t, s, tau).
 template <typename R> struct InnerParams {
     R t[BW], s[BW], u[BW];
 };
 
+// ---------------------------------------------------------------------------
+// The rounds of one block pair on its 64 x 64 block D for the batched path
+// (one block pair bp = (0, 1), NT = 256 threads): if `intra`, the b-1
+// merry-go-round rounds inside each half first (block round 0, reading R1),
+// then the b cyclic-shift cross rounds, with U in registers.  Thread (warp w, lane k) holds rows w + 8 i (i = 0..7) of U
+// at columns k (top half) and 32 + k (bottom half) at the start of a call.
+// Intra rounds pair columns inside each half (lsched): the two columns of a
+// pair sit in two lanes, each lane fetches its partner's value (shuffle) and
+// computes its own side with the same fused multiply-adds as rot().  Cross
+// round s pairs k with 32 + (k + s) mod 32: lane k holds that bottom column
+// (the bottoms move one lane per round), so the rotation is lane-local; after
+// the 32 cross rounds the layout is back to the start.  D is updated as in
+// the shared-memory version did (same element arithmetic, bit-identical
+// results); U's shared-memory traffic, half of a round's, goes away.
+// ---------------------------------------------------------------------------
+struct InnerSharedB {
+    int lp[BW], lq[BW], gp[BW];
+    int part_t[BW], part_b[BW];     // intra rounds: partner column (within the half) of lane k
+    int pair_t[BW], pair_b[BW];     // ... its pair index (parameters)
+    int isp_t[BW], isp_b[BW];       // ... whether lane k's column is the pair's p
+    unsigned nrot;
+};
+
 template <typename R>
-__device__ __forceinline__ unsigned inner_rounds(R *D, R *U, int2 bp, bool intra, const int2 *__restrict__ lsched,
-                                                 R nu, int rule, InnerShared &sh, InnerParams<R> &pr)
+__device__ __forceinline__ void rot_side(R s, R tau, bool isp, R &mine, R other)
+{
+    // rot(): x' = x - s (y + tau x), y' = y + s (x - tau y) (p = x, q = y)
+    mine = isp ? fmaR(-s, fmaR(tau, mine, other), mine) : fmaR(s, fmaR(-tau, mine, other), mine);
+}
+
+template <typename R>
+__device__ __forceinline__ unsigned inner_rounds_b(R *D, R *U, bool intra, const int2 *__restrict__ lsched, R nu,
+                                                   int rule, InnerSharedB &sh, InnerParams<R> &pr)
 {
     constexpr int LD = Lay<R>::LD;
-    const int tid = threadIdx.x;
+    const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+    R ut[8], ub[8];
+    #pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        ut[i] = U[(w + 8 * i) + lane * LD];
+        ub[i] = U[(w + 8 * i) + (BW + lane) * LD];
+    }
     if (tid == 0) sh.nrot = 0;
     __syncthreads();
     const int nrounds = intra ? (BW - 1) + BW : BW;
     for (int s = 0; s < nrounds; ++s) {
+        const bool in_intra = intra && s < BW - 1;
         if (tid < BW) {
             int a, c;
-            if (intra && s < BW - 1) {        // intra-block rounds (block round 0 only)
-                const int hb = BW / 2, w = tid;
-                const int2 lp = lsched[s * hb + (w < hb ? w : w - hb)];
-                const int off = (w < hb) ? 0 : BW;
+            if (in_intra) {
+                const int hb = BW / 2;
+                const int2 lp = lsched[s * hb + (tid < hb ? tid : tid - hb)];
+                const int off = (tid < hb) ? 0 : BW;
                 a = off + lp.x; c = off + lp.y;
             } else {
                 const int sc = intra ? s - (BW - 1) : s;
@@ -66,17 +90,26 @@ __device__ __forceinline__ unsigned inner_rounds(R *D, R *U, int2 bp, bool intra
                 int j = tid + sc; if (j >= BW) j -= BW;
                 c = BW + j;
             }
-            const int ga = gidx(bp, a), gc = gidx(bp, c);
-            const int lp = ga < gc ? a : c, lq = ga < gc ? c : a;
+            const int lp = a < c ? a : c, lq = a < c ? c : a;   // bp = (0, 1): local == global order
             R t, sn, u;
             const int did = rot_params<R>(D[lp + lp * LD], D[lq + lq * LD], D[lp + lq * LD], nu, rule, t, sn, u);
-            sh.lp[tid] = lp; sh.lq[tid] = lq; sh.gp[tid] = ga < gc ? ga : gc;
+            sh.lp[tid] = lp; sh.lq[tid] = lq; sh.gp[tid] = lp;
             pr.t[tid] = t; pr.s[tid] = sn; pr.u[tid] = u;
+            if (in_intra) {
+                if (tid < BW / 2) {
+                    sh.part_t[lp] = lq; sh.part_t[lq] = lp; sh.pair_t[lp] = tid; sh.pair_t[lq] = tid;
+                    sh.isp_t[lp] = 1; sh.isp_t[lq] = 0;
+                } else {
+                    sh.part_b[lp - BW] = lq - BW; sh.part_b[lq - BW] = lp - BW;
+                    sh.pair_b[lp - BW] = tid; sh.pair_b[lq - BW] = tid;
+                    sh.isp_b[lp - BW] = 1; sh.isp_b[lq - BW] = 0;
+                }
+            }
             const unsigned bal = __ballot_sync(0xffffffffu, did);
             if (tid == 0) sh.nrot += __popc(bal);
         }
         __syncthreads();
-        // D <- J^T D J on the 32 x 32 pair tiles (same canonical order as k_round_apply)
+        // D <- J^T D J on the 32 x 32 pair tiles (in place: each tile owned by one thread)
         for (int e = tid; e < BW * BW; e += NT) {
             const int kk = e & (BW - 1), ll = e >> 5;
             const int pk = sh.lp[kk], qk = sh.lq[kk];
@@ -100,21 +133,36 @@ __device__ __forceinline__ unsigned inner_rounds(R *D, R *U, int2 bp, bool intra
             }
             D[pk + pl * LD] = x11; D[qk + pl * LD] = x21; D[pk + ql * LD] = x12; D[qk + ql * LD] = x22;
         }
-        // U <- U J (columns lp, lq)
+        // U <- U J in registers
         if (U) {
-            for (int e = tid; e < BW * TW; e += NT) {
-                const int r = e & (TW - 1), kk = e >> 6;
-                const R sn = pr.s[kk];
-                if (sn != R(0)) {
-                    const int pk = sh.lp[kk], qk = sh.lq[kk];
-                    R x = U[r + pk * LD], y = U[r + qk * LD];
-                    rot<R>(sn, pr.u[kk], x, y);
-                    U[r + pk * LD] = x; U[r + qk * LD] = y;
+            if (in_intra) {
+                const int pt = sh.part_t[lane], pb = sh.part_b[lane];
+                const int jt = sh.pair_t[lane], jb = sh.pair_b[lane];
+                const bool it = sh.isp_t[lane] != 0, ib = sh.isp_b[lane] != 0;
+                const R st = pr.s[jt], tt = pr.u[jt], sb = pr.s[jb], tb = pr.u[jb];
+                #pragma unroll
+                for (int i = 0; i < 8; ++i) {
+                    const R ot = __shfl_sync(0xffffffffu, ut[i], pt), ob = __shfl_sync(0xffffffffu, ub[i], pb);
+                    if (st != R(0)) rot_side<R>(st, tt, it, ut[i], ot);
+                    if (sb != R(0)) rot_side<R>(sb, tb, ib, ub[i], ob);
+                }
+            } else {
+                const R sk = pr.s[lane], tk = pr.u[lane];
+                #pragma unroll
+                for (int i = 0; i < 8; ++i) {
+                    if (sk != R(0)) rot<R>(sk, tk, ut[i], ub[i]);   // p = a_k (top), q = b_k
+                    ub[i] = __shfl_sync(0xffffffffu, ub[i], (lane + 1) & 31);
                 }
             }
         }
         __syncthreads();
     }
+    #pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        U[(w + 8 * i) + lane * LD] = ut[i];
+        U[(w + 8 * i) + (BW + lane) * LD] = ub[i];
+    }
+    __syncthreads();
     return sh.nrot;
 }
 
