@@ -109,19 +109,24 @@ __device__ __forceinline__ unsigned inner_rounds_b(R *D, R *U, bool intra, const
             if (tid == 0) sh.nrot += __popc(bal);
         }
         __syncthreads();
-        // D <- J^T D J on the 32 x 32 pair tiles (in place: each tile owned by one thread)
-        for (int e = tid; e < BW * BW; e += NT) {
-            const int kk = e & (BW - 1), ll = e >> 5;
-            const int pk = sh.lp[kk], qk = sh.lq[kk];
-            if (kk == ll) {
-                const R apq = D[pk + qk * LD], t = pr.t[kk];
+        // D <- J^T D J: the 32 diagonal and 496 upper pair tiles (k < l), each
+        // also stored at its mirror (what the (l, k) tile computes, bit for bit)
+        for (int e = tid; e < BW + BW * (BW - 1) / 2; e += NT) {
+            if (e < BW) {
+                const int pk = sh.lp[e], qk = sh.lq[e];
+                const R apq = D[pk + qk * LD], t = pr.t[e];
                 D[pk + pk * LD] = fmaR(-t, apq, D[pk + pk * LD]);
                 D[qk + qk * LD] = fmaR(t, apq, D[qk + qk * LD]);
                 D[pk + qk * LD] = R(0);
                 D[qk + pk * LD] = R(0);
                 continue;
             }
-            const int pl = sh.lp[ll], ql = sh.lq[ll];
+            const int wt = e - BW;
+            int ll = (int)((1.0f + sqrtf(1.0f + 8.0f * wt)) * 0.5f);
+            while (ll * (ll - 1) / 2 > wt) --ll;
+            while ((ll + 1) * ll / 2 <= wt) ++ll;
+            const int kk = wt - ll * (ll - 1) / 2;
+            const int pk = sh.lp[kk], qk = sh.lq[kk], pl = sh.lp[ll], ql = sh.lq[ll];
             R x11 = D[pk + pl * LD], x21 = D[qk + pl * LD], x12 = D[pk + ql * LD], x22 = D[qk + ql * LD];
             const R sk = pr.s[kk], uk = pr.u[kk], sl = pr.s[ll], ul = pr.u[ll];
             if (sh.gp[kk] < sh.gp[ll]) {
@@ -132,6 +137,7 @@ __device__ __forceinline__ unsigned inner_rounds_b(R *D, R *U, bool intra, const
                 rot<R>(sk, uk, x11, x21); rot<R>(sk, uk, x12, x22);
             }
             D[pk + pl * LD] = x11; D[qk + pl * LD] = x21; D[pk + ql * LD] = x12; D[qk + ql * LD] = x22;
+            D[pl + pk * LD] = x11; D[pl + qk * LD] = x21; D[ql + pk * LD] = x12; D[ql + qk * LD] = x22;
         }
         // U <- U J in registers
         if (U) {
