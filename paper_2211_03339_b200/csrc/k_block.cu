@@ -781,7 +781,11 @@ static bool make_map32(CUtensorMap &m, const void *base, int64_t rows, int64_t c
 static bool launch_apply_f32ws(const ApplyArgs &p, cudaStream_t st)
 {
     CUtensorMap mT, mM;
-    if (!make_map32(mT, p.T, p.S.np, p.S.np, p.ldt) || !make_map32(mM, p.M, p.mrows, p.S.np, p.ldm)) return false;
+    // column updates only (SVD): no T tiles, M's map stands in for T's
+    const bool hasT = p.T != nullptr;
+    if (!make_map32(mT, hasT ? p.T : p.M, hasT ? p.S.np : p.mrows, p.S.np, hasT ? p.ldt : p.ldm) ||
+        !make_map32(mM, p.M, p.mrows, p.S.np, p.ldm))
+        return false;
     const size_t smem = (size_t)WS_NS * 3 * SH_TILE * sizeof(float) + 2 * WS_NS * sizeof(uint64_t);
     static bool attr = false;
     if (!attr) {
@@ -800,7 +804,7 @@ static bool launch_apply_f32ws(const ApplyArgs &p, cudaStream_t st)
 template <typename R>
 static void launch_apply(const ApplyArgs &p, cudaStream_t st)
 {
-    if (sizeof(R) == 4 && fp32_apply_kind() == 2 && p.T && p.mrows % 4 == 0 && launch_apply_f32ws(p, st)) return;
+    if (sizeof(R) == 4 && fp32_apply_kind() == 2 && p.mrows % 4 == 0 && launch_apply_f32ws(p, st)) return;
     if (sizeof(R) == 4 && fp32_apply_kind() >= 1) { launch_apply_f32w(p, st); return; }
     if (apply_stages() == 2) { launch_apply_s<R, 2>(p, st); return; }
     // column updates only (the SVD): two buffers per CTA, 3 CTAs/SM (an

@@ -134,7 +134,11 @@ __global__ void __launch_bounds__(NTW) k_svd_solve(const double *__restrict__ Gp
     for (int e = threadIdx.x; e < TW * TW; e += NTW) {
         const int li = e & (TW - 1), lj = e >> 6;
         Ua[li + lj * TW] = U[li + lj * LD];
-        if (sizeof(R) == 4) UaT[li + lj * TW] = U[lj + li * LD];
+        if (sizeof(R) == 4) {
+            UaT[li + lj * TW] = U[lj + li * LD];
+            // split-half U^T (operand of the TMA fp32 apply, see k_block.cu)
+            UaT[(size_t)mb * TW * TW + (li >> 5) * (BW * TW) + lj * BW + (li & 31)] = U[lj + li * LD];
+        }
     }
     if (threadIdx.x == 0) {
         if (nrot) atomicAdd(cnt, (unsigned long long)nrot);
@@ -227,7 +231,7 @@ static void carve_svd(char *base, size_t &off, int64_t m, int64_t n, SvdPlan &p)
     p.C32 = (float *)take(mnp * 4);
     p.V32 = (float *)take(nn * 4);
     p.Gpart = (double *)take((size_t)p.mb * p.splits * TW * TW * 8);
-    p.Ubuf = take((size_t)p.mb * TW * TW * 8);
+    p.Ubuf = take((size_t)p.mb * TW * TW * 12);   // fp64 U, or fp32 U, U^T and split-half U^T
     p.nrm = (double *)take(p.np * 8);
     p.sig = (double *)take(p.np * 8);
     p.red_part = (double *)take(kRedBlocks * 8);
