@@ -470,7 +470,7 @@ __device__ __forceinline__ void tile_op_sh(const float *A, const float *B, Acc48
         #pragma unroll
         for (int u = 0; u < 4; ++u)
             #pragma unroll
-            for (int w = 0; w < 8; ++w) acc.v[u][w] = __fmaf_rn(av[u], bv[w], acc.v[u][w]);
+            for (int w = 0; w < 8; w += 2) ffma2(av[u], bv[w], bv[w + 1], acc.v[u][w], acc.v[u][w + 1]);
     }
 }
 
@@ -525,7 +525,7 @@ __device__ __forceinline__ void tile_op_88(const float *A, const float *B, Acc88
         #pragma unroll
         for (int u = 0; u < 8; ++u)
             #pragma unroll
-            for (int w = 0; w < 8; ++w) acc.v[u][w] = __fmaf_rn(av[u], bv[w], acc.v[u][w]);
+            for (int w = 0; w < 8; w += 2) ffma2(av[u], bv[w], bv[w + 1], acc.v[u][w], acc.v[u][w + 1]);
     }
 }
 

@@ -636,6 +636,19 @@ __device__ __forceinline__ void store_op(const AccOP &acc, float *C, float *CT)
     }
 }
 
+// c0 += a b0, c1 += a b1 as one packed fp32x2 FMA (SASS FFMA2 with a scalar
+// operand): each lane is a round-to-nearest fused multiply-add, bit-identical
+// to two __fmaf_rn, in half the issue slots.
+__device__ __forceinline__ void ffma2(float a, float b0, float b1, float &c0, float &c1)
+{
+    unsigned long long aa, bb, cc, r;
+    asm("mov.b64 %0, {%1, %1};" : "=l"(aa) : "f"(a));
+    asm("mov.b64 %0, {%1, %2};" : "=l"(bb) : "f"(b0), "f"(b1));
+    asm("mov.b64 %0, {%1, %2};" : "=l"(cc) : "f"(c0), "f"(c1));
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(aa), "l"(bb), "l"(cc));
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(c0), "=f"(c1) : "l"(r));
+}
+
 // fp32 8 x 4 register tiles (128 threads per 64 x 64 tile): thread tid =
 // (tx, ty) = (tid % 8, tid / 8) owns rows 4tx..4tx+3, 32+4tx..32+4tx+3 and
 // columns 4ty..4ty+3; C = A B^T-style k-major product (A[i + k LD], B[j + k LD]).
@@ -663,7 +676,7 @@ __device__ __forceinline__ void tile_op84_t(const float *A, const float *B, Acc8
         #pragma unroll
         for (int u = 0; u < 8; ++u)
             #pragma unroll
-            for (int w = 0; w < 4; ++w) acc.v[u][w] = __fmaf_rn(av[u], bv[w], acc.v[u][w]);
+            for (int w = 0; w < 4; w += 2) ffma2(av[u], bv[w], bv[w + 1], acc.v[u][w], acc.v[u][w + 1]);
     }
 }
 
