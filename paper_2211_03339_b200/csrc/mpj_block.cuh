@@ -22,6 +22,20 @@ template <> struct Lay<float> { static constexpr int LD = 68; };    // 16-byte a
 // groups: 8-way conflicts that made K3 shared-memory bound).
 template <typename R> struct LayK { static constexpr int LD = 65; };
 
+// c0 += a b0, c1 += a b1 as one packed fp32x2 FMA (SASS FFMA2 with a scalar
+// operand): each lane is a round-to-nearest fused multiply-add, bit-identical
+// to two __fmaf_rn, in half the issue slots.
+__device__ __forceinline__ void ffma2(float a, float b0, float b1, float &c0, float &c1)
+{
+    unsigned long long aa, bb, cc, r;
+    asm("mov.b64 %0, {%1, %1};" : "=l"(aa) : "f"(a));
+    asm("mov.b64 %0, {%1, %2};" : "=l"(bb) : "f"(b0), "f"(b1));
+    asm("mov.b64 %0, {%1, %2};" : "=l"(cc) : "f"(c0), "f"(c1));
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(aa), "l"(bb), "l"(cc));
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(c0), "=f"(c1) : "l"(r));
+}
+
+
 // global index of local index li (0..63) of block pair (I, J)
 __device__ __forceinline__ int gidx(int2 bp, int li) { return li < BW ? bp.x * BW + li : bp.y * BW + (li - BW); }
 
@@ -583,6 +597,8 @@ __device__ __forceinline__ void tile_mm_acc(const float *A, const float *B, Acc<
         }
         #pragma unroll
         for (int w = 0; w < 4; ++w) b[w] = B[kk + (ty + 16 * w) * LD];
+        // scalar FMAs: the operands come from scalar strided loads, pairing them
+        // for FFMA2 costs register moves (measured slower in the SVD Gram)
         #pragma unroll
         for (int u = 0; u < 4; ++u)
             #pragma unroll
@@ -618,7 +634,7 @@ __device__ __forceinline__ void tile_op(const float *A, const float *B, AccOP &a
         #pragma unroll
         for (int u = 0; u < 4; ++u)
             #pragma unroll
-            for (int w = 0; w < 4; ++w) acc.v[u][w] = __fmaf_rn(av[u], bv[w], acc.v[u][w]);
+            for (int w = 0; w < 4; w += 2) ffma2(av[u], bv[w], bv[w + 1], acc.v[u][w], acc.v[u][w + 1]);
     }
 }
 // C (column-major) and C^T (column-major) stores of an AccOP, 128-bit each
@@ -634,19 +650,6 @@ __device__ __forceinline__ void store_op(const AccOP &acc, float *C, float *CT)
         for (int u = 0; u < 4; ++u)
             *(float4 *)(CT + c + (r + u) * LD) = make_float4(acc.v[u][0], acc.v[u][1], acc.v[u][2], acc.v[u][3]);
     }
-}
-
-// c0 += a b0, c1 += a b1 as one packed fp32x2 FMA (SASS FFMA2 with a scalar
-// operand): each lane is a round-to-nearest fused multiply-add, bit-identical
-// to two __fmaf_rn, in half the issue slots.
-__device__ __forceinline__ void ffma2(float a, float b0, float b1, float &c0, float &c1)
-{
-    unsigned long long aa, bb, cc, r;
-    asm("mov.b64 %0, {%1, %1};" : "=l"(aa) : "f"(a));
-    asm("mov.b64 %0, {%1, %2};" : "=l"(bb) : "f"(b0), "f"(b1));
-    asm("mov.b64 %0, {%1, %2};" : "=l"(cc) : "f"(c0), "f"(c1));
-    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(aa), "l"(bb), "l"(cc));
-    asm("mov.b64 {%0, %1}, %2;" : "=f"(c0), "=f"(c1) : "l"(r));
 }
 
 // fp32 8 x 4 register tiles (128 threads per 64 x 64 tile): thread tid =
