@@ -198,21 +198,30 @@ __device__ __forceinline__ void apply_body(const ApplyArgs &p, unsigned char *sm
     const int total = p.ntT + (V2 ? ((p.ntV / mb + 1) / 2) * mb : p.ntV);
     const int2 *bsr = p.S.bsched + p.Rb * mb;
     constexpr bool skips = SKIP;
-    auto advance = [&](int i) {
-        while (skips && i < total && item_identity(p, i, mb)) i += gridDim.x;
-        return i;
+    // this CTA's items: blockIdx.x + k G, k < K.  With one stage, the second half
+    // of the grid (the other CTA on an SM) walks its list backwards, so the two
+    // co-resident CTAs are out of phase and one computes while the other loads
+    // or stores (in lockstep both load at once and the DMMA pipe idles)
+    const int G = gridDim.x;
+    const int K = (int)blockIdx.x < total ? (total - 1 - (int)blockIdx.x) / G + 1 : 0;
+    const bool rev = STAGES == 1 && 2 * (int)blockIdx.x >= G;
+    auto item_at = [&](int k) { return (int)blockIdx.x + (rev ? K - 1 - k : k) * G; };
+    auto next_k = [&](int k) {
+        while (skips && k < K && item_identity(p, item_at(k), mb)) ++k;
+        return k;
     };
-    int item = advance(blockIdx.x);
+    int k = next_k(0);
     if (STAGES == 2) {
-        if (item < total) issue_item<R, NT, V2>(p, item, buf, buf + TW * LD, buf + (NB - 1) * TW * LD, skips);
+        if (k < K) issue_item<R, NT, V2>(p, item_at(k), buf, buf + TW * LD, buf + (NB - 1) * TW * LD, skips);
         cp_commit();
     }
-    for (int it = 0; item < total; ++it, item = advance(item + gridDim.x)) {
+    for (int it = 0; k < K; ++it, k = next_k(k + 1)) {
+        const int item = item_at(k);
         const int s = STAGES == 2 ? (it & 1) : 0;
         if (STAGES == 2) {
-            const int next = advance(item + gridDim.x);
+            const int kn = next_k(k + 1);
             R *nb = buf + (size_t)(NB * (s ^ 1)) * TW * LD;
-            if (next < total) issue_item<R, NT, V2>(p, next, nb, nb + TW * LD, nb + (NB - 1) * TW * LD, skips);
+            if (kn < K) issue_item<R, NT, V2>(p, item_at(kn), nb, nb + TW * LD, nb + (NB - 1) * TW * LD, skips);
             cp_commit();
             cp_wait1();
         } else {
@@ -250,8 +259,17 @@ __device__ __forceinline__ void apply_body(const ApplyArgs &p, unsigned char *sm
                     __syncthreads();
                     tile_mm<false>(x, uc, acc);                      // W = Y Uc
                 }
+                // shared memory is free after this barrier: W and W^T go straight from
+                // the accumulators to T while the next item's loads are issued
                 __syncthreads();
-                acc.each([&](int i, int j, R v) { x[i + j * LD] = v; ua[j + i * LD] = v; });   // W and W^T
+                R *T = (R *)p.T;
+                acc.each2([&](int i, int j, R v0, R v1) {    // W(i, j), W(i, j + 1); j even
+                    const int64_t gi = gidx(pa, i), gj = gidx(pc, j);
+                    T[gi + gj * p.ldt] = v0;
+                    T[gi + (gj + 1) * p.ldt] = v1;
+                    *(double2 *)(T + gj + gi * p.ldt) = make_double2(v0, v1);   // W^T(j .. j+1, i)
+                });
+                continue;
             }
             __syncthreads();
             R *T = (R *)p.T;
@@ -272,9 +290,18 @@ __device__ __forceinline__ void apply_body(const ApplyArgs &p, unsigned char *sm
             } else if constexpr (V2) {
                 Acc<R> acc, acc2;
                 tile_mm2(x, ua, uc, acc, acc2);                      // W = X Uc for both row tiles
-                __syncthreads();
-                acc.each([&](int i, int j, R v) { x[i + j * LD] = v; });
-                acc2.each([&](int i, int j, R v) { ua[i + j * LD] = v; });
+                __syncthreads();                                     // shared memory free: store from registers
+                R *M = (R *)p.M;
+                auto put = [&](int i, int j, R v0, R v1) {
+                    if (r0 + i < p.mrows) {
+                        const int64_t gj = gidx(pc, j);
+                        M[(int64_t)(r0 + i) + gj * p.ldm] = v0;
+                        M[(int64_t)(r0 + i) + (gj + 1) * p.ldm] = v1;
+                    }
+                };
+                acc.each2(put);
+                acc2.each2([&](int i, int j, R v0, R v1) { put(i + TW, j, v0, v1); });
+                continue;
             } else {
                 Acc<R> acc;
                 tile_mm<false>(x, uc, acc);                          // W = X Uc
