@@ -556,22 +556,11 @@ __device__ __forceinline__ void tile_op_88(const float *A, const float *B, Acc88
     }
 }
 
-__device__ __forceinline__ void store_op_88(const Acc88 &acc, float *C, int tid)
-{
-    const int q = tid >> 3, l8 = tid & 7;
-    const int r = 32 * (q & 1) + 4 * l8, c = 8 * (q >> 1);
-    #pragma unroll
-    for (int w = 0; w < 8; ++w) {
-        *(float4 *)(C + sh_idx(r, c + w)) = make_float4(acc.v[0][w], acc.v[1][w], acc.v[2][w], acc.v[3][w]);
-        *(float4 *)(C + sh_idx(r + 64, c + w)) = make_float4(acc.v[4][w], acc.v[5][w], acc.v[6][w], acc.v[7][w]);
-    }
-}
-
 template <bool SKIP>
 __device__ __forceinline__ void apply_f32ws_body(const ApplyArgs &p, const CUtensorMap &tmT, const CUtensorMap &tmM,
                                                  unsigned char *smem_raw)
 {
-    constexpr int EPC = 4, CPC = TW / EPC, SBUF = 3 * SH_TILE;
+    constexpr int SBUF = 3 * SH_TILE;
     float *ring = (float *)smem_raw;
     uint64_t *full = (uint64_t *)(smem_raw + (size_t)WS_NS * SBUF * sizeof(float));
     uint64_t *empty = full + WS_NS;
@@ -643,10 +632,17 @@ __device__ __forceinline__ void apply_f32ws_body(const ApplyArgs &p, const CUten
         const int st = j % WS_NS;
         mbar_wait(full + st, (j / WS_NS) & 1);
         float *x = ring + (size_t)st * SBUF, *ua = x + SH_TILE, *uc = ua + SH_TILE;
-        if (item < p.ntT) {
-            int a, c;
+        const bool ttile = item < p.ntT;
+        int a = 0, c, r0 = 0;
+        if (ttile) {
             decode_upper(item, a, c);
-            const int2 pa = bsr[a], pc = bsr[c];
+        } else {
+            const int idx = item - p.ntT;
+            c = idx % mb;
+            r0 = (idx / mb) * 2 * TW;
+        }
+        const int2 pa = bsr[a], pc = bsr[c];
+        if (ttile) {
             const bool ia = block_identity(p, a, skips), ic = block_identity(p, c, skips);
             if (ia) {
                 tile_op_sh(x, uc, acc, gt);                  // W = X U_c   (x = X)
@@ -659,42 +655,53 @@ __device__ __forceinline__ void apply_f32ws_body(const ApplyArgs &p, const CUten
                 group_sync(bar_id);
                 tile_op_sh(x, uc, acc, gt);                  // W = Y U_c
             }
-            group_sync(bar_id);
-            store_op_sh(acc, x, ua, gt);                     // W and W^T
-            group_sync(bar_id);
-            float *T = (float *)p.T;
-            for (int e = gt; e < TW * CPC; e += WS_CG) {
-                const int lj = e / CPC, li = (e - lj * CPC) * EPC;
-                *(int4 *)(T + gidx(pa, li) + (int64_t)gidx(pc, lj) * p.ldt) = *(const int4 *)(x + sh_idx(li, lj));
-                *(int4 *)(T + gidx(pc, li) + (int64_t)gidx(pa, lj) * p.ldt) = *(const int4 *)(ua + sh_idx(li, lj));
-            }
         } else {
-            const int idx = item - p.ntT, c = idx % mb, r0 = (idx / mb) * 2 * TW;
-            const int2 pc = bsr[c];
             tile_op_88(x, uc, acc8, gt);                     // W = X U_c (128 x 64)
-            group_sync(bar_id);
-            store_op_88(acc8, x, gt);
-            group_sync(bar_id);
-            float *M = (float *)p.M;
-            for (int e = gt; e < 2 * TW * CPC; e += WS_CG) {
-                const int lj = e / (2 * CPC), li = (e - lj * 2 * CPC) * EPC;
-                if (r0 + li < p.mrows)   // mrows % 4 == 0 on this path
-                    *(int4 *)(M + (int64_t)(r0 + li) + (int64_t)gidx(pc, lj) * p.ldm) = *(const int4 *)(x + sh_idx(li, lj));
-            }
         }
-        // all generic-proxy accesses of the stage are done before the async proxy refills it
+        // the stage is no longer read: release it (generic-proxy reads are ordered
+        // before the async-proxy refill) and store the results from registers
         asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
         group_sync(bar_id);
         if (gt == 0) mbar_arrive(empty + st);
+        const int q = gt >> 3, l8 = gt & 7;
+        if (ttile) {
+            // Acc48: rows r..r+3 (one 32-row block), columns cc..cc+7
+            const int r = 32 * (q & 1) + 4 * l8, cc = 8 * (q >> 1);
+            float *T = (float *)p.T;
+            const int64_t gr = gidx(pa, r), gcc = gidx(pc, cc);
+            #pragma unroll
+            for (int w = 0; w < 8; ++w)                      // W(r..r+3, cc+w)
+                *(float4 *)(T + gr + (int64_t)gidx(pc, cc + w) * p.ldt) =
+                    make_float4(acc.v[0][w], acc.v[1][w], acc.v[2][w], acc.v[3][w]);
+            #pragma unroll
+            for (int u = 0; u < 4; ++u) {                    // W^T(cc..cc+7, r+u)
+                float *dst = T + gcc + (int64_t)(gr + u) * p.ldt;
+                *(float4 *)dst = make_float4(acc.v[u][0], acc.v[u][1], acc.v[u][2], acc.v[u][3]);
+                *(float4 *)(dst + 4) = make_float4(acc.v[u][4], acc.v[u][5], acc.v[u][6], acc.v[u][7]);
+            }
+        } else {
+            // Acc88: rows r..r+3 and r+64..r+67, columns cc..cc+7
+            const int r = 32 * (q & 1) + 4 * l8, cc = 8 * (q >> 1);
+            float *M = (float *)p.M;
+            #pragma unroll
+            for (int w = 0; w < 8; ++w) {
+                const int64_t col = (int64_t)gidx(pc, cc + w) * p.ldm;
+                if (r0 + r < p.mrows)                        // mrows % 4 == 0 on this path
+                    *(float4 *)(M + (r0 + r) + col) = make_float4(acc8.v[0][w], acc8.v[1][w], acc8.v[2][w], acc8.v[3][w]);
+                if (r0 + r + TW < p.mrows)
+                    *(float4 *)(M + (r0 + r + TW) + col) =
+                        make_float4(acc8.v[4][w], acc8.v[5][w], acc8.v[6][w], acc8.v[7][w]);
+            }
+        }
     }
 }
 
 __global__ void __launch_bounds__(WS_NT, 1) k_block_apply_f32ws(ApplyArgs p, const __grid_constant__ CUtensorMap tmT,
                                                                 const __grid_constant__ CUtensorMap tmM)
 {
-    extern __shared__ __align__(128) unsigned char smem_raw[];
-    if (p.uid && *p.nid > 0) apply_f32ws_body<true>(p, tmT, tmM, smem_raw);
-    else apply_f32ws_body<false>(p, tmT, tmM, smem_raw);
+    extern __shared__ __align__(128) unsigned char smem_ws[];   // TMA boxes need 128-byte alignment
+    if (p.uid && *p.nid > 0) apply_f32ws_body<true>(p, tmT, tmM, smem_ws);
+    else apply_f32ws_body<false>(p, tmT, tmM, smem_ws);
 }
 
 }  // namespace
@@ -845,7 +852,6 @@ mpj_status block_sweep(R *T, int64_t ldt, R *V, int64_t ldv, int vrows, const De
                        unsigned long long *cnt, void *scratch, cudaStream_t st, bool first_sweep)
 {
     if (ds.b != BW) { set_error("block variant needs b = 32"); return MPJ_ERR_INVALID; }
-    constexpr int LD = Lay<R>::LD;
     Sched S;
     S.bsched = ds.bsched; S.lsched = ds.lsched; S.b = ds.b; S.nb = ds.nb; S.np = ds.np;
     const int mb = ds.nb / 2;
