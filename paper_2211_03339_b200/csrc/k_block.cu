@@ -305,8 +305,16 @@ __device__ __forceinline__ void apply_body(const ApplyArgs &p, unsigned char *sm
             } else {
                 Acc<R> acc;
                 tile_mm<false>(x, uc, acc);                          // W = X Uc
-                __syncthreads();
-                acc.each([&](int i, int j, R v) { x[i + j * LD] = v; });
+                __syncthreads();                                     // shared memory free: store from registers
+                R *M = (R *)p.M;
+                acc.each2([&](int i, int j, R v0, R v1) {
+                    if (r0 + i < p.mrows) {
+                        const int64_t gj = gidx(pc, j);
+                        M[(int64_t)(r0 + i) + gj * p.ldm] = v0;
+                        M[(int64_t)(r0 + i) + (gj + 1) * p.ldm] = v1;
+                    }
+                });
+                continue;
             }
             __syncthreads();
             R *M = (R *)p.M;
