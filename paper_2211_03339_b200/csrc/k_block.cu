@@ -95,6 +95,17 @@ __device__ __forceinline__ void cp16(void *dst, const void *src, int src_bytes)
 __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::); }
 __device__ __forceinline__ void cp_wait1() { asm volatile("cp.async.wait_group 1;\n" ::); }
 __device__ __forceinline__ void cp_wait0() { asm volatile("cp.async.wait_group 0;\n" ::); }
+// wait until at most n cp.async groups are pending (n <= 4)
+__device__ __forceinline__ void cp_wait_le(int n)
+{
+    switch (n) {
+    case 0: asm volatile("cp.async.wait_group 0;\n" ::); break;
+    case 1: asm volatile("cp.async.wait_group 1;\n" ::); break;
+    case 2: asm volatile("cp.async.wait_group 2;\n" ::); break;
+    case 3: asm volatile("cp.async.wait_group 3;\n" ::); break;
+    default: asm volatile("cp.async.wait_group 4;\n" ::); break;
+    }
+}
 
 struct ApplyArgs {
     void *T; int64_t ldt;
@@ -182,6 +193,107 @@ __device__ __forceinline__ bool item_identity(const ApplyArgs &p, int item, int 
 
 // STAGES = 2: one CTA per SM prefetches item i+1 while computing item i;
 // STAGES = 1: two CTAs per SM overlap each other's loads and epilogues.
+// One fp64 work item with k-chunked loads (one-stage path): a full T tile
+// issues X and U_a in four row chunks (GEMM 1's k) and then U_c, V tiles issue
+// X columns and U_c rows in four chunks; each product waits only for the chunk
+// it is about to use, so the first k-steps overlap the rest of the loads.
+// Results go from the accumulators straight to global memory.
+template <bool V2, bool SKIP>
+__device__ __forceinline__ void apply_item_f64(const ApplyArgs &p, int item, double *x, double *ua, double *uc, int mb,
+                                               const int2 *bsr)
+{
+    constexpr int LD = Lay<double>::LD, EPC = 2, CPC = TW / EPC;
+    constexpr bool skips = SKIP;
+    const double *Ub = (const double *)p.Ubuf;
+    const int tid = threadIdx.x;
+    if (item < p.ntT) {
+        int a, c;
+        decode_upper(item, a, c);
+        const int2 pa = bsr[a], pc = bsr[c];
+        const bool ia = block_identity(p, a, skips), ic = block_identity(p, c, skips);
+        const double *T = (const double *)p.T;
+        const double *Uag = Ub + (size_t)a * TW * TW, *Ucg = Ub + (size_t)c * TW * TW;
+        Acc<double> acc;
+        if (!ia && !ic) {
+            for (int ch = 0; ch < 4; ++ch) {
+                for (int e = tid; e < TW * 8; e += NT) {     // 64 columns x 8 segments of 2 rows
+                    const int lj = e >> 3, li = 16 * ch + 2 * (e & 7);
+                    cp16(x + li + lj * LD, T + gidx(pa, li) + (int64_t)gidx(pc, lj) * p.ldt, 16);
+                    cp16(ua + li + lj * LD, Uag + li + lj * TW, 16);
+                }
+                cp_commit();
+            }
+            for (int e = tid; e < TW * CPC; e += NT) {
+                const int lj = e / CPC, li = (e - lj * CPC) * EPC;
+                cp16(uc + li + lj * LD, Ucg + li + lj * TW, 16);
+            }
+            cp_commit();
+            tile_mm_chunked<true>(ua, x, acc, [&](int ch) { cp_wait_le(4 - ch); __syncthreads(); });   // Y = Ua^T X
+            __syncthreads();
+            acc.each([&](int i, int j, double v) { x[i + j * LD] = v; });
+            cp_wait0();
+            __syncthreads();
+            tile_mm<false>(x, uc, acc);                      // W = Y Uc
+        } else {
+            // one identity block: a single product, the identity is not loaded
+            for (int e = tid; e < TW * CPC; e += NT) {
+                const int lj = e / CPC, li = (e - lj * CPC) * EPC;
+                cp16(x + li + lj * LD, T + gidx(pa, li) + (int64_t)gidx(pc, lj) * p.ldt, 16);
+                if (!ia) cp16(ua + li + lj * LD, Uag + li + lj * TW, 16);
+                if (!ic) cp16(uc + li + lj * LD, Ucg + li + lj * TW, 16);
+            }
+            cp_commit();
+            cp_wait0();
+            __syncthreads();
+            if (ia) tile_mm<false>(x, uc, acc);              // W = X Uc
+            else tile_mm<true>(ua, x, acc);                  // W = Ua^T X
+        }
+        __syncthreads();                                     // shared memory free: store from registers
+        double *Tw = (double *)p.T;
+        acc.each2([&](int i, int j, double v0, double v1) {  // W(i, j), W(i, j + 1); j even
+            const int64_t gi = gidx(pa, i), gj = gidx(pc, j);
+            Tw[gi + gj * p.ldt] = v0;
+            Tw[gi + (gj + 1) * p.ldt] = v1;
+            *(double2 *)(Tw + gj + gi * p.ldt) = make_double2(v0, v1);   // W^T(j .. j+1, i)
+        });
+        return;
+    }
+    constexpr int NH = V2 ? 2 : 1;                           // row tiles in the item
+    const int idx = item - p.ntT, c = idx % mb, r0 = (idx / mb) * NH * TW;
+    const int2 pc = bsr[c];
+    const double *M = (const double *)p.M;
+    const double *Ucg = Ub + (size_t)c * TW * TW;
+    for (int ch = 0; ch < 4; ++ch) {
+        for (int e = tid; e < 16 * CPC * NH; e += NT) {      // columns 16ch .. 16ch+15 of X (each row tile)
+            const int h = e / (16 * CPC), r = e - h * 16 * CPC;
+            const int lj = 16 * ch + r / CPC, li = (r % CPC) * EPC;
+            const int row = r0 + h * TW + li, rem = p.mrows - row;
+            const int bytes = rem >= EPC ? 16 : (rem > 0 ? rem * 8 : 0);
+            cp16((h ? ua : x) + li + lj * LD, M + (bytes ? (int64_t)row : 0) + (int64_t)gidx(pc, lj) * p.ldm, bytes);
+        }
+        for (int e = tid; e < TW * 8; e += NT) {              // rows 16ch .. 16ch+15 of U_c
+            const int lj = e >> 3, li = 16 * ch + 2 * (e & 7);
+            cp16(uc + li + lj * LD, Ucg + li + lj * TW, 16);
+        }
+        cp_commit();
+    }
+    auto wait = [&](int ch) { cp_wait_le(3 - ch); __syncthreads(); };
+    Acc<double> acc, acc2;
+    if constexpr (V2) tile_mm2_chunked(x, ua, uc, acc, acc2, wait);   // W = X Uc for both row tiles
+    else tile_mm_chunked<false>(x, uc, acc, wait);                     // W = X Uc
+    __syncthreads();                                         // shared memory free: store from registers
+    double *Mw = (double *)p.M;
+    auto put = [&](int i, int j, double v0, double v1) {
+        if (r0 + i < p.mrows) {
+            const int64_t gj = gidx(pc, j);
+            Mw[(int64_t)(r0 + i) + gj * p.ldm] = v0;
+            Mw[(int64_t)(r0 + i) + (gj + 1) * p.ldm] = v1;
+        }
+    };
+    acc.each2(put);
+    if constexpr (V2) acc2.each2([&](int i, int j, double v0, double v1) { put(i + TW, j, v0, v1); });
+}
+
 // SKIP: this block round has identity blocks (skip / one-product logic); the
 // kernel picks the instantiation once per CTA so that launches without
 // identities run the plain loop (the checks cost 3% per full launch).
@@ -218,6 +330,11 @@ __device__ __forceinline__ void apply_body(const ApplyArgs &p, unsigned char *sm
     for (int it = 0; k < K; ++it, k = next_k(k + 1)) {
         const int item = item_at(k);
         const int s = STAGES == 2 ? (it & 1) : 0;
+        if constexpr (sizeof(R) == 8 && STAGES == 1) {
+            double *b64 = (double *)buf;   // X, Ua, Uc (column-only launches: X, Uc)
+            apply_item_f64<V2, SKIP>(p, item, b64, b64 + TW * LD, b64 + (NB - 1) * TW * LD, mb, bsr);
+            continue;
+        }
         if (STAGES == 2) {
             const int kn = next_k(k + 1);
             R *nb = buf + (size_t)(NB * (s ^ 1)) * TW * LD;

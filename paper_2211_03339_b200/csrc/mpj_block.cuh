@@ -582,6 +582,72 @@ __device__ __forceinline__ void tile_mm2(const double *A1, const double *A2, con
     }
 }
 
+// k-chunked fp64 products: before the 4 k-steps of chunk c (k = 16c .. 16c+15)
+// wait(c) runs (a cp.async group wait + barrier), so the product starts as soon
+// as the first chunk of its operands has landed
+template <bool TRANS_A, typename W>
+__device__ __forceinline__ void tile_mm_chunked(const double *A, const double *B, Acc<double> &acc, W wait)
+{
+    constexpr int LD = Lay<double>::LD;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, tig = lane & 3;
+    const int rb = (warp >> 1) * 16 + g, cb = (warp & 1) * 32 + g;
+    acc.zero();
+    #pragma unroll 1
+    for (int ch = 0; ch < 4; ++ch) {
+        wait(ch);
+        #pragma unroll
+        for (int ks = 4 * ch; ks < 4 * ch + 4; ++ks) {
+            const int kk = ks * 4 + tig;
+            double a[2], b[4];
+            #pragma unroll
+            for (int mi = 0; mi < 2; ++mi) {
+                const int row = rb + mi * 8;
+                a[mi] = TRANS_A ? A[kk + row * LD] : A[row + kk * LD];
+            }
+            #pragma unroll
+            for (int ni = 0; ni < 4; ++ni) b[ni] = B[kk + (cb + ni * 8) * LD];
+            #pragma unroll
+            for (int mi = 0; mi < 2; ++mi)
+                #pragma unroll
+                for (int ni = 0; ni < 4; ++ni) dmma884(acc.v[mi][ni][0], acc.v[mi][ni][1], a[mi], b[ni]);
+        }
+    }
+}
+
+template <typename W>
+__device__ __forceinline__ void tile_mm2_chunked(const double *A1, const double *A2, const double *B,
+                                                 Acc<double> &c1, Acc<double> &c2, W wait)
+{
+    constexpr int LD = Lay<double>::LD;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, tig = lane & 3;
+    const int rb = (warp >> 1) * 16 + g, cb = (warp & 1) * 32 + g;
+    c1.zero();
+    c2.zero();
+    #pragma unroll 1
+    for (int ch = 0; ch < 4; ++ch) {
+        wait(ch);
+        #pragma unroll 2
+        for (int ks = 4 * ch; ks < 4 * ch + 4; ++ks) {
+            const int kk = ks * 4 + tig;
+            double a1[2], a2[2], b[4];
+            #pragma unroll
+            for (int mi = 0; mi < 2; ++mi) {
+                a1[mi] = A1[rb + mi * 8 + kk * LD];
+                a2[mi] = A2[rb + mi * 8 + kk * LD];
+            }
+            #pragma unroll
+            for (int ni = 0; ni < 4; ++ni) b[ni] = B[kk + (cb + ni * 8) * LD];
+            #pragma unroll
+            for (int mi = 0; mi < 2; ++mi)
+                #pragma unroll
+                for (int ni = 0; ni < 4; ++ni) {
+                    dmma884(c1.v[mi][ni][0], c1.v[mi][ni][1], a1[mi], b[ni]);
+                    dmma884(c2.v[mi][ni][0], c2.v[mi][ni][1], a2[mi], b[ni]);
+                }
+        }
+    }
+}
+
 template <bool TRANS_A>
 __device__ __forceinline__ void tile_mm_acc(const float *A, const float *B, Acc<float> &acc)
 {
