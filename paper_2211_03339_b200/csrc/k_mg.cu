@@ -166,11 +166,14 @@ __global__ void __launch_bounds__(NT) k_mg_apply(MgApply p)
     const R *Ub = (const R *)p.Ubuf;
     const int total = p.ntT + p.ntV;
     const bool skips = p.uid && *p.nid > 0;
-    auto advance = [&](int i) {
-        while (skips && i < total && mg_item_identity(p, i)) i += gridDim.x;
-        return i;
-    };
-    for (int item = advance(blockIdx.x); item < total; item = advance(item + gridDim.x)) {
+    // this CTA's items blockIdx.x + k G; the second half of the grid walks them
+    // backwards so the two CTAs of an SM do not load and store in lockstep
+    const int G = gridDim.x;
+    const int K = (int)blockIdx.x < total ? (total - 1 - (int)blockIdx.x) / G + 1 : 0;
+    const bool rev = 2 * (int)blockIdx.x >= G;
+    for (int kk = 0; kk < K; ++kk) {
+        const int item = (int)blockIdx.x + (rev ? K - 1 - kk : kk) * G;
+        if (skips && mg_item_identity(p, item)) continue;
         bool ttile;
         int cl, a, r0;
         mg_decode(p, item, ttile, cl, a, r0);
@@ -205,7 +208,21 @@ __global__ void __launch_bounds__(NT) k_mg_apply(MgApply p)
             __syncthreads();
         }
         if (!ic) tile_mm<false>(x, uc, acc);            // W = Y U_c  (or X U_c)
-        __syncthreads();
+        __syncthreads();                                // shared memory free: store from registers
+        if constexpr (sizeof(R) == 8) {
+            acc.each2([&](int i, int j, R v0, R v1) {   // W(i, j), W(i, j + 1); j even, same 32-column block
+                const int64_t col = (int64_t)pcol(sc, j) * p.ld;
+                if (ttile) {
+                    const int64_t gi = gidx(ra, i);
+                    M[gi + col] = v0;
+                    M[gi + col + p.ld] = v1;
+                } else if (r0 + i < p.vrows) {
+                    M[(r0 + i) + col] = v0;
+                    M[(r0 + i) + col + p.ld] = v1;
+                }
+            });
+            continue;
+        }
         acc.each([&](int i, int j, R v) { x[i + j * LD] = v; });
         __syncthreads();
         for (int e = threadIdx.x; e < TW * CPC; e += NT) {
@@ -246,13 +263,14 @@ __global__ void __launch_bounds__(128) k_mg_apply_f32(MgApply p)
     const float *Ub = (const float *)p.Ubuf;         // slot s: U at 8192 s, U^T at 8192 s + 4096
     const int total = p.ntT + p.ntV;
     const bool skips = p.uid && *p.nid > 0;
-    auto advance = [&](int i) {
-        while (skips && i < total && mg_item_identity(p, i)) i += gridDim.x;
-        return i;
-    };
     const int tid = threadIdx.x;
     Acc84 acc;
-    for (int item = advance(blockIdx.x); item < total; item = advance(item + gridDim.x)) {
+    const int G = gridDim.x;
+    const int K = (int)blockIdx.x < total ? (total - 1 - (int)blockIdx.x) / G + 1 : 0;
+    const bool rev = (4 * (int)blockIdx.x / G) & 1;   // alternate directions among the CTAs of an SM
+    for (int kk = 0; kk < K; ++kk) {
+        const int item = (int)blockIdx.x + (rev ? K - 1 - kk : kk) * G;
+        if (skips && mg_item_identity(p, item)) continue;
         bool ttile;
         int cl, a, r0;
         mg_decode(p, item, ttile, cl, a, r0);
@@ -285,20 +303,25 @@ __global__ void __launch_bounds__(128) k_mg_apply_f32(MgApply p)
             tile_op84_t(uaT, x, acc, tid);                   // W = U_a^T Z
             __syncthreads();
         }
-        store_op84_t(acc, x, nullptr, tid);                  // W, column-major
-        __syncthreads();
-        for (int e = tid; e < TW * CPC; e += NTH) {
-            const int lj = e / CPC, li = (e - lj * CPC) * EPC;
-            const int64_t col = (int64_t)pcol(sc, lj) * p.ld;
-            if (ttile) {
-                *(int4 *)(M + gidx(ra, li) + col) = *(const int4 *)(x + li + lj * LD);
-            } else if (r0 + li + EPC <= p.vrows) {
-                *(int4 *)(M + (r0 + li) + col) = *(const int4 *)(x + li + lj * LD);
-            } else {
-                for (int q = 0; q < EPC && r0 + li + q < p.vrows; ++q) M[r0 + li + q + col] = x[li + q + lj * LD];
+        // W from the accumulators: rows r..r+3 and r+32..r+35 (float4 each) of columns cc..cc+3
+        const int r = 4 * (tid & 7), cc = 4 * (tid >> 3);
+        #pragma unroll
+        for (int w = 0; w < 4; ++w) {
+            const int64_t col = (int64_t)pcol(sc, cc + w) * p.ld;
+            #pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const float4 v = make_float4(acc.v[4 * h][w], acc.v[4 * h + 1][w], acc.v[4 * h + 2][w], acc.v[4 * h + 3][w]);
+                const int li = r + 32 * h;
+                if (ttile) {
+                    *(float4 *)(M + gidx(ra, li) + col) = v;
+                } else if (r0 + li + EPC <= p.vrows) {
+                    *(float4 *)(M + (r0 + li) + col) = v;
+                } else {
+                    const float vv[4] = {v.x, v.y, v.z, v.w};
+                    for (int q = 0; q < EPC && r0 + li + q < p.vrows; ++q) M[r0 + li + q + col] = vv[q];
+                }
             }
         }
-        __syncthreads();
     }
 }
 
