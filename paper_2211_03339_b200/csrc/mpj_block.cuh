@@ -313,6 +313,15 @@ __device__ __forceinline__ R *smem_rounds_wide(R *D0, R *D1, R *U, int2 bp, bool
         for (int j = 0; j < 3; ++j)
             if (j < nrow) { ua[j] = U[urow[j] + lane * LD]; ub[j] = U[urow[j] + (BW + lane) * LD]; }
     }
+    // cross rounds (UREG): pair k of cross round x is (k, 32 + (k + x) mod 32), so
+    // its p / q, its position in the order of global p indices and the pair of
+    // a local index are arithmetic -- no dependent shared-memory index loads
+    // on the parameter warp's critical path
+    auto xp = [&](int k, int x) { return flip ? BW + ((k + x) & 31) : k; };
+    auto xq = [&](int k, int x) { return flip ? k : BW + ((k + x) & 31); };
+    auto xkey = [&](int k, int x) { return flip ? ((k + x) & 31) : k; };
+    auto xpos = [&](int i, int x) { return i < BW ? i : ((i - BW - x) & 31); };
+    R ct = R(0), cs = R(0), cu = R(0);      // parameter warp: (t, s, tau) of pair `lane` this round
     // parameters of round 0
     if (warp == 0) {
         int a, c;
@@ -322,6 +331,7 @@ __device__ __forceinline__ R *smem_rounds_wide(R *D0, R *D1, R *U, int2 bp, bool
         R t, sk, uk;
         const int did = rot_params<R>(Dc[pk + pk * LD], Dc[qk + qk * LD], Dc[didx<R, UREG>(pk, qk)], nu, rule, t,
                                       sk, uk);
+        ct = t; cs = sk; cu = uk;
         cnt += did;
         WideParams<R> &P = PP[0];
         P.t[lane] = t; P.s[lane] = sk; P.u[lane] = uk;
@@ -331,7 +341,43 @@ __device__ __forceinline__ R *smem_rounds_wide(R *D0, R *D1, R *U, int2 bp, bool
     __syncthreads();
     for (int s = 0; s < nrounds; ++s) {
         const WideParams<R> &P = PP[s & 1];
-        if (warp == 0) {
+        if (UREG && warp == 0) {
+            if (s + 1 < nrounds) {
+                WideParams<R> &N = PP[(s + 1) & 1];
+                const int pn = xp(lane, s + 1), qn = xq(lane, s + 1);
+                // pairs of round s holding pn and qn, and their parameters (registers of lanes k, l)
+                const int k = xpos(pn, s), l = xpos(qn, s);
+                const int kk = k < l ? k : l, ll = k < l ? l : k;
+                const R tk_ = __shfl_sync(0xffffffffu, ct, k), tl_ = __shfl_sync(0xffffffffu, ct, l);
+                const R sk_ = __shfl_sync(0xffffffffu, cs, kk), uk_ = __shfl_sync(0xffffffffu, cu, kk);
+                const R sl_ = __shfl_sync(0xffffffffu, cs, ll), ul_ = __shfl_sync(0xffffffffu, cu, ll);
+                // D(pn, pn) and D(qn, qn) after round s (diagonal formula of their pairs)
+                const int pk = xp(k, s), qk = xq(k, s), pl = xp(l, s), ql = xq(l, s);
+                const R apq_k = Dc[didx<R, true>(pk, qk)], apq_l = Dc[didx<R, true>(pl, ql)];
+                const R app = pn == pk ? fmaR(-tk_, apq_k, Dc[pk + pk * LD]) : fmaR(tk_, apq_k, Dc[qk + qk * LD]);
+                const R aqq = qn == pl ? fmaR(-tl_, apq_l, Dc[pl + pl * LD]) : fmaR(tl_, apq_l, Dc[ql + ql * LD]);
+                // D(pn, qn) after round s: entry of the canonical tile (kk, ll), as the update warps compute it
+                const int pkk = xp(kk, s), qkk = xq(kk, s), pll = xp(ll, s), qll = xq(ll, s);
+                R x11 = Dc[didx<R, true>(pkk, pll)], x21 = Dc[didx<R, true>(qkk, pll)];
+                R x12 = Dc[didx<R, true>(pkk, qll)], x22 = Dc[didx<R, true>(qkk, qll)];
+                if (xkey(kk, s) < xkey(ll, s)) {
+                    rot<R>(sk_, uk_, x11, x21); rot<R>(sk_, uk_, x12, x22);
+                    rot<R>(sl_, ul_, x11, x12); rot<R>(sl_, ul_, x21, x22);
+                } else {
+                    rot<R>(sl_, ul_, x11, x12); rot<R>(sl_, ul_, x21, x22);
+                    rot<R>(sk_, uk_, x11, x21); rot<R>(sk_, uk_, x12, x22);
+                }
+                // rows of the tile belong to pair kk, columns to ll
+                const int rn = k < l ? pn : qn, cn = k < l ? qn : pn;
+                const R apq = (rn == pkk) ? (cn == pll ? x11 : x12) : (cn == pll ? x21 : x22);
+                R t, sk, uk;
+                const int did = rot_params<R>(app, aqq, apq, nu, rule, t, sk, uk);
+                MPJ_K3_TRACE(0, s);
+                cnt += did;
+                N.t[lane] = t; N.s[lane] = sk; N.u[lane] = uk;
+                ct = t; cs = sk; cu = uk;
+            }
+        } else if (warp == 0) {
             if (s + 1 < nrounds) {
                 WideParams<R> &N = PP[(s + 1) & 1];
                 int a, c;
@@ -361,19 +407,31 @@ __device__ __forceinline__ R *smem_rounds_wide(R *D0, R *D1, R *U, int2 bp, bool
             // static work of this thread (computed before the loop): tile (tk, tl)
             // (tl < 0: diagonal tile tk; tk < 0: none) and U items (ur[j], uk[j])
             if (tk >= 0) {
-                if (tl >= 0) {
+                if (tl >= 0 && UREG) {
+                    // cross round: arithmetic pairs, upper triangle only (mirrored at the end)
+                    const int pk = xp(tk, s), qk = xq(tk, s), pl = xp(tl, s), ql = xq(tl, s);
+                    const R sk = P.s[tk], uk = P.u[tk], sl = P.s[tl], ul = P.u[tl];
+                    R x11 = Dc[didx<R, true>(pk, pl)], x21 = Dc[didx<R, true>(qk, pl)];
+                    R x12 = Dc[didx<R, true>(pk, ql)], x22 = Dc[didx<R, true>(qk, ql)];
+                    if (xkey(tk, s) < xkey(tl, s)) {
+                        rot<R>(sk, uk, x11, x21); rot<R>(sk, uk, x12, x22);
+                        rot<R>(sl, ul, x11, x12); rot<R>(sl, ul, x21, x22);
+                    } else {
+                        rot<R>(sl, ul, x11, x12); rot<R>(sl, ul, x21, x22);
+                        rot<R>(sk, uk, x11, x21); rot<R>(sk, uk, x12, x22);
+                    }
+                    Dn[didx<R, true>(pk, pl)] = x11; Dn[didx<R, true>(qk, pl)] = x21;
+                    Dn[didx<R, true>(pk, ql)] = x12; Dn[didx<R, true>(qk, ql)] = x22;
+                } else if (tl >= 0) {
                     R x11, x21, x12, x22;
                     tile_after<R, UREG>(Dc, P, tk, tl, x11, x21, x12, x22);
                     const int pk = P.p[tk], qk = P.q[tk], pl = P.p[tl], ql = P.q[tl];
-                    if (UREG) {   // cross rounds keep the upper triangle only (mirrored at the end)
-                        Dn[didx<R, true>(pk, pl)] = x11; Dn[didx<R, true>(qk, pl)] = x21;
-                        Dn[didx<R, true>(pk, ql)] = x12; Dn[didx<R, true>(qk, ql)] = x22;
-                    } else {
+                    {
                         Dn[pk + pl * LD] = x11; Dn[qk + pl * LD] = x21; Dn[pk + ql * LD] = x12; Dn[qk + ql * LD] = x22;
                         Dn[pl + pk * LD] = x11; Dn[pl + qk * LD] = x21; Dn[ql + pk * LD] = x12; Dn[ql + qk * LD] = x22;
                     }
                 } else {
-                    const int pk = P.p[tk], qk = P.q[tk];
+                    const int pk = UREG ? xp(tk, s) : P.p[tk], qk = UREG ? xq(tk, s) : P.q[tk];
                     const R apq = Dc[didx<R, UREG>(pk, qk)], t = P.t[tk];
                     Dn[pk + pk * LD] = fmaR(-t, apq, Dc[pk + pk * LD]);
                     Dn[qk + qk * LD] = fmaR(t, apq, Dc[qk + qk * LD]);
