@@ -256,20 +256,21 @@ def run_batched(args):
     torch.cuda.synchronize()
     l0 = mpj.launch_count()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    steps = max(args.steps, 20)   # one step is ~15 ms: time enough of them for a stable number
     with ClockSampler(0) as clk:
         e0.record()
-        for _ in range(args.steps):
+        for _ in range(steps):
             res = mpj.eig_batched(A)
         e1.record()
         torch.cuda.synchronize()
-    ms = e0.elapsed_time(e1) / args.steps
+    ms = e0.elapsed_time(e1) / steps
     lam = res.lam
     V = res.V
     Ac = A
     R = torch.linalg.norm(Ac @ V - V * lam[:, None, :], dim=(1, 2)) / torch.linalg.norm(Ac, dim=(1, 2))
     O = torch.linalg.norm(V.transpose(1, 2) @ V - torch.eye(n, device=A.device, dtype=A.dtype), dim=(1, 2))
     line = {"metric": "batched EVD matrices/s (4096 x n=64)", "value": batch / (ms * 1e-3), "unit": "matrices/s",
-            "n_gpus": 1, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+            "n_gpus": 1, "steps": steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
             "dtype": "f64", "data": "synthetic",
             "config": {"workload": f"{batch} x Example 1 n=64 modes 3/4/5 kappa=1e3 (BASELINE config 3)"},
             "sweeps_mean": float(res.sweeps.float().mean()), "sweeps_low_mean": float(res.sweeps_low.float().mean()),
