@@ -294,6 +294,133 @@ __device__ __forceinline__ void apply_item_f64(const ApplyArgs &p, int item, dou
     if constexpr (V2) acc2.each2([&](int i, int j, double v0, double v1) { put(i + TW, j, v0, v1); });
 }
 
+// ---------------------------------------------------------------------------
+// fp64 apply with two buffers per CTA (3 CTAs / 24 warps per SM): a T tile's
+// U_a is needed only by Y = U_a^T X and U_c only by W = Y U_c, so they share
+// one buffer -- after the barrier that starts chunk c+1 of the first product,
+// U_a's rows of chunk c are dead and U_c's rows of chunk c stream into them.
+// X / Y share the other buffer.  V tiles: X columns and U_c rows in four
+// chunks.  Results go from the accumulators to global memory.  The three
+// CTAs of an SM start at different thirds of their item lists.
+// ---------------------------------------------------------------------------
+template <bool SKIP>
+__device__ __forceinline__ void apply_x3_body(const ApplyArgs &p, unsigned char *smem_raw)
+{
+    constexpr int LD = Lay<double>::LD, EPC = 2, CPC = TW / EPC;
+    constexpr bool skips = SKIP;
+    double *xb = (double *)smem_raw, *ub = xb + TW * LD;
+    const int mb = p.S.nb >> 1;
+    const int total = p.ntT + p.ntV;
+    const int2 *bsr = p.S.bsched + p.Rb * mb;
+    const double *Ub = (const double *)p.Ubuf;
+    const int tid = threadIdx.x;
+    const int G = gridDim.x;
+    const int K = (int)blockIdx.x < total ? (total - 1 - (int)blockIdx.x) / G + 1 : 0;
+    const int phase = (int)(3 * (int64_t)blockIdx.x / G);      // 0, 1, 2: the CTAs of an SM
+    const int k0 = (phase * K) / 3;
+    for (int kk = 0; kk < K; ++kk) {
+        int k = kk + k0;
+        if (k >= K) k -= K;
+        const int item = (int)blockIdx.x + k * G;
+        if (skips && item_identity(p, item, mb)) continue;
+        Acc<double> acc;
+        if (item < p.ntT) {
+            int a, c;
+            decode_upper(item, a, c);
+            const int2 pa = bsr[a], pc = bsr[c];
+            const bool ia = block_identity(p, a, skips), ic = block_identity(p, c, skips);
+            const double *T = (const double *)p.T;
+            const double *Uag = Ub + (size_t)a * TW * TW, *Ucg = Ub + (size_t)c * TW * TW;
+            if (!ia && !ic) {
+                for (int ch = 0; ch < 4; ++ch) {                 // X and U_a rows, 4 groups
+                    for (int e = tid; e < TW * 8; e += NT) {
+                        const int lj = e >> 3, li = 16 * ch + 2 * (e & 7);
+                        cp16(xb + li + lj * LD, T + gidx(pa, li) + (int64_t)gidx(pc, lj) * p.ldt, 16);
+                        cp16(ub + li + lj * LD, Uag + li + lj * TW, 16);
+                    }
+                    cp_commit();
+                }
+                // Y = U_a^T X; after chunk c's barrier, U_c rows of chunk c-1 replace U_a's
+                tile_mm_chunked<true>(ub, xb, acc, [&](int ch) {
+                    cp_wait_le(ch == 0 ? 3 : 2);
+                    __syncthreads();
+                    if (ch > 0) {
+                        for (int e = tid; e < TW * 8; e += NT) {
+                            const int lj = e >> 3, li = 16 * (ch - 1) + 2 * (e & 7);
+                            cp16(ub + li + lj * LD, Ucg + li + lj * TW, 16);
+                        }
+                        cp_commit();
+                    }
+                });
+                __syncthreads();                                  // GEMM 1 done: X and U_a chunk 3 free
+                for (int e = tid; e < TW * 8; e += NT) {
+                    const int lj = e >> 3, li = 48 + 2 * (e & 7);
+                    cp16(ub + li + lj * LD, Ucg + li + lj * TW, 16);
+                }
+                cp_commit();
+                acc.each([&](int i, int j, double v) { xb[i + j * LD] = v; });   // Y
+                // W = Y U_c, chunk c of U_c is group (3 - c) from the end
+                tile_mm_chunked<false>(xb, ub, acc, [&](int ch) { cp_wait_le(3 - ch); __syncthreads(); });
+            } else {
+                for (int e = tid; e < TW * CPC; e += NT) {
+                    const int lj = e / CPC, li = (e - lj * CPC) * EPC;
+                    cp16(xb + li + lj * LD, T + gidx(pa, li) + (int64_t)gidx(pc, lj) * p.ldt, 16);
+                    cp16(ub + li + lj * LD, (ia ? Ucg : Uag) + li + lj * TW, 16);
+                }
+                cp_commit();
+                cp_wait0();
+                __syncthreads();
+                if (ia) tile_mm<false>(xb, ub, acc);             // W = X Uc
+                else tile_mm<true>(ub, xb, acc);                 // W = Ua^T X
+            }
+            __syncthreads();                                     // shared memory free: store from registers
+            double *Tw = (double *)p.T;
+            acc.each2([&](int i, int j, double v0, double v1) {
+                const int64_t gi = gidx(pa, i), gj = gidx(pc, j);
+                Tw[gi + gj * p.ldt] = v0;
+                Tw[gi + (gj + 1) * p.ldt] = v1;
+                *(double2 *)(Tw + gj + gi * p.ldt) = make_double2(v0, v1);
+            });
+        } else {
+            const int idx = item - p.ntT, c = idx % mb, r0 = (idx / mb) * TW;
+            const int2 pc = bsr[c];
+            const double *M = (const double *)p.M;
+            const double *Ucg = Ub + (size_t)c * TW * TW;
+            for (int ch = 0; ch < 4; ++ch) {
+                for (int e = tid; e < 16 * CPC; e += NT) {       // X columns 16ch..
+                    const int lj = 16 * ch + e / CPC, li = (e % CPC) * EPC;
+                    const int rem = p.mrows - (r0 + li);
+                    const int bytes = rem >= EPC ? 16 : (rem > 0 ? rem * 8 : 0);
+                    cp16(xb + li + lj * LD, M + (bytes ? (int64_t)(r0 + li) : 0) + (int64_t)gidx(pc, lj) * p.ldm, bytes);
+                }
+                for (int e = tid; e < TW * 8; e += NT) {         // U_c rows 16ch..
+                    const int lj = e >> 3, li = 16 * ch + 2 * (e & 7);
+                    cp16(ub + li + lj * LD, Ucg + li + lj * TW, 16);
+                }
+                cp_commit();
+            }
+            tile_mm_chunked<false>(xb, ub, acc, [&](int ch) { cp_wait_le(3 - ch); __syncthreads(); });
+            __syncthreads();
+            double *Mw = (double *)p.M;
+            acc.each2([&](int i, int j, double v0, double v1) {
+                if (r0 + i < p.mrows) {
+                    const int64_t gj = gidx(pc, j);
+                    Mw[(int64_t)(r0 + i) + gj * p.ldm] = v0;
+                    Mw[(int64_t)(r0 + i) + (gj + 1) * p.ldm] = v1;
+                }
+            });
+        }
+    }
+    cp_wait0();
+}
+
+__global__ void __launch_bounds__(NT, 3) k_block_apply_f64x3(ApplyArgs p)
+{
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    if (p.uid && *p.nid > 0) apply_x3_body<true>(p, smem_raw);
+    else apply_x3_body<false>(p, smem_raw);
+}
+
 // SKIP: this block round has identity blocks (skip / one-product logic); the
 // kernel picks the instantiation once per CTA so that launches without
 // identities run the plain loop (the checks cost 3% per full launch).
@@ -882,6 +1009,33 @@ static void launch_apply_s(const ApplyArgs &p, cudaStream_t st)
     count_launch();
 }
 
+static int f64_apply_kind()
+{
+    static int v = -1;
+    if (v < 0) {
+        const char *e = getenv("MPJ_F64_APPLY");
+        v = (e && std::string(e) == "2cta") ? 0 : 1;
+    }
+    return v;
+}
+
+static void launch_apply_f64x3(const ApplyArgs &p, cudaStream_t st)
+{
+    const size_t smem = 2 * TW * Lay<double>::LD * sizeof(double);
+    static bool attr = false;
+    static int per_sm = 0;
+    if (!attr) {
+        MPJ_CK_VOID(cudaFuncSetAttribute(k_block_apply_f64x3, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        MPJ_CK_VOID(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_block_apply_f64x3, NT, smem));
+        per_sm = std::max(1, per_sm);
+        attr = true;
+    }
+    const int total = p.ntT + p.ntV;
+    const int grid = std::max(1, std::min(total, sm_count() * per_sm));
+    k_block_apply_f64x3<<<grid, NT, smem, st>>>(p);
+    count_launch();
+}
+
 static int fp32_apply_kind()
 {
     static int v = -1;
@@ -965,6 +1119,10 @@ static void launch_apply(const ApplyArgs &p, cudaStream_t st)
 {
     if (sizeof(R) == 4 && fp32_apply_kind() == 2 && p.mrows % 4 == 0 && launch_apply_f32ws(p, st)) return;
     if (sizeof(R) == 4 && fp32_apply_kind() >= 1) { launch_apply_f32w(p, st); return; }
+    if (sizeof(R) == 8 && p.ntT > 0 && apply_stages() == 1 && f64_apply_kind() == 1) {
+        launch_apply_f64x3(p, st);
+        return;
+    }
     if (apply_stages() == 2) { launch_apply_s<R, 2>(p, st); return; }
     // column updates only (the SVD): two buffers per CTA, 3 CTAs/SM (an
     // EVD launch split into T-only and V-only kernels gained nothing)
