@@ -1119,7 +1119,7 @@ static void launch_apply(const ApplyArgs &p, cudaStream_t st)
 {
     if (sizeof(R) == 4 && fp32_apply_kind() == 2 && p.mrows % 4 == 0 && launch_apply_f32ws(p, st)) return;
     if (sizeof(R) == 4 && fp32_apply_kind() >= 1) { launch_apply_f32w(p, st); return; }
-    if (sizeof(R) == 8 && p.ntT > 0 && apply_stages() == 1 && f64_apply_kind() == 1) {
+    if (sizeof(R) == 8 && apply_stages() == 1 && f64_apply_kind() == 1) {   // also column-only (SVD) launches
         launch_apply_f64x3(p, st);
         return;
     }
