@@ -240,6 +240,126 @@ __global__ void __launch_bounds__(NT) k_mg_apply(MgApply p)
     }
 }
 
+// fp64 apply of the partitioned sweep with two buffers per CTA (3 CTAs per
+// SM), as k_block_apply_f64x3: X / Y share one buffer, U_a and U_c the other
+// (U_c's k-chunks stream into U_a's dead rows during Y = U_a^T X); k-chunked
+// cp.async loads; results from the accumulators to global memory; the CTAs of
+// an SM start at different thirds of their item lists.
+__device__ __forceinline__ void mg_wait_le(int n)
+{
+    switch (n) {
+    case 0: asm volatile("cp.async.wait_group 0;\n" ::); break;
+    case 1: asm volatile("cp.async.wait_group 1;\n" ::); break;
+    case 2: asm volatile("cp.async.wait_group 2;\n" ::); break;
+    default: asm volatile("cp.async.wait_group 3;\n" ::); break;
+    }
+}
+
+__global__ void __launch_bounds__(NT, 3) k_mg_apply_f64x3(MgApply p)
+{
+    constexpr int LD = Lay<double>::LD, EPC = 2, CPC = TW / EPC;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    double *xb = (double *)smem_raw, *ub = xb + TW * LD;
+    const double *Ub = (const double *)p.Ubuf;
+    const int total = p.ntT + p.ntV;
+    const bool skips = p.uid && *p.nid > 0;
+    const int tid = threadIdx.x;
+    const int G = gridDim.x;
+    const int K = (int)blockIdx.x < total ? (total - 1 - (int)blockIdx.x) / G + 1 : 0;
+    const int phase = (int)(3 * (int64_t)blockIdx.x / G);
+    const int k0 = (phase * K) / 3;
+    for (int kk = 0; kk < K; ++kk) {
+        int k = kk + k0;
+        if (k >= K) k -= K;
+        const int item = (int)blockIdx.x + k * G;
+        if (skips && mg_item_identity(p, item)) continue;
+        bool ttile;
+        int cl, a, r0;
+        mg_decode(p, item, ttile, cl, a, r0);
+        const SlotInfo sc = p.slots[cl];
+        const int cg = p.slot0 + cl;
+        double *M = (double *)(ttile ? p.T : p.V);
+        const double *Ucg = Ub + (size_t)cg * TW * TW;
+        Acc<double> acc;
+        if (ttile) {
+            const int2 ra = p.gslots[a];
+            const double *Uag = Ub + (size_t)a * TW * TW;
+            const bool ia = skips && p.uid[a], ic = skips && p.uid[cg];
+            if (!ia && !ic) {
+                for (int ch = 0; ch < 4; ++ch) {                 // X and U_a rows 16ch.., 4 groups
+                    for (int e = tid; e < TW * 8; e += NT) {
+                        const int lj = e >> 3, li = 16 * ch + 2 * (e & 7);
+                        mg_cp16(xb + li + lj * LD, M + gidx(ra, li) + (int64_t)pcol(sc, lj) * p.ld, 16);
+                        mg_cp16(ub + li + lj * LD, Uag + li + lj * TW, 16);
+                    }
+                    asm volatile("cp.async.commit_group;\n" ::);
+                }
+                tile_mm_chunked<true>(ub, xb, acc, [&](int ch) {     // Y = U_a^T X
+                    mg_wait_le(ch == 0 ? 3 : 2);
+                    __syncthreads();
+                    if (ch > 0) {                                    // U_c rows of chunk ch-1
+                        for (int e = tid; e < TW * 8; e += NT) {
+                            const int lj = e >> 3, li = 16 * (ch - 1) + 2 * (e & 7);
+                            mg_cp16(ub + li + lj * LD, Ucg + li + lj * TW, 16);
+                        }
+                        asm volatile("cp.async.commit_group;\n" ::);
+                    }
+                });
+                __syncthreads();
+                for (int e = tid; e < TW * 8; e += NT) {
+                    const int lj = e >> 3, li = 48 + 2 * (e & 7);
+                    mg_cp16(ub + li + lj * LD, Ucg + li + lj * TW, 16);
+                }
+                asm volatile("cp.async.commit_group;\n" ::);
+                acc.each([&](int i, int j, double v) { xb[i + j * LD] = v; });   // Y
+                tile_mm_chunked<false>(xb, ub, acc, [&](int ch) { mg_wait_le(3 - ch); __syncthreads(); });
+            } else {
+                for (int e = tid; e < TW * CPC; e += NT) {
+                    const int lj = e / CPC, li = (e - lj * CPC) * EPC;
+                    mg_cp16(xb + li + lj * LD, M + gidx(ra, li) + (int64_t)pcol(sc, lj) * p.ld, 16);
+                    mg_cp16(ub + li + lj * LD, (ia ? Ucg : Uag) + li + lj * TW, 16);
+                }
+                asm volatile("cp.async.commit_group;\n" ::);
+                asm volatile("cp.async.wait_group 0;\n" ::);
+                __syncthreads();
+                if (ia) tile_mm<false>(xb, ub, acc);             // W = X U_c
+                else tile_mm<true>(ub, xb, acc);                 // W = U_a^T X
+            }
+            __syncthreads();
+            acc.each2([&](int i, int j, double v0, double v1) {
+                const int64_t gi = gidx(ra, i), col = (int64_t)pcol(sc, j) * p.ld;
+                M[gi + col] = v0;
+                M[gi + col + p.ld] = v1;
+            });
+        } else {
+            for (int ch = 0; ch < 4; ++ch) {
+                for (int e = tid; e < 16 * CPC; e += NT) {       // X columns 16ch..
+                    const int lj = 16 * ch + e / CPC, li = (e % CPC) * EPC;
+                    const int rem = p.vrows - (r0 + li);
+                    const int bytes = rem >= EPC ? 16 : (rem > 0 ? rem * 8 : 0);
+                    mg_cp16(xb + li + lj * LD, M + (bytes ? (int64_t)(r0 + li) : 0) + (int64_t)pcol(sc, lj) * p.ld,
+                            bytes);
+                }
+                for (int e = tid; e < TW * 8; e += NT) {         // U_c rows 16ch..
+                    const int lj = e >> 3, li = 16 * ch + 2 * (e & 7);
+                    mg_cp16(ub + li + lj * LD, Ucg + li + lj * TW, 16);
+                }
+                asm volatile("cp.async.commit_group;\n" ::);
+            }
+            tile_mm_chunked<false>(xb, ub, acc, [&](int ch) { mg_wait_le(3 - ch); __syncthreads(); });
+            __syncthreads();
+            acc.each2([&](int i, int j, double v0, double v1) {
+                if (r0 + i < p.vrows) {
+                    const int64_t col = (int64_t)pcol(sc, j) * p.ld;
+                    M[(r0 + i) + col] = v0;
+                    M[(r0 + i) + col + p.ld] = v1;
+                }
+            });
+        }
+    }
+    asm volatile("cp.async.wait_group 0;\n" ::);
+}
+
 // fp32 apply of the partitioned sweep: 128-thread CTAs with 8 x 4 FFMA tiles
 // (4 CTAs/SM; k-major operands U^T from the slot's second half).  T tiles:
 // Z = X U_c with X as stored (rows of slot a, own columns), then W = U_a^T Z
@@ -583,12 +703,16 @@ static mpj_status mg_sweep(Group &g, R **Ts, R **Vs, R nu, int rule)
     MPJ_CK(cudaStreamSynchronize(g.st));   // the host vectors above are about to die
     constexpr int LD = Lay<R>::LD;
     const size_t sm_solve = 3 * TW * LayK<R>::LD * sizeof(R), sm_apply = 3 * TW * LD * sizeof(R);
+    const size_t sm_apply64x3 = 2 * TW * Lay<double>::LD * sizeof(double);
     static bool attr[2] = {false, false};
     if (!attr[sizeof(R) == 8]) {
         MPJ_CK(cudaFuncSetAttribute(k_mg_solve<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_solve));
         MPJ_CK(cudaFuncSetAttribute(k_mg_apply<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_apply));
         if (sizeof(R) == 4)
             MPJ_CK(cudaFuncSetAttribute(k_mg_apply_f32, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_apply));
+        else
+            MPJ_CK(cudaFuncSetAttribute(k_mg_apply_f64x3, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        (int)sm_apply64x3));
         attr[sizeof(R) == 8] = true;
     }
     int *nid = g.uid + P.mb;
@@ -633,8 +757,8 @@ static mpj_status mg_sweep(Group &g, R **Ts, R **Vs, R nu, int rule)
                 const int grid = std::min(ap.ntT + ap.ntV, 4 * nsm);
                 k_mg_apply_f32<<<grid, 128, sm_apply, g.st>>>(ap);
             } else {
-                const int grid = std::min(ap.ntT + ap.ntV, 2 * nsm);
-                k_mg_apply<R><<<grid, NT, sm_apply, g.st>>>(ap);
+                const int grid = std::min(ap.ntT + ap.ntV, 3 * nsm);
+                k_mg_apply_f64x3<<<grid, NT, sm_apply64x3, g.st>>>(ap);
             }
             count_launch();
         }
