@@ -42,6 +42,7 @@ __global__ void __launch_bounds__(NTW) k_block_solve(R *__restrict__ T, int64_t 
                                                      unsigned long long *__restrict__ cnt,
                                                      int *__restrict__ uid, int *__restrict__ nid)
 {
+    asm volatile("griddepcontrol.wait;\n" ::: "memory");   // launched early (PDL): wait for K4
     constexpr int LD = LayK<R>::LD;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     R *D0 = (R *)smem_raw;          // 64 x LD, column-major (double-buffered)
@@ -417,6 +418,7 @@ __device__ __forceinline__ void apply_x3_body(const ApplyArgs &p, unsigned char 
 __global__ void __launch_bounds__(NT, 3) k_block_apply_f64x3(ApplyArgs p)
 {
     extern __shared__ __align__(16) unsigned char smem_raw[];
+    asm volatile("griddepcontrol.wait;\n" ::: "memory");   // launched early (PDL): wait for K3
     if (p.uid && *p.nid > 0) apply_x3_body<true>(p, smem_raw);
     else apply_x3_body<false>(p, smem_raw);
 }
@@ -952,6 +954,7 @@ __global__ void __launch_bounds__(WS_NT, 1) k_block_apply_f32ws(ApplyArgs p, con
                                                                 const __grid_constant__ CUtensorMap tmM)
 {
     extern __shared__ __align__(128) unsigned char smem_ws[];   // TMA boxes need 128-byte alignment
+    asm volatile("griddepcontrol.wait;\n" ::: "memory");       // launched early (PDL): wait for K3
     if (p.uid && *p.nid > 0) apply_f32ws_body<true>(p, tmT, tmM, smem_ws);
     else apply_f32ws_body<false>(p, tmT, tmM, smem_ws);
 }
@@ -1009,6 +1012,24 @@ static void launch_apply_s(const ApplyArgs &p, cudaStream_t st)
     count_launch();
 }
 
+// launch with programmatic stream serialisation: the kernel may start while
+// the previous one drains; it waits (griddepcontrol.wait) before touching data
+template <typename... KA, typename... A>
+static void launch_pdl(void (*k)(KA...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, A... args)
+{
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    MPJ_CK_VOID(cudaLaunchKernelEx(&cfg, k, args...));
+}
+
 static int f64_apply_kind()
 {
     static int v = -1;
@@ -1032,7 +1053,7 @@ static void launch_apply_f64x3(const ApplyArgs &p, cudaStream_t st)
     }
     const int total = p.ntT + p.ntV;
     const int grid = std::max(1, std::min(total, sm_count() * per_sm));
-    k_block_apply_f64x3<<<grid, NT, smem, st>>>(p);
+    launch_pdl(k_block_apply_f64x3, dim3(grid), dim3(NT), smem, st, p);
     count_launch();
 }
 
@@ -1109,7 +1130,7 @@ static bool launch_apply_f32ws(const ApplyArgs &p, cudaStream_t st)
     }
     const int total = p.ntT + p.ntV;
     const int grid = std::max(1, std::min(total, sm_count()));
-    k_block_apply_f32ws<<<grid, WS_NT, smem, st>>>(p, mT, mM);
+    launch_pdl(k_block_apply_f32ws, dim3(grid), dim3(WS_NT), smem, st, p, mT, mM);
     count_launch();
     return true;
 }
@@ -1158,7 +1179,8 @@ mpj_status block_sweep(R *T, int64_t ldt, R *V, int64_t ldv, int vrows, const De
     const bool prof = prof_on();
     for (int Rb = 0; Rb < ds.nb - 1; ++Rb) {
         if (prof) prof_mark(nsolve, st, true);
-        k_block_solve<R><<<mb, NTW, sm_solve, st>>>(T, ldt, S, Rb, nu, rule, Ubuf, cnt, uid, nid + Rb);
+        launch_pdl(k_block_solve<R>, dim3(mb), dim3(NTW), sm_solve, st, T, ldt, S, Rb, nu, rule, Ubuf, cnt, uid,
+                   nid + Rb);
         count_launch();
         if (prof) { prof_mark(nsolve, st, false); prof_mark(napply, st, true); }
         ap.Rb = Rb;
