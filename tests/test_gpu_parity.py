@@ -314,6 +314,40 @@ def test_fp32_apply_kernels_bit_identical(tmp_path, n):
     assert np.array_equal(outs["4x4"].view(np.uint32), outs["ws"].view(np.uint32))
 
 
+_FP64_APPLY_SCRIPT = r"""
+import sys, numpy as np, torch
+sys.path.insert(0, sys.argv[1])
+import paper_2211_03339_b200 as mpj, workloads as W
+n = int(sys.argv[2])
+A, _ = W.example1(n, 1e3, 4, 5151 + n)
+T = torch.from_numpy(A).cuda().T.contiguous().T
+V = torch.eye(n, dtype=torch.float64, device="cuda").T.contiguous().T
+cfg = mpj.default_config("eig", variant=mpj.VARIANT_BLOCK, block_b=32)
+mpj.jacobi(T, V, tol=0.0, max_sweeps=2, cfg=cfg)
+np.save(sys.argv[3], np.concatenate([T.cpu().numpy().ravel(), V.cpu().numpy().ravel()]))
+"""
+
+
+@pytest.mark.parametrize("n", [256, 300])
+def test_fp64_apply_kernels_bit_identical(tmp_path, n):
+    """The fp64 K4 kernels (3 CTAs/SM with two buffers, the default; 2 CTAs/SM
+    with three, MPJ_F64_APPLY=2cta) run the same k-ordered DMMA sequence per
+    output: two block sweeps give bit-identical T and V."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    script = tmp_path / "run64.py"
+    script.write_text(_FP64_APPLY_SCRIPT)
+    outs = {}
+    for kind in ("x3", "2cta"):
+        env = dict(os.environ, MPJ_F64_APPLY=kind)
+        out = tmp_path / f"{kind}.npy"
+        subprocess.run([sys.executable, str(script), root, str(n), str(out)], env=env, check=True, timeout=300)
+        outs[kind] = np.load(out)
+    assert np.array_equal(outs["x3"].view(np.uint64), outs["2cta"].view(np.uint64))
+
+
 @pytest.mark.parametrize("n", [512, 1000])
 def test_eig_block_end_to_end(mpj, orc, n):
     A, lam_true = W.example1(n, 1e3, 4, W.seed_for(2, 4, 1e3))
