@@ -199,6 +199,8 @@ __global__ void k_svd_extract(const double *__restrict__ C, int64_t ldc, int m, 
 // ---------------------------------------------------------------------------
 struct SvdPlan {
     int64_t m, n;
+    int64_t ldc;              // leading dimension of the internal m-row buffers (Ad, C, C32): m rounded up
+                              // to 8 so that every column starts 16-byte aligned (cp.async, TMA strides)
     int np, mb, splits, kc;
     double *Ad, *C, *V, *G, *Gpart, *nrm, *red_part, *red_out, *sig;
     float *C32, *V32;
@@ -219,11 +221,12 @@ static void carve_svd(char *base, size_t &off, int64_t m, int64_t n, SvdPlan &p)
         return r;
     };
     p.m = m; p.n = n;
+    p.ldc = (m + 7) / 8 * 8;
     p.np = padded_n(n, BW);
     p.mb = p.np / TW;
     p.splits = std::max(1, std::min<int>((int)((296 + p.mb - 1) / p.mb), (int)((m + TW - 1) / TW)));
     p.kc = (int)(((m + p.splits - 1) / p.splits + TW - 1) / TW * TW);
-    const size_t mnp = (size_t)m * p.np, nn = (size_t)p.np * p.np;
+    const size_t mnp = (size_t)p.ldc * p.np, nn = (size_t)p.np * p.np;
     p.Ad = (double *)take(mnp * 8);
     p.C = (double *)take(mnp * 8);
     p.V = (double *)take(nn * 8);
@@ -263,12 +266,12 @@ static mpj_status svd_block_sweep(SvdPlan &p, R *C, R *V, const DevSched &ds, R 
     MPJ_CK(cudaMemsetAsync(nid, 0, (size_t)(ds.nb - 1) * sizeof(int), st));
     for (int Rb = 0; Rb < ds.nb - 1; ++Rb) {
         if (prof) prof_mark(ng, st, true);
-        k_gram<R><<<dim3(p.mb, p.splits), NT, sm_x, st>>>(C, p.m, (int)p.m, S, Rb, p.kc, p.Gpart, p.splits);
+        k_gram<R><<<dim3(p.mb, p.splits), NT, sm_x, st>>>(C, p.ldc, (int)p.m, S, Rb, p.kc, p.Gpart, p.splits);
         if (prof) { prof_mark(ng, st, false); prof_mark(ns, st, true); }
         k_svd_solve<R><<<p.mb, NTW, sm_du, st>>>(p.Gpart, p.splits, S, Rb, nu, (R *)p.Ubuf, p.cnt, uid, nid + Rb);
         count_launch(2);
         if (prof) { prof_mark(ns, st, false); prof_mark(na, st, true); }
-        launch_block_apply_cols<R>(C, p.m, (int)p.m, ds, Rb, (const R *)p.Ubuf, st, uid, nid + Rb);
+        launch_block_apply_cols<R>(C, p.ldc, (int)p.m, ds, Rb, (const R *)p.Ubuf, st, uid, nid + Rb);
         launch_block_apply_cols<R>(V, p.np, p.np, ds, Rb, (const R *)p.Ubuf, st, uid, nid + Rb);
         if (prof) prof_mark(na, st, false);
     }
@@ -294,8 +297,8 @@ static mpj_status svd_loop(SvdPlan &p, R *C, R *V, double *Cd, const DevSched &d
     MPJ_CK(cudaMemsetAsync(p.cnt, 0, sizeof(unsigned long long), st));
     for (;;) {
         if ((void *)Cd != (void *)C)
-            launch_copy_pad<R, double>(C, p.m, (int)p.m, p.np, Cd, p.m, (int)p.m, p.np, st);
-        launch_dgemm(true, false, p.np, p.np, p.m, 1.0, Cd, p.m, Cd, p.m, 0.0, p.G, p.np, st);
+            launch_copy_pad<R, double>(C, p.ldc, (int)p.m, p.np, Cd, p.ldc, (int)p.m, p.np, st);
+        launch_dgemm(true, false, p.np, p.np, p.m, 1.0, Cd, p.ldc, Cd, p.ldc, 0.0, p.G, p.np, st);
         launch_norm<double>(p.G, p.np, p.np, p.np, true, p.red_part, p.red_out, st);
         launch_norm<double>(p.G, p.np, p.np, p.np, false, p.red_part, p.red_out + 1, st);
         MPJ_CK(cudaMemcpyAsync(h_pin, p.red_out, 2 * sizeof(double), cudaMemcpyDeviceToHost, st));
@@ -357,12 +360,13 @@ mpj_status svd_run(const double *A, int64_t m, int64_t n, int64_t lda, double *S
     ds.bsched = p.bsched; ds.lsched = p.lsched; ds.b = BW; ds.nb = hs.nb; ds.np = np; ds.rounds = hs.rounds;
 
     // a0: stage A (zero-padded columns), ||A||_F, finiteness
-    MPJ_CK(cudaMemsetAsync(p.Ad, 0, (size_t)m * np * 8, st));
-    MPJ_CK(cudaMemcpy2DAsync(p.Ad, m * 8, A, lda * 8, m * 8, n,
+    const int64_t ldc = p.ldc;
+    MPJ_CK(cudaMemsetAsync(p.Ad, 0, (size_t)ldc * np * 8, st));
+    MPJ_CK(cudaMemcpy2DAsync(p.Ad, ldc * 8, A, lda * 8, m * 8, n,
                              a_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, st));
     MPJ_CK(cudaMemsetAsync(p.flag, 0, sizeof(int), st));
-    launch_check_finite(p.Ad, m, (int)m, (int)n, p.flag, st);
-    launch_norm<double>(p.Ad, m, (int)m, np, false, p.red_part, p.red_out, st);
+    launch_check_finite(p.Ad, ldc, (int)m, (int)n, p.flag, st);
+    launch_norm<double>(p.Ad, ldc, (int)m, np, false, p.red_part, p.red_out, st);
     MPJ_CK(cudaMemcpyAsync(h_pin, p.red_out, sizeof(double), cudaMemcpyDeviceToHost, st));
     MPJ_CK(cudaMemcpyAsync(h_pin + 1, p.flag, sizeof(int), cudaMemcpyDeviceToHost, st));
     MPJ_CK(cudaStreamSynchronize(st));
@@ -381,7 +385,7 @@ mpj_status svd_run(const double *A, int64_t m, int64_t n, int64_t lda, double *S
         cudaEvent_t e0, e1;
         cudaEventCreate(&e0); cudaEventCreate(&e1);
         cudaEventRecord(e0, st);
-        launch_copy_pad<double, float>(p.Ad, m, (int)m, np, p.C32, m, (int)m, np, st);
+        launch_copy_pad<double, float>(p.Ad, ldc, (int)m, np, p.C32, ldc, (int)m, np, st);
         MPJ_CK(cudaMemsetAsync(p.V32, 0, (size_t)np * np * 4, st));
         launch_identity<float>(p.V32, np, (int)n, (int)n, st);
         SvdStage lo;
@@ -404,8 +408,8 @@ mpj_status svd_run(const double *A, int64_t m, int64_t n, int64_t lda, double *S
         cudaEventElapsedTime(&ms, e0, e1); r.t_orth = ms * 1e-3;
         // a3: C = A Q
         cudaEventRecord(e0, st);
-        MPJ_CK(cudaMemsetAsync(p.C, 0, (size_t)m * np * 8, st));
-        launch_dgemm(false, false, m, n, n, 1.0, p.Ad, m, p.V, np, 0.0, p.C, m, st);
+        MPJ_CK(cudaMemsetAsync(p.C, 0, (size_t)ldc * np * 8, st));
+        launch_dgemm(false, false, m, n, n, 1.0, p.Ad, ldc, p.V, np, 0.0, p.C, ldc, st);
         cudaEventRecord(e1, st);
         cudaEventSynchronize(e1);
         cudaEventElapsedTime(&ms, e0, e1); r.t_precond = ms * 1e-3;
@@ -430,7 +434,7 @@ mpj_status svd_run(const double *A, int64_t m, int64_t n, int64_t lda, double *S
         if (sweeps) *sweeps = hi.sweeps;
     }
     // a10: extraction
-    k_colnorm<<<(unsigned)n, 256, 0, st>>>(p.C, m, (int)m, p.nrm);
+    k_colnorm<<<(unsigned)n, 256, 0, st>>>(p.C, ldc, (int)m, p.nrm);
     MPJ_CK(cudaMemsetAsync(p.flag, 0, sizeof(int), st));
     k_rank_vec<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(p.nrm, (int)n, p.rank, p.sig, (double)n * omega * normA,
                                                             p.flag);
@@ -441,7 +445,7 @@ mpj_status svd_run(const double *A, int64_t m, int64_t n, int64_t lda, double *S
     const int64_t lduo = out_dev ? ldu : m, ldvo = out_dev ? ldv : np;
     if (out_dev) MPJ_CK(cudaMemcpyAsync(Sigma, p.sig, n * 8, cudaMemcpyDeviceToDevice, st));
     k_svd_extract<<<dim3(std::max<int64_t>(1, std::min<int64_t>(64, (m + 255) / 256)), (unsigned)n), 256, 0, st>>>(
-        p.C, m, (int)m, p.V, np, (int)n, p.rank, p.nrm, Ud, lduo, Vd, ldvo);
+        p.C, ldc, (int)m, p.V, np, (int)n, p.rank, p.nrm, Ud, lduo, Vd, ldvo);
     count_launch();
     (void)Sd;
     if (!out_dev) {

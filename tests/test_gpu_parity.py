@@ -380,7 +380,7 @@ def test_eig_batched_invalid(mpj):
 
 
 # ----------------------------------------------------------------- SVD (Alg. 5)
-@pytest.mark.parametrize("m,n,mode", [(96, 48, 3), (200, 64, 4), (300, 130, 5), (512, 256, 3)])
+@pytest.mark.parametrize("m,n,mode", [(96, 48, 3), (200, 64, 4), (300, 130, 5), (512, 256, 3), (301, 100, 4)])
 def test_svd_end_to_end(mpj, orc, m, n, mode):
     """Alg. 5 on the GPU (block one-sided Jacobi) vs the oracle's Alg. 5 (same
     ordering): sigma within 1e-13 sigma_1, residual / orthogonality at the
