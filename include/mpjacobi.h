@@ -229,9 +229,15 @@ mpj_status mpjacobi_nccl_unique_id(void *out, size_t bytes);
 /* Kernel timing (diagnostics for the bench's roofline numbers).  While
  * enabled, the library brackets each launch of its dominant kernels with CUDA
  * events ON THE STREAM IT LAUNCHES THEM ON and accumulates their durations per
- * kernel name ("block_apply_f64", "block_apply_f32", "block_solve_f64",
- * "block_solve_f32", "round_apply_f64", "round_apply_f32").  Process-wide;
- * not for concurrent calls.  get() returns 0 launches for unknown names. */
+ * kernel name: "block_apply_f64|f32", "block_solve_f64|f32" (and
+ * "block_apply_*.sweep1": the first sweep's launches alone), "round_apply_*",
+ * "svd_gram_*", "svd_solve_*", "svd_apply_*", "mg_apply_*", "mg_solve_*",
+ * "batched_evd".  Counters without a time (seconds = 0, launches = count):
+ * "block_apply_*.items" (work items), ".skipped_t" / ".skipped_v" (T / V tiles
+ * skipped because their rotation blocks are exactly I), ".half_t" (T tiles
+ * with one identity block: one product), ".identity_blocks", and the same
+ * with ".sweep1".  Process-wide; not for concurrent calls.  get() returns 0
+ * launches for unknown names. */
 void mpjacobi_profile_enable(int on);
 void mpjacobi_profile_reset(void);
 void mpjacobi_profile_get(const char *kernel, double *seconds, long long *launches);
