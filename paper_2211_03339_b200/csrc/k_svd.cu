@@ -39,6 +39,44 @@ __device__ __forceinline__ void g_cp16(void *dst, const void *src, int src_bytes
 // Only the upper triangle of G is read (k_svd_solve), so in fp64 the two warps
 // of the lower-left 32 x 32 quadrant (rows 32.., columns ..31) skip it: 3/4 of
 // the DMMA work.
+// fp32 chunk Gram: acc[u][w] = sum_k X[k + i LD] X[k + j LD] for the thread's
+// rows i = tx + 16u and columns j = ty + 16w, k ascending (the same sum order as
+// tile_mm<true>).  The chunk is column-major (rows of C contiguous), so four
+// consecutive k of one column are one 128-bit load: 8 LDS.128 per 64 FFMA
+// instead of 8 scalar LDS per 16.  A warp spans 8 row indices tx and 4 column
+// indices ty (gram_tx / gram_ty), so each load touches 8 or 4 float4 words 68
+// floats apart -- one shared-memory wavefront each (the 16 x 2 split cost ~3).
+__device__ __forceinline__ int gram_tx() { return ((threadIdx.x >> 5) & 1) * 8 + (threadIdx.x & 7); }
+__device__ __forceinline__ int gram_ty() { return (threadIdx.x >> 6) * 4 + ((threadIdx.x >> 3) & 3); }
+__device__ __forceinline__ void gram_chunk_f32(const float *X, float (&acc)[4][4])
+{
+    constexpr int LD = Lay<float>::LD;
+    const int tx = gram_tx(), ty = gram_ty();
+    #pragma unroll
+    for (int u = 0; u < 4; ++u)
+        #pragma unroll
+        for (int w = 0; w < 4; ++w) acc[u][w] = 0.f;
+    #pragma unroll 2
+    for (int kk = 0; kk < TW; kk += 4) {
+        float4 a[4], b[4];
+        #pragma unroll
+        for (int u = 0; u < 4; ++u) a[u] = *(const float4 *)(X + kk + (tx + 16 * u) * LD);
+        #pragma unroll
+        for (int w = 0; w < 4; ++w) b[w] = *(const float4 *)(X + kk + (ty + 16 * w) * LD);
+        #pragma unroll
+        for (int u = 0; u < 4; ++u)
+            #pragma unroll
+            for (int w = 0; w < 4; ++w) {
+                float s = acc[u][w];
+                s = __fmaf_rn(a[u].x, b[w].x, s);
+                s = __fmaf_rn(a[u].y, b[w].y, s);
+                s = __fmaf_rn(a[u].z, b[w].z, s);
+                s = __fmaf_rn(a[u].w, b[w].w, s);
+                acc[u][w] = s;
+            }
+    }
+}
+
 template <typename R>
 __global__ void __launch_bounds__(NT) k_gram(const R *__restrict__ C, int64_t ldc, int m, Sched S, int Rb, int kc,
                                              double *__restrict__ Gpart, int splits)
@@ -81,12 +119,12 @@ __global__ void __launch_bounds__(NT) k_gram(const R *__restrict__ C, int64_t ld
         if constexpr (sizeof(R) == 8) {
             if (!lower_left) tile_mm_acc<true>((const double *)X, (const double *)X, tot);
         } else {
-            Acc<float> part;
-            tile_mm<true>((const float *)X, (const float *)X, part);
+            float part[4][4];
+            gram_chunk_f32((const float *)X, part);
             #pragma unroll
             for (int u = 0; u < 4; ++u)
                 #pragma unroll
-                for (int w = 0; w < 4; ++w) totf[u * 4 + w] += (double)part.v[u][w];
+                for (int w = 0; w < 4; ++w) totf[u * 4 + w] += (double)part[u][w];
         }
         __syncthreads();
     }
@@ -94,7 +132,7 @@ __global__ void __launch_bounds__(NT) k_gram(const R *__restrict__ C, int64_t ld
     if constexpr (sizeof(R) == 8) {
         if (!lower_left) tot.each([&](int i, int j, double v) { G[i + j * TW] = v; });
     } else {
-        const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;   // Acc<float> mapping: rows tx+16u, cols ty+16w
+        const int tx = gram_tx(), ty = gram_ty();   // gram_chunk_f32's mapping: rows tx+16u, cols ty+16w
         #pragma unroll
         for (int u = 0; u < 4; ++u)
             #pragma unroll
@@ -201,7 +239,8 @@ struct SvdPlan {
     int64_t m, n;
     int64_t ldc;              // leading dimension of the internal m-row buffers (Ad, C, C32): m rounded up
                               // to 8 so that every column starts 16-byte aligned (cp.async, TMA strides)
-    int np, mb, splits, kc;
+    int np, mb;
+    int splits[2], kc[2];     // k_gram row splits / rows per split, [0] fp32, [1] fp64
     double *Ad, *C, *V, *G, *Gpart, *nrm, *red_part, *red_out, *sig;
     float *C32, *V32;
     int2 *bsched, *lsched;
@@ -224,8 +263,23 @@ static void carve_svd(char *base, size_t &off, int64_t m, int64_t n, SvdPlan &p)
     p.ldc = (m + 7) / 8 * 8;
     p.np = padded_n(n, BW);
     p.mb = p.np / TW;
-    p.splits = std::max(1, std::min<int>((int)((296 + p.mb - 1) / p.mb), (int)((m + TW - 1) / TW)));
-    p.kc = (int)(((m + p.splits - 1) / p.splits + TW - 1) / TW * TW);
+    // k_gram grid (mb, s): choose s <= 16 to minimise waves x (64-row chunks per
+    // CTA + 1 for the unhidden first load), with 148 SMs x the resident CTAs per
+    // SM (fp32: 2, register bound; fp64: 3, shared-memory bound).  The old
+    // s = ceil(296 / mb) put 320 fp32 CTAs in two waves, the second 24 CTAs long.
+    const int chunks = (int)((m + TW - 1) / TW);
+    for (int f = 0; f < 2; ++f) {
+        const int slots = 148 * (f ? 3 : 2);
+        int best = 1;
+        long best_cost = -1;
+        for (int s = 1; s <= std::min(16, chunks); ++s) {
+            const long waves = ((long)p.mb * s + slots - 1) / slots;
+            const long cost = waves * ((chunks + s - 1) / s + 1);
+            if (best_cost < 0 || cost < best_cost) { best_cost = cost; best = s; }
+        }
+        p.splits[f] = best;
+        p.kc[f] = (int)(((m + best - 1) / best + TW - 1) / TW * TW);
+    }
     const size_t mnp = (size_t)p.ldc * p.np, nn = (size_t)p.np * p.np;
     p.Ad = (double *)take(mnp * 8);
     p.C = (double *)take(mnp * 8);
@@ -233,7 +287,7 @@ static void carve_svd(char *base, size_t &off, int64_t m, int64_t n, SvdPlan &p)
     p.G = (double *)take(nn * 8);
     p.C32 = (float *)take(mnp * 4);
     p.V32 = (float *)take(nn * 4);
-    p.Gpart = (double *)take((size_t)p.mb * p.splits * TW * TW * 8);
+    p.Gpart = (double *)take((size_t)p.mb * std::max(p.splits[0], p.splits[1]) * TW * TW * 8);
     p.Ubuf = take((size_t)p.mb * TW * TW * 12);   // fp64 U, or fp32 U, U^T and split-half U^T
     p.nrm = (double *)take(p.np * 8);
     p.sig = (double *)take(p.np * 8);
@@ -263,12 +317,13 @@ static mpj_status svd_block_sweep(SvdPlan &p, R *C, R *V, const DevSched &ds, R 
     const char *ns = sizeof(R) == 8 ? "svd_solve_f64" : "svd_solve_f32";
     const char *na = sizeof(R) == 8 ? "svd_apply_f64" : "svd_apply_f32";
     int *uid = p.uid, *nid = p.uid + p.mb;
+    const int splits = p.splits[sizeof(R) == 8], kc = p.kc[sizeof(R) == 8];
     MPJ_CK(cudaMemsetAsync(nid, 0, (size_t)(ds.nb - 1) * sizeof(int), st));
     for (int Rb = 0; Rb < ds.nb - 1; ++Rb) {
         if (prof) prof_mark(ng, st, true);
-        k_gram<R><<<dim3(p.mb, p.splits), NT, sm_x, st>>>(C, p.ldc, (int)p.m, S, Rb, p.kc, p.Gpart, p.splits);
+        k_gram<R><<<dim3(p.mb, splits), NT, sm_x, st>>>(C, p.ldc, (int)p.m, S, Rb, kc, p.Gpart, splits);
         if (prof) { prof_mark(ng, st, false); prof_mark(ns, st, true); }
-        k_svd_solve<R><<<p.mb, NTW, sm_du, st>>>(p.Gpart, p.splits, S, Rb, nu, (R *)p.Ubuf, p.cnt, uid, nid + Rb);
+        k_svd_solve<R><<<p.mb, NTW, sm_du, st>>>(p.Gpart, splits, S, Rb, nu, (R *)p.Ubuf, p.cnt, uid, nid + Rb);
         count_launch(2);
         if (prof) { prof_mark(ns, st, false); prof_mark(na, st, true); }
         launch_block_apply_cols<R>(C, p.ldc, (int)p.m, ds, Rb, (const R *)p.Ubuf, st, uid, nid + Rb);
