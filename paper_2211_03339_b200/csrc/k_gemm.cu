@@ -90,8 +90,9 @@ __global__ void __launch_bounds__(128) k_dgemm(int64_t m, int64_t n, int64_t k, 
                                                const double *__restrict__ A, int64_t lda,
                                                const double *__restrict__ B, int64_t ldb, double beta,
                                                double *__restrict__ C, int64_t ldc, int kchunk,
-                                               double *__restrict__ partial)
+                                               double *__restrict__ partial, int upper_only)
 {
+    if (upper_only && (int64_t)blockIdx.x * BM >= ((int64_t)blockIdx.y + 1) * BN) return;   // strictly lower tile
     __shared__ __align__(16) double sA[2][TILE];
     __shared__ __align__(16) double sB[2][TILE];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -183,7 +184,7 @@ __global__ void k_splitk_reduce(int64_t m, int64_t n, int splits, const double *
 
 void launch_dgemm(bool ta, bool tb, int64_t m, int64_t n, int64_t k, double alpha, const double *A,
                   int64_t lda, const double *B, int64_t ldb, double beta, double *C, int64_t ldc,
-                  cudaStream_t st, double *scratch, size_t scratch_elems)
+                  cudaStream_t st, double *scratch, size_t scratch_elems, bool upper_only)
 {
     if (m <= 0 || n <= 0) return;
     const int64_t gm = (m + BM - 1) / BM, gn = (n + BN - 1) / BN;
@@ -197,7 +198,8 @@ void launch_dgemm(bool ta, bool tb, int64_t m, int64_t n, int64_t k, double alph
     if (kchunk <= 0) kchunk = BK;
     dim3 grd((unsigned)gm, (unsigned)gn, (unsigned)splits);
     double *part = splits > 1 ? scratch : nullptr;
-#define GO(a, b) k_dgemm<a, b><<<grd, 128, 0, st>>>(m, n, k, alpha, A, lda, B, ldb, beta, C, ldc, kchunk, part)
+#define GO(a, b) k_dgemm<a, b><<<grd, 128, 0, st>>>(m, n, k, alpha, A, lda, B, ldb, beta, C, ldc, kchunk, part, \
+                                                   upper_only ? 1 : 0)
     if (!ta && !tb) GO(false, false);
     else if (ta && !tb) GO(true, false);
     else if (!ta && tb) GO(false, true);

@@ -353,9 +353,11 @@ static mpj_status svd_loop(SvdPlan &p, R *C, R *V, double *Cd, const DevSched &d
     for (;;) {
         if ((void *)Cd != (void *)C)
             launch_copy_pad<R, double>(C, p.ldc, (int)p.m, p.np, Cd, p.ldc, (int)p.m, p.np, st);
-        launch_dgemm(true, false, p.np, p.np, p.m, 1.0, Cd, p.ldc, Cd, p.ldc, 0.0, p.G, p.np, st);
-        launch_norm<double>(p.G, p.np, p.np, p.np, true, p.red_part, p.red_out, st);
-        launch_norm<double>(p.G, p.np, p.np, p.np, false, p.red_part, p.red_out + 1, st);
+        // C^T C is symmetric: only its upper tiles are formed and read (half the flops)
+        launch_dgemm(true, false, p.np, p.np, p.m, 1.0, Cd, p.ldc, Cd, p.ldc, 0.0, p.G, p.np, st, nullptr, 0,
+                     true);
+        launch_norm_sym_upper(p.G, p.np, p.np, true, p.red_part, p.red_out, st);
+        launch_norm_sym_upper(p.G, p.np, p.np, false, p.red_part, p.red_out + 1, st);
         MPJ_CK(cudaMemcpyAsync(h_pin, p.red_out, 2 * sizeof(double), cudaMemcpyDeviceToHost, st));
         MPJ_CK(cudaStreamSynchronize(st));
         const double off = h_pin[0], tot = h_pin[1];

@@ -43,6 +43,33 @@ void launch_norm(const R *T, int64_t ld, int m, int n, bool offdiag, double *par
     count_launch(2);
 }
 template void launch_norm<double>(const double *, int64_t, int, int, bool, double *, double *, cudaStream_t);
+
+// sum over i <= j of w_ij T_ij^2 with w = 2 above the diagonal, 1 on it (0 if
+// offdiag): the full sums of launch_norm for a symmetric T, lower half unread
+__global__ void __launch_bounds__(256) k_norm_sym_upper(const double *__restrict__ T, int64_t ld, int n,
+                                                        int offdiag, double *__restrict__ part)
+{
+    __shared__ double sh[32];
+    double acc = 0.0;
+    const int64_t total = (int64_t)n * n;
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total;
+         e += (int64_t)gridDim.x * blockDim.x) {
+        const int j = (int)(e / n), i = (int)(e - (int64_t)j * n);
+        if (i > j || (offdiag && i == j)) continue;
+        const double x = T[i + j * ld];
+        acc = __fma_rn(i < j ? 2.0 * x : x, x, acc);
+    }
+    const double s = block_sum<256>(acc, sh);
+    if (threadIdx.x == 0) part[blockIdx.x] = s;
+}
+
+void launch_norm_sym_upper(const double *T, int64_t ld, int n, bool offdiag, double *partial, double *out,
+                           cudaStream_t st)
+{
+    k_norm_sym_upper<<<kRedBlocks, 256, 0, st>>>(T, ld, n, offdiag ? 1 : 0, partial);
+    k_norm_final<<<1, 256, 0, st>>>(partial, kRedBlocks, out);
+    count_launch(2);
+}
 template void launch_norm<float>(const float *, int64_t, int, int, bool, double *, double *, cudaStream_t);
 
 template <typename Rs, typename Rd>

@@ -81,6 +81,10 @@ constexpr int kRedBlocks = 296;
 template <typename R>
 void launch_norm(const R *T, int64_t ld, int m, int n, bool offdiag, double *partial,
                  double *out, cudaStream_t st);
+// the same two norms of a symmetric n x n matrix read from its upper triangle
+// only (strict upper entries counted twice); the lower triangle is not read.
+void launch_norm_sym_upper(const double *T, int64_t ld, int n, bool offdiag, double *partial,
+                           double *out, cudaStream_t st);
 // copy an m x n block between leading dimensions, zero-filling dst rows/cols
 // beyond (m, n) up to (mp, np_)
 template <typename Rs, typename Rd>
@@ -105,7 +109,9 @@ void launch_extract_evd(const double *T, int64_t ldt, const double *V, int64_t l
 void launch_dgemm(bool ta, bool tb, int64_t m, int64_t n, int64_t k, double alpha,
                   const double *A, int64_t lda, const double *B, int64_t ldb, double beta,
                   double *C, int64_t ldc, cudaStream_t st, double *scratch = nullptr,
-                  size_t scratch_elems = 0);
+                  size_t scratch_elems = 0, bool upper_only = false);
+// upper_only: only the 64 x 64 tiles of C that meet its upper triangle are
+// computed (a symmetric product such as C^T C); the rest of C is left as is.
 // split-K scratch the library reserves for tall-skinny products (doubles)
 size_t dgemm_scratch_elems(int64_t m, int64_t n);
 
