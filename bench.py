@@ -344,7 +344,7 @@ def run_svd(args):
     ms = e0.elapsed_time(e1) / args.steps
     rep = res.report
     kern = {}
-    for name in ("svd_gram_f64", "svd_gram_f32", "svd_solve_f64", "svd_solve_f32", "svd_apply_f64",
+    for name in ("svd_gram_exact", "svd_gram_f64", "svd_gram_f32", "svd_solve_f64", "svd_solve_f32", "svd_apply_f64",
                  "svd_apply_f32"):
         sec, cnt = mpj.profile_get(name)
         if cnt:

@@ -385,10 +385,12 @@ def test_svd_end_to_end(mpj, orc, m, n, mode):
     """Alg. 5 on the GPU (block one-sided Jacobi) vs the oracle's Alg. 5 (same
     ordering): sigma within 1e-13 sigma_1, residual / orthogonality at the
     north_star tolerances.  Sweeps (reading R21): with nu = omega the
-    rotate test |c_p^T c_q| > omega ||c_p|| ||c_q|| is decided at the rounding
-    noise of an fp64 Gram entry, so the GPU (fp64 DMMA Gram blocks) performs
-    spurious noise-level rotations that the long-double oracle does not and
-    reaches the 2e-4 early stop later: never earlier, at most 5 sweeps later."""
+    rotate test |c_p^T c_q| > omega ||c_p|| ||c_q|| sits at the rounding noise
+    of a plain fp64 dot product, so the GPU's fp64 stage forms its Gram blocks
+    noise-free (k_gram_exact: exact fixed-point leading product), as the
+    long-double oracle does.  The two runs still start from different fp32
+    stages (fp32 rounding order) and stop at the 2e-4 early-stop cliff, so the
+    counts may differ by one (plain DMMA Gram blocks: up to three more)."""
     A, sig_true = W.example3(m, n, 1e3, mode, W.seed_for(5, mode, 1e3))
     res = mpj.svd(dev(A))
     ref = orc.mp_svd(A, orc.default_cfg("svd", b=32))
@@ -398,7 +400,25 @@ def test_svd_end_to_end(mpj, orc, m, n, mode):
     assert np.linalg.norm(A @ V - U * sig) / np.linalg.norm(A) <= n * 1e-15
     assert np.linalg.norm(U.T @ U - np.eye(n)) <= n * 1e-15
     assert np.linalg.norm(V.T @ V - np.eye(n)) <= n * 1e-15
-    assert ref.report.sweeps <= res.sweeps <= ref.report.sweeps + 5, (res.sweeps, ref.report.sweeps)
+    assert abs(res.sweeps - ref.report.sweeps) <= 1, (res.sweeps, ref.report.sweeps)
+
+
+@pytest.mark.parametrize("m,n,mode", [(96, 48, 3), (512, 256, 3), (1024, 512, 3)])
+def test_svd_noise_free_gram(mpj, m, n, mode, monkeypatch):
+    """Reading R21: the noise-free Gram blocks (default) against the plain DMMA
+    ones (MPJ_SVD_GRAM=dmma, A/B switch): same singular values to 1e-14 sigma_1
+    and never more sweeps -- the plain blocks' extra sweeps are noise-level
+    rotations -- and the bounded policy (plain blocks while a sweep rotated
+    >= 10% of the pairs) converges to the same sigma."""
+    A, _ = W.example3(m, n, 1e3, mode, W.seed_for(5, mode, 1e3))
+    out = {}
+    for g in ("", "dmma", "0.1"):
+        monkeypatch.setenv("MPJ_SVD_GRAM", g)
+        out[g] = mpj.svd(dev(A))
+    s0 = host(out[""].sigma)
+    for g in ("dmma", "0.1"):
+        assert np.max(np.abs(host(out[g].sigma) - s0)) <= 1e-14 * s0[0]
+    assert out[""].sweeps <= out["dmma"].sweeps, (out[""].sweeps, out["dmma"].sweeps)
 
 
 def test_svd_host_buffers_and_errors(mpj):
