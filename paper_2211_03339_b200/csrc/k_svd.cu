@@ -43,22 +43,34 @@ __device__ __forceinline__ void g_cp16(void *dst, const void *src, int src_bytes
 // of the lower-left 32 x 32 quadrant (rows 32.., columns ..31) skip it: 3/4 of
 // the DMMA work.
 // fp32 chunk Gram: acc[u][w] = sum_k X[k + i LD] X[k + j LD] for the thread's
-// rows i = tx + 16u and columns j = ty + 16w, k ascending (the same sum order as
-// tile_mm<true>).  The chunk is column-major (rows of C contiguous), so four
-// consecutive k of one column are one 128-bit load: 8 LDS.128 per 64 FFMA
-// instead of 8 scalar LDS per 16.  A warp spans 8 row indices tx and 4 column
-// indices ty (gram_tx / gram_ty), so each load touches 8 or 4 float4 words 68
-// floats apart -- one shared-memory wavefront each (the 16 x 2 split cost ~3).
+// rows i = tx + 16u and columns j = ty + 16w, as two interleaved partial sums
+// (even k, odd k; each k ascending) added at the end of the chunk.  The chunk is
+// column-major (rows of C contiguous), so four consecutive k of one column are
+// one 128-bit load, and the (even, odd) pairs of two such loads are adjacent
+// register pairs: one packed fma.rn.f32x2 per two products (8 LDS.128 per 32
+// FFMA2).  A warp spans 8 row indices tx and 4 column indices ty (gram_tx /
+// gram_ty), so each load touches 8 or 4 float4 words 68 floats apart -- one
+// shared-memory wavefront each (the 16 x 2 split cost ~3).
 __device__ __forceinline__ int gram_tx() { return ((threadIdx.x >> 5) & 1) * 8 + (threadIdx.x & 7); }
 __device__ __forceinline__ int gram_ty() { return (threadIdx.x >> 6) * 4 + ((threadIdx.x >> 3) & 3); }
+__device__ __forceinline__ void ffma2v(float a0, float a1, float b0, float b1, float &c0, float &c1)
+{
+    unsigned long long aa, bb, cc, r;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(aa) : "f"(a0), "f"(a1));
+    asm("mov.b64 %0, {%1, %2};" : "=l"(bb) : "f"(b0), "f"(b1));
+    asm("mov.b64 %0, {%1, %2};" : "=l"(cc) : "f"(c0), "f"(c1));
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(aa), "l"(bb), "l"(cc));
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(c0), "=f"(c1) : "l"(r));
+}
 __device__ __forceinline__ void gram_chunk_f32(const float *X, float (&acc)[4][4])
 {
     constexpr int LD = Lay<float>::LD;
     const int tx = gram_tx(), ty = gram_ty();
+    float se[4][4], so[4][4];
     #pragma unroll
     for (int u = 0; u < 4; ++u)
         #pragma unroll
-        for (int w = 0; w < 4; ++w) acc[u][w] = 0.f;
+        for (int w = 0; w < 4; ++w) se[u][w] = so[u][w] = 0.f;
     #pragma unroll 2
     for (int kk = 0; kk < TW; kk += 4) {
         float4 a[4], b[4];
@@ -70,14 +82,14 @@ __device__ __forceinline__ void gram_chunk_f32(const float *X, float (&acc)[4][4
         for (int u = 0; u < 4; ++u)
             #pragma unroll
             for (int w = 0; w < 4; ++w) {
-                float s = acc[u][w];
-                s = __fmaf_rn(a[u].x, b[w].x, s);
-                s = __fmaf_rn(a[u].y, b[w].y, s);
-                s = __fmaf_rn(a[u].z, b[w].z, s);
-                s = __fmaf_rn(a[u].w, b[w].w, s);
-                acc[u][w] = s;
+                ffma2v(a[u].x, a[u].y, b[w].x, b[w].y, se[u][w], so[u][w]);
+                ffma2v(a[u].z, a[u].w, b[w].z, b[w].w, se[u][w], so[u][w]);
             }
     }
+    #pragma unroll
+    for (int u = 0; u < 4; ++u)
+        #pragma unroll
+        for (int w = 0; w < 4; ++w) acc[u][w] = se[u][w] + so[u][w];
 }
 
 template <typename R>
