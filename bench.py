@@ -232,7 +232,10 @@ def run_reference(args):
         "impl": "reference", "metric": "fp64 EVD seconds (n=8192)", "value": v, "unit": "s",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": v * 1e3,
         "higher_is_better": False, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic", "config": {"workload": f"Example 1 mode {args.mode}, kappa={args.kappa:g}, n={args.n}"},
+        "data": "synthetic",
+        "config": {"workload": f"Example 1 (P:681) mode {args.mode} graded spectrum, kappa={args.kappa:g}, "
+                               f"n={args.n}, one EVD per step", "n": args.n, "mode": args.mode, "kappa": args.kappa,
+                   "parallelism": "host cores (oracle)"},
         "cpu_baseline": info,
         "e2e": {"value": v, "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
