@@ -162,7 +162,8 @@ __global__ void __launch_bounds__(NT) k_gram(const R *__restrict__ C, int64_t ld
 // blocks from a per-column fixed-point split whose leading product the DMMA
 // pipe sums exactly:
 //   c_ij = 2^(e_j - k) (h_ij + r_ij),  h integer, |h| <= 2^k, |r| <= 1/2 exact,
-// with 2^e_j > max_i |c_ij| (k_colexp) and k = (53 - log2 kc) / 2 for kc rows
+// with 2^e_j > max_i |c_ij| (k_colexp before a sweep's first round, then the
+// bound k_svd_solve derives from each round's U) and k = (53 - log2 kc) / 2 for kc rows
 // per split (k = 21 at kc = 2048).  Then
 //   G_pq = 2^(e_p + e_q - 2k) (H^T H + M + M^T),  M = (H + R/2)^T R
 // (M + M^T = H^T R + R^T H + R^T R).  H^T H is a sum of kc integers of
@@ -297,7 +298,7 @@ template <typename R, bool EXACT = false>
 __global__ void __launch_bounds__(NTW) k_svd_solve(const double *__restrict__ Gpart, int splits, Sched S, int Rb,
                                                    R nu, R *__restrict__ Ubuf, unsigned long long *__restrict__ cnt,
                                                    int *__restrict__ uid, int *__restrict__ nid,
-                                                   const int *__restrict__ ex = nullptr, int kbits = 0)
+                                                   int *__restrict__ ex = nullptr, int kbits = 0)
 {
     constexpr int LD = LayK<R>::LD;
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -306,6 +307,7 @@ __global__ void __launch_bounds__(NTW) k_svd_solve(const double *__restrict__ Gp
     R *U = D1 + TW * LD;
     __shared__ unsigned nrot;
     __shared__ WideParams<R> P[2];
+    __shared__ double gnorm[EXACT ? TW : 1];   // ||c_k|| of the block pair's columns (EXACT)
     const int a = blockIdx.x;
     const int mb = S.nb >> 1;
     const int2 bp = S.bsched[Rb * mb + a];
@@ -322,9 +324,29 @@ __global__ void __launch_bounds__(NTW) k_svd_solve(const double *__restrict__ Gp
         }
         D0[li + lj * LD] = (R)g;
         U[li + lj * LD] = (li == lj) ? R(1) : R(0);
+        if (EXACT && li == lj) gnorm[li] = sqrt(fmax(g, 0.0));
     }
     __syncthreads();
     inner_rounds_wide<R>(D0, D1, U, bp, Rb == 0, S.lsched, nu, /*rule=*/1, P, &nrot);
+    if constexpr (EXACT) {
+        // exponents for the next round's k_gram_exact (replaces a k_colexp pass over C):
+        // max_i |c'_ij| <= ||c'_j|| <= sum_k |U_kj| ||c_k|| for c'_j = C(:, P_a) U(:, j);
+        // the 2^-20 margin covers the rounding of this sum and of the column apply.
+        // Every column sits in exactly one block pair per round, so all of ex is renewed;
+        // this CTA read its columns' ex above (before inner_rounds_wide's barriers).
+        __syncthreads();
+        const int j = threadIdx.x >> 4, part = threadIdx.x & 15;   // 16 threads per column
+        double bnd = 0.0;
+        #pragma unroll
+        for (int k = part * 4; k < part * 4 + 4; ++k) bnd += fabs((double)U[k + j * LD]) * gnorm[k];
+        #pragma unroll
+        for (int o = 8; o; o >>= 1) bnd += __shfl_xor_sync(0xffffffffu, bnd, o);
+        if (part == 0) {
+            int e = 0;
+            if (bnd > 0.0) frexp(bnd * (1.0 + 0x1p-20), &e);
+            ex[gidx(bp, j)] = e;
+        }
+    }
     R *Ua = Ubuf + (size_t)a * TW * TW;
     R *UaT = Ubuf + (size_t)mb * TW * TW + (size_t)a * TW * TW;   // U^T: operand of the fp32 apply
     for (int e = threadIdx.x; e < TW * TW; e += NTW) {
@@ -495,13 +517,15 @@ static mpj_status svd_block_sweep(SvdPlan &p, R *C, R *V, const DevSched &ds, R 
     for (int Rb = 0; Rb < ds.nb - 1; ++Rb) {
         if (exact) {
             if (prof) prof_mark("svd_gram_exact", st, true);
-            k_colexp<<<p.np, 256, 0, st>>>((const double *)C, p.ldc, (int)p.m, p.ex);
+            // column exponents: measured before the sweep's first round, then carried
+            // forward by k_svd_solve's bounds
+            if (Rb == 0) k_colexp<<<p.np, 256, 0, st>>>((const double *)C, p.ldc, (int)p.m, p.ex);
             k_gram_exact<<<dim3(p.mb, p.splits[2]), NT, sm_xx, st>>>((const double *)C, p.ldc, (int)p.m, S, Rb,
                                                                      p.kc[2], p.kbits, p.ex, p.Gpart, p.splits[2]);
             if (prof) { prof_mark("svd_gram_exact", st, false); prof_mark(ns, st, true); }
             k_svd_solve<double, true><<<p.mb, NTW, sm_du, st>>>(p.Gpart, p.splits[2], S, Rb, (double)nu,
                                                                 (double *)p.Ubuf, p.cnt, uid, nid + Rb, p.ex, p.kbits);
-            count_launch(3);
+            count_launch(Rb == 0 ? 3 : 2);
         } else {
             if (prof) prof_mark(ng, st, true);
             k_gram<R><<<dim3(p.mb, splits), NT, sm_x, st>>>(C, p.ldc, (int)p.m, S, Rb, kc, p.Gpart, splits);
