@@ -739,19 +739,28 @@ __device__ __forceinline__ void tile_op_sh(const float *A, const float *B, Acc48
     for (int u = 0; u < 4; ++u)
         #pragma unroll
         for (int w = 0; w < 8; ++w) acc.v[u][w] = 0.f;
-    float4 a = *(const float4 *)Ar, b0 = *(const float4 *)Bc, b1 = *(const float4 *)(Bc + 4);
-    #pragma unroll 4
-    for (int k = 0; k < TW; ++k) {
+    // two register sets for consecutive k (set 0: even k, set 1: odd k); each set is
+    // reloaded right after it is consumed, so no register rotation at the back edge
+    // (the single-set pipelined form cost one MOV per ~4 FFMA2)
+    auto step = [&](const float4 &a, const float4 &b0, const float4 &b1) {
         const float av[4] = {a.x, a.y, a.z, a.w}, bv[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
-        if (k + 1 < TW) {
-            a = *(const float4 *)(Ar + (k + 1) * BW);
-            b0 = *(const float4 *)(Bc + (k + 1) * BW);
-            b1 = *(const float4 *)(Bc + 4 + (k + 1) * BW);
-        }
         #pragma unroll
         for (int u = 0; u < 4; ++u)
             #pragma unroll
             for (int w = 0; w < 8; w += 2) ffma2(av[u], bv[w], bv[w + 1], acc.v[u][w], acc.v[u][w + 1]);
+    };
+    float4 a0 = *(const float4 *)Ar, p0 = *(const float4 *)Bc, q0 = *(const float4 *)(Bc + 4);
+    #pragma unroll 2
+    for (int k = 0; k < TW; k += 2) {
+        const float4 a1 = *(const float4 *)(Ar + (k + 1) * BW), p1 = *(const float4 *)(Bc + (k + 1) * BW),
+                     q1 = *(const float4 *)(Bc + 4 + (k + 1) * BW);
+        step(a0, p0, q0);
+        if (k + 2 < TW) {
+            a0 = *(const float4 *)(Ar + (k + 2) * BW);
+            p0 = *(const float4 *)(Bc + (k + 2) * BW);
+            q0 = *(const float4 *)(Bc + 4 + (k + 2) * BW);
+        }
+        step(a1, p1, q1);
     }
 }
 
@@ -791,22 +800,29 @@ __device__ __forceinline__ void tile_op_88(const float *A, const float *B, Acc88
     for (int u = 0; u < 8; ++u)
         #pragma unroll
         for (int w = 0; w < 8; ++w) acc.v[u][w] = 0.f;
-    float4 a0 = *(const float4 *)A0, a1 = *(const float4 *)A1, b0 = *(const float4 *)Bc,
-           b1 = *(const float4 *)(Bc + 4);
-    #pragma unroll 2
-    for (int k = 0; k < TW; ++k) {
-        const float av[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
-        const float bv[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
-        if (k + 1 < TW) {
-            a0 = *(const float4 *)(A0 + (k + 1) * BW);
-            a1 = *(const float4 *)(A1 + (k + 1) * BW);
-            b0 = *(const float4 *)(Bc + (k + 1) * BW);
-            b1 = *(const float4 *)(Bc + 4 + (k + 1) * BW);
-        }
+    // two register sets (even / odd k), as in tile_op_sh
+    auto step = [&](const float4 &x0, const float4 &x1, const float4 &y0, const float4 &y1) {
+        const float av[8] = {x0.x, x0.y, x0.z, x0.w, x1.x, x1.y, x1.z, x1.w};
+        const float bv[8] = {y0.x, y0.y, y0.z, y0.w, y1.x, y1.y, y1.z, y1.w};
         #pragma unroll
         for (int u = 0; u < 8; ++u)
             #pragma unroll
             for (int w = 0; w < 8; w += 2) ffma2(av[u], bv[w], bv[w + 1], acc.v[u][w], acc.v[u][w + 1]);
+    };
+    float4 a0 = *(const float4 *)A0, a1 = *(const float4 *)A1, b0 = *(const float4 *)Bc,
+           b1 = *(const float4 *)(Bc + 4);
+    #pragma unroll 1
+    for (int k = 0; k < TW; k += 2) {
+        const float4 c0 = *(const float4 *)(A0 + (k + 1) * BW), c1 = *(const float4 *)(A1 + (k + 1) * BW),
+                     d0 = *(const float4 *)(Bc + (k + 1) * BW), d1 = *(const float4 *)(Bc + 4 + (k + 1) * BW);
+        step(a0, a1, b0, b1);
+        if (k + 2 < TW) {
+            a0 = *(const float4 *)(A0 + (k + 2) * BW);
+            a1 = *(const float4 *)(A1 + (k + 2) * BW);
+            b0 = *(const float4 *)(Bc + (k + 2) * BW);
+            b1 = *(const float4 *)(Bc + 4 + (k + 2) * BW);
+        }
+        step(c0, c1, d0, d1);
     }
 }
 
