@@ -78,3 +78,32 @@ def test_theorem51_proxy_with_lapack_low_stage(orc, mode):
     _, _, Vt = scipy.linalg.svd(A.astype(np.float32), lapack_driver="gesvd")
     r = orc.mp_svd(A, Z=np.asfortranarray(Vt.T.astype(np.float32)))
     assert r.report.off0 <= 2 * n * sig[0] ** 2 * UPSILON
+
+
+def test_two_columns_one_rotation_closed_form(orc):
+    """Lemma 5.1 on m x 2 inputs: one rotation of columns (1,2)
+    makes them orthogonal, so Alg. 4 needs exactly one rotation, and
+    sigma^2 are the roots of the 2 x 2 Gram's characteristic polynomial,
+    (alpha + beta +- sqrt((alpha - beta)^2 + 4 gamma^2)) / 2 with
+    alpha = ||a_1||^2, beta = ||a_2||^2, gamma = a_1^T a_2.  V must be the
+    plane rotation [[c, s], [-s, c]] of the lemma's t (up to the column
+    order and signs the sort fixes).  A wrong sign of mu or a swapped
+    (alpha, beta) rotates the wrong way and leaves gamma != 0."""
+    rng = np.random.default_rng(20221103)
+    for m in (2, 5, 17):
+        A = rng.standard_normal((m, 2))
+        al, be, ga = A[:, 0] @ A[:, 0], A[:, 1] @ A[:, 1], A[:, 0] @ A[:, 1]
+        disc = np.sqrt((al - be) ** 2 + 4 * ga * ga)
+        sig_ref = np.sqrt(np.array([(al + be + disc) / 2, (al + be - disc) / 2]))
+        r = orc.plain_svd(A, orc.default_cfg("svd", b=1))
+        assert r.status == 0 and r.report.rotations == 1, (m, r.report.rotations)
+        assert np.allclose(r.sigma, sig_ref, rtol=64 * OMEGA, atol=0)
+        mu = (be - al) / (2 * ga)
+        t = 1 / (mu + np.sqrt(1 + mu * mu)) if mu >= 0 else 1 / (mu - np.sqrt(1 + mu * mu))
+        c = 1 / np.sqrt(1 + t * t)
+        s = t * c
+        J = np.array([[c, s], [-s, c]])
+        # columns of V are those of J up to order and sign
+        M = np.abs(J.T @ r.V)
+        assert np.allclose(np.sort(M, axis=None), [0, 0, 1, 1], atol=64 * OMEGA)
+        assert abs((A @ r.V)[:, 0] @ (A @ r.V)[:, 1]) <= 64 * OMEGA * (al + be)
