@@ -98,6 +98,7 @@ typedef struct mpj_report {
     int variant;              /* MPJ_VARIANT_SCALAR or MPJ_VARIANT_BLOCK                  */
     long long launches;       /* kernels launched by the call                             */
     double off_hist_low[64];  /* ||off(T32)||_F before fp32 sweep k (first 64)            */
+    long long rot_hist[64];   /* rotations applied in fp64 sweep k+1 (k < sweeps, first 64) */
 } mpj_report;
 
 /* ------------------------------------------------------------------------
@@ -122,6 +123,23 @@ mpj_status mpjacobi_eig(const double *A, int64_t n, int64_t lda, double *Lambda,
                         int64_t ldv, int *sweeps, void *workspace, size_t ws_bytes, void *stream,
                         const mpj_config *cfg, mpj_report *rep);
 
+/* Alg. 3 with step 1's output supplied or exported ("Compute the
+ * spectral decomposition in low precision ... A = Z Lambda Z^T"; the paper's
+ * own step 1 was a library SSYEV / cusolverDnSsyevd):
+ *   Z_in   in:  NULL -> run the low-precision stage (fp32 Jacobi, reading
+ *               R12); otherwise an n x n binary32 matrix (column-major,
+ *               ld = ldz >= n; host or device) used as Z in step 2, and the
+ *               low-precision stage is skipped (rep->sweeps_low = 0).
+ *   Z_out  out: NULL, or n x n binary32 (ld = ldz; host or device) that
+ *               receives the Z step 2 consumed (the fp32 stage's V, or Z_in).
+ * Feeding the same Z to this call and to the oracle isolates the fp64 stage:
+ * its sweep count must then be identical.  Other arguments,
+ * outputs and errors as mpjacobi_eig (MPJ_ERR_INVALID if ldz < n while Z_in or
+ * Z_out is given). */
+mpj_status mpjacobi_eig_z(const double *A, int64_t n, int64_t lda, const float *Z_in, float *Z_out, int64_t ldz,
+                          double *Lambda, double *V, int64_t ldv, int *sweeps, void *workspace, size_t ws_bytes,
+                          void *stream, const mpj_config *cfg, mpj_report *rep);
+
 /* Alg. 2 from T = A, P = I: "plain" fp64 parallel Jacobi with the
  * same kernels and ordering (the baseline of BASELINE.json config 2).  Same
  * arguments and outputs as mpjacobi_eig. */
@@ -137,7 +155,10 @@ mpj_status mpjacobi_eig_plain(const double *A, int64_t n, int64_t lda, double *L
  *   tol: the while test is ||off(T)||_F > tol (pass eps * ||A||_F).
  *   nu:  threshold of the test |t_pq| <= nu min(|t_pp|,|t_qq|).
  *   max_sweeps: cap; max_rounds >= 0 stops after that many rounds in total
- *        (round-level parity tests), -1 = no limit.
+ *        (round-level parity tests), -1 = no limit.  With the block variant
+ *        the limit must fall on a block-round boundary: block round 0 of a
+ *        sweep holds 2b-1 rounds, each later one b (reading R1); otherwise
+ *        MPJ_ERR_INVALID.
  *   The f32 variant runs the identical algorithm in binary32 (the
  *   low-precision stage, reading R12).  Only cfg->variant, cfg->block_b and
  *   cfg->stop_rule are read from cfg (may be NULL).
@@ -181,6 +202,13 @@ mpj_status mpjacobi_svd(const double *A, int64_t m, int64_t n, int64_t lda, doub
                         double *U, int64_t ldu, double *V, int64_t ldv, int *sweeps,
                         void *workspace, size_t ws_bytes, void *stream, const mpj_config *cfg,
                         mpj_report *rep);
+
+/* Alg. 5 with step 1's output (the n x n right singular vector estimate Z of
+ * the low-precision SVD) supplied (Z_in) or exported
+ * (Z_out), as mpjacobi_eig_z: binary32, n x n, ld = ldz >= n, host or device. */
+mpj_status mpjacobi_svd_z(const double *A, int64_t m, int64_t n, int64_t lda, const float *Z_in, float *Z_out,
+                          int64_t ldz, double *Sigma, double *U, int64_t ldu, double *V, int64_t ldv, int *sweeps,
+                          void *workspace, size_t ws_bytes, void *stream, const mpj_config *cfg, mpj_report *rep);
 
 /* ------------------------------------------------------------------------
  * Batched Alg. 3: `batch` independent n x n matrices, contiguous with stride

@@ -76,6 +76,7 @@ class Report(C.Structure):
         ("sweeps", C.c_int), ("sweeps_low", C.c_int), ("status", C.c_int), ("status_low", C.c_int),
         ("rotations", C.c_longlong), ("rotations_low", C.c_longlong),
         ("normA", C.c_double), ("off0", C.c_double), ("off_hist", C.c_double * 64),
+        ("rot_hist", C.c_double * 64),
     ]
 
 
@@ -120,7 +121,7 @@ def _declare(L):
         f = getattr(L, nm)
         f.restype = C.c_int
         f.argtypes = [tp, tp, C.c_int, C.c_int, C.c_int, C.c_double, C.c_double, C.c_double,
-                      C.c_int, _ip, _llp, _dp]
+                      C.c_int, _ip, _llp, _dp, _dp]
     L.orc_gram_offnorm.restype = None
     L.orc_gram_offnorm.argtypes = [_dp, C.c_int, C.c_int, _dp, _dp]
     L.orc_mp_svd.restype = C.c_int
@@ -366,9 +367,12 @@ def jacobi_svd(Cm, V=None, *, b=32, eps_rel=0.1 * OMEGA, nu=OMEGA, early_stop=2e
     m = Cm.shape[0]
     sw, rot = C.c_int(), C.c_longlong()
     hist = np.zeros(64)
+    rh = np.zeros(64)
     st = fn(_p(Cm), _p(V), m, n, b, eps_rel, nu, early_stop, max_sweeps, C.byref(sw),
-            C.byref(rot), _p(hist))
-    return JacobiResult(Cm, V, sw.value, rot.value, st, hist[: min(sw.value + 1, 64)].copy())
+            C.byref(rot), _p(hist), _p(rh))
+    res = JacobiResult(Cm, V, sw.value, rot.value, st, hist[: min(sw.value + 1, 64)].copy())
+    res.rot_hist = rh[: min(sw.value, 64)].copy()
+    return res
 
 
 def gram_offnorm(Cm):

@@ -494,6 +494,7 @@ typedef struct {
     long long rotations, rotations_low;
     double normA, off0;     /* ||A||_F and ||off(Q^T A Q)||_F                      */
     double off_hist[64];
+    double rot_hist[64];    /* svd: rotations applied in fp64 sweep k+1 (k < 64)   */
 } orc_report;
 
 #define OMEGA 1.1102230246251565e-16     /* 2^-53 */
@@ -641,7 +642,8 @@ void orc_gram_offnorm(const double *C, int m, int n, double *off, double *tot)
 #define DEFINE_ONESIDED(SUF, REAL)                                                     \
     int orc_jacobi_svd_##SUF(REAL *C, REAL *V, int m, int n, int b, double eps_rel,    \
                              double nu_d, double early_stop, int max_sweeps,           \
-                             int *sweeps_out, long long *rot_out, double *off_hist)   \
+                             int *sweeps_out, long long *rot_out, double *off_hist,   \
+                             double *rot_hist)                                         \
     {                                                                                  \
         int np = orc_padded_n(n, b), h = np / 2, nr = np - 1;                          \
         int *P = (int *)malloc(sizeof(int) * (size_t)nr * h);                          \
@@ -684,6 +686,7 @@ void orc_gram_offnorm(const double *C, int m, int n, double *off, double *tot)
                 }                                                                      \
             }                                                                          \
             rot += rs;                                                                 \
+            if (rot_hist && sweeps <= 64) rot_hist[sweeps - 1] = (double)rs;           \
             if (early_stop > 0 && N > 0 && (double)rs / N < early_stop) {              \
                 /* recompute the history entry for the final state */                  \
                 status = 0;                                                            \
@@ -745,7 +748,7 @@ int orc_mp_svd(const double *A, int m, int n, const orc_cfg *cfg, const float *Z
         int sw = 0; long long rot = 0;
         r0.status_low = orc_jacobi_svd_f32(C32, Z, m, n, cfg->b, orc_eps_low(cfg, n) * UPSILON,
                                            cfg->nu_low_factor * UPSILON, cfg->early_stop,
-                                           cfg->max_sweeps_low, &sw, &rot, NULL);
+                                           cfg->max_sweeps_low, &sw, &rot, NULL, NULL);
         r0.sweeps_low = sw; r0.rotations_low = rot;
         free(C32);
     }
@@ -761,7 +764,7 @@ int orc_mp_svd(const double *A, int m, int n, const orc_cfg *cfg, const float *Z
     r0.off0 = off;
     int sw = 0; long long rot = 0;
     st = orc_jacobi_svd_f64(C, Q, m, n, cfg->b, cfg->eps_factor * OMEGA, cfg->nu_factor * OMEGA,
-                            cfg->early_stop, cfg->max_sweeps, &sw, &rot, r0.off_hist);
+                            cfg->early_stop, cfg->max_sweeps, &sw, &rot, r0.off_hist, r0.rot_hist);
     r0.sweeps = sw; r0.rotations = rot; r0.status = st;
     int st2 = extract_svd(C, Q, m, n, r0.normA, sig, U, V);
     if (rep) *rep = r0;
@@ -785,7 +788,7 @@ int orc_plain_svd(const double *A, int m, int n, const orc_cfg *cfg, double *sig
     r0.off0 = off;
     int sw = 0; long long rot = 0;
     int st = orc_jacobi_svd_f64(C, W, m, n, cfg->b, cfg->eps_factor * OMEGA, cfg->nu_factor * OMEGA,
-                                cfg->early_stop, cfg->max_sweeps, &sw, &rot, r0.off_hist);
+                                cfg->early_stop, cfg->max_sweeps, &sw, &rot, r0.off_hist, r0.rot_hist);
     r0.sweeps = sw; r0.rotations = rot; r0.status = st;
     int st2 = extract_svd(C, W, m, n, r0.normA, sig, U, V);
     if (rep) *rep = r0;

@@ -54,10 +54,12 @@ class mpj_report(C.Structure):
         ("t_orth", C.c_double), ("t_precond", C.c_double), ("t_jacobi", C.c_double),
         ("t_extract", C.c_double), ("t_total", C.c_double), ("n_padded", C.c_int), ("block_b", C.c_int),
         ("variant", C.c_int), ("launches", C.c_longlong), ("off_hist_low", C.c_double * 64),
+        ("rot_hist", C.c_longlong * 64),
     ]
 
     def as_dict(self):
-        d = {k: getattr(self, k) for k, _ in self._fields_ if k not in ("off_hist", "off_hist_low")}
+        d = {k: getattr(self, k) for k, _ in self._fields_ if k not in ("off_hist", "off_hist_low", "rot_hist")}
+        d["rot_hist"] = list(self.rot_hist[: self.sweeps])
         d["off_hist"] = list(self.off_hist[: max(self.sweeps + 1, 1)])
         d["off_hist_low"] = list(self.off_hist_low[: max(self.sweeps_low + 1, 1)])
         return d
@@ -87,6 +89,8 @@ def lib():
         for nm in ("mpjacobi_eig", "mpjacobi_eig_plain"):
             getattr(L, nm).restype = C.c_int
             getattr(L, nm).argtypes = eig_args
+        L.mpjacobi_eig_z.restype = C.c_int
+        L.mpjacobi_eig_z.argtypes = eig_args[:3] + [_vp, _vp, _i64] + eig_args[3:]
         for nm in ("mpjacobi_jacobi_f64", "mpjacobi_jacobi_f32"):
             getattr(L, nm).restype = C.c_int
             getattr(L, nm).argtypes = [_vp, _i64, _vp, _i64, _i64, _dp, _dp, C.c_int, _i64,
@@ -106,6 +110,9 @@ def lib():
             L.mpjacobi_svd.restype = C.c_int
             L.mpjacobi_svd.argtypes = [_vp, _i64, _i64, _i64, _vp, _vp, _i64, _vp, _i64,
                                        C.POINTER(C.c_int), _vp, C.c_size_t, _vp, cfgp, repp]
+            L.mpjacobi_svd_z.restype = C.c_int
+            L.mpjacobi_svd_z.argtypes = [_vp, _i64, _i64, _i64, _vp, _vp, _i64, _vp, _vp, _i64, _vp, _i64,
+                                         C.POINTER(C.c_int), _vp, C.c_size_t, _vp, cfgp, repp]
         L.mpjacobi_eig_mg.restype = C.c_int
         L.mpjacobi_eig_mg.argtypes = [_vp, _i64, _i64, _vp, _vp, _i64, C.POINTER(C.c_int), _vp, C.c_int, C.c_int,
                                       C.c_int, _vp, cfgp, repp]
@@ -126,7 +133,7 @@ EXPORTED = (
     "mpjacobi_precond", "mpjacobi_dgemm", "mpjacobi_svd_workspace", "mpjacobi_svd",
     "mpjacobi_eig_batched", "mpjacobi_last_error", "mpjacobi_launch_count",
     "mpjacobi_profile_enable", "mpjacobi_profile_reset", "mpjacobi_profile_get",
-    "mpjacobi_eig_mg", "mpjacobi_nccl_unique_id", "mpjacobi_mg_plan",
+    "mpjacobi_eig_mg", "mpjacobi_nccl_unique_id", "mpjacobi_mg_plan", "mpjacobi_eig_z", "mpjacobi_svd_z",
 )
 
 
@@ -193,13 +200,32 @@ class EigResult:
     V: torch.Tensor
     sweeps: int
     report: mpj_report
+    Z: torch.Tensor | None = None
+
+
+def _z_args(n, Z_in, Z_out, dev):
+    """(Z_in column-major or None, Z_out tensor or None, ldz) for the *_z entry points."""
+    zi = None
+    if Z_in is not None:
+        if Z_in.shape != (n, n) or Z_in.dtype != torch.float32:
+            raise ValueError("Z_in must be an (n, n) float32 matrix")
+        zi = colmajor(Z_in)
+    zo = empty_colmajor(n, n, dtype=torch.float32, device=dev.type, pin=(dev.type == "cpu")) if Z_out else None
+    ld = zi.stride(1) if zi is not None else n
+    if zi is not None and zo is not None and ld != n:
+        zi = zi.T.contiguous().T
+        ld = n
+    return zi, zo, max(ld, n)
 
 
 def mpjacobi_eig(A, cfg: mpj_config | None = None, *, plain=False, workspace=None, out=None,
-                 allow_noconv=False) -> EigResult:
+                 allow_noconv=False, Z_in=None, Z_out=False) -> EigResult:
     """Alg. 3 (or Alg. 2 with plain=True).  A: (n, n) float64 tensor on the GPU
     or on the host (host tensors are staged by the library; pin them for async
-    copies).  Returns descending eigenvalues and column-major eigenvectors."""
+    copies).  Returns descending eigenvalues and column-major eigenvectors.
+    Z_in (n, n) float32 replaces the low-precision stage's output (step 1,
+    P:188); Z_out=True returns the Z step 2 consumed in ``.Z``
+    (mpjacobi_eig_z)."""
     n = A.shape[0]
     if A.shape != (n, n) or A.dtype != torch.float64:
         raise ValueError("A must be a square float64 matrix")
@@ -216,11 +242,19 @@ def mpjacobi_eig(A, cfg: mpj_config | None = None, *, plain=False, workspace=Non
     ws_ptr, ws_bytes = None, 0
     if workspace is not None:
         ws_ptr, ws_bytes = _ptr(workspace), workspace.numel() * workspace.element_size()
-    fn = lib().mpjacobi_eig_plain if plain else lib().mpjacobi_eig
-    st = fn(_ptr(Acm), n, Acm.stride(1), _ptr(lam), _ptr(V), V.stride(1), C.byref(sw), ws_ptr, ws_bytes,
-            _stream(), C.byref(cfg), C.byref(rep))
+    zo = None
+    if Z_in is not None or Z_out:
+        if plain:
+            raise ValueError("Z_in / Z_out apply to Alg. 3 only")
+        zi, zo, ldz = _z_args(n, Z_in, Z_out, dev)
+        st = lib().mpjacobi_eig_z(_ptr(Acm), n, Acm.stride(1), _ptr(zi), _ptr(zo), ldz, _ptr(lam), _ptr(V),
+                                  V.stride(1), C.byref(sw), ws_ptr, ws_bytes, _stream(), C.byref(cfg), C.byref(rep))
+    else:
+        fn = lib().mpjacobi_eig_plain if plain else lib().mpjacobi_eig
+        st = fn(_ptr(Acm), n, Acm.stride(1), _ptr(lam), _ptr(V), V.stride(1), C.byref(sw), ws_ptr, ws_bytes,
+                _stream(), C.byref(cfg), C.byref(rep))
     _check(st, (MPJ_OK, MPJ_ERR_NOCONV) if allow_noconv else (MPJ_OK,))
-    return EigResult(lam, V, sw.value, rep)
+    return EigResult(lam, V, sw.value, rep, zo)
 
 
 def eig_workspace(n, cfg: mpj_config | None = None, device="cuda"):
@@ -300,11 +334,13 @@ class SvdResult:
     V: torch.Tensor       # (n, n) column-major, math orientation
     sweeps: int
     report: mpj_report
+    Z: torch.Tensor | None = None
 
 
 def mpjacobi_svd(A, cfg: mpj_config | None = None, *, workspace=None, out=None,
-                 allow_noconv=False) -> SvdResult:
-    """Alg. 5: A (m, n), m >= n, float64, on the GPU or the host."""
+                 allow_noconv=False, Z_in=None, Z_out=False) -> SvdResult:
+    """Alg. 5: A (m, n), m >= n, float64, on the GPU or the host.
+    Z_in / Z_out as in eig() (step 1's n x n Z; mpjacobi_svd_z)."""
     m, n = A.shape
     if A.dtype != torch.float64 or m < n:
         raise ValueError("A must be float64 with m >= n")
@@ -323,10 +359,17 @@ def mpjacobi_svd(A, cfg: mpj_config | None = None, *, workspace=None, out=None,
     ws_ptr, ws_bytes = None, 0
     if workspace is not None:
         ws_ptr, ws_bytes = _ptr(workspace), workspace.numel() * workspace.element_size()
-    st = lib().mpjacobi_svd(_ptr(Acm), m, n, Acm.stride(1), _ptr(sig), _ptr(U), U.stride(1), _ptr(V), V.stride(1),
-                            C.byref(sw), ws_ptr, ws_bytes, _stream(), C.byref(cfg), C.byref(rep))
+    zo = None
+    if Z_in is not None or Z_out:
+        zi, zo, ldz = _z_args(n, Z_in, Z_out, dev)
+        st = lib().mpjacobi_svd_z(_ptr(Acm), m, n, Acm.stride(1), _ptr(zi), _ptr(zo), ldz, _ptr(sig), _ptr(U),
+                                  U.stride(1), _ptr(V), V.stride(1), C.byref(sw), ws_ptr, ws_bytes, _stream(),
+                                  C.byref(cfg), C.byref(rep))
+    else:
+        st = lib().mpjacobi_svd(_ptr(Acm), m, n, Acm.stride(1), _ptr(sig), _ptr(U), U.stride(1), _ptr(V),
+                                V.stride(1), C.byref(sw), ws_ptr, ws_bytes, _stream(), C.byref(cfg), C.byref(rep))
     _check(st, (MPJ_OK, MPJ_ERR_NOCONV) if allow_noconv else (MPJ_OK,))
-    return SvdResult(sig, U, V, sw.value, rep)
+    return SvdResult(sig, U, V, sw.value, rep, zo)
 
 
 def svd_workspace(m, n, cfg: mpj_config | None = None, device="cuda"):

@@ -24,6 +24,7 @@
 
 #include <algorithm>
 #include <cstdlib>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -1009,29 +1010,24 @@ static int apply_stages()
 }
 
 template <typename R, int STAGES, bool VONLY = false>
-static void launch_apply_s(const ApplyArgs &p, cudaStream_t st)
+static cudaError_t launch_apply_s(const ApplyArgs &p, cudaStream_t st)
 {
     constexpr int LD = Lay<R>::LD;
     const size_t smem = (VONLY ? 2 : 3) * STAGES * TW * LD * sizeof(R);
-    static bool attr = false;
-    static int per_sm = 0;
-    if (!attr) {
-        MPJ_CK_VOID(cudaFuncSetAttribute(k_block_apply<R, STAGES, VONLY>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)smem));
-        MPJ_CK_VOID(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_block_apply<R, STAGES, VONLY>, NT, smem));
-        per_sm = std::max(1, per_sm);
-        attr = true;
-    }
+    int per_sm = 1;
+    cudaError_t e = smem_optin((const void *)k_block_apply<R, STAGES, VONLY>, smem, NT, &per_sm);
+    if (e != cudaSuccess) return e;
     const int total = p.ntT + p.ntV;
     const int grid = std::max(1, std::min(total, sm_count() * per_sm));
     k_block_apply<R, STAGES, VONLY><<<grid, NT, smem, st>>>(p);
     count_launch();
+    return cudaGetLastError();
 }
 
 // launch with programmatic stream serialisation: the kernel may start while
 // the previous one drains; it waits (griddepcontrol.wait) before touching data
 template <typename... KA, typename... A>
-static void launch_pdl(void (*k)(KA...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, A... args)
+static cudaError_t launch_pdl(void (*k)(KA...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, A... args)
 {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = grid;
@@ -1043,7 +1039,7 @@ static void launch_pdl(void (*k)(KA...), dim3 grid, dim3 block, size_t smem, cud
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    MPJ_CK_VOID(cudaLaunchKernelEx(&cfg, k, args...));
+    return cudaLaunchKernelEx(&cfg, k, args...);
 }
 
 static int f64_apply_kind()
@@ -1056,21 +1052,16 @@ static int f64_apply_kind()
     return v;
 }
 
-static void launch_apply_f64x3(const ApplyArgs &p, cudaStream_t st)
+static cudaError_t launch_apply_f64x3(const ApplyArgs &p, cudaStream_t st)
 {
     const size_t smem = 2 * TW * Lay<double>::LD * sizeof(double);
-    static bool attr = false;
-    static int per_sm = 0;
-    if (!attr) {
-        MPJ_CK_VOID(cudaFuncSetAttribute(k_block_apply_f64x3, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        MPJ_CK_VOID(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_block_apply_f64x3, NT, smem));
-        per_sm = std::max(1, per_sm);
-        attr = true;
-    }
+    int per_sm = 1;
+    cudaError_t e = smem_optin((const void *)k_block_apply_f64x3, smem, NT, &per_sm);
+    if (e != cudaSuccess) return e;
     const int total = p.ntT + p.ntV;
     const int grid = std::max(1, std::min(total, sm_count() * per_sm));
-    launch_pdl(k_block_apply_f64x3, dim3(grid), dim3(NT), smem, st, p);
     count_launch();
+    return launch_pdl(k_block_apply_f64x3, dim3(grid), dim3(NT), smem, st, p);
 }
 
 static int fp32_apply_kind()
@@ -1083,35 +1074,30 @@ static int fp32_apply_kind()
     return v;
 }
 
-static void launch_apply_f32w(const ApplyArgs &p, cudaStream_t st)
+static cudaError_t launch_apply_f32w(const ApplyArgs &p, cudaStream_t st)
 {
     const size_t smem = 3 * TW * Lay<float>::LD * sizeof(float);
-    static bool attr = false;
-    static int per_sm = 0;
-    if (!attr) {
-        MPJ_CK_VOID(cudaFuncSetAttribute(k_block_apply_f32w, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        MPJ_CK_VOID(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_block_apply_f32w, NT128, smem));
-        per_sm = std::max(1, per_sm);
-        attr = true;
-    }
+    int per_sm = 1;
+    cudaError_t e = smem_optin((const void *)k_block_apply_f32w, smem, NT128, &per_sm);
+    if (e != cudaSuccess) return e;
     const int total = p.ntT + p.ntV;
     const int grid = std::max(1, std::min(total, sm_count() * per_sm));
     k_block_apply_f32w<<<grid, NT128, smem, st>>>(p);
     count_launch();
+    return cudaGetLastError();
 }
 
 static PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder()
 {
     static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
-    static bool tried = false;
-    if (!tried) {
-        tried = true;
+    static std::once_flag once;
+    std::call_once(once, [] {
         void *f = nullptr;
         cudaDriverEntryPointQueryResult q;
         if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) == cudaSuccess &&
             q == cudaDriverEntryPointSuccess)
             fn = (PFN_cuTensorMapEncodeTiled_v12000)f;
-    }
+    });
     return fn;
 }
 
@@ -1128,7 +1114,9 @@ static bool make_map32(CUtensorMap &m, const void *base, int64_t rows, int64_t c
                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-static bool launch_apply_f32ws(const ApplyArgs &p, cudaStream_t st)
+// false: the TMA kernel is unavailable for these operands (the caller falls
+// back to the 8x4 kernel); a launch error is returned through *err
+static bool launch_apply_f32ws(const ApplyArgs &p, cudaStream_t st, cudaError_t *err)
 {
     CUtensorMap mT, mM;
     // column updates only (SVD): no T tiles, M's map stands in for T's
@@ -1137,39 +1125,35 @@ static bool launch_apply_f32ws(const ApplyArgs &p, cudaStream_t st)
         !make_map32(mM, p.M, p.mrows, p.S.np, p.ldm))
         return false;
     const size_t smem = (size_t)WS_NS * 3 * SH_TILE * sizeof(float) + 2 * WS_NS * sizeof(uint64_t);
-    static bool attr = false;
-    if (!attr) {
-        if (cudaFuncSetAttribute(k_block_apply_f32ws, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
-            cudaSuccess)
-            return false;
-        attr = true;
+    if (smem_optin((const void *)k_block_apply_f32ws, smem, WS_NT, nullptr) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
     }
     const int total = p.ntT + p.ntV;
     const int grid = std::max(1, std::min(total, sm_count()));
-    launch_pdl(k_block_apply_f32ws, dim3(grid), dim3(WS_NT), smem, st, p, mT, mM);
+    *err = launch_pdl(k_block_apply_f32ws, dim3(grid), dim3(WS_NT), smem, st, p, mT, mM);
     count_launch();
     return true;
 }
 
 template <typename R>
-static void launch_apply(const ApplyArgs &p, cudaStream_t st)
+static cudaError_t launch_apply(const ApplyArgs &p, cudaStream_t st)
 {
-    if (sizeof(R) == 4 && fp32_apply_kind() == 2 && p.mrows % 4 == 0 && launch_apply_f32ws(p, st)) return;
-    if (sizeof(R) == 4 && fp32_apply_kind() >= 1) { launch_apply_f32w(p, st); return; }
-    if (sizeof(R) == 8 && apply_stages() == 1 && f64_apply_kind() == 1) {   // also column-only (SVD) launches
-        launch_apply_f64x3(p, st);
-        return;
-    }
-    if (apply_stages() == 2) { launch_apply_s<R, 2>(p, st); return; }
+    cudaError_t e = cudaSuccess;
+    if (sizeof(R) == 4 && fp32_apply_kind() == 2 && p.mrows % 4 == 0 && launch_apply_f32ws(p, st, &e)) return e;
+    if (sizeof(R) == 4 && fp32_apply_kind() >= 1) return launch_apply_f32w(p, st);
+    if (sizeof(R) == 8 && apply_stages() == 1 && f64_apply_kind() == 1)   // also column-only (SVD) launches
+        return launch_apply_f64x3(p, st);
+    if (apply_stages() == 2) return launch_apply_s<R, 2>(p, st);
     // column updates only (the SVD): two buffers per CTA, 3 CTAs/SM (an
     // EVD launch split into T-only and V-only kernels gained nothing)
-    if (p.ntT == 0) { launch_apply_s<R, 1, true>(p, st); return; }
-    launch_apply_s<R, 1>(p, st);
+    if (p.ntT == 0) return launch_apply_s<R, 1, true>(p, st);
+    return launch_apply_s<R, 1>(p, st);
 }
 
 template <typename R>
 mpj_status block_sweep(R *T, int64_t ldt, R *V, int64_t ldv, int vrows, const DevSched &ds, R nu, int rule,
-                       unsigned long long *cnt, void *scratch, cudaStream_t st, bool first_sweep)
+                       unsigned long long *cnt, void *scratch, cudaStream_t st, bool first_sweep, int max_brounds)
 {
     if (ds.b != BW) { set_error("block variant needs b = 32"); return MPJ_ERR_INVALID; }
     Sched S;
@@ -1180,12 +1164,7 @@ mpj_status block_sweep(R *T, int64_t ldt, R *V, int64_t ldv, int vrows, const De
     int *nid = uid + mb;                         // nb - 1 <= 2 mb block rounds
     MPJ_CK(cudaMemsetAsync(nid, 0, (size_t)(ds.nb - 1) * sizeof(int), st));
     const size_t sm_solve = 3 * TW * LayK<R>::LD * sizeof(R);
-    static bool attr_done[2] = {false, false};
-    const int ti = sizeof(R) == 8 ? 0 : 1;
-    if (!attr_done[ti]) {
-        MPJ_CK(cudaFuncSetAttribute(k_block_solve<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_solve));
-        attr_done[ti] = true;
-    }
+    MPJ_CK(smem_optin((const void *)k_block_solve<R>, sm_solve, NTW, nullptr));
     ApplyArgs ap;
     ap.T = T; ap.ldt = ldt; ap.M = V; ap.ldm = ldv; ap.mrows = vrows; ap.S = S; ap.Ubuf = Ubuf; ap.uid = uid;
     ap.ntT = mb * (mb - 1) / 2;
@@ -1193,10 +1172,11 @@ mpj_status block_sweep(R *T, int64_t ldt, R *V, int64_t ldv, int vrows, const De
     const char *nsolve = sizeof(R) == 8 ? "block_solve_f64" : "block_solve_f32";
     const char *napply = sizeof(R) == 8 ? "block_apply_f64" : "block_apply_f32";
     const bool prof = prof_on();
-    for (int Rb = 0; Rb < ds.nb - 1; ++Rb) {
+    const int nbr = max_brounds >= 0 ? std::min(max_brounds, ds.nb - 1) : ds.nb - 1;
+    for (int Rb = 0; Rb < nbr; ++Rb) {
         if (prof) prof_mark(nsolve, st, true);
-        launch_pdl(k_block_solve<R>, dim3(mb), dim3(NTW), sm_solve, st, T, ldt, S, Rb, nu, rule, Ubuf, cnt, uid,
-                   nid + Rb);
+        MPJ_CK(launch_pdl(k_block_solve<R>, dim3(mb), dim3(NTW), sm_solve, st, T, ldt, S, Rb, nu, rule, Ubuf, cnt,
+                          uid, nid + Rb));
         count_launch();
         if (prof) { prof_mark(nsolve, st, false); prof_mark(napply, st, true); }
         ap.Rb = Rb;
@@ -1205,7 +1185,7 @@ mpj_status block_sweep(R *T, int64_t ldt, R *V, int64_t ldv, int vrows, const De
         // identity blocks, so they give the full-launch efficiency
         const std::string nfirst = std::string(napply) + ".sweep1";
         if (prof && first_sweep) prof_mark(nfirst.c_str(), st, true);
-        launch_apply<R>(ap, st);
+        MPJ_CK(launch_apply<R>(ap, st));
         if (prof && first_sweep) prof_mark(nfirst.c_str(), st, false);
         if (prof) prof_mark(napply, st, false);
     }
@@ -1239,7 +1219,7 @@ mpj_status block_sweep(R *T, int64_t ldt, R *V, int64_t ldv, int vrows, const De
 // `rows` rows): the column update of the one-sided (SVD) block variant.
 // uid / nid (optional): identity flags and count of this block round (skip).
 template <typename R>
-void launch_block_apply_cols(R *M, int64_t ld, int rows, const DevSched &ds, int Rb, const R *Ubuf,
+cudaError_t launch_block_apply_cols(R *M, int64_t ld, int rows, const DevSched &ds, int Rb, const R *Ubuf,
                              cudaStream_t st, const int *uid, const int *nid)
 {
     Sched S;
@@ -1248,18 +1228,18 @@ void launch_block_apply_cols(R *M, int64_t ld, int rows, const DevSched &ds, int
     ap.T = nullptr; ap.ldt = 0; ap.M = M; ap.ldm = ld; ap.mrows = rows; ap.S = S; ap.Rb = Rb; ap.Ubuf = Ubuf; ap.uid = uid; ap.nid = nid;
     ap.ntT = 0;
     ap.ntV = ((rows + TW - 1) / TW) * (ds.nb / 2);
-    launch_apply<R>(ap, st);
+    return launch_apply<R>(ap, st);
 }
-template void launch_block_apply_cols<double>(double *, int64_t, int, const DevSched &, int, const double *,
+template cudaError_t launch_block_apply_cols<double>(double *, int64_t, int, const DevSched &, int, const double *,
                                               cudaStream_t, const int *, const int *);
-template void launch_block_apply_cols<float>(float *, int64_t, int, const DevSched &, int, const float *,
+template cudaError_t launch_block_apply_cols<float>(float *, int64_t, int, const DevSched &, int, const float *,
                                              cudaStream_t, const int *, const int *);
 
 template size_t block_scratch_bytes<double>(int, int);
 template size_t block_scratch_bytes<float>(int, int);
 template mpj_status block_sweep<double>(double *, int64_t, double *, int64_t, int, const DevSched &, double,
-                                        int, unsigned long long *, void *, cudaStream_t, bool);
+                                        int, unsigned long long *, void *, cudaStream_t, bool, int);
 template mpj_status block_sweep<float>(float *, int64_t, float *, int64_t, int, const DevSched &, float, int,
-                                       unsigned long long *, void *, cudaStream_t, bool);
+                                       unsigned long long *, void *, cudaStream_t, bool, int);
 
 }  // namespace mpj

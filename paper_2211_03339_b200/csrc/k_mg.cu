@@ -23,6 +23,7 @@
 // Emulation: the same code runs G ranks in one process on one GPU with shared
 // U buffers and device copies instead of NCCL (tests; no kernel waits on
 // another).
+#include <cmath>
 #include <nccl.h>
 
 #include "mpj_block.cuh"
@@ -704,17 +705,12 @@ static mpj_status mg_sweep(Group &g, R **Ts, R **Vs, R nu, int rule)
     constexpr int LD = Lay<R>::LD;
     const size_t sm_solve = 3 * TW * LayK<R>::LD * sizeof(R), sm_apply = 3 * TW * LD * sizeof(R);
     const size_t sm_apply64x3 = 2 * TW * Lay<double>::LD * sizeof(double);
-    static bool attr[2] = {false, false};
-    if (!attr[sizeof(R) == 8]) {
-        MPJ_CK(cudaFuncSetAttribute(k_mg_solve<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_solve));
-        MPJ_CK(cudaFuncSetAttribute(k_mg_apply<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_apply));
-        if (sizeof(R) == 4)
-            MPJ_CK(cudaFuncSetAttribute(k_mg_apply_f32, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_apply));
-        else
-            MPJ_CK(cudaFuncSetAttribute(k_mg_apply_f64x3, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        (int)sm_apply64x3));
-        attr[sizeof(R) == 8] = true;
-    }
+    MPJ_CK(smem_optin((const void *)k_mg_solve<R>, sm_solve, NTW, nullptr));
+    MPJ_CK(smem_optin((const void *)k_mg_apply<R>, sm_apply, NT, nullptr));
+    if (sizeof(R) == 4)
+        MPJ_CK(smem_optin((const void *)k_mg_apply_f32, sm_apply, 128, nullptr));
+    else
+        MPJ_CK(smem_optin((const void *)k_mg_apply_f64x3, sm_apply64x3, NT, nullptr));
     int *nid = g.uid + P.mb;
     MPJ_CK(cudaMemsetAsync(nid, 0, (size_t)rounds * sizeof(int), g.st));
     int nsm = 148, dev = 0;
@@ -827,7 +823,7 @@ static mpj_status mg_loop(Group &g, R **Ts, R **Vs, double tol, R nu, int rule, 
         double off = 0;
         MPJ_TRY(mg_norm<R>(g, true, Ts, off));
         if (hist && sweeps < 64) hist[sweeps] = off;
-        if (!(off == off)) { set_error("non-finite off-norm"); return MPJ_ERR_NONFINITE; }
+        if (!std::isfinite(off)) { set_error("non-finite off-norm"); return MPJ_ERR_NONFINITE; }
         if (off <= tol) { status = MPJ_OK; break; }
         if (sweeps >= max_sweeps) { status = MPJ_ERR_NOCONV; break; }
         ++sweeps;

@@ -22,6 +22,7 @@
 #include "mpj_device.cuh"
 #include "mpj_internal.h"
 
+#include <cmath>
 #include <algorithm>
 #include <cstdlib>
 #include <cstring>
@@ -534,8 +535,8 @@ static mpj_status svd_block_sweep(SvdPlan &p, R *C, R *V, const DevSched &ds, R 
             count_launch(2);
         }
         if (prof) { prof_mark(ns, st, false); prof_mark(na, st, true); }
-        launch_block_apply_cols<R>(C, p.ldc, (int)p.m, ds, Rb, (const R *)p.Ubuf, st, uid, nid + Rb);
-        launch_block_apply_cols<R>(V, p.np, p.np, ds, Rb, (const R *)p.Ubuf, st, uid, nid + Rb);
+        MPJ_CK(launch_block_apply_cols<R>(C, p.ldc, (int)p.m, ds, Rb, (const R *)p.Ubuf, st, uid, nid + Rb));
+        MPJ_CK(launch_block_apply_cols<R>(V, p.np, p.np, ds, Rb, (const R *)p.Ubuf, st, uid, nid + Rb));
         if (prof) prof_mark(na, st, false);
     }
     return MPJ_OK;
@@ -563,6 +564,7 @@ struct SvdStage {
     int sweeps = 0;
     long long rotations = 0;
     double hist[64] = {0};
+    long long rot_hist[64] = {0};   // rotations applied in sweep k+1
     int nhist = 0;
 };
 
@@ -590,7 +592,7 @@ static mpj_status svd_loop(SvdPlan &p, R *C, R *V, double *Cd, const DevSched &d
         MPJ_CK(cudaStreamSynchronize(st));
         const double off = h_pin[0], tot = h_pin[1];
         if (out.sweeps < 64) { out.hist[out.sweeps] = off; out.nhist = out.sweeps + 1; }
-        if (!(off == off)) { set_error("non-finite Gram"); return MPJ_ERR_NONFINITE; }
+        if (!std::isfinite(off)) { set_error("non-finite Gram"); return MPJ_ERR_NONFINITE; }
         if (off <= eps_rel * tot) { status = MPJ_OK; break; }
         if (out.sweeps >= max_sweeps) { status = MPJ_ERR_NOCONV; break; }
         ++out.sweeps;
@@ -602,6 +604,7 @@ static mpj_status svd_loop(SvdPlan &p, R *C, R *V, double *Cd, const DevSched &d
         const unsigned long long rs = now - prev;
         prev = now;
         out.rotations = (long long)now;
+        if (out.sweeps <= 64) out.rot_hist[out.sweeps - 1] = (long long)rs;
         ratio = N > 0 ? (double)rs / N : 0.0;
         if (early > 0 && N > 0 && (double)rs / N < early) { status = MPJ_OK; break; }
     }
@@ -618,16 +621,23 @@ size_t svd_workspace(int64_t m, int64_t n)
 
 mpj_status svd_run(const double *A, int64_t m, int64_t n, int64_t lda, double *Sigma, double *U, int64_t ldu,
                    double *V, int64_t ldv, int *sweeps, void *workspace, size_t ws_bytes, cudaStream_t st,
-                   const mpj_config &cfg, mpj_report &r, double *h_pin, bool a_dev, bool out_dev)
+                   const mpj_config &cfg, mpj_report &r, double *h_pin, bool a_dev, bool out_dev,
+                   const float *Zin, bool zin_dev, float *Zout, bool zout_dev, int64_t ldz)
 {
     const double omega = 1.1102230246251565e-16, upsilon = 5.9604644775390625e-08;
     size_t off = 0;
     SvdPlan p;
     carve_svd(nullptr, off, m, n, p);
-    void *own = nullptr;
+    // a library-owned workspace is released on every exit, error exits included
+    struct OwnWs {
+        void *p = nullptr;
+        cudaStream_t st;
+        ~OwnWs() { if (p) cudaFreeAsync(p, st); }
+    } own;
+    own.st = st;
     if (!workspace) {
-        MPJ_CK(cudaMallocAsync(&own, off + 256, st));
-        workspace = own;
+        MPJ_CK(cudaMallocAsync(&own.p, off + 256, st));
+        workspace = own.p;
     } else if (ws_bytes < off + 256) {
         set_error("workspace too small");
         return MPJ_ERR_NOMEM;
@@ -660,10 +670,7 @@ mpj_status svd_run(const double *A, int64_t m, int64_t n, int64_t lda, double *S
     int bad = 0;
     std::memcpy(&bad, h_pin + 1, sizeof(int));
     r.norm_a = normA;
-    auto fin = [&](mpj_status s) {
-        if (own) cudaFreeAsync(own, st);
-        return s;
-    };
+    auto fin = [&](mpj_status s) { return s; };
     if (bad) { set_error("input has NaN/Inf"); return fin(MPJ_ERR_NONFINITE); }
 
     // a1: fp32 one-sided Jacobi on fl32(A) from V = I (reading R12)
@@ -671,15 +678,25 @@ mpj_status svd_run(const double *A, int64_t m, int64_t n, int64_t lda, double *S
         cudaEvent_t e0, e1;
         cudaEventCreate(&e0); cudaEventCreate(&e1);
         cudaEventRecord(e0, st);
-        launch_copy_pad<double, float>(p.Ad, ldc, (int)m, np, p.C32, ldc, (int)m, np, st);
-        MPJ_CK(cudaMemsetAsync(p.V32, 0, (size_t)np * np * 4, st));
-        launch_identity<float>(p.V32, np, (int)n, (int)n, st);
-        SvdStage lo;
-        mpj_status sl = svd_loop<float>(p, p.C32, p.V32, p.C, ds, eps_low_factor(cfg, n) * upsilon,
-                                        (float)(cfg.nu_low_factor * upsilon), cfg.early_stop_ratio,
-                                        cfg.max_sweeps_low, h_pin, st, lo);
-        if (sl != MPJ_OK && sl != MPJ_ERR_NOCONV) return fin(sl);
-        r.sweeps_low = lo.sweeps; r.rotations_low = lo.rotations; r.status_low = sl;
+        if (Zin) {   // the caller's Z replaces the low-precision stage
+            MPJ_CK(cudaMemsetAsync(p.V32, 0, (size_t)np * np * 4, st));
+            MPJ_CK(cudaMemcpy2DAsync(p.V32, np * 4, Zin, ldz * 4, n * 4, n,
+                                     zin_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, st));
+            r.status_low = MPJ_OK;
+        } else {
+            launch_copy_pad<double, float>(p.Ad, ldc, (int)m, np, p.C32, ldc, (int)m, np, st);
+            MPJ_CK(cudaMemsetAsync(p.V32, 0, (size_t)np * np * 4, st));
+            launch_identity<float>(p.V32, np, (int)n, (int)n, st);
+            SvdStage lo;
+            mpj_status sl = svd_loop<float>(p, p.C32, p.V32, p.C, ds, eps_low_factor(cfg, n) * upsilon,
+                                            (float)(cfg.nu_low_factor * upsilon), cfg.early_stop_ratio,
+                                            cfg.max_sweeps_low, h_pin, st, lo);
+            if (sl != MPJ_OK && sl != MPJ_ERR_NOCONV) return fin(sl);
+            r.sweeps_low = lo.sweeps; r.rotations_low = lo.rotations; r.status_low = sl;
+        }
+        if (Zout)
+            MPJ_CK(cudaMemcpy2DAsync(Zout, ldz * 4, p.V32, np * 4, n * 4, n,
+                                     zout_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, st));
         cudaEventRecord(e1, st);
         cudaEventSynchronize(e1);
         float ms = 0; cudaEventElapsedTime(&ms, e0, e1); r.t_low = ms * 1e-3;
@@ -712,6 +729,7 @@ mpj_status svd_run(const double *A, int64_t m, int64_t n, int64_t lda, double *S
         r.sweeps = hi.sweeps; r.rotations = hi.rotations; r.status = sh;
         r.off0 = hi.hist[0];
         for (int k = 0; k < hi.nhist && k < 64; ++k) r.off_hist[k] = hi.hist[k];
+        for (int k = 0; k < 64; ++k) r.rot_hist[k] = hi.rot_hist[k];
         cudaEventRecord(e1, st);
         cudaEventSynchronize(e1);
         float ms = 0; cudaEventElapsedTime(&ms, e0, e1); r.t_jacobi = ms * 1e-3;

@@ -20,6 +20,12 @@ void prof_mark(const char *name, cudaStream_t st, bool begin);
 void prof_flush();   // after the stream has been synchronised
 void prof_add(const std::string &name, long long n);   // a counter (launches field only)
 
+// Opt a kernel into `bytes` of dynamic shared memory on the CURRENT device
+// (the attribute is per device context) and return its resident CTAs per SM
+// for `threads` threads (per_sm may be NULL).  Thread-safe; the attribute is
+// set once per (kernel, device, size).
+cudaError_t smem_optin(const void *func, size_t bytes, int threads, int *per_sm);
+
 #define MPJ_CK(expr)                                                                    \
     do {                                                                                \
         cudaError_t e_ = (expr);                                                        \
@@ -71,7 +77,7 @@ void launch_round_apply_v(R *V, int64_t ldv, int vrows, const int2 *pq, const R 
 
 // ---- block variant pieces (k_block.cu) ---------------------------------------
 template <typename R>
-void launch_block_apply_cols(R *M, int64_t ld, int rows, const DevSched &ds, int Rb, const R *Ubuf,
+cudaError_t launch_block_apply_cols(R *M, int64_t ld, int rows, const DevSched &ds, int Rb, const R *Ubuf,
                              cudaStream_t st, const int *uid = nullptr, const int *nid = nullptr);
 
 // ---- utilities (k_util.cu) --------------------------------------------------

@@ -14,6 +14,8 @@
 #include <algorithm>
 #include <cmath>
 #include <map>
+#include <mutex>
+#include <tuple>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -32,12 +34,14 @@ mpj_status mg_eig(bool mixed, const double *A, int64_t n, int64_t lda, double *L
 size_t svd_workspace(int64_t m, int64_t n);
 mpj_status svd_run(const double *A, int64_t m, int64_t n, int64_t lda, double *Sigma, double *U, int64_t ldu,
                    double *V, int64_t ldv, int *sweeps, void *workspace, size_t ws_bytes, cudaStream_t st,
-                   const mpj_config &cfg, mpj_report &r, double *h_pin, bool a_dev, bool out_dev);
+                   const mpj_config &cfg, mpj_report &r, double *h_pin, bool a_dev, bool out_dev,
+                   const float *Zin, bool zin_dev, float *Zout, bool zout_dev, int64_t ldz);
 
 // Block-variant entry (k_block.cu).
 template <typename R>
 mpj_status block_sweep(R *T, int64_t ldt, R *V, int64_t ldv, int vrows, const DevSched &S, R nu,
-                       int rule, unsigned long long *cnt, void *scratch, cudaStream_t st, bool first_sweep);
+                       int rule, unsigned long long *cnt, void *scratch, cudaStream_t st, bool first_sweep,
+                       int max_brounds);
 template <typename R>
 size_t block_scratch_bytes(int np, int b);
 
@@ -48,6 +52,28 @@ thread_local long long g_launches = 0;
 
 void set_error(const std::string &msg) { g_err = msg; }
 void count_launch(long long k) { g_launches += k; }
+
+cudaError_t smem_optin(const void *func, size_t bytes, int threads, int *per_sm)
+{
+    static std::mutex mu;
+    static std::map<std::tuple<const void *, int, size_t, int>, int> done;   // -> CTAs per SM
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    std::lock_guard<std::mutex> lk(mu);
+    auto key = std::make_tuple(func, dev, bytes, threads);
+    auto it = done.find(key);
+    if (it == done.end()) {
+        e = cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+        if (e != cudaSuccess) return e;
+        int occ = 0;
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, func, threads, bytes);
+        if (e != cudaSuccess) return e;
+        it = done.emplace(key, std::max(1, occ)).first;
+    }
+    if (per_sm) *per_sm = it->second;
+    return cudaSuccess;
+}
 
 // ---- kernel timing ---------------------------------------------------------
 namespace {
@@ -302,6 +328,7 @@ struct JacobiOut {
     int sweeps = 0;
     long long rotations = 0;
     double hist[64] = {0};
+    long long rot_hist[64] = {0};   // rotations applied in sweep k+1
     int nhist = 0;
 };
 
@@ -328,20 +355,48 @@ static mpj_status jacobi_run(Ctx &cx, R *T, R *V, int n, int b, int variant, dou
     int64_t rounds_done = 0;
     int sweeps = 0;
     mpj_status status = MPJ_ERR_NOCONV;
+    unsigned long long rot_prev = 0;
     for (;;) {
         launch_norm<R>(T, np, np, np, true, jb.part, jb.off, st);
         MPJ_CK(cudaMemcpyAsync(cx.h_pin, jb.off, sizeof(double), cudaMemcpyDeviceToHost, st));
+        MPJ_CK(cudaMemcpyAsync(cx.h_pin + 1, jb.cnt, sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
         MPJ_CK(cudaStreamSynchronize(st));
         const double off = cx.h_pin[0];
+        unsigned long long rot_now = 0;
+        std::memcpy(&rot_now, cx.h_pin + 1, sizeof(rot_now));
+        if (sweeps >= 1 && sweeps <= 64) out.rot_hist[sweeps - 1] = (long long)(rot_now - rot_prev);
+        rot_prev = rot_now;
         if (sweeps < 64) { out.hist[sweeps] = off; out.nhist = sweeps + 1; }
-        if (!(off == off)) { set_error("non-finite off-norm"); status = MPJ_ERR_NONFINITE; break; }
+        if (!std::isfinite(off)) { set_error("non-finite off-norm"); status = MPJ_ERR_NONFINITE; break; }
         if (off <= tol) { status = MPJ_OK; break; }
         if (sweeps >= max_sweeps) { status = MPJ_ERR_NOCONV; break; }
         if (max_rounds >= 0 && rounds_done >= max_rounds) { status = MPJ_OK; break; }
         ++sweeps;
         if (variant == MPJ_VARIANT_BLOCK) {
-            MPJ_TRY(block_sweep<R>(T, np, V, np, np, ds, nu, rule, jb.cnt, jb.block_scratch, st, sweeps == 1));
-            rounds_done += hs.rounds;
+            // block round 0 holds 2b - 1 scalar rounds (b - 1 intra-block + b
+            // cross), every later one b (reading R1); a round limit must fall
+            // on a block-round boundary
+            int nbr = hs.nb - 1;
+            int64_t used = hs.rounds;
+            if (max_rounds >= 0 && max_rounds - rounds_done < hs.rounds) {
+                const int64_t left = max_rounds - rounds_done;
+                int k = 0;
+                used = 0;
+                while (k < nbr) {
+                    const int64_t c = k == 0 ? 2 * b - 1 : b;
+                    if (used + c > left) break;
+                    used += c;
+                    ++k;
+                }
+                if (used != left) {
+                    set_error("max_rounds must end on a block-round boundary (2b-1, then +b)");
+                    return MPJ_ERR_INVALID;
+                }
+                nbr = k;
+            }
+            MPJ_TRY(block_sweep<R>(T, np, V, np, np, ds, nu, rule, jb.cnt, jb.block_scratch, st, sweeps == 1,
+                                   nbr));
+            rounds_done += used;
         } else if (use_graph) {
             if (!gexec) {
                 cudaGraph_t g;
@@ -462,10 +517,11 @@ static const double kUpsilon = 5.9604644775390625e-08;  // 2^-24
 
 static mpj_status eig_impl(bool mixed, const double *A, int64_t n, int64_t lda, double *Lambda,
                            double *V, int64_t ldv, int *sweeps, void *workspace, size_t ws_bytes,
-                           void *stream, const mpj_config *cfg_in, mpj_report *rep)
+                           void *stream, const mpj_config *cfg_in, mpj_report *rep,
+                           const float *Zin = nullptr, float *Zout = nullptr, int64_t ldz = 0)
 {
     g_err.clear();
-    if (n < 1 || lda < n || ldv < n || !A || !Lambda || !V) {
+    if (n < 1 || lda < n || ldv < n || !A || !Lambda || !V || ((Zin || Zout) && ldz < n)) {
         set_error("mpjacobi_eig: invalid argument");
         return MPJ_ERR_INVALID;
     }
@@ -510,6 +566,20 @@ static mpj_status eig_impl(bool mixed, const double *A, int64_t n, int64_t lda, 
         mpj_status c = cx.close();
         return s != MPJ_OK ? s : c;
     };
+    // every error exit below releases the workspace and fills rep (finish)
+#define MPJ_CKF(expr)                                                                   \
+    do {                                                                                \
+        cudaError_t e_ = (expr);                                                        \
+        if (e_ != cudaSuccess) {                                                        \
+            set_error(std::string(#expr) + ": " + cudaGetErrorString(e_));              \
+            return finish(MPJ_ERR_CUDA);                                                \
+        }                                                                               \
+    } while (0)
+#define MPJ_TRYF(expr)                                                                  \
+    do {                                                                                \
+        mpj_status s_ = (expr);                                                         \
+        if (s_ != MPJ_OK) return finish(s_);                                            \
+    } while (0)
 
     // a0: stage A (host or device) into T, symmetrise into Asym, check finite, ||A||_F
     const bool a_dev = is_device_ptr(A);
@@ -523,9 +593,9 @@ static mpj_status eig_impl(bool mixed, const double *A, int64_t n, int64_t lda, 
     launch_check_finite(p.T, np, (int)n, (int)n, p.flag, cx.st);
     launch_symmetrize(p.T, np, (int)n, p.Asym, np, np, cx.st);
     launch_norm<double>(p.Asym, np, np, np, false, p.red_part, p.red_out, cx.st);
-    MPJ_CK(cudaMemcpyAsync(cx.h_pin, p.red_out, sizeof(double), cudaMemcpyDeviceToHost, cx.st));
-    MPJ_CK(cudaMemcpyAsync(cx.h_pin + 1, p.flag, sizeof(int), cudaMemcpyDeviceToHost, cx.st));
-    MPJ_CK(cudaStreamSynchronize(cx.st));
+    MPJ_CKF(cudaMemcpyAsync(cx.h_pin, p.red_out, sizeof(double), cudaMemcpyDeviceToHost, cx.st));
+    MPJ_CKF(cudaMemcpyAsync(cx.h_pin + 1, p.flag, sizeof(int), cudaMemcpyDeviceToHost, cx.st));
+    MPJ_CKF(cudaStreamSynchronize(cx.st));
     const double normA = cx.h_pin[0];
     int bad = 0;
     std::memcpy(&bad, cx.h_pin + 1, sizeof(int));
@@ -534,49 +604,59 @@ static mpj_status eig_impl(bool mixed, const double *A, int64_t n, int64_t lda, 
 
     mpj_status s = MPJ_OK;
     if (mixed) {
-        // a1: low-precision stage (reading R12)
+        // a1: low-precision stage (reading R12) -- or the caller's Z
         Timer tl(cx.st);
-        launch_copy_pad<double, float>(p.Asym, np, np, np, p.T32, np, np, np, cx.st);
-        MPJ_CK(cudaMemsetAsync(p.V32, 0, (size_t)np * np * sizeof(float), cx.st));
-        launch_identity<float>(p.V32, np, (int)n, (int)n, cx.st);
-        launch_norm<float>(p.T32, np, np, np, false, p.red_part, p.red_out, cx.st);
-        double nA32 = 0;
-        MPJ_TRY(read_scalar(cx, p.red_out, nA32));
-        JacobiOut jo;
-        mpj_status sl = jacobi_run<float>(cx, p.T32, p.V32, (int)n, p.b, p.variant,
-                                          eps_low_factor(cfg, n) * kUpsilon * nA32,
-                                          (float)(cfg.nu_low_factor * kUpsilon), cfg.stop_rule,
-                                          cfg.max_sweeps_low, -1, p.j32, jo);
-        if (sl != MPJ_OK && sl != MPJ_ERR_NOCONV) return finish(sl);
-        r.sweeps_low = jo.sweeps;
-        r.rotations_low = jo.rotations;
-        r.status_low = sl;
-        for (int k = 0; k < jo.nhist && k < 64; ++k) r.off_hist_low[k] = jo.hist[k];
+        if (Zin) {
+            MPJ_CKF(cudaMemsetAsync(p.V32, 0, (size_t)np * np * sizeof(float), cx.st));
+            MPJ_TRYF(copy2d(p.V32, np, Zin, ldz, n, n, sizeof(float),
+                            is_device_ptr(Zin) ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, cx.st));
+            r.status_low = MPJ_OK;
+        } else {
+            launch_copy_pad<double, float>(p.Asym, np, np, np, p.T32, np, np, np, cx.st);
+            MPJ_CKF(cudaMemsetAsync(p.V32, 0, (size_t)np * np * sizeof(float), cx.st));
+            launch_identity<float>(p.V32, np, (int)n, (int)n, cx.st);
+            launch_norm<float>(p.T32, np, np, np, false, p.red_part, p.red_out, cx.st);
+            double nA32 = 0;
+            MPJ_TRYF(read_scalar(cx, p.red_out, nA32));
+            JacobiOut jo;
+            mpj_status sl = jacobi_run<float>(cx, p.T32, p.V32, (int)n, p.b, p.variant,
+                                              eps_low_factor(cfg, n) * kUpsilon * nA32,
+                                              (float)(cfg.nu_low_factor * kUpsilon), cfg.stop_rule,
+                                              cfg.max_sweeps_low, -1, p.j32, jo);
+            if (sl != MPJ_OK && sl != MPJ_ERR_NOCONV) return finish(sl);
+            r.sweeps_low = jo.sweeps;
+            r.rotations_low = jo.rotations;
+            r.status_low = sl;
+            for (int k = 0; k < jo.nhist && k < 64; ++k) r.off_hist_low[k] = jo.hist[k];
+        }
+        if (Zout)
+            MPJ_TRYF(copy2d(Zout, ldz, p.V32, np, n, n, sizeof(float),
+                            is_device_ptr(Zout) ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, cx.st));
         r.t_low = tl.stop();
 
         // a2: Q = orth(Z), Z = fp64(V32) (n x n real block)
         Timer to(cx.st);
         launch_copy_pad<float, double>(p.V32, np, (int)n, (int)n, p.W, np, (int)n, (int)n, cx.st);
-        MPJ_CK(cudaMemsetAsync(p.V, 0, (size_t)np * np * sizeof(double), cx.st));
+        MPJ_CKF(cudaMemsetAsync(p.V, 0, (size_t)np * np * sizeof(double), cx.st));
         s = orth_cgs2(p.W, np, p.V, np, n, n, p.orth_ws, cx.st);
         if (s != MPJ_OK) return finish(s);
         r.t_orth = to.stop();
 
         // a3: T = Q^T A Q (W = A Q, T = Q^T W), symmetrised (reading R11)
         Timer tp(cx.st);
-        MPJ_CK(cudaMemsetAsync(p.T, 0, (size_t)np * np * sizeof(double), cx.st));
+        MPJ_CKF(cudaMemsetAsync(p.T, 0, (size_t)np * np * sizeof(double), cx.st));
         launch_dgemm(false, false, n, n, n, 1.0, p.Asym, np, p.V, np, 0.0, p.W, np, cx.st);
         launch_dgemm(true, false, n, n, n, 1.0, p.V, np, p.W, np, 0.0, p.T, np, cx.st);
         launch_symmetrize_inplace(p.T, np, (int)n, cx.st);
         launch_norm<double>(p.T, np, np, np, true, p.red_part, p.red_out, cx.st);
-        MPJ_TRY(read_scalar(cx, p.red_out, r.off0));
+        MPJ_TRYF(read_scalar(cx, p.red_out, r.off0));
         r.t_precond = tp.stop();
     } else {
-        MPJ_CK(cudaMemcpyAsync(p.T, p.Asym, (size_t)np * np * sizeof(double), cudaMemcpyDeviceToDevice, cx.st));
-        MPJ_CK(cudaMemsetAsync(p.V, 0, (size_t)np * np * sizeof(double), cx.st));
+        MPJ_CKF(cudaMemcpyAsync(p.T, p.Asym, (size_t)np * np * sizeof(double), cudaMemcpyDeviceToDevice, cx.st));
+        MPJ_CKF(cudaMemsetAsync(p.V, 0, (size_t)np * np * sizeof(double), cx.st));
         launch_identity<double>(p.V, np, (int)n, (int)n, cx.st);
         launch_norm<double>(p.T, np, np, np, true, p.red_part, p.red_out, cx.st);
-        MPJ_TRY(read_scalar(cx, p.red_out, r.off0));
+        MPJ_TRYF(read_scalar(cx, p.red_out, r.off0));
     }
 
     // a4-a8: fp64 sweeps
@@ -589,6 +669,7 @@ static mpj_status eig_impl(bool mixed, const double *A, int64_t n, int64_t lda, 
         r.rotations = jo.rotations;
         r.status = s;
         for (int k = 0; k < jo.nhist && k < 64; ++k) r.off_hist[k] = jo.hist[k];
+        for (int k = 0; k < 64; ++k) r.rot_hist[k] = jo.rot_hist[k];
         r.t_jacobi = tj.stop();
         if (s != MPJ_OK && s != MPJ_ERR_NOCONV) return finish(s);
     }
@@ -602,15 +683,17 @@ static mpj_status eig_impl(bool mixed, const double *A, int64_t n, int64_t lda, 
         double *v_d = v_dev ? V : p.W;
         const int64_t ldvo = v_dev ? ldv : np;
         launch_extract_evd(p.T, np, p.V, np, (int)n, (int)n, lam_d, v_d, ldvo, p.rank, cx.st);
-        if (!l_dev) MPJ_CK(cudaMemcpyAsync(Lambda, p.lam, n * sizeof(double), cudaMemcpyDeviceToHost, cx.st));
+        if (!l_dev) MPJ_CKF(cudaMemcpyAsync(Lambda, p.lam, n * sizeof(double), cudaMemcpyDeviceToHost, cx.st));
         if (!v_dev) {
             mpj_status c = copy2d(V, ldv, p.W, np, n, n, sizeof(double), cudaMemcpyDeviceToHost, cx.st);
             if (c != MPJ_OK) return finish(c);
         }
-        MPJ_CK(cudaStreamSynchronize(cx.st));
+        MPJ_CKF(cudaStreamSynchronize(cx.st));
         r.t_extract = te.stop();
     }
     return finish(s);
+#undef MPJ_CKF
+#undef MPJ_TRYF
 }
 
 template <typename R>
@@ -725,6 +808,14 @@ mpj_status mpjacobi_eig(const double *A, int64_t n, int64_t lda, double *Lambda,
     return eig_impl(true, A, n, lda, Lambda, V, ldv, sweeps, workspace, ws_bytes, stream, cfg, rep);
 }
 
+mpj_status mpjacobi_eig_z(const double *A, int64_t n, int64_t lda, const float *Z_in, float *Z_out, int64_t ldz,
+                          double *Lambda, double *V, int64_t ldv, int *sweeps, void *workspace, size_t ws_bytes,
+                          void *stream, const mpj_config *cfg, mpj_report *rep)
+{
+    return eig_impl(true, A, n, lda, Lambda, V, ldv, sweeps, workspace, ws_bytes, stream, cfg, rep, Z_in, Z_out,
+                    ldz);
+}
+
 mpj_status mpjacobi_eig_plain(const double *A, int64_t n, int64_t lda, double *Lambda, double *V,
                               int64_t ldv, int *sweeps, void *workspace, size_t ws_bytes, void *stream,
                               const mpj_config *cfg, mpj_report *rep)
@@ -834,14 +925,15 @@ size_t mpjacobi_svd_workspace(int64_t m, int64_t n, const mpj_config *)
     return mpj::svd_workspace(m, n);
 }
 
-mpj_status mpjacobi_svd(const double *A, int64_t m, int64_t n, int64_t lda, double *Sigma, double *U, int64_t ldu,
-                        double *V, int64_t ldv, int *sweeps, void *workspace, size_t ws_bytes, void *stream,
-                        const mpj_config *cfg_in, mpj_report *rep)
+static mpj_status svd_impl(const double *A, int64_t m, int64_t n, int64_t lda, double *Sigma, double *U,
+                           int64_t ldu, double *V, int64_t ldv, int *sweeps, void *workspace, size_t ws_bytes,
+                           void *stream, const mpj_config *cfg_in, mpj_report *rep, const float *Zin, float *Zout,
+                           int64_t ldz)
 {
     using namespace mpj;
     set_error("");
-    if (n < 1 || m < n || lda < m || ldu < m || ldv < n || !A || !Sigma || !U || !V) {
-        set_error("mpjacobi_svd: need m >= n >= 1, lda, ldu >= m, ldv >= n, non-NULL buffers");
+    if (n < 1 || m < n || lda < m || ldu < m || ldv < n || !A || !Sigma || !U || !V || ((Zin || Zout) && ldz < n)) {
+        set_error("mpjacobi_svd: need m >= n >= 1, lda, ldu >= m, ldv >= n (ldz >= n), non-NULL buffers");
         return MPJ_ERR_INVALID;
     }
     mpj_config cfg;
@@ -855,11 +947,27 @@ mpj_status mpjacobi_svd(const double *A, int64_t m, int64_t n, int64_t lda, doub
     const bool a_dev = is_device_ptr(A);
     const bool out_dev = is_device_ptr(U) && is_device_ptr(V) && is_device_ptr(Sigma);
     mpj_status s = svd_run(A, m, n, lda, Sigma, U, ldu, V, ldv, sweeps, workspace, ws_bytes, cx.st, cfg, r,
-                           cx.h_pin, a_dev, out_dev);
+                           cx.h_pin, a_dev, out_dev, Zin, is_device_ptr(Zin), Zout, is_device_ptr(Zout), ldz);
     r.t_total = t_all.stop();
     r.launches = mpjacobi_launch_count() - l0;
     if (rep) *rep = r;
     mpj_status c = cx.close();
     return s != MPJ_OK ? s : c;
+}
+
+mpj_status mpjacobi_svd(const double *A, int64_t m, int64_t n, int64_t lda, double *Sigma, double *U, int64_t ldu,
+                        double *V, int64_t ldv, int *sweeps, void *workspace, size_t ws_bytes, void *stream,
+                        const mpj_config *cfg, mpj_report *rep)
+{
+    return svd_impl(A, m, n, lda, Sigma, U, ldu, V, ldv, sweeps, workspace, ws_bytes, stream, cfg, rep, nullptr,
+                    nullptr, 0);
+}
+
+mpj_status mpjacobi_svd_z(const double *A, int64_t m, int64_t n, int64_t lda, const float *Z_in, float *Z_out,
+                          int64_t ldz, double *Sigma, double *U, int64_t ldu, double *V, int64_t ldv, int *sweeps,
+                          void *workspace, size_t ws_bytes, void *stream, const mpj_config *cfg, mpj_report *rep)
+{
+    return svd_impl(A, m, n, lda, Sigma, U, ldu, V, ldv, sweeps, workspace, ws_bytes, stream, cfg, rep, Z_in, Z_out,
+                    ldz);
 }
 }
