@@ -663,7 +663,7 @@ static mpj_status mg_norm(Group &g, bool offdiag, R **Ts, double &out)
         k_mg_norm<R><<<kRedBlocks, 256, 0, g.st>>>(Ts[i], g.np, g.np, g.ncl, b.colg, offdiag ? 1 : 0, b.part);
         k_mg_sum<<<1, 256, 0, g.st>>>(b.part, kRedBlocks, b.part + kRedBlocks);
         count_launch(2);
-        if (g.nlocal == 1 && g.G > 1) {
+        if (g.comm) {   // NCCL (one process per rank; also with a single rank)
             MPJ_TRY(nccl_ck(ncclAllReduce(b.part + kRedBlocks, b.part + kRedBlocks, 1, ncclDouble, ncclSum, g.comm, g.st),
                             "ncclAllReduce"));
         }
@@ -729,7 +729,7 @@ static mpj_status mg_sweep(Group &g, R **Ts, R **Vs, R nu, int rule)
             count_launch();
         }
         if (prof) prof_mark(nsolve, g.st, false);
-        if (g.nlocal == 1 && g.G > 1) {
+        if (g.comm) {   // NCCL (one process per rank; also with a single rank)
             const size_t per = (size_t)P.mbl * TW * TW * (8 / sizeof(R));   // fp32: U and U^T per slot
             R *U = (R *)g.Ubuf;
             MPJ_TRY(nccl_ck(ncclAllGather(U + g.me * per, U, per * sizeof(R), ncclChar, g.comm, g.st),
@@ -770,12 +770,17 @@ static mpj_status mg_sweep(Group &g, R **Ts, R **Vs, R nu, int rule)
             }
             MPJ_TRY(nccl_ck(ncclGroupStart(), "ncclGroupStart"));
             for (const Xfer &x : out) {
-                ncclSend(Ts[0] + (size_t)x.sphys * BW * g.np, blk_bytes, ncclChar, x.dst, g.comm, g.st);
-                ncclSend(Vs[0] + (size_t)x.sphys * BW * g.np, blk_bytes, ncclChar, x.dst, g.comm, g.st);
+                MPJ_TRY(nccl_ck(ncclSend(Ts[0] + (size_t)x.sphys * BW * g.np, blk_bytes, ncclChar, x.dst, g.comm, g.st),
+                                "ncclSend(T)"));
+                MPJ_TRY(nccl_ck(ncclSend(Vs[0] + (size_t)x.sphys * BW * g.np, blk_bytes, ncclChar, x.dst, g.comm, g.st),
+                                "ncclSend(V)"));
             }
             for (size_t k = 0; k < in.size(); ++k) {
-                ncclRecv(g.rk[0].stage + 2 * k * blk_bytes, blk_bytes, ncclChar, in[k].src, g.comm, g.st);
-                ncclRecv(g.rk[0].stage + (2 * k + 1) * blk_bytes, blk_bytes, ncclChar, in[k].src, g.comm, g.st);
+                MPJ_TRY(nccl_ck(ncclRecv(g.rk[0].stage + 2 * k * blk_bytes, blk_bytes, ncclChar, in[k].src, g.comm, g.st),
+                                "ncclRecv(T)"));
+                MPJ_TRY(nccl_ck(ncclRecv(g.rk[0].stage + (2 * k + 1) * blk_bytes, blk_bytes, ncclChar, in[k].src,
+                                         g.comm, g.st),
+                                "ncclRecv(V)"));
             }
             MPJ_TRY(nccl_ck(ncclGroupEnd(), "ncclGroupEnd"));
             for (size_t k = 0; k < in.size(); ++k) {
@@ -834,7 +839,7 @@ static mpj_status mg_loop(Group &g, R **Ts, R **Vs, double tol, R nu, int rule, 
     MPJ_CK(cudaMemcpyAsync(g.h, g.cnt, sizeof(c), cudaMemcpyDeviceToHost, g.st));
     MPJ_CK(cudaStreamSynchronize(g.st));
     std::memcpy(&c, g.h, sizeof(c));
-    if (g.nlocal == 1 && g.G > 1) {
+    if (g.comm) {   // NCCL (one process per rank; also with a single rank)
         double v = (double)c;
         double *d = g.rk[0].part + kRedBlocks + 1;
         MPJ_CK(cudaMemcpyAsync(d, &v, sizeof(double), cudaMemcpyHostToDevice, g.st));
@@ -865,7 +870,7 @@ template <typename R>
 static mpj_status mg_allgather_cols(Group &g, R **loc_bufs, R *all)
 {
     const size_t loc = (size_t)g.np * g.ncl;
-    if (g.nlocal == 1 && g.G > 1) {
+    if (g.comm) {   // NCCL (one process per rank; also with a single rank)
         MPJ_CK(cudaMemcpyAsync(all + (size_t)g.me * loc, loc_bufs[0], loc * sizeof(R), cudaMemcpyDeviceToDevice, g.st));
         MPJ_TRY(nccl_ck(ncclAllGather(all + (size_t)g.me * loc, all, loc * sizeof(R), ncclChar, g.comm, g.st),
                         "ncclAllGather(cols)"));
@@ -895,7 +900,7 @@ mpj_status mg_eig(bool mixed, const double *A, int64_t n, int64_t lda, double *L
     Group g;
     g.st = user;
     g.h = h_pin;
-    const bool use_nccl = nccl_id != nullptr && nranks > 1;
+    const bool use_nccl = nccl_id != nullptr;   // a one-rank communicator runs the same NCCL calls
     g.G = use_nccl ? nranks : std::max(1, emulate);
     g.nlocal = use_nccl ? 1 : g.G;
     g.me = use_nccl ? rank : 0;
@@ -1052,7 +1057,7 @@ mpj_status mg_eig(bool mixed, const double *A, int64_t n, int64_t lda, double *L
         // all-gather the diagonals (ncl doubles per rank) through the column gather with np = 1 row
         std::vector<double *> dloc(g.nlocal);
         for (int i = 0; i < g.nlocal; ++i) dloc[i] = (double *)g.rk[i].T32;
-        if (g.nlocal == 1 && g.G > 1) {
+        if (g.comm) {   // NCCL (one process per rank; also with a single rank)
             MPJ_TRY(nccl_ck(ncclAllGather(dloc[0], W, ncl, ncclDouble, g.comm, g.st), "ncclAllGather(diag)"));
         } else {
             for (int i = 0; i < g.nlocal; ++i)

@@ -29,6 +29,7 @@ import pytest
 
 import workloads as W
 from conftest import OMEGA, UPSILON
+from parity_rules import svd_sweeps_match, sweeps_match
 
 torch = pytest.importorskip("torch")
 pytestmark = pytest.mark.gpu
@@ -65,18 +66,6 @@ def sgesvd_z(A):
     import scipy.linalg as sl
     _, _, Vh = sl.svd(A.astype(np.float32), full_matrices=False, lapack_driver="gesvd")
     return np.asfortranarray(Vh.T).astype(np.float32)
-
-
-def sweeps_match(sw_a, hist_a, sw_b, hist_b, tol):
-    """Reading R20: identical counts, except that they may differ by one when,
-    at the sweep where the runs part, both off-norms lie within 10x of the
-    stop tolerance (a rounding-noise-level decision)."""
-    if sw_a == sw_b:
-        return True
-    if abs(sw_a - sw_b) != 1:
-        return False
-    k = min(sw_a, sw_b)
-    return hist_a[k] <= 10 * tol and hist_b[k] <= 10 * tol
 
 
 # ------------------------------------------------------------- n = 8192 block rounds
@@ -264,32 +253,9 @@ def test_svd_shared_z_sweeps(mpj, orc, m, n, mode, zsrc):
     assert np.max(np.abs(sig - ref.sigma)) <= 1e-13 * ref.sigma[0]
     assert np.max(np.abs(sig - sig_true)) <= 1e-13 * sig_true[0]
     assert svd_sweeps_match(res, ref, A), (res.sweeps, ref.report.sweeps, list(res.report.rot_hist)[:12],
-                                           list(ref.report.rot_hist)[:12])
-
-
-def svd_sweeps_match(res, ref, A, early=2e-4):
-    """Reading R23: identical fp64 sweep counts, except that they may differ by
-    one when the decision after the sweep where the runs part was taken at a
-    threshold in BOTH runs: both off-norms within 10x of eps ||C^T C||_F
-    (rounding-noise level), or both sweeps' rotations / N within a factor 2
-    of the early-stop ratio."""
-    a, b = res.sweeps, ref.report.sweeps
-    if a == b:
-        return True
-    if abs(a - b) != 1:
-        return False
-    k = min(a, b)
-    n = A.shape[1]
-    N = n * (n - 1) / 2
-    tot = np.linalg.norm(A.T @ A)                  # ||C^T C||_F = ||A^T A||_F (C = A Q, Q orthogonal)
-    tol = 0.1 * OMEGA
-    off_g = res.report.off_hist[k] / tot           # GPU: absolute; oracle: relative
-    off_o = ref.report.off_hist[k]
-    if off_g <= 10 * tol and off_o <= 10 * tol:
-        return True
-    rg = res.report.rot_hist[k - 1] / N
-    ro = ref.report.rot_hist[k - 1] / N
-    return early / 2 <= rg <= 2 * early and early / 2 <= ro <= 2 * early
+                                           list(ref.report.rot_hist)[:12],
+                                           [x / np.linalg.norm(A.T @ A) for x in res.report.off_hist[:8]],
+                                           list(ref.report.off_hist)[:8])
 
 
 # ------------------------------------------------------------- Remark 3.1 stop rule (f3)
