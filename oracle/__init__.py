@@ -67,7 +67,7 @@ class Cfg(C.Structure):
         ("eps_factor", C.c_double), ("nu_factor", C.c_double),
         ("eps_low_factor", C.c_double), ("nu_low_factor", C.c_double),
         ("early_stop", C.c_double), ("max_sweeps", C.c_int), ("max_sweeps_low", C.c_int),
-        ("rule", C.c_int), ("b", C.c_int),
+        ("rule", C.c_int), ("b", C.c_int), ("low_solver", C.c_int),
     ]
 
 
@@ -132,6 +132,14 @@ def _declare(L):
                                 C.POINTER(Report)]
     L.orc_mp_evd_batched.restype = C.c_int
     L.orc_mp_evd_batched.argtypes = [_dp, C.c_int, C.c_int, C.POINTER(Cfg), _dp, _dp, _ip, _ip]
+    L.orc_sytrd_f32.restype = C.c_int
+    L.orc_sytrd_f32.argtypes = [_fp, C.c_int, _fp, _fp, _fp]
+    L.orc_orgtr_f32.restype = None
+    L.orc_orgtr_f32.argtypes = [_fp, C.c_int, _fp, _fp]
+    L.orc_tridiag_qr_f32.restype = C.c_int
+    L.orc_tridiag_qr_f32.argtypes = [_fp, _fp, C.c_int, _fp]
+    L.orc_low_evd_symqr.restype = C.c_int
+    L.orc_low_evd_symqr.argtypes = [_dp, C.c_int, _fp, _fp, C.POINTER(Report)]
     L.orc_report_size.restype = C.c_size_t
     L.orc_cfg_size.restype = C.c_size_t
     assert L.orc_report_size() == C.sizeof(Report)
@@ -158,11 +166,16 @@ def _p(a):
     raise TypeError(a.dtype)
 
 
+LOW_SYMQR, LOW_JACOBI = 2, 1
+
+
 def default_cfg(kind: str = "eig", b: int = 32, **kw) -> Cfg:
     """The paper's settings: eps = 0.1 omega; nu = 20 omega (EVD) or
-    omega (SVD, with the 2e-4 early stop).  Low stage (reading R12): eps_low =
-    max(10, 1.25 sqrt(n)) upsilon (eps_low_factor = 0 selects the rule), nu_low
-    = 20 upsilon (EVD) / upsilon (SVD)."""
+    omega (SVD, with the 2e-4 early stop).  EVD step 1 (reading R12'):
+    low_solver 0 / LOW_SYMQR = symmetric QR in binary32, LOW_JACOBI =
+    the fp32 parallel Jacobi, whose stop rule is eps_low = max(10, 1.25
+    sqrt(n)) upsilon (eps_low_factor = 0 selects the rule), nu_low = 20
+    upsilon (EVD) / upsilon (SVD, whose low stage is always one-sided Jacobi)."""
     c = Cfg()
     c.eps_factor = 0.1
     c.nu_factor = 20.0 if kind == "eig" else 1.0
@@ -173,6 +186,7 @@ def default_cfg(kind: str = "eig", b: int = 32, **kw) -> Cfg:
     c.max_sweeps_low = 60
     c.rule = 0
     c.b = b
+    c.low_solver = 0
     for k, v in kw.items():
         setattr(c, k, v)
     return c
@@ -308,7 +322,8 @@ def sort_desc(keys):
 
 
 def low_evd(A, cfg: Cfg | None = None):
-    """Alg. 3 step 1 as read by R12 (fp32 Jacobi).  Returns (Z fp32, Report)."""
+    """Alg. 3 step 1 by the fp32 parallel Jacobi (reading R12, low_solver =
+    LOW_JACOBI).  Returns (Z fp32, Report)."""
     A = _f64(A)
     n = A.shape[0]
     cfg = cfg or default_cfg("eig")
@@ -316,6 +331,53 @@ def low_evd(A, cfg: Cfg | None = None):
     rep = Report()
     lib().orc_low_evd(_p(A), n, C.byref(cfg), _p(Z), C.byref(rep))
     return Z, rep
+
+
+def sytrd(A32):
+    """Householder tridiagonalisation in binary32 (GvL Alg. 8.3.1, LAPACK
+    reflector convention): (d, e, tau, Aout) with the reflectors v_k(1:) in
+    Aout(k+2:, k)."""
+    A = _f32(A32).copy(order="F")
+    n = A.shape[0]
+    d = np.zeros(n, dtype=np.float32)
+    e = np.zeros(max(n - 1, 1), dtype=np.float32)
+    tau = np.zeros(n, dtype=np.float32)
+    lib().orc_sytrd_f32(_p(A), n, _p(d), _p(e), _p(tau))
+    return d, e[: max(n - 1, 0)], tau, A
+
+
+def orgtr(Aout, tau):
+    """Q = H_0 ... H_{n-3} from sytrd's output (binary32)."""
+    Aout = _f32(Aout)
+    n = Aout.shape[0]
+    Q = np.zeros((n, n), dtype=np.float32, order="F")
+    lib().orc_orgtr_f32(_p(Aout), n, _p(np.ascontiguousarray(tau, dtype=np.float32)), _p(Q))
+    return Q
+
+
+def tridiag_qr(d, e, Z=None):
+    """Symmetric QR algorithm (GvL Alg. 8.3.3, Wilkinson shift) on the
+    tridiagonal (d, e) in binary32, rotations accumulated into Z (default I).
+    Returns (eigenvalues unsorted, Z, implicit QR steps or -1)."""
+    n = len(d)
+    dd = np.ascontiguousarray(d, dtype=np.float32).copy()
+    ee = np.zeros(max(n, 1), dtype=np.float32)
+    ee[: n - 1] = e
+    Z = _f32(np.eye(n, dtype=np.float32) if Z is None else Z).copy(order="F")
+    steps = lib().orc_tridiag_qr_f32(_p(dd), _p(ee), n, _p(Z))
+    return dd, Z, steps
+
+
+def low_evd_symqr(A):
+    """Alg. 3 step 1 by symmetric QR on fl32(A): (Z fp32 columns in
+    descending eigenvalue order, lam32, Report)."""
+    A = _f64(A)
+    n = A.shape[0]
+    Z = np.zeros((n, n), dtype=np.float32, order="F")
+    lam = np.zeros(n, dtype=np.float32)
+    rep = Report()
+    lib().orc_low_evd_symqr(_p(A), n, _p(Z), _p(lam), C.byref(rep))
+    return Z, lam, rep
 
 
 @dataclass

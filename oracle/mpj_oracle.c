@@ -487,6 +487,9 @@ typedef struct {
     int max_sweeps_low;     /* low stage cap (R13: 60)                             */
     int rule;               /* 0 = min rule, 1 = sqrt rule        */
     int b;                  /* ordering block size (R1)                           */
+    int low_solver;         /* EVD step 1 (R12): 0/2 = symmetric QR (Householder    */
+                            /* tridiagonalisation + implicit QR), 1 = fp32 */
+                            /* parallel Jacobi                                     */
 } orc_cfg;
 
 typedef struct {
@@ -546,6 +549,220 @@ int orc_low_evd(const double *A, int n, const orc_cfg *cfg, float *Z, orc_report
     return st;
 }
 
+/* ------------------------------------------------------------------------ */
+/* Alg. 3 step 1 as the paper states it ("[Z,~] = eig(A)  Symmetric   */
+/* QR factorization in low precision upsilon"; the paper ran LAPACK SSYEV /  */
+/* cusolverDnSsyevd), reading R12': in binary32,               */
+/*   1. Householder tridiagonalisation T = Q^T fl32(A) Q (Golub & Van Loan,  */
+/*      Alg. 8.3.1), reflectors in the LAPACK convention                     */
+/*        H = I - tau v v^T, v(0) = 1, beta = -sign(alpha) ||x||,             */
+/*        tau = (beta - alpha) / beta, v(1:) = x(1:) / (alpha - beta)          */
+/*      (H = I, tau = 0, when x(1:) = 0);                                    */
+/*   2. Q = H_0 H_1 ... H_{n-3} formed explicitly (backward accumulation);   */
+/*   3. the symmetric QR algorithm on T (GvL Alg. 8.3.3: implicit QR steps   */
+/*      with the Wilkinson shift, Alg. 8.3.2, deflation when |t_{k+1,k}| <=  */
+/*      upsilon (|t_kk| + |t_{k+1,k+1}|)), rotations accumulated Z = Q G ...; */
+/*   4. eigenvalues diag(T) sorted descending (stable), Z's columns alike.   */
+/* T is kept dense (plain and obviously the algorithm; O(n^3) per QR step    */
+/* pass is fine at oracle sizes).  Element updates are binary32 values;     */
+/* each dot product / multi-term update is accumulated in long double and    */
+/* rounded once.                                                             */
+/* ------------------------------------------------------------------------ */
+
+/* LAPACK-convention Householder vector of x (length m >= 1): returns tau,    */
+/* writes beta and v (v[0] = 1).                                             */
+static float house_f32(const float *x, int m, float *v, float *beta_out)
+{
+    const float alpha = x[0];
+    ldbl s = 0;
+    for (int i = 1; i < m; ++i) s += (ldbl)x[i] * (ldbl)x[i];
+    v[0] = 1.0f;
+    if (s == 0) {
+        for (int i = 1; i < m; ++i) v[i] = 0.0f;
+        *beta_out = alpha;
+        return 0.0f;
+    }
+    const float nrm = (float)sqrtl((ldbl)alpha * (ldbl)alpha + s);
+    const float beta = alpha >= 0 ? -nrm : nrm;
+    const float tau = (beta - alpha) / beta;
+    const float scal = alpha - beta;
+    for (int i = 1; i < m; ++i) v[i] = x[i] / scal;
+    *beta_out = beta;
+    return tau;
+}
+
+/* 1. In place on the n x n symmetric A (both triangles kept): on return      */
+/* d[k] = T_kk, e[k] = T_{k+1,k}, A(k+2:n, k) = v_k(1:), tau[k] (k < n-2).    */
+int orc_sytrd_f32(float *A, int n, float *d, float *e, float *tau)
+{
+    float *x = (float *)malloc(sizeof(float) * (n > 0 ? n : 1));
+    float *v = (float *)malloc(sizeof(float) * (n > 0 ? n : 1));
+    float *p = (float *)malloc(sizeof(float) * (n > 0 ? n : 1));
+    float *w = (float *)malloc(sizeof(float) * (n > 0 ? n : 1));
+    for (int k = 0; k + 2 < n; ++k) {
+        const int m = n - k - 1;                    /* trailing size */
+        for (int i = 0; i < m; ++i) x[i] = A[IDX(k + 1 + i, k, n)];
+        float beta;
+        const float t = house_f32(x, m, v, &beta);
+        tau[k] = t;
+        /* p = tau A22 v, K = tau/2 p^T v, w = p - K v */
+        for (int i = 0; i < m; ++i) {
+            ldbl acc = 0;
+            for (int j = 0; j < m; ++j) acc += (ldbl)A[IDX(k + 1 + i, k + 1 + j, n)] * (ldbl)v[j];
+            p[i] = (float)((ldbl)t * acc);
+        }
+        ldbl pv = 0;
+        for (int i = 0; i < m; ++i) pv += (ldbl)p[i] * (ldbl)v[i];
+        const float K = (float)((ldbl)t * pv / 2);
+        for (int i = 0; i < m; ++i) w[i] = (float)((ldbl)p[i] - (ldbl)K * (ldbl)v[i]);
+        /* A22 -= v w^T + w v^T */
+        for (int j = 0; j < m; ++j)
+            for (int i = 0; i < m; ++i) {
+                float *a = &A[IDX(k + 1 + i, k + 1 + j, n)];
+                *a = (float)((ldbl)*a - (ldbl)v[i] * (ldbl)w[j] - (ldbl)w[i] * (ldbl)v[j]);
+            }
+        A[IDX(k + 1, k, n)] = beta;
+        A[IDX(k, k + 1, n)] = beta;
+        for (int i = 1; i < m; ++i) { A[IDX(k + 1 + i, k, n)] = v[i]; A[IDX(k, k + 1 + i, n)] = 0.0f; }
+    }
+    for (int k = 0; k < n; ++k) d[k] = A[IDX(k, k, n)];
+    for (int k = 0; k + 1 < n; ++k) e[k] = A[IDX(k + 1, k, n)];
+    for (int k = n - 2; k < n; ++k) if (k >= 0) tau[k] = 0.0f;
+    free(x); free(v); free(p); free(w);
+    return 0;
+}
+
+/* 2. Q = H_0 ... H_{n-3} from orc_sytrd_f32's output (v_k below the first   */
+/* subdiagonal of column k, tau).  Backward accumulation Q <- H_k Q.         */
+void orc_orgtr_f32(const float *A, int n, const float *tau, float *Q)
+{
+    memset(Q, 0, sizeof(float) * (size_t)n * n);
+    for (int i = 0; i < n; ++i) Q[IDX(i, i, n)] = 1.0f;
+    float *v = (float *)malloc(sizeof(float) * (n > 0 ? n : 1));
+    for (int k = n - 3; k >= 0; --k) {
+        const int m = n - k - 1;
+        v[0] = 1.0f;
+        for (int i = 1; i < m; ++i) v[i] = A[IDX(k + 1 + i, k, n)];
+        for (int j = 0; j < n; ++j) {
+            ldbl acc = 0;
+            for (int i = 0; i < m; ++i) acc += (ldbl)v[i] * (ldbl)Q[IDX(k + 1 + i, j, n)];
+            const ldbl f = (ldbl)tau[k] * acc;
+            for (int i = 0; i < m; ++i) {
+                float *q = &Q[IDX(k + 1 + i, j, n)];
+                *q = (float)((ldbl)*q - f * (ldbl)v[i]);
+            }
+        }
+    }
+    free(v);
+}
+
+/* GvL Alg. 5.1.3: c, s with [c s; -s c]^T [a; b] = [r; 0]. */
+static void givens_f32(float a, float b, float *c, float *s)
+{
+    if (b == 0.0f) { *c = 1.0f; *s = 0.0f; return; }
+    if (fabsf(b) > fabsf(a)) {
+        const float t = -a / b;
+        *s = 1.0f / sqrtf(fmaf(t, t, 1.0f));
+        *c = *s * t;
+    } else {
+        const float t = -b / a;
+        *c = 1.0f / sqrtf(fmaf(t, t, 1.0f));
+        *s = *c * t;
+    }
+}
+
+/* rows (i, k) of the dense T: [r_i; r_k] <- G^T [r_i; r_k]; columns alike */
+static void rot_rows_f32(float *T, int n, int i, int k, float c, float s)
+{
+    for (int j = 0; j < n; ++j) {
+        const float x = T[IDX(i, j, n)], y = T[IDX(k, j, n)];
+        T[IDX(i, j, n)] = (float)((ldbl)c * x - (ldbl)s * y);
+        T[IDX(k, j, n)] = (float)((ldbl)s * x + (ldbl)c * y);
+    }
+}
+static void rot_cols_f32(float *M, int rows, int ld, int i, int k, float c, float s)
+{
+    for (int r = 0; r < rows; ++r) {
+        const float x = M[IDX(r, i, ld)], y = M[IDX(r, k, ld)];
+        M[IDX(r, i, ld)] = (float)((ldbl)c * x - (ldbl)s * y);
+        M[IDX(r, k, ld)] = (float)((ldbl)s * x + (ldbl)c * y);
+    }
+}
+
+/* 3. The symmetric QR algorithm (GvL Alg. 8.3.3) on the tridiagonal (d, e),  */
+/* rotations accumulated into Z (n x n, in: Q, out: Q G_1 G_2 ...).  On      */
+/* return d holds the eigenvalues (unsorted).  Returns the number of         */
+/* implicit QR steps, or -1 if 30 n steps did not converge.                  */
+int orc_tridiag_qr_f32(float *d, float *e, int n, float *Z)
+{
+    float *T = (float *)calloc((size_t)n * n, sizeof(float));
+    for (int k = 0; k < n; ++k) T[IDX(k, k, n)] = d[k];
+    for (int k = 0; k + 1 < n; ++k) { T[IDX(k + 1, k, n)] = e[k]; T[IDX(k, k + 1, n)] = e[k]; }
+    int steps = 0;
+    for (;;) {
+        /* deflation (GvL 8.3.4 with tol = upsilon) */
+        for (int k = 0; k + 1 < n; ++k)
+            if (fabsf(T[IDX(k + 1, k, n)]) <= UPSILON * (fabsf(T[IDX(k, k, n)]) + fabsf(T[IDX(k + 1, k + 1, n)]))) {
+                T[IDX(k + 1, k, n)] = 0.0f;
+                T[IDX(k, k + 1, n)] = 0.0f;
+            }
+        /* largest trailing diagonal part, then the unreduced block above it */
+        int m = n - 1;
+        while (m > 0 && T[IDX(m, m - 1, n)] == 0.0f) --m;
+        if (m == 0) break;
+        int l = m - 1;
+        while (l > 0 && T[IDX(l, l - 1, n)] != 0.0f) --l;
+        if (++steps > 30 * n) { free(T); return -1; }
+        /* one implicit QR step with Wilkinson shift on T(l:m, l:m) (GvL 8.3.2) */
+        const float tmm = T[IDX(m, m, n)], tm1 = T[IDX(m - 1, m - 1, n)], em = T[IDX(m, m - 1, n)];
+        const float dd = (tm1 - tmm) / 2.0f;
+        const float sg = dd >= 0.0f ? 1.0f : -1.0f;
+        const float mu = tmm - em * em / (dd + sg * sqrtf(fmaf(dd, dd, em * em)));
+        float x = T[IDX(l, l, n)] - mu, z = T[IDX(l + 1, l, n)];
+        for (int k = l; k < m; ++k) {
+            float c, s;
+            givens_f32(x, z, &c, &s);
+            rot_rows_f32(T, n, k, k + 1, c, s);
+            rot_cols_f32(T, n, n, k, k + 1, c, s);
+            if (k > l) {            /* the bulge the rotation was chosen to annihilate */
+                T[IDX(k + 1, k - 1, n)] = 0.0f;
+                T[IDX(k - 1, k + 1, n)] = 0.0f;
+            }
+            rot_cols_f32(Z, n, n, k, k + 1, c, s);
+            if (k + 1 < m) { x = T[IDX(k + 1, k, n)]; z = T[IDX(k + 2, k, n)]; }
+        }
+    }
+    for (int k = 0; k < n; ++k) d[k] = T[IDX(k, k, n)];
+    free(T);
+    return steps;
+}
+
+/* Step 1 by symmetric QR (steps 1-4 above) on fl32(A): Z (n x n, columns in */
+/* descending eigenvalue order), lam32 (n, may be NULL).  Returns 0, or 2 if */
+/* the QR iteration did not converge.                                        */
+int orc_low_evd_symqr(const double *A, int n, float *Z, float *lam32, orc_report *rep)
+{
+    size_t nn = (size_t)n * n;
+    float *A32 = (float *)malloc(sizeof(float) * nn);
+    for (size_t i = 0; i < nn; ++i) A32[i] = (float)A[i];
+    float *d = (float *)malloc(sizeof(float) * n), *e = (float *)malloc(sizeof(float) * n);
+    float *tau = (float *)malloc(sizeof(float) * n), *Q = (float *)malloc(sizeof(float) * nn);
+    orc_sytrd_f32(A32, n, d, e, tau);
+    orc_orgtr_f32(A32, n, tau, Q);
+    const int steps = orc_tridiag_qr_f32(d, e, n, Q);
+    double *key = (double *)malloc(sizeof(double) * n);
+    int *perm = (int *)malloc(sizeof(int) * n);
+    for (int k = 0; k < n; ++k) key[k] = d[k];
+    orc_sort_desc(key, n, perm);
+    for (int k = 0; k < n; ++k) {
+        memcpy(Z + (size_t)k * n, Q + (size_t)perm[k] * n, sizeof(float) * n);
+        if (lam32) lam32[k] = d[perm[k]];
+    }
+    if (rep) { rep->sweeps_low = 0; rep->rotations_low = steps; rep->status_low = steps < 0 ? 2 : 0; }
+    free(A32); free(d); free(e); free(tau); free(Q); free(key); free(perm);
+    return steps < 0 ? 2 : 0;
+}
+
 /* Alg. 3 end to end.  A: n x n (symmetrised internally, R14).   */
 /* Outputs lam (n, descending), V (n x n).  If Zin != NULL it is used as the */
 /* low-precision eigenvector matrix instead of the fp32 Jacobi stage (the    */
@@ -561,7 +778,8 @@ int orc_mp_evd(const double *Ain, int n, const orc_cfg *cfg, const float *Zin,
     float *Z = (float *)malloc(sizeof(float) * nn);
     orc_report r0; memset(&r0, 0, sizeof(r0));
     if (Zin) memcpy(Z, Zin, sizeof(float) * nn);
-    else orc_low_evd(A, n, cfg, Z, &r0);
+    else if (cfg->low_solver == 1) orc_low_evd(A, n, cfg, Z, &r0);
+    else orc_low_evd_symqr(A, n, Z, NULL, &r0);
     double *Zd = (double *)malloc(sizeof(double) * nn), *T = (double *)malloc(sizeof(double) * nn);
     for (size_t i = 0; i < nn; ++i) Zd[i] = (double)Z[i];
     int st = orc_mgs_f64(Zd, n, n, V, NULL);
@@ -801,11 +1019,14 @@ int orc_plain_svd(const double *A, int m, int n, const orc_cfg *cfg, double *sig
 int orc_mp_evd_batched(const double *A, int n, int batch, const orc_cfg *cfg, double *lam,
                        double *V, int *sweeps, int *sweeps_low)
 {
+    /* the batched path's low stage is the fp32 Jacobi (reading R12) */
+    orc_cfg c1 = *cfg;
+    c1.low_solver = 1;
     int worst = 0;
     _Pragma("omp parallel for schedule(dynamic,1) reduction(max:worst)")
     for (int k = 0; k < batch; ++k) {
         orc_report rep;
-        int st = orc_mp_evd(A + (size_t)k * n * n, n, cfg, NULL, lam + (size_t)k * n,
+        int st = orc_mp_evd(A + (size_t)k * n * n, n, &c1, NULL, lam + (size_t)k * n,
                             V + (size_t)k * n * n, &rep);
         if (sweeps) sweeps[k] = rep.sweeps;
         if (sweeps_low) sweeps_low[k] = rep.sweeps_low;

@@ -234,7 +234,7 @@ def test_batched_equals_loop(orc):
     lam, V, sw, swl, st = orc.mp_evd_batched(As)
     assert st == 0
     for k in range(batch):
-        one = orc.mp_evd(As[k])
+        one = orc.mp_evd(As[k], orc.default_cfg(low_solver=orc.LOW_JACOBI))
         assert np.array_equal(lam[k], one.lam) and sw[k] == one.report.sweeps
         # V[k] is the row-major image of the column-major k-th matrix
         assert np.array_equal(V[k].T, one.V)
