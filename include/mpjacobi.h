@@ -76,9 +76,22 @@ typedef struct mpj_config {
                                  1: |t_pq| <= nu sqrt(t_pp t_qq) (Remark 3.1)      */
     int variant;              /* MPJ_VARIANT_*                                             */
     int block_b;              /* ordering block size b (1 or even); 0 = auto (32)        */
+    int low_solver;           /* EVD step 1 (reading R12'): MPJ_LOW_*             */
 } mpj_config;
 
-/* Fill *cfg with the paper's EVD / SVD settings. */
+/* Low-precision eigensolver of Alg. 3 step 1 (mpjacobi_eig / _eig_z). */
+enum {
+    MPJ_LOW_AUTO = 0,         /* = MPJ_LOW_SYMQR                                          */
+    MPJ_LOW_JACOBI = 1,       /* the fp32 parallel Jacobi (the same sweep kernels on
+                                 binary32; eps_low / nu_low / max_sweeps_low apply)      */
+    MPJ_LOW_SYMQR = 2         /* "symmetric QR factorization in low precision":
+                                 binary32 Householder tridiagonalisation, the
+                                 tridiagonal's eigenpairs (bisection + twisted
+                                 factorisation, binary64), back-transformation        */
+};
+
+/* Fill *cfg with the paper's EVD / SVD settings.  The multi-GPU and
+ * batched entry points and the SVD always use a Jacobi low stage. */
 void mpj_config_default_eig(mpj_config *cfg);
 void mpj_config_default_svd(mpj_config *cfg);
 

@@ -27,6 +27,7 @@ UPSILON = 2.0 ** -24
 MPJ_OK, MPJ_ERR_INVALID, MPJ_ERR_NOCONV, MPJ_ERR_RANKDEF = 0, 1, 2, 3
 MPJ_ERR_NONFINITE, MPJ_ERR_CUDA, MPJ_ERR_NCCL, MPJ_ERR_NOMEM = 4, 5, 6, 7
 VARIANT_AUTO, VARIANT_SCALAR, VARIANT_BLOCK = 0, 1, 2
+LOW_AUTO, LOW_JACOBI, LOW_SYMQR = 0, 1, 2
 
 STATUS_NAMES = {0: "OK", 1: "INVALID", 2: "NOCONV", 3: "RANKDEF", 4: "NONFINITE", 5: "CUDA",
                 6: "NCCL", 7: "NOMEM"}
@@ -43,6 +44,7 @@ class mpj_config(C.Structure):
         ("eps_factor", C.c_double), ("nu_factor", C.c_double), ("eps_low_factor", C.c_double),
         ("nu_low_factor", C.c_double), ("early_stop_ratio", C.c_double), ("max_sweeps", C.c_int),
         ("max_sweeps_low", C.c_int), ("stop_rule", C.c_int), ("variant", C.c_int), ("block_b", C.c_int),
+        ("low_solver", C.c_int),
     ]
 
 

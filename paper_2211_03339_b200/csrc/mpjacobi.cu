@@ -464,6 +464,7 @@ static mpj_status copy2d(void *dst, int64_t ldd, const void *src, int64_t lds, i
 // ---------------------------------------------------------------------------
 struct EigPlan {
     int n, b, np, variant;
+    void *symqr_ws;
     double *Asym, *T, *V, *W;
     float *T32, *V32;
     double *red_part, *red_out;
@@ -493,6 +494,7 @@ static void carve_eig(Arena &ar, int64_t n, const mpj_config *cfg, EigPlan &p)
     p.rank = ar.take<int>(p.np);
     p.lam = ar.take<double>(p.np);
     p.orth_ws = ar.take<char>(orth_workspace(p.np));
+    p.symqr_ws = ar.take<char>(symqr_workspace(p.np));
     carve_jacobi<double>(ar, p.np, p.b, p.variant, p.j64);
     carve_jacobi<float>(ar, p.np, p.b, p.variant, p.j32);
 }
@@ -610,6 +612,11 @@ static mpj_status eig_impl(bool mixed, const double *A, int64_t n, int64_t lda, 
             MPJ_CKF(cudaMemsetAsync(p.V32, 0, (size_t)np * np * sizeof(float), cx.st));
             MPJ_TRYF(copy2d(p.V32, np, Zin, ldz, n, n, sizeof(float),
                             is_device_ptr(Zin) ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, cx.st));
+            r.status_low = MPJ_OK;
+        } else if (cfg.low_solver != MPJ_LOW_JACOBI) {
+            // "symmetric QR factorization in low precision" (reading R12')
+            launch_copy_pad<double, float>(p.Asym, np, np, np, p.T32, np, np, np, cx.st);
+            MPJ_TRYF(low_evd_symqr(p.T32, np, (int)n, p.V32, np, p.W, np, p.T, p.V, p.symqr_ws, cx.st));
             r.status_low = MPJ_OK;
         } else {
             launch_copy_pad<double, float>(p.Asym, np, np, np, p.T32, np, np, np, cx.st);
@@ -763,6 +770,7 @@ void mpj_config_default_eig(mpj_config *c)
     c->stop_rule = 0;
     c->variant = MPJ_VARIANT_AUTO;
     c->block_b = 0;
+    c->low_solver = MPJ_LOW_AUTO;
 }
 
 void mpj_config_default_svd(mpj_config *c)

@@ -63,7 +63,7 @@ def test_full_size_batched_4096x64(mpj):
     lam_h, sw, swl = lam.cpu().numpy(), res.sweeps.cpu().numpy(), res.sweeps_low.cpu().numpy()
     rng = np.random.default_rng(4096)
     for k in sorted(rng.choice(batch, 16, replace=False)):
-        ref = orc.mp_evd(As[k], orc.default_cfg("eig", b=32))
+        ref = orc.mp_evd(As[k], orc.default_cfg("eig", b=32, low_solver=orc.LOW_JACOBI))   # batched: fp32 Jacobi step 1
         assert np.max(np.abs(lam_h[k] - ref.lam)) <= 1e-13 * np.max(np.abs(ref.lam))
         assert int(sw[k]) == ref.report.sweeps and int(swl[k]) == ref.report.sweeps_low
 

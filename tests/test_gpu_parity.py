@@ -150,9 +150,9 @@ def _check_evd(A, lam, V, ref_lam, ref_sweeps, sweeps, hist=None, ref_hist=None)
                                           (256, 3, 1e6)])
 def test_eig_end_to_end(mpj, orc, n, mode, kappa):
     A, lam_true = W.example1(n, kappa, mode, W.seed_for(1, mode, kappa))
-    res = mpj.eig(dev(A))
+    res = mpj.eig(dev(A), mpj.default_config("eig", low_solver=mpj.LOW_JACOBI))   # fp32 Jacobi step 1 (R12)
     rep = res.report
-    ref = orc.mp_evd(A, orc.default_cfg("eig", b=rep.block_b))
+    ref = orc.mp_evd(A, orc.default_cfg("eig", b=rep.block_b, low_solver=orc.LOW_JACOBI))
     _check_evd(A, host(res.lam), host(res.V), ref.lam, ref.report.sweeps, res.sweeps,
                list(rep.off_hist), list(ref.report.off_hist))
     if rep.variant == mpj.VARIANT_SCALAR:
@@ -352,9 +352,9 @@ def test_fp64_apply_kernels_bit_identical(tmp_path, n):
 @pytest.mark.parametrize("n", [512, 1000])
 def test_eig_block_end_to_end(mpj, orc, n):
     A, lam_true = W.example1(n, 1e3, 4, W.seed_for(2, 4, 1e3))
-    res = mpj.eig(dev(A))
+    res = mpj.eig(dev(A), mpj.default_config("eig", low_solver=mpj.LOW_JACOBI))
     assert res.report.variant == mpj.VARIANT_BLOCK
-    ref = orc.mp_evd(A, orc.default_cfg("eig", b=32))
+    ref = orc.mp_evd(A, orc.default_cfg("eig", b=32, low_solver=orc.LOW_JACOBI))
     _check_evd(A, host(res.lam), host(res.V), ref.lam, ref.report.sweeps, res.sweeps,
                list(res.report.off_hist), list(ref.report.off_hist))
 
@@ -370,7 +370,7 @@ def test_eig_batched(mpj, orc, n, batch):
     lam, V = host(res.lam), host(res.V)
     sw, swl = host(res.sweeps), host(res.sweeps_low)
     for k in range(batch):
-        ref = orc.mp_evd(As[k], orc.default_cfg("eig", b=32))
+        ref = orc.mp_evd(As[k], orc.default_cfg("eig", b=32, low_solver=orc.LOW_JACOBI))   # batched: fp32 Jacobi step 1
         _check_evd(As[k], lam[k], V[k], ref.lam, ref.report.sweeps, int(sw[k]))
         assert int(swl[k]) == ref.report.sweeps_low
 
@@ -450,7 +450,7 @@ def test_eig_mg_emulated(mpj, orc, n, mode):
     ordering): north_star tolerances and sweep counts (R20); and G-invariance:
     G = 1, 2, 4 give the same eigenvalues to rounding."""
     A, lam_true = W.example1(n, 1e3, mode, W.seed_for(4, mode, 1e3))
-    ref = orc.mp_evd(A, orc.default_cfg("eig", b=32))
+    ref = orc.mp_evd(A, orc.default_cfg("eig", b=32, low_solver=orc.LOW_JACOBI))   # mg: fp32 Jacobi step 1
     lams = []
     for G in (1, 2, 4):
         res = mpj.eig_mg(dev(A), emulate_ranks=G)

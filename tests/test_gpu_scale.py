@@ -149,15 +149,19 @@ def test_block_rounds_boundary_enforced(mpj):
 
 # ------------------------------------------------------------- n = 2048 full Alg. 3
 @pytest.mark.slow
-def test_mp_evd_n2048_vs_oracle(mpj, orc):
+@pytest.mark.parametrize("low", ["jacobi", "symqr"])
+def test_mp_evd_n2048_vs_oracle(mpj, orc, low):
     """Alg. 3 end to end at n = 2048 (Example 1 mode 3, kappa = 1e6; 32 column
-    blocks, 31 block rounds per sweep): identical fp32 and fp64 sweep counts
-    (R20 only), |dlam| <= 1e-13 ||A||_2, off(T0) within 10%."""
+    blocks, 31 block rounds per sweep), with either step-1 solver on both
+    sides: identical fp32 sweep counts (Jacobi) and fp64 sweep counts (R20
+    only), |dlam| <= 1e-13 ||A||_2, off(T0) within 10% (Jacobi) / a factor 2
+    (symmetric QR: two algorithms for the binary32 eigenvectors)."""
     n, mode, kappa = 2048, 3, 1e6
     A, lam_true = W.example1(n, kappa, mode, W.seed_for(2, mode, kappa, 7))
-    res = mpj.eig(dev(A))
+    jac = low == "jacobi"
+    res = mpj.eig(dev(A), mpj.default_config("eig", low_solver=mpj.LOW_JACOBI if jac else mpj.LOW_SYMQR))
     rep = res.report
-    ref = orc.mp_evd(A, orc.default_cfg("eig", b=32))
+    ref = orc.mp_evd(A, orc.default_cfg("eig", b=32, low_solver=orc.LOW_JACOBI if jac else orc.LOW_SYMQR))
     lam = host(res.lam)
     nrm2 = np.abs(ref.lam).max()
     assert np.max(np.abs(lam - ref.lam)) <= 1e-13 * nrm2
@@ -169,7 +173,7 @@ def test_mp_evd_n2048_vs_oracle(mpj, orc):
     tol = 0.1 * OMEGA * np.linalg.norm(A)
     assert sweeps_match(res.sweeps, list(rep.off_hist), ref.report.sweeps, list(ref.report.off_hist), tol), \
         (res.sweeps, ref.report.sweeps)
-    assert abs(rep.off0 - ref.report.off0) <= 0.1 * ref.report.off0
+    assert abs(rep.off0 - ref.report.off0) <= (0.1 if jac else 1.0) * ref.report.off0
 
 
 def test_orth_n2048_vs_mgs(mpj, orc):
@@ -187,13 +191,19 @@ def test_orth_n2048_vs_mgs(mpj, orc):
 
 # ------------------------------------------------------------- shared Z: strict fp64-stage parity
 @pytest.mark.parametrize("n,mode,kappa,zsrc", [
-    (128, 4, 1e3, "oracle"), (256, 3, 1e6, "oracle"), (320, 5, 1e3, "ssyevd"),
+    (128, 4, 1e3, "oracle"), (256, 3, 1e6, "oracle"), (320, 5, 1e3, "ssyevd"), (200, 4, 1e3, "symqr"),
+    (448, 3, 1e6, "symqr"),
     (512, 3, 1e6, "ssyevd"), (1000, 4, 1e3, "ssyevd"), (1024, 3, 1e6, "ssyevd"),
 ])
 def test_eig_shared_z_sweeps(mpj, orc, n, mode, kappa, zsrc):
     A, _ = W.example1(n, kappa, mode, W.seed_for(1, mode, kappa, 31))
     cfg_o = orc.default_cfg("eig", b=32)
-    Z = orc.low_evd(A, cfg_o)[0] if zsrc == "oracle" else ssyevd_z(A)
+    if zsrc == "oracle":
+        Z = orc.low_evd(A, cfg_o)[0]
+    elif zsrc == "symqr":
+        Z = orc.low_evd_symqr(A)[0]
+    else:
+        Z = ssyevd_z(A)
     res = mpj.eig(dev(A), Z_in=torch.from_numpy(np.ascontiguousarray(Z.T)).cuda().T, Z_out=True)
     assert np.array_equal(host(res.Z), Z)              # the Z step 2 consumed is the one given
     assert res.report.sweeps_low == 0
@@ -224,7 +234,7 @@ def test_eig_z_out_is_the_fp32_stage(mpj, orc):
     """Z_out returns the fp32 stage's V; feeding it back reproduces the run."""
     n = 256
     A, _ = W.example1(n, 1e3, 4, 77)
-    r1 = mpj.eig(dev(A), Z_out=True)
+    r1 = mpj.eig(dev(A), mpj.default_config("eig", low_solver=mpj.LOW_JACOBI), Z_out=True)
     assert r1.report.sweeps_low > 0
     r2 = mpj.eig(dev(A), Z_in=r1.Z)
     assert r2.sweeps == r1.sweeps
@@ -264,9 +274,9 @@ def test_sqrt_rule_vs_oracle(mpj, orc, n, mode):
     """Remark 3.1: for SPD A the threshold |t_ij| <= nu sqrt(t_ii
     t_jj) (stop_rule = 1) -- GPU vs oracle with the same rule."""
     A, lam_true = W.example1(n, 1e3, mode, W.seed_for(1, mode, 1e3, 5))
-    cfg = mpj.default_config("eig", stop_rule=1)
+    cfg = mpj.default_config("eig", stop_rule=1, low_solver=mpj.LOW_JACOBI)
     res = mpj.eig(dev(A), cfg)
-    ref = orc.mp_evd(A, orc.default_cfg("eig", b=res.report.block_b, rule=1))
+    ref = orc.mp_evd(A, orc.default_cfg("eig", b=res.report.block_b, rule=1, low_solver=orc.LOW_JACOBI))
     lam = host(res.lam)
     assert np.max(np.abs(lam - ref.lam)) <= 1e-13 * np.abs(ref.lam).max()
     V = host(res.V)
