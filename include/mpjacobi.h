@@ -191,6 +191,24 @@ mpj_status mpjacobi_jacobi_f32(float *T, int64_t ldt, float *V, int64_t ldv, int
  * DEVICE, ld = n.  Returns MPJ_ERR_RANKDEF on a zero column. */
 mpj_status mpjacobi_orth(const double *Z, double *Q, int64_t n, void *stream);
 
+/* The stages of Alg. 3 step 1 by symmetric QR (reading R12'), for
+ * stage-level parity tests:
+ *   mpjacobi_sytrd: Householder tridiagonalisation in binary32 (GvL Alg.
+ *     8.3.1 blocked as LAPACK ssytrd, lower): A (n x n symmetric, lda >= n and
+ *     even, DEVICE) is overwritten with the reflectors in the LAPACK layout
+ *     (v_j(2:) below the subdiagonal of column j; H_j = I - tau_j v_j v_j^T,
+ *     v_j(1) = 1, beta = -sign(alpha) ||x||); d (n), e (n-1), tau (n) DEVICE
+ *     receive T's diagonal, subdiagonal and the reflector scalars.
+ *   mpjacobi_tridiag_eig: the eigenpairs of the symmetric tridiagonal (d, e)
+ *     (binary32 in, DEVICE) in binary64: lam (n) descending, Y (n x n, ldy)
+ *     the unit eigenvectors alike (columns' signs unspecified).  Bisection on
+ *     Sturm counts + one twisted-factorisation solve per eigenvalue; the
+ *     matrix is split where |e_i| <= omega sqrt(|d_i d_{i+1}|).  n <= 65536.
+ * Both synchronise `stream` before returning. */
+mpj_status mpjacobi_sytrd(float *A, int64_t n, int64_t lda, float *d, float *e, float *tau, void *stream);
+mpj_status mpjacobi_tridiag_eig(const float *d, const float *e, int64_t n, double *lam, double *Y, int64_t ldy,
+                                void *stream);
+
 /* Alg. 3 step 3: T = Q^T A Q, symmetrised; A, Q, T: n x n DEVICE,
  * ld = n.  fp64 tensor-core (DMMA) GEMMs. */
 mpj_status mpjacobi_precond(const double *A, const double *Q, double *T, int64_t n, void *stream);

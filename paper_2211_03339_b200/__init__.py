@@ -98,6 +98,10 @@ def lib():
             getattr(L, nm).argtypes = [_vp, _i64, _vp, _i64, _i64, _dp, _dp, C.c_int, _i64,
                                        C.POINTER(C.c_int), C.POINTER(C.c_longlong), C.POINTER(C.c_double),
                                        _vp, cfgp]
+        L.mpjacobi_sytrd.restype = C.c_int
+        L.mpjacobi_sytrd.argtypes = [_vp, _i64, _i64, _vp, _vp, _vp, _vp]
+        L.mpjacobi_tridiag_eig.restype = C.c_int
+        L.mpjacobi_tridiag_eig.argtypes = [_vp, _vp, _i64, _vp, _vp, _i64, _vp]
         L.mpjacobi_orth.restype = C.c_int
         L.mpjacobi_orth.argtypes = [_vp, _vp, _i64, _vp]
         L.mpjacobi_precond.restype = C.c_int
@@ -136,6 +140,7 @@ EXPORTED = (
     "mpjacobi_eig_batched", "mpjacobi_last_error", "mpjacobi_launch_count",
     "mpjacobi_profile_enable", "mpjacobi_profile_reset", "mpjacobi_profile_get",
     "mpjacobi_eig_mg", "mpjacobi_nccl_unique_id", "mpjacobi_mg_plan", "mpjacobi_eig_z", "mpjacobi_svd_z",
+    "mpjacobi_sytrd", "mpjacobi_tridiag_eig",
 )
 
 
@@ -291,6 +296,33 @@ def mpjacobi_jacobi(T, V, *, tol=0.0, nu=20 * OMEGA, max_sweeps=60, max_rounds=-
     if Tc.data_ptr() != T.data_ptr():
         T.copy_(Tc)
     return JacobiResult(sw.value, rot.value, st, list(hist[: min(sw.value + 1, 64)]))
+
+
+def mpjacobi_sytrd(A32):
+    """Alg. 3 step 1, part 1: binary32 Householder tridiagonalisation
+    of a symmetric float32 CUDA matrix.  Returns (d, e, tau, Aout) with the
+    reflectors in Aout (LAPACK lower layout)."""
+    n = A32.shape[0]
+    ld = n + (n % 2)           # even leading dimension: the panel kernel reads row pairs
+    buf = torch.zeros((n, ld), dtype=torch.float32, device=A32.device)
+    buf[:, :n] = A32.T         # buf row j = column j of A (column-major with ld)
+    d = torch.empty(n, dtype=torch.float32, device=A32.device)
+    e = torch.empty(max(n - 1, 1), dtype=torch.float32, device=A32.device)
+    tau = torch.empty(n, dtype=torch.float32, device=A32.device)
+    _check(lib().mpjacobi_sytrd(_ptr(buf), n, ld, _ptr(d), _ptr(e), _ptr(tau), _stream()))
+    return d, e[: n - 1], tau, buf[:, :n].T
+
+
+def mpjacobi_tridiag_eig(d, e):
+    """Eigenpairs (binary64) of the tridiagonal (d, e) (float32 CUDA vectors):
+    (lam descending, Y column-major)."""
+    n = d.shape[0]
+    lam = torch.empty(n, dtype=torch.float64, device=d.device)
+    Y = empty_colmajor(n, n, device=d.device.type)
+    ee = e if n > 1 else torch.zeros(1, dtype=torch.float32, device=d.device)
+    _check(lib().mpjacobi_tridiag_eig(_ptr(d.contiguous()), _ptr(ee.contiguous()), n, _ptr(lam), _ptr(Y), n,
+                                      _stream()))
+    return lam, Y
 
 
 def mpjacobi_orth(Z):
@@ -459,5 +491,7 @@ svd = mpjacobi_svd
 eig = mpjacobi_eig
 jacobi = mpjacobi_jacobi
 orth = mpjacobi_orth
+sytrd = mpjacobi_sytrd
+tridiag_eig = mpjacobi_tridiag_eig
 precond = mpjacobi_precond
 dgemm = mpjacobi_dgemm

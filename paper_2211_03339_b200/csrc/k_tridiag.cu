@@ -428,6 +428,7 @@ __global__ void __launch_bounds__(1024) k_tri_prep(const float *__restrict__ d, 
             e2[i] = 0.0;
         }
     }
+    __syncthreads();   // e2 of the neighbouring chunk is read below
     // block starts: inclusive max-scan of "row i starts a block" positions
     int last = -1;
     for (int i = i0; i < i1; ++i) if (i == 0 || e2[i - 1] == 0.0) last = i;
@@ -637,6 +638,17 @@ __global__ void k_round_perm(const double *__restrict__ Z, int64_t ldz, int n, c
         Z32[i + (size_t)rt * ld32] = (float)Z[i + (size_t)t * ldz];
 }
 
+// Y(:, rank[t]) = Yb(:, t), lam_out[rank[t]] = lam[t]
+__global__ void k_perm_cols(const double *__restrict__ Yb, int64_t ldb, int n, const int *__restrict__ rank,
+                            const double *__restrict__ lam, double *Y, int64_t ldy, double *lam_out)
+{
+    const int t = blockIdx.y;
+    const int rt = rank[t];
+    if (blockIdx.x == 0 && threadIdx.x == 0) lam_out[rt] = lam[t];
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+        Y[i + (size_t)rt * ldy] = Yb[i + (size_t)t * ldb];
+}
+
 // tail of the reduction: the last 2 x 2 block after the last panel
 __global__ void k_tri_tail(const float *__restrict__ A, int64_t lda, int n, float *d, float *e, float *tau)
 {
@@ -720,17 +732,10 @@ size_t symqr_workspace(int64_t np)
     return carve_symqr(nullptr, np, w);
 }
 
-// Alg. 3 step 1 by "symmetric QR" (reading R12'): A32 (n x n, ld lda, binary32,
-// symmetric; overwritten by the reduction) -> Z32 (n x n, ld ldz, columns in
-// descending eigenvalue order).  Scratch: Y (fp64, >= ld_big x n, ld ld_big;
-// holds Z in fp64 on return), Dp, Dm (fp64, >= n x n each).
-mpj_status low_evd_symqr(float *A32, int64_t lda, int n, float *Z32, int64_t ldz, double *Y, int64_t ldy,
-                         double *Dp, double *Dm, void *ws, cudaStream_t st)
+// 1. binary32 tridiagonalisation of A32 (n x n, lda; overwritten by the
+// reflectors): d, e, tau in the workspace
+static mpj_status sytrd_run(float *A32, int64_t lda, int n, SymqrWs &w, int64_t np, cudaStream_t st)
 {
-    if (n < 1) return MPJ_OK;
-    const int64_t np = ((n + TB - 1) / TB) * TB;
-    SymqrWs w;
-    carve_symqr((char *)(((uintptr_t)ws + 255) & ~(uintptr_t)255), np, w);
     const int nt = (int)(np / TB);
     const int G = coop_ctas();
     const size_t smem = 4 * TB * TB * sizeof(float);
@@ -739,7 +744,6 @@ mpj_status low_evd_symqr(float *A32, int64_t lda, int n, float *Z32, int64_t ldz
     MPJ_CK(cudaMemsetAsync(w.d, 0, np * 4, st));
     MPJ_CK(cudaMemsetAsync(w.e, 0, np * 4, st));
     MPJ_CK(cudaMemsetAsync(w.tau, 0, np * 4, st));
-    // 1. tridiagonalisation, one cooperative launch per 64-column panel
     const int ncolumns = n - 2;    // reflector columns 0 .. n-3
     SytrdArgs a;
     a.A = A32; a.ld = lda; a.n = n; a.nt = nt; a.V = w.V; a.W = w.W; a.ldp = np; a.acol = w.acol;
@@ -754,15 +758,29 @@ mpj_status low_evd_symqr(float *A32, int64_t lda, int n, float *Z32, int64_t ldz
         count_launch();
     }
     k_tri_tail<<<1, 32, 0, st>>>(A32, lda, n, w.d, w.e, w.tau);
-    // 2. tridiagonal eigenpairs (binary64)
+    count_launch();
+    return MPJ_OK;
+}
+
+// 2. eigenpairs of the tridiagonal (w.d, w.e): w.lam (block order), w.rank
+// (descending rank), Y (n x n, ldy) the unit eigenvectors in block order
+static mpj_status tri_eig_run(int n, SymqrWs &w, double *Y, int64_t ldy, double *Dp, double *Dm, cudaStream_t st)
+{
     k_tri_prep<<<1, 1024, 0, st>>>(w.d, w.e, n, w.d64, w.e64, w.e2, w.bstart, w.bend, w.piv);
     k_tri_bisect<<<(n + 127) / 128, 128, 0, st>>>(w.d64, w.e64, w.e2, w.bstart, w.bend, w.piv, n, w.lam);
     MPJ_CK(cudaMemset2DAsync(Y, ldy * 8, 0, (size_t)n * 8, n, st));
     k_tri_twisted<<<(n + 127) / 128, 128, 0, st>>>(w.d64, w.e64, w.e2, w.bstart, w.bend, w.piv, w.lam, n, Dp, Dm, Y,
                                                     ldy);
     k_rank_lam<<<(n + 255) / 256, 256, 0, st>>>(w.lam, n, w.rank);
-    count_launch(5);
-    // 3. Z = H_0 ... H_{n-3} Y, panels from the last to the first
+    count_launch(4);
+    return MPJ_OK;
+}
+
+// 3. Y <- H_0 ... H_{n-3} Y (panels from the last to the first)
+static mpj_status backtransform_run(const float *A32, int64_t lda, int n, SymqrWs &w, int64_t np, double *Y,
+                                    int64_t ldy, cudaStream_t st)
+{
+    const int ncolumns = n - 2;
     for (int k0 = ((ncolumns - 1) / TB) * TB; ncolumns > 0 && k0 >= 0; k0 -= TB) {
         const int nr = std::min(TB, ncolumns - k0);
         const int r0 = k0 + 1, m = n - r0;
@@ -776,10 +794,114 @@ mpj_status low_evd_symqr(float *A32, int64_t lda, int n, float *Z32, int64_t ldz
         launch_dgemm(false, false, TB, n, TB, 1.0, w.Tp, TB, w.W1, TB, 0.0, w.W2, TB, st);
         launch_dgemm(false, false, m, n, TB, -1.0, w.Vp, np, w.W2, TB, 1.0, Y + r0, ldy, st);
     }
+    MPJ_CK(cudaGetLastError());
+    return MPJ_OK;
+}
+
+static int64_t pad64(int64_t n) { return ((n + TB - 1) / TB) * TB; }
+
+// Alg. 3 step 1 by "symmetric QR" (reading R12'): A32 (n x n, ld lda, binary32,
+// symmetric; overwritten by the reduction) -> Z32 (n x n, ld ldz, columns in
+// descending eigenvalue order).  Scratch: Y (fp64, ld ldy, >= n columns; holds
+// Z in fp64, block order, on return), Dp, Dm (fp64, >= n x n each).
+mpj_status low_evd_symqr(float *A32, int64_t lda, int n, float *Z32, int64_t ldz, double *Y, int64_t ldy,
+                         double *Dp, double *Dm, void *ws, cudaStream_t st)
+{
+    if (n < 1) return MPJ_OK;
+    const int64_t np = pad64(n);
+    SymqrWs w;
+    carve_symqr((char *)(((uintptr_t)ws + 255) & ~(uintptr_t)255), np, w);
+    MPJ_TRY(sytrd_run(A32, lda, n, w, np, st));
+    MPJ_TRY(tri_eig_run(n, w, Y, ldy, Dp, Dm, st));
+    MPJ_TRY(backtransform_run(A32, lda, n, w, np, Y, ldy, st));
     k_round_perm<<<dim3((n + 255) / 256 > 32 ? 32 : (n + 255) / 256, n), 256, 0, st>>>(Y, ldy, n, w.rank, Z32, ldz);
     count_launch();
     MPJ_CK(cudaGetLastError());
     return MPJ_OK;
 }
 
+// the stages alone, for the stage-level parity tests (C ABI below)
+mpj_status sytrd_stage(float *A32, int64_t lda, int n, float *d, float *e, float *tau, cudaStream_t st)
+{
+    const int64_t np = pad64(n);
+    void *ws = nullptr;
+    MPJ_CK(cudaMallocAsync(&ws, symqr_workspace(np), st));
+    SymqrWs w;
+    carve_symqr((char *)(((uintptr_t)ws + 255) & ~(uintptr_t)255), np, w);
+    mpj_status s = sytrd_run(A32, lda, n, w, np, st);
+    if (s == MPJ_OK) {
+        MPJ_CK(cudaMemcpyAsync(d, w.d, (size_t)n * 4, cudaMemcpyDeviceToDevice, st));
+        if (n > 1) MPJ_CK(cudaMemcpyAsync(e, w.e, (size_t)(n - 1) * 4, cudaMemcpyDeviceToDevice, st));
+        MPJ_CK(cudaMemcpyAsync(tau, w.tau, (size_t)n * 4, cudaMemcpyDeviceToDevice, st));
+    }
+    cudaFreeAsync(ws, st);
+    return s;
+}
+
+mpj_status tridiag_eig_stage(const float *d, const float *e, int n, double *lam, double *Y, int64_t ldy,
+                             cudaStream_t st)
+{
+    const int64_t np = pad64(n);
+    void *ws = nullptr;
+    double *scr = nullptr;
+    MPJ_CK(cudaMallocAsync(&ws, symqr_workspace(np), st));
+    MPJ_CK(cudaMallocAsync(&scr, (size_t)3 * n * n * sizeof(double), st));
+    SymqrWs w;
+    carve_symqr((char *)(((uintptr_t)ws + 255) & ~(uintptr_t)255), np, w);
+    MPJ_CK(cudaMemcpyAsync(w.d, d, (size_t)n * 4, cudaMemcpyDeviceToDevice, st));
+    if (n > 1) MPJ_CK(cudaMemcpyAsync(w.e, e, (size_t)(n - 1) * 4, cudaMemcpyDeviceToDevice, st));
+    double *Yb = scr, *Dp = scr + (size_t)n * n, *Dm = Dp + (size_t)n * n;
+    mpj_status s = tri_eig_run(n, w, Yb, n, Dp, Dm, st);
+    if (s == MPJ_OK) {
+        k_perm_cols<<<dim3((n + 255) / 256 > 32 ? 32 : (n + 255) / 256, n), 256, 0, st>>>(Yb, n, n, w.rank, w.lam,
+                                                                                          Y, ldy, lam);
+        count_launch();
+    }
+    cudaFreeAsync(scr, st);
+    cudaFreeAsync(ws, st);
+    MPJ_CK(cudaGetLastError());
+    return s;
+}
+
 }  // namespace mpj
+
+extern "C" {
+
+mpj_status mpjacobi_sytrd(float *A, int64_t n, int64_t lda, float *d, float *e, float *tau, void *stream)
+{
+    mpj::set_error("");
+    if (n < 1 || lda < n || !A || !d || !tau || (n > 1 && !e) || n > (1 << 20)) {
+        mpj::set_error("mpjacobi_sytrd: invalid argument");
+        return MPJ_ERR_INVALID;
+    }
+    if (lda % 2) {   // the panel kernel reads float2 pairs of rows
+        mpj::set_error("mpjacobi_sytrd: lda must be even");
+        return MPJ_ERR_INVALID;
+    }
+    cudaStream_t st = (cudaStream_t)stream;
+    mpj_status s = mpj::sytrd_stage(A, lda, (int)n, d, e, tau, st);
+    if (s == MPJ_OK && cudaStreamSynchronize(st) != cudaSuccess) {
+        mpj::set_error("mpjacobi_sytrd: CUDA error");
+        return MPJ_ERR_CUDA;
+    }
+    return s;
+}
+
+mpj_status mpjacobi_tridiag_eig(const float *d, const float *e, int64_t n, double *lam, double *Y, int64_t ldy,
+                                void *stream)
+{
+    mpj::set_error("");
+    if (n < 1 || ldy < n || !d || !lam || !Y || (n > 1 && !e) || n > (1 << 16)) {
+        mpj::set_error("mpjacobi_tridiag_eig: invalid argument");
+        return MPJ_ERR_INVALID;
+    }
+    cudaStream_t st = (cudaStream_t)stream;
+    mpj_status s = mpj::tridiag_eig_stage(d, e, (int)n, lam, Y, ldy, st);
+    if (s == MPJ_OK && cudaStreamSynchronize(st) != cudaSuccess) {
+        mpj::set_error("mpjacobi_tridiag_eig: CUDA error");
+        return MPJ_ERR_CUDA;
+    }
+    return s;
+}
+
+}  // extern "C"
