@@ -506,7 +506,8 @@ def main():
     flops_apply = nt_t * 2 * 2 * 64 ** 3 + nt_v * 2 * 64 ** 3
     bytes_apply = (nt_t * 3 + nt_v * 2) * 64 * 64 * 8   # T: read + tile + mirror; V: read + write
     kernels = {}
-    for name in ("block_apply_f64", "block_apply_f32", "block_solve_f64", "block_solve_f32",
+    for name in ("symqr_sytrd", "symqr_trieig", "symqr_backtransform",
+                 "block_apply_f64", "block_apply_f32", "block_solve_f64", "block_solve_f32",
                  "mg_apply_f64", "mg_apply_f32", "mg_solve_f64", "mg_solve_f32"):
         sec, cnt = mpj.profile_get(name)
         if cnt:

@@ -194,8 +194,8 @@ mpj_status mpjacobi_orth(const double *Z, double *Q, int64_t n, void *stream);
 /* The stages of Alg. 3 step 1 by symmetric QR (reading R12'), for
  * stage-level parity tests:
  *   mpjacobi_sytrd: Householder tridiagonalisation in binary32 (GvL Alg.
- *     8.3.1 blocked as LAPACK ssytrd, lower): A (n x n symmetric, lda >= n and
- *     even, DEVICE) is overwritten with the reflectors in the LAPACK layout
+ *     8.3.1 blocked as LAPACK ssytrd, lower): A (n x n symmetric, lda >= n a
+ *     multiple of 4, DEVICE) is overwritten with the reflectors in the LAPACK layout
  *     (v_j(2:) below the subdiagonal of column j; H_j = I - tau_j v_j v_j^T,
  *     v_j(1) = 1, beta = -sign(alpha) ||x||); d (n), e (n-1), tau (n) DEVICE
  *     receive T's diagonal, subdiagonal and the reflector scalars.

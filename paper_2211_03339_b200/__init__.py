@@ -303,7 +303,7 @@ def mpjacobi_sytrd(A32):
     of a symmetric float32 CUDA matrix.  Returns (d, e, tau, Aout) with the
     reflectors in Aout (LAPACK lower layout)."""
     n = A32.shape[0]
-    ld = n + (n % 2)           # even leading dimension: the panel kernel reads row pairs
+    ld = (n + 3) // 4 * 4      # leading dimension a multiple of 4 (16-byte TMA strides)
     buf = torch.zeros((n, ld), dtype=torch.float32, device=A32.device)
     buf[:, :n] = A32.T         # buf row j = column j of A (column-major with ld)
     d = torch.empty(n, dtype=torch.float32, device=A32.device)

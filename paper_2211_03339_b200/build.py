@@ -19,7 +19,7 @@ NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
     "-O3", "-lineinfo", "-std=c++17", "-fmad=false",
     "-Xcompiler", "-fPIC", "-shared",
-]
+] + os.environ.get("MPJ_NVCC_EXTRA", "").split()   # diagnostics builds only (e.g. -DMPJ_SYTRD_TRACE)
 
 
 def nccl_lib_dir():

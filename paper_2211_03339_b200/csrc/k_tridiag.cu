@@ -28,10 +28,14 @@
 //     panels (I - V T V^T, LAPACK slarft) on the DMMA GEMM, then Z rounded to
 //     binary32 with its columns in descending eigenvalue order.
 #include "mpj_device.cuh"
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include "mpj_internal.h"
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
+#include <mutex>
 
 namespace mpj {
 
@@ -39,7 +43,57 @@ namespace {
 
 constexpr int TB = 64;       // tile = panel width
 constexpr int NTH = 256;     // threads per CTA (8 warps)
-constexpr int RED = 2 * TB + 4;   // per-CTA partial slots: norm, quad, 2 x TB dots
+constexpr int RSLOT = 2 * TB + 2;  // per-row-block partials: [0] tail norm^2, [1 + s] panel dots (s < 2 TB)
+constexpr int NCACHE = 1;          // own row blocks whose panel V / W rows live in shared memory
+constexpr int NSTAGE = 3;          // TMA ring of 64 x 64 A22 tiles for the symmetric product
+// dynamic shared memory: [V/W cache of NCACHE row blocks | NSTAGE tile stages]
+// during the column loop; the syr2k's four 64 x 64 operand tiles after it
+constexpr size_t SYTRD_SMEM = (2 * NCACHE + NSTAGE) * TB * TB * sizeof(float) > 4 * TB * TB * sizeof(float)
+                                  ? (2 * NCACHE + NSTAGE) * TB * TB * sizeof(float)
+                                  : 4 * TB * TB * sizeof(float);
+
+// phase timestamps for tools/sytrd_trace.py (a build with -DMPJ_SYTRD_TRACE only)
+#ifdef MPJ_SYTRD_TRACE
+__device__ unsigned long long g_sytrd_trace[64 * 8 * 320];   // [column % 64][event][cta]
+__device__ int g_trace_k0 = 0;                                // the panel recorded
+__device__ __forceinline__ void sytrd_trace(int k0, int jj, int ev)
+{
+    if (threadIdx.x == 0 && k0 == g_trace_k0) {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        g_sytrd_trace[((size_t)jj * 8 + ev) * 320 + blockIdx.x] = t;
+    }
+}
+#define SYTRD_TRACE(jj, ev) sytrd_trace(a.k0, jj, ev)
+#else
+#define SYTRD_TRACE(jj, ev)
+#endif
+
+__device__ __forceinline__ unsigned su32(const void *p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mb_init(uint64_t *b, unsigned count)
+{
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(su32(b)), "r"(count));
+}
+__device__ __forceinline__ void mb_arrive_tx(uint64_t *b, unsigned bytes)
+{
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(su32(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mb_arrive(uint64_t *b)
+{
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(su32(b)) : "memory");
+}
+__device__ __forceinline__ void mb_wait(uint64_t *b, unsigned parity)
+{
+    asm volatile("{\n .reg .pred p;\n WAIT_%=:\n"
+                 " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+                 " @!p bra WAIT_%=;\n}\n" ::"r"(su32(b)), "r"(parity) : "memory");
+}
+// one 64 x 64 fp32 box of A (rows r, columns c; out-of-range parts zero-filled)
+__device__ __forceinline__ void tma_tile(float *dst, const CUtensorMap *map, int r, int c, uint64_t *bar)
+{
+    asm volatile("cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];\n"
+                 ::"r"(su32(dst)), "l"(map), "r"(r), "r"(c), "r"(su32(bar)) : "memory");
+}
 
 struct SytrdArgs {
     float *A;            // n x n, ld (lower triangle is the live matrix)
@@ -49,46 +103,80 @@ struct SytrdArgs {
     int64_t ldp;
     float *acol;         // 2 x ldp: the corrected current column (double-buffered)
     float *d, *e, *tau;
-    float *Prow, *Pcol;  // partial vectors, (nt (nt + 1) / 2) x TB each
-    float *red;          // G x RED per-CTA partials
+    float *Prow, *Pcol;  // partial vectors of A22 v, (nt (nt + 1) / 2) x TB each
+    float *rred;         // RSLOT x ntp partials per row block (slot-major; written by the owner CTA)
+    int ntp;             // nt rounded up to a multiple of 4 (float4 reductions)
+    float *qred;         // G partials of v^T A22 v (one per CTA)
     unsigned *bar;       // grid barrier (count, generation)
     int k0, ncols;       // panel start column and its number of reflector columns
 };
 
 // ---- grid barrier (all CTAs co-resident: cooperative launch) ---------------
-__device__ __forceinline__ void grid_sync(unsigned *bar)
+// bar[0] counts arrivals since the launch (zeroed before it); barrier number
+// e (0, 1, ...) is passed when it reaches (e + 1) gridDim.x.  Only thread 0
+// of each CTA arrives (release) and polls (acquire).
+__device__ __forceinline__ void grid_sync(unsigned *bar, unsigned &epoch)
 {
     __syncthreads();
+    ++epoch;
     if (threadIdx.x == 0) {
-        volatile unsigned *gen = bar + 1;
-        const unsigned g = *gen;
-        __threadfence();
-        if (atomicAdd(bar, 1u) == gridDim.x - 1) {
-            atomicExch(bar, 0u);
-            __threadfence();
-            atomicAdd(bar + 1, 1u);
-        } else {
-            while (*gen == g) {
-            }
-        }
-        __threadfence();
+        const unsigned target = epoch * gridDim.x;
+        asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(bar) : "memory");
+        unsigned v;
+        do {
+            asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(bar) : "memory");
+        } while ((int)(v - target) < 0);
     }
     __syncthreads();
 }
 
-// sum of v over the CTA (all threads call; result in every thread)
-__device__ __forceinline__ float cta_sum_f(float v, float *sh)
+// butterfly sum over a warp: every lane gets the same value (a + b == b + a)
+__device__ __forceinline__ float warp_sum(float v)
 {
     #pragma unroll
     for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-    __syncthreads();
-    if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = v;
-    __syncthreads();
-    float r = 0.f;
+    return v;
+}
+
+// the 8 sums of c[0..7] over the warp's 32 lanes (transpose-reduce, 9 shuffles):
+// the result lands in every lane whose bits (4, 3, 2) index the sum; returns
+// it, and the index through u
+__device__ __forceinline__ float warp_sum8(float (&c)[8], int &u)
+{
+    const int lane = threadIdx.x & 31;
+    const bool h4 = lane & 16;
     #pragma unroll
-    for (int i = 0; i < NTH / 32; ++i) r += sh[i];
-    __syncthreads();
+    for (int k = 0; k < 4; ++k) {
+        const float got = __shfl_xor_sync(0xffffffffu, h4 ? c[k] : c[k + 4], 16);
+        c[k] = (h4 ? c[k + 4] : c[k]) + got;
+    }
+    const bool h3 = lane & 8;
+    #pragma unroll
+    for (int k = 0; k < 2; ++k) {
+        const float got = __shfl_xor_sync(0xffffffffu, h3 ? c[k] : c[k + 2], 8);
+        c[k] = (h3 ? c[k + 2] : c[k]) + got;
+    }
+    const bool h2 = lane & 4;
+    const float got = __shfl_xor_sync(0xffffffffu, h2 ? c[0] : c[1], 4);
+    float r = (h2 ? c[1] : c[0]) + got;
+    r += __shfl_xor_sync(0xffffffffu, r, 2);
+    r += __shfl_xor_sync(0xffffffffu, r, 1);
+    u = ((lane >> 4) & 1) * 4 + ((lane >> 3) & 1) * 2 + ((lane >> 2) & 1);
     return r;
+}
+
+// sum of p[k * stride], k in [k0, k1), by one warp in a fixed order
+__device__ __forceinline__ float warp_sum_list(const float *p, int stride, int k0, int k1)
+{
+    const int lane = threadIdx.x & 31;
+    float s0 = 0.f, s1 = 0.f;
+    int k = k0 + lane;
+    for (; k + 32 < k1; k += 64) {
+        s0 += p[(size_t)k * stride];
+        s1 += p[(size_t)(k + 32) * stride];
+    }
+    if (k < k1) s0 += p[(size_t)k * stride];
+    return warp_sum(s0 + s1);
 }
 
 // lower-triangle tile list of the trailing tiles T0..nt-1, row-major
@@ -102,21 +190,38 @@ __device__ __forceinline__ void tile_of(int f, int T0, int &I, int &J)
 }
 __device__ __forceinline__ int flat_of(int I, int J, int T0) { return (I - T0) * (I - T0 + 1) / 2 + (J - T0); }
 
-// y_i of the symmetric product (after barrier 2): fixed-order sum of the
-// partial vectors of row i's tile row (one per chunk segment: the tile list is
-// cut into chunks of L tiles, a segment starts at J = T0 or at a chunk start)
-// and of its tile column (one per tile, the diagonal tile's strict lower part
-// included)
-__device__ __forceinline__ float y_of(const SytrdArgs &a, int i, int T0, int L)
+// the transposed contributions A_KI^T v_K (K >= I) to output block I are
+// stored contiguously: Pcol[(cofs(I) + K - I) * 64 + r]
+__device__ __forceinline__ int cofs(int I, int T0, int nt)
 {
-    const int I = i >> 6, r = i & 63;
-    float y = 0.f;
-    for (int J = T0; J <= I; ++J) {
-        const int f = flat_of(I, J, T0);
-        if (J == T0 || f % L == 0) y += a.Prow[(size_t)f * TB + r];
+    const int m = I - T0;
+    return m * nt - (m * T0 + m * (m - 1) / 2);
+}
+
+// part g (of `parts`) of y_i, the symmetric product at row i = I*64 + r: a
+// fixed-order sum over the partial vectors of tile row I (one per chunk
+// segment: the row-major tile list is cut into chunks of L tiles; a segment
+// starts at J = T0 or at a chunk start inside the row; part 0 takes these) and
+// of tile column I (one per tile K >= I, the diagonal tile's strict lower part
+// included; part g takes K - I = g mod parts)
+__device__ __forceinline__ float y_part(const SytrdArgs &a, int I, int r, int T0, int L, int g, int parts)
+{
+    float y0 = 0.f, y1 = 0.f, y2 = 0.f;
+    if (g == 0) {
+        const int fa = flat_of(I, T0, T0), fb = flat_of(I, I, T0);
+        y0 = a.Prow[(size_t)fa * TB + r];
+        for (int f = (fa / L + 1) * L; f <= fb; f += L) y0 += a.Prow[(size_t)f * TB + r];
     }
-    for (int K = I; K < a.nt; ++K) y += a.Pcol[(size_t)flat_of(K, I, T0) * TB + r];
-    return y;
+    const float *pc = a.Pcol + (size_t)cofs(I, T0, a.nt) * TB + r;
+    const int cnt = a.nt - I;
+    int k = g;
+    #pragma unroll 8
+    for (; k + parts < cnt; k += 2 * parts) {
+        y1 += pc[(size_t)k * TB];
+        y2 += pc[(size_t)(k + parts) * TB];
+    }
+    if (k < cnt) y1 += pc[(size_t)k * TB];
+    return y0 + (y1 + y2);
 }
 
 // v_i of column j's reflector (v_{j+1} = 1, v_i = a_i scal below, 0 above)
@@ -125,55 +230,115 @@ __device__ __forceinline__ float v_of(const float *acol, int i, int j, float sca
     return i <= j ? 0.f : (i == j + 1 ? 1.f : acol[i] * scal);
 }
 
-__global__ void __launch_bounds__(NTH, 2) k_sytrd_panel(SytrdArgs a)
+__global__ void __launch_bounds__(NTH, 2) k_sytrd_panel(SytrdArgs a, const __grid_constant__ CUtensorMap tmA)
 {
-    __shared__ float sh[NTH / 32];
-    __shared__ float dots[2 * TB];    // v^T V(:, t), v^T W(:, t) (reduced)
+    extern __shared__ __align__(128) float smem[];
+    __shared__ __align__(8) uint64_t fullb[NSTAGE], emptyb[NSTAGE];
+    __shared__ float dots[2 * TB];     // v^T V(:, t), v^T W(:, t) (reduced)
     __shared__ float rowbuf[NTH / 32][TB];
     __shared__ float wq[NTH / 32];
-    __shared__ float vj[TB], wj[TB];  // row j of the panel's V and W (t < jj)
-    __shared__ float wnext;           // row j+1 of the column just finished (recomputed)
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    __shared__ float vj[TB], wj[TB];   // row j of the panel's V and W (t < jj)
+    __shared__ float bc[4];            // broadcast scalars: tail norm^2, v^T A22 v, row j+1 of w
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, grp = tid >> 6, r64 = tid & 63;
     const int G = gridDim.x, cta = blockIdx.x;
-    const int n = a.n;
+    const int n = a.n, nt = a.nt;
     const int64_t ld = a.ld, ldp = a.ldp;
-    float *myred = a.red + (size_t)cta * RED;
+    const int nown = cta < nt ? (nt - 1 - cta) / G + 1 : 0;    // own row blocks I = cta + q G
+    // V / W rows of the first NCACHE own row blocks: cache[q] = {V[t][r], W[t][r]}
+    auto cV = [&](int q) { return smem + (size_t)q * 2 * TB * TB; };
+    auto cW = [&](int q) { return smem + (size_t)q * 2 * TB * TB + TB * TB; };
+    for (int e = tid; e < NCACHE * 2 * TB * TB; e += NTH) smem[e] = 0.f;
+    float *stage = smem + NCACHE * 2 * TB * TB;     // NSTAGE x 64 x 64 (column-major tiles)
+    if (tid == 0) {
+        for (int k = 0; k < NSTAGE; ++k) { mb_init(&fullb[k], 1); mb_init(&emptyb[k], NTH / 32); }
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    unsigned it_issued = 0, it_used = 0;           // tiles through the ring (this CTA, whole kernel)
+    unsigned epoch = 0;                             // grid barriers passed
+    // symv tile producer state (thread 0): next tile to issue and the ring index
+    // at which the current column's chunk ends
+    int pI = 0, pJ = 0, pT0 = 0;
+    unsigned it_end = 0;
+    auto issue = [&]() {
+        const unsigned k = it_issued % NSTAGE;
+        if (it_issued >= NSTAGE) mb_wait(&emptyb[k], ((it_issued / NSTAGE) - 1) & 1);
+        mb_arrive_tx(&fullb[k], TB * TB * sizeof(float));
+        tma_tile(stage + (size_t)k * TB * TB, &tmA, pI * TB, pJ * TB, &fullb[k]);
+        ++it_issued;
+        if (++pJ > pI) { ++pI; pJ = pT0; }
+    };
+    // thread 0: start streaming the chunk of column jc's symmetric product
+    // (A22 is the panel-start matrix: its tiles can be fetched before v is known)
+    auto start_column = [&](int jc) {
+        const int T0c = (jc + 1) >> 6, mtc = nt - T0c, totc = mtc * (mtc + 1) / 2;
+        const int Lc = (totc + G - 1) / G, fa = cta * Lc, fb = min(totc, fa + Lc);
+        it_end = it_issued + (fb > fa ? (unsigned)(fb - fa) : 0u);
+        if (fb > fa) {
+            tile_of(fa, T0c, pI, pJ);
+            pT0 = T0c;
+            while (it_issued < it_end && it_issued < it_used + NSTAGE) issue();
+        }
+    };
+    float pv = 0.f, pw = 0.f;        // V(j, tid), W(j, tid) of the next column (prefetched, tid < jj)
+    float anext = 0.f;               // A(i, j) of the next column at this thread's own row (group 0)
+    float wnext = 0.f;
+    __syncthreads();
 
     for (int jj = 0; jj < a.ncols; ++jj) {
         const int j = a.k0 + jj;
         float *acol = a.acol + (size_t)(jj & 1) * ldp;
+        SYTRD_TRACE(jj, 0);
         // ------------------------------------------------------------ phase A
         // a_i = A(i, j) - sum_{t < jj} V(i,t) W(j,t) + W(i,t) V(j,t), rows i >= j.
         // Row j of column jj-1 (V = 1, W = wnext) was recomputed by this CTA in
         // phase C; rows of earlier columns are at least one barrier old.
         if (tid < jj) {
             const bool last = tid == jj - 1;
-            vj[tid] = last ? 1.0f : a.V[j + (size_t)tid * ldp];
-            wj[tid] = last ? wnext : a.W[j + (size_t)tid * ldp];
+            vj[tid] = last ? 1.0f : pv;
+            wj[tid] = last ? wnext : pw;
         }
+        if (jj == 0 && tid == 0) start_column(j);
         __syncthreads();
-        float part = 0.f;
-        if (tid < TB) {
-            for (int I = cta; I * TB < n; I += G) {
-                const int i = I * TB + tid;
-                if (i < j || i >= n) continue;
-                float x = a.A[i + (size_t)j * ld];
-                for (int t = 0; t < jj; ++t) {
-                    x = __fmaf_rn(-a.V[i + (size_t)t * ldp], wj[t], x);
-                    x = __fmaf_rn(-a.W[i + (size_t)t * ldp], vj[t], x);
+        for (int q = grp; q < nown; q += NTH / 64) {
+            const int I = cta + q * G, i = I * TB + r64;
+            float x = 0.f, part = 0.f;
+            if (i >= j && i < n) {
+                x = (q == 0 && jj > 0) ? anext : a.A[i + (size_t)j * ld];                if (q < NCACHE) {
+                    const float *sv = cV(q), *sw = cW(q);
+                    #pragma unroll 8
+                    for (int t = 0; t < jj; ++t) {
+                        x = __fmaf_rn(-sv[t * TB + r64], wj[t], x);
+                        x = __fmaf_rn(-sw[t * TB + r64], vj[t], x);
+                    }
+                } else {
+                    for (int t = 0; t < jj; ++t) {
+                        x = __fmaf_rn(-a.V[i + (size_t)t * ldp], wj[t], x);
+                        x = __fmaf_rn(-a.W[i + (size_t)t * ldp], vj[t], x);
+                    }
                 }
                 acol[i] = x;
-                if (i >= j + 2) part = __fmaf_rn(x, x, part);
+                if (i >= j + 2) part = x * x;
             }
+            part = warp_sum(part);
+            // the two warps of this group: combine in a fixed order
+            if (lane == 0) rowbuf[warp][0] = part;
+            __syncwarp();
+            asm volatile("bar.sync %0, 64;" ::"r"(1 + grp));
+            if (r64 == 0) a.rred[I] = rowbuf[2 * grp][0] + rowbuf[2 * grp + 1][0];
+            asm volatile("bar.sync %0, 64;" ::"r"(1 + grp));
         }
-        part = cta_sum_f(part, sh);
-        if (tid == 0) myred[0] = part;
-        grid_sync(a.bar);
+        SYTRD_TRACE(jj, 1);
+        grid_sync(a.bar, epoch);
+        SYTRD_TRACE(jj, 2);
         // ------------------------------------------------------------ phase B
+        if (warp == 0) {
+            const float s = warp_sum_list(a.rred, 1, (j + 2) >> 6, nt);
+            if (lane == 0) bc[0] = s;
+        }
+        __syncthreads();
         float tau, scal;
         {
-            float s = 0.f;
-            for (int c = 0; c < G; ++c) s += a.red[(size_t)c * RED];    // fixed order: same in every CTA
+            const float s = bc[0];
             const float alpha = (j + 1 < n) ? acol[j + 1] : 0.f;
             float beta;
             if (s == 0.f) {
@@ -190,18 +355,32 @@ __global__ void __launch_bounds__(NTH, 2) k_sytrd_panel(SytrdArgs a)
                 a.tau[j] = tau;
             }
         }
+        // v at this thread's row of the first own row block (group 0), for phase C
+        const float vown = (nown > 0 && tid < TB) ? v_of(acol, cta * TB + tid, j, scal) : 0.f;
         // y = A22 v over the lower tiles of A22 (rows / columns >= j+1)
         const int T0 = (j + 1) >> 6;
-        const int mt = a.nt - T0;
+        const int mt = nt - T0;
         const int total = mt * (mt + 1) / 2;
         const int L = (total + G - 1) / G;
         const int f0 = cta * L, f1 = min(total, f0 + L);
-        float q = 0.f;                         // this lane's share of v^T A22 v
+        float qv = 0.f;                        // this lane's share of v^T A22 v
         float yr0 = 0.f, yr1 = 0.f;            // row partials of the current tile row (rows 2 lane, 2 lane + 1)
         if (f0 < f1) {
+            // thread 0 started the chunk's TMA stream (start_column); it keeps NSTAGE ahead
             int I, J;
             tile_of(f0, T0, I, J);
             int curI = I, segf = f0;
+            // raw acol values of the next tile (scaled / masked when consumed)
+            float acn[8], ain0, ain1;
+            auto loadv = [&](int Ii, int Jj) {
+                const int r0 = Ii * TB + 2 * lane, cb = Jj * TB + 8 * warp;
+                #pragma unroll
+                for (int u = 0; u < 8; ++u) acn[u] = acol[cb + u];
+                ain0 = acol[r0];
+                ain1 = acol[r0 + 1];
+            };
+            auto vmask = [&](int i, float raw) { return i <= j ? 0.f : (i == j + 1 ? 1.f : raw * scal); };
+            loadv(I, J);
             for (int f = f0; f <= f1; ++f) {
                 if (f == f1 || I != curI) {
                     // combine the 8 warps' row partials of tile row curI into Prow[segf]
@@ -219,25 +398,38 @@ __global__ void __launch_bounds__(NTH, 2) k_sytrd_panel(SytrdArgs a)
                     if (f == f1) break;
                     curI = I; segf = f;
                 }
-                // this warp: columns c = 8 warp + u (u < 8) of tile (I, J); lane: rows 2 lane, 2 lane + 1
                 const int r0 = I * TB + 2 * lane;
                 const int cb = J * TB + 8 * warp;
-                const float vi0 = v_of(acol, r0, j, scal), vi1 = v_of(acol, r0 + 1, j, scal);
+                float vcc[8];
+                #pragma unroll
+                for (int u = 0; u < 8; ++u) vcc[u] = vmask(cb + u, acn[u]);
+                const float vi0 = vmask(r0, ain0), vi1 = vmask(r0 + 1, ain1);
+                int In = I, Jn = J + 1;
+                if (Jn > In) { ++In; Jn = T0; }
+                if (f + 1 < f1) loadv(In, Jn);
+                // this warp: columns 8 warp + u of the staged tile, lane rows 2 lane, 2 lane + 1
+                const unsigned k = it_used % NSTAGE;
+                mb_wait(&fullb[k], (it_used / NSTAGE) & 1);
+                const float *tl = stage + (size_t)k * TB * TB;
                 float2 x[8];
                 #pragma unroll
-                for (int u = 0; u < 8; ++u) x[u] = *reinterpret_cast<const float2 *>(a.A + r0 + (size_t)(cb + u) * ld);
+                for (int u = 0; u < 8; ++u) x[u] = *reinterpret_cast<const float2 *>(tl + (8 * warp + u) * TB + 2 * lane);
+                __syncwarp();
+                if (lane == 0) mb_arrive(&emptyb[k]);
+                ++it_used;
+                if (tid == 0 && it_issued < it_end) issue();
                 float cz[8];
                 #pragma unroll
                 for (int u = 0; u < 8; ++u) {
                     const int c = cb + u;
-                    const float vc = v_of(acol, c, j, scal);
+                    const float vc = vcc[u];
                     float x0 = x[u].x, x1 = x[u].y;
                     if (I == J) {                 // diagonal tile: the lower triangle r >= c only
                         const float y0 = r0 >= c ? x0 : 0.f, y1 = r0 + 1 >= c ? x1 : 0.f;
                         yr0 = __fmaf_rn(y0, vc, yr0);
                         yr1 = __fmaf_rn(y1, vc, yr1);
-                        if (r0 == c) q = __fmaf_rn(y0 * vc, vc, q);          // A_cc v_c^2
-                        if (r0 + 1 == c) q = __fmaf_rn(y1 * vc, vc, q);
+                        if (r0 == c) qv = __fmaf_rn(y0 * vc, vc, qv);        // A_cc v_c^2
+                        if (r0 + 1 == c) qv = __fmaf_rn(y1 * vc, vc, qv);
                         x0 = r0 > c ? x0 : 0.f;                              // strict lower part transposed
                         x1 = r0 + 1 > c ? x1 : 0.f;
                     } else {
@@ -268,88 +460,198 @@ __global__ void __launch_bounds__(NTH, 2) k_sytrd_panel(SytrdArgs a)
                 }
                 if ((lane & 3) == 0) {
                     const int u = ((lane >> 4) & 1) * 4 + ((lane >> 3) & 1) * 2 + ((lane >> 2) & 1);
-                    const float vc = v_of(acol, cb + u, j, scal);
-                    q = __fmaf_rn(2.0f * cz[0], vc, q);   // A_IJ and its mirror A_JI (strict lower part if I == J)
-                    a.Pcol[(size_t)f * TB + 8 * warp + u] = cz[0];
+                    float vc = vcc[0];
+                    #pragma unroll
+                    for (int q2 = 1; q2 < 8; ++q2) vc = (u == q2) ? vcc[q2] : vc;   // no local-memory indexing
+                    qv = __fmaf_rn(2.0f * cz[0], vc, qv);   // A_IJ and its mirror (strict lower part if I == J)
+                    a.Pcol[(size_t)(cofs(J, T0, nt) + I - J) * TB + 8 * warp + u] = cz[0];
                 }
-                if (++J > I) { ++I; J = T0; }
+                I = In; J = Jn;
             }
         }
+        SYTRD_TRACE(jj, 3);
         // v^T A22 v of this CTA
-        #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) q += __shfl_xor_sync(0xffffffffu, q, o);
-        if (lane == 0) wq[warp] = q;
+        qv = warp_sum(qv);
+        if (lane == 0) wq[warp] = qv;
         __syncthreads();
         if (tid == 0) {
             float qs = 0.f;
             #pragma unroll
             for (int w = 0; w < NTH / 32; ++w) qs += wq[w];
-            myred[1] = qs;
+            a.qred[cta] = qs;
         }
-        // panel dot products v^T V(:, t), v^T W(:, t) (t < jj) over this CTA's rows
-        for (int t = warp; t < 2 * jj; t += NTH / 32) {
-            const float *col = (t < jj ? a.V + (size_t)t * ldp : a.W + (size_t)(t - jj) * ldp);
-            float acc = 0.f;
-            for (int I = cta; I * TB < n; I += G)
-                for (int r = lane; r < TB; r += 32) {
-                    const int i = I * TB + r;
-                    if (i >= j + 1 && i < n) acc = __fmaf_rn(col[i], v_of(acol, i, j, scal), acc);
+        // panel dot products v^T V(:, t), v^T W(:, t) (t < jj) over the own row blocks:
+        // warp w takes batches of 8 consecutive slots (slot sl < jj: V(:, sl), else W(:, sl - jj))
+        for (int q = 0; q < nown; ++q) {
+            const int I = cta + q * G;
+            const int i0 = I * TB + lane, i1 = i0 + 32;
+            const float v0 = i0 < n ? v_of(acol, i0, j, scal) : 0.f;
+            const float v1 = i1 < n ? v_of(acol, i1, j, scal) : 0.f;
+            for (int b8 = warp * 8; b8 < 2 * jj; b8 += NTH / 32 * 8) {
+                float c[8];
+                #pragma unroll
+                for (int k = 0; k < 8; ++k) {
+                    const int sl = b8 + k;
+                    float x0 = 0.f, x1 = 0.f;
+                    if (sl < 2 * jj) {
+                        const int t = sl < jj ? sl : sl - jj;
+                        if (q < NCACHE) {
+                            const float *cc = (sl < jj ? cV(q) : cW(q)) + t * TB;
+                            x0 = cc[lane]; x1 = cc[lane + 32];
+                        } else {
+                            const float *cc = (sl < jj ? a.V : a.W) + (size_t)t * ldp;
+                            x0 = cc[i0]; x1 = cc[i1];
+                        }
+                    }
+                    c[k] = __fmaf_rn(x1, v1, x0 * v0);
                 }
-            #pragma unroll
-            for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-            if (lane == 0) myred[2 + t] = acc;
+                int u;
+                const float acc = warp_sum8(c, u);
+                if ((lane & 3) == 0 && b8 + u < 2 * jj) a.rred[(size_t)(1 + b8 + u) * a.ntp + I] = acc;
+            }
         }
-        grid_sync(a.bar);
+        SYTRD_TRACE(jj, 4);
+        grid_sync(a.bar, epoch);
+        SYTRD_TRACE(jj, 5);
         // ------------------------------------------------------------ phase C
-        // the dots and v^T A22 v (fixed order: identical in every CTA)
-        for (int t = tid; t < 2 * jj; t += NTH) {
-            float s = 0.f;
-            for (int c = 0; c < G; ++c) s += a.red[(size_t)c * RED + 2 + t];
-            dots[t] = s;
+        // C1: every partial sum this CTA needs, loads issued together: the dots
+        // (thread (half, slot)), v^T A22 v (warp 7, extra), y of the first own
+        // row block (thread group grp takes part grp of the tile-column list);
+        // and the next column's inputs that are already final: its symv tiles
+        // (thread 0), V / W at its row j+1 (t < jj), A(:, j+1) at the own rows
+        if (jj + 1 < a.ncols) {
+            if (tid == 0) start_column(j + 1);
+            if (tid < jj) { pv = a.V[(j + 1) + (size_t)tid * ldp]; pw = a.W[(j + 1) + (size_t)tid * ldp]; }
+            if (tid < TB && nown > 0 && cta * TB + tid < n) anext = a.A[cta * TB + tid + (size_t)(j + 1) * ld];
         }
-        if (tid == 0) {
+        {
+            const int sl = tid & 127, half = tid >> 7;
             float s = 0.f;
-            for (int c = 0; c < G; ++c) s += a.red[(size_t)c * RED + 1];
-            wq[0] = s;
+            if (sl < 2 * jj) {
+                const float4 *p = reinterpret_cast<const float4 *>(a.rred + (size_t)(1 + sl) * a.ntp);
+                const int nq = a.ntp >> 2;
+                float s0 = 0.f, s1 = 0.f;
+                #pragma unroll 8
+                for (int q4 = half; q4 < nq; q4 += 2) {
+                    const float4 v4 = p[q4];
+                    s0 += v4.x + v4.y;
+                    s1 += v4.z + v4.w;
+                }
+                s = s0 + s1;
+            }
+            float yp = 0.f;
+            const int I0 = cta;                          // first own row block (if any)
+            const bool own0 = nown > 0 && (I0 + 1) * TB > j + 1;
+            if (own0) yp = y_part(a, I0, r64, T0, L, grp, NTH / 64);
+            if (warp == NTH / 32 - 1) {
+                const float4 *p = reinterpret_cast<const float4 *>(a.qred);
+                const int nq = (G + 3) >> 2;
+                float s0 = 0.f, s1 = 0.f;
+                #pragma unroll 4
+                for (int q4 = lane; q4 < nq; q4 += 32) {
+                    const float4 v4 = p[q4];
+                    s0 += v4.x + v4.y;
+                    s1 += v4.z + v4.w;
+                }
+                const float qs = warp_sum(s0 + s1);
+                if (lane == 0) bc[1] = qs;
+            }
+            if (half == 1 && sl < 2 * jj) dots[sl] = s;
+            if (own0) rowbuf[grp * 2][r64] = yp;
+            __syncthreads();
+            if (half == 0 && sl < 2 * jj) dots[sl] = s + dots[sl];
+            __syncthreads();
+        }
+        // C2: sum_t (v^T V_t)(v^T W_t) by warp 0, then v^T p = tau (v^T A22 v - 2 sum),
+        // alpha' = -(tau/2) v^T p
+        if (warp == 0) {
+            float sp = 0.f;
+            for (int t = lane; t < jj; t += 32) sp = __fmaf_rn(dots[t], dots[jj + t], sp);
+            sp = warp_sum(sp);
+            if (lane == 0) bc[3] = sp;
         }
         __syncthreads();
-        // v^T p = tau (v^T A22 v - 2 sum_t (v^T V_t)(v^T W_t)); alpha' = -(tau/2) v^T p
-        float vtp = wq[0];
-        for (int t = 0; t < jj; ++t) vtp = __fmaf_rn(-2.0f * dots[t], dots[jj + t], vtp);
-        vtp *= tau;
+        const float vtp = tau * __fmaf_rn(-2.0f, bc[3], bc[1]);
         const float alph = -0.5f * tau * vtp;
         // w_i = tau (y_i - V(i,:) (W^T v) - W(i,:) (V^T v)) + alpha' v_i  (rows i >= j+1)
-        auto w_at = [&](int i) {
-            float y = y_of(a, i, T0, L);
-            for (int t = 0; t < jj; ++t) {
-                y = __fmaf_rn(-a.V[i + (size_t)t * ldp], dots[jj + t], y);
-                y = __fmaf_rn(-a.W[i + (size_t)t * ldp], dots[t], y);
+        for (int q = 0; q < nown; ++q) {
+            const int I = cta + q * G;
+            if ((I + 1) * TB <= j + 1) continue;
+            if (q > 0) {      // (only when the grid has fewer CTAs than row blocks)
+                rowbuf[grp * 2][r64] = y_part(a, I, r64, T0, L, grp, NTH / 64);
+                __syncthreads();
             }
-            return __fmaf_rn(alph, v_of(acol, i, j, scal), tau * y);
-        };
-        if (tid < TB) {
-            for (int I = cta; I * TB < n; I += G) {
-                const int i = I * TB + tid;
-                if (i < j + 1 || i >= n) continue;
-                const float vi = v_of(acol, i, j, scal);
-                a.W[i + (size_t)jj * ldp] = w_at(i);
-                a.V[i + (size_t)jj * ldp] = vi;
-                if (i >= j + 2) a.A[i + (size_t)j * ld] = vi;     // reflector storage (LAPACK layout)
+            if (grp == 0) {
+                const int i = I * TB + r64;
+                float y = ((rowbuf[0][r64] + rowbuf[2][r64]) + rowbuf[4][r64]) + rowbuf[6][r64];
+                if (i >= j + 1 && i < n) {
+                    float y2 = 0.f;
+                    if (q < NCACHE) {
+                        const float *sv = cV(q), *sw = cW(q);
+                        #pragma unroll 8
+                        for (int t = 0; t < jj; ++t) {
+                            y = __fmaf_rn(-sv[t * TB + r64], dots[jj + t], y);
+                            y2 = __fmaf_rn(-sw[t * TB + r64], dots[t], y2);
+                        }
+                    } else {
+                        for (int t = 0; t < jj; ++t) {
+                            y = __fmaf_rn(-a.V[i + (size_t)t * ldp], dots[jj + t], y);
+                            y2 = __fmaf_rn(-a.W[i + (size_t)t * ldp], dots[t], y2);
+                        }
+                    }
+                    y += y2;
+                    const float vi = q == 0 ? vown : v_of(acol, i, j, scal);
+                    const float w = __fmaf_rn(alph, vi, tau * y);
+                    a.W[i + (size_t)jj * ldp] = w;
+                    a.V[i + (size_t)jj * ldp] = vi;
+                    if (q < NCACHE) { cW(q)[jj * TB + r64] = w; cV(q)[jj * TB + r64] = vi; }
+                    if (i >= j + 2) a.A[i + (size_t)j * ld] = vi;     // reflector storage (LAPACK layout)
+                }
             }
+            __syncthreads();
         }
-        if (tid == 0 && j + 1 < n) wnext = w_at(j + 1);         // row j+1, for the next column's phase A
+        SYTRD_TRACE(jj, 7);
+        // row j+1 of this column's w, for the next column's phase A (every CTA):
+        // warps 0-3 split the partial vectors of y_{j+1} and the correction
+        if (jj + 1 < a.ncols && j + 1 < n) {
+            const int i = j + 1, I = i >> 6, r = i & 63;
+            if (warp < 4) {
+                const int t4 = tid;          // 0..127
+                float y = 0.f;
+                const int fa = flat_of(I, T0, T0), fb = flat_of(I, I, T0);
+                if (t4 == 0) y = a.Prow[(size_t)fa * TB + r];
+                for (int f = (fa / L + 1 + t4) * L; f <= fb; f += 128 * L) y += a.Prow[(size_t)f * TB + r];
+                const float *pc = a.Pcol + (size_t)cofs(I, T0, nt) * TB + r;
+                if (t4 < nt - I) y += pc[(size_t)t4 * TB];
+                if (t4 + 128 < nt - I) y += pc[(size_t)(t4 + 128) * TB];
+                for (int k = t4 + 256; k < nt - I; k += 128) y += pc[(size_t)k * TB];
+                float corr = 0.f;
+                if (t4 < jj) corr = __fmaf_rn(pv, dots[jj + t4], pw * dots[t4]);   // V, W(j+1, t4) (prefetched)
+                y = warp_sum(y);
+                corr = warp_sum(corr);
+                if (lane == 0) { rowbuf[warp][0] = y; rowbuf[warp][1] = corr; }
+            }
+            __syncthreads();
+            if (tid == 0) {
+                const float y = (rowbuf[0][0] + rowbuf[1][0]) + (rowbuf[2][0] + rowbuf[3][0]);
+                const float corr = (rowbuf[0][1] + rowbuf[1][1]) + (rowbuf[2][1] + rowbuf[3][1]);
+                bc[2] = __fmaf_rn(alph, 1.0f, tau * (y - corr));
+            }
+            __syncthreads();
+            wnext = bc[2];
+        }
         __syncthreads();
+        SYTRD_TRACE(jj, 6);
     }
     // ------------------------------------------------------------ trailing update
     // A(s0:, s0:) -= V W^T + W V^T on the lower tiles (s0 = first row / column
     // after the panel)
-    grid_sync(a.bar);
+    grid_sync(a.bar, epoch);
     const int s0 = a.k0 + a.ncols;
     if (s0 >= n) return;
     const int T1 = s0 >> 6;
-    const int mt = a.nt - T1;
+    const int mt = nt - T1;
     const int total = mt * (mt + 1) / 2;
-    extern __shared__ __align__(16) float smem[];
     float *sVI = smem, *sWI = sVI + TB * TB, *sVJ = sWI + TB * TB, *sWJ = sVJ + TB * TB;   // [t][r]
     const int tr = (tid & 15) * 4, tc = (tid >> 4) * 4;
     const int nk = a.ncols;
@@ -658,6 +960,20 @@ __global__ void k_tri_tail(const float *__restrict__ A, int64_t lda, int n, floa
     if (n >= 2) e[n - 2] = A[(n - 1) + (size_t)(n - 2) * lda];
 }
 
+PFN_cuTensorMapEncodeTiled_v12000 tmap_encoder()
+{
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void *f = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = (PFN_cuTensorMapEncodeTiled_v12000)f;
+    });
+    return fn;
+}
+
 int coop_ctas()
 {
     static int g = 0;
@@ -665,10 +981,12 @@ int coop_ctas()
         int dev = 0, sms = 148, occ = 1;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        const size_t smem = 4 * TB * TB * sizeof(float);
+        const size_t smem = SYTRD_SMEM;
         cudaFuncSetAttribute(k_sytrd_panel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_sytrd_panel, NTH, smem);
-        g = sms * std::max(1, std::min(occ, 2));
+        int want = 2;
+        if (const char *e = getenv("MPJ_SYTRD_OCC")) want = std::max(1, atoi(e));   // A/B: CTAs per SM
+        g = sms * std::max(1, std::min(occ, want));
     }
     return g;
 }
@@ -679,7 +997,7 @@ int coop_ctas()
 // workspace and driver
 // ---------------------------------------------------------------------------
 struct SymqrWs {
-    float *V, *W, *acol, *d, *e, *tau, *Prow, *Pcol, *red;
+    float *V, *W, *acol, *d, *e, *tau, *Prow, *Pcol, *rred, *qred;
     unsigned *bar;
     double *d64, *e64, *e2, *lam, *piv, *Vp, *Gm, *Tp, *W1, *W2, *skw;
     int *bstart, *bend, *rank;
@@ -706,7 +1024,8 @@ static size_t carve_symqr(char *base, int64_t np, SymqrWs &w)
     w.tau = (float *)take(np * 4);
     w.Prow = (float *)take(ntiles * TB * 4);
     w.Pcol = (float *)take(ntiles * TB * 4);
-    w.red = (float *)take((size_t)G * RED * 4);
+    w.rred = (float *)take((size_t)RSLOT * ((nt + 3) / 4 * 4) * 4);
+    w.qred = (float *)take((size_t)(G + 4) * 4);
     w.bar = (unsigned *)take(64);
     w.d64 = (double *)take(np * 8);
     w.e64 = (double *)take(np * 8);
@@ -738,7 +1057,7 @@ static mpj_status sytrd_run(float *A32, int64_t lda, int n, SymqrWs &w, int64_t 
 {
     const int nt = (int)(np / TB);
     const int G = coop_ctas();
-    const size_t smem = 4 * TB * TB * sizeof(float);
+    const size_t smem = SYTRD_SMEM;
     MPJ_CK(cudaMemsetAsync(w.bar, 0, 64, st));
     MPJ_CK(cudaMemsetAsync(w.acol, 0, 2 * np * 4, st));
     MPJ_CK(cudaMemsetAsync(w.d, 0, np * 4, st));
@@ -747,14 +1066,36 @@ static mpj_status sytrd_run(float *A32, int64_t lda, int n, SymqrWs &w, int64_t 
     const int ncolumns = n - 2;    // reflector columns 0 .. n-3
     SytrdArgs a;
     a.A = A32; a.ld = lda; a.n = n; a.nt = nt; a.V = w.V; a.W = w.W; a.ldp = np; a.acol = w.acol;
-    a.d = w.d; a.e = w.e; a.tau = w.tau; a.Prow = w.Prow; a.Pcol = w.Pcol; a.red = w.red; a.bar = w.bar;
+    a.d = w.d; a.e = w.e; a.tau = w.tau; a.Prow = w.Prow; a.Pcol = w.Pcol; a.rred = w.rred; a.qred = w.qred;
+    a.ntp = (nt + 3) / 4 * 4;
+    MPJ_CK(cudaMemsetAsync(w.rred, 0, (size_t)RSLOT * a.ntp * 4, st));
+    MPJ_CK(cudaMemsetAsync(w.qred, 0, (size_t)(G + 4) * 4, st));
+    a.bar = w.bar;
+    CUtensorMap tm;
+    if (ncolumns > 0) {
+        auto enc = tmap_encoder();
+        if (!enc) { set_error("sytrd: cuTensorMapEncodeTiled unavailable"); return MPJ_ERR_CUDA; }
+        cuuint64_t dims[2] = {(cuuint64_t)n, (cuuint64_t)n};      // out-of-range rows / columns read as 0
+        cuuint64_t strides[1] = {(cuuint64_t)lda * sizeof(float)};
+        cuuint32_t box[2] = {TB, TB}, es[2] = {1, 1};
+        if (enc(&tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, A32, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS) {
+            set_error("sytrd: tensor map (lda must be a multiple of 4)");
+            return MPJ_ERR_INVALID;
+        }
+    }
     for (int k0 = 0; k0 < ncolumns; k0 += TB) {
         a.k0 = k0;
         a.ncols = std::min(TB, ncolumns - k0);
         MPJ_CK(cudaMemsetAsync(w.V, 0, np * TB * 4, st));
         MPJ_CK(cudaMemsetAsync(w.W, 0, np * TB * 4, st));
-        void *args[] = {&a};
+        MPJ_CK(cudaMemsetAsync(w.bar, 0, 64, st));     // the grid barrier's arrival counter
+        void *args[] = {&a, &tm};
+        const bool prof = prof_on();
+        if (prof) prof_mark("symqr_sytrd", st, true);
         MPJ_CK(cudaLaunchCooperativeKernel((const void *)k_sytrd_panel, dim3(G), dim3(NTH), args, smem, st));
+        if (prof) prof_mark("symqr_sytrd", st, false);
         count_launch();
     }
     k_tri_tail<<<1, 32, 0, st>>>(A32, lda, n, w.d, w.e, w.tau);
@@ -811,9 +1152,13 @@ mpj_status low_evd_symqr(float *A32, int64_t lda, int n, float *Z32, int64_t ldz
     const int64_t np = pad64(n);
     SymqrWs w;
     carve_symqr((char *)(((uintptr_t)ws + 255) & ~(uintptr_t)255), np, w);
+    const bool prof = prof_on();
     MPJ_TRY(sytrd_run(A32, lda, n, w, np, st));
+    if (prof) prof_mark("symqr_trieig", st, true);
     MPJ_TRY(tri_eig_run(n, w, Y, ldy, Dp, Dm, st));
+    if (prof) { prof_mark("symqr_trieig", st, false); prof_mark("symqr_backtransform", st, true); }
     MPJ_TRY(backtransform_run(A32, lda, n, w, np, Y, ldy, st));
+    if (prof) prof_mark("symqr_backtransform", st, false);
     k_round_perm<<<dim3((n + 255) / 256 > 32 ? 32 : (n + 255) / 256, n), 256, 0, st>>>(Y, ldy, n, w.rank, Z32, ldz);
     count_launch();
     MPJ_CK(cudaGetLastError());
@@ -867,6 +1212,18 @@ mpj_status tridiag_eig_stage(const float *d, const float *e, int n, double *lam,
 
 extern "C" {
 
+#ifdef MPJ_SYTRD_TRACE
+// copy the last panel's phase timestamps (64 x 8 x 320 u64) to host memory
+int mpjacobi_debug_sytrd_trace(unsigned long long *out)
+{
+    return cudaMemcpyFromSymbol(out, mpj::g_sytrd_trace, sizeof(mpj::g_sytrd_trace)) == cudaSuccess ? 0 : 1;
+}
+int mpjacobi_debug_sytrd_trace_panel(int k0)
+{
+    return cudaMemcpyToSymbol(mpj::g_trace_k0, &k0, sizeof(int)) == cudaSuccess ? 0 : 1;
+}
+#endif
+
 mpj_status mpjacobi_sytrd(float *A, int64_t n, int64_t lda, float *d, float *e, float *tau, void *stream)
 {
     mpj::set_error("");
@@ -874,8 +1231,8 @@ mpj_status mpjacobi_sytrd(float *A, int64_t n, int64_t lda, float *d, float *e, 
         mpj::set_error("mpjacobi_sytrd: invalid argument");
         return MPJ_ERR_INVALID;
     }
-    if (lda % 2) {   // the panel kernel reads float2 pairs of rows
-        mpj::set_error("mpjacobi_sytrd: lda must be even");
+    if (lda % 4) {   // the panel kernel's TMA tensor map needs 16-byte column strides
+        mpj::set_error("mpjacobi_sytrd: lda must be a multiple of 4");
         return MPJ_ERR_INVALID;
     }
     cudaStream_t st = (cudaStream_t)stream;
