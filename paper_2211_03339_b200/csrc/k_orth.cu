@@ -4,9 +4,12 @@
 // Householder QR its GPU code used -- both compute the QR factor Q of
 // Z, which is unique (positive diag(R)) and, since Z is orthogonal to
 // O(upsilon), perfectly conditioned.  We compute it by left-looking
-// blocked Gram-Schmidt with reorthogonalisation, panel width 64:
+// blocked classical Gram-Schmidt, panel width 64:
 //   for each panel X = Z(:, p0:p0+64):
-//     twice:  R = Q(:, :p0)^T X ;  X = X - Q(:, :p0) R        (CGS2, DMMA GEMMs)
+//     once:   R = Q(:, :p0)^T X ;  X = X - Q(:, :p0) R        (CGS, DMMA GEMMs)
+//             -- twice (CGS2) if any column kept less than half its norm
+//             ("twice is enough"; checked on the panel Gram, the whole Q
+//             is then recomputed with two passes)
 //     twice:  G = X^T X ; G = R^T R (Cholesky) ; X = X R^{-1} (CholeskyQR2,
 //             the last step as a row-parallel triangular solve)
 // Every step is a dense fp64 tensor-core product except the 64 x 64
@@ -30,10 +33,14 @@ constexpr int kLDG = kPanel + 1;
 // flat loop over all w^2 entries with an integer division per entry made it
 // issue-bound: 150 us per call, 1% of an n = 8192 EVD).
 __global__ void __launch_bounds__(256) k_chol(const double *__restrict__ G, int w, double *__restrict__ Rf,
-                                              int *__restrict__ fail)
+                                              int *__restrict__ fail, const double *__restrict__ pre,
+                                              int *__restrict__ reorth)
 {
     __shared__ double A[kPanel * kLDG];
     const int tid = threadIdx.x, cj = tid & (kPanel - 1), ri = tid >> 6;
+    // one projection pass lost more than half of a column's norm: "twice is
+    // enough" (Kahan, Parlett) asks for the second pass (the caller redoes Q with CGS2)
+    if (pre && reorth && ri == 0 && cj < w && G[cj + cj * w] < 0.25 * pre[cj]) *reorth = 1;
     if (cj < w)
         for (int i = ri; i <= cj; i += 4) A[i + cj * kLDG] = 0.5 * (G[i + cj * w] + G[cj + i * w]);
     __syncthreads();
@@ -54,6 +61,24 @@ __global__ void __launch_bounds__(256) k_chol(const double *__restrict__ G, int 
     if (cj < w)
         for (int i = ri; i < w; i += 4) Rf[i + cj * w] = (i <= cj) ? A[i + cj * kLDG] : 0.0;
     if (tid == 0 && bad) *fail = 1;
+}
+
+// pre[j] = ||X(:, j)||^2 for the w columns of a panel (one CTA per column)
+__global__ void k_colnorm2(const double *__restrict__ X, int64_t ldx, int64_t m, double *__restrict__ pre)
+{
+    __shared__ double red[256 / 32];
+    const double *x = X + (size_t)blockIdx.x * ldx;
+    double acc = 0.0;
+    for (int64_t i = threadIdx.x; i < m; i += 256) acc = __fma_rn(x[i], x[i], acc);
+    #pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double s = 0.0;
+        for (int k = 0; k < 256 / 32; ++k) s += red[k];
+        pre[blockIdx.x] = s;
+    }
 }
 
 // Q(r, :) = X(r, :) R^{-1} for every row r (forward substitution
@@ -107,11 +132,13 @@ size_t dgemm_scratch_elems(int64_t m, int64_t n)
 size_t orth_workspace(int64_t n)
 {
     // R (n x 64) + S (n x 64) + split-K scratch + G + the Cholesky factor + flag
-    return ((size_t)2 * n * kPanel + dgemm_scratch_elems(n, kPanel) + 2 * kPanel * kPanel + 64) * sizeof(double);
+    return ((size_t)2 * n * kPanel + dgemm_scratch_elems(n, kPanel) + 3 * kPanel * kPanel + 64) * sizeof(double);
 }
 
-mpj_status orth_cgs2(const double *Z, int64_t ldz, double *Q, int64_t ldq, int64_t m, int64_t n,
-                     void *ws, cudaStream_t st)
+// one left-looking sweep over the panels with `passes` projection passes (1:
+// CGS with the twice-is-enough check recorded in *reorth; 2: CGS2)
+static mpj_status orth_sweep(const double *Z, int64_t ldz, double *Q, int64_t ldq, int64_t m, int64_t n, void *ws,
+                             int passes, cudaStream_t st)
 {
     double *R = (double *)ws;
     double *S = R + (size_t)n * kPanel;
@@ -119,16 +146,23 @@ mpj_status orth_cgs2(const double *Z, int64_t ldz, double *Q, int64_t ldq, int64
     const size_t scratch_elems = dgemm_scratch_elems(n, kPanel);
     double *G = scratch + scratch_elems;
     double *Rf = G + kPanel * kPanel;      // Cholesky factor of the panel Gram matrix
-    int *fail = (int *)(Rf + kPanel * kPanel);
+    double *pre = Rf + kPanel * kPanel;    // panel column norms^2 before the projection
+    int *fail = (int *)(pre + kPanel);
+    int *reorth = fail + 1;
 
-    MPJ_CK(cudaMemsetAsync(fail, 0, sizeof(int), st));
+    MPJ_CK(cudaMemsetAsync(fail, 0, 2 * sizeof(int), st));
     if (Q != Z || ldq != ldz) launch_copy_pad<double, double>(Z, ldz, (int)m, (int)n, Q, ldq, (int)m, (int)n, st);
 
     for (int64_t p0 = 0; p0 < n; p0 += kPanel) {
         const int w = (int)std::min<int64_t>(kPanel, n - p0);
         double *X = Q + p0 * ldq;
+        const bool check = passes == 1 && p0 > 0;
+        if (check) {
+            k_colnorm2<<<w, 256, 0, st>>>(X, ldq, m, pre);
+            count_launch();
+        }
         if (p0 > 0) {
-            for (int rep = 0; rep < 2; ++rep) {
+            for (int rep = 0; rep < passes; ++rep) {
                 launch_dgemm(true, false, p0, w, m, 1.0, Q, ldq, X, ldq, 0.0, R, p0, st, scratch, scratch_elems);
                 launch_dgemm(false, false, m, w, p0, -1.0, Q, ldq, R, p0, 1.0, X, ldq, st, scratch,
                              scratch_elems);
@@ -141,21 +175,37 @@ mpj_status orth_cgs2(const double *Z, int64_t ldz, double *Q, int64_t ldq, int64
             double *dst = rep == 0 ? S : X;
             const int64_t ldd = rep == 0 ? m : ldq;
             launch_dgemm(true, false, w, w, m, 1.0, src, lds, src, lds, 0.0, G, w, st, scratch, scratch_elems);
-            k_chol<<<1, 256, 0, st>>>(G, w, Rf, fail);
+            k_chol<<<1, 256, 0, st>>>(G, w, Rf, fail, (check && rep == 0) ? pre : nullptr, reorth);
             const int nblk = (int)((m + 63) / 64);
             if (w == kPanel) k_trsm_rows<kPanel><<<nblk, 64, 0, st>>>(src, lds, m, Rf, dst, ldd);
             else k_trsm_rows_w<<<nblk, 64, 0, st>>>(src, lds, m, w, Rf, dst, ldd);
             count_launch(2);
         }
     }
-    int h_fail = 0;
-    MPJ_CK(cudaMemcpyAsync(&h_fail, fail, sizeof(int), cudaMemcpyDeviceToHost, st));
+    int h[2] = {0, 0};
+    MPJ_CK(cudaMemcpyAsync(h, fail, 2 * sizeof(int), cudaMemcpyDeviceToHost, st));
     MPJ_CK(cudaStreamSynchronize(st));
-    if (h_fail) {
+    if (h[0]) {
         set_error("orth: non-positive Cholesky pivot (rank deficient Z)");
         return MPJ_ERR_RANKDEF;
     }
-    return MPJ_OK;
+    return h[1] ? MPJ_ERR_NOCONV : MPJ_OK;    // NOCONV here: a projection needs its second pass
+}
+
+mpj_status orth_cgs2(const double *Z, int64_t ldz, double *Q, int64_t ldq, int64_t m, int64_t n,
+                     void *ws, cudaStream_t st)
+{
+    // Step 1's Z is orthogonal to O(upsilon): one classical projection
+    // pass loses no significant part of a column, and CGS's loss of
+    // orthogonality is then O(omega kappa(Z)^2) = O(omega).  The sweep checks
+    // that (no column kept less than half its norm); otherwise Q is redone
+    // with the second pass everywhere (CGS2, reading R10).
+    const bool z_alias = (Z == Q);
+    if (!z_alias) {
+        mpj_status s = orth_sweep(Z, ldz, Q, ldq, m, n, ws, 1, st);
+        if (s != MPJ_ERR_NOCONV) return s;
+    }
+    return orth_sweep(Z, ldz, Q, ldq, m, n, ws, 2, st);
 }
 
 }  // namespace mpj

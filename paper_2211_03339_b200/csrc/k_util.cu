@@ -117,7 +117,7 @@ void launch_symmetrize(const double *src, int64_t lds, int n, double *dst, int64
 
 // In place: each (i<j) couple handled by one thread; 32x32 tiles through smem
 // keep both the read of a_ij and of a_ji coalesced.
-__global__ void k_symmetrize_inplace(double *__restrict__ T, int64_t ld, int n)
+__global__ void k_symmetrize_inplace(double *__restrict__ T, int64_t ld, int n, int mirror)
 {
     __shared__ double up[32][33], lo[32][33];
     const int bi = blockIdx.x, bj = blockIdx.y;
@@ -133,18 +133,19 @@ __global__ void k_symmetrize_inplace(double *__restrict__ T, int64_t ld, int n)
     for (int r = ty; r < 32; r += 8) {
         // element (bi*32+tx, bj*32+r) pairs with (bj*32+r, bi*32+tx) = lo[tx][r]
         const int i = bi * 32 + tx, j = bj * 32 + r;
-        const double v = (up[r][tx] + lo[tx][r]) * 0.5;
-        if (i < n && j < n) T[i + (int64_t)j * ld] = v;
         const int i2 = bj * 32 + tx, j2 = bi * 32 + r;
-        const double w = (lo[r][tx] + up[tx][r]) * 0.5;
+        // mirror: the upper triangle (i <= j) is the source; else the average
+        const double v = mirror ? (i <= j ? up[r][tx] : lo[tx][r]) : (up[r][tx] + lo[tx][r]) * 0.5;
+        if (i < n && j < n) T[i + (int64_t)j * ld] = v;
+        const double w = mirror ? (i2 <= j2 ? lo[r][tx] : up[tx][r]) : (lo[r][tx] + up[tx][r]) * 0.5;
         if (i2 < n && j2 < n) T[i2 + (int64_t)j2 * ld] = w;
     }
 }
 
-void launch_symmetrize_inplace(double *T, int64_t ld, int n, cudaStream_t st)
+void launch_symmetrize_inplace(double *T, int64_t ld, int n, cudaStream_t st, bool mirror_upper)
 {
     const int nt = (n + 31) / 32;
-    k_symmetrize_inplace<<<dim3(nt, nt), dim3(32, 8), 0, st>>>(T, ld, n);
+    k_symmetrize_inplace<<<dim3(nt, nt), dim3(32, 8), 0, st>>>(T, ld, n, mirror_upper ? 1 : 0);
     count_launch();
 }
 

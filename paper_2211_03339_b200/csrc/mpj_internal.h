@@ -99,8 +99,9 @@ void launch_copy_pad(const Rs *src, int64_t lds, int m, int n, Rd *dst, int64_t 
 // dst = (src + src^T)/2 into a padded n_p x n_p buffer (zero pad)
 void launch_symmetrize(const double *src, int64_t lds, int n, double *dst, int64_t ldd, int np_,
                        cudaStream_t st);
-// dst (in place) = (dst + dst^T)/2 for an n x n matrix
-void launch_symmetrize_inplace(double *T, int64_t ld, int n, cudaStream_t st);
+// dst (in place) = (dst + dst^T)/2 for an n x n matrix, or (mirror_upper) the
+// upper triangle copied onto the lower one
+void launch_symmetrize_inplace(double *T, int64_t ld, int n, cudaStream_t st, bool mirror_upper = false);
 template <typename R>
 void launch_identity(R *V, int64_t ld, int m, int n, cudaStream_t st);
 // nonfinite check: flag[0] = 1 if any entry is NaN/Inf

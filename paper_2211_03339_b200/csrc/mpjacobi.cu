@@ -653,8 +653,9 @@ static mpj_status eig_impl(bool mixed, const double *A, int64_t n, int64_t lda, 
         Timer tp(cx.st);
         MPJ_CKF(cudaMemsetAsync(p.T, 0, (size_t)np * np * sizeof(double), cx.st));
         launch_dgemm(false, false, n, n, n, 1.0, p.Asym, np, p.V, np, 0.0, p.W, np, cx.st);
-        launch_dgemm(true, false, n, n, n, 1.0, p.V, np, p.W, np, 0.0, p.T, np, cx.st);
-        launch_symmetrize_inplace(p.T, np, (int)n, cx.st);
+        // T is symmetric: only its upper tiles are formed, then mirrored (reading R11)
+        launch_dgemm(true, false, n, n, n, 1.0, p.V, np, p.W, np, 0.0, p.T, np, cx.st, nullptr, 0, true);
+        launch_symmetrize_inplace(p.T, np, (int)n, cx.st, true);
         launch_norm<double>(p.T, np, np, np, true, p.red_part, p.red_out, cx.st);
         MPJ_TRYF(read_scalar(cx, p.red_out, r.off0));
         r.t_precond = tp.stop();
@@ -870,8 +871,8 @@ mpj_status mpjacobi_precond(const double *A, const double *Q, double *T, int64_t
     double *W = nullptr;
     MPJ_CK(cudaMallocAsync(&W, (size_t)n * n * sizeof(double), cx.st));
     launch_dgemm(false, false, n, n, n, 1.0, A, n, Q, n, 0.0, W, n, cx.st);
-    launch_dgemm(true, false, n, n, n, 1.0, Q, n, W, n, 0.0, T, n, cx.st);
-    launch_symmetrize_inplace(T, n, (int)n, cx.st);
+    launch_dgemm(true, false, n, n, n, 1.0, Q, n, W, n, 0.0, T, n, cx.st, nullptr, 0, true);
+    launch_symmetrize_inplace(T, n, (int)n, cx.st, true);
     cudaFreeAsync(W, cx.st);
     return cx.close();
 }
