@@ -785,33 +785,62 @@ __device__ __forceinline__ int sturm_count(const double *__restrict__ d, const d
     return cnt;
 }
 
-// thread t: the (t - bstart)-th smallest eigenvalue of its block, by bisection
-__global__ void k_tri_bisect(const double *__restrict__ d, const double *__restrict__ e64,
-                             const double *__restrict__ e2, const int *__restrict__ bstart,
-                             const int *__restrict__ bend, const double *__restrict__ pivmin_p, int n,
-                             double *lam)
+// eigenvalue t (the (t - bstart)-th smallest of its block) by multisection:
+// the 8 lanes of a group evaluate Sturm counts at 8 interior points of the
+// current interval, which shrinks 9x per round (3.17 bits), until it holds
+// adjacent doubles.  Thread t = 8 group + lane8 of a 256-thread CTA; 32
+// eigenvalues per CTA.
+constexpr int MSEC = 8;
+__global__ void __launch_bounds__(256) k_tri_bisect(const double *__restrict__ d, const double *__restrict__ e64,
+                                                    const double *__restrict__ e2, const int *__restrict__ bstart,
+                                                    const int *__restrict__ bend,
+                                                    const double *__restrict__ pivmin_p, int n, double *lam)
 {
-    const int t = blockIdx.x * blockDim.x + threadIdx.x;
-    if (t >= n) return;
-    const int s = bstart[t], e = bend[t], k = t - s;
+    const int lane8 = threadIdx.x & (MSEC - 1);
+    const int t = blockIdx.x * (blockDim.x / MSEC) + threadIdx.x / MSEC;
+    const bool valid = t < n;
+    const int tt = valid ? t : n - 1;
+    const int s = bstart[tt], e = bend[tt], k = tt - s;
     const double pivmin = pivmin_p[0];
-    if (s == e) { lam[t] = d[s]; return; }
+    const unsigned gmask = 0xffu << (threadIdx.x & 31 & ~(MSEC - 1));
     double lo = 1e308, hi = -1e308;
-    for (int i = s; i <= e; ++i) {
+    // Gershgorin interval of the block (split over the group's lanes)
+    for (int i = s + lane8; i <= e; i += MSEC) {
         const double r = (i > s ? fabs(e64[i - 1]) : 0.0) + (i < e ? fabs(e64[i]) : 0.0);
         lo = fmin(lo, d[i] - r);
         hi = fmax(hi, d[i] + r);
     }
+    #pragma unroll
+    for (int o = MSEC / 2; o > 0; o >>= 1) {
+        lo = fmin(lo, __shfl_xor_sync(gmask, lo, o));
+        hi = fmax(hi, __shfl_xor_sync(gmask, hi, o));
+    }
     const double pad = 2.0 * kOmega * fmax(fabs(lo), fabs(hi)) + pivmin;
     lo -= pad;
     hi += pad;
-    for (int it = 0; it < 80; ++it) {
-        const double mid = 0.5 * (lo + hi);
-        if (mid <= lo || mid >= hi) break;
-        if (sturm_count(d, e2, s, e, mid, pivmin) > k) hi = mid;
-        else lo = mid;
+    if (s < e) {
+        for (int round = 0; round < 40; ++round) {
+            const double w = (hi - lo) / (MSEC + 1);
+            double x = lo + w * (lane8 + 1);
+            if (!(x > lo)) x = lo;
+            if (!(x < hi)) x = hi;
+            const int c = sturm_count(d, e2, s, e, x, pivmin);
+            // first point with more than k eigenvalues below it bounds from above
+            const unsigned ball = __ballot_sync(gmask, c > k) & gmask;
+            const int base = threadIdx.x & 31 & ~(MSEC - 1);
+            const int m_hi = ball ? __ffs(ball) - 1 - base : MSEC;       // index of that point (MSEC: hi)
+            const double nlo = m_hi > 0 ? __shfl_sync(gmask, x, base + m_hi - 1) : lo;
+            const double nhi = m_hi < MSEC ? __shfl_sync(gmask, x, base + m_hi) : hi;
+            const bool done = !(nlo < nhi) || (nlo == lo && nhi == hi);
+            lo = nlo;
+            hi = nhi;
+            if (done) break;
+            // adjacent doubles: no interior point left
+            const double mid = 0.5 * (lo + hi);
+            if (mid <= lo || mid >= hi) break;
+        }
     }
-    lam[t] = 0.5 * (lo + hi);
+    if (valid && lane8 == 0) lam[t] = s < e ? 0.5 * (lo + hi) : d[s];
 }
 
 // thread t: eigenvector of lam[t] on its block by the twisted factorisation
@@ -821,8 +850,8 @@ __global__ void k_tri_bisect(const double *__restrict__ d, const double *__restr
 __global__ void k_tri_twisted(const double *__restrict__ d, const double *__restrict__ e64,
                               const double *__restrict__ e2, const int *__restrict__ bstart,
                               const int *__restrict__ bend, const double *__restrict__ pivmin_p,
-                              const double *__restrict__ lam, int n, double *Dp, double *Dm, double *Y,
-                              int64_t ldy)
+                              const double *__restrict__ lam, int n, double *__restrict__ Dp,
+                              double *__restrict__ Dm, double *__restrict__ Y, int64_t ldy)
 {
     const int t = blockIdx.x * blockDim.x + threadIdx.x;
     if (t >= n) return;
@@ -904,30 +933,34 @@ __global__ void k_build_vp(const float *__restrict__ A, int64_t lda, int n, int 
     }
 }
 
-// Tp (64 x 64, ld 64) of H_k0 ... H_{k0+nr-1} = I - Vp Tp Vp^T (LAPACK dlarft,
-// forward, columnwise) from the Gram matrix G = Vp^T Vp (ld 64).  One CTA.
-__global__ void k_build_tp(const double *__restrict__ G, const float *__restrict__ tau, int k0, int nr, double *Tp)
+// Tp (BT x BT, ld BT) of H_k0 ... H_{k0+nr-1} = I - Vp Tp Vp^T (LAPACK dlarft,
+// forward, columnwise) from the Gram matrix G = Vp^T Vp (ld BT).  One CTA of
+// 256 threads: column t is T(0:t, t) = -tau_t T(0:t, 0:t) G(0:t, t), the
+// triangular product split over four thread groups per row.
+constexpr int BT = 2 * TB;       // back-transformation block (two sytrd panels)
+__global__ void __launch_bounds__(256) k_build_tp(const double *__restrict__ G, const float *__restrict__ tau, int k0,
+                                                  int nr, double *Tp)
 {
-    __shared__ double T[TB * TB];
-    __shared__ double z[TB];
-    const int tid = threadIdx.x;
-    for (int e = tid; e < TB * TB; e += blockDim.x) T[e] = 0.0;
+    extern __shared__ double tsm[];          // T (BT x BT+1), z (BT), part (2 x BT)
+    double *T = tsm, *z = T + BT * (BT + 1), *part = z + BT;
+    const int tid = threadIdx.x, row = tid & (BT - 1), grp = tid >> 7;   // 2 groups x 128 rows
+    for (int e = tid; e < BT * (BT + 1); e += 256) T[e] = 0.0;
     __syncthreads();
     for (int t = 0; t < nr; ++t) {
         const double ta = (double)tau[k0 + t];
-        // z = -tau_t Vp(:, 0:t)^T v_t = -tau_t G(0:t, t)
-        if (tid < t) z[tid] = -ta * G[tid + t * TB];
+        if (tid < t) z[tid] = -ta * G[tid + t * BT];
         __syncthreads();
-        // T(0:t, t) = T(0:t, 0:t) z
-        if (tid < t) {
-            double acc = 0.0;
-            for (int u = tid; u < t; ++u) acc = __fma_rn(T[tid + u * TB], z[u], acc);
-            T[tid + t * TB] = acc;
-        }
-        if (tid == 0) T[t + t * TB] = ta;
+        // T(row, t) = sum_{u = row}^{t-1} T(row, u) z(u): group grp takes u = row + grp, +2, ...
+        double acc = 0.0;
+        if (row < t)
+            for (int u = row + grp; u < t; u += 2) acc = __fma_rn(T[row + u * (BT + 1)], z[u], acc);
+        part[grp * BT + row] = acc;
+        __syncthreads();
+        if (tid < t) T[tid + t * (BT + 1)] = part[tid] + part[BT + tid];
+        if (tid == 0) T[t + t * (BT + 1)] = ta;
         __syncthreads();
     }
-    for (int e = tid; e < TB * TB; e += blockDim.x) Tp[e] = T[e];
+    for (int e = tid; e < BT * BT; e += 256) Tp[e] = T[(e & (BT - 1)) + (e / BT) * (BT + 1)];
 }
 
 // V32(:, rank[t]) = fl32(Z(:, t))
@@ -1035,12 +1068,12 @@ static size_t carve_symqr(char *base, int64_t np, SymqrWs &w)
     w.bstart = (int *)take(np * 4);
     w.bend = (int *)take(np * 4);
     w.rank = (int *)take(np * 4);
-    w.Vp = (double *)take(np * TB * 8);
-    w.Gm = (double *)take(TB * TB * 8);
-    w.Tp = (double *)take(TB * TB * 8);
-    w.W1 = (double *)take(np * TB * 8);
-    w.W2 = (double *)take(np * TB * 8);
-    w.skw_elems = (size_t)8 * TB * np;
+    w.Vp = (double *)take(np * BT * 8);
+    w.Gm = (double *)take(BT * BT * 8);
+    w.Tp = (double *)take(BT * BT * 8);
+    w.W1 = (double *)take(np * BT * 8);
+    w.W2 = (double *)take(np * BT * 8);
+    w.skw_elems = (size_t)8 * BT * np;
     w.skw = (double *)take(w.skw_elems * 8);
     return off + 256;
 }
@@ -1108,7 +1141,8 @@ static mpj_status sytrd_run(float *A32, int64_t lda, int n, SymqrWs &w, int64_t 
 static mpj_status tri_eig_run(int n, SymqrWs &w, double *Y, int64_t ldy, double *Dp, double *Dm, cudaStream_t st)
 {
     k_tri_prep<<<1, 1024, 0, st>>>(w.d, w.e, n, w.d64, w.e64, w.e2, w.bstart, w.bend, w.piv);
-    k_tri_bisect<<<(n + 127) / 128, 128, 0, st>>>(w.d64, w.e64, w.e2, w.bstart, w.bend, w.piv, n, w.lam);
+    k_tri_bisect<<<(n + 256 / MSEC - 1) / (256 / MSEC), 256, 0, st>>>(w.d64, w.e64, w.e2, w.bstart, w.bend, w.piv, n,
+                                                                     w.lam);
     MPJ_CK(cudaMemset2DAsync(Y, ldy * 8, 0, (size_t)n * 8, n, st));
     k_tri_twisted<<<(n + 127) / 128, 128, 0, st>>>(w.d64, w.e64, w.e2, w.bstart, w.bend, w.piv, w.lam, n, Dp, Dm, Y,
                                                     ldy);
@@ -1122,18 +1156,20 @@ static mpj_status backtransform_run(const float *A32, int64_t lda, int n, SymqrW
                                     int64_t ldy, cudaStream_t st)
 {
     const int ncolumns = n - 2;
-    for (int k0 = ((ncolumns - 1) / TB) * TB; ncolumns > 0 && k0 >= 0; k0 -= TB) {
-        const int nr = std::min(TB, ncolumns - k0);
+    for (int k0 = ((ncolumns - 1) / BT) * BT; ncolumns > 0 && k0 >= 0; k0 -= BT) {
+        const int nr = std::min(BT, ncolumns - k0);
         const int r0 = k0 + 1, m = n - r0;
-        k_build_vp<<<dim3((m + 255) / 256 > 32 ? 32 : (m + 255) / 256, TB), 256, 0, st>>>(A32, lda, n, k0, nr, w.Vp,
+        k_build_vp<<<dim3((m + 255) / 256 > 32 ? 32 : (m + 255) / 256, BT), 256, 0, st>>>(A32, lda, n, k0, nr, w.Vp,
                                                                                           np);
         count_launch();
-        launch_dgemm(true, false, TB, TB, m, 1.0, w.Vp, np, w.Vp, np, 0.0, w.Gm, TB, st, w.skw, w.skw_elems);
-        k_build_tp<<<1, TB, 0, st>>>(w.Gm, w.tau, k0, nr, w.Tp);
+        launch_dgemm(true, false, BT, BT, m, 1.0, w.Vp, np, w.Vp, np, 0.0, w.Gm, BT, st, w.skw, w.skw_elems);
+        const size_t tsm = ((size_t)BT * (BT + 1) + 3 * BT) * sizeof(double);
+        MPJ_CK(smem_optin((const void *)k_build_tp, tsm, 256, nullptr));
+        k_build_tp<<<1, 256, tsm, st>>>(w.Gm, w.tau, k0, nr, w.Tp);
         count_launch();
-        launch_dgemm(true, false, TB, n, m, 1.0, w.Vp, np, Y + r0, ldy, 0.0, w.W1, TB, st, w.skw, w.skw_elems);
-        launch_dgemm(false, false, TB, n, TB, 1.0, w.Tp, TB, w.W1, TB, 0.0, w.W2, TB, st);
-        launch_dgemm(false, false, m, n, TB, -1.0, w.Vp, np, w.W2, TB, 1.0, Y + r0, ldy, st);
+        launch_dgemm(true, false, BT, n, m, 1.0, w.Vp, np, Y + r0, ldy, 0.0, w.W1, BT, st, w.skw, w.skw_elems);
+        launch_dgemm(false, false, BT, n, BT, 1.0, w.Tp, BT, w.W1, BT, 0.0, w.W2, BT, st);
+        launch_dgemm(false, false, m, n, BT, -1.0, w.Vp, np, w.W2, BT, 1.0, Y + r0, ldy, st);
     }
     MPJ_CK(cudaGetLastError());
     return MPJ_OK;
