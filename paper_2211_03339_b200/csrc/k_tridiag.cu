@@ -1089,7 +1089,10 @@ size_t symqr_workspace(int64_t np)
 static mpj_status sytrd_run(float *A32, int64_t lda, int n, SymqrWs &w, int64_t np, cudaStream_t st)
 {
     const int nt = (int)(np / TB);
-    const int G = coop_ctas();
+    // a grid sized to the work: small matrices pay per-column barrier and
+    // reduction latency over every CTA, so they get ~8 tiles per CTA
+    const int tiles0 = nt * (nt + 1) / 2;
+    const int G = std::max(1, std::min(coop_ctas(), std::max(8, (tiles0 + 7) / 8)));
     const size_t smem = SYTRD_SMEM;
     MPJ_CK(cudaMemsetAsync(w.bar, 0, 64, st));
     MPJ_CK(cudaMemsetAsync(w.acol, 0, 2 * np * 4, st));
