@@ -138,46 +138,56 @@ __global__ void __launch_bounds__(NT, 2) k_batched_evd(BatchedArgs a)
     // a1 ran in k_batched_low: Z = V32 of this matrix
     const float *Zg = a.Z + mat * (size_t)TW * TW;
 
-    // a2: Q = CGS2(Z), Z = fp64(V32) (real n x n block)
-    for (int e = tid; e < TW * TW; e += NT) {
-        const int i = e & (TW - 1), j = e >> 6;
-        RB[i + j * LD] = (i < n && j < n) ? (double)Zg[i + j * TW] : 0.0;
-    }
-    __syncthreads();
+    // a2: Q = CGS(Z), Z = fp64(V32) (real n x n block).  Z is the fp32
+    // stage's V, orthogonal to O(upsilon) with unit columns: one projection
+    // pass loses no significant part of a column (reading R10); if one does
+    // (norm after the pass < 1/2, "twice is enough"), Q is redone with CGS2.
     const int warp = tid >> 5, lane = tid & 31;
     int bad = 0;
-    for (int k = 0; k < n; ++k) {
-        double *v = RB + k * LD;
-        for (int pass = 0; pass < 2 && k > 0; ++pass) {
-            for (int j = warp; j < k; j += NT / 32) {
-                const double *qj = RB + j * LD;
-                double d = __fma_rn(qj[lane], v[lane], 0.0);
-                d = __fma_rn(qj[lane + 32], v[lane + 32], d);
+    __shared__ int redo;
+    for (int npass = 1; npass <= 2; ++npass) {
+        for (int e = tid; e < TW * TW; e += NT) {
+            const int i = e & (TW - 1), j = e >> 6;
+            RB[i + j * LD] = (i < n && j < n) ? (double)Zg[i + j * TW] : 0.0;
+        }
+        if (tid == 0) redo = 0;
+        __syncthreads();
+        for (int k = 0; k < n; ++k) {
+            double *v = RB + k * LD;
+            for (int pass = 0; pass < npass && k > 0; ++pass) {
+                for (int j = warp; j < k; j += NT / 32) {
+                    const double *qj = RB + j * LD;
+                    double d = __fma_rn(qj[lane], v[lane], 0.0);
+                    d = __fma_rn(qj[lane + 32], v[lane + 32], d);
+                    #pragma unroll
+                    for (int o = 16; o > 0; o >>= 1) d += __shfl_xor_sync(0xffffffffu, d, o);
+                    if (lane == 0) coef[j] = d;
+                }
+                __syncthreads();
+                if (tid < TW) {
+                    double x = v[tid];
+                    for (int j = 0; j < k; ++j) x = __fma_rn(-coef[j], RB[tid + j * LD], x);
+                    v[tid] = x;
+                }
+                __syncthreads();
+            }
+            double d = 0.0;
+            if (tid < 32) {
+                d = __fma_rn(v[lane], v[lane], 0.0);
+                d = __fma_rn(v[lane + 32], v[lane + 32], d);
                 #pragma unroll
                 for (int o = 16; o > 0; o >>= 1) d += __shfl_xor_sync(0xffffffffu, d, o);
-                if (lane == 0) coef[j] = d;
+                if (lane == 0) coef[0] = sqrt(d);
             }
             __syncthreads();
-            if (tid < TW) {
-                double x = v[tid];
-                for (int j = 0; j < k; ++j) x = __fma_rn(-coef[j], RB[tid + j * LD], x);
-                v[tid] = x;
-            }
+            const double nrm = coef[0];
+            if (!(nrm > 0.0)) bad = 1;
+            else if (tid < TW) v[tid] = v[tid] / nrm;
+            if (npass == 1 && tid == 0 && !(nrm >= 0.5)) redo = 1;
             __syncthreads();
         }
-        double d = 0.0;
-        if (tid < 32) {
-            d = __fma_rn(v[lane], v[lane], 0.0);
-            d = __fma_rn(v[lane + 32], v[lane + 32], d);
-            #pragma unroll
-            for (int o = 16; o > 0; o >>= 1) d += __shfl_xor_sync(0xffffffffu, d, o);
-            if (lane == 0) coef[0] = sqrt(d);
-        }
-        __syncthreads();
-        const double nrm = coef[0];
-        if (!(nrm > 0.0)) bad = 1;
-        else if (tid < TW) v[tid] = v[tid] / nrm;
-        __syncthreads();
+        if (!redo) break;
+        bad = 0;
     }
 
     // a3: T = Q^T (As Q), symmetrised

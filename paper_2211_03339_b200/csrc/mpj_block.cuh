@@ -86,6 +86,22 @@ __device__ __forceinline__ unsigned inner_rounds_b(R *D, R *U, bool intra, const
         ut[i] = U[(w + 8 * i) + lane * LD];
         ub[i] = U[(w + 8 * i) + (BW + lane) * LD];
     }
+    // static tile items of this thread: e = tid + NT u -> off-diagonal tile (k, l), k < l
+    constexpr int NE = (BW + BW * (BW - 1) / 2 + NT - 1) / NT;
+    int tk[NE], tl[NE];
+    #pragma unroll
+    for (int u = 0; u < NE; ++u) {
+        const int wt = tid + NT * u - BW;
+        int ll = 1, kk = 0;
+        if (wt >= 0) {
+            ll = (int)((1.0f + sqrtf(1.0f + 8.0f * wt)) * 0.5f);
+            while (ll * (ll - 1) / 2 > wt) --ll;
+            while ((ll + 1) * ll / 2 <= wt) ++ll;
+            kk = wt - ll * (ll - 1) / 2;
+        }
+        tk[u] = kk;
+        tl[u] = ll;
+    }
     if (tid == 0) sh.nrot = 0;
     __syncthreads();
     const int nrounds = intra ? (BW - 1) + BW : BW;
@@ -124,8 +140,13 @@ __device__ __forceinline__ unsigned inner_rounds_b(R *D, R *U, bool intra, const
         }
         __syncthreads();
         // D <- J^T D J: the 32 diagonal and 496 upper pair tiles (k < l), each
-        // also stored at its mirror (what the (l, k) tile computes, bit for bit)
-        for (int e = tid; e < BW + BW * (BW - 1) / 2; e += NT) {
+        // also stored at its mirror (what the (l, k) tile computes, bit for bit).
+        // Thread tid owns items e = tid + NT u (u < NE); their (k, l) were decoded
+        // once before the rounds (tk / tl, tl < 0: diagonal tile tk)
+        #pragma unroll
+        for (int u = 0; u < NE; ++u) {
+            const int e = tid + NT * u;
+            if (e >= BW + BW * (BW - 1) / 2) break;
             if (e < BW) {
                 const int pk = sh.lp[e], qk = sh.lq[e];
                 const R apq = D[pk + qk * LD], t = pr.t[e];
@@ -135,11 +156,7 @@ __device__ __forceinline__ unsigned inner_rounds_b(R *D, R *U, bool intra, const
                 D[qk + pk * LD] = R(0);
                 continue;
             }
-            const int wt = e - BW;
-            int ll = (int)((1.0f + sqrtf(1.0f + 8.0f * wt)) * 0.5f);
-            while (ll * (ll - 1) / 2 > wt) --ll;
-            while ((ll + 1) * ll / 2 <= wt) ++ll;
-            const int kk = wt - ll * (ll - 1) / 2;
+            const int kk = tk[u], ll = tl[u];
             const int pk = sh.lp[kk], qk = sh.lq[kk], pl = sh.lp[ll], ql = sh.lq[ll];
             R x11 = D[pk + pl * LD], x21 = D[qk + pl * LD], x12 = D[pk + ql * LD], x22 = D[qk + ql * LD];
             const R sk = pr.s[kk], uk = pr.u[kk], sl = pr.s[ll], ul = pr.u[ll];
