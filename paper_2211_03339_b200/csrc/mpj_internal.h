@@ -67,7 +67,14 @@ struct DevSched {
 // ---- launchers (k_rounds.cu) ------------------------------------------------
 template <typename R>
 void launch_round_params(const R *T, int64_t ldt, const DevSched &S, int r, R nu, int rule,
-                         int2 *pq, R *t, R *s, R *u, unsigned long long *cnt, cudaStream_t st);
+                         int2 *pq, R *t, R *s, R *u, unsigned long long *cnt, cudaStream_t st,
+                         int *pos = nullptr);
+// T and V of one round in one coalesced pass (pos: row -> slot | is_q << 30,
+// written by launch_round_params)
+template <typename R>
+void launch_round_apply_fused_oop(const R *T, R *Tout, int64_t ldt, R *V, int64_t ldv, int vrows, int np,
+                                  const int2 *pq, const int *pos, const R *t, const R *s, const R *u,
+                                  cudaStream_t st);
 template <typename R>
 void launch_round_apply(R *T, int64_t ldt, const int2 *pq, const R *t, const R *s, const R *u,
                         int h, cudaStream_t st);

@@ -305,6 +305,8 @@ struct JacobiBufs {
     double *part, *off;
     int2 *bsched, *lsched;
     void *block_scratch;
+    R *Tn;          // scalar variant: the other T buffer of the fused round kernel
+    int *pos;       // scalar variant: row -> (slot, is q)
 };
 
 template <typename R>
@@ -322,6 +324,20 @@ static void carve_jacobi(Arena &ar, int np, int b, int variant, JacobiBufs<R> &j
     jb.bsched = ar.take<int2>((size_t)std::max(nb - 1, 1) * std::max(nb / 2, 1));
     jb.lsched = ar.take<int2>((size_t)std::max(b - 1, 1) * std::max(b / 2, 1));
     jb.block_scratch = (variant == MPJ_VARIANT_BLOCK) ? ar.take<char>(block_scratch_bytes<R>(np, b)) : nullptr;
+    jb.Tn = (variant == MPJ_VARIANT_SCALAR) ? ar.take<R>((size_t)np * np) : nullptr;
+    jb.pos = ar.take<int>(np);
+}
+
+// the scalar round kernels: K1 + fused K2/K3 (coalesced, out of place into the
+// other T buffer; default) or K1 + K2 + K3 in place (MPJ_SCALAR_FUSED=0, A/B)
+static bool scalar_fused()
+{
+    static int v = -1;
+    if (v < 0) {
+        const char *e = getenv("MPJ_SCALAR_FUSED");
+        v = (e && e[0] == '0') ? 0 : 1;
+    }
+    return v == 1;
 }
 
 struct JacobiOut {
@@ -397,32 +413,45 @@ static mpj_status jacobi_run(Ctx &cx, R *T, R *V, int n, int b, int variant, dou
             MPJ_TRY(block_sweep<R>(T, np, V, np, np, ds, nu, rule, jb.cnt, jb.block_scratch, st, sweeps == 1,
                                    nbr));
             rounds_done += used;
-        } else if (use_graph) {
-            if (!gexec) {
-                cudaGraph_t g;
-                const long long l0 = g_launches;
-                MPJ_CK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
-                for (int r = 0; r < hs.rounds; ++r) {
-                    launch_round_params<R>(T, np, ds, r, nu, rule, jb.pq, jb.t, jb.s, jb.u, jb.cnt, st);
-                    launch_round_apply<R>(T, np, jb.pq, jb.t, jb.s, jb.u, h, st);
-                    launch_round_apply_v<R>(V, np, np, jb.pq, jb.s, jb.u, h, st);
-                }
-                MPJ_CK(cudaStreamEndCapture(st, &g));
-                graph_kernels = g_launches - l0;
-                g_launches = l0;
-                MPJ_CK(cudaGraphInstantiate(&gexec, g, 0));
-                cudaGraphDestroy(g);
-            }
-            MPJ_CK(cudaGraphLaunch(gexec, st));
-            count_launch(graph_kernels);
-            rounds_done += hs.rounds;
         } else {
-            for (int r = 0; r < hs.rounds; ++r) {
-                if (max_rounds >= 0 && rounds_done >= max_rounds) break;
-                launch_round_params<R>(T, np, ds, r, nu, rule, jb.pq, jb.t, jb.s, jb.u, jb.cnt, st);
-                launch_round_apply<R>(T, np, jb.pq, jb.t, jb.s, jb.u, h, st);
-                launch_round_apply_v<R>(V, np, np, jb.pq, jb.s, jb.u, h, st);
-                ++rounds_done;
+            // scalar rounds; the fused kernel writes T into the other buffer, so a
+            // sweep (an odd number of rounds) ends with one copy back
+            const bool fused = scalar_fused();
+            auto sweep_rounds = [&](int r0, int r1) {
+                R *cur = T, *nxt = jb.Tn;
+                for (int r = r0; r < r1; ++r) {
+                    launch_round_params<R>(cur, np, ds, r, nu, rule, jb.pq, jb.t, jb.s, jb.u, jb.cnt, st, jb.pos);
+                    if (fused) {
+                        launch_round_apply_fused_oop<R>(cur, nxt, np, V, np, np, np, jb.pq, jb.pos, jb.t, jb.s, jb.u,
+                                                        st);
+                        std::swap(cur, nxt);
+                    } else {
+                        launch_round_apply<R>(cur, np, jb.pq, jb.t, jb.s, jb.u, h, st);
+                        launch_round_apply_v<R>(V, np, np, jb.pq, jb.s, jb.u, h, st);
+                    }
+                }
+                if (cur != T) MPJ_CK_VOID(cudaMemcpyAsync(T, cur, (size_t)np * np * sizeof(R), cudaMemcpyDeviceToDevice, st));
+            };
+            if (use_graph) {
+                if (!gexec) {
+                    cudaGraph_t g;
+                    const long long l0 = g_launches;
+                    MPJ_CK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+                    sweep_rounds(0, hs.rounds);
+                    MPJ_CK(cudaStreamEndCapture(st, &g));
+                    graph_kernels = g_launches - l0;
+                    g_launches = l0;
+                    MPJ_CK(cudaGraphInstantiate(&gexec, g, 0));
+                    cudaGraphDestroy(g);
+                }
+                MPJ_CK(cudaGraphLaunch(gexec, st));
+                count_launch(graph_kernels);
+                rounds_done += hs.rounds;
+            } else {
+                int r1 = hs.rounds;
+                if (max_rounds >= 0) r1 = (int)std::min<int64_t>(r1, max_rounds - rounds_done);
+                sweep_rounds(0, r1);
+                rounds_done += r1;
             }
         }
     }

@@ -500,3 +500,38 @@ def test_config2_n1024_mp_vs_plain(mpj, kind, mode, kappa):
         assert np.linalg.norm(A @ V - V * lam) / np.linalg.norm(A) <= n * 1e-15
     if kind == "uniform":
         assert mp.sweeps <= 4 and pl.sweeps >= 8 and mp.sweeps < pl.sweeps
+
+
+_SCALAR_SCRIPT = r"""
+import sys, numpy as np, torch
+sys.path.insert(0, sys.argv[1])
+import paper_2211_03339_b200 as mpj, workloads as W
+n = int(sys.argv[2])
+A, _ = W.example1(n, 1e3, 3, 777 + n)
+T = torch.from_numpy(A).cuda().T.contiguous().T
+V = torch.eye(n, dtype=torch.float64, device="cuda").T.contiguous().T
+cfg = mpj.default_config("eig", variant=mpj.VARIANT_SCALAR, block_b=int(sys.argv[4]))
+r = mpj.jacobi(T, V, tol=0.0, max_sweeps=2, cfg=cfg)
+np.save(sys.argv[3], np.concatenate([T.cpu().numpy().ravel(), V.cpu().numpy().ravel(), [r.rotations]]))
+"""
+
+
+@pytest.mark.parametrize("n,b", [(130, 1), (256, 32), (300, 2)])
+def test_scalar_fused_round_bit_identical(tmp_path, n, b):
+    """North_star (4)'s fused scalar round (K2 + K3 in one coalesced pass,
+    out of place; the default) against the in-place K2 + K3 pair
+    (MPJ_SCALAR_FUSED=0): two full sweeps give bit-identical T, V and rotation
+    counts (the same canonical expression per 2x2 tile)."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    script = tmp_path / "scalar.py"
+    script.write_text(_SCALAR_SCRIPT)
+    outs = {}
+    for kind in ("1", "0"):
+        env = dict(os.environ, MPJ_SCALAR_FUSED=kind)
+        out = tmp_path / f"{kind}.npy"
+        subprocess.run([sys.executable, str(script), root, str(n), str(out), str(b)], env=env, check=True, timeout=300)
+        outs[kind] = np.load(out)
+    assert np.array_equal(outs["1"].view(np.uint64), outs["0"].view(np.uint64))
