@@ -140,6 +140,9 @@ def _declare(L):
     L.orc_tridiag_qr_f32.argtypes = [_fp, _fp, C.c_int, _fp]
     L.orc_low_evd_symqr.restype = C.c_int
     L.orc_low_evd_symqr.argtypes = [_dp, C.c_int, _fp, _fp, C.POINTER(Report)]
+    L.orc_block_jacobi_evd_f64.restype = C.c_int
+    L.orc_block_jacobi_evd_f64.argtypes = [_dp, _dp, C.c_int, C.c_int, C.c_double, C.c_double, C.c_int, C.c_int,
+                                           C.c_int, _ip, _llp, _dp]
     L.orc_report_size.restype = C.c_size_t
     L.orc_cfg_size.restype = C.c_size_t
     assert L.orc_report_size() == C.sizeof(Report)
@@ -268,6 +271,20 @@ def jacobi_evd(T, V=None, *, b=32, tol=0.0, nu=20 * OMEGA, rule=0, max_sweeps=60
     hist = np.zeros(64)
     st = fn(_p(T), _p(V), n, b, tol, nu, rule, max_sweeps, max_rounds, C.byref(sw), C.byref(rot),
             _p(hist))
+    return JacobiResult(T, V, sw.value, rot.value, st, hist[: min(sw.value + 1, 64)].copy())
+
+
+def block_jacobi(T, V=None, *, b=32, tol=0.0, nu=20 * OMEGA, rule=0, max_sweeps=60,
+                 max_inner=30) -> JacobiResult:
+    """Classic block Jacobi with full inner diagonalisation of the 2b x 2b
+    blocks (reading R26); rotations = inner rotations."""
+    T = _f64(T).copy(order="F")
+    n = T.shape[0]
+    V = _f64(np.eye(n) if V is None else V).copy(order="F")
+    sw, rot = C.c_int(), C.c_longlong()
+    hist = np.zeros(64)
+    st = lib().orc_block_jacobi_evd_f64(_p(T), _p(V), n, b, tol, nu, rule, max_sweeps, max_inner, C.byref(sw),
+                                        C.byref(rot), _p(hist))
     return JacobiResult(T, V, sw.value, rot.value, st, hist[: min(sw.value + 1, 64)].copy())
 
 

@@ -550,6 +550,132 @@ int orc_low_evd(const double *A, int n, const orc_cfg *cfg, float *Z, orc_report
 }
 
 /* ------------------------------------------------------------------------ */
+/* Classic block Jacobi with full inner diagonalisation (SURVEY 8(f) row 4;  */
+/* the parallel Jacobi context of P:27), reading R26: the indices are cut    */
+/* into nb = n_p/b blocks of b; a block round pairs the blocks by the         */
+/* merry-go-round on blocks; for every block pair (I, J) the 2b x 2b  */
+/* submatrix S = T(P, P), P = block I u block J, is diagonalised by inner     */
+/* Jacobi sweeps (the 2b - 1 rounds of the R1 ordering on 2b indices with     */
+/* block size b, Lemma 3.1 with the same threshold nu) until an inner sweep  */
+/* rotates no pair (or max_inner sweeps), accumulating U = J_1 J_2 ...; then */
+/* T(P_a, P_c) <- U_a^T T(P_a, P_c) U_c for every two block pairs a != c      */
+/* (the two products each accumulated in long double and rounded),            */
+/* T(P_a, P_a) <- the diagonalised S_a, V(:, P_c) <- V(:, P_c) U_c.  A sweep */
+/* is the nb - 1 block rounds; the stop test as Alg. 2.  off_hist    */
+/* and the return value as orc_jacobi_evd.  rot counts inner rotations.       */
+/* ------------------------------------------------------------------------ */
+int orc_block_jacobi_evd_f64(double *T, double *V, int n, int b, double tol, double nu, int rule,
+                             int max_sweeps, int max_inner, int *sweeps_out, long long *rot_out,
+                             double *off_hist)
+{
+    if (n < 1 || b < 1 || (b > 1 && (b & 1))) return 1;
+    const int np = orc_padded_n(n, b), nb = np / b, mb = nb / 2, w = 2 * b;
+    double *Tp = (double *)calloc((size_t)np * np, sizeof(double));
+    double *Vp = (double *)calloc((size_t)np * np, sizeof(double));
+    for (int j = 0; j < n; ++j)
+        for (int i = 0; i < n; ++i) {
+            Tp[IDX(i, j, np)] = T[IDX(i, j, n)];
+            Vp[IDX(i, j, np)] = V[IDX(i, j, n)];
+        }
+    int *btop = (int *)malloc(sizeof(int) * (mb > 0 ? mb : 1)), *bbot = (int *)malloc(sizeof(int) * (mb > 0 ? mb : 1));
+    int *idx = (int *)malloc(sizeof(int) * (size_t)(mb > 0 ? mb : 1) * w);
+    double *Us = (double *)malloc(sizeof(double) * (size_t)(mb > 0 ? mb : 1) * w * w);
+    double *Ss = (double *)malloc(sizeof(double) * (size_t)(mb > 0 ? mb : 1) * w * w);
+    double *Tn = (double *)malloc(sizeof(double) * (size_t)np * np);
+    int sweeps = 0, status = 2;
+    long long rot = 0;
+    for (;;) {
+        const double off = orc_off_f64(Tp, np, np);
+        if (off_hist && sweeps < 64) off_hist[sweeps] = off;
+        if (off <= tol) { status = 0; break; }
+        if (sweeps >= max_sweeps) { status = 2; break; }
+        ++sweeps;
+        for (int k = 0; k < mb; ++k) { btop[k] = 2 * k; bbot[k] = 2 * k + 1; }
+        for (int R = 0; R < nb - 1; ++R) {
+            long long rr = 0;
+            /* inner diagonalisation of every block pair's S (disjoint: independent) */
+            _Pragma("omp parallel for reduction(+:rr) schedule(dynamic,1)")
+            for (int k = 0; k < mb; ++k) {
+                const int I = btop[k] < bbot[k] ? btop[k] : bbot[k], J = btop[k] < bbot[k] ? bbot[k] : btop[k];
+                int *ix = idx + (size_t)k * w;
+                for (int i = 0; i < b; ++i) { ix[i] = I * b + i; ix[b + i] = J * b + i; }
+                double *S = Ss + (size_t)k * w * w, *U = Us + (size_t)k * w * w;
+                for (int j = 0; j < w; ++j)
+                    for (int i = 0; i < w; ++i) {
+                        S[IDX(i, j, w)] = Tp[IDX(ix[i], ix[j], np)];
+                        U[IDX(i, j, w)] = i == j ? 1.0 : 0.0;
+                    }
+                for (int it = 0; it < max_inner; ++it) {
+                    int sw = 0;
+                    long long r1 = 0;
+                    orc_jacobi_evd_f64(S, U, w, b, 0.0, nu, rule, 1, -1, &sw, &r1, NULL);
+                    rr += r1;
+                    if (r1 == 0) break;
+                }
+            }
+            rot += rr;
+            /* T <- U^T T U by blocks (off-diagonal pairs), diagonal blocks from S */
+            memcpy(Tn, Tp, sizeof(double) * (size_t)np * np);
+            _Pragma("omp parallel for schedule(dynamic,1)")
+            for (int a = 0; a < mb; ++a) {
+                const int *ia = idx + (size_t)a * w;
+                const double *Ua = Us + (size_t)a * w * w;
+                double *Y = (double *)malloc(sizeof(double) * (size_t)w * w);
+                for (int c = 0; c < mb; ++c) {
+                    const int *ic = idx + (size_t)c * w;
+                    if (c == a) {
+                        const double *S = Ss + (size_t)a * w * w;
+                        for (int j = 0; j < w; ++j)
+                            for (int i = 0; i < w; ++i) Tn[IDX(ia[i], ia[j], np)] = S[IDX(i, j, w)];
+                        continue;
+                    }
+                    const double *Uc = Us + (size_t)c * w * w;
+                    for (int j = 0; j < w; ++j)          /* Y = U_a^T X */
+                        for (int i = 0; i < w; ++i) {
+                            ldbl acc = 0;
+                            for (int l = 0; l < w; ++l) acc += (ldbl)Ua[IDX(l, i, w)] * (ldbl)Tp[IDX(ia[l], ic[j], np)];
+                            Y[IDX(i, j, w)] = (double)acc;
+                        }
+                    for (int j = 0; j < w; ++j)          /* W = Y U_c */
+                        for (int i = 0; i < w; ++i) {
+                            ldbl acc = 0;
+                            for (int l = 0; l < w; ++l) acc += (ldbl)Y[IDX(i, l, w)] * (ldbl)Uc[IDX(l, j, w)];
+                            Tn[IDX(ia[i], ic[j], np)] = (double)acc;
+                        }
+                }
+                free(Y);
+            }
+            memcpy(Tp, Tn, sizeof(double) * (size_t)np * np);
+            /* V(:, P_c) <- V(:, P_c) U_c */
+            _Pragma("omp parallel for schedule(static)")
+            for (int r = 0; r < np; ++r) {
+                double row[256];
+                for (int c = 0; c < mb; ++c) {
+                    const int *ic = idx + (size_t)c * w;
+                    const double *Uc = Us + (size_t)c * w * w;
+                    for (int j = 0; j < w; ++j) {
+                        ldbl acc = 0;
+                        for (int l = 0; l < w; ++l) acc += (ldbl)Vp[IDX(r, ic[l], np)] * (ldbl)Uc[IDX(l, j, w)];
+                        row[j] = (double)acc;
+                    }
+                    for (int j = 0; j < w; ++j) Vp[IDX(r, ic[j], np)] = row[j];
+                }
+            }
+            music(btop, bbot, mb);
+        }
+    }
+    for (int j = 0; j < n; ++j)
+        for (int i = 0; i < n; ++i) {
+            T[IDX(i, j, n)] = Tp[IDX(i, j, np)];
+            V[IDX(i, j, n)] = Vp[IDX(i, j, np)];
+        }
+    if (sweeps_out) *sweeps_out = sweeps;
+    if (rot_out) *rot_out = rot;
+    free(Tp); free(Vp); free(btop); free(bbot); free(idx); free(Us); free(Ss); free(Tn);
+    return status;
+}
+
+/* ------------------------------------------------------------------------ */
 /* Alg. 3 step 1 as the paper states it ("[Z,~] = eig(A)  Symmetric   */
 /* QR factorization in low precision upsilon"; the paper ran LAPACK SSYEV /  */
 /* cusolverDnSsyevd), reading R12': in binary32,               */

@@ -26,7 +26,7 @@ UPSILON = 2.0 ** -24
 
 MPJ_OK, MPJ_ERR_INVALID, MPJ_ERR_NOCONV, MPJ_ERR_RANKDEF = 0, 1, 2, 3
 MPJ_ERR_NONFINITE, MPJ_ERR_CUDA, MPJ_ERR_NCCL, MPJ_ERR_NOMEM = 4, 5, 6, 7
-VARIANT_AUTO, VARIANT_SCALAR, VARIANT_BLOCK = 0, 1, 2
+VARIANT_AUTO, VARIANT_SCALAR, VARIANT_BLOCK, VARIANT_BLOCK_FULL = 0, 1, 2, 3
 LOW_AUTO, LOW_JACOBI, LOW_SYMQR = 0, 1, 2
 
 STATUS_NAMES = {0: "OK", 1: "INVALID", 2: "NOCONV", 3: "RANKDEF", 4: "NONFINITE", 5: "CUDA",

@@ -41,7 +41,7 @@ template <typename R>
 __global__ void __launch_bounds__(NTW) k_block_solve(R *__restrict__ T, int64_t ldt, Sched S, int Rb, R nu,
                                                      int rule, R *__restrict__ Ubuf,
                                                      unsigned long long *__restrict__ cnt,
-                                                     int *__restrict__ uid, int *__restrict__ nid)
+                                                     int *__restrict__ uid, int *__restrict__ nid, int max_inner)
 {
     asm volatile("griddepcontrol.wait;\n" ::: "memory");   // launched early (PDL): wait for K4
     constexpr int LD = LayK<R>::LD;
@@ -60,7 +60,7 @@ __global__ void __launch_bounds__(NTW) k_block_solve(R *__restrict__ T, int64_t 
         U[li + lj * LD] = (li == lj) ? R(1) : R(0);
     }
     __syncthreads();
-    const R *D = inner_rounds_wide<R>(D0, D1, U, bp, Rb == 0, S.lsched, nu, rule, P, &nrot);
+    const R *D = inner_rounds_wide<R>(D0, D1, U, bp, Rb == 0, S.lsched, nu, rule, P, &nrot, max_inner);
     R *Uk = Ubuf + (size_t)k * TW * TW;
     R *UkT = Ubuf + (size_t)mb * TW * TW + (size_t)k * TW * TW;   // U^T (fp32 apply operand)
     R *UkS = Ubuf + 2 * (size_t)mb * TW * TW + (size_t)k * TW * TW;   // U^T, split-half layout
@@ -1153,7 +1153,8 @@ static cudaError_t launch_apply(const ApplyArgs &p, cudaStream_t st)
 
 template <typename R>
 mpj_status block_sweep(R *T, int64_t ldt, R *V, int64_t ldv, int vrows, const DevSched &ds, R nu, int rule,
-                       unsigned long long *cnt, void *scratch, cudaStream_t st, bool first_sweep, int max_brounds)
+                       unsigned long long *cnt, void *scratch, cudaStream_t st, bool first_sweep, int max_brounds,
+                       int max_inner)
 {
     if (ds.b != BW) { set_error("block variant needs b = 32"); return MPJ_ERR_INVALID; }
     Sched S;
@@ -1176,7 +1177,7 @@ mpj_status block_sweep(R *T, int64_t ldt, R *V, int64_t ldv, int vrows, const De
     for (int Rb = 0; Rb < nbr; ++Rb) {
         if (prof) prof_mark(nsolve, st, true);
         MPJ_CK(launch_pdl(k_block_solve<R>, dim3(mb), dim3(NTW), sm_solve, st, T, ldt, S, Rb, nu, rule, Ubuf, cnt,
-                          uid, nid + Rb));
+                          uid, nid + Rb, max_inner));
         count_launch();
         if (prof) { prof_mark(nsolve, st, false); prof_mark(napply, st, true); }
         ap.Rb = Rb;
@@ -1238,8 +1239,8 @@ template cudaError_t launch_block_apply_cols<float>(float *, int64_t, int, const
 template size_t block_scratch_bytes<double>(int, int);
 template size_t block_scratch_bytes<float>(int, int);
 template mpj_status block_sweep<double>(double *, int64_t, double *, int64_t, int, const DevSched &, double,
-                                        int, unsigned long long *, void *, cudaStream_t, bool, int);
+                                        int, unsigned long long *, void *, cudaStream_t, bool, int, int);
 template mpj_status block_sweep<float>(float *, int64_t, float *, int64_t, int, const DevSched &, float, int,
-                                       unsigned long long *, void *, cudaStream_t, bool, int);
+                                       unsigned long long *, void *, cudaStream_t, bool, int, int);
 
 }  // namespace mpj

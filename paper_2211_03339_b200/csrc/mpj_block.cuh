@@ -514,21 +514,34 @@ __device__ __forceinline__ R *smem_rounds_wide(R *D0, R *D1, R *U, int2 bp, bool
 template <typename R>
 __device__ __forceinline__ R *inner_rounds_wide(R *D0, R *D1, R *U, int2 bp, bool intra,
                                                 const int2 *__restrict__ lsched, R nu, int rule,
-                                                WideParams<R> (&PP)[2], unsigned *nrot)
+                                                WideParams<R> (&PP)[2], unsigned *nrot, int max_inner = 0)
 {
-    unsigned cnt = 0;
     R *Dc = D0, *X = D1;
-    if (intra) {
-        Dc = smem_rounds_wide<R, false>(D0, D1, U, bp, true, BW - 1, lsched, nu, rule, PP, cnt);
-        X = (Dc == D0) ? D1 : D0;
-    }
-    Dc = smem_rounds_wide<R, true>(Dc, X, U, bp, false, BW, lsched, nu, rule, PP, cnt);
-    // rotation count: per-thread counts of the diagonal threads and the parameter warp
-    for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
     if (threadIdx.x == 0) *nrot = 0;
-    __syncthreads();
-    if ((threadIdx.x & 31) == 0 && cnt) atomicAdd(nrot, cnt);
-    __syncthreads();
+    // max_inner > 0: classic block Jacobi (reading R26) -- full inner sweeps
+    // (intra + cross rounds: every pair of the 2b indices) until one rotates
+    // no pair; else one pass (intra rounds in block round 0, then cross rounds)
+    const int nsweep = max_inner > 0 ? max_inner : 1;
+    __shared__ unsigned sweep_rot;
+    for (int it = 0; it < nsweep; ++it) {
+        unsigned cnt = 0;
+        if (intra || max_inner > 0) {
+            Dc = smem_rounds_wide<R, false>(Dc, X, U, bp, true, BW - 1, lsched, nu, rule, PP, cnt);
+            X = (Dc == D0) ? D1 : D0;
+        }
+        Dc = smem_rounds_wide<R, true>(Dc, X, U, bp, false, BW, lsched, nu, rule, PP, cnt);
+        X = (Dc == D0) ? D1 : D0;
+        // rotation count: per-thread counts of the diagonal threads and the parameter warp
+        for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+        if (threadIdx.x == 0) sweep_rot = 0;
+        __syncthreads();
+        if ((threadIdx.x & 31) == 0 && cnt) atomicAdd(&sweep_rot, cnt);
+        __syncthreads();
+        const unsigned sr = sweep_rot;
+        if (threadIdx.x == 0) *nrot += sr;
+        __syncthreads();
+        if (sr == 0) break;
+    }
     return Dc;
 }
 

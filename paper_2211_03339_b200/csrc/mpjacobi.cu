@@ -41,7 +41,7 @@ mpj_status svd_run(const double *A, int64_t m, int64_t n, int64_t lda, double *S
 template <typename R>
 mpj_status block_sweep(R *T, int64_t ldt, R *V, int64_t ldv, int vrows, const DevSched &S, R nu,
                        int rule, unsigned long long *cnt, void *scratch, cudaStream_t st, bool first_sweep,
-                       int max_brounds);
+                       int max_brounds, int max_inner);
 template <typename R>
 size_t block_scratch_bytes(int np, int b);
 
@@ -208,9 +208,11 @@ static int resolve_variant(int np, int b, const mpj_config *cfg)
 {
     int v = cfg ? cfg->variant : MPJ_VARIANT_AUTO;
     if (v == MPJ_VARIANT_AUTO) v = (np >= 128 && b == 32) ? MPJ_VARIANT_BLOCK : MPJ_VARIANT_SCALAR;
-    if (v == MPJ_VARIANT_BLOCK && b != 32) v = MPJ_VARIANT_SCALAR;   // block kernels are b = 32
+    if ((v == MPJ_VARIANT_BLOCK || v == MPJ_VARIANT_BLOCK_FULL) && b != 32) v = MPJ_VARIANT_SCALAR;   // b = 32 kernels
     return v;
 }
+static bool is_block(int v) { return v == MPJ_VARIANT_BLOCK || v == MPJ_VARIANT_BLOCK_FULL; }
+constexpr int kMaxInner = 30;     // inner sweeps of the classic block Jacobi (reading R26)
 
 // ---------------------------------------------------------------------------
 // Per-call stream context: private stream joined to the caller's stream.
@@ -323,7 +325,7 @@ static void carve_jacobi(Arena &ar, int np, int b, int variant, JacobiBufs<R> &j
     const int nb = np / b;
     jb.bsched = ar.take<int2>((size_t)std::max(nb - 1, 1) * std::max(nb / 2, 1));
     jb.lsched = ar.take<int2>((size_t)std::max(b - 1, 1) * std::max(b / 2, 1));
-    jb.block_scratch = (variant == MPJ_VARIANT_BLOCK) ? ar.take<char>(block_scratch_bytes<R>(np, b)) : nullptr;
+    jb.block_scratch = is_block(variant) ? ar.take<char>(block_scratch_bytes<R>(np, b)) : nullptr;
     jb.Tn = (variant == MPJ_VARIANT_SCALAR) ? ar.take<R>((size_t)np * np) : nullptr;
     jb.pos = ar.take<int>(np);
 }
@@ -388,7 +390,7 @@ static mpj_status jacobi_run(Ctx &cx, R *T, R *V, int n, int b, int variant, dou
         if (sweeps >= max_sweeps) { status = MPJ_ERR_NOCONV; break; }
         if (max_rounds >= 0 && rounds_done >= max_rounds) { status = MPJ_OK; break; }
         ++sweeps;
-        if (variant == MPJ_VARIANT_BLOCK) {
+        if (is_block(variant)) {
             // block round 0 holds 2b - 1 scalar rounds (b - 1 intra-block + b
             // cross), every later one b (reading R1); a round limit must fall
             // on a block-round boundary
@@ -411,7 +413,7 @@ static mpj_status jacobi_run(Ctx &cx, R *T, R *V, int n, int b, int variant, dou
                 nbr = k;
             }
             MPJ_TRY(block_sweep<R>(T, np, V, np, np, ds, nu, rule, jb.cnt, jb.block_scratch, st, sweeps == 1,
-                                   nbr));
+                                   nbr, variant == MPJ_VARIANT_BLOCK_FULL ? kMaxInner : 0));
             rounds_done += used;
         } else {
             // scalar rounds; the fused kernel writes T into the other buffer, so a
