@@ -81,7 +81,15 @@ typedef struct mpj_config {
     int variant;              /* MPJ_VARIANT_*                                             */
     int block_b;              /* ordering block size b (1 or even); 0 = auto (32)        */
     int low_solver;           /* EVD step 1 (reading R12'): MPJ_LOW_*             */
+    int orth;                 /* EVD step 2: MPJ_ORTH_*                            */
 } mpj_config;
+
+/* Orthogonaliser of Alg. 3 step 2 (both give the unique QR factor Q of Z with
+ * a positive diagonal of R, the MGS Q; reading R10). */
+enum {
+    MPJ_ORTH_CGS = 0,         /* blocked CGS (twice-is-enough) + panel CholeskyQR2 (default) */
+    MPJ_ORTH_HOUSEHOLDER = 1  /* blocked Householder QR (the paper's GPU choice)     */
+};
 
 /* Low-precision eigensolver of Alg. 3 step 1 (mpjacobi_eig / _eig_z). */
 enum {
@@ -212,6 +220,11 @@ mpj_status mpjacobi_orth(const double *Z, double *Q, int64_t n, void *stream);
 mpj_status mpjacobi_sytrd(float *A, int64_t n, int64_t lda, float *d, float *e, float *tau, void *stream);
 mpj_status mpjacobi_tridiag_eig(const float *d, const float *e, int64_t n, double *lam, double *Y, int64_t ldy,
                                 void *stream);
+
+/* Alg. 3 step 2 by blocked Householder QR: Q =
+ * H_0 ... H_{n-1} with the columns' signs making diag(R) positive.  Z, Q: n x n
+ * DEVICE, ld = n.  Returns MPJ_ERR_RANKDEF on a zero diagonal of R. */
+mpj_status mpjacobi_orth_householder(const double *Z, double *Q, int64_t n, void *stream);
 
 /* Alg. 3 step 3: T = Q^T A Q, symmetrised; A, Q, T: n x n DEVICE,
  * ld = n.  fp64 tensor-core (DMMA) GEMMs. */

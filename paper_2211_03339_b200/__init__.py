@@ -28,6 +28,7 @@ MPJ_OK, MPJ_ERR_INVALID, MPJ_ERR_NOCONV, MPJ_ERR_RANKDEF = 0, 1, 2, 3
 MPJ_ERR_NONFINITE, MPJ_ERR_CUDA, MPJ_ERR_NCCL, MPJ_ERR_NOMEM = 4, 5, 6, 7
 VARIANT_AUTO, VARIANT_SCALAR, VARIANT_BLOCK, VARIANT_BLOCK_FULL = 0, 1, 2, 3
 LOW_AUTO, LOW_JACOBI, LOW_SYMQR = 0, 1, 2
+ORTH_CGS, ORTH_HOUSEHOLDER = 0, 1
 
 STATUS_NAMES = {0: "OK", 1: "INVALID", 2: "NOCONV", 3: "RANKDEF", 4: "NONFINITE", 5: "CUDA",
                 6: "NCCL", 7: "NOMEM"}
@@ -44,7 +45,7 @@ class mpj_config(C.Structure):
         ("eps_factor", C.c_double), ("nu_factor", C.c_double), ("eps_low_factor", C.c_double),
         ("nu_low_factor", C.c_double), ("early_stop_ratio", C.c_double), ("max_sweeps", C.c_int),
         ("max_sweeps_low", C.c_int), ("stop_rule", C.c_int), ("variant", C.c_int), ("block_b", C.c_int),
-        ("low_solver", C.c_int),
+        ("low_solver", C.c_int), ("orth", C.c_int),
     ]
 
 
@@ -102,6 +103,8 @@ def lib():
         L.mpjacobi_sytrd.argtypes = [_vp, _i64, _i64, _vp, _vp, _vp, _vp]
         L.mpjacobi_tridiag_eig.restype = C.c_int
         L.mpjacobi_tridiag_eig.argtypes = [_vp, _vp, _i64, _vp, _vp, _i64, _vp]
+        L.mpjacobi_orth_householder.restype = C.c_int
+        L.mpjacobi_orth_householder.argtypes = [_vp, _vp, _i64, _vp]
         L.mpjacobi_orth.restype = C.c_int
         L.mpjacobi_orth.argtypes = [_vp, _vp, _i64, _vp]
         L.mpjacobi_precond.restype = C.c_int
@@ -140,7 +143,7 @@ EXPORTED = (
     "mpjacobi_eig_batched", "mpjacobi_last_error", "mpjacobi_launch_count",
     "mpjacobi_profile_enable", "mpjacobi_profile_reset", "mpjacobi_profile_get",
     "mpjacobi_eig_mg", "mpjacobi_nccl_unique_id", "mpjacobi_mg_plan", "mpjacobi_eig_z", "mpjacobi_svd_z",
-    "mpjacobi_sytrd", "mpjacobi_tridiag_eig",
+    "mpjacobi_sytrd", "mpjacobi_tridiag_eig", "mpjacobi_orth_householder",
 )
 
 
@@ -325,14 +328,17 @@ def mpjacobi_tridiag_eig(d, e):
     return lam, Y
 
 
-def mpjacobi_orth(Z):
-    """Alg. 3 step 2: fp64 CGS2 of a square column-major device matrix."""
+def mpjacobi_orth(Z, method="cgs"):
+    """Alg. 3 step 2: the QR factor Q of a square column-major device matrix
+    (method "cgs": blocked CGS + CholeskyQR2; "householder": blocked
+    Householder QR)."""
     n = Z.shape[0]
     Zc = colmajor(Z)
     if Zc.stride(1) != n:
         Zc = Zc.T.contiguous().T
     Q = empty_colmajor(n, n)
-    _check(lib().mpjacobi_orth(_ptr(Zc), _ptr(Q), n, _stream()))
+    fn = lib().mpjacobi_orth_householder if method == "householder" else lib().mpjacobi_orth
+    _check(fn(_ptr(Zc), _ptr(Q), n, _stream()))
     return Q
 
 

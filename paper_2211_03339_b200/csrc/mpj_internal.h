@@ -134,6 +134,11 @@ size_t orth_workspace(int64_t n);
 mpj_status orth_cgs2(const double *Z, int64_t ldz, double *Q, int64_t ldq, int64_t m, int64_t n,
                      void *ws, cudaStream_t st);
 
+// ---- orthogonalisation by Householder QR (k_hqr.cu) ---------------------------
+size_t hqr_workspace(int64_t m, int64_t n);
+mpj_status orth_householder(const double *Z, int64_t ldz, double *Q, int64_t ldq, int64_t m, int64_t n, void *ws,
+                            cudaStream_t st);
+
 // ---- low-precision stage by symmetric QR (k_tridiag.cu, reading R12') ---------
 size_t symqr_workspace(int64_t np);
 mpj_status low_evd_symqr(float *A32, int64_t lda, int n, float *Z32, int64_t ldz, double *Y, int64_t ldy,

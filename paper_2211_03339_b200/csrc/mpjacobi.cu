@@ -524,7 +524,8 @@ static void carve_eig(Arena &ar, int64_t n, const mpj_config *cfg, EigPlan &p)
     p.flag = ar.take<int>(4);
     p.rank = ar.take<int>(p.np);
     p.lam = ar.take<double>(p.np);
-    p.orth_ws = ar.take<char>(orth_workspace(p.np));
+    p.orth_ws = ar.take<char>((cfg && cfg->orth == MPJ_ORTH_HOUSEHOLDER) ? hqr_workspace(p.np, p.np)
+                                                                           : orth_workspace(p.np));
     p.symqr_ws = ar.take<char>(symqr_workspace(p.np));
     carve_jacobi<double>(ar, p.np, p.b, p.variant, p.j64);
     carve_jacobi<float>(ar, p.np, p.b, p.variant, p.j32);
@@ -676,7 +677,8 @@ static mpj_status eig_impl(bool mixed, const double *A, int64_t n, int64_t lda, 
         Timer to(cx.st);
         launch_copy_pad<float, double>(p.V32, np, (int)n, (int)n, p.W, np, (int)n, (int)n, cx.st);
         MPJ_CKF(cudaMemsetAsync(p.V, 0, (size_t)np * np * sizeof(double), cx.st));
-        s = orth_cgs2(p.W, np, p.V, np, n, n, p.orth_ws, cx.st);
+        s = cfg.orth == MPJ_ORTH_HOUSEHOLDER ? orth_householder(p.W, np, p.V, np, n, n, p.orth_ws, cx.st)
+                                             : orth_cgs2(p.W, np, p.V, np, n, n, p.orth_ws, cx.st);
         if (s != MPJ_OK) return finish(s);
         r.t_orth = to.stop();
 
@@ -803,6 +805,7 @@ void mpj_config_default_eig(mpj_config *c)
     c->variant = MPJ_VARIANT_AUTO;
     c->block_b = 0;
     c->low_solver = MPJ_LOW_AUTO;
+    c->orth = MPJ_ORTH_CGS;
 }
 
 void mpj_config_default_svd(mpj_config *c)
@@ -888,6 +891,20 @@ mpj_status mpjacobi_orth(const double *Z, double *Q, int64_t n, void *stream)
     void *ws = nullptr;
     MPJ_CK(cudaMallocAsync(&ws, orth_workspace(n), cx.st));
     mpj_status s = orth_cgs2(Z, n, Q, n, n, n, ws, cx.st);
+    cudaFreeAsync(ws, cx.st);
+    mpj_status c = cx.close();
+    return s != MPJ_OK ? s : c;
+}
+
+mpj_status mpjacobi_orth_householder(const double *Z, double *Q, int64_t n, void *stream)
+{
+    g_err.clear();
+    if (n < 1 || !Z || !Q) { set_error("invalid argument"); return MPJ_ERR_INVALID; }
+    Ctx cx;
+    MPJ_TRY(cx.open(stream));
+    void *ws = nullptr;
+    MPJ_CK(cudaMallocAsync(&ws, hqr_workspace(n, n), cx.st));
+    mpj_status s = orth_householder(Z, n, Q, n, n, n, ws, cx.st);
     cudaFreeAsync(ws, cx.st);
     mpj_status c = cx.close();
     return s != MPJ_OK ? s : c;

@@ -53,7 +53,7 @@ def test_struct_sizes_match_header(mpjlib):
     # mpj_report: 4 ints, 2 long long, 2 doubles, 64 doubles, 6 doubles, 3 ints, 1 long long,
     # 64 doubles, 64 long long
     assert C.sizeof(mpjlib.mpj_report) == 4 * 4 + 2 * 8 + 2 * 8 + 64 * 8 + 6 * 8 + 3 * 4 + 4 + 8 + 64 * 8 + 64 * 8
-    assert C.sizeof(mpjlib.mpj_config) == 5 * 8 + 6 * 4
+    assert C.sizeof(mpjlib.mpj_config) == 5 * 8 + 7 * 4 + 4   # (+4: struct padding to 8)
 
 
 def test_workspace_query_needs_no_gpu(mpjlib):
