@@ -54,14 +54,14 @@ constexpr size_t SYTRD_SMEM = (2 * NCACHE + NSTAGE) * TB * TB * sizeof(float) > 
 
 // phase timestamps for tools/sytrd_trace.py (a build with -DMPJ_SYTRD_TRACE only)
 #ifdef MPJ_SYTRD_TRACE
-__device__ unsigned long long g_sytrd_trace[64 * 8 * 320];   // [column % 64][event][cta]
+__device__ unsigned long long g_sytrd_trace[64 * 12 * 320];   // [column % 64][event][cta]
 __device__ int g_trace_k0 = 0;                                // the panel recorded
 __device__ __forceinline__ void sytrd_trace(int k0, int jj, int ev)
 {
     if (threadIdx.x == 0 && k0 == g_trace_k0) {
         unsigned long long t;
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-        g_sytrd_trace[((size_t)jj * 8 + ev) * 320 + blockIdx.x] = t;
+        g_sytrd_trace[((size_t)jj * 12 + ev) * 320 + blockIdx.x] = t;
     }
 }
 #define SYTRD_TRACE(jj, ev) sytrd_trace(a.k0, jj, ev)
@@ -319,6 +319,7 @@ __global__ void __launch_bounds__(NTH, 2) k_sytrd_panel(SytrdArgs a, const __gri
                 acol[i] = x;
                 if (i >= j + 2) part = x * x;
             }
+            SYTRD_TRACE(jj, 10);
             part = warp_sum(part);
             // the two warps of this group: combine in a fixed order
             if (lane == 0) rowbuf[warp][0] = part;
@@ -514,6 +515,14 @@ __global__ void __launch_bounds__(NTH, 2) k_sytrd_panel(SytrdArgs a, const __gri
         grid_sync(a.bar, epoch);
         SYTRD_TRACE(jj, 5);
         // ------------------------------------------------------------ phase C
+        // only CTAs owning rows >= j+1 have work here (and need the reduced
+        // dots, v^T A22 v and row j+1 of w); the others only keep the symv's
+        // tile stream going (start_column) -- no redundant partial-sum traffic
+        const bool active = nown > 0 && (cta + (nown - 1) * G) * TB + TB - 1 >= j + 1;
+        if (!active) {
+            if (jj + 1 < a.ncols && tid == 0) start_column(j + 1);
+            continue;
+        }
         // C1: every partial sum this CTA needs, loads issued together: the dots
         // (thread (half, slot)), v^T A22 v (warp 7, extra), y of the first own
         // row block (thread group grp takes part grp of the tile-column list);
@@ -539,6 +548,7 @@ __global__ void __launch_bounds__(NTH, 2) k_sytrd_panel(SytrdArgs a, const __gri
                 }
                 s = s0 + s1;
             }
+            SYTRD_TRACE(jj, 11);
             float yp = 0.f;
             const int I0 = cta;                          // first own row block (if any)
             const bool own0 = nown > 0 && (I0 + 1) * TB > j + 1;
@@ -562,6 +572,7 @@ __global__ void __launch_bounds__(NTH, 2) k_sytrd_panel(SytrdArgs a, const __gri
             if (half == 0 && sl < 2 * jj) dots[sl] = s + dots[sl];
             __syncthreads();
         }
+        SYTRD_TRACE(jj, 8);
         // C2: sum_t (v^T V_t)(v^T W_t) by warp 0, then v^T p = tau (v^T A22 v - 2 sum),
         // alpha' = -(tau/2) v^T p
         if (warp == 0) {
@@ -571,6 +582,7 @@ __global__ void __launch_bounds__(NTH, 2) k_sytrd_panel(SytrdArgs a, const __gri
             if (lane == 0) bc[3] = sp;
         }
         __syncthreads();
+        SYTRD_TRACE(jj, 9);
         const float vtp = tau * __fmaf_rn(-2.0f, bc[3], bc[1]);
         const float alph = -0.5f * tau * vtp;
         // w_i = tau (y_i - V(i,:) (W^T v) - W(i,:) (V^T v)) + alpha' v_i  (rows i >= j+1)
