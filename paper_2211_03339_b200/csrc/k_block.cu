@@ -320,98 +320,152 @@ __device__ __forceinline__ void apply_x3_body(const ApplyArgs &p, unsigned char 
     const int K = (int)blockIdx.x < total ? (total - 1 - (int)blockIdx.x) / G + 1 : 0;
     const int phase = (int)(3 * (int64_t)blockIdx.x / G);      // 0, 1, 2: the CTAs of an SM
     const int k0 = (phase * K) / 3;
-    for (int kk = 0; kk < K; ++kk) {
+    auto item_of = [&](int kk) {
         int k = kk + k0;
         if (k >= K) k -= K;
-        const int item = (int)blockIdx.x + k * G;
-        if (skips && item_identity(p, item, mb)) continue;
-        Acc<double> acc;
-        if (item < p.ntT) {
-            int a, c;
-            decode_upper(item, a, c);
-            const int2 pa = bsr[a], pc = bsr[c];
-            const bool ia = block_identity(p, a, skips), ic = block_identity(p, c, skips);
+        return (int)blockIdx.x + k * G;
+    };
+    auto next_kk = [&](int kk) {
+        while (skips && kk < K && item_identity(p, item_of(kk), mb)) ++kk;
+        return kk;
+    };
+    struct It {
+        int item, a, c, r0;
+        int2 pa, pc;
+        bool isT, ia, ic;
+        const double *Uag, *Ucg;
+    };
+    auto decode = [&](int item) {
+        It s;
+        s.item = item;
+        s.isT = item < p.ntT;
+        if (s.isT) {
+            decode_upper(item, s.a, s.c);
+            s.pa = bsr[s.a]; s.pc = bsr[s.c];
+            s.ia = block_identity(p, s.a, skips); s.ic = block_identity(p, s.c, skips);
+            s.Uag = Ub + (size_t)s.a * TW * TW;
+            s.r0 = 0;
+        } else {
+            const int idx = item - p.ntT;
+            s.c = idx % mb; s.a = 0; s.r0 = (idx / mb) * TW;
+            s.pc = bsr[s.c]; s.pa = s.pc;
+            s.ia = s.ic = false;
+            s.Uag = nullptr;
+        }
+        s.Ucg = Ub + (size_t)s.c * TW * TW;
+        return s;
+    };
+    // the loads that precede an item's first product (issued while the
+    // previous item's results are being stored)
+    auto issue = [&](const It &s) {
+        if (s.isT) {
             const double *T = (const double *)p.T;
-            const double *Uag = Ub + (size_t)a * TW * TW, *Ucg = Ub + (size_t)c * TW * TW;
-            if (!ia && !ic) {
+            if (!s.ia && !s.ic) {
                 for (int ch = 0; ch < 4; ++ch) {                 // X and U_a rows, 4 groups
                     for (int e = tid; e < TW * 8; e += NT) {
                         const int lj = e >> 3, li = 16 * ch + 2 * (e & 7);
-                        cp16(xb + li + lj * LD, T + gidx(pa, li) + (int64_t)gidx(pc, lj) * p.ldt, 16);
-                        cp16(ub + li + lj * LD, Uag + li + lj * TW, 16);
+                        cp16(xb + li + lj * LD, T + gidx(s.pa, li) + (int64_t)gidx(s.pc, lj) * p.ldt, 16);
+                        cp16(ub + li + lj * LD, s.Uag + li + lj * TW, 16);
                     }
                     cp_commit();
                 }
-                // Y = U_a^T X; after chunk c's barrier, U_c rows of chunk c-1 replace U_a's
-                tile_mm_chunked<true>(ub, xb, acc, [&](int ch) {
-                    cp_wait_le(ch == 0 ? 3 : 2);
-                    __syncthreads();
-                    if (ch > 0) {
-                        for (int e = tid; e < TW * 8; e += NT) {
-                            const int lj = e >> 3, li = 16 * (ch - 1) + 2 * (e & 7);
-                            cp16(ub + li + lj * LD, Ucg + li + lj * TW, 16);
-                        }
-                        cp_commit();
-                    }
-                });
-                __syncthreads();                                  // GEMM 1 done: X and U_a chunk 3 free
-                for (int e = tid; e < TW * 8; e += NT) {
-                    const int lj = e >> 3, li = 48 + 2 * (e & 7);
-                    cp16(ub + li + lj * LD, Ucg + li + lj * TW, 16);
-                }
-                cp_commit();
-                acc.each([&](int i, int j, double v) { xb[i + j * LD] = v; });   // Y
-                // W = Y U_c, chunk c of U_c is group (3 - c) from the end
-                tile_mm_chunked<false>(xb, ub, acc, [&](int ch) { cp_wait_le(3 - ch); __syncthreads(); });
             } else {
                 for (int e = tid; e < TW * CPC; e += NT) {
                     const int lj = e / CPC, li = (e - lj * CPC) * EPC;
-                    cp16(xb + li + lj * LD, T + gidx(pa, li) + (int64_t)gidx(pc, lj) * p.ldt, 16);
-                    cp16(ub + li + lj * LD, (ia ? Ucg : Uag) + li + lj * TW, 16);
+                    cp16(xb + li + lj * LD, T + gidx(s.pa, li) + (int64_t)gidx(s.pc, lj) * p.ldt, 16);
+                    cp16(ub + li + lj * LD, (s.ia ? s.Ucg : s.Uag) + li + lj * TW, 16);
                 }
                 cp_commit();
-                cp_wait0();
-                __syncthreads();
-                if (ia) tile_mm<false>(xb, ub, acc);             // W = X Uc
-                else tile_mm<true>(ub, xb, acc);                 // W = Ua^T X
             }
-            __syncthreads();                                     // shared memory free: store from registers
+        } else {
+            const double *M = (const double *)p.M;
+            for (int ch = 0; ch < 4; ++ch) {
+                for (int e = tid; e < 16 * CPC; e += NT) {       // X columns 16ch..
+                    const int lj = 16 * ch + e / CPC, li = (e % CPC) * EPC;
+                    const int rem = p.mrows - (s.r0 + li);
+                    const int bytes = rem >= EPC ? 16 : (rem > 0 ? rem * 8 : 0);
+                    cp16(xb + li + lj * LD, M + (bytes ? (int64_t)(s.r0 + li) : 0) + (int64_t)gidx(s.pc, lj) * p.ldm,
+                         bytes);
+                }
+                for (int e = tid; e < TW * 8; e += NT) {         // U_c rows 16ch..
+                    const int lj = e >> 3, li = 16 * ch + 2 * (e & 7);
+                    cp16(ub + li + lj * LD, s.Ucg + li + lj * TW, 16);
+                }
+                cp_commit();
+            }
+        }
+    };
+    auto compute = [&](const It &s, Acc<double> &acc) {
+        if (s.isT && !s.ia && !s.ic) {
+            // Y = U_a^T X; after chunk c's barrier, U_c rows of chunk c-1 replace U_a's
+            tile_mm_chunked<true>(ub, xb, acc, [&](int ch) {
+                cp_wait_le(ch == 0 ? 3 : 2);
+                __syncthreads();
+                if (ch > 0) {
+                    for (int e = tid; e < TW * 8; e += NT) {
+                        const int lj = e >> 3, li = 16 * (ch - 1) + 2 * (e & 7);
+                        cp16(ub + li + lj * LD, s.Ucg + li + lj * TW, 16);
+                    }
+                    cp_commit();
+                }
+            });
+            __syncthreads();                                      // GEMM 1 done: X and U_a chunk 3 free
+            for (int e = tid; e < TW * 8; e += NT) {
+                const int lj = e >> 3, li = 48 + 2 * (e & 7);
+                cp16(ub + li + lj * LD, s.Ucg + li + lj * TW, 16);
+            }
+            cp_commit();
+            acc.each([&](int i, int j, double v) { xb[i + j * LD] = v; });   // Y
+            // W = Y U_c, chunk c of U_c is group (3 - c) from the end
+            tile_mm_chunked<false>(xb, ub, acc, [&](int ch) { cp_wait_le(3 - ch); __syncthreads(); });
+        } else if (s.isT) {
+            cp_wait0();
+            __syncthreads();
+            if (s.ia) tile_mm<false>(xb, ub, acc);               // W = X Uc
+            else tile_mm<true>(ub, xb, acc);                     // W = Ua^T X
+        } else {
+            tile_mm_chunked<false>(xb, ub, acc, [&](int ch) { cp_wait_le(3 - ch); __syncthreads(); });
+        }
+    };
+    auto store = [&](const It &s, const Acc<double> &acc) {
+        if (s.isT) {
             double *Tw = (double *)p.T;
             acc.each2([&](int i, int j, double v0, double v1) {
-                const int64_t gi = gidx(pa, i), gj = gidx(pc, j);
+                const int64_t gi = gidx(s.pa, i), gj = gidx(s.pc, j);
                 Tw[gi + gj * p.ldt] = v0;
                 Tw[gi + (gj + 1) * p.ldt] = v1;
                 *(double2 *)(Tw + gj + gi * p.ldt) = make_double2(v0, v1);
             });
         } else {
-            const int idx = item - p.ntT, c = idx % mb, r0 = (idx / mb) * TW;
-            const int2 pc = bsr[c];
-            const double *M = (const double *)p.M;
-            const double *Ucg = Ub + (size_t)c * TW * TW;
-            for (int ch = 0; ch < 4; ++ch) {
-                for (int e = tid; e < 16 * CPC; e += NT) {       // X columns 16ch..
-                    const int lj = 16 * ch + e / CPC, li = (e % CPC) * EPC;
-                    const int rem = p.mrows - (r0 + li);
-                    const int bytes = rem >= EPC ? 16 : (rem > 0 ? rem * 8 : 0);
-                    cp16(xb + li + lj * LD, M + (bytes ? (int64_t)(r0 + li) : 0) + (int64_t)gidx(pc, lj) * p.ldm, bytes);
-                }
-                for (int e = tid; e < TW * 8; e += NT) {         // U_c rows 16ch..
-                    const int lj = e >> 3, li = 16 * ch + 2 * (e & 7);
-                    cp16(ub + li + lj * LD, Ucg + li + lj * TW, 16);
-                }
-                cp_commit();
-            }
-            tile_mm_chunked<false>(xb, ub, acc, [&](int ch) { cp_wait_le(3 - ch); __syncthreads(); });
-            __syncthreads();
             double *Mw = (double *)p.M;
             acc.each2([&](int i, int j, double v0, double v1) {
-                if (r0 + i < p.mrows) {
-                    const int64_t gj = gidx(pc, j);
-                    Mw[(int64_t)(r0 + i) + gj * p.ldm] = v0;
-                    Mw[(int64_t)(r0 + i) + (gj + 1) * p.ldm] = v1;
+                if (s.r0 + i < p.mrows) {
+                    const int64_t gj = gidx(s.pc, j);
+                    Mw[(int64_t)(s.r0 + i) + gj * p.ldm] = v0;
+                    Mw[(int64_t)(s.r0 + i) + (gj + 1) * p.ldm] = v1;
                 }
             });
         }
+    };
+    int kk = next_kk(0);
+    It cur;
+    if (kk < K) {
+        cur = decode(item_of(kk));
+        issue(cur);
+    }
+    while (kk < K) {
+        Acc<double> acc;
+        compute(cur, acc);
+        __syncthreads();                                         // shared memory free
+        const int kn = next_kk(kk + 1);
+        It nxt = cur;
+        if (kn < K) {
+            nxt = decode(item_of(kn));
+            issue(nxt);                                          // next item's loads in flight ...
+        }
+        store(cur, acc);                                         // ... while this one's results go out
+        cur = nxt;
+        kk = kn;
     }
     cp_wait0();
 }

@@ -90,8 +90,10 @@ __global__ void __launch_bounds__(128) k_dgemm(int64_t m, int64_t n, int64_t k, 
                                                const double *__restrict__ A, int64_t lda,
                                                const double *__restrict__ B, int64_t ldb, double beta,
                                                double *__restrict__ C, int64_t ldc, int kchunk,
-                                               double *__restrict__ partial, int upper_only)
+                                               double *__restrict__ partial, int upper_only,
+                                               const int *__restrict__ skip)
 {
+    if (skip && *skip) return;                       // a conditional product (device-side decision)
     if (upper_only && (int64_t)blockIdx.x * BM >= ((int64_t)blockIdx.y + 1) * BN) return;   // strictly lower tile
     __shared__ __align__(16) double sA[2][TILE];
     __shared__ __align__(16) double sB[2][TILE];
@@ -166,8 +168,10 @@ __global__ void __launch_bounds__(128) k_dgemm(int64_t m, int64_t n, int64_t k, 
 }
 
 __global__ void k_splitk_reduce(int64_t m, int64_t n, int splits, const double *__restrict__ partial,
-                                double alpha, double beta, double *__restrict__ C, int64_t ldc)
+                                double alpha, double beta, double *__restrict__ C, int64_t ldc,
+                                const int *__restrict__ skip)
 {
+    if (skip && *skip) return;
     const int64_t total = m * n;
     for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total;
          e += (int64_t)gridDim.x * blockDim.x) {
@@ -184,7 +188,7 @@ __global__ void k_splitk_reduce(int64_t m, int64_t n, int splits, const double *
 
 void launch_dgemm(bool ta, bool tb, int64_t m, int64_t n, int64_t k, double alpha, const double *A,
                   int64_t lda, const double *B, int64_t ldb, double beta, double *C, int64_t ldc,
-                  cudaStream_t st, double *scratch, size_t scratch_elems, bool upper_only)
+                  cudaStream_t st, double *scratch, size_t scratch_elems, bool upper_only, const int *skip)
 {
     if (m <= 0 || n <= 0) return;
     const int64_t gm = (m + BM - 1) / BM, gn = (n + BN - 1) / BN;
@@ -199,7 +203,7 @@ void launch_dgemm(bool ta, bool tb, int64_t m, int64_t n, int64_t k, double alph
     dim3 grd((unsigned)gm, (unsigned)gn, (unsigned)splits);
     double *part = splits > 1 ? scratch : nullptr;
 #define GO(a, b) k_dgemm<a, b><<<grd, 128, 0, st>>>(m, n, k, alpha, A, lda, B, ldb, beta, C, ldc, kchunk, part, \
-                                                   upper_only ? 1 : 0)
+                                                   upper_only ? 1 : 0, skip)
     if (!ta && !tb) GO(false, false);
     else if (ta && !tb) GO(true, false);
     else if (!ta && tb) GO(false, true);
@@ -207,7 +211,7 @@ void launch_dgemm(bool ta, bool tb, int64_t m, int64_t n, int64_t k, double alph
 #undef GO
     count_launch();
     if (splits > 1) {
-        k_splitk_reduce<<<592, 256, 0, st>>>(m, n, splits, part, alpha, beta, C, ldc);
+        k_splitk_reduce<<<592, 256, 0, st>>>(m, n, splits, part, alpha, beta, C, ldc, skip);
         count_launch();
     }
 }

@@ -10,8 +10,10 @@
 //             -- twice (CGS2) if any column kept less than half its norm
 //             ("twice is enough"; checked on the panel Gram, the whole Q
 //             is then recomputed with two passes)
-//     twice:  G = X^T X ; G = R^T R (Cholesky) ; X = X R^{-1} (CholeskyQR2,
-//             the last step as a row-parallel triangular solve)
+//     G = X^T X ; G = R^T R (Cholesky) ; X = X R^{-1} (CholeskyQR, the last
+//             step as a row-parallel triangular solve) -- a second pass
+//             (CholeskyQR2) only when the first G was not within 1e-3 of I
+//             (device-side decision: the pass's kernels read a flag)
 // Every step is a dense fp64 tensor-core product except the 64 x 64
 // Cholesky (one CTA) and the row-wise forward substitution.  Orthogonality O(omega), same Q as
 // MGS to O(n omega) (tests/test_gpu_parity.py::test_orth_cgs2_matches_mgs).
@@ -34,10 +36,25 @@ constexpr int kLDG = kPanel + 1;
 // issue-bound: 150 us per call, 1% of an n = 8192 EVD).
 __global__ void __launch_bounds__(256) k_chol(const double *__restrict__ G, int w, double *__restrict__ Rf,
                                               int *__restrict__ fail, const double *__restrict__ pre,
-                                              int *__restrict__ reorth)
+                                              int *__restrict__ reorth, int *__restrict__ single,
+                                              const int *__restrict__ skip)
 {
     __shared__ double A[kPanel * kLDG];
+    __shared__ int far_from_I;
+    if (skip && *skip) return;
     const int tid = threadIdx.x, cj = tid & (kPanel - 1), ri = tid >> 6;
+    // single: the panel is orthonormal to 1e-3 (max |G - I|), so one CholeskyQR
+    // pass already gives an O(omega kappa^2) = O(omega) orthogonality and the
+    // second pass is skipped (the caller's conditional kernels read *single)
+    if (single) {
+        if (tid == 0) far_from_I = 0;
+        __syncthreads();
+        if (cj < w)
+            for (int i = ri; i < w; i += 4)
+                if (!(fabs(G[i + cj * w] - (i == cj ? 1.0 : 0.0)) <= 1e-3)) far_from_I = 1;
+        __syncthreads();
+        if (tid == 0) *single = far_from_I ? 0 : 1;
+    }
     // one projection pass lost more than half of a column's norm: "twice is
     // enough" (Kahan, Parlett) asks for the second pass (the caller redoes Q with CGS2)
     if (pre && reorth && ri == 0 && cj < w && G[cj + cj * w] < 0.25 * pre[cj]) *reorth = 1;
@@ -63,6 +80,16 @@ __global__ void __launch_bounds__(256) k_chol(const double *__restrict__ G, int 
     if (tid == 0 && bad) *fail = 1;
 }
 
+// X(:, 0:w) = S(:, 0:w) when *run (the panel's single CholeskyQR pass sufficed)
+__global__ void k_copy_panel_if(const double *__restrict__ S, int64_t lds, int64_t m, double *__restrict__ X,
+                                int64_t ldx, const int *__restrict__ run)
+{
+    if (!*run) return;
+    const int j = blockIdx.y;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x)
+        X[i + j * ldx] = S[i + j * lds];
+}
+
 // pre[j] = ||X(:, j)||^2 for the w columns of a panel (one CTA per column)
 __global__ void k_colnorm2(const double *__restrict__ X, int64_t ldx, int64_t m, double *__restrict__ pre)
 {
@@ -86,9 +113,11 @@ __global__ void k_colnorm2(const double *__restrict__ X, int64_t ldx, int64_t m,
 // registers, R broadcast from shared memory.  Replaces R^{-1} + a GEMM.
 template <int W>
 __global__ void __launch_bounds__(64) k_trsm_rows(const double *__restrict__ X, int64_t ldx, int64_t m,
-                                                  const double *__restrict__ Rf, double *__restrict__ Q, int64_t ldq)
+                                                  const double *__restrict__ Rf, double *__restrict__ Q, int64_t ldq,
+                                                  const int *__restrict__ skip)
 {
     __shared__ double R[W * W];
+    if (skip && *skip) return;
     for (int e = threadIdx.x; e < W * W; e += blockDim.x) R[e] = Rf[e];
     __syncthreads();
     const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -108,9 +137,11 @@ __global__ void __launch_bounds__(64) k_trsm_rows(const double *__restrict__ X, 
 
 // the same for a narrow last panel (w < 64)
 __global__ void __launch_bounds__(64) k_trsm_rows_w(const double *__restrict__ X, int64_t ldx, int64_t m, int w,
-                                                    const double *__restrict__ Rf, double *__restrict__ Q, int64_t ldq)
+                                                    const double *__restrict__ Rf, double *__restrict__ Q, int64_t ldq,
+                                                    const int *__restrict__ skip)
 {
     __shared__ double R[kPanel * kPanel];
+    if (skip && *skip) return;
     for (int e = threadIdx.x; e < w * w; e += blockDim.x) R[e] = Rf[e];
     __syncthreads();
     const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -149,8 +180,9 @@ static mpj_status orth_sweep(const double *Z, int64_t ldz, double *Q, int64_t ld
     double *pre = Rf + kPanel * kPanel;    // panel column norms^2 before the projection
     int *fail = (int *)(pre + kPanel);
     int *reorth = fail + 1;
+    int *single = fail + 2;
 
-    MPJ_CK(cudaMemsetAsync(fail, 0, 2 * sizeof(int), st));
+    MPJ_CK(cudaMemsetAsync(fail, 0, 3 * sizeof(int), st));
     if (Q != Z || ldq != ldz) launch_copy_pad<double, double>(Z, ldz, (int)m, (int)n, Q, ldq, (int)m, (int)n, st);
 
     for (int64_t p0 = 0; p0 < n; p0 += kPanel) {
@@ -168,19 +200,26 @@ static mpj_status orth_sweep(const double *Z, int64_t ldz, double *Q, int64_t ld
                              scratch_elems);
             }
         }
-        // CholeskyQR2 of the panel: X -> S -> X
+        // CholeskyQR of the panel X -> S; the second pass S -> X only if the
+        // first Gram was not within 1e-3 of I (device-side decision), else S -> X
+        const int nblk = (int)((m + 63) / 64);
         for (int rep = 0; rep < 2; ++rep) {
             const double *src = rep == 0 ? X : S;
             const int64_t lds = rep == 0 ? ldq : m;
             double *dst = rep == 0 ? S : X;
             const int64_t ldd = rep == 0 ? m : ldq;
-            launch_dgemm(true, false, w, w, m, 1.0, src, lds, src, lds, 0.0, G, w, st, scratch, scratch_elems);
-            k_chol<<<1, 256, 0, st>>>(G, w, Rf, fail, (check && rep == 0) ? pre : nullptr, reorth);
-            const int nblk = (int)((m + 63) / 64);
-            if (w == kPanel) k_trsm_rows<kPanel><<<nblk, 64, 0, st>>>(src, lds, m, Rf, dst, ldd);
-            else k_trsm_rows_w<<<nblk, 64, 0, st>>>(src, lds, m, w, Rf, dst, ldd);
+            const int *skip = rep == 1 ? single : nullptr;
+            launch_dgemm(true, false, w, w, m, 1.0, src, lds, src, lds, 0.0, G, w, st, scratch, scratch_elems, false,
+                         skip);
+            k_chol<<<1, 256, 0, st>>>(G, w, Rf, fail, (check && rep == 0) ? pre : nullptr, reorth,
+                                      rep == 0 ? single : nullptr, skip);
+            if (w == kPanel) k_trsm_rows<kPanel><<<nblk, 64, 0, st>>>(src, lds, m, Rf, dst, ldd, skip);
+            else k_trsm_rows_w<<<nblk, 64, 0, st>>>(src, lds, m, w, Rf, dst, ldd, skip);
             count_launch(2);
         }
+        k_copy_panel_if<<<dim3((unsigned)std::min<int64_t>(64, (m + 255) / 256), w), 256, 0, st>>>(S, m, m, X, ldq,
+                                                                                                    single);
+        count_launch();
     }
     int h[2] = {0, 0};
     MPJ_CK(cudaMemcpyAsync(h, fail, 2 * sizeof(int), cudaMemcpyDeviceToHost, st));

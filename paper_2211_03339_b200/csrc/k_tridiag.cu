@@ -863,13 +863,14 @@ __global__ void k_tri_twisted(const double *__restrict__ d, const double *__rest
                               const double *__restrict__ e2, const int *__restrict__ bstart,
                               const int *__restrict__ bend, const double *__restrict__ pivmin_p,
                               const double *__restrict__ lam, int n, double *__restrict__ Dp,
-                              double *__restrict__ Dm, double *__restrict__ Y, int64_t ldy)
+                              double *__restrict__ Dm, double *__restrict__ inv_nrm)
 {
     const int t = blockIdx.x * blockDim.x + threadIdx.x;
     if (t >= n) return;
     const int s = bstart[t], e = bend[t];
-    double *y = Y + (size_t)t * ldy;
-    if (s == e) { y[s] = 1.0; return; }
+    // x is written row-major into Dp (x_i at Dp[i n + t], over D+_i once it is
+    // consumed): consecutive threads write consecutive words
+    if (s == e) { Dp[(size_t)s * n + t] = 1.0; inv_nrm[t] = 1.0; return; }
     const double pivmin = pivmin_p[0], l = lam[t];
     auto guard = [&](double q) { return fabs(q) < pivmin ? (q < 0.0 ? -pivmin : pivmin) : q; };
     // forward
@@ -890,22 +891,45 @@ __global__ void k_tri_twisted(const double *__restrict__ d, const double *__rest
         const double g = fabs(Dp[(size_t)i * n + t] + q - (d[i] - l));
         if (g < gbest) { gbest = g; r = i; }
     }
-    // solve
+    // solve (the ratios e_i / D are off the x chain: many in flight)
     double nrm = 1.0, x = 1.0;
-    y[r] = 1.0;
+    Dp[(size_t)r * n + t] = 1.0;
+    #pragma unroll 4
     for (int i = r - 1; i >= s; --i) {
         x = -__ddiv_rn(e64[i], Dp[(size_t)i * n + t]) * x;
-        y[i] = x;
+        Dp[(size_t)i * n + t] = x;
         nrm = __fma_rn(x, x, nrm);
     }
     x = 1.0;
+    #pragma unroll 4
     for (int i = r; i < e; ++i) {
         x = -__ddiv_rn(e64[i], Dm[(size_t)(i + 1) * n + t]) * x;
-        y[i + 1] = x;
+        Dp[(size_t)(i + 1) * n + t] = x;
         nrm = __fma_rn(x, x, nrm);
     }
-    const double inv = 1.0 / sqrt(nrm);
-    for (int i = s; i <= e; ++i) y[i] *= inv;
+    inv_nrm[t] = 1.0 / sqrt(nrm);
+}
+
+// Y(i, t) = x_i^(t) / ||x^(t)|| inside eigenvector t's block, 0 outside: a
+// 32 x 32 tiled transpose of the row-major X (= Dp) into column-major Y
+__global__ void k_tri_transpose(const double *__restrict__ X, int n, const int *__restrict__ bstart,
+                                const int *__restrict__ bend, const double *__restrict__ inv_nrm, double *Y,
+                                int64_t ldy)
+{
+    __shared__ double tile[32][33];
+    const int i0 = blockIdx.y * 32, t0 = blockIdx.x * 32;
+    const int tx = threadIdx.x, ty = threadIdx.y;            // 32 x 8
+    for (int r = ty; r < 32; r += 8) {                        // read rows i0 + r, columns t0 + tx
+        const int i = i0 + r, t = t0 + tx;
+        double v = 0.0;
+        if (i < n && t < n && i >= bstart[t] && i <= bend[t]) v = X[(size_t)i * n + t] * inv_nrm[t];
+        tile[r][tx] = v;
+    }
+    __syncthreads();
+    for (int r = ty; r < 32; r += 8) {                        // write column t0 + r, rows i0 + tx
+        const int t = t0 + r, i = i0 + tx;
+        if (i < n && t < n) Y[i + (size_t)t * ldy] = tile[tx][r];
+    }
 }
 
 // rank of lam[t] in descending order (ties by index: stable)
@@ -1044,7 +1068,7 @@ int coop_ctas()
 struct SymqrWs {
     float *V, *W, *acol, *d, *e, *tau, *Prow, *Pcol, *rred, *qred;
     unsigned *bar;
-    double *d64, *e64, *e2, *lam, *piv, *Vp, *Gm, *Tp, *W1, *W2, *skw;
+    double *d64, *e64, *e2, *lam, *piv, *Vp, *Gm, *Tp, *W1, *W2, *skw, *inrm;
     int *bstart, *bend, *rank;
     size_t skw_elems;
 };
@@ -1076,6 +1100,7 @@ static size_t carve_symqr(char *base, int64_t np, SymqrWs &w)
     w.e64 = (double *)take(np * 8);
     w.e2 = (double *)take(np * 8);
     w.lam = (double *)take(np * 8);
+    w.inrm = (double *)take(np * 8);
     w.piv = (double *)take(64);
     w.bstart = (int *)take(np * 4);
     w.bend = (int *)take(np * 4);
@@ -1158,9 +1183,10 @@ static mpj_status tri_eig_run(int n, SymqrWs &w, double *Y, int64_t ldy, double 
     k_tri_prep<<<1, 1024, 0, st>>>(w.d, w.e, n, w.d64, w.e64, w.e2, w.bstart, w.bend, w.piv);
     k_tri_bisect<<<(n + 256 / MSEC - 1) / (256 / MSEC), 256, 0, st>>>(w.d64, w.e64, w.e2, w.bstart, w.bend, w.piv, n,
                                                                      w.lam);
-    MPJ_CK(cudaMemset2DAsync(Y, ldy * 8, 0, (size_t)n * 8, n, st));
-    k_tri_twisted<<<(n + 127) / 128, 128, 0, st>>>(w.d64, w.e64, w.e2, w.bstart, w.bend, w.piv, w.lam, n, Dp, Dm, Y,
-                                                    ldy);
+    k_tri_twisted<<<(n + 127) / 128, 128, 0, st>>>(w.d64, w.e64, w.e2, w.bstart, w.bend, w.piv, w.lam, n, Dp, Dm,
+                                                    w.inrm);
+    k_tri_transpose<<<dim3((n + 31) / 32, (n + 31) / 32), dim3(32, 8), 0, st>>>(Dp, n, w.bstart, w.bend, w.inrm, Y,
+                                                                                 ldy);
     k_rank_lam<<<(n + 255) / 256, 256, 0, st>>>(w.lam, n, w.rank);
     count_launch(4);
     return MPJ_OK;
