@@ -789,7 +789,8 @@ __device__ __forceinline__ int sturm_count(const double *__restrict__ d, const d
     double q = d[s] - x;
     if (fabs(q) <= pivmin) q = -pivmin;
     int cnt = q < 0.0;
-    for (int i = s + 1; i <= e; ++i) {
+    #pragma unroll 8
+    for (int i = s + 1; i <= e; ++i) {      // unrolled: the d / e2 loads run ahead of the q chain
         q = (d[i] - x) - __ddiv_rn(e2[i - 1], q);
         if (fabs(q) <= pivmin) q = -pivmin;
         cnt += q < 0.0;
@@ -865,49 +866,85 @@ __global__ void k_tri_twisted(const double *__restrict__ d, const double *__rest
                               const double *__restrict__ lam, int n, double *__restrict__ Dp,
                               double *__restrict__ Dm, double *__restrict__ inv_nrm)
 {
-    const int t = blockIdx.x * blockDim.x + threadIdx.x;
-    if (t >= n) return;
-    const int s = bstart[t], e = bend[t];
+    // two lanes per eigenvalue: role 0 runs the forward factorisation (D+) and
+    // the solve above r, role 1 the backward one (D-) and the solve below r --
+    // the two division chains run side by side
+    const int gt = blockIdx.x * blockDim.x + threadIdx.x;
+    const int t = gt >> 1, role = gt & 1;
+    const unsigned pmask = 3u << (threadIdx.x & 30);
+    const bool valid = t < n;
+    const int tt = valid ? t : n - 1;
+    const int s = bstart[tt], e = bend[tt];
     // x is written row-major into Dp (x_i at Dp[i n + t], over D+_i once it is
-    // consumed): consecutive threads write consecutive words
-    if (s == e) { Dp[(size_t)s * n + t] = 1.0; inv_nrm[t] = 1.0; return; }
-    const double pivmin = pivmin_p[0], l = lam[t];
+    // consumed): consecutive eigenvalues write consecutive words
+    if (s == e) {
+        if (valid && role == 0) { Dp[(size_t)s * n + t] = 1.0; inv_nrm[t] = 1.0; }
+        return;
+    }
+    const double pivmin = pivmin_p[0], l = lam[tt];
     auto guard = [&](double q) { return fabs(q) < pivmin ? (q < 0.0 ? -pivmin : pivmin) : q; };
-    // forward
-    double q = guard(d[s] - l);
-    Dp[(size_t)s * n + t] = q;
-    for (int i = s + 1; i <= e; ++i) {
-        q = guard((d[i] - l) - __ddiv_rn(e2[i - 1], q));
-        Dp[(size_t)i * n + t] = q;
+    if (valid) {
+        if (role == 0) {                                   // forward
+            double q = guard(d[s] - l);
+            Dp[(size_t)s * n + t] = q;
+            #pragma unroll 8
+            for (int i = s + 1; i <= e; ++i) {
+                q = guard((d[i] - l) - __ddiv_rn(e2[i - 1], q));
+                Dp[(size_t)i * n + t] = q;
+            }
+        } else {                                           // backward
+            double q = guard(d[e] - l);
+            Dm[(size_t)e * n + t] = q;
+            #pragma unroll 8
+            for (int i = e - 1; i >= s; --i) {
+                q = guard((d[i] - l) - __ddiv_rn(e2[i], q));
+                Dm[(size_t)i * n + t] = q;
+            }
+        }
     }
-    // backward, with gamma_i = D+_i + D-_i - (d_i - lam)
-    q = guard(d[e] - l);
-    Dm[(size_t)e * n + t] = q;
-    int r = e;
-    double gbest = fabs(Dp[(size_t)e * n + t] + q - (d[e] - l));
-    for (int i = e - 1; i >= s; --i) {
-        q = guard((d[i] - l) - __ddiv_rn(e2[i], q));
-        Dm[(size_t)i * n + t] = q;
-        const double g = fabs(Dp[(size_t)i * n + t] + q - (d[i] - l));
-        if (g < gbest) { gbest = g; r = i; }
+    __syncwarp(pmask);
+    // r = argmin |gamma_i|, gamma_i = D+_i + D-_i - (d_i - lam) (ties: the larger i,
+    // as a scan from e downwards); each lane scans half of [s, e]
+    const int mid = (s + e + 1) >> 1;
+    const int i0 = role == 0 ? s : mid, i1 = role == 0 ? mid - 1 : e;
+    double gbest = 1e308;
+    int r = -1;
+    if (valid)
+        for (int i = i1; i >= i0; --i) {
+            const double g = fabs(Dp[(size_t)i * n + t] + Dm[(size_t)i * n + t] - (d[i] - l));
+            if (g < gbest) { gbest = g; r = i; }
+        }
+    const double go = __shfl_xor_sync(pmask, gbest, 1);
+    const int ro = __shfl_xor_sync(pmask, r, 1);
+    // role 1's half holds the larger indices: it wins ties
+    const bool mine_hi = role == 1;
+    if (go < gbest || (go == gbest && !mine_hi && ro >= 0)) { gbest = go; r = ro; }
+    __syncwarp(pmask);
+    double nrm = 0.0;
+    if (valid) {
+        if (role == 0) {                                   // x_r = 1, then upwards
+            double x = 1.0;
+            nrm = 1.0;
+            #pragma unroll 8
+            for (int i = r - 1; i >= s; --i) {
+                x = -__ddiv_rn(e64[i], Dp[(size_t)i * n + t]) * x;
+                Dp[(size_t)i * n + t] = x;
+                nrm = __fma_rn(x, x, nrm);
+            }
+        } else {                                           // downwards
+            double x = 1.0;
+            #pragma unroll 8
+            for (int i = r; i < e; ++i) {
+                x = -__ddiv_rn(e64[i], Dm[(size_t)(i + 1) * n + t]) * x;
+                Dp[(size_t)(i + 1) * n + t] = x;
+                nrm = __fma_rn(x, x, nrm);
+            }
+        }
     }
-    // solve (the ratios e_i / D are off the x chain: many in flight)
-    double nrm = 1.0, x = 1.0;
-    Dp[(size_t)r * n + t] = 1.0;
-    #pragma unroll 4
-    for (int i = r - 1; i >= s; --i) {
-        x = -__ddiv_rn(e64[i], Dp[(size_t)i * n + t]) * x;
-        Dp[(size_t)i * n + t] = x;
-        nrm = __fma_rn(x, x, nrm);
-    }
-    x = 1.0;
-    #pragma unroll 4
-    for (int i = r; i < e; ++i) {
-        x = -__ddiv_rn(e64[i], Dm[(size_t)(i + 1) * n + t]) * x;
-        Dp[(size_t)(i + 1) * n + t] = x;
-        nrm = __fma_rn(x, x, nrm);
-    }
-    inv_nrm[t] = 1.0 / sqrt(nrm);
+    __syncwarp(pmask);
+    if (valid && role == 0) Dp[(size_t)r * n + t] = 1.0;
+    const double nrm_all = nrm + __shfl_xor_sync(pmask, nrm, 1);
+    if (valid && role == 0) inv_nrm[t] = 1.0 / sqrt(nrm_all);
 }
 
 // Y(i, t) = x_i^(t) / ||x^(t)|| inside eigenvector t's block, 0 outside: a
@@ -982,9 +1019,12 @@ __global__ void __launch_bounds__(256) k_build_tp(const double *__restrict__ G, 
     const int tid = threadIdx.x, row = tid & (BT - 1), grp = tid >> 7;   // 2 groups x 128 rows
     for (int e = tid; e < BT * (BT + 1); e += 256) T[e] = 0.0;
     __syncthreads();
+    double gnext = (tid < BT && nr > 0) ? G[tid] : 0.0;        // G(tid, t), loaded one step ahead
     for (int t = 0; t < nr; ++t) {
         const double ta = (double)tau[k0 + t];
-        if (tid < t) z[tid] = -ta * G[tid + t * BT];
+        const double gcur = gnext;
+        if (tid < BT && t + 1 < nr) gnext = G[tid + (t + 1) * BT];
+        if (tid < t) z[tid] = -ta * gcur;
         __syncthreads();
         // T(row, t) = sum_{u = row}^{t-1} T(row, u) z(u): group grp takes u = row + grp, +2, ...
         double acc = 0.0;
@@ -1183,8 +1223,8 @@ static mpj_status tri_eig_run(int n, SymqrWs &w, double *Y, int64_t ldy, double 
     k_tri_prep<<<1, 1024, 0, st>>>(w.d, w.e, n, w.d64, w.e64, w.e2, w.bstart, w.bend, w.piv);
     k_tri_bisect<<<(n + 256 / MSEC - 1) / (256 / MSEC), 256, 0, st>>>(w.d64, w.e64, w.e2, w.bstart, w.bend, w.piv, n,
                                                                      w.lam);
-    k_tri_twisted<<<(n + 127) / 128, 128, 0, st>>>(w.d64, w.e64, w.e2, w.bstart, w.bend, w.piv, w.lam, n, Dp, Dm,
-                                                    w.inrm);
+    k_tri_twisted<<<(2 * n + 127) / 128, 128, 0, st>>>(w.d64, w.e64, w.e2, w.bstart, w.bend, w.piv, w.lam, n, Dp,
+                                                        Dm, w.inrm);
     k_tri_transpose<<<dim3((n + 31) / 32, (n + 31) / 32), dim3(32, 8), 0, st>>>(Dp, n, w.bstart, w.bend, w.inrm, Y,
                                                                                  ldy);
     k_rank_lam<<<(n + 255) / 256, 256, 0, st>>>(w.lam, n, w.rank);
