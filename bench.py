@@ -53,6 +53,8 @@ def parse():
     ap.add_argument("--workload", default="evd", choices=["evd", "batched", "svd", "config2"],
                     help="evd: BASELINE config 4 (the bench line); batched: config 3 (4096 x n=64)")
     ap.add_argument("--batch", type=int, default=4096)
+    ap.add_argument("--low", default="symqr", choices=["symqr", "jacobi"],
+                    help="Alg. 3 step 1 of --workload batched: symmetric QR (default, R12') or fp32 Jacobi (R12)")
     ap.add_argument("--eps-low", type=float, default=0.0,
                     help="low stage eps = f * upsilon; 0 = the rule of reading R12")
     return ap.parse_args()
@@ -305,8 +307,9 @@ def run_batched(args):
     n, batch = 64, args.batch
     As = np.stack([W.example1(n, 1e3, 3 + k % 3, W.seed_for(3, 3 + k % 3, 1e3, k))[0] for k in range(batch)])
     A = torch.from_numpy(As).cuda()
+    cfg = mpj.default_config("eig", low_solver=mpj.LOW_JACOBI if args.low == "jacobi" else mpj.LOW_SYMQR)
     for _ in range(args.warmup):
-        res = mpj.eig_batched(A)
+        res = mpj.eig_batched(A, cfg)
     torch.cuda.synchronize()
     l0 = mpj.launch_count()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -314,7 +317,7 @@ def run_batched(args):
     with ClockSampler(0) as clk:
         e0.record()
         for _ in range(steps):
-            res = mpj.eig_batched(A)
+            res = mpj.eig_batched(A, cfg)
         e1.record()
         torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / steps
@@ -326,7 +329,8 @@ def run_batched(args):
     line = {"metric": "batched EVD matrices/s (4096 x n=64)", "value": batch / (ms * 1e-3), "unit": "matrices/s",
             "n_gpus": 1, "steps": steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
             "dtype": "f64", "data": "synthetic",
-            "config": {"workload": f"{batch} x Example 1 n=64 modes 3/4/5 kappa=1e3 (BASELINE config 3)"},
+            "config": {"workload": f"{batch} x Example 1 n=64 modes 3/4/5 kappa=1e3 (BASELINE config 3)",
+                       "step1": args.low},
             "sweeps_mean": float(res.sweeps.float().mean()), "sweeps_low_mean": float(res.sweeps_low.float().mean()),
             "check": {"max_residual": float(R.max()), "max_orth": float(O.max())},
             "gpu_launches": mpj.launch_count() - l0, "clocks": clk.summary()}

@@ -262,12 +262,24 @@ mpj_status mpjacobi_svd_z(const double *A, int64_t m, int64_t n, int64_t lda, co
  * Batched Alg. 3: `batch` independent n x n matrices, contiguous with stride
  * n*n (each column-major), one matrix per CTA (n <= 64).  Lambda: batch x n;
  * V: batch x n x n (each column-major); sweeps / sweeps_low: batch ints
- * (DEVICE, may be NULL).  All pointers DEVICE.  Returns MPJ_ERR_NOCONV if any
- * matrix hit max_sweeps.
+ * (DEVICE, may be NULL).  All pointers DEVICE.  Step 1 follows
+ * cfg->low_solver: symmetric QR in binary32 by default (reading R12'),
+ * the fp32 Jacobi with MPJ_LOW_JACOBI (R12; sweeps_low is 0 for symmetric QR).
+ * Returns MPJ_ERR_NONFINITE if some matrix holds a NaN / Inf,
+ * MPJ_ERR_RANKDEF if some Z is rank deficient in step 2, MPJ_ERR_NOCONV if
+ * any matrix hit max_sweeps.
  * ---------------------------------------------------------------------- */
 mpj_status mpjacobi_eig_batched(const double *A, int64_t n, int64_t batch, double *Lambda,
                                 double *V, int *sweeps, int *sweeps_low, void *stream,
                                 const mpj_config *cfg);
+
+/* Batched Alg. 3 with step 1's output supplied (Z_in: step 1 is skipped) or
+ * exported (Z_out), as mpjacobi_eig_z: batch x n x n binary32, each n x n
+ * column-major (stride n*n), DEVICE; either may be NULL.  A shared Z isolates
+ * the fp64 stage (sweep parity with the oracle). */
+mpj_status mpjacobi_eig_batched_z(const double *A, int64_t n, int64_t batch, const float *Z_in, float *Z_out,
+                                  double *Lambda, double *V, int *sweeps, int *sweeps_low, void *stream,
+                                  const mpj_config *cfg);
 
 /* ------------------------------------------------------------------------
  * Multi-GPU Alg. 3, one process per GPU: the block-pair slots

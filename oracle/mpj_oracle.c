@@ -1145,9 +1145,8 @@ int orc_plain_svd(const double *A, int m, int n, const orc_cfg *cfg, double *sig
 int orc_mp_evd_batched(const double *A, int n, int batch, const orc_cfg *cfg, double *lam,
                        double *V, int *sweeps, int *sweeps_low)
 {
-    /* the batched path's low stage is the fp32 Jacobi (reading R12) */
+    /* step 1 as cfg->low_solver says (symmetric QR by default, reading R12') */
     orc_cfg c1 = *cfg;
-    c1.low_solver = 1;
     int worst = 0;
     _Pragma("omp parallel for schedule(dynamic,1) reduction(max:worst)")
     for (int k = 0; k < batch; ++k) {

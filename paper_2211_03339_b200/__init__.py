@@ -132,6 +132,8 @@ def lib():
         if hasattr(L, "mpjacobi_eig_batched"):
             L.mpjacobi_eig_batched.restype = C.c_int
             L.mpjacobi_eig_batched.argtypes = [_vp, _i64, _i64, _vp, _vp, _vp, _vp, _vp, cfgp]
+            L.mpjacobi_eig_batched_z.restype = C.c_int
+            L.mpjacobi_eig_batched_z.argtypes = [_vp, _i64, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp, cfgp]
         _lib = L
     return _lib
 
@@ -143,7 +145,7 @@ EXPORTED = (
     "mpjacobi_eig_batched", "mpjacobi_last_error", "mpjacobi_launch_count",
     "mpjacobi_profile_enable", "mpjacobi_profile_reset", "mpjacobi_profile_get",
     "mpjacobi_eig_mg", "mpjacobi_nccl_unique_id", "mpjacobi_mg_plan", "mpjacobi_eig_z", "mpjacobi_svd_z",
-    "mpjacobi_sytrd", "mpjacobi_tridiag_eig", "mpjacobi_orth_householder",
+    "mpjacobi_sytrd", "mpjacobi_tridiag_eig", "mpjacobi_orth_householder", "mpjacobi_eig_batched_z",
 )
 
 
@@ -424,13 +426,17 @@ class BatchedResult:
     sweeps: torch.Tensor       # (batch,) int32 fp64 sweeps
     sweeps_low: torch.Tensor   # (batch,) int32 fp32 sweeps
     status: int
+    Z: torch.Tensor | None = None   # (batch, n, n) float32 step-1 output (Z_out=True)
 
 
-def mpjacobi_eig_batched(A, cfg: mpj_config | None = None, allow_noconv=False) -> BatchedResult:
+def mpjacobi_eig_batched(A, cfg: mpj_config | None = None, allow_noconv=False, Z_in=None,
+                         Z_out=False) -> BatchedResult:
     """Batched Alg. 3, one matrix per CTA (n <= 64).  A: (batch, n, n) float64
     CUDA tensor; A[k] is matrix k (symmetric, so either memory order is its
     column-major image).  Outputs are column-major per matrix, returned as
-    math-orientation views."""
+    math-orientation views.  Z_in: (batch, n, n) float32 CUDA tensor, step 1's
+    output Z[k] (math orientation) -- step 1 is skipped; Z_out: return the Z
+    step 2 consumed (mpjacobi_eig_batched_z)."""
     if A.dim() != 3 or A.shape[1] != A.shape[2] or A.dtype != torch.float64 or not A.is_cuda:
         raise ValueError("A must be a (batch, n, n) float64 CUDA tensor")
     batch, n, _ = A.shape
@@ -439,10 +445,17 @@ def mpjacobi_eig_batched(A, cfg: mpj_config | None = None, allow_noconv=False) -
     V = torch.empty((batch, n, n), dtype=torch.float64, device=A.device)
     sw = torch.empty(batch, dtype=torch.int32, device=A.device)
     swl = torch.empty(batch, dtype=torch.int32, device=A.device)
-    st = lib().mpjacobi_eig_batched(_ptr(Ac), n, batch, _ptr(lam), _ptr(V), _ptr(sw), _ptr(swl), _stream(),
-                                    C.byref(cfg or default_config("eig")))
+    zi = None
+    if Z_in is not None:
+        if Z_in.shape != A.shape or Z_in.dtype != torch.float32 or not Z_in.is_cuda:
+            raise ValueError("Z_in must be a (batch, n, n) float32 CUDA tensor")
+        zi = Z_in.transpose(1, 2).contiguous()   # column-major per matrix
+    zo = torch.empty((batch, n, n), dtype=torch.float32, device=A.device) if Z_out else None
+    st = lib().mpjacobi_eig_batched_z(_ptr(Ac), n, batch, _ptr(zi) if zi is not None else None,
+                                      _ptr(zo) if zo is not None else None, _ptr(lam), _ptr(V), _ptr(sw),
+                                      _ptr(swl), _stream(), C.byref(cfg or default_config("eig")))
     _check(st, (MPJ_OK, MPJ_ERR_NOCONV) if allow_noconv else (MPJ_OK,))
-    return BatchedResult(lam, V.transpose(1, 2), sw, swl, st)
+    return BatchedResult(lam, V.transpose(1, 2), sw, swl, st, zo.transpose(1, 2) if zo is not None else None)
 
 
 def mg_plan(n: int, nranks: int):

@@ -74,11 +74,10 @@ __device__ __forceinline__ void rot_side(R s, R tau, bool isp, R &mine, R other)
     mine = isp ? fmaR(-s, fmaR(tau, mine, other), mine) : fmaR(s, fmaR(-tau, mine, other), mine);
 }
 
-template <typename R>
+template <typename R, int LD = Lay<R>::LD>
 __device__ __forceinline__ unsigned inner_rounds_b(R *D, R *U, bool intra, const int2 *__restrict__ lsched, R nu,
                                                    int rule, InnerSharedB &sh, InnerParams<R> &pr)
 {
-    constexpr int LD = Lay<R>::LD;
     const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
     R ut[8], ub[8];
     #pragma unroll
@@ -574,6 +573,19 @@ template <> struct Acc<double> {
             for (int b = 0; b < 4; ++b) { v[a][b][0] = 0.0; v[a][b][1] = 0.0; }
     }
     template <typename F> __device__ __forceinline__ void each(F f) const
+    {
+        const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+        const int r0 = (warp >> 1) * 16 + (lane >> 2), c0 = (warp & 1) * 32 + 2 * (lane & 3);
+        #pragma unroll
+        for (int mi = 0; mi < 2; ++mi)
+            #pragma unroll
+            for (int ni = 0; ni < 4; ++ni) {
+                f(r0 + mi * 8, c0 + ni * 8, v[mi][ni][0]);
+                f(r0 + mi * 8, c0 + ni * 8 + 1, v[mi][ni][1]);
+            }
+    }
+    // as each, the entry by reference
+    template <typename F> __device__ __forceinline__ void each_ref(F f)
     {
         const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
         const int r0 = (warp >> 1) * 16 + (lane >> 2), c0 = (warp & 1) * 32 + 2 * (lane & 3);

@@ -231,10 +231,12 @@ def test_sort_is_stable_descending(orc):
 def test_batched_equals_loop(orc):
     n, batch = 16, 6
     As = np.stack([W.example1(n, 1e3, 3 + k % 3, 77 + k)[0] for k in range(batch)])
-    lam, V, sw, swl, st = orc.mp_evd_batched(As)
-    assert st == 0
-    for k in range(batch):
-        one = orc.mp_evd(As[k], orc.default_cfg(low_solver=orc.LOW_JACOBI))
-        assert np.array_equal(lam[k], one.lam) and sw[k] == one.report.sweeps
-        # V[k] is the row-major image of the column-major k-th matrix
-        assert np.array_equal(V[k].T, one.V)
+    for low in (orc.LOW_SYMQR, orc.LOW_JACOBI):
+        lam, V, sw, swl, st = orc.mp_evd_batched(As, orc.default_cfg(low_solver=low))
+        assert st == 0
+        for k in range(batch):
+            one = orc.mp_evd(As[k], orc.default_cfg(low_solver=low))
+            assert np.array_equal(lam[k], one.lam) and sw[k] == one.report.sweeps
+            assert swl[k] == one.report.sweeps_low
+            # V[k] is the row-major image of the column-major k-th matrix
+            assert np.array_equal(V[k].T, one.V)
