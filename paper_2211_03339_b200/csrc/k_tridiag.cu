@@ -782,6 +782,21 @@ __global__ void __launch_bounds__(1024) k_tri_prep(const float *__restrict__ d, 
     }
 }
 
+// 1 / q to about one ulp: the MUFU reciprocal seed and two Newton steps
+// (2^-23 -> 2^-46 -> rounding); q is never 0 or subnormal here (pivmin
+// guard).  Not correctly rounded: the Sturm counts and the twisted
+// factorisations stay backward stable (a few-ulp relative perturbation of
+// e_i^2 per step), at about half the dependent latency of a rounded division.
+__device__ __forceinline__ double rcp_nr(double q)
+{
+    double r;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(q));
+    double e = __fma_rn(-q, r, 1.0);
+    r = __fma_rn(r, e, r);
+    e = __fma_rn(-q, r, 1.0);
+    return __fma_rn(r, e, r);
+}
+
 // number of eigenvalues < x of the unreduced block [s, e] (Sturm count)
 __device__ __forceinline__ int sturm_count(const double *__restrict__ d, const double *__restrict__ e2, int s, int e,
                                            double x, double pivmin)
@@ -791,7 +806,7 @@ __device__ __forceinline__ int sturm_count(const double *__restrict__ d, const d
     int cnt = q < 0.0;
     #pragma unroll 8
     for (int i = s + 1; i <= e; ++i) {      // unrolled: the d / e2 loads run ahead of the q chain
-        q = (d[i] - x) - __ddiv_rn(e2[i - 1], q);
+        q = __fma_rn(-e2[i - 1], rcp_nr(q), d[i] - x);
         if (fabs(q) <= pivmin) q = -pivmin;
         cnt += q < 0.0;
     }
@@ -799,11 +814,13 @@ __device__ __forceinline__ int sturm_count(const double *__restrict__ d, const d
 }
 
 // eigenvalue t (the (t - bstart)-th smallest of its block) by multisection:
-// the 8 lanes of a group evaluate Sturm counts at 8 interior points of the
-// current interval, which shrinks 9x per round (3.17 bits), until it holds
-// adjacent doubles.  Thread t = 8 group + lane8 of a 256-thread CTA; 32
-// eigenvalues per CTA.
-constexpr int MSEC = 8;
+// the MSEC lanes of a group evaluate Sturm counts at MSEC interior points of
+// the current interval, which shrinks (MSEC + 1)x per round, until it is
+// within 2 omega of max(|lo|, |hi|) or of the block's Gershgorin bound (the
+// Sturm count resolves nothing finer).  MSEC = 32 (5 bits per round, a warp
+// per eigenvalue) for n <= 2048, where the n eigenvalues alone would not
+// fill the GPU; 8 above.
+template <int MSEC>
 __global__ void __launch_bounds__(256) k_tri_bisect(const double *__restrict__ d, const double *__restrict__ e64,
                                                     const double *__restrict__ e2, const int *__restrict__ bstart,
                                                     const int *__restrict__ bend,
@@ -815,7 +832,8 @@ __global__ void __launch_bounds__(256) k_tri_bisect(const double *__restrict__ d
     const int tt = valid ? t : n - 1;
     const int s = bstart[tt], e = bend[tt], k = tt - s;
     const double pivmin = pivmin_p[0];
-    const unsigned gmask = 0xffu << (threadIdx.x & 31 & ~(MSEC - 1));
+    const int base = threadIdx.x & 31 & ~(MSEC - 1);
+    const unsigned gmask = (MSEC == 32 ? 0xffffffffu : ((1u << MSEC) - 1)) << base;
     double lo = 1e308, hi = -1e308;
     // Gershgorin interval of the block (split over the group's lanes)
     for (int i = s + lane8; i <= e; i += MSEC) {
@@ -828,11 +846,13 @@ __global__ void __launch_bounds__(256) k_tri_bisect(const double *__restrict__ d
         lo = fmin(lo, __shfl_xor_sync(gmask, lo, o));
         hi = fmax(hi, __shfl_xor_sync(gmask, hi, o));
     }
-    const double pad = 2.0 * kOmega * fmax(fabs(lo), fabs(hi)) + pivmin;
+    const double gnorm = fmax(fabs(lo), fabs(hi));
+    const double pad = 2.0 * kOmega * gnorm + pivmin;
     lo -= pad;
     hi += pad;
     if (s < e) {
-        for (int round = 0; round < 40; ++round) {
+        for (int round = 0; round < 80; ++round) {
+            if (hi - lo <= 2.0 * kOmega * fmax(gnorm, fmax(fabs(lo), fabs(hi)))) break;
             const double w = (hi - lo) / (MSEC + 1);
             double x = lo + w * (lane8 + 1);
             if (!(x > lo)) x = lo;
@@ -840,7 +860,6 @@ __global__ void __launch_bounds__(256) k_tri_bisect(const double *__restrict__ d
             const int c = sturm_count(d, e2, s, e, x, pivmin);
             // first point with more than k eigenvalues below it bounds from above
             const unsigned ball = __ballot_sync(gmask, c > k) & gmask;
-            const int base = threadIdx.x & 31 & ~(MSEC - 1);
             const int m_hi = ball ? __ffs(ball) - 1 - base : MSEC;       // index of that point (MSEC: hi)
             const double nlo = m_hi > 0 ? __shfl_sync(gmask, x, base + m_hi - 1) : lo;
             const double nhi = m_hi < MSEC ? __shfl_sync(gmask, x, base + m_hi) : hi;
@@ -848,9 +867,6 @@ __global__ void __launch_bounds__(256) k_tri_bisect(const double *__restrict__ d
             lo = nlo;
             hi = nhi;
             if (done) break;
-            // adjacent doubles: no interior point left
-            const double mid = 0.5 * (lo + hi);
-            if (mid <= lo || mid >= hi) break;
         }
     }
     if (valid && lane8 == 0) lam[t] = s < e ? 0.5 * (lo + hi) : d[s];
@@ -889,7 +905,7 @@ __global__ void k_tri_twisted(const double *__restrict__ d, const double *__rest
             Dp[(size_t)s * n + t] = q;
             #pragma unroll 8
             for (int i = s + 1; i <= e; ++i) {
-                q = guard((d[i] - l) - __ddiv_rn(e2[i - 1], q));
+                q = guard(__fma_rn(-e2[i - 1], rcp_nr(q), d[i] - l));
                 Dp[(size_t)i * n + t] = q;
             }
         } else {                                           // backward
@@ -897,7 +913,7 @@ __global__ void k_tri_twisted(const double *__restrict__ d, const double *__rest
             Dm[(size_t)e * n + t] = q;
             #pragma unroll 8
             for (int i = e - 1; i >= s; --i) {
-                q = guard((d[i] - l) - __ddiv_rn(e2[i], q));
+                q = guard(__fma_rn(-e2[i], rcp_nr(q), d[i] - l));
                 Dm[(size_t)i * n + t] = q;
             }
         }
@@ -922,20 +938,26 @@ __global__ void k_tri_twisted(const double *__restrict__ d, const double *__rest
     __syncwarp(pmask);
     double nrm = 0.0;
     if (valid) {
+        // the divisors are loaded one step ahead of the x chain (the store of x_i
+        // goes to the slot just read, so the compiler cannot hoist the next load)
         if (role == 0) {                                   // x_r = 1, then upwards
             double x = 1.0;
             nrm = 1.0;
-            #pragma unroll 8
+            double dn = r - 1 >= s ? Dp[(size_t)(r - 1) * n + t] : 1.0;
             for (int i = r - 1; i >= s; --i) {
-                x = -__ddiv_rn(e64[i], Dp[(size_t)i * n + t]) * x;
+                const double dc = dn;
+                if (i - 1 >= s) dn = Dp[(size_t)(i - 1) * n + t];
+                x = -(e64[i] * rcp_nr(dc)) * x;
                 Dp[(size_t)i * n + t] = x;
                 nrm = __fma_rn(x, x, nrm);
             }
         } else {                                           // downwards
             double x = 1.0;
-            #pragma unroll 8
+            double dn = r < e ? Dm[(size_t)(r + 1) * n + t] : 1.0;
             for (int i = r; i < e; ++i) {
-                x = -__ddiv_rn(e64[i], Dm[(size_t)(i + 1) * n + t]) * x;
+                const double dc = dn;
+                if (i + 2 <= e) dn = Dm[(size_t)(i + 2) * n + t];
+                x = -(e64[i] * rcp_nr(dc)) * x;
                 Dp[(size_t)(i + 1) * n + t] = x;
                 nrm = __fma_rn(x, x, nrm);
             }
@@ -1014,11 +1036,71 @@ constexpr int BT = 2 * TB;       // back-transformation block (two sytrd panels)
 __global__ void __launch_bounds__(256) k_build_tp(const double *__restrict__ G, const float *__restrict__ tau, int k0,
                                                   int nr, double *Tp)
 {
-    extern __shared__ double tsm[];          // T (BT x BT+1), z (BT), part (2 x BT)
+    extern __shared__ double tsm[];          // T (BT x BT+1), z (BT), part (2 x BT), M (3 x 32 x 32)
     double *T = tsm, *z = T + BT * (BT + 1), *part = z + BT;
     const int tid = threadIdx.x, row = tid & (BT - 1), grp = tid >> 7;   // 2 groups x 128 rows
+    constexpr int LS = BT + 1, QB = 32;      // leading dimension, diagonal block size
+    double *M = part + 2 * BT;
+    __shared__ int zero_tau;
+    if (tid == 0) zero_tau = 0;
+    __syncthreads();
+    if (tid < nr && tau[k0 + tid] == 0.f) zero_tau = 1;
+    __syncthreads();
+    if (!zero_tau) {
+        // T = S^{-1}, S = diag(1 / tau) + strict upper part of G (the compact-WY
+        // identity T^{-1} + T^{-T} = V^T V in its triangular form, Joffrain et
+        // al. 2006; exact for any nonzero tau): the 32 x 32 diagonal blocks by
+        // back substitution (thread per column), then the off-diagonal blocks
+        // T_ij = -T_ii sum_{k=i+1..j} S_ik T_kj by block diagonals -- 2 barriers
+        // per block diagonal instead of 3 per reflector.  One array: S's strict
+        // upper part above the diagonal, T transposed on and below it.
+        auto tinv = [&](int i) { return i < nr ? (double)tau[k0 + i] : 1.0; };   // padding: identity
+        for (int e = tid; e < BT * LS; e += 256) T[e] = 0.0;
+        __syncthreads();
+        for (int e = tid; e < BT * BT; e += 256) {
+            const int i = e & (BT - 1), j = e / BT;
+            if (i < j && j < nr) T[i + j * LS] = G[i + j * BT];
+        }
+        __syncthreads();
+        if (tid < BT) {                                         // T_bb: column t of its 32-block
+            const int t = tid, b0 = (t / QB) * QB;
+            T[t + t * LS] = tinv(t);
+            for (int i = t - 1; i >= b0; --i) {
+                double acc = 0.0;
+                for (int u = i + 1; u <= t; ++u) acc = __fma_rn(T[i + u * LS], T[t + u * LS], acc);
+                T[t + i * LS] = -tinv(i) * acc;
+            }
+        }
+        __syncthreads();
+        for (int dg = 1; dg < BT / QB; ++dg) {                  // block diagonal dg: blocks (bi, bi + dg)
+            const int nb = BT / QB - dg;
+            for (int e = tid; e < nb * QB * QB; e += 256) {     // M = sum_{k=i+1..j} S_ik T_kj
+                const int bi = e / (QB * QB), r = (e / QB) % QB, cc = e % QB;
+                const int i0 = bi * QB, col = (bi + dg) * QB + cc;
+                double acc = 0.0;
+                for (int u = i0 + QB; u <= col; ++u) acc = __fma_rn(T[(i0 + r) + u * LS], T[col + u * LS], acc);
+                M[(size_t)bi * QB * QB + r + cc * QB] = acc;
+            }
+            __syncthreads();
+            for (int e = tid; e < nb * QB * QB; e += 256) {     // T_ij = -T_ii M
+                const int bi = e / (QB * QB), r = (e / QB) % QB, cc = e % QB;
+                const int i0 = bi * QB, col = (bi + dg) * QB + cc;
+                double acc = 0.0;
+                for (int u = r; u < QB; ++u)
+                    acc = __fma_rn(T[(i0 + u) + (i0 + r) * LS], M[(size_t)bi * QB * QB + u + cc * QB], acc);
+                T[col + (i0 + r) * LS] = -acc;
+            }
+            __syncthreads();
+        }
+        for (int e = tid; e < BT * BT; e += 256) {
+            const int i = e & (BT - 1), j = e / BT;
+            Tp[e] = (i <= j && j < nr) ? T[j + i * LS] : 0.0;
+        }
+        return;
+    }
     for (int e = tid; e < BT * (BT + 1); e += 256) T[e] = 0.0;
     __syncthreads();
+    // a zero tau (an identity reflector): LAPACK's column recurrence
     double gnext = (tid < BT && nr > 0) ? G[tid] : 0.0;        // G(tid, t), loaded one step ahead
     for (int t = 0; t < nr; ++t) {
         const double ta = (double)tau[k0 + t];
@@ -1163,8 +1245,350 @@ size_t symqr_workspace(int64_t np)
 
 // 1. binary32 tridiagonalisation of A32 (n x n, lda; overwritten by the
 // reflectors): d, e, tau in the workspace
+namespace {
+// ---------------------------------------------------------------------------
+// 1'. Small n (the whole lower triangle fits the distributed shared memory of
+// one 16-CTA cluster, n <= ~1150): the unblocked reduction (LAPACK ssytd2,
+// the same reflectors as above) with the matrix resident in shared memory for
+// all n - 2 columns.  CTA c owns rows i = 16 r + c (lower part, packed); per
+// column k:
+//   publish x = A(k+1:, k) at the own rows and the partial ||x(1:)||^2;
+//   cluster barrier; gather x and the 16 partials (DSMEM, fixed order) ->
+//   beta, tau, v, identical in every CTA;
+//   y = A22 v: own-row dots (16 lanes per row) and own-column sums of the
+//   strict lower part (thread per column), summed into this CTA's partial y;
+//   cluster barrier; y_j = sum of the 16 partials (fixed order), p = tau y,
+//   w = p - (tau/2)(p^T v) v in every CTA; A22 -= v w^T + w v^T on the own rows.
+// Two cluster barriers per column (~0.2 us each) instead of the panel
+// kernel's two grid barriers and L2 round trips per column -- what bounds the
+// panel kernel at n ~ 1000 (tools/sytrd_trace.py: ~13-18 us per column).
+// ---------------------------------------------------------------------------
+constexpr int SCL = 16;          // CTAs per cluster (non-portable size)
+constexpr int SCNT = 1024;       // threads per CTA
+
+__host__ __device__ __forceinline__ int sc_rows(int n, int c) { return c < n ? (n - c + SCL - 1) / SCL : 0; }
+__host__ __device__ __forceinline__ int sc_rm(int n) { return ((n + SCL - 1) / SCL + 3) / 4 * 4; }   // rows, padded
+__host__ __device__ __forceinline__ int sc_rowlen(int r, int c) { return (SCL * r + c + 1 + 3) & ~3; }
+// shared memory (floats): the exchange buffers at the same offsets in every CTA,
+// then the local vectors and the packed own rows
+struct ScLay {
+    int rm, np4;
+    int xin, nin, pin, pfull, vv, ww, part4, roff, own;
+    __host__ __device__ ScLay(int n)
+    {
+        rm = sc_rm(n); np4 = (n + 3) / 4 * 4;
+        xin = 0; nin = xin + SCL * rm; pin = nin + SCL; pfull = pin + SCL * rm;
+        vv = pfull + SCL * rm; ww = vv + np4; part4 = ww + np4; roff = part4 + 4 * np4;
+        own = roff + rm + 4;
+    }
+};
+static size_t sc_smem(int n)
+{
+    ScLay L(n);
+    int64_t mx = 0;
+    for (int c = 0; c < SCL; ++c) {
+        int64_t o = 0;
+        for (int r = 0; r < sc_rows(n, c); ++r) o += sc_rowlen(r, c);
+        mx = std::max(mx, o);
+    }
+    return ((size_t)L.own + (size_t)mx) * 4;
+}
+
+__device__ __forceinline__ unsigned sc_map(const void *p, int rank)
+{
+    unsigned r;
+    asm("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"((unsigned)__cvta_generic_to_shared(p)), "r"(rank));
+    return r;
+}
+__device__ __forceinline__ void sc_st4(unsigned a, float4 v)
+{
+    asm volatile("st.shared::cluster.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(a), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w)
+                 : "memory");
+}
+__device__ __forceinline__ void sc_st(unsigned a, float v)
+{
+    asm volatile("st.shared::cluster.f32 [%0], %1;" ::"r"(a), "f"(v) : "memory");
+}
+__device__ __forceinline__ void sc_cluster_sync()
+{
+    asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+}
+
+#ifdef MPJ_SYTRD_TRACE
+#define SCT(ev) if (k >= g_trace_k0 && k < g_trace_k0 + 64 && threadIdx.x == 0) { unsigned long long t_; \
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_)); g_sytrd_trace[((size_t)(k - g_trace_k0) * 12 + (ev)) * 320 + c] = t_; }
+#else
+#define SCT(ev)
+#endif
+
+// Exchange pattern per column (all remote traffic is 16-byte stores, pushed
+// by the owner; every read is local): x and the norm partials of the own rows
+// to every CTA; the partial y of every row to the row's owner; the owner's p
+// to every CTA.  Three cluster barriers per column.
+__global__ void __launch_bounds__(SCNT, 1) k_sytrd_cluster(float *A, int64_t ld, int n, float *dout, float *eout,
+                                                           float *tout)
+{
+    extern __shared__ __align__(16) float smem[];
+    __shared__ float red[2][SCNT / 32];
+    unsigned crank;
+    asm("mov.u32 %0, %%cluster_ctarank;" : "=r"(crank));
+    const int c = (int)crank, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int R = sc_rows(n, c);
+    const ScLay L(n);
+    const int RM = L.rm;
+    float *xin = smem + L.xin, *nin = smem + L.nin, *pin = smem + L.pin, *pfull = smem + L.pfull;
+    float *vv = smem + L.vv, *ww = smem + L.ww, *part4 = smem + L.part4;
+    int *roff = (int *)(smem + L.roff);
+    float *Aown = smem + L.own;
+    if (tid == 0) {
+        int o = 0;
+        for (int r = 0; r <= R; ++r) { roff[r] = o; if (r < R) o += sc_rowlen(r, c); }
+    }
+    __syncthreads();
+    // own rows of the lower triangle (A32 is symmetric: row i = column i, contiguous), zero padded
+    for (int r = 0; r < R; ++r) {
+        const int i = SCL * r + c, len = sc_rowlen(r, c);
+        for (int j = tid; j < len; j += SCNT) Aown[roff[r] + j] = j <= i ? A[j + (size_t)i * ld] : 0.f;
+    }
+    __syncthreads();
+    // push the x of column kx (own rows i >= kx+1) and the partial norm (i >= kx+2) to every CTA
+    auto push_x = [&](int kx) {
+        if (tid < SCL * (RM / 4)) {
+            const int dst = tid / (RM / 4), r4 = tid % (RM / 4);
+            float v[4];
+            #pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int r = 4 * r4 + u, i = SCL * r + c;
+                v[u] = (r < R && i >= kx + 1) ? Aown[roff[r] + kx] : 0.f;
+            }
+            sc_st4(sc_map(xin + c * RM + 4 * r4, dst), make_float4(v[0], v[1], v[2], v[3]));
+        } else if (warp == SCNT / 32 - 1) {
+            float sq = 0.f;
+            for (int r = lane; r < R; r += 32) {
+                const int i = SCL * r + c;
+                if (i >= kx + 2) { const float x = Aown[roff[r] + kx]; sq = __fmaf_rn(x, x, sq); }
+            }
+            #pragma unroll
+            for (int o = 16; o > 0; o >>= 1) sq += __shfl_xor_sync(0xffffffffu, sq, o);
+            if (lane < SCL) sc_st(sc_map(nin + c, lane), sq);
+        }
+    };
+    int k = 0;
+    push_x(0);
+    int rb = 0;
+    for (k = 0; k + 2 < n; ++k) {
+        SCT(0);
+        sc_cluster_sync();                                               // #1: x, norm partials
+        SCT(1);
+        float s = 0.f;
+        #pragma unroll
+        for (int q = 0; q < SCL; ++q) s += nin[q];
+        const float alpha = xin[((k + 1) % SCL) * RM + (k + 1) / SCL];
+        float beta, tau, scal;
+        if (s == 0.f) { beta = alpha; tau = 0.f; scal = 0.f; }
+        else {
+            const float nrm = sqrtf(__fmaf_rn(alpha, alpha, s));
+            beta = alpha >= 0.f ? -nrm : nrm;
+            tau = (beta - alpha) / beta;
+            scal = 1.0f / (alpha - beta);
+        }
+        for (int j = tid; j < L.np4; j += SCNT)
+            vv[j] = (j <= k || j >= n) ? 0.f : (j == k + 1 ? 1.f : xin[(j % SCL) * RM + j / SCL] * scal);
+        if (tid == 0) {
+            if (c == k % SCL) dout[k] = Aown[roff[k / SCL] + k];
+            if (c == 0) { eout[k] = beta; tout[k] = tau; }
+        }
+        __syncthreads();                                                 // v
+        SCT(2);
+        const float4 *vv4 = reinterpret_cast<const float4 *>(vv);
+        const int j40 = (k + 1) >> 2, nj4 = L.np4 >> 2;
+        // own-row dots y_i = sum_{k < j <= i} A_ij v_j: 16 lanes per row, float4 columns
+        float rdot[2] = {0.f, 0.f};
+        #pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const int r = h * (SCNT / 16) + (tid >> 4), l16 = tid & 15;
+            float acc = 0.f;
+            if (r < R) {
+                const int i = SCL * r + c;
+                const float4 *row = reinterpret_cast<const float4 *>(Aown + roff[r]);
+                for (int j4 = j40 + l16; 4 * j4 <= i; j4 += 16) {
+                    const float4 a = row[j4], v = vv4[j4];         // v_j = 0 for j <= k; masked j > i
+                    const int j = 4 * j4;
+                    acc = __fmaf_rn(a.x, v.x, acc);
+                    if (j + 1 <= i) acc = __fmaf_rn(a.y, v.y, acc);
+                    if (j + 2 <= i) acc = __fmaf_rn(a.z, v.z, acc);
+                    if (j + 3 <= i) acc = __fmaf_rn(a.w, v.w, acc);
+                }
+            }
+            #pragma unroll
+            for (int o = 8; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+            rdot[h] = acc;
+        }
+        // own-column sums of the strict lower part: 256 float4 column groups x 4 row groups
+        {
+            const int rg = tid >> 8, cg = tid & 255;
+            for (int j4 = j40 + cg; j4 < nj4; j4 += 256) {
+                const int j = 4 * j4;
+                float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
+                int r = (j + 1 - c + SCL - 1) / SCL;             // first own row i > j
+                r += (rg - r % 4 + 4) % 4;                       // ... of this row group
+                for (; r < R; r += 4) {
+                    const int i = SCL * r + c;
+                    const float4 a = reinterpret_cast<const float4 *>(Aown + roff[r])[j4];
+                    const float vi = vv[i];
+                    a0 = __fmaf_rn(a.x, vi, a0);
+                    if (i > j + 1) a1 = __fmaf_rn(a.y, vi, a1);
+                    if (i > j + 2) a2 = __fmaf_rn(a.z, vi, a2);
+                    if (i > j + 3) a3 = __fmaf_rn(a.w, vi, a3);
+                }
+                reinterpret_cast<float4 *>(part4 + rg * L.np4)[j4] = make_float4(a0, a1, a2, a3);
+            }
+        }
+        if ((tid & 15) == 0) {                                           // own-row dots next to the column sums
+            #pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const int r = h * (SCNT / 16) + (tid >> 4);
+                if (r < R) ww[SCL * r + c] = rdot[h];                    // ww: scratch until w is formed
+            }
+        }
+        __syncthreads();                                                 // part4, row dots
+        SCT(3);
+        // partial y of every row j >= k+1 to its owner: pin[c][r] of CTA j % 16
+        if (tid < SCL * (RM / 4)) {
+            const int dst = tid / (RM / 4), r4 = tid % (RM / 4);
+            float v[4];
+            #pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int j = SCL * (4 * r4 + u) + dst;
+                float y = 0.f;
+                if (j >= k + 1 && j < n) {
+                    y = ((part4[j] + part4[L.np4 + j]) + part4[2 * L.np4 + j]) + part4[3 * L.np4 + j];
+                    if (dst == c) y += ww[j];                            // own row: its row dot
+                }
+                v[u] = y;
+            }
+            sc_st4(sc_map(pin + c * RM + 4 * r4, dst), make_float4(v[0], v[1], v[2], v[3]));
+        }
+        SCT(4);
+        sc_cluster_sync();                                               // #2: partial y at the owners
+        SCT(5);
+        // owner: p_i = tau sum_c pin[c][r] for the own rows, pushed to every CTA
+        if (tid < SCL * (RM / 4)) {
+            const int dst = tid / (RM / 4), r4 = tid % (RM / 4);
+            float v[4];
+            #pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int r = 4 * r4 + u;
+                float y = 0.f;
+                #pragma unroll
+                for (int q = 0; q < SCL; ++q) y += pin[q * RM + r];
+                v[u] = tau * y;
+            }
+            sc_st4(sc_map(pfull + c * RM + 4 * r4, dst), make_float4(v[0], v[1], v[2], v[3]));
+        }
+        sc_cluster_sync();                                               // #3: p everywhere
+        SCT(6);
+        float pvp = 0.f;
+        for (int j = k + 1 + tid; j < n; j += SCNT) {
+            const float p = pfull[(j % SCL) * RM + j / SCL];
+            ww[j] = p;
+            pvp = __fmaf_rn(p, vv[j], pvp);
+        }
+        #pragma unroll
+        for (int o = 16; o > 0; o >>= 1) pvp += __shfl_xor_sync(0xffffffffu, pvp, o);
+        if (lane == 0) red[rb][warp] = pvp;
+        __syncthreads();                                                 // p, dot partials
+        float pv = 0.f;
+        #pragma unroll
+        for (int w = 0; w < SCNT / 32; ++w) pv += red[rb][w];
+        rb ^= 1;
+        const float K = 0.5f * tau * pv;
+        for (int j = tid; j < L.np4; j += SCNT) ww[j] = (j <= k || j >= n) ? 0.f : __fmaf_rn(-K, vv[j], ww[j]);
+        __syncthreads();                                                 // w
+        SCT(7);
+        // A22 -= v w^T + w v^T on the own rows (elements k < j <= i)
+        {
+            const int rg = tid >> 8, cg = tid & 255;
+            const float4 *ww4 = reinterpret_cast<const float4 *>(ww);
+            for (int j4 = j40 + cg; j4 < nj4; j4 += 256) {
+                const int j = 4 * j4;
+                const float4 vj = vv4[j4], wj = ww4[j4];          // zero for j <= k and j >= n
+                int r = (j - c + SCL - 1) / SCL;                  // first own row i >= j
+                if (r < 0) r = 0;
+                r += (rg - r % 4 + 4) % 4;
+                for (; r < R; r += 4) {
+                    const int i = SCL * r + c;
+                    float4 *px = reinterpret_cast<float4 *>(Aown + roff[r]) + j4;
+                    float4 a = *px;
+                    const float vi = vv[i], wi = ww[i];
+                    a.x = __fmaf_rn(-vi, wj.x, __fmaf_rn(-wi, vj.x, a.x));
+                    if (j + 1 <= i) a.y = __fmaf_rn(-vi, wj.y, __fmaf_rn(-wi, vj.y, a.y));
+                    if (j + 2 <= i) a.z = __fmaf_rn(-vi, wj.z, __fmaf_rn(-wi, vj.z, a.z));
+                    if (j + 3 <= i) a.w = __fmaf_rn(-vi, wj.w, __fmaf_rn(-wi, vj.w, a.w));
+                    *px = a;
+                }
+            }
+        }
+        __syncthreads();                                                 // updated rows
+        SCT(8);
+        if (tid < R) {                                                   // column k keeps the reflector
+            const int i = SCL * tid + c;
+            if (i >= k + 2) Aown[roff[tid] + k] = vv[i];
+            else if (i == k + 1) Aown[roff[tid] + k] = beta;
+        }
+        if (k + 3 < n) push_x(k + 1);                                    // next column (reads column k+1 only)
+        SCT(9);
+    }
+    __syncthreads();
+    // tail: d(n-2), d(n-1), e(n-2); tau(n-2) = tau(n-1) = 0
+    if (tid == 0) {
+        for (int i = (n >= 2 ? n - 2 : 0); i < n; ++i)
+            if (i % SCL == c) dout[i] = Aown[roff[i / SCL] + i];
+        if (n >= 2 && (n - 1) % SCL == c) eout[n - 2] = Aown[roff[(n - 1) / SCL] + (n - 2)];
+        if (c == 0) for (int i = (n >= 2 ? n - 2 : 0); i < n; ++i) tout[i] = 0.f;
+    }
+    // the reflectors back to A (below the subdiagonal, as the panel kernel leaves them)
+    for (int r = 0; r < R; ++r) {
+        const int i = SCL * r + c;
+        for (int kk = tid; kk <= i; kk += SCNT) A[i + (size_t)kk * ld] = Aown[roff[r] + kk];
+    }
+    sc_cluster_sync();                                                   // no CTA exits while peers may store into it
+}
+
+}  // namespace
+
 static mpj_status sytrd_run(float *A32, int64_t lda, int n, SymqrWs &w, int64_t np, cudaStream_t st)
 {
+    if (n >= 3 && n <= 1536) {          // the one-cluster kernel when the matrix fits its shared memory
+        const char *env = getenv("MPJ_SYTRD_CLUSTER");
+        const size_t smem = sc_smem(n);
+        bool use = !(env && env[0] == '0') && smem <= 227 * 1024 - 1024;
+        if (use) {
+            use = cudaFuncSetAttribute(k_sytrd_cluster, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) ==
+                      cudaSuccess &&
+                  smem_optin((const void *)k_sytrd_cluster, smem, SCNT, nullptr) == cudaSuccess;
+            cudaLaunchConfig_t cfg = {};
+            cudaLaunchAttribute at[1];
+            cfg.gridDim = dim3(SCL); cfg.blockDim = dim3(SCNT); cfg.dynamicSmemBytes = smem; cfg.stream = st;
+            at[0].id = cudaLaunchAttributeClusterDimension;
+            at[0].val.clusterDim.x = SCL; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
+            cfg.attrs = at; cfg.numAttrs = 1;
+            int ncl = 0;
+            if (use) use = cudaOccupancyMaxActiveClusters(&ncl, k_sytrd_cluster, &cfg) == cudaSuccess && ncl > 0;
+            cudaGetLastError();            // a refused size only selects the panel kernel
+            if (use) {
+                MPJ_CK(cudaMemsetAsync(w.d, 0, np * 4, st));
+                MPJ_CK(cudaMemsetAsync(w.e, 0, np * 4, st));
+                MPJ_CK(cudaMemsetAsync(w.tau, 0, np * 4, st));
+                const bool prof = prof_on();
+                if (prof) prof_mark("symqr_sytrd", st, true);
+                MPJ_CK(cudaLaunchKernelEx(&cfg, k_sytrd_cluster, A32, lda, n, w.d, w.e, w.tau));
+                if (prof) prof_mark("symqr_sytrd", st, false);
+                count_launch();
+                return MPJ_OK;
+            }
+        }
+    }
     const int nt = (int)(np / TB);
     // a grid sized to the work: small matrices pay per-column barrier and
     // reduction latency over every CTA, so they get ~8 tiles per CTA
@@ -1221,7 +1645,11 @@ static mpj_status sytrd_run(float *A32, int64_t lda, int n, SymqrWs &w, int64_t 
 static mpj_status tri_eig_run(int n, SymqrWs &w, double *Y, int64_t ldy, double *Dp, double *Dm, cudaStream_t st)
 {
     k_tri_prep<<<1, 1024, 0, st>>>(w.d, w.e, n, w.d64, w.e64, w.e2, w.bstart, w.bend, w.piv);
-    k_tri_bisect<<<(n + 256 / MSEC - 1) / (256 / MSEC), 256, 0, st>>>(w.d64, w.e64, w.e2, w.bstart, w.bend, w.piv, n,
+    if (n <= 2048)
+        k_tri_bisect<32><<<(n + 256 / 32 - 1) / (256 / 32), 256, 0, st>>>(w.d64, w.e64, w.e2, w.bstart, w.bend, w.piv,
+                                                                           n, w.lam);
+    else
+        k_tri_bisect<8><<<(n + 256 / 8 - 1) / (256 / 8), 256, 0, st>>>(w.d64, w.e64, w.e2, w.bstart, w.bend, w.piv, n,
                                                                      w.lam);
     k_tri_twisted<<<(2 * n + 127) / 128, 128, 0, st>>>(w.d64, w.e64, w.e2, w.bstart, w.bend, w.piv, w.lam, n, Dp,
                                                         Dm, w.inrm);
@@ -1244,7 +1672,7 @@ static mpj_status backtransform_run(const float *A32, int64_t lda, int n, SymqrW
                                                                                           np);
         count_launch();
         launch_dgemm(true, false, BT, BT, m, 1.0, w.Vp, np, w.Vp, np, 0.0, w.Gm, BT, st, w.skw, w.skw_elems);
-        const size_t tsm = ((size_t)BT * (BT + 1) + 3 * BT) * sizeof(double);
+        const size_t tsm = ((size_t)BT * (BT + 1) + 3 * BT + 3 * 32 * 32) * sizeof(double);
         MPJ_CK(smem_optin((const void *)k_build_tp, tsm, 256, nullptr));
         k_build_tp<<<1, 256, tsm, st>>>(w.Gm, w.tau, k0, nr, w.Tp);
         count_launch();

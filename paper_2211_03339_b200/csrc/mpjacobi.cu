@@ -55,21 +55,30 @@ void count_launch(long long k) { g_launches += k; }
 
 cudaError_t smem_optin(const void *func, size_t bytes, int threads, int *per_sm)
 {
+    // the attribute is a per-(function, device) MAXIMUM: only ever raised, so a
+    // launch with any size set before stays valid (a cache keyed by size alone
+    // would skip re-raising it after a smaller size lowered it)
     static std::mutex mu;
-    static std::map<std::tuple<const void *, int, size_t, int>, int> done;   // -> CTAs per SM
+    static std::map<std::pair<const void *, int>, size_t> attr;
+    static std::map<std::tuple<const void *, int, size_t, int>, int> occ_tab;   // -> CTAs per SM
     int dev = 0;
     cudaError_t e = cudaGetDevice(&dev);
     if (e != cudaSuccess) return e;
     std::lock_guard<std::mutex> lk(mu);
-    auto key = std::make_tuple(func, dev, bytes, threads);
-    auto it = done.find(key);
-    if (it == done.end()) {
+    auto ak = std::make_pair(func, dev);
+    auto ai = attr.find(ak);
+    if (ai == attr.end() || ai->second < bytes) {
         e = cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
         if (e != cudaSuccess) return e;
+        attr[ak] = bytes;
+    }
+    auto key = std::make_tuple(func, dev, bytes, threads);
+    auto it = occ_tab.find(key);
+    if (it == occ_tab.end()) {
         int occ = 0;
         e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, func, threads, bytes);
         if (e != cudaSuccess) return e;
-        it = done.emplace(key, std::max(1, occ)).first;
+        it = occ_tab.emplace(key, std::max(1, occ)).first;
     }
     if (per_sm) *per_sm = it->second;
     return cudaSuccess;

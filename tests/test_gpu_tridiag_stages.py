@@ -23,8 +23,9 @@ def mpj():
     return m
 
 
-@pytest.mark.parametrize("n", [3, 4, 63, 64, 65, 130, 257, 600])
-def test_sytrd_vs_oracle(mpj, orc, n):
+@pytest.mark.parametrize("path", ["cluster", "panel"])
+@pytest.mark.parametrize("n", [3, 4, 17, 63, 64, 65, 130, 257, 600, 1024, 1250])
+def test_sytrd_vs_oracle(mpj, orc, n, path, monkeypatch):
     """The reduction is backward stable, not forward stable: T is the Lanczos
     tridiagonal of A started at e_1 (implicit-Q theorem), whose later entries
     are ill-conditioned functions of A, so two valid rounding orders (blocked
@@ -34,7 +35,12 @@ def test_sytrd_vs_oracle(mpj, orc, n):
         and tau_0 as the oracle's (LAPACK convention, GvL 5.1.2);
       * T has the spectrum of fl32(A) (and of the oracle's T) to c n upsilon;
       * the GPU's stored reflectors, expanded by the oracle's orgtr, give an
-        orthogonal Q with Q^T fl32(A) Q = T to c n upsilon ||A||_F."""
+        orthogonal Q with Q^T fl32(A) Q = T to c n upsilon ||A||_F.
+    Both GPU reductions: the one-cluster kernel with the matrix resident in
+    distributed shared memory (n <= ~1250, the default there) and the panel
+    kernel (MPJ_SYTRD_CLUSTER=0)."""
+    if path == "panel":
+        monkeypatch.setenv("MPJ_SYTRD_CLUSTER", "0")
     A = rand_sym(n, 500 + n)
     A32 = A.astype(np.float32)
     d, e, tau, Aout = mpj.sytrd(torch.from_numpy(A32).cuda())

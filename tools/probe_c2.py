@@ -19,6 +19,8 @@ for kind, gen, mode in (("uniform", W.example1, 4), ("clustered", W.example2, 4)
             torch.cuda.synchronize(); ts.append(1e3 * (time.perf_counter() - t0))
             mpj.profile_enable(False)
         rep = r.report
-        ks = {k: round(1e3 * mpj.profile_get(k)[0], 2) for k in ("block_apply_f64", "block_solve_f64", "block_apply_f32", "block_solve_f32")}
+        ks = {k: round(1e3 * mpj.profile_get(k)[0], 2) for k in ("block_apply_f64", "block_solve_f64", "block_apply_f32",
+                                                                  "block_solve_f32", "symqr_sytrd", "symqr_trieig",
+                                                                  "symqr_backtransform")}
         print(kind, "plain" if plain else "mp", "ms/call", [round(t, 1) for t in ts], "sweeps", r.sweeps, rep.sweeps_low,
               "stages", round(rep.t_low * 1e3, 1), round(rep.t_orth * 1e3, 1), round(rep.t_precond * 1e3, 1), round(rep.t_jacobi * 1e3, 1), ks, flush=True)
