@@ -31,6 +31,7 @@
 #include "mpj_internal.h"
 
 #include <algorithm>
+#include <chrono>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -988,7 +989,33 @@ mpj_status mg_eig(bool mixed, const double *A, int64_t n, int64_t lda, double *L
     upload_colg(g);
     const int gx = std::max(1, std::min(64, (np + 255) / 256));
     mpj_status s = MPJ_OK;
-    if (mixed) {
+    if (mixed && cfg.low_solver != MPJ_LOW_JACOBI) {
+        // a1 by symmetric QR in binary32 (reading R12'), the default:
+        // every rank holds A, so every rank runs the single-GPU step 1 on it
+        // (sequential per column; the same Z bits on every rank), then a2 / a3
+        // exactly as below.  Scratch: A32, Z32, Y and D- here, D+ in `gath`.
+        float *A32 = (float *)alloc((size_t)np * np * 4), *Z32 = (float *)alloc((size_t)np * np * 4);
+        double *Y = (double *)alloc((size_t)np * np * 8), *Dm = (double *)alloc((size_t)np * np * 8);
+        void *sws = alloc(symqr_workspace(np));
+        if (oom) { set_error("mg: out of device memory (symmetric-QR step 1)"); return MPJ_ERR_NOMEM; }
+        launch_copy_pad<double, float>(g.As, np, (int)n, (int)n, A32, np, (int)n, (int)n, g.st);
+        const auto t0 = std::chrono::steady_clock::now();
+        MPJ_TRY(low_evd_symqr(A32, np, (int)n, Z32, np, Y, np, gath, Dm, sws, g.st));
+        launch_copy_pad<float, double>(Z32, np, (int)n, (int)n, full, np, np, np, g.st);
+        MPJ_CK(cudaStreamSynchronize(g.st));
+        rep.t_low = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+        rep.sweeps_low = 0; rep.rotations_low = 0; rep.status_low = MPJ_OK;
+        s = orth_cgs2(full, np, full, np, n, n, orth_ws, g.st);
+        if (s != MPJ_OK) return s;
+        for (int i = 0; i < g.nlocal; ++i) {
+            gather_cols<double, double>(full, np, g.rk[i].colg, np, ncl, g.rk[i].V, np, g.st);
+            launch_dgemm(false, false, np, ncl, np, 1.0, g.As, np, g.rk[i].V, np, 0.0, W, np, g.st);
+            launch_dgemm(true, false, np, ncl, np, 1.0, full, np, W, np, 0.0, g.rk[i].T, np, g.st);
+        }
+        double off0 = 0;
+        MPJ_TRY(mg_norm<double>(g, true, Ts.data(), off0));
+        rep.off0 = off0;
+    } else if (mixed) {
         // a1: fp32 stage on the column partition (reading R12)
         for (int i = 0; i < g.nlocal; ++i) {
             gather_cols<double, float>(g.As, np, g.rk[i].colg, np, ncl, g.rk[i].T32, np, g.st);

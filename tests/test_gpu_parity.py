@@ -524,20 +524,30 @@ def test_svd_host_buffers_and_errors(mpj):
 
 
 # ----------------------------------------------------------------- multi-GPU partition (emulated ranks)
+@pytest.mark.parametrize("low", ["jacobi", "symqr"])
 @pytest.mark.parametrize("n,mode", [(256, 4), (512, 3), (200, 5)])
-def test_eig_mg_emulated(mpj, orc, n, mode):
+def test_eig_mg_emulated(mpj, orc, n, mode, low):
     """the column-block partitioned Alg. 3 (slots split over G
     ranks, U all-gather, boundary block exchange, off-norm all-reduce) run as
     G ranks inside one process on one GPU.  vs the oracle (same b = 32
-    ordering): north_star tolerances and sweep counts (R20); and G-invariance:
-    G = 1, 2, 4 give the same eigenvalues to rounding."""
+    ordering, same step 1): north_star tolerances and sweep counts (R20 with
+    the fp32 Jacobi step 1 run on the partition; within one with the
+    replicated symmetric-QR step 1, whose Z differs from the oracle's at the
+    binary32 rounding level); and G-invariance: G = 1, 2, 4 give the same
+    eigenvalues to rounding."""
     A, lam_true = W.example1(n, 1e3, mode, W.seed_for(4, mode, 1e3))
-    ref = orc.mp_evd(A, orc.default_cfg("eig", b=32, low_solver=orc.LOW_JACOBI))   # mg: fp32 Jacobi step 1
+    jac = low == "jacobi"
+    ref = orc.mp_evd(A, orc.default_cfg("eig", b=32, low_solver=orc.LOW_JACOBI if jac else orc.LOW_SYMQR))
+    cfg = mpj.default_config("eig", low_solver=mpj.LOW_JACOBI if jac else mpj.LOW_SYMQR)
     lams = []
     for G in (1, 2, 4):
-        res = mpj.eig_mg(dev(A), emulate_ranks=G)
-        _check_evd(A, host(res.lam), host(res.V), ref.lam, ref.report.sweeps, res.sweeps,
-                   list(res.report.off_hist), list(ref.report.off_hist))
+        res = mpj.eig_mg(dev(A), cfg, emulate_ranks=G)
+        if jac:
+            _check_evd(A, host(res.lam), host(res.V), ref.lam, ref.report.sweeps, res.sweeps,
+                       list(res.report.off_hist), list(ref.report.off_hist))
+        else:
+            _check_evd(A, host(res.lam), host(res.V), ref.lam, res.sweeps, res.sweeps)
+            assert abs(res.sweeps - ref.report.sweeps) <= 1 and res.report.sweeps_low == 0
         lams.append(host(res.lam))
     assert np.max(np.abs(lams[1] - lams[0])) <= 1e-14 * np.abs(lams[0]).max()
     assert np.max(np.abs(lams[2] - lams[0])) <= 1e-14 * np.abs(lams[0]).max()
