@@ -14,11 +14,13 @@
 //   a3  T = Q^T As Q on the FP64 tensor pipe (two 64^3 DMMA tile products),
 //       symmetrised (R11)
 //   a4-a8 fp64 sweeps on T with V = Q, stop test ||off(T)||_F <= eps ||As||_F
+//       (inner_rounds_pipe: the next round's parameters computed by one warp
+//       while the other seven apply the current round out of place)
 //   a10 lambda = diag(T) stable-descending, V's columns alike.
 // a1 runs as its own kernel (k_batched_symqr: 49 KB of shared memory -> 4
 // CTAs per SM; k_batched_low: T32 and V32 only, 35 KB -> 5 CTAs per SM); the
-// rest (a0, a2-a10) in k_batched_evd: three
-// 64 x 68 fp64 panels (104 KB) -> 2 CTAs per SM.
+// rest (a0, a2-a10) in k_batched_evd: two
+// 64 x 68 fp64 panels (70 KB; As is re-formed from A for a3) -> 3 CTAs per SM.
 #include "mpj_block.cuh"
 #include "mpj_device.cuh"
 #include "mpj_internal.h"
@@ -452,35 +454,28 @@ __global__ void __launch_bounds__(NT, 4) k_batched_symqr(BatchedArgs a)
     if (tid == 0 && a.sweeps_low) a.sweeps_low[mat] = 0;
 }
 
-__global__ void __launch_bounds__(NT, 2) k_batched_evd(BatchedArgs a)
+__global__ void __launch_bounds__(NT, 3) k_batched_evd(BatchedArgs a)
 {
     constexpr int LD = Lay<double>::LD;
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    double *RA = (double *)smem_raw;   // As, later T
-    double *RB = RA + TW * LD;         // A staging, later Q = V
-    double *RC = RB + TW * LD;         // T32/V32, later W
+    double *RA = (double *)smem_raw;   // U (step 2), then As, W, T
+    double *RB = RA + TW * LD;         // Z, then Q = V
     __shared__ double red[NT / 32];
     __shared__ double coef[TW];
-    __shared__ InnerSharedB sh;
-    __shared__ InnerParams<double> pd;
+    __shared__ WideParams<double> PP[2];
+    __shared__ PipeMaps pm;
     __shared__ int rank_[TW];
     const int n = a.n, tid = threadIdx.x;
     const size_t mat = blockIdx.x;
     const double *Ag = a.A + mat * (size_t)n * n;
-    const int2 bp = make_int2(0, 1);   // one block pair: local index == global index
-
-    // a0
-    for (int e = tid; e < TW * TW; e += NT) {
-        const int i = e & (TW - 1), j = e >> 6;
-        RB[i + j * LD] = (i < n && j < n) ? Ag[i + (size_t)j * n] : 0.0;
+    // As = (A + A^T) / 2 (formed when needed, a3), ||As||_F, finiteness
+    auto as_at = [&](int i, int j) { return (Ag[i + (size_t)j * n] + Ag[j + (size_t)i * n]) * 0.5; };
+    double acc0 = 0.0;
+    for (int e = tid; e < n * n; e += NT) {
+        const double x = as_at(e % n, e / n);
+        acc0 = __fma_rn(x, x, acc0);
     }
-    __syncthreads();
-    for (int e = tid; e < TW * TW; e += NT) {
-        const int i = e & (TW - 1), j = e >> 6;
-        RA[i + j * LD] = (RB[i + j * LD] + RB[j + i * LD]) * 0.5;
-    }
-    __syncthreads();
-    const double normA = sqrt(sq_norm<double>(RA, false, red));
+    const double normA = sqrt(cta_sum(acc0, red));
     if (!isfinite(normA)) {                  // NaN / Inf input: flagged, no sweeps
         if (tid == 0) atomicOr(a.flag, 4);
         return;
@@ -517,13 +512,13 @@ __global__ void __launch_bounds__(NT, 2) k_batched_evd(BatchedArgs a)
         series = nE <= 1e-4;
         if (series) {
             auto phi = [&](int i, int j, double x) {
-                RC[i + j * LD] = i < j ? x : (i == j ? 0.5 * x : 0.0);
+                RA[i + j * LD] = i < j ? x : (i == j ? 0.5 * x : 0.0);
             };
             E.each(phi);                                         // U0 = Phi(E)
             __syncthreads();
             for (int it = 0; it < 2; ++it) {                     // U <- Phi(E - U^T U)
                 Acc<double> P;
-                tile_mm<true>(RC, RC, P);
+                tile_mm<true>(RA, RA, P);
                 __syncthreads();
                 #pragma unroll
                 for (int mi = 0; mi < 2; ++mi)
@@ -539,7 +534,7 @@ __global__ void __launch_bounds__(NT, 2) k_batched_evd(BatchedArgs a)
             S.each_ref([&](int i, int j, double &x) { x = RB[i + j * LD]; });
             for (int t = 1; t <= 3; ++t) {
                 Acc<double> Y;
-                tile_mm<false>(RB, RC, Y);
+                tile_mm<false>(RB, RA, Y);
                 __syncthreads();
                 const double sg = (t & 1) ? -1.0 : 1.0;
                 #pragma unroll
@@ -604,15 +599,20 @@ __global__ void __launch_bounds__(NT, 2) k_batched_evd(BatchedArgs a)
         bad = 0;
     }
 
-    // a3: T = Q^T (As Q), symmetrised
+    // a3: T = Q^T (As Q), symmetrised (As into RA, W = As Q over it)
     {
+        for (int e = tid; e < TW * TW; e += NT) {
+            const int i = e & (TW - 1), j = e >> 6;
+            RA[i + j * LD] = (i < n && j < n) ? as_at(i, j) : 0.0;
+        }
+        __syncthreads();
         Acc<double> w;
         tile_mm<false>(RA, RB, w);       // W = As Q
         __syncthreads();
-        w.each([&](int i, int j, double x) { RC[i + j * LD] = x; });
+        w.each([&](int i, int j, double x) { RA[i + j * LD] = x; });
         __syncthreads();
         Acc<double> t;
-        tile_mm<true>(RB, RC, t);        // T = Q^T W
+        tile_mm<true>(RB, RA, t);        // T = Q^T W
         __syncthreads();
         t.each([&](int i, int j, double x) { RA[i + j * LD] = x; });
         __syncthreads();
@@ -651,20 +651,23 @@ __global__ void __launch_bounds__(NT, 2) k_batched_evd(BatchedArgs a)
     const double tol = a.eps * normA;
     int sw = 0;
     bool conv = false;
+    double *Tc = RA, *Vc = RB;               // the rounds swap the two buffers
     for (;;) {
-        const double off = sqrt(sq_norm<double, LR>(RA, true, red));
+        const double off = sqrt(sq_norm<double, LR>(Tc, true, red));
         if (off <= tol) { conv = true; break; }
         if (sw >= a.max_sweeps) break;
         ++sw;
-        inner_rounds_b<double, LR>(RA, RB, true, a.lsched, a.nu, a.rule, sh, pd);
+        double *uo;
+        Tc = inner_rounds_pipe<double>(Tc, Vc, a.lsched, a.nu, a.rule, PP, pm, &uo);
+        Vc = uo;
     }
 
     // a10: extraction (stable descending rank)
     if (tid < n) {
-        const double di = RA[tid + tid * LR];
+        const double di = Tc[tid + tid * LR];
         int r = 0;
         for (int j = 0; j < n; ++j) {
-            const double dj = RA[j + j * LR];
+            const double dj = Tc[j + j * LR];
             r += (dj > di) || (dj == di && j < tid);
         }
         rank_[tid] = r;
@@ -674,7 +677,7 @@ __global__ void __launch_bounds__(NT, 2) k_batched_evd(BatchedArgs a)
     double *Vg = a.V + mat * (size_t)n * n;
     for (int e = tid; e < n * n; e += NT) {
         const int i = e % n, j = e / n;
-        Vg[i + (size_t)rank_[j] * n] = RB[i + j * LR];
+        Vg[i + (size_t)rank_[j] * n] = Vc[i + j * LR];
     }
     if (tid == 0) {
         if (a.sweeps) a.sweeps[mat] = sw;
@@ -713,7 +716,7 @@ mpj_status batched_evd(const double *A, int64_t n, int64_t batch, double *Lambda
     a.eps = cfg.eps_factor * omega; a.nu = cfg.nu_factor * omega;
     a.eps_low = eps_low_factor(cfg, n) * upsilon; a.nu_low = cfg.nu_low_factor * upsilon;
     a.max_sweeps = cfg.max_sweeps; a.max_sweeps_low = cfg.max_sweeps_low; a.rule = cfg.stop_rule;
-    const int smem = 3 * TW * Lay<double>::LD * sizeof(double);
+    const int smem = 2 * TW * Lay<double>::LD * sizeof(double);
     const int smem_low = 2 * TW * LayK<float>::LD * sizeof(float);
     MPJ_CK(smem_optin((const void *)k_batched_evd, smem, NT, nullptr));
     MPJ_CK(smem_optin((const void *)k_batched_symqr, kSymqrSmem, NT, nullptr));

@@ -507,6 +507,158 @@ __device__ __forceinline__ R *smem_rounds_wide(R *D0, R *D1, R *U, int2 bp, bool
     return Dc;
 }
 
+// ---------------------------------------------------------------------------
+// One full sweep of the rounds of the single block pair bp = (0, 1) with NT =
+// 256 threads, pipelined as smem_rounds_wide: warp 7 computes round s+1's
+// parameters from D before round s (the after-round formulas diag_after /
+// tile_after, the very arithmetic of the update) while warps 0-6 apply round s
+// out of place (Dc -> Dn).  One barrier per round instead of two, and the
+// parameter latency (divides, square roots) off the critical path.  U in
+// registers exactly as inner_rounds_b (warp w: rows w + 8 i).  D0, D1 and U in
+// LayK layout (LD 65); U may alias D1 (it is read into registers first and
+// written back to the buffer that does not hold the final D).  Results are
+// bit-identical to inner_rounds_b.  Returns the buffer holding the final D
+// (*uout: the one holding U).
+struct PipeMaps {      // bytes: three CTAs of the batched kernel share an SM's shared memory
+    unsigned char part_t[2][BW], part_b[2][BW], pair_t[2][BW], pair_b[2][BW], isp_t[2][BW], isp_b[2][BW];
+};
+
+template <typename R>
+__device__ __forceinline__ R *inner_rounds_pipe(R *D0, R *D1, const int2 *__restrict__ lsched, R nu, int rule,
+                                                WideParams<R> (&PP)[2], PipeMaps &pm, R **uout)
+{
+    constexpr int LD = LayK<R>::LD;
+    constexpr int NU = NT - 32;                          // update threads (warps 0-6)
+    constexpr int NI = BW + BW * (BW - 1) / 2;           // tile items: 32 diagonal + 496 pair tiles
+    constexpr int NE = (NI + NU - 1) / NU;
+    const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+    const bool pwarp = w == NT / 32 - 1;
+    R *U = D1;
+    R ut[8], ub[8];
+    #pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        ut[i] = U[(w + 8 * i) + lane * LD];
+        ub[i] = U[(w + 8 * i) + (BW + lane) * LD];
+    }
+    int tk[NE], tl[NE];
+    #pragma unroll
+    for (int u = 0; u < NE; ++u) {
+        const int wt = tid + NU * u - BW;
+        int ll = -1, kk = 0;
+        if (wt >= 0 && wt < BW * (BW - 1) / 2) {
+            ll = (int)((1.0f + sqrtf(1.0f + 8.0f * wt)) * 0.5f);
+            while (ll * (ll - 1) / 2 > wt) --ll;
+            while ((ll + 1) * ll / 2 <= wt) ++ll;
+            kk = wt - ll * (ll - 1) / 2;
+        }
+        tk[u] = kk; tl[u] = ll;
+    }
+    // parameters (and the intra-round partner maps) of round s into buffer b;
+    // s = 0 from D itself, later from Dc after round s-1 (params P)
+    auto params = [&](int s, int b, const R *Dc, const WideParams<R> *P) {
+        const bool in_intra = s < BW - 1;
+        int a, c;
+        round_pair(s, lane, true, lsched, a, c);
+        const int pn = a < c ? a : c, qn = a < c ? c : a;   // bp = (0, 1): local order == global order
+        R app, aqq, apq;
+        if (!P) {
+            app = Dc[pn + pn * LD]; aqq = Dc[qn + qn * LD]; apq = Dc[pn + qn * LD];
+        } else {
+            app = diag_after<R, false>(Dc, *P, pn);
+            aqq = diag_after<R, false>(Dc, *P, qn);
+            const int k = P->pos[pn], l = P->pos[qn];
+            R x11, x21, x12, x22;
+            if (k < l) {
+                tile_after<R, false>(Dc, *P, k, l, x11, x21, x12, x22);
+                apq = (pn == P->p[k]) ? (qn == P->p[l] ? x11 : x12) : (qn == P->p[l] ? x21 : x22);
+            } else {
+                tile_after<R, false>(Dc, *P, l, k, x11, x21, x12, x22);
+                apq = (qn == P->p[l]) ? (pn == P->p[k] ? x11 : x12) : (pn == P->p[k] ? x21 : x22);
+            }
+        }
+        R t, sk, uk;
+        rot_params<R>(app, aqq, apq, nu, rule, t, sk, uk);
+        WideParams<R> &N = PP[b];
+        N.t[lane] = t; N.s[lane] = sk; N.u[lane] = uk;
+        N.p[lane] = pn; N.q[lane] = qn; N.gp[lane] = pn;
+        N.pos[pn] = lane; N.pos[qn] = lane;
+        if (in_intra) {
+            if (lane < BW / 2) {
+                pm.part_t[b][pn] = qn; pm.part_t[b][qn] = pn; pm.pair_t[b][pn] = lane; pm.pair_t[b][qn] = lane;
+                pm.isp_t[b][pn] = 1; pm.isp_t[b][qn] = 0;
+            } else {
+                pm.part_b[b][pn - BW] = qn - BW; pm.part_b[b][qn - BW] = pn - BW;
+                pm.pair_b[b][pn - BW] = lane; pm.pair_b[b][qn - BW] = lane;
+                pm.isp_b[b][pn - BW] = 1; pm.isp_b[b][qn - BW] = 0;
+            }
+        }
+    };
+    __syncthreads();                                     // U in registers: D1 is free
+    if (pwarp) params(0, 0, D0, nullptr);
+    __syncthreads();
+    constexpr int NR = (BW - 1) + BW;
+    R *Dc = D0, *Dn = D1;
+    for (int s = 0; s < NR; ++s) {
+        const int b = s & 1;
+        const WideParams<R> &P = PP[b];
+        const bool in_intra = s < BW - 1;
+        if (pwarp) {
+            if (s + 1 < NR) params(s + 1, b ^ 1, Dc, &P);
+        } else {
+            #pragma unroll
+            for (int u = 0; u < NE; ++u) {
+                const int e = tid + NU * u;
+                if (e >= NI) break;
+                if (e < BW) {
+                    const int pk = P.p[e], qk = P.q[e];
+                    const R apq = Dc[pk + qk * LD], t = P.t[e];
+                    Dn[pk + pk * LD] = fmaR(-t, apq, Dc[pk + pk * LD]);
+                    Dn[qk + qk * LD] = fmaR(t, apq, Dc[qk + qk * LD]);
+                    Dn[pk + qk * LD] = R(0);
+                    Dn[qk + pk * LD] = R(0);
+                } else {
+                    R x11, x21, x12, x22;
+                    tile_after<R, false>(Dc, P, tk[u], tl[u], x11, x21, x12, x22);
+                    const int pk = P.p[tk[u]], qk = P.q[tk[u]], pl = P.p[tl[u]], ql = P.q[tl[u]];
+                    Dn[pk + pl * LD] = x11; Dn[qk + pl * LD] = x21; Dn[pk + ql * LD] = x12; Dn[qk + ql * LD] = x22;
+                    Dn[pl + pk * LD] = x11; Dn[pl + qk * LD] = x21; Dn[ql + pk * LD] = x12; Dn[ql + qk * LD] = x22;
+                }
+            }
+        }
+        // U <- U J in registers (every warp: its rows)
+        if (in_intra) {
+            const int pt = pm.part_t[b][lane], pb = pm.part_b[b][lane];
+            const int jt = pm.pair_t[b][lane], jb = pm.pair_b[b][lane];
+            const bool it = pm.isp_t[b][lane] != 0, ib = pm.isp_b[b][lane] != 0;
+            const R st = P.s[jt], tt = P.u[jt], sb = P.s[jb], tb = P.u[jb];
+            #pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                const R ot = __shfl_sync(0xffffffffu, ut[i], pt), ob = __shfl_sync(0xffffffffu, ub[i], pb);
+                if (st != R(0)) rot_side<R>(st, tt, it, ut[i], ot);
+                if (sb != R(0)) rot_side<R>(sb, tb, ib, ub[i], ob);
+            }
+        } else {
+            const R sk = P.s[lane], tk2 = P.u[lane];
+            #pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                if (sk != R(0)) rot<R>(sk, tk2, ut[i], ub[i]);   // p = a_k (top), q = b_k
+                ub[i] = __shfl_sync(0xffffffffu, ub[i], (lane + 1) & 31);
+            }
+        }
+        __syncthreads();
+        R *tmp = Dc; Dc = Dn; Dn = tmp;
+    }
+    // U back into the buffer that does not hold D
+    #pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        Dn[(w + 8 * i) + lane * LD] = ut[i];
+        Dn[(w + 8 * i) + (BW + lane) * LD] = ub[i];
+    }
+    __syncthreads();
+    *uout = Dn;
+    return Dc;
+}
+
 // K3's inner rounds: the intra-block rounds of block round 0 in shared memory
 // (their pairs follow the local schedule), then the cross rounds with U in
 // registers.
