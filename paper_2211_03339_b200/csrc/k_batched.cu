@@ -721,7 +721,6 @@ mpj_status batched_evd(const double *A, int64_t n, int64_t batch, double *Lambda
     MPJ_CK(smem_optin((const void *)k_batched_evd, smem, NT, nullptr));
     MPJ_CK(smem_optin((const void *)k_batched_symqr, kSymqrSmem, NT, nullptr));
     const bool prof = prof_on();
-    if (prof) prof_mark("batched_evd", st, true);
     for (int64_t b0 = 0; b0 < batch; b0 += kChunk) {
         BatchedArgs ab = a;
         const int64_t nb = std::min<int64_t>(kChunk, batch - b0);
@@ -731,15 +730,18 @@ mpj_status batched_evd(const double *A, int64_t n, int64_t batch, double *Lambda
         if (Zin) ab.Z = const_cast<float *>(Zin) + b0 * n * n;      // read only (k_batched_evd)
         else if (Zout) ab.Z = Zout + b0 * n * n;
         if (!Zin) {
+            if (prof) prof_mark("batched_step1", st, true);
             if (cfg.low_solver == MPJ_LOW_JACOBI) k_batched_low<<<(unsigned)nb, NT, smem_low, st>>>(ab);
             else k_batched_symqr<<<(unsigned)nb, NT, kSymqrSmem, st>>>(ab);
+            if (prof) prof_mark("batched_step1", st, false);
             count_launch();
         }
+        if (prof) prof_mark("batched_evd_f64", st, true);
         k_batched_evd<<<(unsigned)nb, NT, smem, st>>>(ab);
+        if (prof) prof_mark("batched_evd_f64", st, false);
         count_launch();
         MPJ_CK(cudaGetLastError());
     }
-    if (prof) prof_mark("batched_evd", st, false);
     int h_flag = 0;
     MPJ_CK(cudaMemcpyAsync(&h_flag, flag, sizeof(int), cudaMemcpyDeviceToHost, st));
     MPJ_CK(cudaStreamSynchronize(st));

@@ -35,6 +35,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdlib>
+#include <map>
 #include <mutex>
 
 namespace mpj {
@@ -1563,19 +1564,32 @@ static mpj_status sytrd_run(float *A32, int64_t lda, int n, SymqrWs &w, int64_t 
         const char *env = getenv("MPJ_SYTRD_CLUSTER");
         const size_t smem = sc_smem(n);
         bool use = !(env && env[0] == '0') && smem <= 227 * 1024 - 1024;
+        cudaLaunchConfig_t cfg = {};
+        cudaLaunchAttribute at[1];
+        cfg.gridDim = dim3(SCL); cfg.blockDim = dim3(SCNT); cfg.dynamicSmemBytes = smem; cfg.stream = st;
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = SCL; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
+        cfg.attrs = at; cfg.numAttrs = 1;
         if (use) {
-            use = cudaFuncSetAttribute(k_sytrd_cluster, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) ==
-                      cudaSuccess &&
-                  smem_optin((const void *)k_sytrd_cluster, smem, SCNT, nullptr) == cudaSuccess;
-            cudaLaunchConfig_t cfg = {};
-            cudaLaunchAttribute at[1];
-            cfg.gridDim = dim3(SCL); cfg.blockDim = dim3(SCNT); cfg.dynamicSmemBytes = smem; cfg.stream = st;
-            at[0].id = cudaLaunchAttributeClusterDimension;
-            at[0].val.clusterDim.x = SCL; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
-            cfg.attrs = at; cfg.numAttrs = 1;
-            int ncl = 0;
-            if (use) use = cudaOccupancyMaxActiveClusters(&ncl, k_sytrd_cluster, &cfg) == cudaSuccess && ncl > 0;
-            cudaGetLastError();            // a refused size only selects the panel kernel
+            // whether a 16-CTA cluster with this much shared memory fits: asked once per
+            // (device, size) -- the occupancy query costs more than a small n's whole kernel
+            static std::mutex mu;
+            static std::map<std::pair<int, size_t>, bool> fits;
+            int dev = 0;
+            cudaGetDevice(&dev);
+            std::lock_guard<std::mutex> lk(mu);
+            auto key = std::make_pair(dev, smem);
+            auto it = fits.find(key);
+            if (it == fits.end()) {
+                bool ok = cudaFuncSetAttribute(k_sytrd_cluster, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) ==
+                              cudaSuccess &&
+                          smem_optin((const void *)k_sytrd_cluster, smem, SCNT, nullptr) == cudaSuccess;
+                int ncl = 0;
+                if (ok) ok = cudaOccupancyMaxActiveClusters(&ncl, k_sytrd_cluster, &cfg) == cudaSuccess && ncl > 0;
+                cudaGetLastError();        // a refused size only selects the panel kernel
+                it = fits.emplace(key, ok).first;
+            }
+            use = it->second && smem_optin((const void *)k_sytrd_cluster, smem, SCNT, nullptr) == cudaSuccess;
             if (use) {
                 MPJ_CK(cudaMemsetAsync(w.d, 0, np * 4, st));
                 MPJ_CK(cudaMemsetAsync(w.e, 0, np * 4, st));
