@@ -259,6 +259,23 @@ mpj_status mpjacobi_svd_z(const double *A, int64_t m, int64_t n, int64_t lda, co
                           void *workspace, size_t ws_bytes, void *stream, const mpj_config *cfg, mpj_report *rep);
 
 /* ------------------------------------------------------------------------
+ * Multi-GPU Alg. 5 (the column partition of Alg. 5's
+ * one-sided rotations): one call per rank (NCCL communicator from
+ * mpjacobi_nccl_unique_id, as mpjacobi_eig_mg), or emulate_ranks = G ranks
+ * inside one process (nccl_id NULL; device copies instead of NCCL).  Rank g
+ * runs the block-pair slots [g mb/G, (g+1) mb/G) of every block round (mb =
+ * n_p/64); the 32-column blocks that move to another rank's slot are sent
+ * there (ncclSend / ncclRecv), every block is broadcast from its owner before
+ * each sweep's stop test; steps 2-3 (Q = orth(Z), C = A Q) are replicated.
+ * Bit-identical to mpjacobi_svd when n is a multiple of 64 G (same padding).
+ *   A: m x n (lda >= m), host or device, the same bits on every rank;
+ *   Sigma (n), U (m x n, ldu), V (n x n, ldv): DEVICE, replicated on every
+ *   rank.  Errors as mpjacobi_svd; MPJ_ERR_NCCL from NCCL. */
+mpj_status mpjacobi_svd_mg(const double *A, int64_t m, int64_t n, int64_t lda, double *Sigma, double *U,
+                           int64_t ldu, double *V, int64_t ldv, int *sweeps, const void *nccl_id, int rank,
+                           int nranks, int emulate_ranks, void *stream, const mpj_config *cfg, mpj_report *rep);
+
+/* ------------------------------------------------------------------------
  * Batched Alg. 3: `batch` independent n x n matrices, contiguous with stride
  * n*n (each column-major), one matrix per CTA (n <= 64).  Lambda: batch x n;
  * V: batch x n x n (each column-major); sweeps / sweeps_low: batch ints

@@ -125,6 +125,9 @@ def lib():
         L.mpjacobi_eig_mg.restype = C.c_int
         L.mpjacobi_eig_mg.argtypes = [_vp, _i64, _i64, _vp, _vp, _i64, C.POINTER(C.c_int), _vp, C.c_int, C.c_int,
                                       C.c_int, _vp, cfgp, repp]
+        L.mpjacobi_svd_mg.restype = C.c_int
+        L.mpjacobi_svd_mg.argtypes = [_vp, _i64, _i64, _i64, _vp, _vp, _i64, _vp, _i64, C.POINTER(C.c_int), _vp,
+                                      C.c_int, C.c_int, C.c_int, _vp, cfgp, repp]
         L.mpjacobi_mg_plan.restype = C.c_int
         L.mpjacobi_mg_plan.argtypes = [_i64, C.c_int, C.POINTER(C.c_int), C.POINTER(C.c_int), _vp, _vp, _vp]
         L.mpjacobi_nccl_unique_id.restype = C.c_int
@@ -146,6 +149,7 @@ EXPORTED = (
     "mpjacobi_profile_enable", "mpjacobi_profile_reset", "mpjacobi_profile_get",
     "mpjacobi_eig_mg", "mpjacobi_nccl_unique_id", "mpjacobi_mg_plan", "mpjacobi_eig_z", "mpjacobi_svd_z",
     "mpjacobi_sytrd", "mpjacobi_tridiag_eig", "mpjacobi_orth_householder", "mpjacobi_eig_batched_z",
+    "mpjacobi_svd_mg",
 )
 
 
@@ -503,7 +507,31 @@ def mpjacobi_eig_mg(A, cfg: mpj_config | None = None, *, nccl_id: bytes | None =
     return EigResult(lam, V, sw.value, rep)
 
 
+def mpjacobi_svd_mg(A, cfg: mpj_config | None = None, *, nccl_id: bytes | None = None, rank: int = 0,
+                    nranks: int = 1, emulate_ranks: int = 1, allow_noconv=False) -> SvdResult:
+    """Multi-GPU Alg. 5 (column partition of the one-sided rotations,
+    SURVEY 8(f) row 2): one call per rank with nccl_id, or `emulate_ranks`
+    ranks inside this process.  A (m, n), m >= n, float64 (host or device, the
+    same on every rank); Sigma, U, V returned on the current GPU, replicated."""
+    m, n = A.shape
+    if A.dtype != torch.float64 or m < n:
+        raise ValueError("A must be float64 with m >= n")
+    Acm = colmajor(A)
+    sig = torch.empty(n, dtype=torch.float64, device="cuda")
+    U = empty_colmajor(m, n, device="cuda")
+    V = empty_colmajor(n, n, device="cuda")
+    cfg = cfg or default_config("svd")
+    rep = mpj_report()
+    sw = C.c_int(0)
+    idbuf = C.create_string_buffer(nccl_id, 128) if nccl_id is not None else None
+    st = lib().mpjacobi_svd_mg(_ptr(Acm), m, n, Acm.stride(1), _ptr(sig), _ptr(U), U.stride(1), _ptr(V), V.stride(1),
+                               C.byref(sw), idbuf, rank, nranks, emulate_ranks, _stream(), C.byref(cfg), C.byref(rep))
+    _check(st, (MPJ_OK, MPJ_ERR_NOCONV) if allow_noconv else (MPJ_OK,))
+    return SvdResult(sig, U, V, sw.value, rep, None)
+
+
 # short aliases
+svd_mg = mpjacobi_svd_mg
 eig_mg = mpjacobi_eig_mg
 eig_batched = mpjacobi_eig_batched
 svd = mpjacobi_svd

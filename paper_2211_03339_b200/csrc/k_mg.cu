@@ -34,6 +34,7 @@
 #include <chrono>
 #include <cstring>
 #include <map>
+#include <mutex>
 #include <memory>
 #include <vector>
 
@@ -644,6 +645,7 @@ struct Group {
 };
 
 static std::map<std::string, ncclComm_t> g_comms;
+static std::mutex g_comms_mu;
 
 mpj_status nccl_ck(ncclResult_t r, const char *what)
 {
@@ -855,6 +857,25 @@ static mpj_status mg_loop(Group &g, R **Ts, R **Vs, double tol, R nu, int rule, 
 
 }  // namespace
 
+// the communicator of (unique id, rank, nranks), created once per process
+mpj_status mg_comm(const void *nccl_id, int rank, int nranks, void **out)
+{
+    std::lock_guard<std::mutex> lk(g_comms_mu);
+    std::string key((const char *)nccl_id, 128);
+    key += std::to_string(rank) + "/" + std::to_string(nranks);
+    auto it = g_comms.find(key);
+    if (it == g_comms.end()) {
+        ncclUniqueId id;
+        std::memcpy(&id, nccl_id, sizeof(id));
+        ncclComm_t c;
+        MPJ_TRY(nccl_ck(ncclCommInitRank(&c, nranks, id, rank), "ncclCommInitRank"));
+        it = g_comms.emplace(key, c).first;
+    }
+    *out = (void *)it->second;
+    return MPJ_OK;
+}
+
+
 // local-columns gather of a full matrix: dst(:, j) = src(:, colg[j]) (colg on device)
 template <typename Rs, typename Rd>
 static void gather_cols(const Rs *src, int64_t lds, const int *colg, int rows, int ncols, Rd *dst, int64_t ldd,
@@ -912,17 +933,9 @@ mpj_status mg_eig(bool mixed, const double *A, int64_t n, int64_t lda, double *L
     const int np = g.np, ncl = g.ncl, mb = g.plan.mb;
     rep.n_padded = np; rep.block_b = BW; rep.variant = MPJ_VARIANT_BLOCK;
     if (use_nccl) {
-        std::string key((const char *)nccl_id, 128);
-        key += std::to_string(rank) + "/" + std::to_string(nranks);
-        auto it = g_comms.find(key);
-        if (it == g_comms.end()) {
-            ncclUniqueId id;
-            std::memcpy(&id, nccl_id, sizeof(id));
-            ncclComm_t c;
-            MPJ_TRY(nccl_ck(ncclCommInitRank(&c, nranks, id, rank), "ncclCommInitRank"));
-            it = g_comms.emplace(key, c).first;
-        }
-        g.comm = it->second;
+        void *c = nullptr;
+        MPJ_TRY(mg_comm(nccl_id, rank, nranks, &c));
+        g.comm = (ncclComm_t)c;
     }
     // stream-ordered allocations, released on every exit
     std::vector<void *> owned;

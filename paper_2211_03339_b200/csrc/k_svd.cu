@@ -22,10 +22,13 @@
 #include "mpj_device.cuh"
 #include "mpj_internal.h"
 
+#include <nccl.h>
+
 #include <cmath>
 #include <algorithm>
 #include <cstdlib>
 #include <cstring>
+#include <vector>
 
 namespace mpj {
 namespace {
@@ -492,53 +495,62 @@ static void carve_svd(char *base, size_t &off, int64_t m, int64_t n, SvdPlan &p)
     p.orth_ws = take(orth_workspace(p.np));
 }
 
+// one block round Rb of the one-sided sweep on (C, V): Gram blocks of the
+// block pairs of ds (ds.nb / 2 slots), their inner solves, the column updates.
+// uid / nid: identity flags (ds.nb / 2) and this round's identity count.
 template <typename R>
-static mpj_status svd_block_sweep(SvdPlan &p, R *C, R *V, const DevSched &ds, R nu, cudaStream_t st, bool exact)
+static mpj_status svd_block_round(SvdPlan &p, R *C, R *V, const DevSched &ds, int Rb, R nu, cudaStream_t st,
+                                  bool exact, int *uid, int *nid)
 {
     exact = exact && sizeof(R) == 8;
     Sched S;
     S.bsched = ds.bsched; S.lsched = ds.lsched; S.b = ds.b; S.nb = ds.nb; S.np = ds.np;
+    const int mb = ds.nb / 2;
     constexpr int LD = Lay<R>::LD;
     const size_t sm_x = 2 * TW * LD * sizeof(R), sm_du = 3 * TW * LayK<R>::LD * sizeof(R);
-    MPJ_CK(cudaFuncSetAttribute(k_gram<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_x));
-    MPJ_CK(cudaFuncSetAttribute(k_svd_solve<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_du));
+    MPJ_CK(smem_optin((const void *)k_gram<R>, sm_x, NT, nullptr));
+    MPJ_CK(smem_optin((const void *)k_svd_solve<R>, sm_du, NTW, nullptr));
     const size_t sm_xx = 3 * TW * Lay<double>::LD * sizeof(double);
     if (exact) {
-        MPJ_CK(cudaFuncSetAttribute(k_gram_exact, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_xx));
-        MPJ_CK(cudaFuncSetAttribute(k_svd_solve<double, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    (int)sm_du));
+        MPJ_CK(smem_optin((const void *)k_gram_exact, sm_xx, NT, nullptr));
+        MPJ_CK(smem_optin((const void *)k_svd_solve<double, true>, sm_du, NTW, nullptr));
     }
     const bool prof = prof_on();
     const char *ng = sizeof(R) == 8 ? "svd_gram_f64" : "svd_gram_f32";
     const char *ns = sizeof(R) == 8 ? "svd_solve_f64" : "svd_solve_f32";
     const char *na = sizeof(R) == 8 ? "svd_apply_f64" : "svd_apply_f32";
-    int *uid = p.uid, *nid = p.uid + p.mb;
     const int splits = p.splits[sizeof(R) == 8], kc = p.kc[sizeof(R) == 8];
-    MPJ_CK(cudaMemsetAsync(nid, 0, (size_t)(ds.nb - 1) * sizeof(int), st));
-    for (int Rb = 0; Rb < ds.nb - 1; ++Rb) {
-        if (exact) {
-            if (prof) prof_mark("svd_gram_exact", st, true);
-            // column exponents: measured before the sweep's first round, then carried
-            // forward by k_svd_solve's bounds
-            if (Rb == 0) k_colexp<<<p.np, 256, 0, st>>>((const double *)C, p.ldc, (int)p.m, p.ex);
-            k_gram_exact<<<dim3(p.mb, p.splits[2]), NT, sm_xx, st>>>((const double *)C, p.ldc, (int)p.m, S, Rb,
-                                                                     p.kc[2], p.kbits, p.ex, p.Gpart, p.splits[2]);
-            if (prof) { prof_mark("svd_gram_exact", st, false); prof_mark(ns, st, true); }
-            k_svd_solve<double, true><<<p.mb, NTW, sm_du, st>>>(p.Gpart, p.splits[2], S, Rb, (double)nu,
-                                                                (double *)p.Ubuf, p.cnt, uid, nid + Rb, p.ex, p.kbits);
-            count_launch(Rb == 0 ? 3 : 2);
-        } else {
-            if (prof) prof_mark(ng, st, true);
-            k_gram<R><<<dim3(p.mb, splits), NT, sm_x, st>>>(C, p.ldc, (int)p.m, S, Rb, kc, p.Gpart, splits);
-            if (prof) { prof_mark(ng, st, false); prof_mark(ns, st, true); }
-            k_svd_solve<R><<<p.mb, NTW, sm_du, st>>>(p.Gpart, splits, S, Rb, nu, (R *)p.Ubuf, p.cnt, uid, nid + Rb);
-            count_launch(2);
-        }
-        if (prof) { prof_mark(ns, st, false); prof_mark(na, st, true); }
-        MPJ_CK(launch_block_apply_cols<R>(C, p.ldc, (int)p.m, ds, Rb, (const R *)p.Ubuf, st, uid, nid + Rb));
-        MPJ_CK(launch_block_apply_cols<R>(V, p.np, p.np, ds, Rb, (const R *)p.Ubuf, st, uid, nid + Rb));
-        if (prof) prof_mark(na, st, false);
+    if (exact) {
+        if (prof) prof_mark("svd_gram_exact", st, true);
+        // column exponents: measured before the sweep's first round, then carried
+        // forward by k_svd_solve's bounds
+        if (Rb == 0) k_colexp<<<p.np, 256, 0, st>>>((const double *)C, p.ldc, (int)p.m, p.ex);
+        k_gram_exact<<<dim3(mb, p.splits[2]), NT, sm_xx, st>>>((const double *)C, p.ldc, (int)p.m, S, Rb, p.kc[2],
+                                                               p.kbits, p.ex, p.Gpart, p.splits[2]);
+        if (prof) { prof_mark("svd_gram_exact", st, false); prof_mark(ns, st, true); }
+        k_svd_solve<double, true><<<mb, NTW, sm_du, st>>>(p.Gpart, p.splits[2], S, Rb, (double)nu, (double *)p.Ubuf,
+                                                          p.cnt, uid, nid, p.ex, p.kbits);
+        count_launch(Rb == 0 ? 3 : 2);
+    } else {
+        if (prof) prof_mark(ng, st, true);
+        k_gram<R><<<dim3(mb, splits), NT, sm_x, st>>>(C, p.ldc, (int)p.m, S, Rb, kc, p.Gpart, splits);
+        if (prof) { prof_mark(ng, st, false); prof_mark(ns, st, true); }
+        k_svd_solve<R><<<mb, NTW, sm_du, st>>>(p.Gpart, splits, S, Rb, nu, (R *)p.Ubuf, p.cnt, uid, nid);
+        count_launch(2);
     }
+    if (prof) { prof_mark(ns, st, false); prof_mark(na, st, true); }
+    MPJ_CK(launch_block_apply_cols<R>(C, p.ldc, (int)p.m, ds, Rb, (const R *)p.Ubuf, st, uid, nid));
+    MPJ_CK(launch_block_apply_cols<R>(V, p.np, p.np, ds, Rb, (const R *)p.Ubuf, st, uid, nid));
+    if (prof) prof_mark(na, st, false);
+    return MPJ_OK;
+}
+
+template <typename R>
+static mpj_status svd_block_sweep(SvdPlan &p, R *C, R *V, const DevSched &ds, R nu, cudaStream_t st, bool exact)
+{
+    int *uid = p.uid, *nid = p.uid + p.mb;
+    MPJ_CK(cudaMemsetAsync(nid, 0, (size_t)(ds.nb - 1) * sizeof(int), st));
+    for (int Rb = 0; Rb < ds.nb - 1; ++Rb) MPJ_TRY(svd_block_round<R>(p, C, V, ds, Rb, nu, st, exact, uid, nid + Rb));
     return MPJ_OK;
 }
 
@@ -764,6 +776,310 @@ mpj_status svd_run(const double *A, int64_t m, int64_t n, int64_t lda, double *S
     mpj_status s = (mpj_status)r.status;
     if (s == MPJ_OK && rd) { set_error("rank deficient: some sigma_j <= n omega ||A||_F"); s = MPJ_ERR_RANKDEF; }
     return fin(s);
+}
+
+// ---------------------------------------------------------------------------
+// Multi-GPU Alg. 5 (column partition, ring only):
+// one-sided rotations touch only the two column blocks of a block pair, so
+// rank g owns the block-pair slots [g mb/G, (g+1) mb/G) of every block round
+// and runs the single-GPU round kernels (Gram blocks, inner solve, column
+// updates of C and V) on them alone -- a compacted copy of the schedule with
+// the same global block ids, so every slot computes exactly what the
+// single-GPU run computes.  C (m x n_p) and V (n_p x n_p) are stored whole on
+// every rank, in global column positions; a rank keeps its current blocks up
+// to date.  After a block round the 32-column blocks whose slot moves to
+// another rank are sent there (ncclSend / ncclRecv into the same columns: the
+// ring of the merry-go-round); before each sweep every block is broadcast
+// from its owner (the stop test's Gram ||off(C^T C)||_F needs all of C; V
+// rides along), then the stop decision is every rank's, identically.
+// Step 1 (fp32 one-sided Jacobi) runs the same way; steps 2 and 3 (Q =
+// orth(Z), C = A Q) are replicated.  Emulation (emulate = G > 1, no NCCL):
+// G rank copies inside this process, transfers as device copies -- no kernel
+// waits on another.  Results are bit-identical to mpjacobi_svd's for every G
+// when n is a multiple of 64 G (same padding).
+// ---------------------------------------------------------------------------
+mpj_status mg_comm(const void *nccl_id, int rank, int nranks, void **out);
+
+namespace {
+mpj_status svd_nccl_ck(ncclResult_t r, const char *what)
+{
+    if (r != ncclSuccess) {
+        set_error(std::string(what) + ": " + ncclGetErrorString(r));
+        return MPJ_ERR_NCCL;
+    }
+    return MPJ_OK;
+}
+}  // namespace
+
+mpj_status svd_mg_run(const double *A, int64_t m, int64_t n, int64_t lda, double *Sigma, double *U, int64_t ldu,
+                      double *V, int64_t ldv, int *sweeps, const void *nccl_id, int rank, int nranks, int emulate,
+                      cudaStream_t st, const mpj_config &cfg, mpj_report &r, double *h_pin)
+{
+    const double omega = 1.1102230246251565e-16, upsilon = 5.9604644775390625e-08;
+    const bool use_nccl = nccl_id != nullptr;
+    const int G = use_nccl ? nranks : std::max(1, emulate);
+    const int nloc = use_nccl ? 1 : G;
+    ncclComm_t comm = nullptr;
+    if (use_nccl) {
+        void *c = nullptr;
+        MPJ_TRY(mg_comm(nccl_id, rank, nranks, &c));
+        comm = (ncclComm_t)c;
+    }
+    const int np = padded_n(n, BW * G);                  // mb = np / 64 slots, a multiple of G
+    HostSchedule hs;
+    build_schedule(np, BW, hs);
+    const int nb = hs.nb, mb = nb / 2, mbl = mb / G, rounds = nb - 1;
+    // per local copy: a full single-GPU plan (buffers sized for np columns)
+    size_t off = 0;
+    SvdPlan probe;
+    carve_svd(nullptr, off, m, np, probe);
+    std::vector<void *> owned;
+    struct Rel {
+        std::vector<void *> &v; cudaStream_t st;
+        ~Rel() { for (void *p : v) cudaFreeAsync(p, st); }
+    } rel{owned, st};
+    std::vector<SvdPlan> P(nloc);
+    std::vector<DevSched> D(nloc);
+    std::vector<int> grank(nloc);
+    for (int c = 0; c < nloc; ++c) {
+        void *w = nullptr;
+        if (cudaMallocAsync(&w, off + 256, st) != cudaSuccess) {
+            cudaGetLastError();
+            set_error("svd_mg: out of device memory");
+            return MPJ_ERR_NOMEM;
+        }
+        owned.push_back(w);
+        char *base = (char *)(((uintptr_t)w + 255) & ~(uintptr_t)255);
+        size_t o2 = 0;
+        carve_svd(base, o2, m, np, P[c]);
+        P[c].n = n;
+        P[c].mb = mbl;
+        grank[c] = use_nccl ? rank : c;
+        std::vector<int2> cb((size_t)std::max(rounds, 1) * mbl);
+        for (int R = 0; R < rounds; ++R)
+            for (int a = 0; a < mbl; ++a) cb[(size_t)R * mbl + a] = hs.bsched[(size_t)R * mb + grank[c] * mbl + a];
+        MPJ_CK(cudaMemcpyAsync(P[c].bsched, cb.data(), cb.size() * sizeof(int2), cudaMemcpyHostToDevice, st));
+        MPJ_CK(cudaMemcpyAsync(P[c].lsched, hs.lsched.data(), hs.lsched.size() * sizeof(int2), cudaMemcpyHostToDevice,
+                               st));
+        D[c].bsched = P[c].bsched; D[c].lsched = P[c].lsched; D[c].b = BW; D[c].nb = 2 * mbl; D[c].np = np;
+        D[c].rounds = hs.rounds;
+    }
+    r.n_padded = np; r.block_b = BW; r.variant = MPJ_VARIANT_BLOCK;
+    // block owners per round and the moves between consecutive rounds of a sweep
+    std::vector<std::vector<int>> owner(rounds, std::vector<int>(nb));
+    for (int R = 0; R < rounds; ++R)
+        for (int k = 0; k < mb; ++k) {
+            const int2 bp = hs.bsched[(size_t)R * mb + k];
+            owner[R][bp.x] = owner[R][bp.y] = k / mbl;
+        }
+    struct Mv { int blk, src, dst; };
+    std::vector<std::vector<Mv>> moves(std::max(rounds - 1, 0));
+    for (int R = 0; R + 1 < rounds; ++R)
+        for (int b = 0; b < nb; ++b)
+            if (owner[R][b] != owner[R + 1][b]) moves[R].push_back(Mv{b, owner[R][b], owner[R + 1][b]});
+    const int64_t ldc = P[0].ldc;
+    auto loc = [&](int g) { return use_nccl ? (g == rank ? 0 : -1) : g; };   // local copy of rank g
+    // column block blk of the m-row matrix X (ld ldx) / of V (ld np), element size es
+    auto blk_ptr = [&](void *X, int64_t ldx, size_t es, int blk) { return (char *)X + (size_t)blk * BW * ldx * es; };
+    // move / broadcast helpers over the per-copy buffers Cs, Vs (element size es)
+    auto transfer = [&](std::vector<void *> &Cs, std::vector<void *> &Vs, size_t es, const std::vector<Mv> &mv,
+                        bool with_ex) -> mpj_status {
+        if (mv.empty()) return MPJ_OK;
+        const size_t cb = (size_t)BW * ldc * es, vb = (size_t)BW * np * es, eb = BW * sizeof(int);
+        if (!use_nccl) {
+            for (const Mv &x : mv) {
+                MPJ_CK(cudaMemcpyAsync(blk_ptr(Cs[x.dst], ldc, es, x.blk), blk_ptr(Cs[x.src], ldc, es, x.blk), cb,
+                                       cudaMemcpyDeviceToDevice, st));
+                MPJ_CK(cudaMemcpyAsync(blk_ptr(Vs[x.dst], np, es, x.blk), blk_ptr(Vs[x.src], np, es, x.blk), vb,
+                                       cudaMemcpyDeviceToDevice, st));
+                if (with_ex)
+                    MPJ_CK(cudaMemcpyAsync(P[x.dst].ex + (size_t)x.blk * BW, P[x.src].ex + (size_t)x.blk * BW, eb,
+                                           cudaMemcpyDeviceToDevice, st));
+            }
+            return MPJ_OK;
+        }
+        MPJ_TRY(svd_nccl_ck(ncclGroupStart(), "ncclGroupStart"));
+        for (const Mv &x : mv) {
+            if (x.src == rank) {
+                MPJ_TRY(svd_nccl_ck(ncclSend(blk_ptr(Cs[0], ldc, es, x.blk), cb, ncclChar, x.dst, comm, st), "ncclSend"));
+                MPJ_TRY(svd_nccl_ck(ncclSend(blk_ptr(Vs[0], np, es, x.blk), vb, ncclChar, x.dst, comm, st), "ncclSend"));
+                if (with_ex)
+                    MPJ_TRY(svd_nccl_ck(ncclSend(P[0].ex + (size_t)x.blk * BW, eb, ncclChar, x.dst, comm, st), "ncclSend"));
+            } else if (x.dst == rank) {
+                MPJ_TRY(svd_nccl_ck(ncclRecv(blk_ptr(Cs[0], ldc, es, x.blk), cb, ncclChar, x.src, comm, st), "ncclRecv"));
+                MPJ_TRY(svd_nccl_ck(ncclRecv(blk_ptr(Vs[0], np, es, x.blk), vb, ncclChar, x.src, comm, st), "ncclRecv"));
+                if (with_ex)
+                    MPJ_TRY(svd_nccl_ck(ncclRecv(P[0].ex + (size_t)x.blk * BW, eb, ncclChar, x.src, comm, st), "ncclRecv"));
+            }
+        }
+        MPJ_TRY(svd_nccl_ck(ncclGroupEnd(), "ncclGroupEnd"));
+        return MPJ_OK;
+    };
+    // every block from its owner (ownership of round Rlast) to every copy
+    auto gather_all = [&](std::vector<void *> &Cs, std::vector<void *> &Vs, size_t es, int Rlast) -> mpj_status {
+        const size_t cb = (size_t)BW * ldc * es, vb = (size_t)BW * np * es;
+        if (!use_nccl) {
+            for (int b = 0; b < nb; ++b) {
+                const int o = owner[Rlast][b];
+                for (int c = 0; c < nloc; ++c) {
+                    if (c == o) continue;
+                    MPJ_CK(cudaMemcpyAsync(blk_ptr(Cs[c], ldc, es, b), blk_ptr(Cs[o], ldc, es, b), cb,
+                                           cudaMemcpyDeviceToDevice, st));
+                    MPJ_CK(cudaMemcpyAsync(blk_ptr(Vs[c], np, es, b), blk_ptr(Vs[o], np, es, b), vb,
+                                           cudaMemcpyDeviceToDevice, st));
+                }
+            }
+            return MPJ_OK;
+        }
+        if (G == 1) return MPJ_OK;
+        MPJ_TRY(svd_nccl_ck(ncclGroupStart(), "ncclGroupStart"));
+        for (int b = 0; b < nb; ++b) {
+            const int o = owner[Rlast][b];
+            void *pc = blk_ptr(Cs[0], ldc, es, b), *pv = blk_ptr(Vs[0], np, es, b);
+            MPJ_TRY(svd_nccl_ck(ncclBroadcast(pc, pc, cb, ncclChar, o, comm, st), "ncclBroadcast"));
+            MPJ_TRY(svd_nccl_ck(ncclBroadcast(pv, pv, vb, ncclChar, o, comm, st), "ncclBroadcast"));
+        }
+        MPJ_TRY(svd_nccl_ck(ncclGroupEnd(), "ncclGroupEnd"));
+        return MPJ_OK;
+    };
+    // total rotations so far (all ranks)
+    auto total_rot = [&]() -> unsigned long long {
+        unsigned long long tot = 0;
+        if (!use_nccl) {
+            for (int c = 0; c < nloc; ++c) {
+                unsigned long long v = 0;
+                cudaMemcpyAsync(h_pin, P[c].cnt, sizeof(v), cudaMemcpyDeviceToHost, st);
+                cudaStreamSynchronize(st);
+                std::memcpy(&v, h_pin, sizeof(v));
+                tot += v;
+            }
+            return tot;
+        }
+        unsigned long long *scr = (unsigned long long *)(P[0].red_out + 4);
+        ncclAllReduce(P[0].cnt, scr, 1, ncclUint64, ncclSum, comm, st);
+        cudaMemcpyAsync(h_pin, scr, sizeof(tot), cudaMemcpyDeviceToHost, st);
+        cudaStreamSynchronize(st);
+        std::memcpy(&tot, h_pin, sizeof(tot));
+        return tot;
+    };
+    // the one-sided loop on every copy (R = float: step 1; double: the fp64 stage)
+    auto loop = [&](auto tag, double eps_rel, double nu, double early, int max_sweeps, SvdStage &out) -> mpj_status {
+        using R = decltype(tag);
+        std::vector<void *> Cs(nloc), Vs(nloc);
+        for (int c = 0; c < nloc; ++c) {
+            Cs[c] = sizeof(R) == 8 ? (void *)P[c].C : (void *)P[c].C32;
+            Vs[c] = sizeof(R) == 8 ? (void *)P[c].V : (void *)P[c].V32;
+        }
+        const double N = 0.5 * (double)n * (double)(n - 1);
+        mpj_status status = MPJ_ERR_NOCONV;
+        unsigned long long prev = 0;
+        double ratio = 1.0;
+        const double xb = svd_exact_below();
+        for (int c = 0; c < nloc; ++c) MPJ_CK(cudaMemsetAsync(P[c].cnt, 0, sizeof(unsigned long long), st));
+        for (;;) {
+            if (out.sweeps > 0) MPJ_TRY(gather_all(Cs, Vs, sizeof(R), rounds - 1));
+            // stop test on copy 0 (every copy holds the same C now)
+            SvdPlan &p = P[0];
+            if (sizeof(R) == 4) launch_copy_pad<float, double>((float *)Cs[0], ldc, (int)m, np, p.C, ldc, (int)m, np, st);
+            launch_dgemm(true, false, np, np, m, 1.0, p.C, ldc, p.C, ldc, 0.0, p.G, np, st, nullptr, 0, true);
+            launch_norm_sym_upper(p.G, np, np, true, p.red_part, p.red_out, st);
+            launch_norm_sym_upper(p.G, np, np, false, p.red_part, p.red_out + 1, st);
+            MPJ_CK(cudaMemcpyAsync(h_pin, p.red_out, 2 * sizeof(double), cudaMemcpyDeviceToHost, st));
+            MPJ_CK(cudaStreamSynchronize(st));
+            const double offv = h_pin[0], tot = h_pin[1];
+            if (out.sweeps < 64) { out.hist[out.sweeps] = offv; out.nhist = out.sweeps + 1; }
+            if (!std::isfinite(offv)) { set_error("non-finite Gram"); return MPJ_ERR_NONFINITE; }
+            if (offv <= eps_rel * tot) { status = MPJ_OK; break; }
+            if (out.sweeps >= max_sweeps) { status = MPJ_ERR_NOCONV; break; }
+            ++out.sweeps;
+            const bool exact = sizeof(R) == 8 && ratio < xb;
+            for (int c = 0; c < nloc; ++c)
+                MPJ_CK(cudaMemsetAsync(P[c].uid + mbl, 0, (size_t)rounds * sizeof(int), st));
+            for (int R0 = 0; R0 < rounds; ++R0) {
+                for (int c = 0; c < nloc; ++c)
+                    MPJ_TRY(svd_block_round<R>(P[c], (R *)Cs[c], (R *)Vs[c], D[c], R0, (R)nu, st, exact, P[c].uid,
+                                               P[c].uid + mbl + R0));
+                if (R0 + 1 < rounds) MPJ_TRY(transfer(Cs, Vs, sizeof(R), moves[R0], exact));
+            }
+            const unsigned long long now = total_rot();
+            const unsigned long long rs = now - prev;
+            prev = now;
+            out.rotations = (long long)now;
+            if (out.sweeps <= 64) out.rot_hist[out.sweeps - 1] = (long long)rs;
+            ratio = N > 0 ? (double)rs / N : 0.0;
+            if (early > 0 && N > 0 && (double)rs / N < early) { status = MPJ_OK; break; }
+        }
+        MPJ_TRY(gather_all(Cs, Vs, sizeof(R), rounds - 1));
+        return status;
+    };
+    (void)loc;
+
+    // a0: A staged into every copy (zero padded), ||A||_F, finiteness
+    for (int c = 0; c < nloc; ++c) {
+        MPJ_CK(cudaMemsetAsync(P[c].Ad, 0, (size_t)ldc * np * 8, st));
+        MPJ_CK(cudaMemcpy2DAsync(P[c].Ad, ldc * 8, A, lda * 8, m * 8, n, cudaMemcpyDefault, st));
+    }
+    MPJ_CK(cudaMemsetAsync(P[0].flag, 0, sizeof(int), st));
+    launch_check_finite(P[0].Ad, ldc, (int)m, (int)n, P[0].flag, st);
+    launch_norm<double>(P[0].Ad, ldc, (int)m, np, false, P[0].red_part, P[0].red_out, st);
+    MPJ_CK(cudaMemcpyAsync(h_pin, P[0].red_out, sizeof(double), cudaMemcpyDeviceToHost, st));
+    MPJ_CK(cudaMemcpyAsync(h_pin + 1, P[0].flag, sizeof(int), cudaMemcpyDeviceToHost, st));
+    MPJ_CK(cudaStreamSynchronize(st));
+    const double normA = h_pin[0];
+    int bad = 0;
+    std::memcpy(&bad, h_pin + 1, sizeof(int));
+    r.norm_a = normA;
+    if (bad) { set_error("input has NaN/Inf"); return MPJ_ERR_NONFINITE; }
+    // a1: fp32 one-sided Jacobi on fl32(A), partitioned
+    for (int c = 0; c < nloc; ++c) {
+        launch_copy_pad<double, float>(P[c].Ad, ldc, (int)m, np, P[c].C32, ldc, (int)m, np, st);
+        MPJ_CK(cudaMemsetAsync(P[c].V32, 0, (size_t)np * np * 4, st));
+        launch_identity<float>(P[c].V32, np, (int)n, (int)n, st);
+    }
+    {
+        SvdStage lo;
+        mpj_status sl = loop(float(0), eps_low_factor(cfg, n) * upsilon, cfg.nu_low_factor * upsilon,
+                             cfg.early_stop_ratio, cfg.max_sweeps_low, lo);
+        if (sl != MPJ_OK && sl != MPJ_ERR_NOCONV) return sl;
+        r.sweeps_low = lo.sweeps; r.rotations_low = lo.rotations; r.status_low = sl;
+    }
+    // a2, a3 (replicated): Q = orth(fp64(V32)) into V, C = A Q
+    for (int c = 0; c < nloc; ++c) {
+        SvdPlan &p = P[c];
+        launch_copy_pad<float, double>(p.V32, np, (int)n, (int)n, p.G, np, (int)n, (int)n, st);
+        MPJ_CK(cudaMemsetAsync(p.V, 0, (size_t)np * np * 8, st));
+        MPJ_TRY(orth_cgs2(p.G, np, p.V, np, n, n, p.orth_ws, st));
+        MPJ_CK(cudaMemsetAsync(p.C, 0, (size_t)ldc * np * 8, st));
+        launch_dgemm(false, false, m, n, n, 1.0, p.Ad, ldc, p.V, np, 0.0, p.C, ldc, st);
+    }
+    // fp64 sweeps, partitioned
+    SvdStage hi;
+    mpj_status sh = loop(double(0), cfg.eps_factor * omega, cfg.nu_factor * omega, cfg.early_stop_ratio,
+                         cfg.max_sweeps, hi);
+    r.sweeps = hi.sweeps; r.rotations = hi.rotations; r.status = sh;
+    r.off0 = hi.hist[0];
+    for (int k = 0; k < hi.nhist && k < 64; ++k) r.off_hist[k] = hi.hist[k];
+    for (int k = 0; k < 64; ++k) r.rot_hist[k] = hi.rot_hist[k];
+    if (sh != MPJ_OK && sh != MPJ_ERR_NOCONV) return sh;
+    if (sweeps) *sweeps = hi.sweeps;
+    // a10: extraction from copy 0 (every copy holds the same C and V)
+    SvdPlan &p = P[0];
+    k_colnorm<<<(unsigned)n, 256, 0, st>>>(p.C, ldc, (int)m, p.nrm);
+    MPJ_CK(cudaMemsetAsync(p.flag, 0, sizeof(int), st));
+    k_rank_vec<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(p.nrm, (int)n, p.rank, p.sig, (double)n * omega * normA,
+                                                            p.flag);
+    count_launch(2);
+    MPJ_CK(cudaMemcpyAsync(Sigma, p.sig, n * 8, cudaMemcpyDefault, st));
+    k_svd_extract<<<dim3(std::max<int64_t>(1, std::min<int64_t>(64, (m + 255) / 256)), (unsigned)n), 256, 0, st>>>(
+        p.C, ldc, (int)m, p.V, np, (int)n, p.rank, p.nrm, U, ldu, V, ldv);
+    count_launch();
+    MPJ_CK(cudaMemcpyAsync(h_pin + 2, p.flag, sizeof(int), cudaMemcpyDeviceToHost, st));
+    MPJ_CK(cudaStreamSynchronize(st));
+    int rd = 0;
+    std::memcpy(&rd, h_pin + 2, sizeof(int));
+    mpj_status s2 = (mpj_status)r.status;
+    if (s2 == MPJ_OK && rd) { set_error("rank deficient: some sigma_j <= n omega ||A||_F"); s2 = MPJ_ERR_RANKDEF; }
+    return s2;
 }
 
 }  // namespace mpj

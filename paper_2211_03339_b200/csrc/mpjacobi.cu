@@ -37,6 +37,10 @@ mpj_status svd_run(const double *A, int64_t m, int64_t n, int64_t lda, double *S
                    const mpj_config &cfg, mpj_report &r, double *h_pin, bool a_dev, bool out_dev,
                    const float *Zin, bool zin_dev, float *Zout, bool zout_dev, int64_t ldz);
 
+mpj_status svd_mg_run(const double *A, int64_t m, int64_t n, int64_t lda, double *Sigma, double *U, int64_t ldu,
+                      double *V, int64_t ldv, int *sweeps, const void *nccl_id, int rank, int nranks, int emulate,
+                      cudaStream_t st, const mpj_config &cfg, mpj_report &r, double *h_pin);
+
 // Block-variant entry (k_block.cu).
 template <typename R>
 mpj_status block_sweep(R *T, int64_t ldt, R *V, int64_t ldv, int vrows, const DevSched &S, R nu,
@@ -1027,6 +1031,36 @@ mpj_status mpjacobi_svd(const double *A, int64_t m, int64_t n, int64_t lda, doub
 {
     return svd_impl(A, m, n, lda, Sigma, U, ldu, V, ldv, sweeps, workspace, ws_bytes, stream, cfg, rep, nullptr,
                     nullptr, 0);
+}
+
+mpj_status mpjacobi_svd_mg(const double *A, int64_t m, int64_t n, int64_t lda, double *Sigma, double *U,
+                           int64_t ldu, double *V, int64_t ldv, int *sweeps, const void *nccl_id, int rank,
+                           int nranks, int emulate_ranks, void *stream, const mpj_config *cfg_in, mpj_report *rep)
+{
+    using namespace mpj;
+    set_error("");
+    const int G = nccl_id ? nranks : std::max(1, emulate_ranks);
+    if (n < 1 || m < n || lda < m || ldu < m || ldv < n || !A || !Sigma || !U || !V || G < 1 ||
+        (nccl_id && (rank < 0 || rank >= nranks)) || !is_device_ptr(U) || !is_device_ptr(V) ||
+        !is_device_ptr(Sigma)) {
+        set_error("mpjacobi_svd_mg: need m >= n >= 1, lda, ldu >= m, ldv >= n, DEVICE Sigma / U / V");
+        return MPJ_ERR_INVALID;
+    }
+    mpj_config cfg;
+    if (cfg_in) cfg = *cfg_in; else mpj_config_default_svd(&cfg);
+    Ctx cx;
+    MPJ_TRY(cx.open(stream));
+    const long long l0 = mpjacobi_launch_count();
+    Timer t_all(cx.st);
+    mpj_report r;
+    std::memset(&r, 0, sizeof(r));
+    mpj_status s = svd_mg_run(A, m, n, lda, Sigma, U, ldu, V, ldv, sweeps, nccl_id, rank, nranks, emulate_ranks,
+                              cx.st, cfg, r, cx.h_pin);
+    r.t_total = t_all.stop();
+    r.launches = mpjacobi_launch_count() - l0;
+    if (rep) *rep = r;
+    mpj_status c = cx.close();
+    return s != MPJ_OK ? s : c;
 }
 
 mpj_status mpjacobi_svd_z(const double *A, int64_t m, int64_t n, int64_t lda, const float *Z_in, float *Z_out,

@@ -570,6 +570,45 @@ def test_eig_mg_nccl_single_rank(mpj, n):
     assert np.array_equal(host(nccl.V), host(emu.V))
 
 
+# ----------------------------------------------------------------- multi-GPU SVD
+@pytest.mark.parametrize("m,n,mode,Gs", [(300, 256, 3, (1, 2, 4)), (640, 256, 4, (2, 4)), (512, 128, 5, (1, 2)),
+                                         (400, 200, 3, (2,))])
+def test_svd_mg_emulated(mpj, orc, m, n, mode, Gs):
+    """Alg. 5 with the column partition (mpjacobi_svd_mg): each of G ranks
+    (emulated in one process) runs its block-pair slots of every block round
+    with the single-GPU round kernels, column blocks move between ranks with
+    the merry-go-round, every block is broadcast before the stop test.  The
+    same slots get the same arithmetic wherever they run, so sigma, U, V and
+    the sweep counts are bit-identical to mpjacobi_svd when the padding agrees
+    (n a multiple of 64 G, or padded alike); and the north_star tolerances
+    against the oracle's Alg. 5."""
+    A, sig_true = W.example3(m, n, 1e3, mode, W.seed_for(5, mode, 1e3, 7))
+    one = mpj.svd(dev(A))
+    ref = orc.mp_svd(A, orc.default_cfg("svd", b=32))
+    for G in Gs:
+        res = mpj.svd_mg(dev(A), emulate_ranks=G)
+        sig, U, V = host(res.sigma), host(res.U), host(res.V)
+        if -(-n // (64 * G)) * 64 * G == -(-n // 64) * 64:    # same padded order as the single-GPU run
+            assert res.sweeps == one.sweeps and res.report.sweeps_low == one.report.sweeps_low
+            assert np.array_equal(sig, host(one.sigma))
+            assert np.array_equal(U, host(one.U)) and np.array_equal(V, host(one.V))
+        assert np.max(np.abs(sig - ref.sigma)) <= 1e-13 * ref.sigma[0]
+        assert np.linalg.norm(A @ V - U * sig) / np.linalg.norm(A) <= n * 1e-15
+        assert np.linalg.norm(V.T @ V - np.eye(n)) <= n * 1e-15
+        assert np.linalg.norm(U.T @ U - np.eye(n)) <= n * 1e-15
+
+
+def test_svd_mg_nccl_single_rank(mpj):
+    """The NCCL code path of mpjacobi_svd_mg on a one-rank communicator
+    (ncclAllReduce of the rotation counts; no send / recv or broadcast has a
+    peer with one rank) is bit-identical to the emulated G = 1 run."""
+    A, _ = W.example3(320, 128, 1e3, 4, W.seed_for(5, 4, 1e3, 8))
+    emu = mpj.svd_mg(dev(A), emulate_ranks=1)
+    nccl = mpj.svd_mg(dev(A), nccl_id=mpj.nccl_unique_id(), rank=0, nranks=1)
+    assert nccl.sweeps == emu.sweeps
+    assert np.array_equal(host(nccl.sigma), host(emu.sigma)) and np.array_equal(host(nccl.V), host(emu.V))
+
+
 # ----------------------------------------------------------------- BASELINE config 2 (n = 1024)
 @pytest.mark.parametrize("kind,mode,kappa", [("uniform", 4, 1e3), ("clustered", 4, 1e3), ("ex1_mode1", 1, 1e3)])
 def test_config2_n1024_mp_vs_plain(mpj, kind, mode, kappa):
