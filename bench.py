@@ -415,8 +415,18 @@ def run_svd(args):
     sig = torch.empty(n, dtype=torch.float64, device="cuda")
     U = mpj.empty_colmajor(m, n)
     V = mpj.empty_colmajor(n, n)
+    if args.force_mg:   # the multi-GPU SVD (column partition) with one NCCL rank
+        nccl_id = mpj.nccl_unique_id()
+
+        def call():
+            r = mpj.svd_mg(A, cfg, nccl_id=nccl_id, rank=0, nranks=1, allow_noconv=True)
+            sig.copy_(r.sigma); U.copy_(r.U); V.copy_(r.V)
+            return r
+    else:
+        def call():
+            return mpj.svd(A, cfg, workspace=ws, out=(sig, U, V), allow_noconv=True)
     for _ in range(args.warmup):
-        res = mpj.svd(A, cfg, workspace=ws, out=(sig, U, V), allow_noconv=True)
+        res = call()
     torch.cuda.synchronize()
     mpj.profile_reset()
     mpj.profile_enable(True)
@@ -425,7 +435,7 @@ def run_svd(args):
     with ClockSampler(0) as clk:
         e0.record()
         for _ in range(args.steps):
-            res = mpj.svd(A, cfg, workspace=ws, out=(sig, U, V), allow_noconv=True)
+            res = call()
         e1.record()
         torch.cuda.synchronize()
     mpj.profile_enable(False)
@@ -443,7 +453,8 @@ def run_svd(args):
     line = {"metric": f"fp64 SVD seconds ({m}x{n})", "value": ms * 1e-3, "unit": "s", "n_gpus": 1,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": False,
             "dtype": "f64", "data": "synthetic",
-            "config": {"workload": f"Example 3 (P:1112) mode 3 kappa=1e3, {m} x {n} (BASELINE config 5a)"},
+            "config": {"workload": f"Example 3 (P:1112) mode 3 kappa=1e3, {m} x {n} (BASELINE config 5a)",
+                       "parallelism": "column partition, 1 NCCL rank (mpjacobi_svd_mg)" if args.force_mg else "1 GPU"},
             "sweeps": rep.sweeps, "sweeps_low": rep.sweeps_low,
             "ju": rep.rotations / (n * (n - 1) / 2), "ju_low": rep.rotations_low / (n * (n - 1) / 2),
             "stage_seconds": {"low_fp32": rep.t_low, "orth": rep.t_orth, "precond": rep.t_precond,

@@ -275,6 +275,15 @@ mpj_status mpjacobi_svd_mg(const double *A, int64_t m, int64_t n, int64_t lda, d
                            int64_t ldu, double *V, int64_t ldv, int *sweeps, const void *nccl_id, int rank,
                            int nranks, int emulate_ranks, void *stream, const mpj_config *cfg, mpj_report *rep);
 
+/* Host-only view of mpjacobi_svd_mg's partition (no GPU needed): the padded
+ * order n_p (multiple of 64 nranks), the block rounds per sweep, the 32-column
+ * block pairs of every round (pairs: rounds x n_p/64 x 2 ints; slot k belongs
+ * to rank k / (n_p / 64 / nranks)) and the blocks that change rank between
+ * consecutive rounds (moves: (rounds - 1) x 4 nranks x 3 ints (block, src,
+ * dst); nmoves: rounds - 1).  Any output pointer may be NULL. */
+mpj_status mpjacobi_svd_mg_plan(int64_t n, int nranks, int *np_out, int *rounds_out, int *pairs, int *moves,
+                                int *nmoves);
+
 /* ------------------------------------------------------------------------
  * Batched Alg. 3: `batch` independent n x n matrices, contiguous with stride
  * n*n (each column-major), one matrix per CTA (n <= 64).  Lambda: batch x n;

@@ -128,6 +128,8 @@ def lib():
         L.mpjacobi_svd_mg.restype = C.c_int
         L.mpjacobi_svd_mg.argtypes = [_vp, _i64, _i64, _i64, _vp, _vp, _i64, _vp, _i64, C.POINTER(C.c_int), _vp,
                                       C.c_int, C.c_int, C.c_int, _vp, cfgp, repp]
+        L.mpjacobi_svd_mg_plan.restype = C.c_int
+        L.mpjacobi_svd_mg_plan.argtypes = [_i64, C.c_int, C.POINTER(C.c_int), C.POINTER(C.c_int), _vp, _vp, _vp]
         L.mpjacobi_mg_plan.restype = C.c_int
         L.mpjacobi_mg_plan.argtypes = [_i64, C.c_int, C.POINTER(C.c_int), C.POINTER(C.c_int), _vp, _vp, _vp]
         L.mpjacobi_nccl_unique_id.restype = C.c_int
@@ -149,7 +151,7 @@ EXPORTED = (
     "mpjacobi_profile_enable", "mpjacobi_profile_reset", "mpjacobi_profile_get",
     "mpjacobi_eig_mg", "mpjacobi_nccl_unique_id", "mpjacobi_mg_plan", "mpjacobi_eig_z", "mpjacobi_svd_z",
     "mpjacobi_sytrd", "mpjacobi_tridiag_eig", "mpjacobi_orth_householder", "mpjacobi_eig_batched_z",
-    "mpjacobi_svd_mg",
+    "mpjacobi_svd_mg", "mpjacobi_svd_mg_plan",
 )
 
 
@@ -460,6 +462,20 @@ def mpjacobi_eig_batched(A, cfg: mpj_config | None = None, allow_noconv=False, Z
                                       _ptr(swl), _stream(), C.byref(cfg or default_config("eig")))
     _check(st, (MPJ_OK, MPJ_ERR_NOCONV) if allow_noconv else (MPJ_OK,))
     return BatchedResult(lam, V.transpose(1, 2), sw, swl, st, zo.transpose(1, 2) if zo is not None else None)
+
+
+def svd_mg_plan(n: int, nranks: int):
+    """The partition plan of mpjacobi_svd_mg (host-only, no GPU): (n_p,
+    pairs[rounds, mb, 2], moves: list per round transition of (blk, src, dst))."""
+    import numpy as np
+    npd, rounds = C.c_int(0), C.c_int(0)
+    _check(lib().mpjacobi_svd_mg_plan(n, nranks, C.byref(npd), C.byref(rounds), None, None, None))
+    mb = npd.value // 64
+    pairs = np.zeros((rounds.value, mb, 2), dtype=np.int32)
+    mv = np.zeros((max(rounds.value - 1, 1), 4 * nranks, 3), dtype=np.int32)
+    nm = np.zeros(max(rounds.value - 1, 1), dtype=np.int32)
+    _check(lib().mpjacobi_svd_mg_plan(n, nranks, None, None, pairs.ctypes.data, mv.ctypes.data, nm.ctypes.data))
+    return npd.value, pairs, [mv[r, : nm[r]].tolist() for r in range(rounds.value - 1)]
 
 
 def mg_plan(n: int, nranks: int):

@@ -800,6 +800,27 @@ mpj_status svd_run(const double *A, int64_t m, int64_t n, int64_t lda, double *S
 // ---------------------------------------------------------------------------
 mpj_status mg_comm(const void *nccl_id, int rank, int nranks, void **out);
 
+// the partition's data movement, from the schedule alone: owner[R][blk] = the
+// rank whose slot holds column block blk in block round R (slot k belongs to
+// rank k / (mb / G)); moves[R] = the blocks whose owner changes from round R
+// to R+1 (src -> dst).  Identical on every rank.
+struct Mv { int blk, src, dst; };
+static void svd_mg_plan(const HostSchedule &hs, int G, std::vector<std::vector<int>> &owner,
+                        std::vector<std::vector<Mv>> &moves)
+{
+    const int nb = hs.nb, mb = nb / 2, mbl = mb / G, rounds = nb - 1;
+    owner.assign(rounds, std::vector<int>(nb));
+    for (int R = 0; R < rounds; ++R)
+        for (int k = 0; k < mb; ++k) {
+            const int2 bp = hs.bsched[(size_t)R * mb + k];
+            owner[R][bp.x] = owner[R][bp.y] = k / mbl;
+        }
+    moves.assign(std::max(rounds - 1, 0), {});
+    for (int R = 0; R + 1 < rounds; ++R)
+        for (int b = 0; b < nb; ++b)
+            if (owner[R][b] != owner[R + 1][b]) moves[R].push_back(Mv{b, owner[R][b], owner[R + 1][b]});
+}
+
 namespace {
 mpj_status svd_nccl_ck(ncclResult_t r, const char *what)
 {
@@ -866,17 +887,9 @@ mpj_status svd_mg_run(const double *A, int64_t m, int64_t n, int64_t lda, double
     }
     r.n_padded = np; r.block_b = BW; r.variant = MPJ_VARIANT_BLOCK;
     // block owners per round and the moves between consecutive rounds of a sweep
-    std::vector<std::vector<int>> owner(rounds, std::vector<int>(nb));
-    for (int R = 0; R < rounds; ++R)
-        for (int k = 0; k < mb; ++k) {
-            const int2 bp = hs.bsched[(size_t)R * mb + k];
-            owner[R][bp.x] = owner[R][bp.y] = k / mbl;
-        }
-    struct Mv { int blk, src, dst; };
-    std::vector<std::vector<Mv>> moves(std::max(rounds - 1, 0));
-    for (int R = 0; R + 1 < rounds; ++R)
-        for (int b = 0; b < nb; ++b)
-            if (owner[R][b] != owner[R + 1][b]) moves[R].push_back(Mv{b, owner[R][b], owner[R + 1][b]});
+    std::vector<std::vector<int>> owner;
+    std::vector<std::vector<Mv>> moves;
+    svd_mg_plan(hs, G, owner, moves);
     const int64_t ldc = P[0].ldc;
     auto loc = [&](int g) { return use_nccl ? (g == rank ? 0 : -1) : g; };   // local copy of rank g
     // column block blk of the m-row matrix X (ld ldx) / of V (ld np), element size es
@@ -1083,3 +1096,41 @@ mpj_status svd_mg_run(const double *A, int64_t m, int64_t n, int64_t lda, double
 }
 
 }  // namespace mpj
+
+// Host-only view of mpjacobi_svd_mg's partition plan (gloo test of the data
+// movement): the padded order, the rounds, the block pairs of each round
+// (rounds x mb int pairs, slot k on rank k / (mb / nranks)) and the moves
+// between consecutive rounds (per round up to 4 nranks triples (blk, src, dst)).
+extern "C" mpj_status mpjacobi_svd_mg_plan(int64_t n, int nranks, int *np_out, int *rounds_out, int *pairs,
+                                           int *moves, int *nmoves)
+{
+    using namespace mpj;
+    set_error("");
+    if (n < 1 || nranks < 1) { set_error("mpjacobi_svd_mg_plan: invalid argument"); return MPJ_ERR_INVALID; }
+    const int np = padded_n(n, BW * nranks);
+    HostSchedule hs;
+    build_schedule(np, BW, hs);
+    const int mb = hs.nb / 2, rounds = hs.nb - 1;
+    if (np_out) *np_out = np;
+    if (rounds_out) *rounds_out = rounds;
+    std::vector<std::vector<int>> owner;
+    std::vector<std::vector<Mv>> mv;
+    svd_mg_plan(hs, nranks, owner, mv);
+    if (pairs)
+        for (int R = 0; R < rounds; ++R)
+            for (int k = 0; k < mb; ++k) {
+                pairs[2 * ((size_t)R * mb + k)] = hs.bsched[(size_t)R * mb + k].x;
+                pairs[2 * ((size_t)R * mb + k) + 1] = hs.bsched[(size_t)R * mb + k].y;
+            }
+    const int maxm = 4 * nranks;
+    for (int R = 0; R + 1 < rounds; ++R) {
+        if ((int)mv[R].size() > maxm) { set_error("mpjacobi_svd_mg_plan: too many moves"); return MPJ_ERR_INVALID; }
+        if (nmoves) nmoves[R] = (int)mv[R].size();
+        if (moves)
+            for (size_t i = 0; i < mv[R].size(); ++i) {
+                int *t = moves + 3 * ((size_t)R * maxm + i);
+                t[0] = mv[R][i].blk; t[1] = mv[R][i].src; t[2] = mv[R][i].dst;
+            }
+    }
+    return MPJ_OK;
+}
