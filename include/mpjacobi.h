@@ -87,8 +87,12 @@ typedef struct mpj_config {
 /* Orthogonaliser of Alg. 3 step 2 (both give the unique QR factor Q of Z with
  * a positive diagonal of R, the MGS Q; reading R10). */
 enum {
-    MPJ_ORTH_CGS = 0,         /* blocked CGS (twice-is-enough) + panel CholeskyQR2 (default) */
-    MPJ_ORTH_HOUSEHOLDER = 1  /* blocked Householder QR (the paper's GPU choice)     */
+    MPJ_ORTH_AUTO = 0,        /* default: MPJ_ORTH_SERIES for n <= 2048, else MPJ_ORTH_CGS */
+    MPJ_ORTH_HOUSEHOLDER = 1, /* blocked Householder QR (the paper's GPU choice)     */
+    MPJ_ORTH_CGS = 2,         /* blocked CGS (twice-is-enough) + panel CholeskyQR2          */
+    MPJ_ORTH_SERIES = 3       /* Cholesky QR with the factor from a fixed-point series on
+                                 DMMA GEMMs (reading R10b; needs ||Z^T Z - I||_F <= 1e-4,
+                                 else CGS runs)                                             */
 };
 
 /* Low-precision eigensolver of Alg. 3 step 1 (mpjacobi_eig / _eig_z). */
@@ -225,6 +229,12 @@ mpj_status mpjacobi_tridiag_eig(const float *d, const float *e, int64_t n, doubl
  * H_0 ... H_{n-1} with the columns' signs making diag(R) positive.  Z, Q: n x n
  * DEVICE, ld = n.  Returns MPJ_ERR_RANKDEF on a zero diagonal of R. */
 mpj_status mpjacobi_orth_householder(const double *Z, double *Q, int64_t n, void *stream);
+/* Step 2 by Cholesky QR with the factor from a fixed-point series (reading
+ * R10b): Q = Z (I + U)^{-1}, U = Phi(E - U^T U), E = Z^T Z - I, six n^3 DMMA
+ * GEMMs; the same unique Q (positive diag R) as MGS to O(||E||^4 + n omega).
+ * Z, Q: n x n column-major DEVICE.  MPJ_ERR_NOCONV (Q untouched) when
+ * ||E||_F > 1e-4 -- a Z that needs CGS. */
+mpj_status mpjacobi_orth_series(const double *Z, double *Q, int64_t n, void *stream);
 
 /* Alg. 3 step 3: T = Q^T A Q, symmetrised; A, Q, T: n x n DEVICE,
  * ld = n.  fp64 tensor-core (DMMA) GEMMs. */

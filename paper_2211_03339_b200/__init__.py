@@ -28,7 +28,7 @@ MPJ_OK, MPJ_ERR_INVALID, MPJ_ERR_NOCONV, MPJ_ERR_RANKDEF = 0, 1, 2, 3
 MPJ_ERR_NONFINITE, MPJ_ERR_CUDA, MPJ_ERR_NCCL, MPJ_ERR_NOMEM = 4, 5, 6, 7
 VARIANT_AUTO, VARIANT_SCALAR, VARIANT_BLOCK, VARIANT_BLOCK_FULL = 0, 1, 2, 3
 LOW_AUTO, LOW_JACOBI, LOW_SYMQR = 0, 1, 2
-ORTH_CGS, ORTH_HOUSEHOLDER = 0, 1
+ORTH_AUTO, ORTH_HOUSEHOLDER, ORTH_CGS, ORTH_SERIES = 0, 1, 2, 3
 
 STATUS_NAMES = {0: "OK", 1: "INVALID", 2: "NOCONV", 3: "RANKDEF", 4: "NONFINITE", 5: "CUDA",
                 6: "NCCL", 7: "NOMEM"}
@@ -105,6 +105,8 @@ def lib():
         L.mpjacobi_tridiag_eig.argtypes = [_vp, _vp, _i64, _vp, _vp, _i64, _vp]
         L.mpjacobi_orth_householder.restype = C.c_int
         L.mpjacobi_orth_householder.argtypes = [_vp, _vp, _i64, _vp]
+        L.mpjacobi_orth_series.restype = C.c_int
+        L.mpjacobi_orth_series.argtypes = [_vp, _vp, _i64, _vp]
         L.mpjacobi_orth.restype = C.c_int
         L.mpjacobi_orth.argtypes = [_vp, _vp, _i64, _vp]
         L.mpjacobi_precond.restype = C.c_int
@@ -151,7 +153,7 @@ EXPORTED = (
     "mpjacobi_profile_enable", "mpjacobi_profile_reset", "mpjacobi_profile_get",
     "mpjacobi_eig_mg", "mpjacobi_nccl_unique_id", "mpjacobi_mg_plan", "mpjacobi_eig_z", "mpjacobi_svd_z",
     "mpjacobi_sytrd", "mpjacobi_tridiag_eig", "mpjacobi_orth_householder", "mpjacobi_eig_batched_z",
-    "mpjacobi_svd_mg", "mpjacobi_svd_mg_plan",
+    "mpjacobi_svd_mg", "mpjacobi_svd_mg_plan", "mpjacobi_orth_series",
 )
 
 
@@ -339,13 +341,14 @@ def mpjacobi_tridiag_eig(d, e):
 def mpjacobi_orth(Z, method="cgs"):
     """Alg. 3 step 2: the QR factor Q of a square column-major device matrix
     (method "cgs": blocked CGS + CholeskyQR2; "householder": blocked
-    Householder QR)."""
+    Householder QR; "series": Cholesky QR with the fixed-point factor, R10b)."""
     n = Z.shape[0]
     Zc = colmajor(Z)
     if Zc.stride(1) != n:
         Zc = Zc.T.contiguous().T
     Q = empty_colmajor(n, n)
-    fn = lib().mpjacobi_orth_householder if method == "householder" else lib().mpjacobi_orth
+    fn = {"householder": lib().mpjacobi_orth_householder, "series": lib().mpjacobi_orth_series,
+          "cgs": lib().mpjacobi_orth}[method]
     _check(fn(_ptr(Zc), _ptr(Q), n, _stream()))
     return Q
 

@@ -926,11 +926,13 @@ __global__ void k_tri_twisted(const double *__restrict__ d, const double *__rest
     const int i0 = role == 0 ? s : mid, i1 = role == 0 ? mid - 1 : e;
     double gbest = 1e308;
     int r = -1;
-    if (valid)
+    if (valid) {
+        #pragma unroll 8
         for (int i = i1; i >= i0; --i) {
             const double g = fabs(Dp[(size_t)i * n + t] + Dm[(size_t)i * n + t] - (d[i] - l));
             if (g < gbest) { gbest = g; r = i; }
         }
+    }
     const double go = __shfl_xor_sync(pmask, gbest, 1);
     const int ro = __shfl_xor_sync(pmask, r, 1);
     // role 1's half holds the larger indices: it wins ties
@@ -939,28 +941,38 @@ __global__ void k_tri_twisted(const double *__restrict__ d, const double *__rest
     __syncwarp(pmask);
     double nrm = 0.0;
     if (valid) {
-        // the divisors are loaded one step ahead of the x chain (the store of x_i
-        // goes to the slot just read, so the compiler cannot hoist the next load)
+        // the divisors are loaded 8 at a time ahead of the x chain (the store of
+        // x_i goes to the slot just read, so the compiler cannot hoist the loads;
+        // one exposed L2 latency per 8 steps instead of one per step)
+        constexpr int PF = 8;
         if (role == 0) {                                   // x_r = 1, then upwards
             double x = 1.0;
             nrm = 1.0;
-            double dn = r - 1 >= s ? Dp[(size_t)(r - 1) * n + t] : 1.0;
-            for (int i = r - 1; i >= s; --i) {
-                const double dc = dn;
-                if (i - 1 >= s) dn = Dp[(size_t)(i - 1) * n + t];
-                x = -(e64[i] * rcp_nr(dc)) * x;
-                Dp[(size_t)i * n + t] = x;
-                nrm = __fma_rn(x, x, nrm);
+            for (int i = r - 1; i >= s; i -= PF) {
+                double dv[PF];
+                #pragma unroll
+                for (int u = 0; u < PF; ++u) dv[u] = (i - u >= s) ? Dp[(size_t)(i - u) * n + t] : 1.0;
+                #pragma unroll
+                for (int u = 0; u < PF; ++u)
+                    if (i - u >= s) {
+                        x = -(e64[i - u] * rcp_nr(dv[u])) * x;
+                        Dp[(size_t)(i - u) * n + t] = x;
+                        nrm = __fma_rn(x, x, nrm);
+                    }
             }
         } else {                                           // downwards
             double x = 1.0;
-            double dn = r < e ? Dm[(size_t)(r + 1) * n + t] : 1.0;
-            for (int i = r; i < e; ++i) {
-                const double dc = dn;
-                if (i + 2 <= e) dn = Dm[(size_t)(i + 2) * n + t];
-                x = -(e64[i] * rcp_nr(dc)) * x;
-                Dp[(size_t)(i + 1) * n + t] = x;
-                nrm = __fma_rn(x, x, nrm);
+            for (int i = r; i < e; i += PF) {
+                double dv[PF];
+                #pragma unroll
+                for (int u = 0; u < PF; ++u) dv[u] = (i + u < e) ? Dm[(size_t)(i + u + 1) * n + t] : 1.0;
+                #pragma unroll
+                for (int u = 0; u < PF; ++u)
+                    if (i + u < e) {
+                        x = -(e64[i + u] * rcp_nr(dv[u])) * x;
+                        Dp[(size_t)(i + u + 1) * n + t] = x;
+                        nrm = __fma_rn(x, x, nrm);
+                    }
             }
         }
     }

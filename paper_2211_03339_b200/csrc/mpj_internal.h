@@ -137,6 +137,7 @@ mpj_status orth_cgs2(const double *Z, int64_t ldz, double *Q, int64_t ldq, int64
 
 // ---- orthogonalisation by Householder QR (k_hqr.cu) ---------------------------
 size_t hqr_workspace(int64_t m, int64_t n);
+mpj_status orth_series(const double *Z, int64_t ldz, double *Q, int64_t ldq, int64_t n, cudaStream_t st);
 mpj_status orth_householder(const double *Z, int64_t ldz, double *Q, int64_t ldq, int64_t m, int64_t n, void *ws,
                             cudaStream_t st);
 

@@ -690,8 +690,16 @@ static mpj_status eig_impl(bool mixed, const double *A, int64_t n, int64_t lda, 
         Timer to(cx.st);
         launch_copy_pad<float, double>(p.V32, np, (int)n, (int)n, p.W, np, (int)n, (int)n, cx.st);
         MPJ_CKF(cudaMemsetAsync(p.V, 0, (size_t)np * np * sizeof(double), cx.st));
-        s = cfg.orth == MPJ_ORTH_HOUSEHOLDER ? orth_householder(p.W, np, p.V, np, n, n, p.orth_ws, cx.st)
-                                             : orth_cgs2(p.W, np, p.V, np, n, n, p.orth_ws, cx.st);
+        if (cfg.orth == MPJ_ORTH_HOUSEHOLDER) {
+            s = orth_householder(p.W, np, p.V, np, n, n, p.orth_ws, cx.st);
+        } else {
+            // MPJ_ORTH_AUTO: the fixed-point Cholesky QR (R10b) up to n = 2048, CGS above;
+            // it declines (NOCONV) when Z is not orthogonal enough, and CGS runs
+            s = MPJ_ERR_NOCONV;
+            if (cfg.orth == MPJ_ORTH_SERIES || (cfg.orth == MPJ_ORTH_AUTO && n <= 2048))
+                s = orth_series(p.W, np, p.V, np, n, cx.st);
+            if (s == MPJ_ERR_NOCONV) s = orth_cgs2(p.W, np, p.V, np, n, n, p.orth_ws, cx.st);
+        }
         if (s != MPJ_OK) return finish(s);
         r.t_orth = to.stop();
 
@@ -818,7 +826,7 @@ void mpj_config_default_eig(mpj_config *c)
     c->variant = MPJ_VARIANT_AUTO;
     c->block_b = 0;
     c->low_solver = MPJ_LOW_AUTO;
-    c->orth = MPJ_ORTH_CGS;
+    c->orth = MPJ_ORTH_AUTO;
 }
 
 void mpj_config_default_svd(mpj_config *c)
@@ -905,6 +913,18 @@ mpj_status mpjacobi_orth(const double *Z, double *Q, int64_t n, void *stream)
     MPJ_CK(cudaMallocAsync(&ws, orth_workspace(n), cx.st));
     mpj_status s = orth_cgs2(Z, n, Q, n, n, n, ws, cx.st);
     cudaFreeAsync(ws, cx.st);
+    mpj_status c = cx.close();
+    return s != MPJ_OK ? s : c;
+}
+
+mpj_status mpjacobi_orth_series(const double *Z, double *Q, int64_t n, void *stream)
+{
+    g_err.clear();
+    if (n < 1 || !Z || !Q) { set_error("invalid argument"); return MPJ_ERR_INVALID; }
+    Ctx cx;
+    MPJ_TRY(cx.open(stream));
+    mpj_status s = orth_series(Z, n, Q, n, n, cx.st);
+    if (s == MPJ_ERR_NOCONV) set_error("orth_series: ||Z^T Z - I||_F > 1e-4");
     mpj_status c = cx.close();
     return s != MPJ_OK ? s : c;
 }

@@ -26,7 +26,7 @@ def dev(a):
     return torch.from_numpy(np.ascontiguousarray(np.asarray(a).T)).cuda().T
 
 
-@pytest.mark.parametrize("method", ["cgs", "householder"])
+@pytest.mark.parametrize("method", ["cgs", "householder", "series"])
 @pytest.mark.parametrize("n", [1, 16, 65, 100, 300, 1000])
 def test_orth_matches_mgs(mpj, orc, method, n):
     Z = W.rounded_haar(n, 4000 + n)
