@@ -60,7 +60,14 @@ __global__ void __launch_bounds__(NTW) k_block_solve(R *__restrict__ T, int64_t 
         U[li + lj * LD] = (li == lj) ? R(1) : R(0);
     }
     __syncthreads();
-    const R *D = inner_rounds_wide<R>(D0, D1, U, bp, Rb == 0, S.lsched, nu, rule, P, &nrot, max_inner);
+    // the parameter warp's divide / square-root chain with MUFU seeds + Newton (fp64; MPJ_K3_IEEE=1 at
+    // build time keeps the correctly rounded chain)
+#ifdef MPJ_K3_IEEE
+    const R *D = inner_rounds_wide<R, false>(D0, D1, U, bp, Rb == 0, S.lsched, nu, rule, P, &nrot, max_inner);
+#else
+    const R *D = inner_rounds_wide<R, sizeof(R) == 8>(D0, D1, U, bp, Rb == 0, S.lsched, nu, rule, P, &nrot,
+                                                       max_inner);
+#endif
     R *Uk = Ubuf + (size_t)k * TW * TW;
     R *UkT = Ubuf + (size_t)mb * TW * TW + (size_t)k * TW * TW;   // U^T (fp32 apply operand)
     R *UkS = Ubuf + 2 * (size_t)mb * TW * TW + (size_t)k * TW * TW;   // U^T, split-half layout

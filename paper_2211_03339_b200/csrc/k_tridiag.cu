@@ -1046,12 +1046,13 @@ __global__ void k_build_vp(const float *__restrict__ A, int64_t lda, int n, int 
 // 256 threads: column t is T(0:t, t) = -tau_t T(0:t, 0:t) G(0:t, t), the
 // triangular product split over four thread groups per row.
 constexpr int BT = 2 * TB;       // back-transformation block (two sytrd panels)
-__global__ void __launch_bounds__(256) k_build_tp(const double *__restrict__ G, const float *__restrict__ tau, int k0,
+__global__ void __launch_bounds__(1024) k_build_tp(const double *__restrict__ G, const float *__restrict__ tau, int k0,
                                                   int nr, double *Tp)
 {
     extern __shared__ double tsm[];          // T (BT x BT+1), z (BT), part (2 x BT), M (3 x 32 x 32)
     double *T = tsm, *z = T + BT * (BT + 1), *part = z + BT;
-    const int tid = threadIdx.x, row = tid & (BT - 1), grp = tid >> 7;   // 2 groups x 128 rows
+    const int tid = threadIdx.x, row = tid & (BT - 1), grp = tid >> 7;   // fallback: 2 groups x 128 rows
+    const int nthr = blockDim.x;
     constexpr int LS = BT + 1, QB = 32;      // leading dimension, diagonal block size
     double *M = part + 2 * BT;
     __shared__ int zero_tau;
@@ -1068,9 +1069,9 @@ __global__ void __launch_bounds__(256) k_build_tp(const double *__restrict__ G, 
         // per block diagonal instead of 3 per reflector.  One array: S's strict
         // upper part above the diagonal, T transposed on and below it.
         auto tinv = [&](int i) { return i < nr ? (double)tau[k0 + i] : 1.0; };   // padding: identity
-        for (int e = tid; e < BT * LS; e += 256) T[e] = 0.0;
+        for (int e = tid; e < BT * LS; e += nthr) T[e] = 0.0;
         __syncthreads();
-        for (int e = tid; e < BT * BT; e += 256) {
+        for (int e = tid; e < BT * BT; e += nthr) {
             const int i = e & (BT - 1), j = e / BT;
             if (i < j && j < nr) T[i + j * LS] = G[i + j * BT];
         }
@@ -1087,7 +1088,7 @@ __global__ void __launch_bounds__(256) k_build_tp(const double *__restrict__ G, 
         __syncthreads();
         for (int dg = 1; dg < BT / QB; ++dg) {                  // block diagonal dg: blocks (bi, bi + dg)
             const int nb = BT / QB - dg;
-            for (int e = tid; e < nb * QB * QB; e += 256) {     // M = sum_{k=i+1..j} S_ik T_kj
+            for (int e = tid; e < nb * QB * QB; e += nthr) {     // M = sum_{k=i+1..j} S_ik T_kj
                 const int bi = e / (QB * QB), r = (e / QB) % QB, cc = e % QB;
                 const int i0 = bi * QB, col = (bi + dg) * QB + cc;
                 double acc = 0.0;
@@ -1095,7 +1096,7 @@ __global__ void __launch_bounds__(256) k_build_tp(const double *__restrict__ G, 
                 M[(size_t)bi * QB * QB + r + cc * QB] = acc;
             }
             __syncthreads();
-            for (int e = tid; e < nb * QB * QB; e += 256) {     // T_ij = -T_ii M
+            for (int e = tid; e < nb * QB * QB; e += nthr) {     // T_ij = -T_ii M
                 const int bi = e / (QB * QB), r = (e / QB) % QB, cc = e % QB;
                 const int i0 = bi * QB, col = (bi + dg) * QB + cc;
                 double acc = 0.0;
@@ -1105,13 +1106,13 @@ __global__ void __launch_bounds__(256) k_build_tp(const double *__restrict__ G, 
             }
             __syncthreads();
         }
-        for (int e = tid; e < BT * BT; e += 256) {
+        for (int e = tid; e < BT * BT; e += nthr) {
             const int i = e & (BT - 1), j = e / BT;
             Tp[e] = (i <= j && j < nr) ? T[j + i * LS] : 0.0;
         }
         return;
     }
-    for (int e = tid; e < BT * (BT + 1); e += 256) T[e] = 0.0;
+    for (int e = tid; e < BT * (BT + 1); e += nthr) T[e] = 0.0;
     __syncthreads();
     // a zero tau (an identity reflector): LAPACK's column recurrence
     double gnext = (tid < BT && nr > 0) ? G[tid] : 0.0;        // G(tid, t), loaded one step ahead
@@ -1123,15 +1124,15 @@ __global__ void __launch_bounds__(256) k_build_tp(const double *__restrict__ G, 
         __syncthreads();
         // T(row, t) = sum_{u = row}^{t-1} T(row, u) z(u): group grp takes u = row + grp, +2, ...
         double acc = 0.0;
-        if (row < t)
+        if (row < t && grp < 2)
             for (int u = row + grp; u < t; u += 2) acc = __fma_rn(T[row + u * (BT + 1)], z[u], acc);
-        part[grp * BT + row] = acc;
+        if (grp < 2) part[grp * BT + row] = acc;
         __syncthreads();
         if (tid < t) T[tid + t * (BT + 1)] = part[tid] + part[BT + tid];
         if (tid == 0) T[t + t * (BT + 1)] = ta;
         __syncthreads();
     }
-    for (int e = tid; e < BT * BT; e += 256) Tp[e] = T[(e & (BT - 1)) + (e / BT) * (BT + 1)];
+    for (int e = tid; e < BT * BT; e += nthr) Tp[e] = T[(e & (BT - 1)) + (e / BT) * (BT + 1)];
 }
 
 // V32(:, rank[t]) = fl32(Z(:, t))
@@ -1699,8 +1700,8 @@ static mpj_status backtransform_run(const float *A32, int64_t lda, int n, SymqrW
         count_launch();
         launch_dgemm(true, false, BT, BT, m, 1.0, w.Vp, np, w.Vp, np, 0.0, w.Gm, BT, st, w.skw, w.skw_elems);
         const size_t tsm = ((size_t)BT * (BT + 1) + 3 * BT + 3 * 32 * 32) * sizeof(double);
-        MPJ_CK(smem_optin((const void *)k_build_tp, tsm, 256, nullptr));
-        k_build_tp<<<1, 256, tsm, st>>>(w.Gm, w.tau, k0, nr, w.Tp);
+        MPJ_CK(smem_optin((const void *)k_build_tp, tsm, 1024, nullptr));
+        k_build_tp<<<1, 1024, tsm, st>>>(w.Gm, w.tau, k0, nr, w.Tp);
         count_launch();
         launch_dgemm(true, false, BT, n, m, 1.0, w.Vp, np, Y + r0, ldy, 0.0, w.W1, BT, st, w.skw, w.skw_elems);
         launch_dgemm(false, false, BT, n, BT, 1.0, w.Tp, BT, w.W1, BT, 0.0, w.W2, BT, st);

@@ -289,7 +289,14 @@ __device__ __forceinline__ R diag_after(const R *Dc, const WideParams<R> &P, int
 // stores and index reads -- about half of a round's shared-memory traffic,
 // which bounds the rounds (tools/k3_trace.cu: the parameter warp's dependent
 // loads queue behind it).  Same arithmetic (rot on (U(r,p), U(r,q))).
-template <typename R, bool UREG>
+template <typename R, bool FAST>
+__device__ __forceinline__ int rot_params_sel(R app, R aqq, R apq, R nu, int rule, R &t, R &s, R &tau)
+{
+    if constexpr (FAST) return rot_params_fast<R>(app, aqq, apq, nu, rule, t, s, tau);
+    else return rot_params<R>(app, aqq, apq, nu, rule, t, s, tau);
+}
+
+template <typename R, bool UREG, bool FASTP = false>
 __device__ __forceinline__ R *smem_rounds_wide(R *D0, R *D1, R *U, int2 bp, bool intra, int nrounds,
                                                const int2 *__restrict__ lsched, R nu, int rule,
                                                WideParams<R> (&PP)[2], unsigned &cnt)
@@ -345,7 +352,7 @@ __device__ __forceinline__ R *smem_rounds_wide(R *D0, R *D1, R *U, int2 bp, bool
         const int ga = gidx(bp, a), gc = gidx(bp, c);
         const int pk = ga < gc ? a : c, qk = ga < gc ? c : a;
         R t, sk, uk;
-        const int did = rot_params<R>(Dc[pk + pk * LD], Dc[qk + qk * LD], Dc[didx<R, UREG>(pk, qk)], nu, rule, t,
+        const int did = rot_params_sel<R, FASTP>(Dc[pk + pk * LD], Dc[qk + qk * LD], Dc[didx<R, UREG>(pk, qk)], nu, rule, t,
                                       sk, uk);
         ct = t; cs = sk; cu = uk;
         cnt += did;
@@ -387,7 +394,7 @@ __device__ __forceinline__ R *smem_rounds_wide(R *D0, R *D1, R *U, int2 bp, bool
                 const int rn = k < l ? pn : qn, cn = k < l ? qn : pn;
                 const R apq = (rn == pkk) ? (cn == pll ? x11 : x12) : (cn == pll ? x21 : x22);
                 R t, sk, uk;
-                const int did = rot_params<R>(app, aqq, apq, nu, rule, t, sk, uk);
+                const int did = rot_params_sel<R, FASTP>(app, aqq, apq, nu, rule, t, sk, uk);
                 MPJ_K3_TRACE(0, s);
                 cnt += did;
                 N.t[lane] = t; N.s[lane] = sk; N.u[lane] = uk;
@@ -412,7 +419,7 @@ __device__ __forceinline__ R *smem_rounds_wide(R *D0, R *D1, R *U, int2 bp, bool
                     apq = (qn == P.p[l]) ? (pn == P.p[k] ? x11 : x12) : (pn == P.p[k] ? x21 : x22);
                 }
                 R t, sk, uk;
-                const int did = rot_params<R>(app, aqq, apq, nu, rule, t, sk, uk);
+                const int did = rot_params_sel<R, FASTP>(app, aqq, apq, nu, rule, t, sk, uk);
                 MPJ_K3_TRACE(0, s);
                 cnt += did;
                 N.t[lane] = t; N.s[lane] = sk; N.u[lane] = uk;
@@ -662,7 +669,7 @@ __device__ __forceinline__ R *inner_rounds_pipe(R *D0, R *D1, const int2 *__rest
 // K3's inner rounds: the intra-block rounds of block round 0 in shared memory
 // (their pairs follow the local schedule), then the cross rounds with U in
 // registers.
-template <typename R>
+template <typename R, bool FASTP = false>
 __device__ __forceinline__ R *inner_rounds_wide(R *D0, R *D1, R *U, int2 bp, bool intra,
                                                 const int2 *__restrict__ lsched, R nu, int rule,
                                                 WideParams<R> (&PP)[2], unsigned *nrot, int max_inner = 0)
@@ -677,10 +684,10 @@ __device__ __forceinline__ R *inner_rounds_wide(R *D0, R *D1, R *U, int2 bp, boo
     for (int it = 0; it < nsweep; ++it) {
         unsigned cnt = 0;
         if (intra || max_inner > 0) {
-            Dc = smem_rounds_wide<R, false>(Dc, X, U, bp, true, BW - 1, lsched, nu, rule, PP, cnt);
+            Dc = smem_rounds_wide<R, false, FASTP>(Dc, X, U, bp, true, BW - 1, lsched, nu, rule, PP, cnt);
             X = (Dc == D0) ? D1 : D0;
         }
-        Dc = smem_rounds_wide<R, true>(Dc, X, U, bp, false, BW, lsched, nu, rule, PP, cnt);
+        Dc = smem_rounds_wide<R, true, FASTP>(Dc, X, U, bp, false, BW, lsched, nu, rule, PP, cnt);
         X = (Dc == D0) ? D1 : D0;
         // rotation count: per-thread counts of the diagonal threads and the parameter warp
         for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);

@@ -71,6 +71,60 @@ __device__ __forceinline__ int rot_params(R app, R aqq, R apq, R nu, int rule, R
     return skip ? 0 : 1;
 }
 
+// The same rotation parameters with the divisions and square roots of the
+// chain as MUFU seeds plus Newton steps (a few ulps, not correctly rounded):
+// for K3's parameter warp, whose dependent divide / square-root chain is the
+// latency of every inner round.  Changes the rotations at the rounding level
+// only (the block variant is compared with the oracle to a tolerance); the
+// scalar variant, the batched path and the SVD keep rot_params.
+__device__ __forceinline__ double rcp_fast(double q)
+{
+    double r;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(q));
+    double e = __fma_rn(-q, r, 1.0);
+    r = __fma_rn(r, e, r);
+    e = __fma_rn(-q, r, 1.0);
+    return __fma_rn(r, e, r);
+}
+__device__ __forceinline__ double rsqrt_fast(double z)        // 1 / sqrt(z), z >= 1 here
+{
+    double y;
+    asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(z));
+    double h = __fma_rn(-0.5 * z * y, y, 0.5);                 // y <- y (3/2 - z y^2 / 2), twice
+    y = __fma_rn(y, h, y);
+    h = __fma_rn(-0.5 * z * y, y, 0.5);
+    return __fma_rn(y, h, y);
+}
+__device__ __forceinline__ float rcp_fast(float q) { return __frcp_rn(q); }
+__device__ __forceinline__ float rsqrt_fast(float z) { return 1.0f / __fsqrt_rn(z); }
+
+template <typename R>
+__device__ __forceinline__ int rot_params_fast(R app, R aqq, R apq, R nu, int rule, R &t, R &s, R &tau)
+{
+    bool skip;
+    if (rule == 1) {
+        R g = app * aqq;
+        skip = (g > R(0)) ? (absR(apq) <= nu * sqrtR(g)) : (apq == R(0));
+    } else {
+        skip = absR(apq) <= nu * minR(absR(app), absR(aqq));
+    }
+    const R den = skip ? R(1) : R(2) * apq;
+    const R mu = (aqq - app) * rcp_fast(den);
+    const R amu = absR(mu);
+    const R z = fmaR(mu, mu, R(1));
+    const R r = z * rsqrt_fast(z);                               // sqrt(1 + mu^2)
+    const R d = (amu < Prec<R>::mu_big) ? amu + r : R(2) * amu;
+    const R sgn = (mu >= R(0)) ? R(1) : R(-1);
+    const R tt = sgn * rcp_fast(d);
+    const R c = rsqrt_fast(fmaR(tt, tt, R(1)));
+    const R ss = tt * c;
+    const R uu = ss * rcp_fast(R(1) + c);
+    t = skip ? R(0) : tt;
+    s = skip ? R(0) : ss;
+    tau = skip ? R(0) : uu;
+    return skip ? 0 : 1;
+}
+
 // J applied to an (x at index p, y at index q) pair: (x,y) <- (c x - s y, s x + c y).
 template <typename R>
 __device__ __forceinline__ void rot(R s, R tau, R &x, R &y)
