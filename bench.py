@@ -410,7 +410,7 @@ def run_svd(args):
     m, n = args.m, (args.n if args.n != 8192 else 4096)
     At, sig_true = W.example3_torch(m, n, 1e3, 3, 2211033390 + 5000 + 300 + 30, device="cuda")
     A = At.T          # column-major m x n view
-    cfg = mpj.default_config("svd")
+    cfg = mpj.default_config("svd", **({"eps_low_factor": args.eps_low} if args.eps_low > 0 else {}))
     ws = mpj.svd_workspace(m, n, cfg)
     sig = torch.empty(n, dtype=torch.float64, device="cuda")
     U = mpj.empty_colmajor(m, n)

@@ -69,8 +69,9 @@ enum {
 typedef struct mpj_config {
     double eps_factor;        /* eps = eps_factor * omega; default 0.1            */
     double nu_factor;         /* nu = nu_factor * omega; default 20 (EVD), 1 (SVD)       */
-    double eps_low_factor;    /* low stage: eps_low = f * upsilon; <= 0 (default): the
-                                 rule max(10, 1.25 sqrt(n)) of DESIGN.md reading R12      */
+    double eps_low_factor;    /* low stage: eps_low = f * upsilon; <= 0: the rule
+                                 max(10, 1.25 sqrt(n)) of DESIGN.md reading R12 (EVD
+                                 default); SVD default 10 (SPEC's value)           */
     double nu_low_factor;     /* low stage: nu_low = f * upsilon; default 20 EVD, 1 SVD  */
     double early_stop_ratio;  /* SVD: stop after a sweep with rotations/N below this;
                                  default 2e-4; 0 disables                        */

@@ -178,11 +178,13 @@ def default_cfg(kind: str = "eig", b: int = 32, **kw) -> Cfg:
     low_solver 0 / LOW_SYMQR = symmetric QR in binary32, LOW_JACOBI =
     the fp32 parallel Jacobi, whose stop rule is eps_low = max(10, 1.25
     sqrt(n)) upsilon (eps_low_factor = 0 selects the rule), nu_low = 20
-    upsilon (EVD) / upsilon (SVD, whose low stage is always one-sided Jacobi)."""
+    upsilon (EVD) / upsilon (SVD, whose low stage is always one-sided Jacobi;
+    its eps_low is SPEC's 10 upsilon, S:281 -- DESIGN R12, measured best for
+    Alg. 5)."""
     c = Cfg()
     c.eps_factor = 0.1
     c.nu_factor = 20.0 if kind == "eig" else 1.0
-    c.eps_low_factor = 0.0
+    c.eps_low_factor = 0.0 if kind == "eig" else 10.0
     c.nu_low_factor = 20.0 if kind == "eig" else 1.0
     c.early_stop = 0.0 if kind == "eig" else 2e-4
     c.max_sweeps = 60
