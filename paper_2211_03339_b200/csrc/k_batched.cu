@@ -26,6 +26,8 @@
 #include "mpj_internal.h"
 
 #include <algorithm>
+#include <map>
+#include <mutex>
 
 namespace mpj {
 namespace {
@@ -691,22 +693,37 @@ __global__ void __launch_bounds__(NT, 3) k_batched_evd(BatchedArgs a)
 mpj_status batched_evd(const double *A, int64_t n, int64_t batch, double *Lambda, double *V, int *sweeps,
                        int *sweeps_low, const float *Zin, float *Zout, cudaStream_t st, const mpj_config &cfg)
 {
-    HostSchedule hs;
-    build_schedule(64, 32, hs);
+    // the 64-index intra-block schedule: read-only, uploaded once per device
+    static std::mutex mu;
+    static std::map<int, int2 *> sched_dev;
+    int2 *lsched = nullptr;
+    {
+        int dev = 0;
+        MPJ_CK(cudaGetDevice(&dev));
+        std::lock_guard<std::mutex> lk(mu);
+        auto it = sched_dev.find(dev);
+        if (it == sched_dev.end()) {
+            HostSchedule hs;
+            build_schedule(64, 32, hs);
+            int2 *d = nullptr;
+            MPJ_CK(cudaMalloc(&d, hs.lsched.size() * sizeof(int2)));
+            MPJ_CK(cudaMemcpy(d, hs.lsched.data(), hs.lsched.size() * sizeof(int2), cudaMemcpyHostToDevice));
+            it = sched_dev.emplace(dev, d).first;
+        }
+        lsched = it->second;
+    }
     constexpr int64_t kChunk = 16384;   // matrices per launch pair (Z scratch: 256 MB at most)
     struct Scratch {                    // freed on every exit
         cudaStream_t st; void *p = nullptr, *z = nullptr;
         ~Scratch() { if (p) cudaFreeAsync(p, st); if (z) cudaFreeAsync(z, st); }
     } sc{st};
-    MPJ_CK(cudaMallocAsync(&sc.p, hs.lsched.size() * sizeof(int2) + 256, st));
-    int2 *lsched = (int2 *)sc.p;
-    int *flag = (int *)(lsched + hs.lsched.size());
+    MPJ_CK(cudaMallocAsync(&sc.p, 256, st));
+    int *flag = (int *)sc.p;
     float *Z = nullptr;
     if (!Zin && !Zout) {
         MPJ_CK(cudaMallocAsync(&sc.z, (size_t)std::min<int64_t>(batch, kChunk) * n * n * sizeof(float), st));
         Z = (float *)sc.z;
     }
-    MPJ_CK(cudaMemcpyAsync(lsched, hs.lsched.data(), hs.lsched.size() * sizeof(int2), cudaMemcpyHostToDevice, st));
     MPJ_CK(cudaMemsetAsync(flag, 0, sizeof(int), st));
     if (Zin && sweeps_low) MPJ_CK(cudaMemsetAsync(sweeps_low, 0, batch * sizeof(int), st));
     BatchedArgs a;
