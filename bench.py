@@ -396,8 +396,43 @@ def run_config2(args):
                           "sweeps_low": r.report.sweeps_low,
                           "max_dlam": float(abs(r.lam.cpu().numpy() - lam_true).max())}
         rows.append({"spectrum": kind, **out})
+    # per-kernel device time of one profiled Alg. 3 call (uniform spectrum) and the
+    # roofline of its dominant kernel: at n = 1024 every stage is latency-bound
+    A, _ = W.example1(n, 1e3, 4, W.seed_for(2, 4, 1e3))
+    At = torch.from_numpy(A).cuda()
+    mpj.profile_reset()
+    mpj.profile_enable(True)
+    r = mpj.eig(At)
+    torch.cuda.synchronize()
+    mpj.profile_enable(False)
+    kern = {}
+    for name in ("symqr_sytrd", "symqr_trieig", "symqr_backtransform", "block_apply_f64", "block_solve_f64"):
+        sec, cnt = mpj.profile_get(name)
+        if cnt:
+            kern[name] = {"seconds": sec, "launches": cnt}
+    pk = peaks()
+    dom = max(kern, key=lambda k: kern[k]["seconds"]) if kern else None
+    roof = None
+    if dom:
+        t = kern[dom]["seconds"]
+        npad = r.report.n_padded
+        mb = npad // 64
+        if dom == "symqr_sytrd":        # binary32 Householder reduction: 4/3 n^3 flop
+            fl, peak, bound = 4.0 / 3.0 * n ** 3, pk["ffma_tflops"], "alu"
+        elif dom == "block_apply_f64":  # mirrored T tiles + V tiles per launch
+            fl = kern[dom]["launches"] * (mb * (mb - 1) // 2 * 4 * 64 ** 3 + mb * mb * 2 * 64 ** 3)
+            peak, bound = pk["dmma_tflops"], "tensor"
+        elif dom == "block_solve_f64":  # inner rounds: 496 pair tiles x 32 + U 64 rows x 32 pairs x 8 flop
+            fl = kern[dom]["launches"] * (mb // 2) * 40 * (496 * 32 + 64 * 32 * 8)
+            peak, bound = pk["dfma_tflops"], "alu"
+        else:                            # back-transformation: 2 n^3 DMMA flop
+            fl, peak, bound = 2.0 * n ** 3, pk["dmma_tflops"], "tensor"
+        ach = fl / t / 1e12
+        roof = {"kernel": dom, "bound": bound, "achieved": ach, "peak": peak, "unit": "TFLOP/s", "frac": ach / peak,
+                "traffic": None, "share_of_step": t / max(r.report.t_total, 1e-30),
+                "note": "n = 1024: latency-bound (one cluster / few CTAs per step); the fraction is small by design"}
     print(json.dumps({"metric": "config 2: n=1024 EVD seconds and fp64 sweeps, Alg. 3 vs Alg. 2", "rows": rows,
-                      "steps": args.steps, "warmup": args.warmup}))
+                      "steps": args.steps, "warmup": args.warmup, "kernels_mp_uniform": kern, "roofline": roof}))
 
 
 def run_svd(args):

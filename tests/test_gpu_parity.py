@@ -666,3 +666,54 @@ def test_scalar_fused_round_bit_identical(tmp_path, n, b):
         subprocess.run([sys.executable, str(script), root, str(n), str(out), str(b)], env=env, check=True, timeout=300)
         outs[kind] = np.load(out)
     assert np.array_equal(outs["1"].view(np.uint64), outs["0"].view(np.uint64))
+
+
+# ----------------------------------------------------------------- round-2 edge cases
+def test_svd_mg_three_ranks_square(mpj, orc):
+    """Multi-GPU SVD with a non-power-of-two rank count (G = 3: n padded to a
+    multiple of 192) on a square matrix (m = n): north_star tolerances vs the
+    oracle and the single-GPU SVD's singular values to 1e-13 (the padding
+    differs, so not bit for bit)."""
+    n = 200
+    A, sig_true = W.example3(n, n, 1e3, 4, W.seed_for(5, 4, 1e3, 33))
+    res = mpj.svd_mg(dev(A), emulate_ranks=3)
+    one = mpj.svd(dev(A))
+    sig, U, V = host(res.sigma), host(res.U), host(res.V)
+    assert np.max(np.abs(sig - host(one.sigma))) <= 1e-13 * sig[0]
+    assert np.max(np.abs(sig - sig_true)) <= 1e-13 * sig_true[0]
+    assert np.linalg.norm(A @ V - U * sig) / np.linalg.norm(A) <= n * 1e-15
+    assert np.linalg.norm(V.T @ V - np.eye(n)) <= n * 1e-15
+
+
+def test_batched_more_than_one_chunk(mpj, orc):
+    """More matrices than one launch chunk (16384): the second chunk's Z
+    scratch / output offsets; both chunks vs the oracle on sampled matrices."""
+    n, batch = 16, 16384 + 37
+    base = np.stack([W.example1(n, 1e3, 3 + k % 3, W.seed_for(3, 3 + k % 3, 1e3, 7000 + k))[0] for k in range(64)])
+    As = np.ascontiguousarray(np.concatenate([base] * (batch // 64 + 1))[:batch])
+    res = mpj.eig_batched(torch.from_numpy(As).cuda())
+    lam, V = host(res.lam), host(res.V)
+    for k in (0, 63, 16383, 16384, 16384 + 36):
+        ref = orc.mp_evd(As[k], orc.default_cfg("eig", b=32))
+        assert np.max(np.abs(lam[k] - ref.lam)) <= 1e-13 * np.max(np.abs(ref.lam))
+        assert np.linalg.norm(As[k] @ V[k] - V[k] * lam[k]) / np.linalg.norm(As[k]) <= n * 1e-15
+        assert np.array_equal(lam[k], lam[k % 64])   # same matrix, same bits, whatever its chunk
+
+
+def test_orth_series_declines_to_cgs(mpj, orc):
+    """Step 2's fixed-point Cholesky QR (R10b) needs ||Z^T Z - I||_F <= 1e-4;
+    for a Z that is not orthogonal enough it declines (NOCONV from
+    mpjacobi_orth_series) and Alg. 3 takes CGS -- the result is still right.
+    Example 1 mode 1 (one large eigenvalue, the rest one cluster) at n = 512
+    gives such a step-1 Z."""
+    n = 512
+    Z = W.rounded_haar(n, 77).copy()
+    Z[:, 1] = Z[:, 0] + 1e-3 * Z[:, 1]               # two nearly parallel columns
+    with pytest.raises(mpj.MpjError) as e:
+        mpj.orth(dev(Z), method="series")
+    assert e.value.status == mpj.MPJ_ERR_NOCONV
+    A, lam_true = W.example1(n, 1e3, 1, W.seed_for(1, 1, 1e3, 34))
+    res = mpj.eig(dev(A))
+    lam, V = host(res.lam), host(res.V)
+    assert np.max(np.abs(lam - lam_true)) <= 1e-13 * np.abs(lam_true).max()
+    assert np.linalg.norm(V.T @ V - np.eye(n)) <= n * 1e-15
