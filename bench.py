@@ -423,7 +423,9 @@ def run_config2(args):
             fl = kern[dom]["launches"] * (mb * (mb - 1) // 2 * 4 * 64 ** 3 + mb * mb * 2 * 64 ** 3)
             peak, bound = pk["dmma_tflops"], "tensor"
         elif dom == "block_solve_f64":  # inner rounds: 496 pair tiles x 32 + U 64 rows x 32 pairs x 8 flop
-            fl = kern[dom]["launches"] * (mb // 2) * 40 * (496 * 32 + 64 * 32 * 8)
+            nb = npad // 32
+            rounds = kern[dom]["launches"] / (nb - 1) * (63 + 32 * (nb - 2))   # block round 0: 2b-1, later: b
+            fl = rounds * (mb // 2) * (496 * 32 + 64 * 32 * 8)
             peak, bound = pk["dfma_tflops"], "alu"
         else:                            # back-transformation: 2 n^3 DMMA flop
             fl, peak, bound = 2.0 * n ** 3, pk["dmma_tflops"], "tensor"
