@@ -1093,7 +1093,7 @@ __global__ void __launch_bounds__(1024) k_build_tp(const double *__restrict__ G,
                 const int i0 = bi * QB, col = (bi + dg) * QB + cc;
                 double acc = 0.0;
                 for (int u = i0 + QB; u <= col; ++u) acc = __fma_rn(T[(i0 + r) + u * LS], T[col + u * LS], acc);
-                M[(size_t)bi * QB * QB + r + cc * QB] = acc;
+                M[(size_t)bi * QB * QB + r * QB + cc] = acc;     // row-major: lanes (cc) consecutive
             }
             __syncthreads();
             for (int e = tid; e < nb * QB * QB; e += nthr) {     // T_ij = -T_ii M
@@ -1101,7 +1101,7 @@ __global__ void __launch_bounds__(1024) k_build_tp(const double *__restrict__ G,
                 const int i0 = bi * QB, col = (bi + dg) * QB + cc;
                 double acc = 0.0;
                 for (int u = r; u < QB; ++u)
-                    acc = __fma_rn(T[(i0 + u) + (i0 + r) * LS], M[(size_t)bi * QB * QB + u + cc * QB], acc);
+                    acc = __fma_rn(T[(i0 + u) + (i0 + r) * LS], M[(size_t)bi * QB * QB + u * QB + cc], acc);
                 T[col + (i0 + r) * LS] = -acc;
             }
             __syncthreads();
