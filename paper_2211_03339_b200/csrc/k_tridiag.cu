@@ -1179,21 +1179,26 @@ PFN_cuTensorMapEncodeTiled_v12000 tmap_encoder()
     return fn;
 }
 
+// co-resident CTAs of the cooperative panel kernel on the current device (its
+// shared-memory opt-in is per device: set through smem_optin on every call)
 int coop_ctas()
 {
-    static int g = 0;
-    if (!g) {
-        int dev = 0, sms = 148, occ = 1;
-        cudaGetDevice(&dev);
+    static std::mutex mu;
+    static std::map<int, int> per_dev;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    int occ = 1;
+    if (smem_optin((const void *)k_sytrd_panel, SYTRD_SMEM, NTH, &occ) != cudaSuccess) occ = 1;
+    std::lock_guard<std::mutex> lk(mu);
+    auto it = per_dev.find(dev);
+    if (it == per_dev.end()) {
+        int sms = 148;
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        const size_t smem = SYTRD_SMEM;
-        cudaFuncSetAttribute(k_sytrd_panel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_sytrd_panel, NTH, smem);
         int want = 2;
         if (const char *e = getenv("MPJ_SYTRD_OCC")) want = std::max(1, atoi(e));   // A/B: CTAs per SM
-        g = sms * std::max(1, std::min(occ, want));
+        it = per_dev.emplace(dev, sms * std::max(1, std::min(occ, want))).first;
     }
-    return g;
+    return it->second;
 }
 
 }  // namespace
