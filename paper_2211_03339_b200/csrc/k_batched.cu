@@ -136,6 +136,9 @@ __global__ void __launch_bounds__(NT, 5) k_batched_low(BatchedArgs a)
 // Shared memory: A (64 x 65 fp32) + X (64 x 64 fp64, row-major x_i^(t)) =
 // 49 KB -> 4 CTAs per SM.
 // ---------------------------------------------------------------------------
+#ifndef MPJ_BATCHED_MS
+#define MPJ_BATCHED_MS 2   // lanes per eigenvalue in the batched multisection (A/B builds)
+#endif
 constexpr int LAQ = 65;
 constexpr size_t kSymqrSmem = (size_t)TW * LAQ * sizeof(float) + (size_t)TW * TW * sizeof(double);
 
@@ -295,7 +298,7 @@ __global__ void __launch_bounds__(NT, 4) k_batched_symqr(BatchedArgs a)
         // until it is within 2 omega of max(|lo|, |hi|) or of the block's Gershgorin
         // bound (the Sturm count resolves nothing finer).  The other threads turn
         // the reflectors into explicit columns for B (v_{k+1} = 1, zeros above).
-        constexpr int MS = 2;
+        constexpr int MS = MPJ_BATCHED_MS;
         const int t = tid / MS, l4 = tid % MS, base = lane & ~(MS - 1);
         const unsigned gmask = ((1u << MS) - 1) << base;
         const bool valid = t < n;
