@@ -37,7 +37,7 @@ using namespace blk;
 // ---------------------------------------------------------------------------
 // K3: inner solver.  One CTA per block pair.
 // ---------------------------------------------------------------------------
-template <typename R>
+template <typename R, bool FASTP>
 __global__ void __launch_bounds__(NTW) k_block_solve(R *__restrict__ T, int64_t ldt, Sched S, int Rb, R nu,
                                                      int rule, R *__restrict__ Ubuf,
                                                      unsigned long long *__restrict__ cnt,
@@ -60,14 +60,8 @@ __global__ void __launch_bounds__(NTW) k_block_solve(R *__restrict__ T, int64_t 
         U[li + lj * LD] = (li == lj) ? R(1) : R(0);
     }
     __syncthreads();
-    // the parameter warp's divide / square-root chain with MUFU seeds + Newton (fp64; MPJ_K3_IEEE=1 at
-    // build time keeps the correctly rounded chain)
-#ifdef MPJ_K3_IEEE
-    const R *D = inner_rounds_wide<R, false>(D0, D1, U, bp, Rb == 0, S.lsched, nu, rule, P, &nrot, max_inner);
-#else
-    const R *D = inner_rounds_wide<R, sizeof(R) == 8>(D0, D1, U, bp, Rb == 0, S.lsched, nu, rule, P, &nrot,
-                                                       max_inner);
-#endif
+    // FASTP: the parameter warp's divide / square-root chain with MUFU seeds + Newton (reading R28)
+    const R *D = inner_rounds_wide<R, FASTP>(D0, D1, U, bp, Rb == 0, S.lsched, nu, rule, P, &nrot, max_inner);
     R *Uk = Ubuf + (size_t)k * TW * TW;
     R *UkT = Ubuf + (size_t)mb * TW * TW + (size_t)k * TW * TW;   // U^T (fp32 apply operand)
     R *UkS = Ubuf + 2 * (size_t)mb * TW * TW + (size_t)k * TW * TW;   // U^T, split-half layout
@@ -1226,7 +1220,11 @@ mpj_status block_sweep(R *T, int64_t ldt, R *V, int64_t ldv, int vrows, const De
     int *nid = uid + mb;                         // nb - 1 <= 2 mb block rounds
     MPJ_CK(cudaMemsetAsync(nid, 0, (size_t)(ds.nb - 1) * sizeof(int), st));
     const size_t sm_solve = 3 * TW * LayK<R>::LD * sizeof(R);
-    MPJ_CK(smem_optin((const void *)k_block_solve<R>, sm_solve, NTW, nullptr));
+    // fp64: the fast parameter chain (R28) unless MPJ_K3_IEEE=1 (A/B and its parity test)
+    const char *ie = getenv("MPJ_K3_IEEE");
+    const bool fastp = sizeof(R) == 8 && !(ie && ie[0] == '1');
+    auto solve = fastp ? k_block_solve<R, sizeof(R) == 8> : k_block_solve<R, false>;
+    MPJ_CK(smem_optin((const void *)solve, sm_solve, NTW, nullptr));
     ApplyArgs ap;
     ap.T = T; ap.ldt = ldt; ap.M = V; ap.ldm = ldv; ap.mrows = vrows; ap.S = S; ap.Ubuf = Ubuf; ap.uid = uid;
     ap.ntT = mb * (mb - 1) / 2;
@@ -1237,8 +1235,8 @@ mpj_status block_sweep(R *T, int64_t ldt, R *V, int64_t ldv, int vrows, const De
     const int nbr = max_brounds >= 0 ? std::min(max_brounds, ds.nb - 1) : ds.nb - 1;
     for (int Rb = 0; Rb < nbr; ++Rb) {
         if (prof) prof_mark(nsolve, st, true);
-        MPJ_CK(launch_pdl(k_block_solve<R>, dim3(mb), dim3(NTW), sm_solve, st, T, ldt, S, Rb, nu, rule, Ubuf, cnt,
-                          uid, nid + Rb, max_inner));
+        MPJ_CK(launch_pdl(solve, dim3(mb), dim3(NTW), sm_solve, st, T, ldt, S, Rb, nu, rule, Ubuf, cnt, uid,
+                          nid + Rb, max_inner));
         count_launch();
         if (prof) { prof_mark(nsolve, st, false); prof_mark(napply, st, true); }
         ap.Rb = Rb;

@@ -668,6 +668,37 @@ def test_scalar_fused_round_bit_identical(tmp_path, n, b):
     assert np.array_equal(outs["1"].view(np.uint64), outs["0"].view(np.uint64))
 
 
+# ----------------------------------------------------------------- reading R28
+@pytest.mark.parametrize("n", [256, 640])
+def test_k3_fast_parameter_chain(mpj, orc, n, monkeypatch):
+    """Reading R28: K3's rotation parameters with MUFU seeds + Newton steps
+    (default) against the correctly rounded chain (MPJ_K3_IEEE=1): after one
+    sweep T and V agree to the rounding level (as any two valid evaluation
+    orders), both agree with the oracle's scalar rounds to 64 n omega, and
+    the full runs take the same sweeps with eigenvalues to 1e-13."""
+    T0, Q, A = near_diag_T0(n, 5 * n)
+    nA = np.linalg.norm(A)
+    cfg = mpj.default_config("eig", variant=mpj.VARIANT_BLOCK, block_b=32)
+    ref1 = orc.jacobi_evd(T0, Q, b=32, tol=0.0, max_sweeps=1)
+    out = {}
+    for mode in ("fast", "ieee"):
+        if mode == "ieee":
+            monkeypatch.setenv("MPJ_K3_IEEE", "1")
+        T, V = dev(T0), dev(Q)
+        mpj.jacobi(T, V, tol=0.0, max_sweeps=1, cfg=cfg)
+        assert np.max(np.abs(host(T) - ref1.T)) <= 64 * n * OMEGA * nA
+        assert np.max(np.abs(host(V) - ref1.V)) <= 64 * n * OMEGA
+        tol = 0.1 * OMEGA * nA
+        T2, V2 = dev(T0), dev(Q)
+        r = mpj.jacobi(T2, V2, tol=tol, cfg=cfg)
+        out[mode] = (host(T), host(V), r.sweeps, np.sort(np.diag(host(T2)))[::-1])
+    (Tf, Vf, sf, lf), (Ti, Vi, si, li) = out["fast"], out["ieee"]
+    assert not np.array_equal(Tf, Ti) or not np.array_equal(Vf, Vi)   # the two chains really differ
+    assert np.max(np.abs(Tf - Ti)) <= 64 * n * OMEGA * nA and np.max(np.abs(Vf - Vi)) <= 64 * n * OMEGA
+    assert sf == si
+    assert np.max(np.abs(lf - li)) <= 1e-13 * np.max(np.abs(li))
+
+
 # ----------------------------------------------------------------- round-2 edge cases
 def test_svd_mg_three_ranks_square(mpj, orc):
     """Multi-GPU SVD with a non-power-of-two rank count (G = 3: n padded to a
