@@ -1364,10 +1364,11 @@ __global__ void __launch_bounds__(SCNT, 1) k_sytrd_cluster(float *A, int64_t ld,
         for (int r = 0; r <= R; ++r) { roff[r] = o; if (r < R) o += sc_rowlen(r, c); }
     }
     __syncthreads();
-    // own rows of the lower triangle (A32 is symmetric: row i = column i, contiguous), zero padded
+    // own rows of the lower triangle (only the lower triangle is current when this
+    // runs on the trailing matrix of the panel kernel), zero padded
     for (int r = 0; r < R; ++r) {
         const int i = SCL * r + c, len = sc_rowlen(r, c);
-        for (int j = tid; j < len; j += SCNT) Aown[roff[r] + j] = j <= i ? A[j + (size_t)i * ld] : 0.f;
+        for (int j = tid; j < len; j += SCNT) Aown[roff[r] + j] = j <= i ? A[i + (size_t)j * ld] : 0.f;
     }
     __syncthreads();
     // push the x of column kx (own rows i >= kx+1) and the partial norm (i >= kx+2) to every CTA
@@ -1576,50 +1577,66 @@ __global__ void __launch_bounds__(SCNT, 1) k_sytrd_cluster(float *A, int64_t ld,
 
 }  // namespace
 
+// the one-cluster reduction of the n x n symmetric matrix at A (lower triangle,
+// ld lda) when it fits a cluster's shared memory: d, e, tau (n entries) and the
+// reflectors below the subdiagonal.  false: not launched (does not fit, or
+// MPJ_SYTRD_CLUSTER=0)
+static bool sytrd_cluster_launch(float *A, int64_t lda, int n, float *d, float *e, float *tau, cudaStream_t st,
+                                 mpj_status *err)
+{
+    *err = MPJ_OK;
+    if (n < 3 || n > 1536) return false;
+    const char *env = getenv("MPJ_SYTRD_CLUSTER");
+    const size_t smem = sc_smem(n);
+    if ((env && env[0] == '0') || smem > 227 * 1024 - 1024) return false;
+    cudaLaunchConfig_t cfg = {};
+    cudaLaunchAttribute at[1];
+    cfg.gridDim = dim3(SCL); cfg.blockDim = dim3(SCNT); cfg.dynamicSmemBytes = smem; cfg.stream = st;
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = SCL; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
+    cfg.attrs = at; cfg.numAttrs = 1;
+    // whether a 16-CTA cluster with this much shared memory fits: asked once per
+    // (device, size) -- the occupancy query costs more than a small n's whole kernel
+    static std::mutex mu;
+    static std::map<std::pair<int, size_t>, bool> fits;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    {
+        std::lock_guard<std::mutex> lk(mu);
+        auto key = std::make_pair(dev, smem);
+        auto it = fits.find(key);
+        if (it == fits.end()) {
+            bool ok = cudaFuncSetAttribute(k_sytrd_cluster, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) ==
+                          cudaSuccess &&
+                      smem_optin((const void *)k_sytrd_cluster, smem, SCNT, nullptr) == cudaSuccess;
+            int ncl = 0;
+            if (ok) ok = cudaOccupancyMaxActiveClusters(&ncl, k_sytrd_cluster, &cfg) == cudaSuccess && ncl > 0;
+            cudaGetLastError();            // a refused size only selects the panel kernel
+            it = fits.emplace(key, ok).first;
+        }
+        if (!it->second) return false;
+    }
+    if (smem_optin((const void *)k_sytrd_cluster, smem, SCNT, nullptr) != cudaSuccess) return false;
+    const bool prof = prof_on();
+    if (prof) prof_mark("symqr_sytrd", st, true);
+    const cudaError_t ce = cudaLaunchKernelEx(&cfg, k_sytrd_cluster, A, lda, n, d, e, tau);
+    if (prof) prof_mark("symqr_sytrd", st, false);
+    count_launch();
+    if (ce != cudaSuccess) {
+        set_error(std::string("sytrd cluster launch: ") + cudaGetErrorString(ce));
+        *err = MPJ_ERR_CUDA;
+    }
+    return true;
+}
+
 static mpj_status sytrd_run(float *A32, int64_t lda, int n, SymqrWs &w, int64_t np, cudaStream_t st)
 {
-    if (n >= 3 && n <= 1536) {          // the one-cluster kernel when the matrix fits its shared memory
-        const char *env = getenv("MPJ_SYTRD_CLUSTER");
-        const size_t smem = sc_smem(n);
-        bool use = !(env && env[0] == '0') && smem <= 227 * 1024 - 1024;
-        cudaLaunchConfig_t cfg = {};
-        cudaLaunchAttribute at[1];
-        cfg.gridDim = dim3(SCL); cfg.blockDim = dim3(SCNT); cfg.dynamicSmemBytes = smem; cfg.stream = st;
-        at[0].id = cudaLaunchAttributeClusterDimension;
-        at[0].val.clusterDim.x = SCL; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
-        cfg.attrs = at; cfg.numAttrs = 1;
-        if (use) {
-            // whether a 16-CTA cluster with this much shared memory fits: asked once per
-            // (device, size) -- the occupancy query costs more than a small n's whole kernel
-            static std::mutex mu;
-            static std::map<std::pair<int, size_t>, bool> fits;
-            int dev = 0;
-            cudaGetDevice(&dev);
-            std::lock_guard<std::mutex> lk(mu);
-            auto key = std::make_pair(dev, smem);
-            auto it = fits.find(key);
-            if (it == fits.end()) {
-                bool ok = cudaFuncSetAttribute(k_sytrd_cluster, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) ==
-                              cudaSuccess &&
-                          smem_optin((const void *)k_sytrd_cluster, smem, SCNT, nullptr) == cudaSuccess;
-                int ncl = 0;
-                if (ok) ok = cudaOccupancyMaxActiveClusters(&ncl, k_sytrd_cluster, &cfg) == cudaSuccess && ncl > 0;
-                cudaGetLastError();        // a refused size only selects the panel kernel
-                it = fits.emplace(key, ok).first;
-            }
-            use = it->second && smem_optin((const void *)k_sytrd_cluster, smem, SCNT, nullptr) == cudaSuccess;
-            if (use) {
-                MPJ_CK(cudaMemsetAsync(w.d, 0, np * 4, st));
-                MPJ_CK(cudaMemsetAsync(w.e, 0, np * 4, st));
-                MPJ_CK(cudaMemsetAsync(w.tau, 0, np * 4, st));
-                const bool prof = prof_on();
-                if (prof) prof_mark("symqr_sytrd", st, true);
-                MPJ_CK(cudaLaunchKernelEx(&cfg, k_sytrd_cluster, A32, lda, n, w.d, w.e, w.tau));
-                if (prof) prof_mark("symqr_sytrd", st, false);
-                count_launch();
-                return MPJ_OK;
-            }
-        }
+    {
+        MPJ_CK(cudaMemsetAsync(w.d, 0, np * 4, st));
+        MPJ_CK(cudaMemsetAsync(w.e, 0, np * 4, st));
+        MPJ_CK(cudaMemsetAsync(w.tau, 0, np * 4, st));
+        mpj_status err;
+        if (sytrd_cluster_launch(A32, lda, n, w.d, w.e, w.tau, st, &err)) return err;
     }
     const int nt = (int)(np / TB);
     // a grid sized to the work: small matrices pay per-column barrier and
@@ -1654,7 +1671,23 @@ static mpj_status sytrd_run(float *A32, int64_t lda, int n, SymqrWs &w, int64_t 
             return MPJ_ERR_INVALID;
         }
     }
+    // the trailing matrix goes to the one-cluster kernel once it fits (n - k0 <=
+    // ~1150): its columns cost ~7 us instead of the panel kernel's ~20 us of
+    // grid barriers and partial-sum reductions
+    int handoff = -1;
+    {
+        const char *env = getenv("MPJ_SYTRD_CLUSTER");
+        if (!(env && env[0] == '0'))
+            for (int k0 = TB; k0 < ncolumns; k0 += TB)
+                if (n - k0 <= 1152 && sc_smem(n - k0) <= 227 * 1024 - 1024) { handoff = k0; break; }
+    }
     for (int k0 = 0; k0 < ncolumns; k0 += TB) {
+        if (k0 == handoff) {
+            mpj_status err;
+            if (sytrd_cluster_launch(A32 + k0 + (size_t)k0 * lda, lda, n - k0, w.d + k0, w.e + k0, w.tau + k0, st,
+                                     &err))
+                return err;                // it also wrote the tail (d, e, tau of the last columns)
+        }
         a.k0 = k0;
         a.ncols = std::min(TB, ncolumns - k0);
         MPJ_CK(cudaMemsetAsync(w.V, 0, np * TB * 4, st));
