@@ -569,17 +569,17 @@ __device__ __forceinline__ R *inner_rounds_pipe(R *D0, R *D1, const int2 *__rest
         const int pn = a < c ? a : c, qn = a < c ? c : a;   // bp = (0, 1): local order == global order
         R app, aqq, apq;
         if (!P) {
-            app = Dc[pn + pn * LD]; aqq = Dc[qn + qn * LD]; apq = Dc[pn + qn * LD];
+            app = Dc[pn + pn * LD]; aqq = Dc[qn + qn * LD]; apq = Dc[didx<R, true>(pn, qn)];
         } else {
-            app = diag_after<R, false>(Dc, *P, pn);
-            aqq = diag_after<R, false>(Dc, *P, qn);
+            app = diag_after<R, true>(Dc, *P, pn);
+            aqq = diag_after<R, true>(Dc, *P, qn);
             const int k = P->pos[pn], l = P->pos[qn];
             R x11, x21, x12, x22;
             if (k < l) {
-                tile_after<R, false>(Dc, *P, k, l, x11, x21, x12, x22);
+                tile_after<R, true>(Dc, *P, k, l, x11, x21, x12, x22);
                 apq = (pn == P->p[k]) ? (qn == P->p[l] ? x11 : x12) : (qn == P->p[l] ? x21 : x22);
             } else {
-                tile_after<R, false>(Dc, *P, l, k, x11, x21, x12, x22);
+                tile_after<R, true>(Dc, *P, l, k, x11, x21, x12, x22);
                 apq = (qn == P->p[l]) ? (pn == P->p[k] ? x11 : x12) : (pn == P->p[k] ? x21 : x22);
             }
         }
@@ -618,17 +618,18 @@ __device__ __forceinline__ R *inner_rounds_pipe(R *D0, R *D1, const int2 *__rest
                 if (e >= NI) break;
                 if (e < BW) {
                     const int pk = P.p[e], qk = P.q[e];
-                    const R apq = Dc[pk + qk * LD], t = P.t[e];
+                    const R apq = Dc[didx<R, true>(pk, qk)], t = P.t[e];
                     Dn[pk + pk * LD] = fmaR(-t, apq, Dc[pk + pk * LD]);
                     Dn[qk + qk * LD] = fmaR(t, apq, Dc[qk + qk * LD]);
-                    Dn[pk + qk * LD] = R(0);
-                    Dn[qk + pk * LD] = R(0);
+                    Dn[didx<R, true>(pk, qk)] = R(0);
                 } else {
+                    // upper triangle only during the sweep (mirrored once at its end):
+                    // half the stores of the full-storage update, the same values
                     R x11, x21, x12, x22;
-                    tile_after<R, false>(Dc, P, tk[u], tl[u], x11, x21, x12, x22);
+                    tile_after<R, true>(Dc, P, tk[u], tl[u], x11, x21, x12, x22);
                     const int pk = P.p[tk[u]], qk = P.q[tk[u]], pl = P.p[tl[u]], ql = P.q[tl[u]];
-                    Dn[pk + pl * LD] = x11; Dn[qk + pl * LD] = x21; Dn[pk + ql * LD] = x12; Dn[qk + ql * LD] = x22;
-                    Dn[pl + pk * LD] = x11; Dn[pl + qk * LD] = x21; Dn[ql + pk * LD] = x12; Dn[ql + qk * LD] = x22;
+                    Dn[didx<R, true>(pk, pl)] = x11; Dn[didx<R, true>(qk, pl)] = x21;
+                    Dn[didx<R, true>(pk, ql)] = x12; Dn[didx<R, true>(qk, ql)] = x22;
                 }
             }
         }
@@ -655,11 +656,15 @@ __device__ __forceinline__ R *inner_rounds_pipe(R *D0, R *D1, const int2 *__rest
         __syncthreads();
         R *tmp = Dc; Dc = Dn; Dn = tmp;
     }
-    // U back into the buffer that does not hold D
+    // U back into the buffer that does not hold D; D's lower triangle from its upper one
     #pragma unroll
     for (int i = 0; i < 8; ++i) {
         Dn[(w + 8 * i) + lane * LD] = ut[i];
         Dn[(w + 8 * i) + (BW + lane) * LD] = ub[i];
+    }
+    for (int e = tid; e < TW * TW; e += NT) {
+        const int i = e & (TW - 1), j = e >> 6;
+        if (i > j) Dc[i + j * LD] = Dc[j + i * LD];
     }
     __syncthreads();
     *uout = Dn;
