@@ -682,6 +682,8 @@ def main():
             step_ms.append((s0, s1))
         e1.record()
         torch.cuda.synchronize()
+        if ws > 1:
+            torch.distributed.barrier()
     step_ms = [a.elapsed_time(b) for a, b in step_ms]
     mpj.profile_enable(False)
     launches = mpj.launch_count() - l0
