@@ -748,3 +748,17 @@ def test_orth_series_declines_to_cgs(mpj, orc):
     lam, V = host(res.lam), host(res.V)
     assert np.max(np.abs(lam - lam_true)) <= 1e-13 * np.abs(lam_true).max()
     assert np.linalg.norm(V.T @ V - np.eye(n)) <= n * 1e-15
+
+
+@pytest.mark.parametrize("n,mode", [(1500, 3), (2100, 4), (1153, 5)])
+def test_eig_odd_sizes_vs_generator(mpj, n, mode):
+    """Sizes that are not multiples of 64 above the one-cluster limit: the panel
+    tridiagonalisation hands an odd-sized trailing matrix to the cluster kernel,
+    the block variant pads to n_p; north_star tolerances against the
+    generator's exact spectrum (no oracle run at these sizes)."""
+    A, lam_true = W.example1(n, 1e6 if mode == 3 else 1e3, mode, W.seed_for(1, mode, 1e3, 55))
+    res = mpj.eig(dev(A))
+    lam, V = host(res.lam), host(res.V)
+    assert np.max(np.abs(lam - lam_true)) <= 1e-13 * np.abs(lam_true).max()
+    assert np.linalg.norm(V.T @ V - np.eye(n)) <= n * 1e-15
+    assert np.linalg.norm(A @ V - V * lam) / np.linalg.norm(A) <= n * 1e-15
