@@ -306,21 +306,33 @@ __device__ __forceinline__ void apply_item_f64(const ApplyArgs &p, int item, dou
 // chunks.  Results go from the accumulators to global memory.  The three
 // CTAs of an SM start at different thirds of their item lists.
 // ---------------------------------------------------------------------------
-template <bool SKIP>
+// GROUPED: one CTA per SM of three 256-thread groups, each running this body
+// on its own two buffers with its own named barrier; the groups take the
+// SM's items (static across SMs) from a shared-memory counter, so they finish
+// within one item of each other.  Three separate CTAs per SM (GROUPED =
+// false) hold equal item lists but run at unequal speeds on the shared SM
+// (per-CTA timestamps, tools/k4_trace.py: CTAs of one SM end up to 310 us
+// apart in a 676 us launch; 0.76 of the CTA-slot time occupied).
+template <bool SKIP, bool GROUPED = false>
 __device__ __forceinline__ void apply_x3_body(const ApplyArgs &p, unsigned char *smem_raw)
 {
     constexpr int LD = Lay<double>::LD, EPC = 2, CPC = TW / EPC;
     constexpr bool skips = SKIP;
-    double *xb = (double *)smem_raw, *ub = xb + TW * LD;
+    const int grp = GROUPED ? (int)(threadIdx.x >> 8) : 0;
+    double *xb = (double *)smem_raw + (size_t)grp * 2 * TW * LD, *ub = xb + TW * LD;
     const int mb = p.S.nb >> 1;
     const int total = p.ntT + p.ntV;
     const int2 *bsr = p.S.bsched + p.Rb * mb;
     const double *Ub = (const double *)p.Ubuf;
-    const int tid = threadIdx.x;
+    const int tid = GROUPED ? (int)(threadIdx.x & (NT - 1)) : (int)threadIdx.x;
     const int G = gridDim.x;
     const int K = (int)blockIdx.x < total ? (total - 1 - (int)blockIdx.x) / G + 1 : 0;
-    const int phase = (int)(3 * (int64_t)blockIdx.x / G);      // 0, 1, 2: the CTAs of an SM
+    const int phase = GROUPED ? 0 : (int)(3 * (int64_t)blockIdx.x / G);      // 0, 1, 2: the CTAs of an SM
     const int k0 = (phase * K) / 3;
+    auto __syncthreads = [&]() {
+        if constexpr (GROUPED) asm volatile("bar.sync %0, %1;\n" ::"r"(1 + grp), "r"(NT) : "memory");
+        else ::__syncthreads();
+    };
     auto item_of = [&](int kk) {
         int k = kk + k0;
         if (k >= K) k -= K;
@@ -329,6 +341,15 @@ __device__ __forceinline__ void apply_x3_body(const ApplyArgs &p, unsigned char 
     auto next_kk = [&](int kk) {
         while (skips && kk < K && item_identity(p, item_of(kk), mb)) ++kk;
         return kk;
+    };
+    // GROUPED: the SM's item counter and, per group, the next item index (two
+    // slots by iteration parity: a slot is rewritten only two barriers later)
+    int *s_ctr = (int *)(smem_raw + (size_t)3 * 2 * TW * LD * sizeof(double));
+    int *s_nxt = s_ctr + 1 + 2 * grp;
+    auto fetch = [&]() {                        // the group leader claims the next non-identity item
+        int kk;
+        do { kk = atomicAdd(s_ctr, 1); } while (skips && kk < K && item_identity(p, item_of(kk), mb));
+        return kk < K ? kk : K;
     };
     struct It {
         int item, a, c, r0;
@@ -448,17 +469,29 @@ __device__ __forceinline__ void apply_x3_body(const ApplyArgs &p, unsigned char 
             });
         }
     };
-    int kk = next_kk(0);
+    int kk;
+    if constexpr (GROUPED) {
+        if (threadIdx.x == 0) *s_ctr = 0;
+        ::__syncthreads();
+        if (tid == 0) s_nxt[0] = fetch();
+        __syncthreads();
+        kk = s_nxt[0];
+    } else {
+        kk = next_kk(0);
+    }
     It cur;
     if (kk < K) {
         cur = decode(item_of(kk));
         issue(cur);
     }
-    while (kk < K) {
+    for (int it = 1; kk < K; ++it) {
+        if constexpr (GROUPED) {
+            if (tid == 0) s_nxt[it & 1] = fetch();                // read after the barriers of compute
+        }
         Acc<double> acc;
         compute(cur, acc);
         __syncthreads();                                         // shared memory free
-        const int kn = next_kk(kk + 1);
+        const int kn = GROUPED ? s_nxt[it & 1] : next_kk(kk + 1);
         It nxt = cur;
         if (kn < K) {
             nxt = decode(item_of(kn));
@@ -471,12 +504,46 @@ __device__ __forceinline__ void apply_x3_body(const ApplyArgs &p, unsigned char 
     cp_wait0();
 }
 
+// per-CTA start / end timestamps and SM of the last fp64 apply launch, for
+// tools/k4_trace.py (a build with -DMPJ_K4_TRACE only)
+#ifdef MPJ_K4_TRACE
+__device__ unsigned long long g_k4_trace[1024 * 3];
+__device__ __forceinline__ void k4_trace(int ev)
+{
+    if (threadIdx.x == 0 && blockIdx.x < 1024) {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        g_k4_trace[blockIdx.x * 3 + ev] = t;
+        if (ev == 0) {
+            unsigned sm;
+            asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
+            g_k4_trace[blockIdx.x * 3 + 2] = sm;
+        }
+    }
+}
+#define K4_TRACE(ev) k4_trace(ev)
+#else
+#define K4_TRACE(ev)
+#endif
+
 __global__ void __launch_bounds__(NT, 3) k_block_apply_f64x3(ApplyArgs p)
 {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     asm volatile("griddepcontrol.wait;\n" ::: "memory");   // launched early (PDL): wait for K3
+    K4_TRACE(0);
     if (p.uid && *p.nid > 0) apply_x3_body<true>(p, smem_raw);
     else apply_x3_body<false>(p, smem_raw);
+    K4_TRACE(1);
+}
+
+__global__ void __launch_bounds__(3 * NT, 1) k_block_apply_f64g3(ApplyArgs p)
+{
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    asm volatile("griddepcontrol.wait;\n" ::: "memory");   // launched early (PDL): wait for K3
+    K4_TRACE(0);
+    if (p.uid && *p.nid > 0) apply_x3_body<true, true>(p, smem_raw);
+    else apply_x3_body<false, true>(p, smem_raw);
+    K4_TRACE(1);
 }
 
 // SKIP: this block round has identity blocks (skip / one-product logic); the
@@ -1097,14 +1164,28 @@ static cudaError_t launch_pdl(void (*k)(KA...), dim3 grid, dim3 block, size_t sm
     return cudaLaunchKernelEx(&cfg, k, args...);
 }
 
+// MPJ_F64_APPLY: "2cta" the two-stage kernel, "x3" three CTAs per SM with
+// static item lists, default g3 (three groups in one CTA per SM sharing the
+// SM's items)
 static int f64_apply_kind()
 {
     static int v = -1;
     if (v < 0) {
         const char *e = getenv("MPJ_F64_APPLY");
-        v = (e && std::string(e) == "2cta") ? 0 : 1;
+        v = (e && std::string(e) == "2cta") ? 0 : (e && std::string(e) == "x3") ? 1 : 2;
     }
     return v;
+}
+
+static cudaError_t launch_apply_f64g3(const ApplyArgs &p, cudaStream_t st)
+{
+    const size_t smem = 3 * 2 * TW * Lay<double>::LD * sizeof(double) + 8 * sizeof(int);
+    cudaError_t e = smem_optin((const void *)k_block_apply_f64g3, smem, 3 * NT, nullptr);
+    if (e != cudaSuccess) return e;
+    const int total = p.ntT + p.ntV;
+    const int grid = std::max(1, std::min(total, sm_count()));
+    count_launch();
+    return launch_pdl(k_block_apply_f64g3, dim3(grid), dim3(3 * NT), smem, st, p);
 }
 
 static cudaError_t launch_apply_f64x3(const ApplyArgs &p, cudaStream_t st)
@@ -1197,7 +1278,9 @@ static cudaError_t launch_apply(const ApplyArgs &p, cudaStream_t st)
     cudaError_t e = cudaSuccess;
     if (sizeof(R) == 4 && fp32_apply_kind() == 2 && p.mrows % 4 == 0 && launch_apply_f32ws(p, st, &e)) return e;
     if (sizeof(R) == 4 && fp32_apply_kind() >= 1) return launch_apply_f32w(p, st);
-    if (sizeof(R) == 8 && apply_stages() == 1 && f64_apply_kind() == 1)   // also column-only (SVD) launches
+    if (sizeof(R) == 8 && apply_stages() == 1 && f64_apply_kind() == 2)   // also column-only (SVD) launches
+        return launch_apply_f64g3(p, st);
+    if (sizeof(R) == 8 && apply_stages() == 1 && f64_apply_kind() == 1)
         return launch_apply_f64x3(p, st);
     if (apply_stages() == 2) return launch_apply_s<R, 2>(p, st);
     // column updates only (the SVD): two buffers per CTA, 3 CTAs/SM (an
@@ -1302,4 +1385,12 @@ template mpj_status block_sweep<double>(double *, int64_t, double *, int64_t, in
 template mpj_status block_sweep<float>(float *, int64_t, float *, int64_t, int, const DevSched &, float, int,
                                        unsigned long long *, void *, cudaStream_t, bool, int, int);
 
+#ifdef MPJ_K4_TRACE
+}  // namespace mpj
+extern "C" int mpjacobi_debug_k4_trace(unsigned long long *out)
+{
+    return cudaMemcpyFromSymbol(out, mpj::g_k4_trace, sizeof(mpj::g_k4_trace)) == cudaSuccess ? 0 : 1;
+}
+namespace mpj {
+#endif
 }  // namespace mpj

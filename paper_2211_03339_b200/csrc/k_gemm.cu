@@ -188,7 +188,8 @@ __global__ void k_splitk_reduce(int64_t m, int64_t n, int splits, const double *
 
 void launch_dgemm(bool ta, bool tb, int64_t m, int64_t n, int64_t k, double alpha, const double *A,
                   int64_t lda, const double *B, int64_t ldb, double beta, double *C, int64_t ldc,
-                  cudaStream_t st, double *scratch, size_t scratch_elems, bool upper_only, const int *skip)
+                  cudaStream_t st, double *scratch, size_t scratch_elems, bool upper_only, const int *skip,
+                  int min_splits)
 {
     if (m <= 0 || n <= 0) return;
     const int64_t gm = (m + BM - 1) / BM, gn = (n + BN - 1) / BN;
@@ -196,6 +197,10 @@ void launch_dgemm(bool ta, bool tb, int64_t m, int64_t n, int64_t k, double alph
     const int64_t tiles = gm * gn;
     if (tiles < 148 && k >= 1024 && scratch) {
         splits = (int)std::min<int64_t>((296 + tiles - 1) / tiles, k / 256);
+        while (splits > 1 && (size_t)splits * m * n > scratch_elems) --splits;
+    }
+    if (min_splits > splits && scratch && k >= 256 * min_splits) {   // caller's hint (shapes it measured)
+        splits = min_splits;
         while (splits > 1 && (size_t)splits * m * n > scratch_elems) --splits;
     }
     int kchunk = (int)(((k + splits - 1) / splits + BK - 1) / BK * BK);

@@ -1741,7 +1741,11 @@ static mpj_status backtransform_run(const float *A32, int64_t lda, int n, SymqrW
         MPJ_CK(smem_optin((const void *)k_build_tp, tsm, 1024, nullptr));
         k_build_tp<<<1, 1024, tsm, st>>>(w.Gm, w.tau, k0, nr, w.Tp);
         count_launch();
-        launch_dgemm(true, false, BT, n, m, 1.0, w.Vp, np, Y + r0, ldy, 0.0, w.W1, BT, st, w.skw, w.skw_elems);
+        // W1 = Vp^T Y: only 2 x n/64 output tiles with K = m -- split K 4 ways (n = 8192: 58.6 -> 56.3 ms
+        // for the whole back-transformation; MPJ_BT_SPLITS overrides for A/B runs)
+        static const int bt_splits = getenv("MPJ_BT_SPLITS") ? std::max(1, atoi(getenv("MPJ_BT_SPLITS"))) : 4;
+        launch_dgemm(true, false, BT, n, m, 1.0, w.Vp, np, Y + r0, ldy, 0.0, w.W1, BT, st, w.skw, w.skw_elems, false,
+                     nullptr, bt_splits);
         launch_dgemm(false, false, BT, n, BT, 1.0, w.Tp, BT, w.W1, BT, 0.0, w.W2, BT, st);
         launch_dgemm(false, false, m, n, BT, -1.0, w.Vp, np, w.W2, BT, 1.0, Y + r0, ldy, st);
     }

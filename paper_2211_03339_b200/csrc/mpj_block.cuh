@@ -738,7 +738,7 @@ template <> struct Acc<double> {
     }
     template <typename F> __device__ __forceinline__ void each(F f) const
     {
-        const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+        const int warp = (threadIdx.x >> 5) & 7, lane = threadIdx.x & 31;
         const int r0 = (warp >> 1) * 16 + (lane >> 2), c0 = (warp & 1) * 32 + 2 * (lane & 3);
         #pragma unroll
         for (int mi = 0; mi < 2; ++mi)
@@ -751,7 +751,7 @@ template <> struct Acc<double> {
     // as each, the entry by reference
     template <typename F> __device__ __forceinline__ void each_ref(F f)
     {
-        const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+        const int warp = (threadIdx.x >> 5) & 7, lane = threadIdx.x & 31;
         const int r0 = (warp >> 1) * 16 + (lane >> 2), c0 = (warp & 1) * 32 + 2 * (lane & 3);
         #pragma unroll
         for (int mi = 0; mi < 2; ++mi)
@@ -764,7 +764,7 @@ template <> struct Acc<double> {
     // (i, j) pairs with j, j+1 adjacent: f2(i, j, v_j, v_j+1)
     template <typename F> __device__ __forceinline__ void each2(F f) const
     {
-        const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+        const int warp = (threadIdx.x >> 5) & 7, lane = threadIdx.x & 31;
         const int r0 = (warp >> 1) * 16 + (lane >> 2), c0 = (warp & 1) * 32 + 2 * (lane & 3);
         #pragma unroll
         for (int mi = 0; mi < 2; ++mi)
@@ -795,7 +795,7 @@ template <bool TRANS_A>
 __device__ __forceinline__ void tile_mm_acc(const double *A, const double *B, Acc<double> &acc)
 {
     constexpr int LD = Lay<double>::LD;
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, tig = lane & 3;
+    const int warp = (threadIdx.x >> 5) & 7, lane = threadIdx.x & 31, g = lane >> 2, tig = lane & 3;
     const int rb = (warp >> 1) * 16 + g, cb = (warp & 1) * 32 + g;
     #pragma unroll 4
     for (int ks = 0; ks < TW / 4; ++ks) {
@@ -821,7 +821,7 @@ __device__ __forceinline__ void tile_mm2(const double *A1, const double *A2, con
                                          Acc<double> &c2)
 {
     constexpr int LD = Lay<double>::LD;
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, tig = lane & 3;
+    const int warp = (threadIdx.x >> 5) & 7, lane = threadIdx.x & 31, g = lane >> 2, tig = lane & 3;
     const int rb = (warp >> 1) * 16 + g, cb = (warp & 1) * 32 + g;
     c1.zero();
     c2.zero();
@@ -853,7 +853,7 @@ template <bool TRANS_A, typename W>
 __device__ __forceinline__ void tile_mm_chunked(const double *A, const double *B, Acc<double> &acc, W wait)
 {
     constexpr int LD = Lay<double>::LD;
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, tig = lane & 3;
+    const int warp = (threadIdx.x >> 5) & 7, lane = threadIdx.x & 31, g = lane >> 2, tig = lane & 3;
     const int rb = (warp >> 1) * 16 + g, cb = (warp & 1) * 32 + g;
     acc.zero();
     #pragma unroll 1
@@ -883,7 +883,7 @@ __device__ __forceinline__ void tile_mm2_chunked(const double *A1, const double 
                                                  Acc<double> &c1, Acc<double> &c2, W wait)
 {
     constexpr int LD = Lay<double>::LD;
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, tig = lane & 3;
+    const int warp = (threadIdx.x >> 5) & 7, lane = threadIdx.x & 31, g = lane >> 2, tig = lane & 3;
     const int rb = (warp >> 1) * 16 + g, cb = (warp & 1) * 32 + g;
     c1.zero();
     c2.zero();

@@ -123,7 +123,8 @@ void launch_extract_evd(const double *T, int64_t ldt, const double *V, int64_t l
 void launch_dgemm(bool ta, bool tb, int64_t m, int64_t n, int64_t k, double alpha,
                   const double *A, int64_t lda, const double *B, int64_t ldb, double beta,
                   double *C, int64_t ldc, cudaStream_t st, double *scratch = nullptr,
-                  size_t scratch_elems = 0, bool upper_only = false, const int *skip = nullptr);
+                  size_t scratch_elems = 0, bool upper_only = false, const int *skip = nullptr,
+                  int min_splits = 1);
 // upper_only: only the 64 x 64 tiles of C that meet its upper triangle are
 // computed (a symmetric product such as C^T C); the rest of C is left as is.
 // skip (device int, may be NULL): the product is skipped when *skip != 0.
