@@ -1308,7 +1308,7 @@ mpj_status block_sweep(R *T, int64_t ldt, R *V, int64_t ldv, int vrows, const De
     const bool fastp = sizeof(R) == 8 && !(ie && ie[0] == '1');
     auto solve = fastp ? k_block_solve<R, sizeof(R) == 8> : k_block_solve<R, false>;
     MPJ_CK(smem_optin((const void *)solve, sm_solve, NTW, nullptr));
-    ApplyArgs ap;
+    ApplyArgs ap{};
     ap.T = T; ap.ldt = ldt; ap.M = V; ap.ldm = ldv; ap.mrows = vrows; ap.S = S; ap.Ubuf = Ubuf; ap.uid = uid;
     ap.ntT = mb * (mb - 1) / 2;
     ap.ntV = ((vrows + TW - 1) / TW) * mb;
@@ -1367,7 +1367,7 @@ cudaError_t launch_block_apply_cols(R *M, int64_t ld, int rows, const DevSched &
 {
     Sched S;
     S.bsched = ds.bsched; S.lsched = ds.lsched; S.b = ds.b; S.nb = ds.nb; S.np = ds.np;
-    ApplyArgs ap;
+    ApplyArgs ap{};
     ap.T = nullptr; ap.ldt = 0; ap.M = M; ap.ldm = ld; ap.mrows = rows; ap.S = S; ap.Rb = Rb; ap.Ubuf = Ubuf; ap.uid = uid; ap.nid = nid;
     ap.ntT = 0;
     ap.ntV = ((rows + TW - 1) / TW) * (ds.nb / 2);

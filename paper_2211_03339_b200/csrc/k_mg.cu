@@ -243,11 +243,11 @@ __global__ void __launch_bounds__(NT) k_mg_apply(MgApply p)
     }
 }
 
-// fp64 apply of the partitioned sweep with two buffers per CTA (3 CTAs per
-// SM), as k_block_apply_f64x3: X / Y share one buffer, U_a and U_c the other
-// (U_c's k-chunks stream into U_a's dead rows during Y = U_a^T X); k-chunked
-// cp.async loads; results from the accumulators to global memory; the CTAs of
-// an SM start at different thirds of their item lists.
+// fp64 apply of the partitioned sweep with two buffers per 256-thread group
+// (three groups per SM), as k_block.cu's apply_x3_body: X / Y share one
+// buffer, U_a and U_c the other (U_c's k-chunks stream into U_a's dead rows
+// during Y = U_a^T X); k-chunked cp.async loads; results from the
+// accumulators to global memory.
 __device__ __forceinline__ void mg_wait_le(int n)
 {
     switch (n) {
@@ -258,20 +258,41 @@ __device__ __forceinline__ void mg_wait_le(int n)
     }
 }
 
-__global__ void __launch_bounds__(NT, 3) k_mg_apply_f64x3(MgApply p)
+// GROUPED (the default launch): one CTA per SM of three 256-thread groups,
+// each with its own buffers and named barrier, taking the SM's items from a
+// shared-memory counter (k_block.cu, apply_x3_body: separate CTAs of one SM
+// run at unequal speeds and finish far apart)
+template <bool GROUPED>
+__device__ __forceinline__ void mg_apply_x3_body(const MgApply &p, unsigned char *smem_raw)
 {
     constexpr int LD = Lay<double>::LD, EPC = 2, CPC = TW / EPC;
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    double *xb = (double *)smem_raw, *ub = xb + TW * LD;
+    const int grp = GROUPED ? (int)(threadIdx.x >> 8) : 0;
+    double *xb = (double *)smem_raw + (size_t)grp * 2 * TW * LD, *ub = xb + TW * LD;
     const double *Ub = (const double *)p.Ubuf;
     const int total = p.ntT + p.ntV;
     const bool skips = p.uid && *p.nid > 0;
-    const int tid = threadIdx.x;
+    const int tid = GROUPED ? (int)(threadIdx.x & (NT - 1)) : (int)threadIdx.x;
     const int G = gridDim.x;
     const int K = (int)blockIdx.x < total ? (total - 1 - (int)blockIdx.x) / G + 1 : 0;
-    const int phase = (int)(3 * (int64_t)blockIdx.x / G);
+    const int phase = GROUPED ? 0 : (int)(3 * (int64_t)blockIdx.x / G);
     const int k0 = (phase * K) / 3;
-    for (int kk = 0; kk < K; ++kk) {
+    auto __syncthreads = [&]() {
+        if constexpr (GROUPED) asm volatile("bar.sync %0, %1;\n" ::"r"(1 + grp), "r"(NT) : "memory");
+        else ::__syncthreads();
+    };
+    int *s_ctr = (int *)(smem_raw + (size_t)3 * 2 * TW * LD * sizeof(double));
+    int *s_nxt = s_ctr + 1 + 2 * grp;
+    if constexpr (GROUPED) {
+        if (threadIdx.x == 0) *s_ctr = 0;
+        ::__syncthreads();
+    }
+    for (int kk = 0, it = 0;; ++kk, ++it) {
+        if constexpr (GROUPED) {
+            if (tid == 0) s_nxt[it & 1] = atomicAdd(s_ctr, 1);   // rewritten two barriers later
+            __syncthreads();
+            kk = s_nxt[it & 1];
+        }
+        if (kk >= K) break;
         int k = kk + k0;
         if (k >= K) k -= K;
         const int item = (int)blockIdx.x + k * G;
@@ -361,6 +382,12 @@ __global__ void __launch_bounds__(NT, 3) k_mg_apply_f64x3(MgApply p)
         }
     }
     asm volatile("cp.async.wait_group 0;\n" ::);
+}
+
+__global__ void __launch_bounds__(3 * NT, 1) k_mg_apply_f64g3(MgApply p)
+{
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    mg_apply_x3_body<true>(p, smem_raw);
 }
 
 // fp32 apply of the partitioned sweep: 128-thread CTAs with 8 x 4 FFMA tiles
@@ -707,13 +734,13 @@ static mpj_status mg_sweep(Group &g, R **Ts, R **Vs, R nu, int rule)
     MPJ_CK(cudaStreamSynchronize(g.st));   // the host vectors above are about to die
     constexpr int LD = Lay<R>::LD;
     const size_t sm_solve = 3 * TW * LayK<R>::LD * sizeof(R), sm_apply = 3 * TW * LD * sizeof(R);
-    const size_t sm_apply64x3 = 2 * TW * Lay<double>::LD * sizeof(double);
+    const size_t sm_apply64g3 = 3 * 2 * TW * Lay<double>::LD * sizeof(double) + 8 * sizeof(int);
     MPJ_CK(smem_optin((const void *)k_mg_solve<R>, sm_solve, NTW, nullptr));
     MPJ_CK(smem_optin((const void *)k_mg_apply<R>, sm_apply, NT, nullptr));
     if (sizeof(R) == 4)
         MPJ_CK(smem_optin((const void *)k_mg_apply_f32, sm_apply, 128, nullptr));
     else
-        MPJ_CK(smem_optin((const void *)k_mg_apply_f64x3, sm_apply64x3, NT, nullptr));
+        MPJ_CK(smem_optin((const void *)k_mg_apply_f64g3, sm_apply64g3, 3 * NT, nullptr));
     int *nid = g.uid + P.mb;
     MPJ_CK(cudaMemsetAsync(nid, 0, (size_t)rounds * sizeof(int), g.st));
     int nsm = 148, dev = 0;
@@ -756,8 +783,8 @@ static mpj_status mg_sweep(Group &g, R **Ts, R **Vs, R nu, int rule)
                 const int grid = std::min(ap.ntT + ap.ntV, 4 * nsm);
                 k_mg_apply_f32<<<grid, 128, sm_apply, g.st>>>(ap);
             } else {
-                const int grid = std::min(ap.ntT + ap.ntV, 3 * nsm);
-                k_mg_apply_f64x3<<<grid, NT, sm_apply64x3, g.st>>>(ap);
+                const int grid = std::min(ap.ntT + ap.ntV, nsm);
+                k_mg_apply_f64g3<<<grid, 3 * NT, sm_apply64g3, g.st>>>(ap);
             }
             count_launch();
         }
