@@ -740,7 +740,7 @@ def main():
             by = by - (skt * 3 + skv * 2) * 64 * 64 * (8 if is64 else 4) / nl
         peak = pk["dmma_tflops"] if is64 else pk["ffma_tflops"]
         traffic = traffic_alg = None
-        tp = os.path.join(ROOT, "profiles", "r01_traffic.json")
+        tp = os.path.join(ROOT, "profiles", "r02_traffic.json")
         if os.path.exists(tp):
             t = json.load(open(tp)).get(base)
             if t and t.get("n_padded") == rep.n_padded:

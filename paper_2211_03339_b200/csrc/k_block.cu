@@ -118,6 +118,7 @@ struct ApplyArgs {
     const int *uid;       // per block pair: U is exactly I (nullptr: never skip)
     const int *nid;       // number of such block pairs this block round
     int ntT, ntV;
+    int *ctr;             // zeroed item counter of this launch (nullptr: per-SM item lists only)
 };
 
 __device__ __forceinline__ void decode_upper(int idx, int &a, int &c)
@@ -326,7 +327,13 @@ __device__ __forceinline__ void apply_x3_body(const ApplyArgs &p, unsigned char 
     const double *Ub = (const double *)p.Ubuf;
     const int tid = GROUPED ? (int)(threadIdx.x & (NT - 1)) : (int)threadIdx.x;
     const int G = gridDim.x;
-    const int K = (int)blockIdx.x < total ? (total - 1 - (int)blockIdx.x) / G + 1 : 0;
+    // GROUPED and no identity blocks (full launches): the groups of all SMs take
+    // items in index order (T tiles first) from one global counter, which also
+    // evens out the SMs (ends within 1-2 items instead of ~4%); with identity
+    // blocks the skips would make that a chain of global atomics, so the SM's
+    // static list (items b + kG) and a shared-memory counter are used
+    const bool gdyn = GROUPED && p.ctr != nullptr && !skips;
+    const int K = gdyn ? total : (int)blockIdx.x < total ? (total - 1 - (int)blockIdx.x) / G + 1 : 0;
     const int phase = GROUPED ? 0 : (int)(3 * (int64_t)blockIdx.x / G);      // 0, 1, 2: the CTAs of an SM
     const int k0 = (phase * K) / 3;
     auto __syncthreads = [&]() {
@@ -334,6 +341,7 @@ __device__ __forceinline__ void apply_x3_body(const ApplyArgs &p, unsigned char 
         else ::__syncthreads();
     };
     auto item_of = [&](int kk) {
+        if (gdyn) return kk;
         int k = kk + k0;
         if (k >= K) k -= K;
         return (int)blockIdx.x + k * G;
@@ -347,6 +355,7 @@ __device__ __forceinline__ void apply_x3_body(const ApplyArgs &p, unsigned char 
     int *s_ctr = (int *)(smem_raw + (size_t)3 * 2 * TW * LD * sizeof(double));
     int *s_nxt = s_ctr + 1 + 2 * grp;
     auto fetch = [&]() {                        // the group leader claims the next non-identity item
+        if (gdyn) return min(atomicAdd(p.ctr, 1), K);
         int kk;
         do { kk = atomicAdd(s_ctr, 1); } while (skips && kk < K && item_identity(p, item_of(kk), mb));
         return kk < K ? kk : K;
@@ -1105,8 +1114,8 @@ size_t block_scratch_bytes(int np, int b)
 {
     (void)b;
     const int mb = np / (2 * BW);
-    // U, U^T, identity flags, identity counts per block round
-    return (sizeof(R) == 4 ? 3 : 2) * (size_t)mb * TW * TW * sizeof(R) + (size_t)(mb + 2 * mb) * sizeof(int);
+    // U, U^T, identity flags, identity counts and apply item counters per block round
+    return (sizeof(R) == 4 ? 3 : 2) * (size_t)mb * TW * TW * sizeof(R) + (size_t)(mb + 2 * mb + 2 * mb) * sizeof(int);
 }
 
 static int sm_count()
@@ -1301,7 +1310,8 @@ mpj_status block_sweep(R *T, int64_t ldt, R *V, int64_t ldv, int vrows, const De
     R *Ubuf = (R *)scratch;
     int *uid = (int *)(Ubuf + (sizeof(R) == 4 ? 3 : 2) * (size_t)mb * TW * TW);
     int *nid = uid + mb;                         // nb - 1 <= 2 mb block rounds
-    MPJ_CK(cudaMemsetAsync(nid, 0, (size_t)(ds.nb - 1) * sizeof(int), st));
+    int *ctr = nid + 2 * mb;                     // the apply's item counter per block round
+    MPJ_CK(cudaMemsetAsync(nid, 0, (size_t)4 * mb * sizeof(int), st));
     const size_t sm_solve = 3 * TW * LayK<R>::LD * sizeof(R);
     // fp64: the fast parameter chain (R28) unless MPJ_K3_IEEE=1 (A/B and its parity test)
     const char *ie = getenv("MPJ_K3_IEEE");
@@ -1324,6 +1334,7 @@ mpj_status block_sweep(R *T, int64_t ldt, R *V, int64_t ldv, int vrows, const De
         if (prof) { prof_mark(nsolve, st, false); prof_mark(napply, st, true); }
         ap.Rb = Rb;
         ap.nid = nid + Rb;
+        ap.ctr = ctr + Rb;
         // the first sweep's launches are also timed apart: they have (almost) no
         // identity blocks, so they give the full-launch efficiency
         const std::string nfirst = std::string(napply) + ".sweep1";
