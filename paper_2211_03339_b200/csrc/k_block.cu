@@ -332,7 +332,7 @@ __device__ __forceinline__ void apply_x3_body(const ApplyArgs &p, unsigned char 
     // evens out the SMs (ends within 1-2 items instead of ~4%); with identity
     // blocks the skips would make that a chain of global atomics, so the SM's
     // static list (items b + kG) and a shared-memory counter are used
-    const bool gdyn = GROUPED && p.ctr != nullptr && !skips;
+    const bool gdyn = GROUPED && p.ctr != nullptr && (!skips || 4 * *p.nid <= mb);
     const int K = gdyn ? total : (int)blockIdx.x < total ? (total - 1 - (int)blockIdx.x) / G + 1 : 0;
     const int phase = GROUPED ? 0 : (int)(3 * (int64_t)blockIdx.x / G);      // 0, 1, 2: the CTAs of an SM
     const int k0 = (phase * K) / 3;
@@ -355,8 +355,11 @@ __device__ __forceinline__ void apply_x3_body(const ApplyArgs &p, unsigned char 
     int *s_ctr = (int *)(smem_raw + (size_t)3 * 2 * TW * LD * sizeof(double));
     int *s_nxt = s_ctr + 1 + 2 * grp;
     auto fetch = [&]() {                        // the group leader claims the next non-identity item
-        if (gdyn) return min(atomicAdd(p.ctr, 1), K);
         int kk;
+        if (gdyn) {
+            do { kk = atomicAdd(p.ctr, 1); } while (skips && kk < K && item_identity(p, item_of(kk), mb));
+            return kk < K ? kk : K;
+        }
         do { kk = atomicAdd(s_ctr, 1); } while (skips && kk < K && item_identity(p, item_of(kk), mb));
         return kk < K ? kk : K;
     };
