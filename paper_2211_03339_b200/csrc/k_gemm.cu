@@ -29,6 +29,12 @@ __device__ __forceinline__ void cp_async8(double *dst, const double *src, bool p
     const int sz = pred ? 8 : 0;
     asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(d), "l"(src), "r"(sz));
 }
+// two consecutive elements (16 bytes; src_bytes 8 or 0 zero-fill the rest)
+__device__ __forceinline__ void cp_async16(double *dst, const double *src, int src_bytes)
+{
+    const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 16, %2;\n" ::"r"(d), "l"(src), "r"(src_bytes));
+}
 __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::); }
 template <int N> __device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
 
@@ -42,10 +48,27 @@ __device__ __forceinline__ void dmma(double &d0, double &d1, double a, double b)
 // Load the op(A) tile (rows i0.., k0..) into shared memory.
 //   TA = false: A is m x k column-major -> k-major smem [kk][i]   (stride SKM)
 //   TA = true : A is k x m column-major -> m-major smem [i][kk]   (stride SMK)
-template <bool TA>
+template <bool TA, bool V16>
 __device__ __forceinline__ void load_a(double *s, const double *A, int64_t lda, int64_t m, int64_t k,
                                        int64_t i0, int64_t k0)
 {
+    if constexpr (V16) {   // 16-byte copies along the contiguous index (even lda, aligned A)
+        #pragma unroll
+        for (int e = threadIdx.x; e < BM * BK / 2; e += 128) {
+            if (!TA) {
+                const int kk = e / (BM / 2), ii = 2 * (e - kk * (BM / 2));
+                const int64_t gi = i0 + ii, gk = k0 + kk;
+                const int bytes = gk < k ? (gi + 1 < m ? 16 : (gi < m ? 8 : 0)) : 0;
+                cp_async16(s + kk * SKM + ii, bytes ? A + gi + gk * lda : A, bytes);
+            } else {
+                const int ii = e / (BK / 2), kk = 2 * (e - ii * (BK / 2));
+                const int64_t gi = i0 + ii, gk = k0 + kk;
+                const int bytes = gi < m ? (gk + 1 < k ? 16 : (gk < k ? 8 : 0)) : 0;
+                cp_async16(s + ii * SMK + kk, bytes ? A + gk + gi * lda : A, bytes);
+            }
+        }
+        return;
+    }
     #pragma unroll
     for (int e = threadIdx.x; e < BM * BK; e += 128) {
         if (!TA) {
@@ -64,10 +87,27 @@ __device__ __forceinline__ void load_a(double *s, const double *A, int64_t lda, 
 
 // op(B) tile (k0.., j0..): TB = false: B is k x n -> n-major smem [j][kk];
 // TB = true: B is n x k -> k-major smem [kk][j].
-template <bool TB>
+template <bool TB, bool V16>
 __device__ __forceinline__ void load_b(double *s, const double *B, int64_t ldb, int64_t n, int64_t k,
                                        int64_t j0, int64_t k0)
 {
+    if constexpr (V16) {
+        #pragma unroll
+        for (int e = threadIdx.x; e < BN * BK / 2; e += 128) {
+            if (!TB) {
+                const int jj = e / (BK / 2), kk = 2 * (e - jj * (BK / 2));
+                const int64_t gj = j0 + jj, gk = k0 + kk;
+                const int bytes = gj < n ? (gk + 1 < k ? 16 : (gk < k ? 8 : 0)) : 0;
+                cp_async16(s + jj * SMK + kk, bytes ? B + gk + gj * ldb : B, bytes);
+            } else {
+                const int kk = e / (BN / 2), jj = 2 * (e - kk * (BN / 2));
+                const int64_t gj = j0 + jj, gk = k0 + kk;
+                const int bytes = gk < k ? (gj + 1 < n ? 16 : (gj < n ? 8 : 0)) : 0;
+                cp_async16(s + kk * SKM + jj, bytes ? B + gj + gk * ldb : B, bytes);
+            }
+        }
+        return;
+    }
     #pragma unroll
     for (int e = threadIdx.x; e < BN * BK; e += 128) {
         if (!TB) {
@@ -85,7 +125,7 @@ __device__ __forceinline__ void load_b(double *s, const double *B, int64_t ldb, 
 }
 
 // split == 1: C = alpha acc + beta C.  split > 1: partial[z] = acc (m x n, ld m).
-template <bool TA, bool TB>
+template <bool TA, bool TB, bool V16>
 __global__ void __launch_bounds__(128) k_dgemm(int64_t m, int64_t n, int64_t k, double alpha,
                                                const double *__restrict__ A, int64_t lda,
                                                const double *__restrict__ B, int64_t ldb, double beta,
@@ -104,6 +144,18 @@ __global__ void __launch_bounds__(128) k_dgemm(int64_t m, int64_t n, int64_t k, 
     const int64_t kb = (int64_t)blockIdx.z * kchunk;
     const int64_t ke = min(k, kb + kchunk);
 
+    // C of the epilogue (beta != 0) into L2 now: its loads come after the
+    // k-loop, and for the short-K updates (the back-transformation's rank-128
+    // Y -= V W, K = 128) their HBM latency was the largest stall (ncu: long
+    // scoreboard 5.9 per issue, 52% tensor active)
+    if (beta != 0.0 && !partial) {
+        const int64_t gj = j0 + (threadIdx.x >> 1), gi = i0 + (threadIdx.x & 1) * 32;
+        if (gj < n && gi < m) {
+            const double *pc = C + gi + gj * ldc;
+            asm volatile("prefetch.global.L2 [%0];\n" ::"l"(pc));
+            if (gi + 16 < m) asm volatile("prefetch.global.L2 [%0];\n" ::"l"(pc + 16));
+        }
+    }
     double acc[4][4][2];
     #pragma unroll
     for (int a = 0; a < 4; ++a)
@@ -112,15 +164,15 @@ __global__ void __launch_bounds__(128) k_dgemm(int64_t m, int64_t n, int64_t k, 
 
     const int nk = (int)((ke - kb + BK - 1) / BK);
     if (nk > 0) {
-        load_a<TA>(sA[0], A, lda, m, ke, i0, kb);
-        load_b<TB>(sB[0], B, ldb, n, ke, j0, kb);
+        load_a<TA, V16>(sA[0], A, lda, m, ke, i0, kb);
+        load_b<TB, V16>(sB[0], B, ldb, n, ke, j0, kb);
     }
     cp_commit();
     for (int it = 0; it < nk; ++it) {
         const int cur = it & 1;
         if (it + 1 < nk) {
-            load_a<TA>(sA[cur ^ 1], A, lda, m, ke, i0, kb + (int64_t)(it + 1) * BK);
-            load_b<TB>(sB[cur ^ 1], B, ldb, n, ke, j0, kb + (int64_t)(it + 1) * BK);
+            load_a<TA, V16>(sA[cur ^ 1], A, lda, m, ke, i0, kb + (int64_t)(it + 1) * BK);
+            load_b<TB, V16>(sB[cur ^ 1], B, ldb, n, ke, j0, kb + (int64_t)(it + 1) * BK);
         }
         cp_commit();
         cp_wait<1>();
@@ -207,12 +259,16 @@ void launch_dgemm(bool ta, bool tb, int64_t m, int64_t n, int64_t k, double alph
     if (kchunk <= 0) kchunk = BK;
     dim3 grd((unsigned)gm, (unsigned)gn, (unsigned)splits);
     double *part = splits > 1 ? scratch : nullptr;
-#define GO(a, b) k_dgemm<a, b><<<grd, 128, 0, st>>>(m, n, k, alpha, A, lda, B, ldb, beta, C, ldc, kchunk, part, \
-                                                   upper_only ? 1 : 0, skip)
-    if (!ta && !tb) GO(false, false);
-    else if (ta && !tb) GO(true, false);
-    else if (!ta && tb) GO(false, true);
-    else GO(true, true);
+    // 16-byte operand copies when every column start is 16-byte aligned
+    const bool v16 = lda % 2 == 0 && ldb % 2 == 0 && ((uintptr_t)A & 15) == 0 && ((uintptr_t)B & 15) == 0;
+#define GO(a, b, v) k_dgemm<a, b, v><<<grd, 128, 0, st>>>(m, n, k, alpha, A, lda, B, ldb, beta, C, ldc, kchunk, \
+                                                         part, upper_only ? 1 : 0, skip)
+#define GO2(a, b) do { if (v16) GO(a, b, true); else GO(a, b, false); } while (0)
+    if (!ta && !tb) GO2(false, false);
+    else if (ta && !tb) GO2(true, false);
+    else if (!ta && tb) GO2(false, true);
+    else GO2(true, true);
+#undef GO2
 #undef GO
     count_launch();
     if (splits > 1) {
