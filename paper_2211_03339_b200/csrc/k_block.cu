@@ -327,13 +327,51 @@ __device__ __forceinline__ void apply_x3_body(const ApplyArgs &p, unsigned char 
     const double *Ub = (const double *)p.Ubuf;
     const int tid = GROUPED ? (int)(threadIdx.x & (NT - 1)) : (int)threadIdx.x;
     const int G = gridDim.x;
-    // GROUPED and no identity blocks (full launches): the groups of all SMs take
-    // items in index order (T tiles first) from one global counter, which also
-    // evens out the SMs (ends within 1-2 items instead of ~4%); with identity
-    // blocks the skips would make that a chain of global atomics, so the SM's
-    // static list (items b + kG) and a shared-memory counter are used
-    const bool gdyn = GROUPED && p.ctr != nullptr && (!skips || 4 * *p.nid <= mb);
-    const int K = gdyn ? total : (int)blockIdx.x < total ? (total - 1 - (int)blockIdx.x) / G + 1 : 0;
+    // GROUPED with an item counter (block_sweep's launches): the groups of all
+    // SMs take items from one global counter over the COMPACT list of this
+    // block round's non-identity items (T tiles first, then V tiles), built by
+    // every CTA at its start from the identity flags: L = non-identity blocks,
+    // T items c-major -- c in L: every a < c; c not in L: the a < c in L --
+    // with P = prefix counts to map a counter value to its tile.  No item is
+    // skipped after it is claimed, so all groups of all SMs end within about
+    // one item (static per-SM lists: up to 317 us apart within an SM, ~4%
+    // across SMs; identity skips unevenly spread).  Otherwise (no counter, or
+    // mb > 1024): the SM's static list (items b + kG) and a shared-memory counter.
+    int *s_ctr = (int *)(smem_raw + (size_t)3 * 2 * TW * LD * sizeof(double));
+    int *s_nxt = s_ctr + 1 + 2 * grp;
+    int *sL = s_ctr + 8, *sP = sL + mb;           // compact lists (GROUPED with a counter)
+    const bool gcomp = GROUPED && p.ctr != nullptr && mb <= 1024;
+    int nTc = p.ntT, mL = mb;                    // no identity blocks: the identity map
+    if (gcomp && skips) {
+        if (threadIdx.x < 32) {
+            const int lane = threadIdx.x;
+            int base = 0, pbase = 0;
+            for (int c0 = 0; c0 < mb; c0 += 32) {
+                const int c = c0 + lane;
+                const bool ni = c < mb && !(skips && p.uid[c]);
+                const unsigned bal = __ballot_sync(0xffffffffu, ni);
+                const int before = base + __popc(bal & ((1u << lane) - 1u));
+                if (ni) sL[before] = c;
+                const int cnt = c < mb ? (ni ? c : before) : 0;
+                int x = cnt;                                  // inclusive scan of cnt over the warp
+                #pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const int y = __shfl_up_sync(0xffffffffu, x, o);
+                    if (lane >= o) x += y;
+                }
+                if (c < mb) sP[c] = pbase + x - cnt;
+                pbase += __shfl_sync(0xffffffffu, x, 31);
+                base += __popc(bal);
+            }
+            if (lane == 0) { sP[mb] = pbase; s_ctr[7] = base; }
+        }
+        ::__syncthreads();
+        nTc = sP[mb];
+        mL = s_ctr[7];
+    }
+    const int nrt = p.ntV / mb;                  // row tiles of M
+    const int K = gcomp ? nTc + nrt * mL
+                        : (int)blockIdx.x < total ? (total - 1 - (int)blockIdx.x) / G + 1 : 0;
     const int phase = GROUPED ? 0 : (int)(3 * (int64_t)blockIdx.x / G);      // 0, 1, 2: the CTAs of an SM
     const int k0 = (phase * K) / 3;
     auto __syncthreads = [&]() {
@@ -341,7 +379,22 @@ __device__ __forceinline__ void apply_x3_body(const ApplyArgs &p, unsigned char 
         else ::__syncthreads();
     };
     auto item_of = [&](int kk) {
-        if (gdyn) return kk;
+        if (gcomp && !skips) return kk;
+        if (gcomp) {
+            if (kk < nTc) {                          // T tile: the largest c with P[c] <= kk
+                int lo = 0, hi = mb - 1;
+                while (lo < hi) {
+                    const int mid = (lo + hi + 1) >> 1;
+                    if (sP[mid] <= kk) lo = mid; else hi = mid - 1;
+                }
+                const int c = lo, o = kk - sP[c];
+                const bool cn = !(skips && p.uid[c]);
+                const int a = cn ? o : sL[o];
+                return c * (c - 1) / 2 + a;
+            }
+            const int q = kk - nTc;                      // V tile
+            return p.ntT + (q / mL) * mb + sL[q % mL];
+        }
         int k = kk + k0;
         if (k >= K) k -= K;
         return (int)blockIdx.x + k * G;
@@ -350,16 +403,11 @@ __device__ __forceinline__ void apply_x3_body(const ApplyArgs &p, unsigned char 
         while (skips && kk < K && item_identity(p, item_of(kk), mb)) ++kk;
         return kk;
     };
-    // GROUPED: the SM's item counter and, per group, the next item index (two
-    // slots by iteration parity: a slot is rewritten only two barriers later)
-    int *s_ctr = (int *)(smem_raw + (size_t)3 * 2 * TW * LD * sizeof(double));
-    int *s_nxt = s_ctr + 1 + 2 * grp;
+    // per group, the next item index: two slots by iteration parity (a slot is
+    // rewritten only two barriers later)
     auto fetch = [&]() {                        // the group leader claims the next non-identity item
+        if (gcomp) return min(atomicAdd(p.ctr, 1), K);
         int kk;
-        if (gdyn) {
-            do { kk = atomicAdd(p.ctr, 1); } while (skips && kk < K && item_identity(p, item_of(kk), mb));
-            return kk < K ? kk : K;
-        }
         do { kk = atomicAdd(s_ctr, 1); } while (skips && kk < K && item_identity(p, item_of(kk), mb));
         return kk < K ? kk : K;
     };
@@ -1191,7 +1239,9 @@ static int f64_apply_kind()
 
 static cudaError_t launch_apply_f64g3(const ApplyArgs &p, cudaStream_t st)
 {
-    const size_t smem = 3 * 2 * TW * Lay<double>::LD * sizeof(double) + 8 * sizeof(int);
+    const int mb = p.S.nb >> 1;
+    // three groups' buffers, counters, the compact lists (L, P) of the item counter
+    const size_t smem = 3 * 2 * TW * Lay<double>::LD * sizeof(double) + (8 + 2 * (size_t)mb + 1) * sizeof(int);
     cudaError_t e = smem_optin((const void *)k_block_apply_f64g3, smem, 3 * NT, nullptr);
     if (e != cudaSuccess) return e;
     const int total = p.ntT + p.ntV;
