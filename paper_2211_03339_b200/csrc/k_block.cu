@@ -363,7 +363,7 @@ __device__ __forceinline__ void apply_x3_body(const ApplyArgs &p, unsigned char 
                 pbase += __shfl_sync(0xffffffffu, x, 31);
                 base += __popc(bal);
             }
-            if (lane == 0) { sP[mb] = pbase; s_ctr[7] = base; }
+            if (lane == 0) { sP[mb] = p.ntT ? pbase : 0; s_ctr[7] = base; }   // column-only launches: no T tiles
         }
         ::__syncthreads();
         nTc = sP[mb];
@@ -1427,20 +1427,21 @@ mpj_status block_sweep(R *T, int64_t ldt, R *V, int64_t ldv, int vrows, const De
 // uid / nid (optional): identity flags and count of this block round (skip).
 template <typename R>
 cudaError_t launch_block_apply_cols(R *M, int64_t ld, int rows, const DevSched &ds, int Rb, const R *Ubuf,
-                             cudaStream_t st, const int *uid, const int *nid)
+                             cudaStream_t st, const int *uid, const int *nid, int *ctr)
 {
     Sched S;
     S.bsched = ds.bsched; S.lsched = ds.lsched; S.b = ds.b; S.nb = ds.nb; S.np = ds.np;
     ApplyArgs ap{};
     ap.T = nullptr; ap.ldt = 0; ap.M = M; ap.ldm = ld; ap.mrows = rows; ap.S = S; ap.Rb = Rb; ap.Ubuf = Ubuf; ap.uid = uid; ap.nid = nid;
+    ap.ctr = ctr;                                // zeroed item counter (nullptr: per-SM item lists)
     ap.ntT = 0;
     ap.ntV = ((rows + TW - 1) / TW) * (ds.nb / 2);
     return launch_apply<R>(ap, st);
 }
 template cudaError_t launch_block_apply_cols<double>(double *, int64_t, int, const DevSched &, int, const double *,
-                                              cudaStream_t, const int *, const int *);
+                                              cudaStream_t, const int *, const int *, int *);
 template cudaError_t launch_block_apply_cols<float>(float *, int64_t, int, const DevSched &, int, const float *,
-                                             cudaStream_t, const int *, const int *);
+                                             cudaStream_t, const int *, const int *, int *);
 
 template size_t block_scratch_bytes<double>(int, int);
 template size_t block_scratch_bytes<float>(int, int);

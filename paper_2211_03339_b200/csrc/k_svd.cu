@@ -432,6 +432,7 @@ struct SvdPlan {
     void *Ubuf;
     unsigned long long *cnt;
     int *uid;                 // mb identity flags + (nb - 1) per-round identity counts
+    int *ctr;                 // 2 (nb - 1) item counters of the column updates (single-GPU sweeps)
     int *rank, *flag;
     int *ex;                  // per-column exponents of the exact Gram (k_colexp)
     void *orth_ws;
@@ -489,6 +490,7 @@ static void carve_svd(char *base, size_t &off, int64_t m, int64_t n, SvdPlan &p)
     p.lsched = (int2 *)take((size_t)(BW - 1) * (BW / 2) * sizeof(int2));
     p.cnt = (unsigned long long *)take(64);
     p.uid = (int *)take((size_t)(p.mb + std::max(nb - 1, 1)) * sizeof(int));
+    p.ctr = (int *)take((size_t)2 * std::max(nb - 1, 1) * sizeof(int));
     p.rank = (int *)take(p.np * 4);
     p.flag = (int *)take(64);
     p.ex = (int *)take(p.np * 4);
@@ -500,7 +502,7 @@ static void carve_svd(char *base, size_t &off, int64_t m, int64_t n, SvdPlan &p)
 // uid / nid: identity flags (ds.nb / 2) and this round's identity count.
 template <typename R>
 static mpj_status svd_block_round(SvdPlan &p, R *C, R *V, const DevSched &ds, int Rb, R nu, cudaStream_t st,
-                                  bool exact, int *uid, int *nid)
+                                  bool exact, int *uid, int *nid, int *ctr2 = nullptr)
 {
     exact = exact && sizeof(R) == 8;
     Sched S;
@@ -539,8 +541,9 @@ static mpj_status svd_block_round(SvdPlan &p, R *C, R *V, const DevSched &ds, in
         count_launch(2);
     }
     if (prof) { prof_mark(ns, st, false); prof_mark(na, st, true); }
-    MPJ_CK(launch_block_apply_cols<R>(C, p.ldc, (int)p.m, ds, Rb, (const R *)p.Ubuf, st, uid, nid));
-    MPJ_CK(launch_block_apply_cols<R>(V, p.np, p.np, ds, Rb, (const R *)p.Ubuf, st, uid, nid));
+    MPJ_CK(launch_block_apply_cols<R>(C, p.ldc, (int)p.m, ds, Rb, (const R *)p.Ubuf, st, uid, nid, ctr2));
+    MPJ_CK(launch_block_apply_cols<R>(V, p.np, p.np, ds, Rb, (const R *)p.Ubuf, st, uid, nid,
+                                      ctr2 ? ctr2 + 1 : nullptr));
     if (prof) prof_mark(na, st, false);
     return MPJ_OK;
 }
@@ -550,7 +553,9 @@ static mpj_status svd_block_sweep(SvdPlan &p, R *C, R *V, const DevSched &ds, R 
 {
     int *uid = p.uid, *nid = p.uid + p.mb;
     MPJ_CK(cudaMemsetAsync(nid, 0, (size_t)(ds.nb - 1) * sizeof(int), st));
-    for (int Rb = 0; Rb < ds.nb - 1; ++Rb) MPJ_TRY(svd_block_round<R>(p, C, V, ds, Rb, nu, st, exact, uid, nid + Rb));
+    MPJ_CK(cudaMemsetAsync(p.ctr, 0, (size_t)2 * (ds.nb - 1) * sizeof(int), st));
+    for (int Rb = 0; Rb < ds.nb - 1; ++Rb)
+        MPJ_TRY(svd_block_round<R>(p, C, V, ds, Rb, nu, st, exact, uid, nid + Rb, p.ctr + 2 * Rb));
     return MPJ_OK;
 }
 

@@ -85,7 +85,7 @@ void launch_round_apply_v(R *V, int64_t ldv, int vrows, const int2 *pq, const R 
 // ---- block variant pieces (k_block.cu) ---------------------------------------
 template <typename R>
 cudaError_t launch_block_apply_cols(R *M, int64_t ld, int rows, const DevSched &ds, int Rb, const R *Ubuf,
-                             cudaStream_t st, const int *uid = nullptr, const int *nid = nullptr);
+                             cudaStream_t st, const int *uid = nullptr, const int *nid = nullptr, int *ctr = nullptr);
 
 // ---- utilities (k_util.cu) --------------------------------------------------
 // out[0] = sqrt(sum_{i != j} T_ij^2) (offdiag) or sqrt(sum T_ij^2) over an m x n
