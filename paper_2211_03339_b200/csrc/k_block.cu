@@ -60,8 +60,47 @@ __global__ void __launch_bounds__(NTW) k_block_solve(R *__restrict__ T, int64_t 
         U[li + lj * LD] = (li == lj) ? R(1) : R(0);
     }
     __syncthreads();
-    // FASTP: the parameter warp's divide / square-root chain with MUFU seeds + Newton (reading R28)
-    const R *D = inner_rounds_wide<R, FASTP>(D0, D1, U, bp, Rb == 0, S.lsched, nu, rule, P, &nrot, max_inner);
+    // Block rounds in which no pair the inner rounds visit passes the rotation
+    // test (at n = 8192, 521 of the 1275 block rounds of one EVD): every round
+    // then only sets the visited a_pq to 0 (the skip branch) and U stays
+    // I, so that is done directly -- the same T and U (up to the sign of a
+    // zero) without the 32 / 63 dependent rounds.  Decided from the block as
+    // loaded: with no rotation nothing else changes between rounds.
+    __shared__ int any_rot;
+    if (threadIdx.x == 0) any_rot = 0;
+    __syncthreads();
+    const bool all_pairs = Rb == 0 || max_inner > 0;       // intra-block rounds too
+    const int npairs = all_pairs ? TW * (TW - 1) / 2 : BW * BW;
+    auto pair_of_e = [&](int e, int &p, int &q) {
+        if (all_pairs) {
+            q = (int)((1.0f + sqrtf(1.0f + 8.0f * (float)e)) * 0.5f);
+            while (q * (q - 1) / 2 > e) --q;
+            while ((q + 1) * q / 2 <= e) ++q;
+            p = e - q * (q - 1) / 2;
+        } else {
+            p = e & (BW - 1); q = BW + (e >> 5);
+        }
+    };
+    for (int e = threadIdx.x; e < npairs; e += NTW) {
+        int p, q;
+        pair_of_e(e, p, q);
+        if (!rot_skip<R>(D0[p + p * LD], D0[q + q * LD], D0[p + q * LD], nu, rule)) any_rot = 1;
+    }
+    __syncthreads();
+    const R *D = D0;
+    if (any_rot) {
+        // FASTP: the parameter warp's divide / square-root chain with MUFU seeds + Newton (reading R28)
+        D = inner_rounds_wide<R, FASTP>(D0, D1, U, bp, Rb == 0, S.lsched, nu, rule, P, &nrot, max_inner);
+    } else {
+        for (int e = threadIdx.x; e < npairs; e += NTW) {
+            int p, q;
+            pair_of_e(e, p, q);
+            D0[p + q * LD] = R(0);
+            D0[q + p * LD] = R(0);
+        }
+        if (threadIdx.x == 0) nrot = 0;
+        __syncthreads();
+    }
     R *Uk = Ubuf + (size_t)k * TW * TW;
     R *UkT = Ubuf + (size_t)mb * TW * TW + (size_t)k * TW * TW;   // U^T (fp32 apply operand)
     R *UkS = Ubuf + 2 * (size_t)mb * TW * TW + (size_t)k * TW * TW;   // U^T, split-half layout
@@ -1401,14 +1440,17 @@ mpj_status block_sweep(R *T, int64_t ldt, R *V, int64_t ldv, int vrows, const De
         MPJ_CK(cudaMemcpyAsync(h.data(), nid, h.size() * sizeof(int), cudaMemcpyDeviceToHost, st));
         MPJ_CK(cudaStreamSynchronize(st));
         long long ids = 0, skt = 0, skv = 0, half = 0;
+        long long allid = 0;
         for (int c : h) {
             ids += c;
+            allid += c == mb;
             skt += (long long)c * (c - 1) / 2;
             skv += (long long)c * ((vrows + TW - 1) / TW);
             if (sizeof(R) == 8 || fp32_apply_kind() == 2) half += (long long)c * (mb - c);   // one product
         }
         const std::string base(napply);
         prof_add(base + ".identity_blocks", ids);
+        prof_add(base + ".all_identity_rounds", allid);   // block rounds in which no block pair rotated
         prof_add(base + ".items", (long long)(ds.nb - 1) * (ap.ntT + ap.ntV));
         prof_add(base + ".skipped_t", skt);
         prof_add(base + ".skipped_v", skv);

@@ -37,6 +37,18 @@ __device__ __forceinline__ float absR(float a) { return fabsf(a); }
 __device__ __forceinline__ double minR(double a, double b) { return fmin(a, b); }
 __device__ __forceinline__ float minR(float a, float b) { return fminf(a, b); }
 
+// The threshold decision alone: 1 if the pair is skipped (rot_params and
+// rot_params_fast take exactly this decision).
+template <typename R>
+__device__ __forceinline__ bool rot_skip(R app, R aqq, R apq, R nu, int rule)
+{
+    if (rule == 1) {
+        R g = app * aqq;
+        return (g > R(0)) ? (absR(apq) <= nu * sqrtR(g)) : (apq == R(0));
+    }
+    return absR(apq) <= nu * minR(absR(app), absR(aqq));
+}
+
 // Rotation parameters of Lemma 3.1 plus the threshold decision.
 // Returns 1 if the pair rotates; on skip t = s = tau = 0 (identity update).
 template <typename R>
@@ -48,13 +60,7 @@ __device__ __forceinline__ int rot_params(R app, R aqq, R apq, R nu, int rule, R
     // (so mu = -0 takes the + branch like the literal code), and for |mu| >=
     // 2^26 (2^12 fp32) 0.5/mu == sgn * (1/(2|mu|)) (2|mu| is exact and both
     // are the correctly rounded 1/(2 mu)).
-    bool skip;
-    if (rule == 1) {
-        R g = app * aqq;
-        skip = (g > R(0)) ? (absR(apq) <= nu * sqrtR(g)) : (apq == R(0));
-    } else {
-        skip = absR(apq) <= nu * minR(absR(app), absR(aqq));
-    }
+    const bool skip = rot_skip<R>(app, aqq, apq, nu, rule);
     const R den = skip ? R(1) : R(2) * apq;
     const R mu = divR(aqq - app, den);
     const R amu = absR(mu);
@@ -101,13 +107,7 @@ __device__ __forceinline__ float rsqrt_fast(float z) { return 1.0f / __fsqrt_rn(
 template <typename R>
 __device__ __forceinline__ int rot_params_fast(R app, R aqq, R apq, R nu, int rule, R &t, R &s, R &tau)
 {
-    bool skip;
-    if (rule == 1) {
-        R g = app * aqq;
-        skip = (g > R(0)) ? (absR(apq) <= nu * sqrtR(g)) : (apq == R(0));
-    } else {
-        skip = absR(apq) <= nu * minR(absR(app), absR(aqq));
-    }
+    const bool skip = rot_skip<R>(app, aqq, apq, nu, rule);
     const R den = skip ? R(1) : R(2) * apq;
     const R mu = (aqq - app) * rcp_fast(den);
     const R amu = absR(mu);
