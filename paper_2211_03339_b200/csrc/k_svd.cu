@@ -331,7 +331,31 @@ __global__ void __launch_bounds__(NTW) k_svd_solve(const double *__restrict__ Gp
         if (EXACT && li == lj) gnorm[li] = sqrt(fmax(g, 0.0));
     }
     __syncthreads();
-    inner_rounds_wide<R>(D0, D1, U, bp, Rb == 0, S.lsched, nu, /*rule=*/1, P, &nrot);
+    // no visited pair passes the test on the block as loaded: nothing rotates in
+    // any round (k_block.cu, reading R29), U = I -- skip the dependent rounds
+    // (the Gram block itself is discarded)
+    __shared__ int any_rot;
+    if (threadIdx.x == 0) any_rot = 0;
+    __syncthreads();
+    const int npairs = Rb == 0 ? TW * (TW - 1) / 2 : BW * BW;
+    for (int e = threadIdx.x; e < npairs; e += NTW) {
+        int p, q;
+        if (Rb == 0) {
+            q = (int)((1.0f + sqrtf(1.0f + 8.0f * (float)e)) * 0.5f);
+            while (q * (q - 1) / 2 > e) --q;
+            while ((q + 1) * q / 2 <= e) ++q;
+            p = e - q * (q - 1) / 2;
+        } else {
+            p = e & (BW - 1); q = BW + (e >> 5);
+        }
+        if (!rot_skip<R>(D0[p + p * LD], D0[q + q * LD], D0[p + q * LD], nu, /*rule=*/1)) any_rot = 1;
+    }
+    __syncthreads();
+    if (any_rot) {
+        inner_rounds_wide<R>(D0, D1, U, bp, Rb == 0, S.lsched, nu, /*rule=*/1, P, &nrot);
+    } else if (threadIdx.x == 0) {
+        nrot = 0;
+    }
     if constexpr (EXACT) {
         // exponents for the next round's k_gram_exact (replaces a k_colexp pass over C):
         // max_i |c'_ij| <= ||c'_j|| <= sum_k |U_kj| ||c_k|| for c'_j = C(:, P_a) U(:, j);
