@@ -172,8 +172,8 @@ def oracle_sample(n, mode, kappa, seed, sweeps64, sweeps32, sweeps_src):
       est = (t64 * S64 + t32 * S32) * (n_p - 1) + t_mgs + t_qtaq
 
     t64 / t32: one fp64 / fp32 Jacobi round (one O(n^2) pass over T and V),
-    timed as t(2 rounds) - t(1 round) so the call's fixed cost cancels (the
-    median of three such differences); t_mgs:
+    timed as (t(4 rounds) - t(1 round)) / 3 so the call's fixed cost cancels
+    (the median of three such samples); t_mgs:
     the oracle's MGS (left-looking, m = n rows) of the first k = n/16 columns
     scaled by the exact operation-count ratio (n/k)^2; t_qtaq: the oracle GEMM
     A (n x n) * Q(:, 1:c) with c = 2 x threads columns, scaled by 2 n / c (W =
@@ -217,18 +217,23 @@ def oracle_sample(n, mode, kappa, seed, sweeps64, sweeps32, sweeps_src):
                               nu=20 * UPSILON)
         return time.perf_counter() - t0
 
-    # one round = t(2 rounds) - t(1 round), the median of three such differences per precision
-    per_round = {prec: max(statistics.median(timed(prec, 2) - timed(prec, 1) for _ in range(3)), 1e-9)
-                 for prec in ("f64", "f32")}
+    # one round = (t(4 rounds) - t(1 round)) / 3 (the call's fixed cost cancels), the
+    # median of three such samples per precision (single-round differences varied
+    # by up to 50% between processes on the same host)
+    samples = {prec: [(timed(prec, 4) - timed(prec, 1)) / 3 for _ in range(3)] for prec in ("f64", "f32")}
+    per_round = {prec: max(statistics.median(v), 1e-9) for prec, v in samples.items()}
     # step 1 by symmetric QR (the default, reading R12'): the oracle's binary32
     # reduction + dense implicit QR, O(n^3) and single-threaded -- timed once at
     # n_s and scaled by (n / n_s)^3
     if "symqr" not in _ORACLE_CACHE:
         ns = min(n, 384)
         As, _ = W.example1(ns, kappa, mode, seed)
-        t0 = time.perf_counter()
-        oracle.low_evd_symqr(As)
-        _ORACLE_CACHE["symqr"] = ((time.perf_counter() - t0) * (n / ns) ** 3, ns)
+        ts = []
+        for _ in range(3):                              # median of three runs
+            t0 = time.perf_counter()
+            oracle.low_evd_symqr(As)
+            ts.append(time.perf_counter() - t0)
+        _ORACLE_CACHE["symqr"] = (statistics.median(ts) * (n / ns) ** 3, ns)
     t_symqr, ns_symqr = _ORACLE_CACHE["symqr"]
     rps = oracle.padded_n(n, b) - 1
     t_f64 = per_round["f64"] * rps * sweeps64
@@ -244,8 +249,9 @@ def oracle_sample(n, mode, kappa, seed, sweeps64, sweeps32, sweeps_src):
                         f"symmetric QR (timed at n_s={ns_symqr}, x (n/n_s)^3)",
                         "mgs": t_mgs, "qtaq": t_qtaq, "fp64_sweeps": t_f64},
         "t64_round_s": per_round["f64"], "t32_round_s": per_round["f32"], "S64": sweeps64, "S32": sweeps32,
+        "t64_round_samples_s": samples["f64"], "t32_round_samples_s": samples["f32"],
         "sample_wall_s": time.perf_counter() - t_start,
-        "sample": (f"oracle/mpj_oracle.c at the full n={n}: fp64 and fp32 Jacobi rounds (median of 3) per step "
+        "sample": (f"oracle/mpj_oracle.c at the full n={n}: fp64 and fp32 Jacobi rounds ((t4 - t1)/3, median of 3) per step "
                    f"(x {rps} rounds/sweep x S64={sweeps64}, S32={sweeps32} sweeps: {sweeps_src}); MGS of "
                    f"{k} of the n columns and the GEMM A*Q(:,1:{c}) once, scaled by their exact operation "
                    f"counts"),
