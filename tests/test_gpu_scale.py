@@ -136,6 +136,53 @@ def test_block_rounds_fp32_n8192(mpj, orc):
     assert np.linalg.norm(Vg - Vo) <= 512 * UPSILON * np.sqrt(n), np.linalg.norm(Vg - Vo) / (UPSILON * np.sqrt(n))
 
 
+def _t0_identity_blocks(n, seed, every=5):
+    """A near-diagonal T0 whose rotating entries sit only in the rows / columns
+    of every `every`-th b-block (b = 32); all other off-diagonal entries are
+    nonzero but far below the threshold nu min(|t_pp|, |t_qq|), so in
+    each block round many block pairs rotate nothing (identity U: skipped or
+    one-product tiles in K4, the no-rotation pass of K3, reading R29), and
+    their visited entries must still be set to 0 as the skip branch does."""
+    rng = np.random.default_rng(seed)
+    lam = W.spectrum_ex1(n, 1e3, 4)
+    rng.shuffle(lam)
+    E = rng.standard_normal((n, n))
+    E = (E + E.T) * 0.5
+    act = np.zeros(n, dtype=bool)
+    for blk in range(0, n // 32, every):
+        act[blk * 32:(blk + 1) * 32] = True
+    big = act[:, None] | act[None, :]
+    scale = np.abs(lam).max()
+    T = np.where(big, 1e-6 * scale * E, 1e-22 * scale * E)
+    T[np.diag_indices(n)] = lam
+    return np.asfortranarray(T)
+
+
+def test_block_rounds_identity_blocks_n4096(mpj, orc):
+    """Block rounds with identity rotation blocks at a size (mb = 64 block
+    pairs) where K4's compact non-identity item list spans several warp
+    chunks: the first two block rounds and a full block sweep against the
+    oracle's scalar rounds, element by element."""
+    n = 4096
+    T0 = _t0_identity_blocks(n, 97)
+    V0 = np.asfortranarray(np.random.default_rng(98).standard_normal((n, n)) / np.sqrt(n))
+    nA = np.linalg.norm(T0)
+    cfg = mpj.default_config("eig", variant=mpj.VARIANT_BLOCK, block_b=32)
+    for rounds in (ROUNDS_2BR, (2 * 32 - 1) + 32 * (n // 32 - 2)):
+        ref = orc.jacobi_evd(T0, V0, b=32, tol=0.0, max_sweeps=1, max_rounds=rounds)
+        T, V = dev(T0), dev(V0)
+        r = mpj.jacobi(T, V, tol=0.0, max_sweeps=1, max_rounds=rounds, cfg=cfg)
+        assert r.rotations == ref.rotations, (rounds, r.rotations, ref.rotations)
+        if rounds == ROUNDS_2BR:       # later rounds mix the rotating entries into every row
+            assert 0 < r.rotations < 0.6 * (n // 2) * rounds   # many pairs skipped
+        Tg, Vg = host(T), host(V)
+        assert np.array_equal(Tg, Tg.T)
+        # the skipped pairs' entries are exactly 0 on both sides, the rest agree to rounding
+        assert np.array_equal(Tg == 0, ref.T == 0)
+        assert np.abs(Tg - ref.T).max() <= 64 * n * OMEGA * nA, np.abs(Tg - ref.T).max()
+        assert np.abs(Vg - ref.V).max() <= 64 * n * OMEGA * np.abs(V0).max(), np.abs(Vg - ref.V).max()
+
+
 def test_block_rounds_boundary_enforced(mpj):
     """max_rounds must end on a block-round boundary in the block variant."""
     n = 256
