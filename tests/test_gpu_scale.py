@@ -183,6 +183,28 @@ def test_block_rounds_identity_blocks_n4096(mpj, orc):
         assert np.abs(Vg - ref.V).max() <= 64 * n * OMEGA * np.abs(V0).max(), np.abs(Vg - ref.V).max()
 
 
+def test_block_rounds_no_rotation(mpj, orc):
+    """Every block round rotates nothing (all off-diagonal entries below the
+    threshold): K3's no-rotation pass (reading R29) for every block pair and
+    K4 with an empty item list.  The visited entries become exactly 0 and V is
+    unchanged, exactly as the oracle's skip branch leaves them."""
+    n = 1024
+    rng = np.random.default_rng(99)
+    lam = W.spectrum_ex1(n, 1e3, 4)
+    E = rng.standard_normal((n, n))
+    T0 = np.asfortranarray((E + E.T) * (1e-22 * np.abs(lam).max()))
+    T0[np.diag_indices(n)] = lam
+    V0 = np.asfortranarray(rng.standard_normal((n, n)) / np.sqrt(n))
+    cfg = mpj.default_config("eig", variant=mpj.VARIANT_BLOCK, block_b=32)
+    for rounds in (ROUNDS_2BR, n - 1):
+        ref = orc.jacobi_evd(T0, V0, b=32, tol=0.0, max_sweeps=1, max_rounds=rounds)
+        T, V = dev(T0), dev(V0)
+        r = mpj.jacobi(T, V, tol=0.0, max_sweeps=1, max_rounds=rounds, cfg=cfg)
+        assert r.rotations == ref.rotations == 0
+        assert np.array_equal(host(T), ref.T)
+        assert np.array_equal(host(V), V0)
+
+
 def test_block_rounds_boundary_enforced(mpj):
     """max_rounds must end on a block-round boundary in the block variant."""
     n = 256
