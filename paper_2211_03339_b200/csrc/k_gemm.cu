@@ -133,6 +133,7 @@ __global__ void __launch_bounds__(128) k_dgemm(int64_t m, int64_t n, int64_t k, 
                                                double *__restrict__ partial, int upper_only,
                                                const int *__restrict__ skip)
 {
+    asm volatile("griddepcontrol.wait;\n" ::: "memory");   // launched early (PDL): wait for the producer
     if (skip && *skip) return;                       // a conditional product (device-side decision)
     if (upper_only && (int64_t)blockIdx.x * BM >= ((int64_t)blockIdx.y + 1) * BN) return;   // strictly lower tile
     __shared__ __align__(16) double sA[2][TILE];
@@ -223,6 +224,7 @@ __global__ void k_splitk_reduce(int64_t m, int64_t n, int splits, const double *
                                 double alpha, double beta, double *__restrict__ C, int64_t ldc,
                                 const int *__restrict__ skip)
 {
+    asm volatile("griddepcontrol.wait;\n" ::: "memory");   // launched early (PDL)
     if (skip && *skip) return;
     const int64_t total = m * n;
     for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total;
@@ -234,6 +236,25 @@ __global__ void k_splitk_reduce(int64_t m, int64_t n, int splits, const double *
         if (beta != 0.0) v = __fma_rn(beta, C[i + j * ldc], v);
         C[i + j * ldc] = v;
     }
+}
+
+// launch with programmatic stream serialisation: the kernel may be scheduled
+// while its predecessor drains (the chains of small products in CGS and the
+// back-transformation); it waits (griddepcontrol.wait) before touching data
+template <typename... KA, typename... A>
+static void launch_pdl_g(void (*k)(KA...), dim3 grid, dim3 block, cudaStream_t st, A... args)
+{
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = 0;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cudaLaunchKernelEx(&cfg, k, args...);
 }
 
 }  // namespace
@@ -261,8 +282,8 @@ void launch_dgemm(bool ta, bool tb, int64_t m, int64_t n, int64_t k, double alph
     double *part = splits > 1 ? scratch : nullptr;
     // 16-byte operand copies when every column start is 16-byte aligned
     const bool v16 = lda % 2 == 0 && ldb % 2 == 0 && ((uintptr_t)A & 15) == 0 && ((uintptr_t)B & 15) == 0;
-#define GO(a, b, v) k_dgemm<a, b, v><<<grd, 128, 0, st>>>(m, n, k, alpha, A, lda, B, ldb, beta, C, ldc, kchunk, \
-                                                         part, upper_only ? 1 : 0, skip)
+#define GO(a, b, v) launch_pdl_g(k_dgemm<a, b, v>, grd, dim3(128), st, m, n, k, alpha, A, lda, B, ldb, beta, C, ldc, \
+                                 kchunk, part, upper_only ? 1 : 0, skip)
 #define GO2(a, b) do { if (v16) GO(a, b, true); else GO(a, b, false); } while (0)
     if (!ta && !tb) GO2(false, false);
     else if (ta && !tb) GO2(true, false);
@@ -272,7 +293,8 @@ void launch_dgemm(bool ta, bool tb, int64_t m, int64_t n, int64_t k, double alph
 #undef GO
     count_launch();
     if (splits > 1) {
-        k_splitk_reduce<<<592, 256, 0, st>>>(m, n, splits, part, alpha, beta, C, ldc, skip);
+        launch_pdl_g(k_splitk_reduce, dim3(592), dim3(256), st, m, n, splits, (const double *)part, alpha, beta, C,
+                     ldc, skip);
         count_launch();
     }
 }
