@@ -39,6 +39,7 @@ __global__ void __launch_bounds__(256) k_chol(const double *__restrict__ G, int 
                                               int *__restrict__ reorth, int *__restrict__ single,
                                               const int *__restrict__ skip)
 {
+    asm volatile("griddepcontrol.wait;\n" ::: "memory");   // launched early (PDL)
     __shared__ double A[kPanel * kLDG];
     __shared__ int far_from_I;
     if (skip && *skip) return;
@@ -84,6 +85,7 @@ __global__ void __launch_bounds__(256) k_chol(const double *__restrict__ G, int 
 __global__ void k_copy_panel_if(const double *__restrict__ S, int64_t lds, int64_t m, double *__restrict__ X,
                                 int64_t ldx, const int *__restrict__ run)
 {
+    asm volatile("griddepcontrol.wait;\n" ::: "memory");   // launched early (PDL)
     if (!*run) return;
     const int j = blockIdx.y;
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x)
@@ -93,6 +95,7 @@ __global__ void k_copy_panel_if(const double *__restrict__ S, int64_t lds, int64
 // pre[j] = ||X(:, j)||^2 for the w columns of a panel (one CTA per column)
 __global__ void k_colnorm2(const double *__restrict__ X, int64_t ldx, int64_t m, double *__restrict__ pre)
 {
+    asm volatile("griddepcontrol.wait;\n" ::: "memory");   // launched early (PDL)
     __shared__ double red[256 / 32];
     const double *x = X + (size_t)blockIdx.x * ldx;
     double acc = 0.0;
@@ -116,6 +119,7 @@ __global__ void __launch_bounds__(64) k_trsm_rows(const double *__restrict__ X, 
                                                   const double *__restrict__ Rf, double *__restrict__ Q, int64_t ldq,
                                                   const int *__restrict__ skip)
 {
+    asm volatile("griddepcontrol.wait;\n" ::: "memory");   // launched early (PDL)
     __shared__ double R[W * W];
     if (skip && *skip) return;
     for (int e = threadIdx.x; e < W * W; e += blockDim.x) R[e] = Rf[e];
@@ -140,6 +144,7 @@ __global__ void __launch_bounds__(64) k_trsm_rows_w(const double *__restrict__ X
                                                     const double *__restrict__ Rf, double *__restrict__ Q, int64_t ldq,
                                                     const int *__restrict__ skip)
 {
+    asm volatile("griddepcontrol.wait;\n" ::: "memory");   // launched early (PDL)
     __shared__ double R[kPanel * kPanel];
     if (skip && *skip) return;
     for (int e = threadIdx.x; e < w * w; e += blockDim.x) R[e] = Rf[e];
@@ -190,7 +195,7 @@ static mpj_status orth_sweep(const double *Z, int64_t ldz, double *Q, int64_t ld
         double *X = Q + p0 * ldq;
         const bool check = passes == 1 && p0 > 0;
         if (check) {
-            k_colnorm2<<<w, 256, 0, st>>>(X, ldq, m, pre);
+            launch_pdl_k(k_colnorm2, dim3(w), dim3(256), 0, st, (const double *)X, ldq, m, pre);
             count_launch();
         }
         if (p0 > 0) {
@@ -211,14 +216,19 @@ static mpj_status orth_sweep(const double *Z, int64_t ldz, double *Q, int64_t ld
             const int *skip = rep == 1 ? single : nullptr;
             launch_dgemm(true, false, w, w, m, 1.0, src, lds, src, lds, 0.0, G, w, st, scratch, scratch_elems, false,
                          skip);
-            k_chol<<<1, 256, 0, st>>>(G, w, Rf, fail, (check && rep == 0) ? pre : nullptr, reorth,
-                                      rep == 0 ? single : nullptr, skip);
-            if (w == kPanel) k_trsm_rows<kPanel><<<nblk, 64, 0, st>>>(src, lds, m, Rf, dst, ldd, skip);
-            else k_trsm_rows_w<<<nblk, 64, 0, st>>>(src, lds, m, w, Rf, dst, ldd, skip);
+            launch_pdl_k(k_chol, dim3(1), dim3(256), 0, st, (const double *)G, w, Rf, fail,
+                         (const double *)((check && rep == 0) ? pre : nullptr), reorth, rep == 0 ? single : nullptr,
+                         skip);
+            if (w == kPanel)
+                launch_pdl_k(k_trsm_rows<kPanel>, dim3(nblk), dim3(64), 0, st, src, lds, m, (const double *)Rf, dst, ldd,
+                             skip);
+            else
+                launch_pdl_k(k_trsm_rows_w, dim3(nblk), dim3(64), 0, st, src, lds, m, w, (const double *)Rf, dst, ldd,
+                             skip);
             count_launch(2);
         }
-        k_copy_panel_if<<<dim3((unsigned)std::min<int64_t>(64, (m + 255) / 256), w), 256, 0, st>>>(S, m, m, X, ldq,
-                                                                                                    single);
+        launch_pdl_k(k_copy_panel_if, dim3((unsigned)std::min<int64_t>(64, (m + 255) / 256), w), dim3(256), 0, st,
+                     (const double *)S, m, m, X, ldq, (const int *)single);
         count_launch();
     }
     int h[2] = {0, 0};

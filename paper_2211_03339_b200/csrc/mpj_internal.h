@@ -9,6 +9,25 @@
 
 namespace mpj {
 
+// launch with programmatic stream serialisation (PDL): the kernel may be
+// scheduled while its predecessor drains; it must execute griddepcontrol.wait
+// before touching data the predecessor writes
+template <typename... KA, typename... A>
+inline cudaError_t launch_pdl_k(void (*k)(KA...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, A... args)
+{
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, k, args...);
+}
+
 struct Sched;
 
 // ---- error / launch bookkeeping --------------------------------------------
