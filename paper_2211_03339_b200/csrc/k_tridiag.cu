@@ -1031,6 +1031,7 @@ __global__ void k_rank_lam(const double *__restrict__ lam, int n, int *rank)
 // = j - k0): 0 above row j+1, 1 at j+1, the stored v below; zero for t >= nr.
 __global__ void k_build_vp(const float *__restrict__ A, int64_t lda, int n, int k0, int nr, double *Vp, int64_t ldv)
 {
+    asm volatile("griddepcontrol.wait;\n" ::: "memory");   // launched early (PDL)
     const int t = blockIdx.y;
     const int r0 = k0 + 1;
     const int j = k0 + t;
@@ -1049,6 +1050,7 @@ constexpr int BT = 2 * TB;       // back-transformation block (two sytrd panels)
 __global__ void __launch_bounds__(1024) k_build_tp(const double *__restrict__ G, const float *__restrict__ tau, int k0,
                                                   int nr, double *Tp)
 {
+    asm volatile("griddepcontrol.wait;\n" ::: "memory");   // launched early (PDL)
     extern __shared__ double tsm[];          // T (BT x BT+1), z (BT), part (2 x BT), M (3 x 32 x 32)
     double *T = tsm, *z = T + BT * (BT + 1), *part = z + BT;
     const int tid = threadIdx.x, row = tid & (BT - 1), grp = tid >> 7;   // fallback: 2 groups x 128 rows
@@ -1733,13 +1735,13 @@ static mpj_status backtransform_run(const float *A32, int64_t lda, int n, SymqrW
     for (int k0 = ((ncolumns - 1) / BT) * BT; ncolumns > 0 && k0 >= 0; k0 -= BT) {
         const int nr = std::min(BT, ncolumns - k0);
         const int r0 = k0 + 1, m = n - r0;
-        k_build_vp<<<dim3((m + 255) / 256 > 32 ? 32 : (m + 255) / 256, BT), 256, 0, st>>>(A32, lda, n, k0, nr, w.Vp,
-                                                                                          np);
+        launch_pdl_k(k_build_vp, dim3((m + 255) / 256 > 32 ? 32 : (m + 255) / 256, BT), dim3(256), 0, st, A32, lda, n, k0,
+                     nr, w.Vp, np);
         count_launch();
         launch_dgemm(true, false, BT, BT, m, 1.0, w.Vp, np, w.Vp, np, 0.0, w.Gm, BT, st, w.skw, w.skw_elems);
         const size_t tsm = ((size_t)BT * (BT + 1) + 3 * BT + 3 * 32 * 32) * sizeof(double);
         MPJ_CK(smem_optin((const void *)k_build_tp, tsm, 1024, nullptr));
-        k_build_tp<<<1, 1024, tsm, st>>>(w.Gm, w.tau, k0, nr, w.Tp);
+        launch_pdl_k(k_build_tp, dim3(1), dim3(1024), tsm, st, (const double *)w.Gm, (const float *)w.tau, k0, nr, w.Tp);
         count_launch();
         // W1 = Vp^T Y: only 2 x n/64 output tiles with K = m -- split K 4 ways (n = 8192: 58.6 -> 56.3 ms
         // for the whole back-transformation; MPJ_BT_SPLITS overrides for A/B runs)
