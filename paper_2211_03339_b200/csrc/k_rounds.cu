@@ -36,6 +36,7 @@ __global__ void __launch_bounds__(256) k_round_params(const R *__restrict__ T, i
                                                       unsigned long long *__restrict__ cnt,
                                                       int *__restrict__ pos)
 {
+    asm volatile("griddepcontrol.wait;\n" ::: "memory");   // launched early (PDL)
     const int h = S.np >> 1;
     const int k = blockIdx.x * blockDim.x + threadIdx.x;
     int did = 0;
@@ -58,6 +59,7 @@ __global__ void __launch_bounds__(256) k_round_apply(R *__restrict__ T, int64_t 
                                                      const R *__restrict__ ss,
                                                      const R *__restrict__ uu, int h)
 {
+    asm volatile("griddepcontrol.wait;\n" ::: "memory");   // launched early (PDL)
     const int k = blockIdx.x * 32 + threadIdx.x;   // row pair (fast index -> coalesced)
     const int l = blockIdx.y * 8 + threadIdx.y;    // column pair
     if (k >= h || l >= h) return;
@@ -91,6 +93,7 @@ __global__ void __launch_bounds__(256) k_round_apply_v(R *__restrict__ V, int64_
                                                        const R *__restrict__ ss,
                                                        const R *__restrict__ uu)
 {
+    asm volatile("griddepcontrol.wait;\n" ::: "memory");   // launched early (PDL)
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     const int k = blockIdx.y;
     if (i >= vrows) return;
@@ -111,6 +114,7 @@ __global__ void __launch_bounds__(256) k_round_apply_fused(const R *__restrict__
                                                            const R *__restrict__ tt, const R *__restrict__ ss,
                                                            const R *__restrict__ uu)
 {
+    asm volatile("griddepcontrol.wait;\n" ::: "memory");   // launched early (PDL)
     const int i = blockIdx.x * blockDim.x + threadIdx.x;   // row
     const int l = blockIdx.y;                              // column pair
     const int2 c = pq[l];
@@ -159,7 +163,8 @@ void launch_round_params(const R *T, int64_t ldt, const DevSched &S, int r, R nu
                          int2 *pq, R *t, R *s, R *u, unsigned long long *cnt, cudaStream_t st, int *pos)
 {
     const int h = S.np / 2;
-    k_round_params<R><<<(h + 255) / 256, 256, 0, st>>>(T, ldt, to_sched(S), r, nu, rule, pq, t, s, u, cnt, pos);
+    launch_pdl_k(k_round_params<R>, dim3((h + 255) / 256), dim3(256), 0, st, T, ldt, to_sched(S), r, nu, rule, pq, t, s, u,
+                 cnt, pos);
     count_launch();
 }
 
@@ -169,7 +174,7 @@ void launch_round_apply_fused_oop(const R *T, R *Tout, int64_t ldt, R *V, int64_
 {
     const int rows = vrows > np ? vrows : np;
     dim3 grd((rows + 255) / 256, np / 2);
-    k_round_apply_fused<R><<<grd, 256, 0, st>>>(T, Tout, ldt, V, ldv, vrows, np, pq, pos, t, s, u);
+    launch_pdl_k(k_round_apply_fused<R>, grd, dim3(256), 0, st, T, Tout, ldt, V, ldv, vrows, np, pq, pos, t, s, u);
     count_launch();
 }
 
@@ -178,7 +183,7 @@ void launch_round_apply(R *T, int64_t ldt, const int2 *pq, const R *t, const R *
                         int h, cudaStream_t st)
 {
     dim3 blk(32, 8), grd((h + 31) / 32, (h + 7) / 8);
-    k_round_apply<R><<<grd, blk, 0, st>>>(T, ldt, pq, t, s, u, h);
+    launch_pdl_k(k_round_apply<R>, grd, blk, 0, st, T, ldt, pq, t, s, u, h);
     count_launch();
 }
 
@@ -187,7 +192,7 @@ void launch_round_apply_v(R *V, int64_t ldv, int vrows, const int2 *pq, const R 
                           int h, cudaStream_t st)
 {
     dim3 grd((vrows + 255) / 256, h);
-    k_round_apply_v<R><<<grd, 256, 0, st>>>(V, ldv, vrows, pq, s, u);
+    launch_pdl_k(k_round_apply_v<R>, grd, dim3(256), 0, st, V, ldv, vrows, pq, s, u);
     count_launch();
 }
 
