@@ -355,6 +355,29 @@ static bool scalar_fused()
     return v == 1;
 }
 
+// Instantiated graphs of one scalar-variant sweep, reused across calls with
+// the same buffers and parameters (instantiating one cost ~170 us + ~100 us
+// to destroy per call: a fifth of an n = 32 EVD).  Kernel arguments are
+// baked into a graph, so the key holds every pointer and scalar it captures.
+struct SweepGraphKey {
+    int dev, np, rule, rounds, fused, rsize;
+    double nu;
+    const void *ptr[11];
+    bool operator==(const SweepGraphKey &o) const
+    {
+        return dev == o.dev && np == o.np && rule == o.rule && rounds == o.rounds && fused == o.fused &&
+               rsize == o.rsize && std::memcmp(&nu, &o.nu, sizeof(nu)) == 0 &&
+               std::memcmp(ptr, o.ptr, sizeof(ptr)) == 0;
+    }
+};
+struct SweepGraph {
+    SweepGraphKey key;
+    cudaGraphExec_t exec;
+    long long kernels;
+};
+static std::mutex g_sweep_graph_mu;
+static std::vector<SweepGraph> g_sweep_graphs;   // most recent last; at most 16 kept
+
 struct JacobiOut {
     int sweeps = 0;
     long long rotations = 0;
@@ -449,15 +472,35 @@ static mpj_status jacobi_run(Ctx &cx, R *T, R *V, int n, int b, int variant, dou
             };
             if (use_graph) {
                 if (!gexec) {
-                    cudaGraph_t g;
-                    const long long l0 = g_launches;
-                    MPJ_CK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
-                    sweep_rounds(0, hs.rounds);
-                    MPJ_CK(cudaStreamEndCapture(st, &g));
-                    graph_kernels = g_launches - l0;
-                    g_launches = l0;
-                    MPJ_CK(cudaGraphInstantiate(&gexec, g, 0));
-                    cudaGraphDestroy(g);
+                    SweepGraphKey key;
+                    std::memset(&key, 0, sizeof(key));
+                    cudaGetDevice(&key.dev);
+                    key.np = np; key.rule = rule; key.rounds = hs.rounds; key.fused = fused ? 1 : 0;
+                    key.rsize = (int)sizeof(R); key.nu = (double)nu;
+                    const void *ptrs[11] = {T, V, jb.Tn, jb.pq, jb.pos, jb.t, jb.s, jb.u, jb.cnt, jb.bsched, jb.lsched};
+                    std::memcpy(key.ptr, ptrs, sizeof(ptrs));
+                    {
+                        std::lock_guard<std::mutex> lk(g_sweep_graph_mu);
+                        for (auto &e : g_sweep_graphs)
+                            if (e.key == key) { gexec = e.exec; graph_kernels = e.kernels; break; }
+                    }
+                    if (!gexec) {
+                        cudaGraph_t g;
+                        const long long l0 = g_launches;
+                        MPJ_CK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+                        sweep_rounds(0, hs.rounds);
+                        MPJ_CK(cudaStreamEndCapture(st, &g));
+                        graph_kernels = g_launches - l0;
+                        g_launches = l0;
+                        MPJ_CK(cudaGraphInstantiate(&gexec, g, 0));
+                        cudaGraphDestroy(g);
+                        std::lock_guard<std::mutex> lk(g_sweep_graph_mu);
+                        if (g_sweep_graphs.size() >= 16) {
+                            cudaGraphExecDestroy(g_sweep_graphs.front().exec);
+                            g_sweep_graphs.erase(g_sweep_graphs.begin());
+                        }
+                        g_sweep_graphs.push_back({key, gexec, graph_kernels});
+                    }
                 }
                 MPJ_CK(cudaGraphLaunch(gexec, st));
                 count_launch(graph_kernels);
@@ -470,8 +513,7 @@ static mpj_status jacobi_run(Ctx &cx, R *T, R *V, int n, int b, int variant, dou
             }
         }
     }
-    if (gexec) cudaGraphExecDestroy(gexec);
-    unsigned long long rot = 0;
+    unsigned long long rot = 0;             // (gexec stays in g_sweep_graphs for the next call)
     MPJ_CK(cudaMemcpyAsync(cx.h_pin, jb.cnt, sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
     MPJ_CK(cudaStreamSynchronize(st));
     std::memcpy(&rot, cx.h_pin, sizeof(rot));
