@@ -205,8 +205,9 @@ struct Arena {
 
 static int auto_b(int64_t n)
 {
-    // b = 32 (2b = 64 tiles) unless the matrix is small; keep b even.
-    if (n >= 64) return 32;
+    // b = 32 (2b = 64 tiles) from n = 32 up (n <= 64 is padded to one 64 x 64
+    // block pair: a sweep is one K3 + one K4 launch); smaller b only below
+    if (n >= 32) return 32;
     int b = (int)((n + 3) / 4) * 2;     // about n/2, even
     return std::max(1, std::min(32, b));
 }
@@ -220,7 +221,9 @@ static int resolve_b(int64_t n, const mpj_config *cfg)
 static int resolve_variant(int np, int b, const mpj_config *cfg)
 {
     int v = cfg ? cfg->variant : MPJ_VARIANT_AUTO;
-    if (v == MPJ_VARIANT_AUTO) v = (np >= 128 && b == 32) ? MPJ_VARIANT_BLOCK : MPJ_VARIANT_SCALAR;
+    // block variant whenever the b = 32 kernels apply: at n_p = 64 one block pair
+    // makes a sweep one K3 launch (all 63 rounds in shared memory) plus the V update
+    if (v == MPJ_VARIANT_AUTO) v = (np >= 64 && b == 32) ? MPJ_VARIANT_BLOCK : MPJ_VARIANT_SCALAR;
     if ((v == MPJ_VARIANT_BLOCK || v == MPJ_VARIANT_BLOCK_FULL) && b != 32) v = MPJ_VARIANT_SCALAR;   // b = 32 kernels
     return v;
 }
