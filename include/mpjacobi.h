@@ -57,7 +57,7 @@ typedef enum {
 
 /* Jacobi sweep implementation. */
 enum {
-    MPJ_VARIANT_AUTO = 0,   /* block for n_p >= 256, scalar rounds otherwise       */
+    MPJ_VARIANT_AUTO = 0,   /* block (b = 32) for n >= 32, scalar rounds below     */
     MPJ_VARIANT_SCALAR = 1, /* one launch pair per round, bit-exact with the oracle */
     MPJ_VARIANT_BLOCK = 2,  /* 2b x 2b block solves + fp64 tensor-core (DMMA) apply */
     MPJ_VARIANT_BLOCK_FULL = 3  /* classic block Jacobi (reading R26):
