@@ -101,6 +101,11 @@ template <typename R>
 void launch_round_apply_v(R *V, int64_t ldv, int vrows, const int2 *pq, const R *s, const R *u,
                           int h, cudaStream_t st);
 
+// ---- batched path (k_batched.cu): batch contiguous n x n matrices (n <= 64),
+// device pointers; sweeps / sweeps_low device arrays of `batch` ints ----------
+mpj_status batched_evd(const double *A, int64_t n, int64_t batch, double *Lambda, double *V, int *sweeps,
+                       int *sweeps_low, const float *Zin, float *Zout, cudaStream_t st, const mpj_config &cfg);
+
 // ---- block variant pieces (k_block.cu) ---------------------------------------
 template <typename R>
 cudaError_t launch_block_apply_cols(R *M, int64_t ld, int rows, const DevSched &ds, int Rb, const R *Ubuf,

@@ -628,6 +628,57 @@ static mpj_status eig_impl(bool mixed, const double *A, int64_t n, int64_t lda, 
     Timer t_all(cx.st);
     const long long l0 = g_launches;
 
+    // n <= 64 with the default configuration and device buffers: the
+    // single-CTA kernels of the batched path run the same Alg. 3 (symmetric-QR
+    // step 1, Cholesky-QR step 2, Q^T A Q, the fp64 sweeps of the one 64 x 64
+    // block pair) in one launch pair, where the general path needs ~50
+    // launches and a host round trip per sweep (n = 32: 0.40 vs 0.85 ms).
+    // MPJ_SMALL_BATCHED=0 turns it off.
+    static const bool small_batched = !(getenv("MPJ_SMALL_BATCHED") && getenv("MPJ_SMALL_BATCHED")[0] == '0');
+    if (mixed && small_batched && n <= 64 && !Zin && !Zout && cfg.variant == MPJ_VARIANT_AUTO &&
+        (cfg.low_solver == MPJ_LOW_SYMQR || cfg.low_solver == MPJ_LOW_AUTO)) {
+        // host buffers or leading dimensions other than n are staged (the same kernels either way)
+        const bool a_d = is_device_ptr(A) && lda == n, l_d = is_device_ptr(Lambda), v_d = is_device_ptr(V) && ldv == n;
+        double *stg = nullptr;
+        MPJ_CK(cudaMallocAsync(&stg, (size_t)(2 * n * n + n) * sizeof(double) + 2 * sizeof(int), cx.st));
+        double *Ad = a_d ? const_cast<double *>(A) : stg, *Vd = v_d ? V : stg + n * n, *Ld = l_d ? Lambda : stg + 2 * n * n;
+        int *dsw = (int *)(stg + 2 * n * n + n);
+        MPJ_CK(cudaMemsetAsync(dsw, 0, 2 * sizeof(int), cx.st));
+        mpj_status s = MPJ_OK;
+        if (!a_d)
+            s = copy2d(Ad, n, A, lda, n, n, sizeof(double),
+                       is_device_ptr(A) ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, cx.st);
+        if (s == MPJ_OK) s = batched_evd(Ad, n, 1, Ld, Vd, dsw, dsw + 1, nullptr, nullptr, cx.st, cfg);
+        if (s == MPJ_OK || s == MPJ_ERR_NOCONV) {   // NOCONV: the last iterate is written, as on the general path
+            mpj_status c2 = MPJ_OK;
+            if (!v_d)
+                c2 = copy2d(V, ldv, Vd, n, n, n, sizeof(double),
+                            is_device_ptr(V) ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, cx.st);
+            if (c2 == MPJ_OK && !l_d && cudaMemcpyAsync(Lambda, Ld, n * sizeof(double), cudaMemcpyDeviceToHost,
+                                                        cx.st) != cudaSuccess)
+                c2 = MPJ_ERR_CUDA;
+            if (c2 != MPJ_OK) s = c2;
+        }
+        int hsw[2] = {0, 0};
+        cudaMemcpyAsync(cx.h_pin, dsw, 2 * sizeof(int), cudaMemcpyDeviceToHost, cx.st);
+        cudaFreeAsync(stg, cx.st);
+        cudaStreamSynchronize(cx.st);
+        std::memcpy(hsw, cx.h_pin, sizeof(hsw));
+        mpj_report r;
+        std::memset(&r, 0, sizeof(r));
+        r.n_padded = 64;
+        r.block_b = 32;
+        r.variant = MPJ_VARIANT_BLOCK;
+        r.sweeps = hsw[0];
+        r.sweeps_low = hsw[1];
+        r.t_total = t_all.stop();
+        r.launches = g_launches - l0;
+        if (rep) *rep = r;
+        if (sweeps) *sweeps = hsw[0];
+        mpj_status c = cx.close();
+        return s != MPJ_OK ? s : c;
+    }
+
     Arena ar;
     EigPlan p;
     carve_eig(ar, n, &cfg, p);   // measure
