@@ -147,6 +147,12 @@ typedef struct mpj_report {
  *   rep     out: telemetry (may be NULL; host pointer).
  * Returns MPJ_OK, MPJ_ERR_NOCONV, MPJ_ERR_NONFINITE, MPJ_ERR_RANKDEF (MGS
  * breakdown), MPJ_ERR_INVALID, MPJ_ERR_NOMEM or MPJ_ERR_CUDA.
+ * n <= 64 with cfg->variant == MPJ_VARIANT_AUTO and the default step 1
+ * (MPJ_LOW_SYMQR) runs the same algorithm on the single-CTA kernels of
+ * mpjacobi_eig_batched (batch 1; the workspace is not used, a small staging
+ * buffer is allocated on `stream`); rep then carries sweeps, sweeps_low,
+ * variant, n_padded, block_b, launches and t_total only.  Environment
+ * MPJ_SMALL_BATCHED=0 selects the general path.
  * ---------------------------------------------------------------------- */
 size_t mpjacobi_eig_workspace(int64_t n, const mpj_config *cfg);
 mpj_status mpjacobi_eig(const double *A, int64_t n, int64_t lda, double *Lambda, double *V,
