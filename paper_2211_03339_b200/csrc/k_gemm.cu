@@ -272,7 +272,7 @@ void launch_dgemm(bool ta, bool tb, int64_t m, int64_t n, int64_t k, double alph
         splits = (int)std::min<int64_t>((296 + tiles - 1) / tiles, k / 256);
         while (splits > 1 && (size_t)splits * m * n > scratch_elems) --splits;
     }
-    if (min_splits > splits && scratch && k >= 256 * min_splits) {   // caller's hint (shapes it measured)
+    if (min_splits > splits && scratch && k >= 64 * min_splits) {    // caller's hint (shapes it measured)
         splits = min_splits;
         while (splits > 1 && (size_t)splits * m * n > scratch_elems) --splits;
     }

@@ -27,6 +27,7 @@ namespace mpj {
 namespace {
 constexpr int kPanel = 64;
 constexpr int kLDG = kPanel + 1;
+constexpr int kCholNT = 1024;   // threads of the panel Cholesky: 16 rows of the update per column
 
 // Cholesky G = R^T R of a w x w panel Gram matrix (w <= 64): R upper (ld w,
 // zero below the diagonal); fail = 1 on a non-positive pivot.  Right-looking;
@@ -34,7 +35,7 @@ constexpr int kLDG = kPanel + 1;
 // triangle, so a step is a few FMAs per thread and two barriers (k_chol_inv's
 // flat loop over all w^2 entries with an integer division per entry made it
 // issue-bound: 150 us per call, 1% of an n = 8192 EVD).
-__global__ void __launch_bounds__(256) k_chol(const double *__restrict__ G, int w, double *__restrict__ Rf,
+__global__ void __launch_bounds__(kCholNT) k_chol(const double *__restrict__ G, int w, double *__restrict__ Rf,
                                               int *__restrict__ fail, const double *__restrict__ pre,
                                               int *__restrict__ reorth, int *__restrict__ single,
                                               const int *__restrict__ skip)
@@ -43,7 +44,7 @@ __global__ void __launch_bounds__(256) k_chol(const double *__restrict__ G, int 
     __shared__ double A[kPanel * kLDG];
     __shared__ int far_from_I;
     if (skip && *skip) return;
-    const int tid = threadIdx.x, cj = tid & (kPanel - 1), ri = tid >> 6;
+    const int tid = threadIdx.x, cj = tid & (kPanel - 1), ri = tid >> 6;   // ri < kCholNT / 64
     // single: the panel is orthonormal to 1e-3 (max |G - I|), so one CholeskyQR
     // pass already gives an O(omega kappa^2) = O(omega) orthogonality and the
     // second pass is skipped (the caller's conditional kernels read *single)
@@ -51,7 +52,7 @@ __global__ void __launch_bounds__(256) k_chol(const double *__restrict__ G, int 
         if (tid == 0) far_from_I = 0;
         __syncthreads();
         if (cj < w)
-            for (int i = ri; i < w; i += 4)
+            for (int i = ri; i < w; i += kCholNT / 64)
                 if (!(fabs(G[i + cj * w] - (i == cj ? 1.0 : 0.0)) <= 1e-3)) far_from_I = 1;
         __syncthreads();
         if (tid == 0) *single = far_from_I ? 0 : 1;
@@ -60,7 +61,7 @@ __global__ void __launch_bounds__(256) k_chol(const double *__restrict__ G, int 
     // enough" (Kahan, Parlett) asks for the second pass (the caller redoes Q with CGS2)
     if (pre && reorth && ri == 0 && cj < w && G[cj + cj * w] < 0.25 * pre[cj]) *reorth = 1;
     if (cj < w)
-        for (int i = ri; i <= cj; i += 4) A[i + cj * kLDG] = 0.5 * (G[i + cj * w] + G[cj + i * w]);
+        for (int i = ri; i <= cj; i += kCholNT / 64) A[i + cj * kLDG] = 0.5 * (G[i + cj * w] + G[cj + i * w]);
     __syncthreads();
     bool bad = false;
     for (int k = 0; k < w; ++k) {
@@ -71,13 +72,13 @@ __global__ void __launch_bounds__(256) k_chol(const double *__restrict__ G, int 
         __syncthreads();
         if (cj > k && cj < w) {                                       // A(i, j) -= R(k, i) R(k, j), k < i <= j
             const double rkj = A[k + cj * kLDG];
-            for (int i = k + 1 + ri; i <= cj; i += 4) A[i + cj * kLDG] = __fma_rn(-A[k + i * kLDG], rkj, A[i + cj * kLDG]);
+            for (int i = k + 1 + ri; i <= cj; i += kCholNT / 64) A[i + cj * kLDG] = __fma_rn(-A[k + i * kLDG], rkj, A[i + cj * kLDG]);
         }
         if (ri == 0 && cj == k) A[k + k * kLDG] = r;
         __syncthreads();
     }
     if (cj < w)
-        for (int i = ri; i < w; i += 4) Rf[i + cj * w] = (i <= cj) ? A[i + cj * kLDG] : 0.0;
+        for (int i = ri; i < w; i += kCholNT / 64) Rf[i + cj * w] = (i <= cj) ? A[i + cj * kLDG] : 0.0;
     if (tid == 0 && bad) *fail = 1;
 }
 
@@ -214,9 +215,10 @@ static mpj_status orth_sweep(const double *Z, int64_t ldz, double *Q, int64_t ld
             double *dst = rep == 0 ? S : X;
             const int64_t ldd = rep == 0 ? m : ldq;
             const int *skip = rep == 1 ? single : nullptr;
+            // the panel Gram (one 64 x 64 tile, K = m): split K into 64-row slices, one CTA each
             launch_dgemm(true, false, w, w, m, 1.0, src, lds, src, lds, 0.0, G, w, st, scratch, scratch_elems, false,
-                         skip);
-            launch_pdl_k(k_chol, dim3(1), dim3(256), 0, st, (const double *)G, w, Rf, fail,
+                         skip, (int)std::min<int64_t>(128, m / 64));
+            launch_pdl_k(k_chol, dim3(1), dim3(kCholNT), 0, st, (const double *)G, w, Rf, fail,
                          (const double *)((check && rep == 0) ? pre : nullptr), reorth, rep == 0 ? single : nullptr,
                          skip);
             if (w == kPanel)
