@@ -1280,7 +1280,8 @@ static cudaError_t launch_apply_f64g3(const ApplyArgs &p, cudaStream_t st)
 {
     const int mb = p.S.nb >> 1;
     // three groups' buffers, counters, the compact lists (L, P) of the item counter
-    const size_t smem = 3 * 2 * TW * Lay<double>::LD * sizeof(double) + (8 + 2 * (size_t)mb + 1) * sizeof(int);
+    const size_t smem = 3 * 2 * TW * Lay<double>::LD * sizeof(double) +
+                        (8 + 2 * (size_t)std::min(mb, 1024) + 1) * sizeof(int);   // compact lists only for mb <= 1024
     cudaError_t e = smem_optin((const void *)k_block_apply_f64g3, smem, 3 * NT, nullptr);
     if (e != cudaSuccess) return e;
     const int total = p.ntT + p.ntV;
