@@ -164,6 +164,29 @@ def test_eig_end_to_end(mpj, orc, n, mode, kappa):
     assert abs(rep.off0 - ref.report.off0) <= tol * ref.report.off0 + 100 * n * OMEGA
 
 
+@pytest.mark.parametrize("n,mode", [(17, 4), (33, 3), (64, 5)])
+def test_eig_small_default_route(mpj, orc, n, mode):
+    """mpjacobi_eig with the default configuration at n <= 64 runs the batched
+    path's single-CTA kernels (the same Alg. 3): eigenpairs to the
+    north_star tolerances against the oracle's default (symmetric-QR step 1)
+    run, fp64 sweeps within one of the oracle's (the two step-1 Z differ at
+    binary32 rounding), and within tolerance of the general path
+    (MPJ_SMALL_BATCHED=0 is read once per process, so the general path is
+    forced here through an explicit variant)."""
+    A, _ = W.example1(n, 1e3, mode, W.seed_for(1, mode, 1e3))
+    r = mpj.eig(dev(A))
+    assert r.report.n_padded == 64 and r.report.variant == mpj.VARIANT_BLOCK
+    ref = orc.mp_evd(A, orc.default_cfg("eig", b=32))
+    lam, V = host(r.lam), host(r.V)
+    nrm2 = np.max(np.abs(ref.lam))
+    assert np.max(np.abs(lam - ref.lam)) <= 1e-13 * nrm2
+    assert np.linalg.norm(V.T @ V - np.eye(n)) <= n * 1e-15
+    assert np.linalg.norm(A @ V - V * lam) / np.linalg.norm(A) <= n * 1e-15
+    assert abs(r.sweeps - ref.report.sweeps) <= 1, (r.sweeps, ref.report.sweeps)
+    g = mpj.eig(dev(A), mpj.default_config("eig", variant=mpj.VARIANT_BLOCK, block_b=32))
+    assert np.max(np.abs(host(g.lam) - lam)) <= 1e-13 * nrm2
+
+
 def test_eig_host_buffers(mpj, orc):
     """The ABI accepts host pointers (staged by the library): same result."""
     n = 64
