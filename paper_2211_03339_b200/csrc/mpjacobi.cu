@@ -474,38 +474,36 @@ static mpj_status jacobi_run(Ctx &cx, R *T, R *V, int n, int b, int variant, dou
                 if (cur != T) MPJ_CK_VOID(cudaMemcpyAsync(T, cur, (size_t)np * np * sizeof(R), cudaMemcpyDeviceToDevice, st));
             };
             if (use_graph) {
-                if (!gexec) {
-                    SweepGraphKey key;
-                    std::memset(&key, 0, sizeof(key));
-                    cudaGetDevice(&key.dev);
-                    key.np = np; key.rule = rule; key.rounds = hs.rounds; key.fused = fused ? 1 : 0;
-                    key.rsize = (int)sizeof(R); key.nu = (double)nu;
-                    const void *ptrs[11] = {T, V, jb.Tn, jb.pq, jb.pos, jb.t, jb.s, jb.u, jb.cnt, jb.bsched, jb.lsched};
-                    std::memcpy(key.ptr, ptrs, sizeof(ptrs));
-                    {
-                        std::lock_guard<std::mutex> lk(g_sweep_graph_mu);
-                        for (auto &e : g_sweep_graphs)
-                            if (e.key == key) { gexec = e.exec; graph_kernels = e.kernels; break; }
-                    }
-                    if (!gexec) {
-                        cudaGraph_t g;
-                        const long long l0 = g_launches;
-                        MPJ_CK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
-                        sweep_rounds(0, hs.rounds);
-                        MPJ_CK(cudaStreamEndCapture(st, &g));
-                        graph_kernels = g_launches - l0;
-                        g_launches = l0;
-                        MPJ_CK(cudaGraphInstantiate(&gexec, g, 0));
-                        cudaGraphDestroy(g);
-                        std::lock_guard<std::mutex> lk(g_sweep_graph_mu);
-                        if (g_sweep_graphs.size() >= 16) {
-                            cudaGraphExecDestroy(g_sweep_graphs.front().exec);
-                            g_sweep_graphs.erase(g_sweep_graphs.begin());
-                        }
-                        g_sweep_graphs.push_back({key, gexec, graph_kernels});
-                    }
+                // the cache lock is held from the lookup to the launch: a cached
+                // exec is never evicted (at most 16 are kept; beyond that a call
+                // instantiates its own and destroys it after its final sync)
+                SweepGraphKey key;
+                std::memset(&key, 0, sizeof(key));
+                cudaGetDevice(&key.dev);
+                key.np = np; key.rule = rule; key.rounds = hs.rounds; key.fused = fused ? 1 : 0;
+                key.rsize = (int)sizeof(R); key.nu = (double)nu;
+                const void *ptrs[11] = {T, V, jb.Tn, jb.pq, jb.pos, jb.t, jb.s, jb.u, jb.cnt, jb.bsched, jb.lsched};
+                std::memcpy(key.ptr, ptrs, sizeof(ptrs));
+                std::unique_lock<std::mutex> lk(g_sweep_graph_mu);
+                cudaGraphExec_t ge = gexec;
+                if (!ge)
+                    for (auto &e : g_sweep_graphs)
+                        if (e.key == key) { ge = e.exec; graph_kernels = e.kernels; break; }
+                if (!ge) {
+                    cudaGraph_t g;
+                    const long long l0 = g_launches;
+                    MPJ_CK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+                    sweep_rounds(0, hs.rounds);
+                    MPJ_CK(cudaStreamEndCapture(st, &g));
+                    graph_kernels = g_launches - l0;
+                    g_launches = l0;
+                    MPJ_CK(cudaGraphInstantiate(&ge, g, 0));
+                    cudaGraphDestroy(g);
+                    if (g_sweep_graphs.size() < 16) g_sweep_graphs.push_back({key, ge, graph_kernels});
+                    else gexec = ge;                 // this call's own exec (destroyed below)
                 }
-                MPJ_CK(cudaGraphLaunch(gexec, st));
+                MPJ_CK(cudaGraphLaunch(ge, st));
+                lk.unlock();
                 count_launch(graph_kernels);
                 rounds_done += hs.rounds;
             } else {
@@ -516,9 +514,10 @@ static mpj_status jacobi_run(Ctx &cx, R *T, R *V, int n, int b, int variant, dou
             }
         }
     }
-    unsigned long long rot = 0;             // (gexec stays in g_sweep_graphs for the next call)
+    unsigned long long rot = 0;
     MPJ_CK(cudaMemcpyAsync(cx.h_pin, jb.cnt, sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
     MPJ_CK(cudaStreamSynchronize(st));
+    if (gexec) cudaGraphExecDestroy(gexec);   // an uncached exec of this call (the cache was full)
     std::memcpy(&rot, cx.h_pin, sizeof(rot));
     out.sweeps = sweeps;
     out.rotations = (long long)rot;
